@@ -1,0 +1,212 @@
+/*
+ * vdi.h — C ABI of libvdi: B200-native sort-last parallel compositing of
+ * Volumetric Depth Images (arXiv 2206.14503).
+ *
+ * Citations "PAPER.md:N" are lines of the paper text; readings Qn / Gn are
+ * listed in DESIGN.md §2.  All device pointers are CUDA global-memory
+ * pointers on the calling process's current device; all work is enqueued on
+ * vdi_config.cuda_stream.  No C++ or torch types cross this boundary.
+ *
+ * Error behaviour: every call returns a vdi_status; no exception crosses the
+ * ABI.  vdi_last_error() gives the detail text.  After a CUDA or NCCL error a
+ * context is poisoned: later calls return VDI_ERR_STATE; destroy it.
+ * Threading: a context is single-threaded; separate contexts are independent.
+ */
+#ifndef VDI_H_
+#define VDI_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#pragma GCC visibility push(default) /* the library is built with -fvisibility=hidden */
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  VDI_OK = 0,
+  VDI_ERR_INVALID_ARG = 1,   /* bad pointer / size / config value */
+  VDI_ERR_OUT_OF_MEMORY = 2, /* cudaMalloc failed */
+  VDI_ERR_CUDA = 3,          /* CUDA runtime error (context poisoned) */
+  VDI_ERR_NCCL = 4,          /* NCCL error (context poisoned) */
+  VDI_ERR_STATE = 5,         /* context poisoned or call out of order */
+  VDI_ERR_CAPACITY = 6,      /* caller buffer too small, or a ray needs > k supersegments (Q20) */
+  VDI_ERR_INTERNAL = 7
+} vdi_status;
+
+/* vdi_config.flags */
+#define VDI_FLAG_PIXEL_STATS 0x1u  /* keep per-pixel gamma* and m of the last composite (vdi_pixel_stats) */
+#define VDI_FLAG_VALIDATE 0x2u     /* check inputs: count <= k_in, tf < tb, 0 < alpha <= 1, sorted runs */
+#define VDI_FLAG_STAGE_TIMING 0x4u /* record CUDA-event times of the exchange / merge / gather stages */
+
+typedef struct vdi_ctx vdi_ctx; /* opaque */
+
+/* Compositing configuration.  All ranks pass identical values except `rank`.
+ * PEs (processing elements) are the sources of sub-VDIs; PE s
+ * is homed on rank floor(s * n_ranks / n_pes) ("block manner").
+ * Rank g composites image rows [floor(g H / G), floor((g+1) H / G)) with
+ * G = n_ranks (direct send; Q13). */
+typedef struct {
+  uint32_t width, height;  /* image = N_lists = w h lists */
+  uint32_t k_in;           /* per-PE budget of the sub-VDIs, 1..255 */
+  uint32_t k_out;          /* budget of the composited lists, 1..255 (N_s) */
+  uint32_t n_pes;          /* number of PEs (sources), >= 1 */
+  uint32_t n_ranks, rank;  /* GPUs (one process per GPU) and this process's index */
+  uint32_t max_iters;      /* bisection iterations I; 0 -> 16 (Q5) */
+  float gamma_max;         /* upper end of the gamma search; 0 -> 2.0 (Q5) */
+  uint32_t flags;          /* VDI_FLAG_* */
+  const uint8_t* nccl_unique_id; /* 128 bytes from vdi_get_unique_id on rank 0; required iff n_ranks > 1 */
+  void* cuda_stream;             /* cudaStream_t (borrowed); NULL = legacy default stream */
+} vdi_config;
+
+/* Dense sub-VDI of one PE (Fig. 2): per-list counts, their
+ * exclusive prefix sum, and the packed supersegments of all lists in list
+ * (row-major pixel) order, front-to-back within a list.  A supersegment is
+ * 24 B: depth (t_front, t_back) world-space distance along the
+ * unit ray (Q10) and accumulated premultiplied RGBA (Q7).
+ * Memory: device, caller-owned (borrowed until the stream passes the call),
+ * except when returned by vdi_generate_subvdi (ctx-owned). */
+typedef struct {
+  uint32_t pe_id;
+  uint64_t total;         /* S_s = number of supersegments */
+  const uint8_t* count;   /* [W*H], each <= k_in */
+  const uint32_t* offset; /* [W*H + 1] exclusive scan of count (offset[W*H] == total) */
+  const float* depth;     /* [total][2]  (t_front, t_back) */
+  const float* rgba;      /* [total][4]  premultiplied, accumulated over [t_front, t_back] */
+} vdi_dense_view;
+
+/* Full-resolution representation of image rows [row_begin, row_end)
+ * (PAPER.md:111, :185): k_out slots per list, unused slots all-zero (Q16).
+ * Layout is list-major, slot fastest: element (y, x, j) at
+ * ((y - row_begin) * W + x) * k_out + j.  Caller-owned device memory. */
+typedef struct {
+  uint32_t row_begin, row_end;
+  uint8_t* count; /* [rows*W] */
+  float* depth;   /* [rows*W][k_out][2] */
+  float* rgba;    /* [rows*W][k_out][4] */
+} vdi_full_view;
+
+/* Scene description for the reference raycaster that produces sub-VDIs
+ * (Phase 1; SUPPORT, untimed).  World box: longest side 1,
+ * centred at the origin; voxel i covers continuous coordinate [i, i+1). */
+typedef struct {
+  const void* voxels;       /* device, x-fastest [dz][dy][dx] */
+  uint32_t bytes_per_voxel; /* 1 (u8, /255) or 2 (u16, /65535) */
+  uint32_t dims[3];
+} vdi_volume_desc;
+
+typedef struct {
+  const float* table; /* device [256][4] RGBA, non-premultiplied, linear interpolation */
+} vdi_tf_desc;
+
+typedef struct {
+  float eye[3], fwd[3], right[3], up[3]; /* orthonormal basis, world units */
+  float tan_x, tan_y;                    /* tan(vfov/2)*aspect, tan(vfov/2) */
+} vdi_camera;
+
+/* Axis-aligned brick grid; brick (bx,by,bz) covers voxels [xb[bx], xb[bx+1])
+ * x [yb[by], yb[by+1]) x [zb[bz], zb[bz+1]) (half-open) and belongs to PE
+ * owner[(bz*gy + by)*gx + bx].  Host memory, copied by the call.  Unions of
+ * bricks may be non-convex. */
+typedef struct {
+  uint32_t grid[3]; /* gx, gy, gz; product <= 4096 */
+  const int32_t* xb;
+  const int32_t* yb;
+  const int32_t* zb;
+  const int32_t* owner;
+} vdi_decomp_desc;
+
+/* ---- lifecycle ---------------------------------------------------------- */
+const char* vdi_version(void);
+const char* vdi_status_string(vdi_status s);
+const char* vdi_last_error(const vdi_ctx* ctx); /* NULL-safe; thread-local text of the last failed call */
+
+/* 128-byte NCCL unique id for vdi_config.nccl_unique_id (call on rank 0,
+ * broadcast to the other ranks out of band, e.g. torch.distributed). */
+vdi_status vdi_get_unique_id(uint8_t out[128]);
+
+/* Validates cfg (VDI_ERR_INVALID_ARG), binds the current CUDA device, and for
+ * n_ranks > 1 creates the NCCL communicator (collective over all ranks). */
+vdi_status vdi_composite_init(const vdi_config* cfg, vdi_ctx** out);
+void vdi_composite_destroy(vdi_ctx* ctx); /* NULL-safe; frees ctx-owned device memory */
+
+/* ---- Phase 1 (SUPPORT): sub-VDI of PE pe_id --------------------------------
+ * Two passes per ray: pass 1 finds gamma and the count it
+ * generates (gamma = 0 if count(0) <= k_in, else the bisection of
+ * PAPER.md:100-101, reading G1), an exclusive scan gives the offsets, pass 2
+ * writes each list at its offset.  Samples lie on the global grid
+ * t_i = t_in + (i+0.5)/max(dims) (one voxel, Q18); a sample owned by another
+ * PE forces the open supersegment to end.  The output is
+ * ctx-owned and valid until the next call with the same pe_id or destroy;
+ * synchronises the stream once (to size the payload).
+ * VDI_ERR_CAPACITY: some ray needs more than k_in supersegments (Q20). */
+vdi_status vdi_generate_subvdi(vdi_ctx* ctx, const vdi_volume_desc* vol, const vdi_tf_desc* tf,
+                               const vdi_camera* cam, const vdi_decomp_desc* decomp, uint32_t pe_id,
+                               vdi_dense_view* out);
+
+/* ---- Phase 2: the hot path -------------------------------------------------
+ * Parallel compositing of the sub-VDIs, collective over
+ * all ranks: strip totals, size exchange + all-to-allv of count slices and
+ * dense payload slices (NCCL over NVLink, no-op for n_ranks
+ * == 1), receive-side scans, then per list: depth ordering,
+ * overlap subdivision (Eq. 2 generalised, Q12), verbatim pass-through when
+ * m <= k_out (Q9), otherwise the per-ray gamma bisection over the
+ * sub-supersegments and the final greedy sweep, written in the
+ * full representation.
+ * local_pes: the n_local sub-VDIs homed on this rank, any order, each with a
+ * distinct pe_id.  strip_out: caller-owned, rows of this rank's strip
+ * (VDI_ERR_CAPACITY if the row range does not match).  Synchronises the
+ * stream once when n_ranks > 1 (sizes of the all-to-allv). */
+vdi_status vdi_composite(vdi_ctx* ctx, const vdi_dense_view* local_pes, uint32_t n_local,
+                         vdi_full_view* strip_out);
+
+/* Same as vdi_composite with HOST buffers (the end-to-end entry point):
+ * copies the local sub-VDIs host->device (pinned memory recommended),
+ * composites, and copies the strip back device->host into strip_out.
+ * Pointers in local_pes / strip_out are host pointers.  Synchronises. */
+vdi_status vdi_composite_host(vdi_ctx* ctx, const vdi_dense_view* local_pes, uint32_t n_local,
+                              vdi_full_view* strip_out);
+
+/* Gather of the composited strips onto rank 0 (PAPER.md:185 MPI_Gather; Q14):
+ * image_out (rows [0, H), root only; ignored elsewhere) receives every rank's
+ * strip in rank order.  For n_ranks == 1 it copies the strip if the buffers
+ * differ. */
+vdi_status vdi_gather(vdi_ctx* ctx, const vdi_full_view* strip, vdi_full_view* image_out);
+
+/* ---- introspection ---------------------------------------------------------- */
+/* Per-pixel gamma* (0 for pass-through) and m (samples after sort/subdivision)
+ * of this rank's strip for the last composite; device pointers [rows*W].
+ * Requires VDI_FLAG_PIXEL_STATS. */
+vdi_status vdi_pixel_stats(vdi_ctx* ctx, float* gamma, uint16_t* m);
+
+/* Counters of the last vdi_composite on this rank. */
+typedef struct {
+  uint64_t records_in;      /* sum over local strip lists of m before subdivision (supersegments merged) */
+  uint64_t searched_lists;  /* lists that needed the gamma search or subdivision */
+  uint64_t bytes_sent;      /* all-to-allv payload bytes sent to other ranks */
+  uint64_t bytes_received;  /* all-to-allv payload bytes received */
+  uint32_t kernel_launches; /* libvdi kernels launched by the call */
+  float ms_exchange, ms_merge, ms_gather; /* VDI_FLAG_STAGE_TIMING, else 0 */
+} vdi_counters;
+vdi_status vdi_get_counters(vdi_ctx* ctx, vdi_counters* out);
+
+/* ---- host-only helpers (no GPU needed) --------------------------------------- */
+/* Rows [*row_begin, *row_end) of strip g of G (Q13). */
+vdi_status vdi_strip_rows(uint32_t height, uint32_t n_ranks, uint32_t g, uint32_t* row_begin,
+                          uint32_t* row_end);
+/* Home rank of PE pe: floor(pe * n_ranks / n_pes). */
+uint32_t vdi_pe_home(uint32_t n_pes, uint32_t n_ranks, uint32_t pe);
+/* Bytes of a full-representation view of `rows` rows: rows*W*(1 + 24*k). */
+uint64_t vdi_full_bytes(uint32_t width, uint32_t rows, uint32_t k);
+
+#ifdef __cplusplus
+}
+#endif
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+#endif /* VDI_H_ */

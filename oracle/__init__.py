@@ -201,6 +201,17 @@ class SceneHandle:
         self.W, self.H = cam.W, cam.H
 
 
+def pixels_to_dense(gen, P, pix):
+    """Per-pixel generator output (generate_pixels) -> full-image dense arrays
+    with empty lists outside `pix` (pix sorted ascending)."""
+    k = gen["depth"].shape[1]
+    cnt = np.zeros(P, np.uint8)
+    cnt[pix] = gen["count"]
+    used = np.arange(k)[None, :] < gen["count"][:, None].astype(np.int64)
+    return {"count": cnt, "depth": np.ascontiguousarray(gen["depth"][used]),
+            "rgba": np.ascontiguousarray(gen["rgba"][used])}
+
+
 def scene(vol, dims, tf, cam, dec):
     v = np.asarray(vol)
     bpv = 1 if v.dtype == np.uint8 else 2
@@ -223,7 +234,7 @@ def generate_dense(sc: SceneHandle, pe, k, max_iters=16, gamma_max=2.0, n_thread
     return {"count": cnt, "gamma": gam, "offset": off, "depth": dep[:tot].copy(), "rgba": rgba[:tot].copy()}
 
 
-def generate_pixels(sc: SceneHandle, pe, k, pix, max_iters=16, gamma_max=2.0):
+def generate_pixels(sc: SceneHandle, pe, k, pix, max_iters=16, gamma_max=2.0, n_threads=1):
     pix = np.ascontiguousarray(np.asarray(pix, np.int64))
     n = len(pix)
     cnt = np.zeros(n, np.uint8)
@@ -231,8 +242,8 @@ def generate_pixels(sc: SceneHandle, pe, k, pix, max_iters=16, gamma_max=2.0):
     dep = np.zeros((n, k, 2), np.float32)
     rgba = np.zeros((n, k, 4), np.float32)
     rc = lib().orc_generate_pixels(C.byref(sc.s), C.c_int32(pe), C.c_int32(k), C.c_int32(max_iters),
-                                   C.c_float(gamma_max), C.c_int64(n), _p(pix), _p(cnt), _p(gam), _p(dep),
-                                   _p(rgba))
+                                   C.c_float(gamma_max), C.c_int64(n), _p(pix), C.c_int32(n_threads), _p(cnt),
+                                   _p(gam), _p(dep), _p(rgba))
     return {"count": cnt, "gamma": gam, "depth": dep, "rgba": rgba, "capacity_exceeded": rc == -2}
 
 

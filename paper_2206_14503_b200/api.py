@@ -1,0 +1,199 @@
+"""Python face of libvdi: the header's calls on torch CUDA tensors.
+
+`Compositor` owns one vdi_ctx.  Methods marshal torch tensors / numpy arrays
+into the C structs of include/vdi.h and call the same-named C functions; no
+compositing arithmetic happens here.  torch is used only for device memory
+and streams (and torch.distributed to broadcast the NCCL id).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib as L
+
+
+def _ptr(t) -> int | None:
+    if t is None:
+        return None
+    return t.data_ptr() if isinstance(t, torch.Tensor) else t.ctypes.data
+
+
+@dataclass
+class DenseSubVDI:
+    """A dense sub-VDI: count u8[P], offset u32[P+1] (as
+    int32 bits), depth f32[S,2], rgba f32[S,4]; device or host tensors."""
+    pe_id: int
+    total: int
+    count: torch.Tensor
+    offset: torch.Tensor | None
+    depth: torch.Tensor
+    rgba: torch.Tensor
+
+    def view(self) -> L.vdi_dense_view:
+        return L.vdi_dense_view(self.pe_id, self.total, _ptr(self.count), _ptr(self.offset), _ptr(self.depth),
+                                _ptr(self.rgba))
+
+    def to(self, device, pin=False):
+        def mv(t):
+            if t is None:
+                return None
+            t = t.to(device)
+            return t.pin_memory() if pin and t.device.type == "cpu" else t
+        return DenseSubVDI(self.pe_id, self.total, mv(self.count), mv(self.offset), mv(self.depth), mv(self.rgba))
+
+
+@dataclass
+class FullVDI:
+    """Full representation of rows [row_begin, row_end)."""
+    row_begin: int
+    row_end: int
+    count: torch.Tensor  # u8 [rows*W]
+    depth: torch.Tensor  # f32 [rows*W, k, 2]
+    rgba: torch.Tensor   # f32 [rows*W, k, 4]
+
+    def view(self) -> L.vdi_full_view:
+        return L.vdi_full_view(self.row_begin, self.row_end, _ptr(self.count), _ptr(self.depth), _ptr(self.rgba))
+
+    @staticmethod
+    def empty(width, row_begin, row_end, k, device="cuda", pin=False):
+        P = width * (row_end - row_begin)
+        kw = dict(device=device)
+        t = [torch.empty(P, dtype=torch.uint8, **kw), torch.empty((P, k, 2), dtype=torch.float32, **kw),
+             torch.empty((P, k, 4), dtype=torch.float32, **kw)]
+        if pin:
+            t = [x.pin_memory() for x in t]
+        return FullVDI(row_begin, row_end, *t)
+
+
+class _CudaArray:
+    """Minimal __cuda_array_interface__ holder to wrap ctx-owned memory."""
+
+    def __init__(self, ptr, shape, typestr, owner):
+        self.__cuda_array_interface__ = {"shape": shape, "typestr": typestr, "data": (ptr, False), "version": 3,
+                                         "strides": None}
+        self._owner = owner
+
+
+def _wrap(ptr, shape, typestr, owner):
+    if int(np.prod(shape)) == 0 or not ptr:
+        dt = {"|u1": torch.uint8, "<u4": torch.int32, "<f4": torch.float32}[typestr]
+        return torch.empty(shape, dtype=dt, device="cuda")
+    return torch.as_tensor(_CudaArray(ptr, shape, typestr, owner), device="cuda")
+
+
+def strip_rows(height, n_ranks, g):
+    b, e = C.c_uint32(), C.c_uint32()
+    L.check(L.lib().vdi_strip_rows(height, n_ranks, g, C.byref(b), C.byref(e)), "vdi_strip_rows")
+    return b.value, e.value
+
+
+def pe_home(n_pes, n_ranks, pe):
+    return L.lib().vdi_pe_home(n_pes, n_ranks, pe)
+
+
+def full_bytes(width, rows, k):
+    return L.lib().vdi_full_bytes(width, rows, k)
+
+
+def get_unique_id() -> bytes:
+    buf = (C.c_uint8 * 128)()
+    L.check(L.lib().vdi_get_unique_id(buf), "vdi_get_unique_id")
+    return bytes(buf)
+
+
+class Compositor:
+    """One libvdi context (vdi_composite_init ... vdi_composite_destroy)."""
+
+    def __init__(self, width, height, k_in, k_out, n_pes, n_ranks=1, rank=0, max_iters=16, gamma_max=2.0,
+                 flags=0, unique_id: bytes | None = None, stream: torch.cuda.Stream | None = None):
+        self.lib = L.lib()
+        self.width, self.height, self.k_in, self.k_out, self.n_pes = width, height, k_in, k_out, n_pes
+        self.n_ranks, self.rank = n_ranks, rank
+        self.stream = stream if stream is not None else torch.cuda.current_stream()
+        self._uid = (C.c_uint8 * 128).from_buffer_copy(unique_id) if unique_id else None
+        cfg = L.vdi_config(width, height, k_in, k_out, n_pes, n_ranks, rank, max_iters, gamma_max, flags,
+                           C.cast(self._uid, C.c_void_p) if self._uid is not None else None,
+                           self.stream.cuda_stream)
+        h = C.c_void_p()
+        L.check(self.lib.vdi_composite_init(C.byref(cfg), C.byref(h)), "vdi_composite_init")
+        self.ctx = h
+        self.row_begin, self.row_end = strip_rows(height, n_ranks, rank)
+
+    def close(self):
+        if getattr(self, "ctx", None):
+            self.lib.vdi_composite_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- Phase 1 (SUPPORT) ---------------------------------------------------
+    def generate_subvdi(self, volume: torch.Tensor, tf_table: torch.Tensor, camera, decomposition,
+                        pe_id: int) -> DenseSubVDI:
+        """vdi_generate_subvdi: volume [dz][dy][dx] u8 (or u16 bits in int16),
+        tf_table [256,4] f32 (device), camera with eye/fwd/right/up/tan_x/tan_y,
+        decomposition with xb/yb/zb/owner int arrays.  Returns tensors that
+        alias ctx-owned memory (valid until the next call for this pe_id)."""
+        assert volume.is_cuda and tf_table.is_cuda
+        dz, dy, dx = volume.shape
+        vol = L.vdi_volume_desc(volume.data_ptr(), volume.element_size(), (C.c_uint32 * 3)(dx, dy, dz))
+        tf = L.vdi_tf_desc(tf_table.contiguous().data_ptr())
+        cam = L.vdi_camera((C.c_float * 3)(*camera.eye), (C.c_float * 3)(*camera.fwd),
+                           (C.c_float * 3)(*camera.right), (C.c_float * 3)(*camera.up), camera.tan_x, camera.tan_y)
+        xb = np.ascontiguousarray(decomposition.xb, np.int32)
+        yb = np.ascontiguousarray(decomposition.yb, np.int32)
+        zb = np.ascontiguousarray(decomposition.zb, np.int32)
+        ow = np.ascontiguousarray(decomposition.owner, np.int32)
+        dec = L.vdi_decomp_desc((C.c_uint32 * 3)(len(xb) - 1, len(yb) - 1, len(zb) - 1), xb.ctypes.data,
+                                yb.ctypes.data, zb.ctypes.data, ow.ctypes.data)
+        out = L.vdi_dense_view()
+        L.check(self.lib.vdi_generate_subvdi(self.ctx, C.byref(vol), C.byref(tf), C.byref(cam), C.byref(dec),
+                                             pe_id, C.byref(out)), "vdi_generate_subvdi")
+        P = self.width * self.height
+        S = int(out.total)
+        return DenseSubVDI(pe_id, S, _wrap(out.count, (P,), "|u1", self), _wrap(out.offset, (P + 1,), "<u4", self),
+                           _wrap(out.depth, (S, 2), "<f4", self), _wrap(out.rgba, (S, 4), "<f4", self))
+
+    # -- Phase 2: the hot path ------------------------------------------------
+    def empty_strip(self, device="cuda", pin=False) -> FullVDI:
+        return FullVDI.empty(self.width, self.row_begin, self.row_end, self.k_out, device, pin)
+
+    def composite(self, local_pes, strip: FullVDI) -> FullVDI:
+        """vdi_composite (device buffers)."""
+        views = (L.vdi_dense_view * max(1, len(local_pes)))(*[p.view() for p in local_pes])
+        sv = strip.view()
+        L.check(self.lib.vdi_composite(self.ctx, views, len(local_pes), C.byref(sv)), "vdi_composite")
+        return strip
+
+    def composite_host(self, local_pes, strip: FullVDI) -> FullVDI:
+        """vdi_composite_host (host buffers; H2D + composite + D2H)."""
+        views = (L.vdi_dense_view * max(1, len(local_pes)))(*[p.view() for p in local_pes])
+        sv = strip.view()
+        L.check(self.lib.vdi_composite_host(self.ctx, views, len(local_pes), C.byref(sv)), "vdi_composite_host")
+        return strip
+
+    def gather(self, strip: FullVDI, image: FullVDI | None):
+        """vdi_gather: strips -> rank 0 (image ignored on other ranks)."""
+        sv = strip.view()
+        iv = image.view() if image is not None else None
+        L.check(self.lib.vdi_gather(self.ctx, C.byref(sv), C.byref(iv) if iv is not None else None), "vdi_gather")
+        return image
+
+    def pixel_stats(self):
+        P = (self.row_end - self.row_begin) * self.width
+        g = torch.empty(P, dtype=torch.float32, device="cuda")
+        m = torch.empty(P, dtype=torch.int16, device="cuda")
+        L.check(self.lib.vdi_pixel_stats(self.ctx, g.data_ptr(), m.data_ptr()), "vdi_pixel_stats")
+        return g, m
+
+    def counters(self) -> dict:
+        c = L.vdi_counters()
+        L.check(self.lib.vdi_get_counters(self.ctx, C.byref(c)), "vdi_get_counters")
+        return {f: getattr(c, f) for f, _ in L.vdi_counters._fields_}

@@ -1,0 +1,666 @@
+// api.cu — libvdi C ABI (include/vdi.h): context, validation, the Phase-2
+// orchestration (strip partition, size exchange, all-to-allv over NCCL,
+// receive-side scan, merge) and the gather to the root.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "internal.h"
+
+using namespace vdi;
+
+namespace {
+
+thread_local std::string g_err;
+
+vdi_status fail(vdi_status s, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return s;
+}
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+  cudaError_t grow(size_t need) {
+    if (need <= bytes) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+    size_t want = std::max(need, (size_t)256);
+    cudaError_t e = cudaMalloc(&p, want);
+    if (e == cudaSuccess) bytes = want;
+    return e;
+  }
+  template <class T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+struct GenOut {
+  DevBuf count32, count8, offset, gamma, depth, rgba, owner;
+  uint64_t total = 0;
+};
+
+// device-side counters of one composite
+struct DevCounters {
+  uint32_t wl_count;
+  int err;
+  unsigned long long scratch_used;
+  unsigned long long records_in;
+};
+
+}  // namespace
+
+struct vdi_ctx {
+  vdi_config cfg{};
+  cudaStream_t stream = nullptr;
+  int device = 0;
+  ncclComm_t comm = nullptr;
+  bool poisoned = false;
+  uint32_t row0 = 0, row1 = 0;
+  uint64_t P = 0;  // lists in this rank's strip
+  // merge scratch
+  DevBuf group_sum, group_base, totals, wl, scratch, dcnt, stat_gamma, stat_m, bounds;
+  // exchange receive buffers per source
+  std::vector<DevBuf> rcount, rdepth, rrgba;
+  // generator outputs per pe
+  std::vector<GenOut> gen;
+  DevBuf gen_tmp;
+  void* cub_tmp = nullptr;
+  size_t cub_tmp_bytes = 0;
+  // host e2e staging
+  std::vector<DevBuf> hcount, hoffset, hdepth, hrgba;
+  DevBuf hstrip_count, hstrip_depth, hstrip_rgba;
+  // counters
+  vdi_counters last{};
+  bool have_stats = false;
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  bool timing_pending = false;
+  bool gather_timing_pending = false;
+  cudaEvent_t gev[2] = {nullptr, nullptr};
+  ~vdi_ctx() {
+    if (cub_tmp) cudaFree(cub_tmp);
+    for (auto& e : ev)
+      if (e) cudaEventDestroy(e);
+    for (auto& e : gev)
+      if (e) cudaEventDestroy(e);
+    if (comm) ncclCommDestroy(comm);
+  }
+};
+
+#define CUDA_TRY(ctx, expr)                                                                  \
+  do {                                                                                       \
+    cudaError_t e_ = (expr);                                                                 \
+    if (e_ != cudaSuccess) {                                                                 \
+      (ctx)->poisoned = true;                                                                \
+      return fail(e_ == cudaErrorMemoryAllocation ? VDI_ERR_OUT_OF_MEMORY : VDI_ERR_CUDA,   \
+                  "%s:%d %s: %s", __FILE__, __LINE__, #expr, cudaGetErrorString(e_));       \
+    }                                                                                        \
+  } while (0)
+
+#define NCCL_TRY(ctx, expr)                                                                         \
+  do {                                                                                              \
+    ncclResult_t r_ = (expr);                                                                       \
+    if (r_ != ncclSuccess) {                                                                        \
+      (ctx)->poisoned = true;                                                                       \
+      return fail(VDI_ERR_NCCL, "%s:%d %s: %s", __FILE__, __LINE__, #expr, ncclGetErrorString(r_)); \
+    }                                                                                               \
+  } while (0)
+
+namespace {
+
+__global__ void gather_bounds_kernel(const uint32_t* const* offs, const uint32_t* pes, int n_local,
+                                     const uint32_t* rows, int G, uint32_t W, int n_pes,
+                                     unsigned long long* bnd) {
+  // bnd[pe][g] = offset_pe[rows[g] * W]  (g = 0..G)
+  for (int i = threadIdx.x; i < n_local * (G + 1); i += blockDim.x) {
+    const int l = i / (G + 1), g = i % (G + 1);
+    bnd[(size_t)pes[l] * (G + 1) + g] = offs[l][(size_t)rows[g] * W];
+  }
+}
+
+vdi_status check_ctx(vdi_ctx* ctx) {
+  if (!ctx) return fail(VDI_ERR_INVALID_ARG, "ctx is NULL");
+  if (ctx->poisoned) return fail(VDI_ERR_STATE, "context poisoned by an earlier CUDA/NCCL error");
+  return VDI_OK;
+}
+
+uint32_t strip_row(uint32_t H, uint32_t G, uint32_t g) { return (uint32_t)((uint64_t)g * H / G); }
+
+}  // namespace
+
+extern "C" {
+
+const char* vdi_version(void) { return "libvdi 0.1 (sm_100a)"; }
+
+const char* vdi_status_string(vdi_status s) {
+  switch (s) {
+    case VDI_OK: return "VDI_OK";
+    case VDI_ERR_INVALID_ARG: return "VDI_ERR_INVALID_ARG";
+    case VDI_ERR_OUT_OF_MEMORY: return "VDI_ERR_OUT_OF_MEMORY";
+    case VDI_ERR_CUDA: return "VDI_ERR_CUDA";
+    case VDI_ERR_NCCL: return "VDI_ERR_NCCL";
+    case VDI_ERR_STATE: return "VDI_ERR_STATE";
+    case VDI_ERR_CAPACITY: return "VDI_ERR_CAPACITY";
+    case VDI_ERR_INTERNAL: return "VDI_ERR_INTERNAL";
+  }
+  return "VDI_ERR_UNKNOWN";
+}
+
+const char* vdi_last_error(const vdi_ctx*) { return g_err.c_str(); }
+
+vdi_status vdi_strip_rows(uint32_t height, uint32_t n_ranks, uint32_t g, uint32_t* row_begin,
+                          uint32_t* row_end) {
+  if (!n_ranks || g >= n_ranks || !row_begin || !row_end) return fail(VDI_ERR_INVALID_ARG, "bad strip query");
+  *row_begin = strip_row(height, n_ranks, g);
+  *row_end = strip_row(height, n_ranks, g + 1);
+  return VDI_OK;
+}
+
+uint32_t vdi_pe_home(uint32_t n_pes, uint32_t n_ranks, uint32_t pe) {
+  if (!n_pes) return 0;
+  return (uint32_t)((uint64_t)pe * n_ranks / n_pes);
+}
+
+uint64_t vdi_full_bytes(uint32_t width, uint32_t rows, uint32_t k) {
+  return (uint64_t)width * rows * (1ull + 24ull * k);
+}
+
+vdi_status vdi_get_unique_id(uint8_t out[128]) {
+  if (!out) return fail(VDI_ERR_INVALID_ARG, "out is NULL");
+  ncclUniqueId id;
+  ncclResult_t r = ncclGetUniqueId(&id);
+  if (r != ncclSuccess) return fail(VDI_ERR_NCCL, "ncclGetUniqueId: %s", ncclGetErrorString(r));
+  static_assert(sizeof(id) == 128, "ncclUniqueId size");
+  memcpy(out, &id, 128);
+  return VDI_OK;
+}
+
+vdi_status vdi_composite_init(const vdi_config* cfg, vdi_ctx** out) {
+  if (!cfg || !out) return fail(VDI_ERR_INVALID_ARG, "cfg/out is NULL");
+  *out = nullptr;
+  if (!cfg->width || !cfg->height) return fail(VDI_ERR_INVALID_ARG, "empty image");
+  if (cfg->k_in < 1 || cfg->k_in > 255 || cfg->k_out < 1 || cfg->k_out > 255)
+    return fail(VDI_ERR_INVALID_ARG, "k_in/k_out must be in 1..255");
+  if (cfg->n_pes < 1 || cfg->n_pes > VDI_MAX_SRC)
+    return fail(VDI_ERR_INVALID_ARG, "n_pes must be in 1..%d", VDI_MAX_SRC);
+  if (cfg->n_ranks < 1 || cfg->rank >= cfg->n_ranks) return fail(VDI_ERR_INVALID_ARG, "bad rank/n_ranks");
+  if (cfg->n_ranks > cfg->height) return fail(VDI_ERR_INVALID_ARG, "more ranks than image rows");
+  if (cfg->n_ranks > 1 && !cfg->nccl_unique_id) return fail(VDI_ERR_INVALID_ARG, "nccl_unique_id required");
+  if ((uint64_t)cfg->width * cfg->height > (1ull << 31)) return fail(VDI_ERR_INVALID_ARG, "image too large");
+  vdi_ctx* ctx = new vdi_ctx();
+  ctx->cfg = *cfg;
+  if (!ctx->cfg.max_iters) ctx->cfg.max_iters = 16;
+  if (!(ctx->cfg.gamma_max > 0.0f)) ctx->cfg.gamma_max = 2.0f;
+  ctx->cfg.nccl_unique_id = nullptr;
+  ctx->stream = static_cast<cudaStream_t>(cfg->cuda_stream);
+  cudaError_t e = cudaGetDevice(&ctx->device);
+  if (e != cudaSuccess) {
+    delete ctx;
+    return fail(VDI_ERR_CUDA, "cudaGetDevice: %s", cudaGetErrorString(e));
+  }
+  ctx->row0 = strip_row(cfg->height, cfg->n_ranks, cfg->rank);
+  ctx->row1 = strip_row(cfg->height, cfg->n_ranks, cfg->rank + 1);
+  ctx->P = (uint64_t)(ctx->row1 - ctx->row0) * cfg->width;
+  ctx->rcount.resize(cfg->n_pes);
+  ctx->rdepth.resize(cfg->n_pes);
+  ctx->rrgba.resize(cfg->n_pes);
+  ctx->gen.resize(cfg->n_pes);
+  ctx->hcount.resize(cfg->n_pes);
+  ctx->hoffset.resize(cfg->n_pes);
+  ctx->hdepth.resize(cfg->n_pes);
+  ctx->hrgba.resize(cfg->n_pes);
+  for (auto& ev : ctx->ev) cudaEventCreate(&ev);
+  for (auto& ev : ctx->gev) cudaEventCreate(&ev);
+  if (cfg->n_ranks > 1) {
+    ncclUniqueId id;
+    memcpy(&id, cfg->nccl_unique_id, sizeof id);
+    ncclResult_t r = ncclCommInitRank(&ctx->comm, (int)cfg->n_ranks, id, (int)cfg->rank);
+    if (r != ncclSuccess) {
+      ctx->comm = nullptr;
+      delete ctx;
+      return fail(VDI_ERR_NCCL, "ncclCommInitRank: %s", ncclGetErrorString(r));
+    }
+  }
+  *out = ctx;
+  return VDI_OK;
+}
+
+void vdi_composite_destroy(vdi_ctx* ctx) { delete ctx; }
+
+// ---------------------------------------------------------------------------
+// Phase 1 (SUPPORT)
+// ---------------------------------------------------------------------------
+vdi_status vdi_generate_subvdi(vdi_ctx* ctx, const vdi_volume_desc* vol, const vdi_tf_desc* tf,
+                               const vdi_camera* cam, const vdi_decomp_desc* dec, uint32_t pe_id,
+                               vdi_dense_view* out) {
+  if (vdi_status s = check_ctx(ctx)) return s;
+  if (!vol || !tf || !cam || !dec || !out || !vol->voxels || !tf->table)
+    return fail(VDI_ERR_INVALID_ARG, "NULL argument");
+  if (pe_id >= ctx->cfg.n_pes) return fail(VDI_ERR_INVALID_ARG, "pe_id out of range");
+  if (vol->bytes_per_voxel != 1 && vol->bytes_per_voxel != 2)
+    return fail(VDI_ERR_INVALID_ARG, "bytes_per_voxel must be 1 or 2");
+  for (int a = 0; a < 3; ++a) {
+    if (!vol->dims[a]) return fail(VDI_ERR_INVALID_ARG, "empty volume");
+    if (dec->grid[a] < 1 || dec->grid[a] > VDI_MAX_GRID_AXIS)
+      return fail(VDI_ERR_INVALID_ARG, "decomposition grid must be 1..%d per axis", VDI_MAX_GRID_AXIS);
+  }
+  if (!dec->xb || !dec->yb || !dec->zb || !dec->owner) return fail(VDI_ERR_INVALID_ARG, "NULL decomposition");
+  GenParams gp{};
+  gp.vox = vol->voxels;
+  gp.bytes = (int)vol->bytes_per_voxel;
+  for (int a = 0; a < 3; ++a) {
+    gp.dims[a] = (int)vol->dims[a];
+    gp.grid[a] = (int)dec->grid[a];
+    gp.eye[a] = cam->eye[a];
+    gp.fwd[a] = cam->fwd[a];
+    gp.right[a] = cam->right[a];
+    gp.up[a] = cam->up[a];
+  }
+  gp.tf = reinterpret_cast<const float4*>(tf->table);
+  gp.tan_x = cam->tan_x;
+  gp.tan_y = cam->tan_y;
+  gp.W = (int)ctx->cfg.width;
+  gp.H = (int)ctx->cfg.height;
+  for (uint32_t i = 0; i <= dec->grid[0]; ++i) gp.xb[i] = dec->xb[i];
+  for (uint32_t i = 0; i <= dec->grid[1]; ++i) gp.yb[i] = dec->yb[i];
+  for (uint32_t i = 0; i <= dec->grid[2]; ++i) gp.zb[i] = dec->zb[i];
+  const size_t nb = (size_t)dec->grid[0] * dec->grid[1] * dec->grid[2];
+  std::vector<int8_t> own(nb);
+  float lo[3] = {1e30f, 1e30f, 1e30f}, hi[3] = {-1e30f, -1e30f, -1e30f};
+  bool any = false;
+  for (uint32_t bz = 0; bz < dec->grid[2]; ++bz)
+    for (uint32_t by = 0; by < dec->grid[1]; ++by)
+      for (uint32_t bx = 0; bx < dec->grid[0]; ++bx) {
+        const size_t b = ((size_t)bz * dec->grid[1] + by) * dec->grid[0] + bx;
+        const int o = dec->owner[b];
+        if (o < -1 || o >= 127) return fail(VDI_ERR_INVALID_ARG, "owner id out of range");
+        own[b] = (int8_t)o;
+        if (o == (int)pe_id) {
+          any = true;
+          const int l[3] = {dec->xb[bx], dec->yb[by], dec->zb[bz]};
+          const int h[3] = {dec->xb[bx + 1], dec->yb[by + 1], dec->zb[bz + 1]};
+          for (int a = 0; a < 3; ++a) {
+            lo[a] = std::min(lo[a], (float)l[a]);
+            hi[a] = std::max(hi[a], (float)h[a]);
+          }
+        }
+      }
+  if (!any)
+    for (int a = 0; a < 3; ++a) lo[a] = hi[a] = -1e6f;  // empty domain: no samples
+  for (int a = 0; a < 3; ++a) {
+    gp.lo[a] = lo[a];
+    gp.hi[a] = hi[a];
+  }
+  gp.pe = (int)pe_id;
+  gp.k = (int)ctx->cfg.k_in;
+  gp.max_iters = (int)ctx->cfg.max_iters;
+  gp.gamma_max = ctx->cfg.gamma_max;
+
+  GenOut& g = ctx->gen[pe_id];
+  const size_t P = (size_t)ctx->cfg.width * ctx->cfg.height;
+  CUDA_TRY(ctx, g.owner.grow(nb));
+  CUDA_TRY(ctx, cudaMemcpyAsync(g.owner.p, own.data(), nb, cudaMemcpyHostToDevice, ctx->stream));
+  gp.owner = g.owner.as<int8_t>();
+  CUDA_TRY(ctx, g.count32.grow((P + 1) * 4));
+  CUDA_TRY(ctx, g.count8.grow(P));
+  CUDA_TRY(ctx, g.offset.grow((P + 1) * 4));
+  CUDA_TRY(ctx, g.gamma.grow(P * 4));
+  CUDA_TRY(ctx, ctx->gen_tmp.grow(16));
+  int* derr = ctx->gen_tmp.as<int>();
+  CUDA_TRY(ctx, cudaMemsetAsync(derr, 0, 4, ctx->stream));
+  CUDA_TRY(ctx, launch_gen_pass1(gp, g.count32.as<uint32_t>(), g.gamma.as<float>(), derr, ctx->stream));
+  CUDA_TRY(ctx, gen_scan(g.count32.as<uint32_t>(), g.offset.as<uint32_t>(), P + 1, &ctx->cub_tmp,
+                         &ctx->cub_tmp_bytes, ctx->stream));
+  uint32_t total32 = 0;
+  int herr = 0;
+  CUDA_TRY(ctx, cudaMemcpyAsync(&total32, g.offset.as<uint32_t>() + P, 4, cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(ctx, cudaMemcpyAsync(&herr, derr, 4, cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  if (herr & 2) return fail(VDI_ERR_CAPACITY, "a ray of PE %u needs more than k_in supersegments (Q20)", pe_id);
+  g.total = total32;
+  CUDA_TRY(ctx, g.depth.grow(std::max<size_t>(g.total, 1) * 8));
+  CUDA_TRY(ctx, g.rgba.grow(std::max<size_t>(g.total, 1) * 16));
+  CUDA_TRY(ctx, launch_gen_pass2(gp, g.offset.as<uint32_t>(), g.gamma.as<float>(), g.count32.as<uint32_t>(),
+                                 g.depth.as<float2>(), g.rgba.as<float4>(), ctx->stream));
+  CUDA_TRY(ctx, launch_u32_to_u8(g.count32.as<uint32_t>(), g.count8.as<uint8_t>(), P, ctx->stream));
+  out->pe_id = pe_id;
+  out->total = g.total;
+  out->count = g.count8.as<uint8_t>();
+  out->offset = g.offset.as<uint32_t>();
+  out->depth = g.depth.as<float>();
+  out->rgba = g.rgba.as<float>();
+  return VDI_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Phase 2: the hot path
+// ---------------------------------------------------------------------------
+vdi_status vdi_composite(vdi_ctx* ctx, const vdi_dense_view* local, uint32_t n_local, vdi_full_view* so) {
+  if (vdi_status s = check_ctx(ctx)) return s;
+  const vdi_config& cf = ctx->cfg;
+  const uint32_t G = cf.n_ranks, me = cf.rank, n = cf.n_pes, W = cf.width, k = cf.k_out;
+  if (!so || !so->count || !so->depth || !so->rgba) return fail(VDI_ERR_INVALID_ARG, "strip_out is NULL");
+  if (so->row_begin != ctx->row0 || so->row_end != ctx->row1)
+    return fail(VDI_ERR_CAPACITY, "strip_out rows [%u,%u) != this rank's strip [%u,%u)", so->row_begin,
+                so->row_end, ctx->row0, ctx->row1);
+  if ((reinterpret_cast<uintptr_t>(so->rgba) & 15) || (reinterpret_cast<uintptr_t>(so->depth) & 7))
+    return fail(VDI_ERR_INVALID_ARG, "strip_out depth/rgba must be 8/16-byte aligned");
+  // which PEs are homed here (PAPER.md:218 block placement)
+  std::vector<int> slot(n, -1);
+  uint32_t expect = 0;
+  for (uint32_t s = 0; s < n; ++s)
+    if (vdi_pe_home(n, G, s) == me) ++expect;
+  if (n_local != expect) return fail(VDI_ERR_INVALID_ARG, "rank %u homes %u PEs, got %u", me, expect, n_local);
+  if (n_local && !local) return fail(VDI_ERR_INVALID_ARG, "local_pes is NULL");
+  for (uint32_t l = 0; l < n_local; ++l) {
+    const vdi_dense_view& v = local[l];
+    if (v.pe_id >= n || vdi_pe_home(n, G, v.pe_id) != me || slot[v.pe_id] >= 0)
+      return fail(VDI_ERR_INVALID_ARG, "pe_id %u not homed on rank %u or duplicated", v.pe_id, me);
+    if (!v.count || (v.total && (!v.depth || !v.rgba)) || (G > 1 && !v.offset))
+      return fail(VDI_ERR_INVALID_ARG, "dense view of PE %u has NULL arrays", v.pe_id);
+    if ((reinterpret_cast<uintptr_t>(v.rgba) & 15) || (reinterpret_cast<uintptr_t>(v.depth) & 7))
+      return fail(VDI_ERR_INVALID_ARG, "dense view of PE %u: depth/rgba misaligned", v.pe_id);
+    slot[v.pe_id] = (int)l;
+  }
+  cudaStream_t st = ctx->stream;
+  const bool timing = cf.flags & VDI_FLAG_STAGE_TIMING;
+  int launches = 0;
+  if (timing) CUDA_TRY(ctx, cudaEventRecord(ctx->ev[0], st));
+
+  MergeParams mp{};
+  mp.n_src = (int)n;
+  mp.k_out = (int)k;
+  mp.max_iters = (int)cf.max_iters;
+  mp.gamma_max = cf.gamma_max;
+  mp.P = (uint32_t)ctx->P;
+  mp.n_groups = (uint32_t)((ctx->P + 31) / 32);
+  uint64_t S_here = 0, sent = 0, recvd = 0;
+
+  if (G == 1) {
+    for (uint32_t s = 0; s < n; ++s) {
+      const vdi_dense_view& v = local[slot[s]];
+      mp.src[s] = SrcDesc{v.count, reinterpret_cast<const float2*>(v.depth), reinterpret_cast<const float4*>(v.rgba)};
+      S_here += v.total;
+    }
+  } else {
+    // strip boundaries of every PE's dense payload: bnd[s][g] = offset_s[row_g * W]
+    std::vector<uint32_t> rows(G + 1);
+    for (uint32_t g = 0; g <= G; ++g) rows[g] = strip_row(cf.height, G, g);
+    const size_t nb = (size_t)n * (G + 1);
+    const size_t hdr = 64 * 8 + 64 * 4 + 64 * 4;  // ptrs, pes, rows
+    CUDA_TRY(ctx, ctx->bounds.grow(nb * 8 + hdr));
+    std::vector<uint8_t> h(hdr, 0);
+    const uint32_t** hp = reinterpret_cast<const uint32_t**>(h.data());
+    uint32_t* hpes = reinterpret_cast<uint32_t*>(h.data() + 64 * 8);
+    uint32_t* hrows = reinterpret_cast<uint32_t*>(h.data() + 64 * 8 + 64 * 4);
+    for (uint32_t l = 0; l < n_local; ++l) {
+      hp[l] = local[l].offset;
+      hpes[l] = local[l].pe_id;
+    }
+    for (uint32_t g = 0; g <= G; ++g) hrows[g] = rows[g];
+    uint8_t* dh = ctx->bounds.as<uint8_t>() + nb * 8;
+    unsigned long long* dbnd = ctx->bounds.as<unsigned long long>();
+    CUDA_TRY(ctx, cudaMemcpyAsync(dh, h.data(), hdr, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(ctx, cudaMemsetAsync(dbnd, 0, nb * 8, st));
+    gather_bounds_kernel<<<1, 256, 0, st>>>(reinterpret_cast<const uint32_t* const*>(dh),
+                                            reinterpret_cast<const uint32_t*>(dh + 64 * 8), (int)n_local,
+                                            reinterpret_cast<const uint32_t*>(dh + 64 * 8 + 64 * 4), (int)G, W,
+                                            (int)n, dbnd);
+    ++launches;
+    CUDA_TRY(ctx, cudaGetLastError());
+    // size exchange (every rank contributes the rows of its PEs; sum = gather)
+    NCCL_TRY(ctx, ncclAllReduce(dbnd, dbnd, nb, ncclUint64, ncclSum, ctx->comm, st));
+    std::vector<unsigned long long> bnd(nb);
+    CUDA_TRY(ctx, cudaMemcpyAsync(bnd.data(), dbnd, nb * 8, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(ctx, cudaStreamSynchronize(st));
+    auto T = [&](uint32_t s, uint32_t g) { return bnd[(size_t)s * (G + 1) + g + 1] - bnd[(size_t)s * (G + 1) + g]; };
+    for (uint32_t s = 0; s < n; ++s) {
+      if (slot[s] >= 0) continue;
+      CUDA_TRY(ctx, ctx->rcount[s].grow(ctx->P));
+      CUDA_TRY(ctx, ctx->rdepth[s].grow(std::max<uint64_t>(T(s, me), 1) * 8));
+      CUDA_TRY(ctx, ctx->rrgba[s].grow(std::max<uint64_t>(T(s, me), 1) * 16));
+    }
+    // all-to-allv of count slices and dense payload slices
+    NCCL_TRY(ctx, ncclGroupStart());
+    for (uint32_t g = 0; g < G; ++g) {
+      if (g == me) continue;
+      const uint64_t Pg = (uint64_t)(rows[g + 1] - rows[g]) * W;
+      for (uint32_t s = 0; s < n; ++s) {  // our PEs -> g
+        if (slot[s] < 0) continue;
+        const vdi_dense_view& v = local[slot[s]];
+        const uint64_t b = bnd[(size_t)s * (G + 1) + g], t = T(s, g);
+        NCCL_TRY(ctx, ncclSend(v.count + (size_t)rows[g] * W, Pg, ncclUint8, (int)g, ctx->comm, st));
+        if (t) {
+          NCCL_TRY(ctx, ncclSend(v.depth + b * 2, t * 2, ncclFloat32, (int)g, ctx->comm, st));
+          NCCL_TRY(ctx, ncclSend(v.rgba + b * 4, t * 4, ncclFloat32, (int)g, ctx->comm, st));
+        }
+        sent += Pg + 24 * t;
+      }
+      for (uint32_t s = 0; s < n; ++s) {  // g's PEs -> us
+        if (vdi_pe_home(n, G, s) != g) continue;
+        const uint64_t t = T(s, me);
+        NCCL_TRY(ctx, ncclRecv(ctx->rcount[s].p, ctx->P, ncclUint8, (int)g, ctx->comm, st));
+        if (t) {
+          NCCL_TRY(ctx, ncclRecv(ctx->rdepth[s].p, t * 2, ncclFloat32, (int)g, ctx->comm, st));
+          NCCL_TRY(ctx, ncclRecv(ctx->rrgba[s].p, t * 4, ncclFloat32, (int)g, ctx->comm, st));
+        }
+        recvd += ctx->P + 24 * t;
+      }
+    }
+    NCCL_TRY(ctx, ncclGroupEnd());
+    for (uint32_t s = 0; s < n; ++s) {
+      const uint64_t t = T(s, me);
+      S_here += t;
+      if (slot[s] >= 0) {
+        const vdi_dense_view& v = local[slot[s]];
+        const uint64_t b = bnd[(size_t)s * (G + 1) + me];
+        mp.src[s] = SrcDesc{v.count + (size_t)ctx->row0 * W, reinterpret_cast<const float2*>(v.depth) + b,
+                            reinterpret_cast<const float4*>(v.rgba) + b};
+      } else {
+        mp.src[s] = SrcDesc{ctx->rcount[s].as<uint8_t>(), ctx->rdepth[s].as<float2>(), ctx->rrgba[s].as<float4>()};
+      }
+    }
+  }
+  if (timing) CUDA_TRY(ctx, cudaEventRecord(ctx->ev[1], st));
+
+  // buffers of the merge
+  const size_t ng = mp.n_groups;
+  CUDA_TRY(ctx, ctx->group_sum.grow(ng * n * 4));
+  CUDA_TRY(ctx, ctx->group_base.grow(ng * n * 4));
+  CUDA_TRY(ctx, ctx->totals.grow(n * 8));
+  CUDA_TRY(ctx, ctx->wl.grow(std::max<size_t>(ctx->P, 1) * (3 + n) * 4));
+  CUDA_TRY(ctx, ctx->scratch.grow(std::max<uint64_t>(4 * S_here, 1) * sizeof(Rec)));
+  CUDA_TRY(ctx, ctx->dcnt.grow(sizeof(DevCounters)));
+  const bool stats = cf.flags & VDI_FLAG_PIXEL_STATS;
+  if (stats) {
+    CUDA_TRY(ctx, ctx->stat_gamma.grow(ctx->P * 4));
+    CUDA_TRY(ctx, ctx->stat_m.grow(ctx->P * 2));
+  }
+  DevCounters* dc = ctx->dcnt.as<DevCounters>();
+  CUDA_TRY(ctx, cudaMemsetAsync(dc, 0, sizeof(DevCounters), st));
+  mp.group_base = ctx->group_base.as<uint32_t>();
+  mp.out_count = so->count;
+  mp.out_depth = reinterpret_cast<float2*>(so->depth);
+  mp.out_rgba = reinterpret_cast<float4*>(so->rgba);
+  mp.wl = ctx->wl.as<uint32_t>();
+  mp.wl_count = &dc->wl_count;
+  mp.wl_cap = (uint32_t)std::max<uint64_t>(ctx->P, 1);
+  mp.scratch_used = &dc->scratch_used;
+  mp.scratch_cap = 4 * S_here;
+  mp.scratch = ctx->scratch.as<Rec>();
+  mp.stat_gamma = stats ? ctx->stat_gamma.as<float>() : nullptr;
+  mp.stat_m = stats ? ctx->stat_m.as<uint16_t>() : nullptr;
+  mp.records_in = &dc->records_in;
+  mp.err = &dc->err;
+  mp.validate = (cf.flags & VDI_FLAG_VALIDATE) ? 1 : 0;
+  if (ctx->P) {
+    CUDA_TRY(ctx, launch_group_sums(mp, ctx->group_sum.as<uint32_t>(), st, &launches));
+    CUDA_TRY(ctx, launch_group_scan(mp, ctx->group_sum.as<uint32_t>(), ctx->group_base.as<uint32_t>(),
+                                    ctx->totals.as<uint64_t>(), st, &launches));
+    CUDA_TRY(ctx, launch_merge(mp, st, &launches));
+  }
+  if (timing) {
+    CUDA_TRY(ctx, cudaEventRecord(ctx->ev[2], st));
+    ctx->timing_pending = true;
+  }
+  ctx->have_stats = stats;
+  ctx->last = vdi_counters{};
+  ctx->last.bytes_sent = sent;
+  ctx->last.bytes_received = recvd;
+  ctx->last.kernel_launches = (uint32_t)launches;
+  return VDI_OK;
+}
+
+vdi_status vdi_gather(vdi_ctx* ctx, const vdi_full_view* strip, vdi_full_view* image) {
+  if (vdi_status s = check_ctx(ctx)) return s;
+  const vdi_config& cf = ctx->cfg;
+  const uint32_t G = cf.n_ranks, me = cf.rank, W = cf.width, k = cf.k_out;
+  if (!strip || !strip->count || !strip->depth || !strip->rgba)
+    return fail(VDI_ERR_INVALID_ARG, "strip is NULL");
+  if (strip->row_begin != ctx->row0 || strip->row_end != ctx->row1)
+    return fail(VDI_ERR_CAPACITY, "strip rows do not match this rank");
+  const bool root = me == 0;
+  if (root && (!image || !image->count || !image->depth || !image->rgba || image->row_begin != 0 ||
+               image->row_end != cf.height))
+    return fail(VDI_ERR_INVALID_ARG, "root image_out must cover rows [0, H)");
+  cudaStream_t st = ctx->stream;
+  const bool timing = cf.flags & VDI_FLAG_STAGE_TIMING;
+  if (timing) CUDA_TRY(ctx, cudaEventRecord(ctx->gev[0], st));
+  auto copy_strip = [&](uint32_t row0, const vdi_full_view* src) -> cudaError_t {
+    const size_t P = (size_t)(src->row_end - src->row_begin) * W;
+    const size_t o = (size_t)row0 * W;
+    cudaError_t e = cudaSuccess;
+    if (image->count + o != src->count)
+      e = cudaMemcpyAsync(image->count + o, src->count, P, cudaMemcpyDeviceToDevice, st);
+    if (e == cudaSuccess && image->depth + o * k * 2 != src->depth)
+      e = cudaMemcpyAsync(image->depth + o * k * 2, src->depth, P * k * 8, cudaMemcpyDeviceToDevice, st);
+    if (e == cudaSuccess && image->rgba + o * k * 4 != src->rgba)
+      e = cudaMemcpyAsync(image->rgba + o * k * 4, src->rgba, P * k * 16, cudaMemcpyDeviceToDevice, st);
+    return e;
+  };
+  if (G == 1) {
+    CUDA_TRY(ctx, copy_strip(0, strip));
+  } else {
+    // MPI_Gather of the full-representation strips as grouped send/recv
+    NCCL_TRY(ctx, ncclGroupStart());
+    if (root) {
+      for (uint32_t g = 1; g < G; ++g) {
+        const uint32_t r0 = strip_row(cf.height, G, g), r1 = strip_row(cf.height, G, g + 1);
+        const size_t P = (size_t)(r1 - r0) * W, o = (size_t)r0 * W;
+        NCCL_TRY(ctx, ncclRecv(image->count + o, P, ncclUint8, (int)g, ctx->comm, st));
+        NCCL_TRY(ctx, ncclRecv(image->depth + o * k * 2, P * k * 2, ncclFloat32, (int)g, ctx->comm, st));
+        NCCL_TRY(ctx, ncclRecv(image->rgba + o * k * 4, P * k * 4, ncclFloat32, (int)g, ctx->comm, st));
+      }
+    } else {
+      const size_t P = ctx->P;
+      NCCL_TRY(ctx, ncclSend(strip->count, P, ncclUint8, 0, ctx->comm, st));
+      NCCL_TRY(ctx, ncclSend(strip->depth, P * k * 2, ncclFloat32, 0, ctx->comm, st));
+      NCCL_TRY(ctx, ncclSend(strip->rgba, P * k * 4, ncclFloat32, 0, ctx->comm, st));
+    }
+    NCCL_TRY(ctx, ncclGroupEnd());
+    if (root) CUDA_TRY(ctx, copy_strip(0, strip));
+  }
+  if (timing) {
+    CUDA_TRY(ctx, cudaEventRecord(ctx->gev[1], st));
+    ctx->gather_timing_pending = true;
+  }
+  return VDI_OK;
+}
+
+vdi_status vdi_composite_host(vdi_ctx* ctx, const vdi_dense_view* local, uint32_t n_local, vdi_full_view* so) {
+  if (vdi_status s = check_ctx(ctx)) return s;
+  const vdi_config& cf = ctx->cfg;
+  if (!so || !so->count || !so->depth || !so->rgba) return fail(VDI_ERR_INVALID_ARG, "strip_out is NULL");
+  if (n_local && !local) return fail(VDI_ERR_INVALID_ARG, "local_pes is NULL");
+  if (n_local > cf.n_pes) return fail(VDI_ERR_INVALID_ARG, "too many local PEs");
+  cudaStream_t st = ctx->stream;
+  const size_t P = (size_t)cf.width * cf.height;
+  std::vector<vdi_dense_view> dv(n_local);
+  for (uint32_t l = 0; l < n_local; ++l) {
+    const vdi_dense_view& v = local[l];
+    if (!v.count || (v.total && (!v.depth || !v.rgba)) || (cf.n_ranks > 1 && !v.offset))
+      return fail(VDI_ERR_INVALID_ARG, "host view %u has NULL arrays", l);
+    CUDA_TRY(ctx, ctx->hcount[l].grow(P));
+    CUDA_TRY(ctx, ctx->hdepth[l].grow(std::max<uint64_t>(v.total, 1) * 8));
+    CUDA_TRY(ctx, ctx->hrgba[l].grow(std::max<uint64_t>(v.total, 1) * 16));
+    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->hcount[l].p, v.count, P, cudaMemcpyHostToDevice, st));
+    if (v.total) {
+      CUDA_TRY(ctx, cudaMemcpyAsync(ctx->hdepth[l].p, v.depth, v.total * 8, cudaMemcpyHostToDevice, st));
+      CUDA_TRY(ctx, cudaMemcpyAsync(ctx->hrgba[l].p, v.rgba, v.total * 16, cudaMemcpyHostToDevice, st));
+    }
+    dv[l] = v;
+    dv[l].count = ctx->hcount[l].as<uint8_t>();
+    dv[l].depth = ctx->hdepth[l].as<float>();
+    dv[l].rgba = ctx->hrgba[l].as<float>();
+    if (cf.n_ranks > 1) {
+      CUDA_TRY(ctx, ctx->hoffset[l].grow((P + 1) * 4));
+      CUDA_TRY(ctx, cudaMemcpyAsync(ctx->hoffset[l].p, v.offset, (P + 1) * 4, cudaMemcpyHostToDevice, st));
+      dv[l].offset = ctx->hoffset[l].as<uint32_t>();
+    } else {
+      dv[l].offset = nullptr;
+    }
+  }
+  const size_t Ps = ctx->P, k = cf.k_out;
+  CUDA_TRY(ctx, ctx->hstrip_count.grow(Ps));
+  CUDA_TRY(ctx, ctx->hstrip_depth.grow(Ps * k * 8));
+  CUDA_TRY(ctx, ctx->hstrip_rgba.grow(Ps * k * 16));
+  vdi_full_view ds{ctx->row0, ctx->row1, ctx->hstrip_count.as<uint8_t>(), ctx->hstrip_depth.as<float>(),
+                   ctx->hstrip_rgba.as<float>()};
+  if (vdi_status s = vdi_composite(ctx, dv.data(), n_local, &ds)) return s;
+  CUDA_TRY(ctx, cudaMemcpyAsync(so->count, ds.count, Ps, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(ctx, cudaMemcpyAsync(so->depth, ds.depth, Ps * k * 8, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(ctx, cudaMemcpyAsync(so->rgba, ds.rgba, Ps * k * 16, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(ctx, cudaStreamSynchronize(st));
+  return VDI_OK;
+}
+
+vdi_status vdi_pixel_stats(vdi_ctx* ctx, float* gamma, uint16_t* m) {
+  if (vdi_status s = check_ctx(ctx)) return s;
+  if (!ctx->have_stats) return fail(VDI_ERR_STATE, "VDI_FLAG_PIXEL_STATS was not set for the last composite");
+  if (gamma)
+    CUDA_TRY(ctx, cudaMemcpyAsync(gamma, ctx->stat_gamma.p, ctx->P * 4, cudaMemcpyDeviceToDevice, ctx->stream));
+  if (m) CUDA_TRY(ctx, cudaMemcpyAsync(m, ctx->stat_m.p, ctx->P * 2, cudaMemcpyDeviceToDevice, ctx->stream));
+  return VDI_OK;
+}
+
+vdi_status vdi_get_counters(vdi_ctx* ctx, vdi_counters* out) {
+  if (vdi_status s = check_ctx(ctx)) return s;
+  if (!out) return fail(VDI_ERR_INVALID_ARG, "out is NULL");
+  DevCounters h{};
+  if (ctx->dcnt.p) {
+    CUDA_TRY(ctx, cudaMemcpyAsync(&h, ctx->dcnt.p, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  }
+  if (h.err & 1) return fail(VDI_ERR_INTERNAL, "merge work list / scratch overflow");
+  ctx->last.records_in = h.records_in;
+  ctx->last.searched_lists = h.wl_count;
+  if (ctx->timing_pending) {
+    CUDA_TRY(ctx, cudaEventElapsedTime(&ctx->last.ms_exchange, ctx->ev[0], ctx->ev[1]));
+    CUDA_TRY(ctx, cudaEventElapsedTime(&ctx->last.ms_merge, ctx->ev[1], ctx->ev[2]));
+    ctx->timing_pending = false;
+  }
+  if (ctx->gather_timing_pending) {
+    CUDA_TRY(ctx, cudaEventElapsedTime(&ctx->last.ms_gather, ctx->gev[0], ctx->gev[1]));
+    ctx->gather_timing_pending = false;
+  }
+  *out = ctx->last;
+  return VDI_OK;
+}
+
+}  // extern "C"

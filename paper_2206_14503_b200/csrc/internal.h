@@ -1,0 +1,90 @@
+// internal.h — libvdi internals shared by the .cu translation units.
+// Product code (sm_100a).  Shares nothing with oracle/.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "vdi.h"
+
+#define VDI_MAX_SRC 64        // sources (PEs) supported by one composite
+#define VDI_MAX_GRID_AXIS 16  // bricks per axis in a decomposition
+
+namespace vdi {
+
+// 24-byte record of the sub-supersegment scratch (AoS).
+struct Rec {
+  float tf, tb, r, g, b, a;
+};
+
+// One composite source (PE) as seen by the merge kernels: the strip's count
+// slice and the payload slice, rebased so that the first record of the
+// strip's first list is at index 0.
+struct SrcDesc {
+  const uint8_t* count;
+  const float2* depth;
+  const float4* rgba;
+};
+
+struct MergeParams {
+  SrcDesc src[VDI_MAX_SRC];
+  int n_src;
+  int k_out;
+  int max_iters;
+  float gamma_max;
+  uint32_t P;          // lists in the strip
+  uint32_t n_groups;   // ceil(P / 32)
+  const uint32_t* group_base;  // [n_src][n_groups] exclusive scan of 32-list group sums
+  uint8_t* out_count;          // [P]
+  float2* out_depth;           // [P][k_out]
+  float4* out_rgba;            // [P][k_out]
+  // slow-path work list: entry i = wl[i*(3+n_src) ...] = {p, scratch_base, m, off[0..n_src)}
+  uint32_t* wl;
+  uint32_t* wl_count;
+  uint32_t wl_cap;
+  unsigned long long* scratch_used;
+  unsigned long long scratch_cap;  // in records
+  Rec* scratch;
+  float* stat_gamma;   // optional [P]
+  uint16_t* stat_m;    // optional [P]
+  unsigned long long* records_in;
+  int* err;            // bit 0: work list / scratch overflow, bit 1: invalid input
+  int validate;
+};
+
+// Launchers (merge.cu)
+cudaError_t launch_group_sums(const MergeParams& mp, uint32_t* group_sum, cudaStream_t st, int* launches);
+cudaError_t launch_group_scan(const MergeParams& mp, const uint32_t* group_sum, uint32_t* group_base,
+                              uint64_t* totals, cudaStream_t st, int* launches);
+cudaError_t launch_merge(const MergeParams& mp, cudaStream_t st, int* launches);
+
+// Generator (generate.cu)
+struct GenParams {
+  const void* vox;
+  int bytes;
+  int dims[3];
+  const float4* tf;
+  float eye[3], fwd[3], right[3], up[3];
+  float tan_x, tan_y;
+  int W, H;
+  int grid[3];
+  int xb[VDI_MAX_GRID_AXIS + 1], yb[VDI_MAX_GRID_AXIS + 1], zb[VDI_MAX_GRID_AXIS + 1];
+  const int8_t* owner;  // device [gx*gy*gz]
+  float lo[3], hi[3];   // PE bounding box in continuous voxel coordinates
+  int pe;
+  int k;
+  int max_iters;
+  float gamma_max;
+};
+cudaError_t launch_gen_pass1(const GenParams& gp, uint32_t* count32, float* gamma, int* err,
+                             cudaStream_t st);
+cudaError_t launch_gen_pass2(const GenParams& gp, const uint32_t* offset, const float* gamma,
+                             const uint32_t* count32, float2* depth, float4* rgba, cudaStream_t st);
+cudaError_t gen_scan(const uint32_t* count32, uint32_t* offset, size_t n, void** tmp, size_t* tmp_bytes,
+                     cudaStream_t st);
+cudaError_t launch_u32_to_u8(const uint32_t* in, uint8_t* out, size_t n, cudaStream_t st);
+
+}  // namespace vdi

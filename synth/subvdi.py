@@ -10,8 +10,9 @@ Recipe (SURVEY §8(d) "merge-only microbench", seed 7):
     profile (1 at the centre, 0 outside a disc of radius 0.48 W);
   * a record covers its whole slot, so adjacent occupied slots abut (gaps only
     where slots are empty); alpha ~ U(0.01, 0.9), rgb = alpha * U(0,1)^3;
-  * overlap=True jitters every record by up to +-0.6 slot so records of
-    different PEs overlap (exercises step 2, subdivision).
+  * overlap=True shifts every (list, PE) run by up to +-0.6 slot so records of
+    different PEs overlap while each PE's run stays front-to-back sorted
+     -- exercises step 2, subdivision.
 Per-PE output: count u8[P], depth f32[S,2] (tf, tb), rgba f32[S,4], pixel-major,
 front-to-back within a pixel (the dense layout of PAPER.md:113-115).
 """
@@ -46,8 +47,8 @@ def random_subvdis(n_pes: int, W: int, H: int, k_in: int, lam: float = 8.0, seed
         slot = j * k_in + (u_idx % k_in)
         tf = np.float32(1.0) + slot.astype(np.float32) * w
         tb = np.float32(1.0) + (slot + 1).astype(np.float32) * w
-        if overlap:
-            jit = (rng.random(len(tf), dtype=np.float32) - np.float32(0.5)) * np.float32(1.2) * w
+        if overlap:  # one shift per (list, PE): runs stay sorted, PEs overlap
+            jit = ((rng.random(P, dtype=np.float32) - np.float32(0.5)) * np.float32(1.2) * w)[p_idx]
             tf = tf + jit
             tb = tb + jit
         a = rng.uniform(0.01, 0.9, len(tf)).astype(np.float32)

@@ -1,0 +1,166 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the
+same seeded inputs.  Inputs come from synth/ (neutral generators) or from
+the oracle itself -- never from the CUDA path."""
+import numpy as np
+import pytest
+import torch
+
+import synth
+from parity import compare, dense_to_device, full_to_numpy
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def vdi():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2206_14503_b200 as vdi
+    vdi._lib.lib()  # fail loudly if libvdi.so is missing
+    return vdi
+
+
+def _gpu_composite(vdi, pes_np, W, H, k_in, k_out, flags=0, host=False):
+    n = len(pes_np)
+    comp = vdi.Compositor(W, H, k_in, k_out, n, flags=flags | vdi._lib.VDI_FLAG_PIXEL_STATS)
+    if host:
+        dev = [dense_to_device(p, i, device="cpu") for i, p in enumerate(pes_np)]
+        strip = comp.empty_strip(device="cpu")
+        comp.composite_host(dev, strip)
+    else:
+        dev = [dense_to_device(p, i) for i, p in enumerate(pes_np)]
+        strip = comp.empty_strip()
+        comp.composite(dev, strip)
+    torch.cuda.synchronize()
+    g, m = comp.pixel_stats()
+    cnt = comp.counters()
+    return strip, g.cpu().numpy(), m.cpu().numpy(), cnt
+
+
+CASES = [
+    # n, W, H, k_in, k_out, lam, overlap
+    (2, 64, 48, 4, 4, 3.0, False),
+    (8, 203, 97, 20, 20, 3.0, False),     # ragged: P = 19691 (not a multiple of 32)
+    (8, 203, 97, 20, 20, 20.0, False),    # search-heavy, m up to 160
+    (4, 100, 37, 8, 3, 4.0, False),       # k_out < k_in
+    (3, 64, 33, 4, 4, 6.0, True),         # overlapping records -> subdivision
+    (1, 77, 41, 20, 20, 10.0, False),     # single PE: identity
+    (16, 96, 64, 32, 32, 16.0, False),    # n = 16, k = 32 (C5-like)
+    (5, 50, 50, 6, 1, 4.0, False),        # k_out = 1
+    (12, 40, 40, 10, 20, 8.0, False),     # non-power-of-two n, k_out > k_in
+    (33, 32, 8, 4, 8, 3.0, False),        # n > 16 (generic path)
+]
+
+
+@pytest.mark.parametrize("case", CASES, ids=[f"n{c[0]}_{c[1]}x{c[2]}_k{c[3]}-{c[4]}_lam{c[5]}{'_ov' if c[6] else ''}"
+                                             for c in CASES])
+def test_merge_parity_random(vdi, orc, case):
+    n, W, H, k_in, k_out, lam, overlap = case
+    pes = synth.random_subvdis(n, W, H, k_in, lam=lam, seed=100 + n, overlap=overlap)
+    ref = orc.composite(pes, W, H, 1, k_out)
+    strip, gam, m, cnt = _gpu_composite(vdi, pes, W, H, k_in, k_out)
+    gc, gd, gr = full_to_numpy(strip)
+    nl, ties = compare(gc, gd, gr, ref["count"], ref["depth"], ref["rgba"], ref["stats"]["margin"], str(case))
+    st = ref["stats"]
+    ok = st["margin"] >= 1e-6
+    assert np.array_equal(gam[ok], st["gamma"][ok])      # the per-list gamma* is reproduced
+    assert np.array_equal(m.astype(np.int64)[ok], st["m"][ok].astype(np.int64))
+    assert cnt["records_in"] == sum(int(p["count"].sum()) for p in pes)
+    print(f"{case}: {nl} lists bit-checked, ties listed: {ties[:20]} ({len(ties)}); searched {cnt['searched_lists']}")
+
+
+def test_empty_and_transparent(vdi, orc):
+    W, H = 70, 30
+    empty = [{"count": np.zeros(W * H, np.uint8), "depth": np.zeros((0, 2), np.float32),
+              "rgba": np.zeros((0, 4), np.float32)} for _ in range(3)]
+    strip, _, _, _ = _gpu_composite(vdi, empty, W, H, 4, 4)
+    gc, gd, gr = full_to_numpy(strip)
+    assert not gc.any() and not gd.any() and not gr.any()
+    # alpha == 0 records are dropped (Q23)
+    pes = synth.random_subvdis(4, W, H, 6, lam=5.0, seed=5)
+    rng = np.random.default_rng(0)
+    for p in pes:
+        z = rng.random(len(p["rgba"])) < 0.2
+        p["rgba"][z] = 0.0
+    ref = orc.composite(pes, W, H, 1, 6)
+    strip, _, _, _ = _gpu_composite(vdi, pes, W, H, 6, 6)
+    compare(*full_to_numpy(strip), ref["count"], ref["depth"], ref["rgba"], ref["stats"]["margin"], "alpha0")
+
+
+def test_host_entry_and_determinism(vdi, orc):
+    W, H, n, k = 128, 72, 6, 12
+    pes = synth.random_subvdis(n, W, H, k, lam=9.0, seed=21)
+    a, *_ = _gpu_composite(vdi, pes, W, H, k, k)
+    b, *_ = _gpu_composite(vdi, pes, W, H, k, k)
+    c, *_ = _gpu_composite(vdi, pes, W, H, k, k, host=True)
+    for x, y in ((a, b), (a, c)):
+        for u, v in zip(full_to_numpy(x), full_to_numpy(y)):
+            assert np.array_equal(u, v)
+
+
+def _c1_scene(orc, view=0, angle=0.0, decomp=None, n_pes=None, k=None):
+    cfg = synth.config_by_name("C1")
+    vol_t = synth.make_volume(cfg)
+    tf = synth.tf_table(cfg.tf)
+    cam = synth.make_camera(cfg.W, cfg.H, view=view, angle_deg=angle)
+    dec = decomp if decomp is not None else cfg.decomposition()
+    sc = orc.scene(orc.volume_numpy(vol_t), cfg.dims, tf, cam, dec)
+    return cfg, vol_t, tf, cam, dec, sc
+
+
+@pytest.mark.parametrize("variant", ["slab", "interleaved_v1"])
+def test_generator_parity_c1(vdi, orc, variant):
+    """vdi_generate_subvdi vs the oracle generator (SUPPORT path)."""
+    if variant == "slab":
+        cfg, vol_t, tf, cam, dec, sc = _c1_scene(orc)
+        n, k = cfg.n_pes, cfg.k_in
+    else:
+        dec = synth.interleaved_decomposition((64, 64, 64), 4, (4, 4, 4), seed=3)
+        cfg, vol_t, tf, cam, dec, sc = _c1_scene(orc, view=1, angle=20.0, decomp=dec)
+        n, k = 4, 8
+    comp = vdi.Compositor(cfg.W, cfg.H, k, k, n)
+    tft = torch.from_numpy(tf).cuda()
+    volc = vol_t.cuda()
+    for pe in range(n):
+        g = comp.generate_subvdi(volc, tft, cam, dec, pe)
+        o = orc.generate_dense(sc, pe, k)
+        assert np.array_equal(g.count.cpu().numpy(), o["count"]), f"pe {pe} counts"
+        assert g.total == len(o["depth"])
+        np.testing.assert_allclose(g.depth.cpu().numpy(), o["depth"], rtol=1e-5)
+        np.testing.assert_allclose(g.rgba.cpu().numpy(), o["rgba"], atol=1e-4)
+
+
+def test_composite_parity_c1_oracle_inputs(vdi, orc):
+    cfg, vol_t, tf, cam, dec, sc = _c1_scene(orc)
+    pes = [orc.generate_dense(sc, pe, cfg.k_in) for pe in range(cfg.n_pes)]
+    ref = orc.composite(pes, cfg.W, cfg.H, 1, cfg.k_out)
+    strip, gam, m, _ = _gpu_composite(vdi, pes, cfg.W, cfg.H, cfg.k_in, cfg.k_out)
+    compare(*full_to_numpy(strip), ref["count"], ref["depth"], ref["rgba"], ref["stats"]["margin"], "C1")
+    # end-to-end on the GPU (GPU generator + GPU composite) rendered at the
+    # generation view equals the oracle's whole-volume DVR
+    comp = vdi.Compositor(cfg.W, cfg.H, cfg.k_in, cfg.k_out, cfg.n_pes)
+    tft = torch.from_numpy(tf).cuda()
+    volc = vol_t.cuda()
+    g = [comp.generate_subvdi(volc, tft, cam, dec, pe) for pe in range(cfg.n_pes)]
+    s2 = comp.empty_strip()
+    comp.composite(g, s2)
+    c2, d2, r2 = full_to_numpy(s2)
+    img = orc.render_full(c2, r2)
+    assert np.abs(img - orc.dvr(sc)).max() <= 1e-3
+
+
+def test_full_size_synthetic_sampled(vdi, orc):
+    """1920x1080, 8 PEs, k=20 merge-only inputs in the bench's launch
+    configuration; the oracle recomposes a sample of lists one by one."""
+    W, H, n, k = 1920, 1080, 8, 20
+    pes = synth.random_subvdis(n, W, H, k, lam=10.0, seed=7)
+    strip, gam, m, cnt = _gpu_composite(vdi, pes, W, H, k, k)
+    rng = np.random.default_rng(1)
+    srch = np.nonzero(m > k)[0]
+    pix = np.unique(np.concatenate([rng.choice(W * H, 8000, replace=False),
+                                    rng.choice(srch, min(4000, len(srch)), replace=False) if len(srch) else [],
+                                    [0, W * H - 1]]).astype(np.int64))
+    ref = orc.composite_pixels(pes, pix, k)
+    gc, gd, gr = full_to_numpy(strip)
+    compare(gc[pix], gd[pix], gr[pix], ref["count"], ref["depth"], ref["rgba"], ref["stats"]["margin"], "1080p")
+    assert cnt["records_in"] == sum(int(p["count"].sum()) for p in pes)
