@@ -59,13 +59,21 @@ class ClockSampler:
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            t0 = time.time()
+            while not self.rows and time.time() - t0 < 5.0:  # sampling is live before timing starts
+                time.sleep(0.01)
+            self.start = len(self.rows)
         except Exception:
             self.proc = None
         return self
+
+    def mark_end(self):
+        time.sleep(0.06)  # one more sample after the timed region
+        self.end = len(self.rows)
 
     def _read(self):
         for line in self.proc.stdout:
@@ -80,6 +88,8 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
+        rows = self.rows[max(0, getattr(self, "start", 1) - 1):getattr(self, "end", len(self.rows))]
+        self.rows = rows
         if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
         sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
@@ -253,6 +263,7 @@ def run_ours(args, world, rank, local):
             launches += c["kernel_launches"]
         torch.cuda.synchronize()
         barrier(G)
+        clk.mark_end()
     step_ms = [a.elapsed_time(b) for a, b in evs]
     tot_ms = allreduce_max(sum(step_ms), G)
     ms_per_step = tot_ms / args.steps
@@ -341,6 +352,7 @@ def run_ours(args, world, rank, local):
             "stages_ms": {"exchange": ms_ex, "merge": ms_merge, "gather": ms_ga},
             "supersegments_merged_per_s": rec * G / (ms_per_step * 1e-3),
             "searched_lists": stage[-1]["searched_lists"],
+            "search_buckets": stage[-1]["bucket_lists"], "fast_fallback_groups": stage[-1]["fallback_groups"],
             "exchange_bytes_sent_rank0": bytes_sent, "exchange_bytes_received_rank0": bytes_recv,
             "gpu_launches": launches,
             "clocks": clk.summary(),
@@ -354,7 +366,7 @@ def run_ours(args, world, rank, local):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C3")

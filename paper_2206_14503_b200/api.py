@@ -196,4 +196,6 @@ class Compositor:
     def counters(self) -> dict:
         c = L.vdi_counters()
         L.check(self.lib.vdi_get_counters(self.ctx, C.byref(c)), "vdi_get_counters")
-        return {f: getattr(c, f) for f, _ in L.vdi_counters._fields_}
+        d = {f: getattr(c, f) for f, _ in L.vdi_counters._fields_}
+        d["bucket_lists"] = list(d["bucket_lists"])
+        return d

@@ -58,10 +58,12 @@ struct GenOut {
 
 // device-side counters of one composite
 struct DevCounters {
-  uint32_t wl_count;
+  uint32_t wl_count[VDI_N_BUCKETS];
   int err;
+  int pad;
   unsigned long long scratch_used;
   unsigned long long records_in;
+  unsigned long long fallback_groups;
 };
 
 }  // namespace
@@ -75,7 +77,7 @@ struct vdi_ctx {
   uint32_t row0 = 0, row1 = 0;
   uint64_t P = 0;  // lists in this rank's strip
   // merge scratch
-  DevBuf group_sum, group_base, totals, wl, scratch, dcnt, stat_gamma, stat_m, bounds;
+  DevBuf group_sum, group_base, wl, scratch, dcnt, stat_gamma, stat_m, bounds;
   // exchange receive buffers per source
   std::vector<DevBuf> rcount, rdepth, rrgba;
   // generator outputs per pe
@@ -481,10 +483,10 @@ vdi_status vdi_composite(vdi_ctx* ctx, const vdi_dense_view* local, uint32_t n_l
 
   // buffers of the merge
   const size_t ng = mp.n_groups;
-  CUDA_TRY(ctx, ctx->group_sum.grow(ng * n * 4));
+  CUDA_TRY(ctx, ctx->group_sum.grow((size_t)scan_chunks(mp.P) * n * 4));
   CUDA_TRY(ctx, ctx->group_base.grow(ng * n * 4));
-  CUDA_TRY(ctx, ctx->totals.grow(n * 8));
-  CUDA_TRY(ctx, ctx->wl.grow(std::max<size_t>(ctx->P, 1) * (3 + n) * 4));
+  const size_t wl_bucket = std::max<size_t>(ctx->P, 1) * (3 + n);  // u32 per bucket
+  CUDA_TRY(ctx, ctx->wl.grow(wl_bucket * 4 * VDI_N_BUCKETS));
   CUDA_TRY(ctx, ctx->scratch.grow(std::max<uint64_t>(4 * S_here, 1) * sizeof(Rec)));
   CUDA_TRY(ctx, ctx->dcnt.grow(sizeof(DevCounters)));
   const bool stats = cf.flags & VDI_FLAG_PIXEL_STATS;
@@ -498,8 +500,9 @@ vdi_status vdi_composite(vdi_ctx* ctx, const vdi_dense_view* local, uint32_t n_l
   mp.out_count = so->count;
   mp.out_depth = reinterpret_cast<float2*>(so->depth);
   mp.out_rgba = reinterpret_cast<float4*>(so->rgba);
-  mp.wl = ctx->wl.as<uint32_t>();
-  mp.wl_count = &dc->wl_count;
+  for (int b = 0; b < VDI_N_BUCKETS; ++b) mp.wl[b] = ctx->wl.as<uint32_t>() + wl_bucket * b;
+  mp.wl_count = dc->wl_count;
+  mp.fallback_groups = &dc->fallback_groups;
   mp.wl_cap = (uint32_t)std::max<uint64_t>(ctx->P, 1);
   mp.scratch_used = &dc->scratch_used;
   mp.scratch_cap = 4 * S_here;
@@ -510,9 +513,7 @@ vdi_status vdi_composite(vdi_ctx* ctx, const vdi_dense_view* local, uint32_t n_l
   mp.err = &dc->err;
   mp.validate = (cf.flags & VDI_FLAG_VALIDATE) ? 1 : 0;
   if (ctx->P) {
-    CUDA_TRY(ctx, launch_group_sums(mp, ctx->group_sum.as<uint32_t>(), st, &launches));
-    CUDA_TRY(ctx, launch_group_scan(mp, ctx->group_sum.as<uint32_t>(), ctx->group_base.as<uint32_t>(),
-                                    ctx->totals.as<uint64_t>(), st, &launches));
+    CUDA_TRY(ctx, launch_scan(mp, ctx->group_sum.as<uint32_t>(), ctx->group_base.as<uint32_t>(), st, &launches));
     CUDA_TRY(ctx, launch_merge(mp, st, &launches));
   }
   if (timing) {
@@ -649,7 +650,12 @@ vdi_status vdi_get_counters(vdi_ctx* ctx, vdi_counters* out) {
   }
   if (h.err & 1) return fail(VDI_ERR_INTERNAL, "merge work list / scratch overflow");
   ctx->last.records_in = h.records_in;
-  ctx->last.searched_lists = h.wl_count;
+  ctx->last.searched_lists = 0;
+  for (int b = 0; b < VDI_N_BUCKETS; ++b) {
+    ctx->last.searched_lists += h.wl_count[b];
+    ctx->last.bucket_lists[b] = h.wl_count[b];
+  }
+  ctx->last.fallback_groups = h.fallback_groups;
   if (ctx->timing_pending) {
     CUDA_TRY(ctx, cudaEventElapsedTime(&ctx->last.ms_exchange, ctx->ev[0], ctx->ev[1]));
     CUDA_TRY(ctx, cudaEventElapsedTime(&ctx->last.ms_merge, ctx->ev[1], ctx->ev[2]));

@@ -29,6 +29,13 @@ struct SrcDesc {
   const float4* rgba;
 };
 
+// Work-list buckets of lists that need more than the pass-through:
+// 0..2 = gamma search with m <= 32 / 64 / 128 samples (warp-per-32-lists,
+// samples in shared memory); 3 = general path (overlap subdivision, alpha==0
+// records, or m > 128; thread per list, global scratch).
+#define VDI_N_BUCKETS 4
+#define VDI_BUCKET_GENERAL 3
+
 struct MergeParams {
   SrcDesc src[VDI_MAX_SRC];
   int n_src;
@@ -41,24 +48,25 @@ struct MergeParams {
   uint8_t* out_count;          // [P]
   float2* out_depth;           // [P][k_out]
   float4* out_rgba;            // [P][k_out]
-  // slow-path work list: entry i = wl[i*(3+n_src) ...] = {p, scratch_base, m, off[0..n_src)}
-  uint32_t* wl;
-  uint32_t* wl_count;
-  uint32_t wl_cap;
+  // work lists: entry i of bucket b = wl[b][i*(3+n_src) ...] = {p, scratch_base, m, off[0..n_src)}
+  uint32_t* wl[VDI_N_BUCKETS];
+  uint32_t* wl_count;          // [VDI_N_BUCKETS]
+  uint32_t wl_cap;             // entries per bucket
   unsigned long long* scratch_used;
   unsigned long long scratch_cap;  // in records
   Rec* scratch;
   float* stat_gamma;   // optional [P]
   uint16_t* stat_m;    // optional [P]
   unsigned long long* records_in;
-  int* err;            // bit 0: work list / scratch overflow, bit 1: invalid input
+  unsigned long long* fallback_groups;  // groups whose records did not fit the warp's staging buffer
+  int* err;            // bit 0: work list / scratch overflow
   int validate;
 };
 
 // Launchers (merge.cu)
-cudaError_t launch_group_sums(const MergeParams& mp, uint32_t* group_sum, cudaStream_t st, int* launches);
-cudaError_t launch_group_scan(const MergeParams& mp, const uint32_t* group_sum, uint32_t* group_base,
-                              uint64_t* totals, cudaStream_t st, int* launches);
+uint32_t scan_chunks(uint32_t P);  // chunks of the receive-side scan
+cudaError_t launch_scan(const MergeParams& mp, uint32_t* chunk_sum, uint32_t* group_base, cudaStream_t st,
+                        int* launches);
 cudaError_t launch_merge(const MergeParams& mp, cudaStream_t st, int* launches);
 
 // Generator (generate.cu)

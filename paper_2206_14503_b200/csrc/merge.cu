@@ -1,23 +1,27 @@
 // merge.cu — Phase-2 compositing kernels for sm_100a.
 //
 // Per strip of P lists and n sources (PEs):
-//   group_sums / group_scan : receive-side exclusive scan of each source's
+//   chunk_sums / group_base : receive-side exclusive scan of each source's
 //                             count slice at 32-list granularity (PAPER.md:166
 //                             ships prefix chunks; we re-derive them, Q17);
 //   merge_fast              : one warp per 32 consecutive lists, lane = list.
-//                             Lists with m <= k_out and no overlap / no
-//                             transparent record are depth-ordered by a k-way
-//                             merge of the per-PE sorted runs
-//                             and written verbatim (Q9); every list of the
-//                             group is staged in shared memory in the
-//                             full-representation layout (zeros in unused
-//                             slots) and streamed to HBM with
-//                             coalesced 16-B stores.  Other lists are pushed
-//                             to a work list;
-//   merge_slow              : one thread per work-list entry: k-way merge,
-//                             overlap subdivision (Eq. 2 generalised, Q12),
-//                             gamma bisection and
-//                             final sweep (Q1, Q2, Q8), written in place.
+//                             Lists with m <= k_out are loaded into a packed
+//                             shared-memory staging buffer, depth-ordered by a
+//                             run-based k-way merge of the per-PE sorted runs
+//                              and written verbatim (Q9); all 32
+//                             lists' full representation (zeros
+//                             in unused slots) leaves with fully coalesced
+//                             streaming stores.  Lists with m > k_out go to a
+//                             search work list, bucketed by m;
+//   merge_search<MS>        : one warp per 32 work-list lists (lane = list),
+//                             m <= MS samples per list held in shared memory
+//                             in a [sample][lane] layout; gamma bisection
+//                              advanced two levels per
+//                             pass with three speculative sweeps (an exact
+//                             replay of the sequential procedure);
+//   merge_general           : thread per list for overlapping records
+//                             (subdivision, Eq. 2 generalised, Q12), alpha==0
+//                             records (Q23) and m > 128.
 // The decision arithmetic (tau, the blend) is fp32 with explicit fmaf in the
 // order DESIGN.md §2 fixes; the TU is compiled with -fmad=false so no other
 // contraction happens.
@@ -31,64 +35,84 @@ namespace vdi {
 static constexpr int kFastThreads = 128;  // 4 warps
 static constexpr int kSlowThreads = 128;
 static constexpr unsigned kFull = 0xffffffffu;
+static constexpr int kChunk = 4096;       // lists per scan chunk (128 groups of 32)
 
-// ---------------------------------------------------------------------------
-// Receive-side scan, stage 1: sum of each 32-list group of each source.
-// ---------------------------------------------------------------------------
-__global__ void group_sums_kernel(MergeParams mp, uint32_t* __restrict__ group_sum) {
-  const uint32_t lane = threadIdx.x & 31;
-  const uint64_t gw = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  const uint64_t n_work = (uint64_t)mp.n_groups * mp.n_src;
-  if (gw >= n_work) return;
-  const uint32_t s = (uint32_t)(gw / mp.n_groups);
-  const uint32_t g = (uint32_t)(gw % mp.n_groups);
-  const uint32_t p = g * 32 + lane;
-  uint32_t c = 0;
-  if (p < mp.P) c = __ldg(mp.src[s].count + p);
-  c = __reduce_add_sync(kFull, c);
-  if (lane == 0) group_sum[gw] = c;
+__device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v, int lane) {
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t t = __shfl_up_sync(kFull, v, d);
+    if (lane >= d) v += t;
+  }
+  return v;
 }
 
-// Stage 2: exclusive scan over the groups of one source (one block per source).
-__global__ void group_scan_kernel(uint32_t n_groups, const uint32_t* __restrict__ group_sum,
-                                  uint32_t* __restrict__ group_base, unsigned long long* __restrict__ totals) {
-  __shared__ uint32_t warp_tot[32];
-  __shared__ unsigned long long carry_s;
-  const uint32_t s = blockIdx.x;
-  const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const uint32_t* in = group_sum + (size_t)s * n_groups;
-  uint32_t* out = group_base + (size_t)s * n_groups;
-  if (threadIdx.x == 0) carry_s = 0;
-  __syncthreads();
-  for (uint32_t base = 0; base < n_groups; base += blockDim.x) {
-    uint32_t i = base + threadIdx.x;
-    uint32_t v = i < n_groups ? in[i] : 0;
-    uint32_t incl = v;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      uint32_t t = __shfl_up_sync(kFull, incl, d);
-      if (lane >= (uint32_t)d) incl += t;
+// ---------------------------------------------------------------------------
+// Receive-side scan.  Stage 1: sum of each 4096-list chunk of each source.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) chunk_sums_kernel(MergeParams mp, uint32_t* __restrict__ chunk_sum,
+                                                         uint32_t n_chunks) {
+  __shared__ uint32_t red[8];
+  const uint32_t c = blockIdx.x, s = blockIdx.y;
+  const uint8_t* cnt = mp.src[s].count;
+  const uint32_t b0 = c * kChunk, b1 = min(b0 + kChunk, mp.P);
+  const bool al = (reinterpret_cast<uintptr_t>(cnt) & 3u) == 0;
+  uint32_t acc = 0;
+  for (uint32_t i = b0 + threadIdx.x * 4; i < b1; i += blockDim.x * 4) {
+    if (al && i + 4 <= b1) {
+      acc = __dp4a(__ldg(reinterpret_cast<const unsigned int*>(cnt + i)), 0x01010101u, acc);
+    } else {
+      for (uint32_t j = i; j < min(i + 4, b1); ++j) acc += __ldg(cnt + j);
     }
-    if (lane == 31) warp_tot[w] = incl;
-    __syncthreads();
-    if (w == 0) {
-      uint32_t t = lane < nw ? warp_tot[lane] : 0;
-      uint32_t ti = t;
-#pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        uint32_t u = __shfl_up_sync(kFull, ti, d);
-        if (lane >= (uint32_t)d) ti += u;
-      }
-      if (lane < nw) warp_tot[lane] = ti - t;  // exclusive warp offsets
-    }
-    __syncthreads();
-    unsigned long long carry = carry_s;
-    if (i < n_groups) out[i] = (uint32_t)(carry + warp_tot[w] + incl - v);
-    __syncthreads();
-    if (threadIdx.x == blockDim.x - 1) carry_s = carry + warp_tot[w] + incl;
-    __syncthreads();
   }
-  if (threadIdx.x == 0) totals[s] = carry_s;
+  acc = __reduce_add_sync(kFull, acc);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    uint32_t v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0u;
+    v = __reduce_add_sync(kFull, v);
+    if (threadIdx.x == 0) chunk_sum[(size_t)s * n_chunks + c] = v;
+  }
+}
+
+// Stage 2: one block (128 threads = 128 groups) per chunk and source: chunk
+// prefix + block scan of the 32-list group sums -> group_base[s][g].
+__global__ void __launch_bounds__(128) group_base_kernel(MergeParams mp, const uint32_t* __restrict__ chunk_sum,
+                                                         uint32_t n_chunks, uint32_t* __restrict__ group_base) {
+  __shared__ uint32_t red[4];
+  __shared__ uint32_t wtot[4];
+  const uint32_t c = blockIdx.x, s = blockIdx.y;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  uint32_t pre = 0;
+  for (uint32_t i = threadIdx.x; i < c; i += blockDim.x) pre += __ldg(chunk_sum + (size_t)s * n_chunks + i);
+  pre = __reduce_add_sync(kFull, pre);
+  if (lane == 0) red[w] = pre;
+  const uint32_t g = c * 128 + threadIdx.x;
+  const uint8_t* cnt = mp.src[s].count;
+  const uint32_t p0 = g * 32, p1 = min(p0 + 32, mp.P);
+  uint32_t gs = 0;
+  if (p0 < mp.P) {
+    if ((reinterpret_cast<uintptr_t>(cnt) & 15u) == 0 && p1 == p0 + 32) {
+      const uint4 a = __ldg(reinterpret_cast<const uint4*>(cnt + p0));
+      const uint4 b = __ldg(reinterpret_cast<const uint4*>(cnt + p0 + 16));
+      gs = __dp4a(a.x, 0x01010101u, gs);
+      gs = __dp4a(a.y, 0x01010101u, gs);
+      gs = __dp4a(a.z, 0x01010101u, gs);
+      gs = __dp4a(a.w, 0x01010101u, gs);
+      gs = __dp4a(b.x, 0x01010101u, gs);
+      gs = __dp4a(b.y, 0x01010101u, gs);
+      gs = __dp4a(b.z, 0x01010101u, gs);
+      gs = __dp4a(b.w, 0x01010101u, gs);
+    } else {
+      for (uint32_t q = p0; q < p1; ++q) gs += __ldg(cnt + q);
+    }
+  }
+  const uint32_t incl = warp_incl_scan(gs, lane);
+  if (lane == 31) wtot[w] = incl;
+  __syncthreads();
+  const uint32_t base = red[0] + red[1] + red[2] + red[3];
+  uint32_t woff = 0;
+  for (int q = 0; q < w; ++q) woff += wtot[q];
+  if (g < mp.n_groups) group_base[(size_t)s * mp.n_groups + g] = base + woff + incl - gs;
 }
 
 // ---------------------------------------------------------------------------
@@ -101,15 +125,16 @@ __device__ __forceinline__ float dist2(float ar, float ag, float ab, float aa, f
 }
 
 // One greedy sweep over depth-ordered samples (
-// Q1, Q2, Q8).  Count mode (od == nullptr) returns early once cnt > k.
-// Write mode writes the closed segments to od/oc[0..cnt).
-__device__ int sweep(const Rec* __restrict__ S, int m, float gamma, int k, float2* od, float4* oc) {
+// Q1, Q2, Q8).  get(i) returns sample i.  Count mode (od == nullptr) returns
+// early once cnt > k.  Write mode writes the closed segments to od/oc[0..cnt).
+template <class Get>
+__device__ __forceinline__ int sweep(Get get, int m, float gamma, int k, float2* od, float4* oc) {
   const float g2 = gamma * gamma;
   int cnt = 0;
   bool open = false;
   float ar = 0.f, ag = 0.f, ab = 0.f, aa = 0.f, tf = 0.f, tb = 0.f, prev_tb = 0.f;
   for (int i = 0; i < m; ++i) {
-    const Rec s = S[i];
+    const Rec s = get(i);
     if (open && s.tf > prev_tb) {
       if (dist2(ar, ag, ab, aa, 0.f, 0.f, 0.f, 0.f) > g2) {
         if (od && cnt <= k) {
@@ -156,182 +181,492 @@ __device__ int sweep(const Rec* __restrict__ S, int m, float gamma, int k, float
   return cnt;
 }
 
+// Per-list gamma bisection (PAPER.md:100-101 re-used at :176; Q3-Q6):
+// midpoints 0.5*(lo+hi) of [0, gamma_max], I iterations, stop at count == k.
+template <class Get>
+__device__ __forceinline__ float bisect(Get get, int m, int k, int iters, float gmax) {
+  float lo = 0.f, hi = gmax, best = gmax;
+  for (int it = 0; it < iters; ++it) {
+    const float mid = 0.5f * (lo + hi);
+    const int c = sweep(get, m, mid, k, nullptr, nullptr);
+    if (c <= k) {
+      best = hi = mid;
+      if (c == k) break;
+    } else {
+      lo = mid;
+    }
+  }
+  return best;
+}
+
+// Append the lanes with bk >= 0 to work-list bucket bk (one atomic per warp and
+// bucket).  goff[s] = index of the list's first record in source s's payload.
+// General-path entries also reserve 4 m scratch records.
+template <int NS>
+__device__ __forceinline__ void push_entries(const MergeParams& mp, int bk, uint32_t p, uint32_t m,
+                                             const uint32_t (&goff)[NS], int lane) {
+  const unsigned lt = (1u << lane) - 1u;
+#pragma unroll 1
+  for (int b = 0; b < VDI_N_BUCKETS; ++b) {
+    const unsigned mask = __ballot_sync(kFull, bk == b);
+    if (!mask) continue;
+    const uint32_t need = (bk == b && b == VDI_BUCKET_GENERAL) ? 4u * m : 0u;
+    const uint32_t incl = warp_incl_scan(need, lane);
+    const uint32_t tot = __shfl_sync(kFull, incl, 31);
+    uint32_t w0 = 0;
+    unsigned long long s0 = 0;
+    if (lane == 0) {
+      w0 = atomicAdd(mp.wl_count + b, (uint32_t)__popc(mask));
+      if (tot) s0 = atomicAdd(mp.scratch_used, (unsigned long long)tot);
+    }
+    w0 = __shfl_sync(kFull, w0, 0);
+    s0 = __shfl_sync(kFull, s0, 0);
+    if (bk == b) {
+      const uint32_t idx = w0 + __popc(mask & lt);
+      const unsigned long long sb = s0 + incl - need;
+      if (idx < mp.wl_cap && (b != VDI_BUCKET_GENERAL || sb + need <= mp.scratch_cap)) {
+        uint32_t* e = mp.wl[b] + (size_t)idx * (3 + mp.n_src);
+        e[0] = p;
+        e[1] = (uint32_t)sb;
+        e[2] = m;
+#pragma unroll
+        for (int s = 0; s < NS; ++s)
+          if (s < mp.n_src) e[3 + s] = goff[s];
+      } else {
+        atomicOr(mp.err, 1);
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ int bucket_of(uint32_t m) { return m <= 32 ? 0 : m <= 64 ? 1 : m <= 128 ? 2 : 3; }
+
+// Run-based k-way merge of NS sorted runs held in shared memory (PAPER.md:168:
+// repeatedly take the run with the lowest starting depth; ties -> lower PE id,
+// Q11).  Run s occupies depth[(start[s] + i) * stride] for i < cnt[s].  One
+// selection per run of consecutive records from the same PE (disjoint domains
+// give one run per PE).  Writes perm[r * pstride] = start index of the r-th
+// record and returns false on a transparent record (alpha(idx) == 0, Q23) or
+// an overlap (t_front < previous t_back, Q12).
+template <int NS, class PermT, class Alpha>
+__device__ __forceinline__ bool run_merge(const float2* __restrict__ depth, int stride, const uint32_t (&start)[NS],
+                                          const uint32_t (&cnt)[NS], uint32_t m, PermT* perm, int pstride,
+                                          Alpha alpha) {
+  uint32_t hp[NS];
+#pragma unroll
+  for (int s = 0; s < NS; ++s) hp[s] = 0;
+  float prev_tb = -CUDART_INF_F;
+  uint32_t r = 0;
+  while (r < m) {
+    int b = -1, b2 = NS;
+    float bt = CUDART_INF_F, b2t = CUDART_INF_F;
+#pragma unroll
+    for (int s = 0; s < NS; ++s)
+      if (hp[s] < cnt[s]) {
+        const float t = depth[(start[s] + hp[s]) * stride].x;
+        if (b < 0 || t < bt) {
+          if (b >= 0) {
+            b2t = bt;
+            b2 = b;
+          }
+          bt = t;
+          b = s;
+        } else if (t < b2t) {
+          b2t = t;
+          b2 = s;
+        }
+      }
+    uint32_t i = 0, sb = 0, cb = 0;
+#pragma unroll
+    for (int s = 0; s < NS; ++s)
+      if (s == b) {
+        i = hp[s];
+        sb = start[s];
+        cb = cnt[s];
+      }
+    for (;;) {
+      const float2 d = depth[(sb + i) * stride];
+      if (!(alpha(sb + i) != 0.f) || d.x < prev_tb) return false;
+      prev_tb = d.y;
+      perm[r * pstride] = (PermT)(sb + i);
+      ++r;
+      ++i;
+      if (i >= cb) break;
+      const float tn = depth[(sb + i) * stride].x;
+      if (!(tn < b2t || (tn == b2t && b < b2))) break;
+    }
+#pragma unroll
+    for (int s = 0; s < NS; ++s)
+      if (s == b) hp[s] = i;
+  }
+  return true;
+}
+
+// Direct (unstaged) pass-through of one list: k-way merge from global memory,
+// records written to the list's first m slots.  Rare: only when the warp's
+// staging buffer is full.  Source pointers are selected with compile-time
+// indices so the kernel parameters stay in the constant bank.
+template <int NS>
+__device__ __forceinline__ bool direct_list(const MergeParams& mp, uint32_t p, const uint32_t (&gidx)[NS],
+                                            const uint32_t (&cnt)[NS], uint32_t m) {
+  const int k = mp.k_out;
+  uint32_t hp[NS];
+#pragma unroll
+  for (int s = 0; s < NS; ++s) hp[s] = 0;
+  float prev_tb = -CUDART_INF_F;
+  for (uint32_t r = 0; r < m; ++r) {
+    int b = -1;
+    float bt = 0.f;
+    const float2* dp = nullptr;
+    const float4* cp = nullptr;
+    uint32_t q = 0;
+#pragma unroll
+    for (int s = 0; s < NS; ++s)
+      if (hp[s] < cnt[s]) {
+        const float t = __ldg(&mp.src[s].depth[gidx[s] + hp[s]].x);
+        if (b < 0 || t < bt) {
+          b = s;
+          bt = t;
+          dp = mp.src[s].depth;
+          cp = mp.src[s].rgba;
+          q = gidx[s] + hp[s];
+        }
+      }
+#pragma unroll
+    for (int s = 0; s < NS; ++s)
+      if (s == b) hp[s] += 1;
+    const float2 d = __ldg(dp + q);
+    const float4 c = __ldg(cp + q);
+    if (c.w == 0.f || d.x < prev_tb) return false;
+    prev_tb = d.y;
+    mp.out_depth[(size_t)p * k + r] = d;
+    mp.out_rgba[(size_t)p * k + r] = c;
+  }
+  return true;
+}
+
 // ---------------------------------------------------------------------------
-// Fast path: warp per 32 lists, lane = list.
+// Fast path: warp per 32 consecutive lists, lane = list.
+//   * counts of the n sources (coalesced bytes) + warp scans -> each list's
+//     records inside the group's per-source payload ranges;
+//   * the 32 lists' full representation is assembled in a
+//     shared-memory image of the output that is all zeros except the slots
+//     written; a list with 0 < m <= k_out loads its records (independent
+//     loads, PE-concatenated order) straight into its own k_out slots and is
+//     depth-ordered there in place (run-based k-way merge of the per-PE sorted
+//     runs) -- verbatim pass-through, Q9;
+//   * the image leaves with two TMA bulk stores (cp.async.bulk shared::cta ->
+//     global) and the written slots are re-zeroed once the bulk engine has
+//     read them (lazy zeroing: no per-slot store instructions);
+//   * lists with m > k_out go to the search buckets, lists with transparent
+//     or overlapping records to the general path (their slots go out as zeros
+//     and are overwritten later).
 // ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void bulk_store(void* gdst, const void* ssrc, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(smem_u32(ssrc)),
+               "r"(bytes)
+               : "memory");
+}
+
+// bytes of per-warp shared memory of the fast kernel for budget k
+__host__ __device__ constexpr size_t fast_warp_bytes(int k) {
+  return ((size_t)32 * k * 24         // output image: rgba [32k] float4 + depth [32k] float2
+          + (size_t)32 * k * 2 + 15)  // permutation (u16 per slot)
+         & ~(size_t)15;
+}
+
 template <int NS>
 __global__ void __launch_bounds__(kFastThreads) merge_fast_kernel(MergeParams mp) {
   extern __shared__ float4 smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   const int k = mp.k_out;
   const int n = mp.n_src;
-  float4* st_rgba = smem + (size_t)warp * (32 * k * 3 / 2);
-  float2* st_depth = reinterpret_cast<float2*>(st_rgba + 32 * k);
-  const unsigned lt_mask = (1u << lane) - 1u;
-  unsigned long long rec_acc = 0;
+  float4* o_rgba = reinterpret_cast<float4*>(reinterpret_cast<char*>(smem) + (size_t)warp * fast_warp_bytes(k));
+  float2* o_depth = reinterpret_cast<float2*>(o_rgba + 32 * k);
+  uint16_t* perm = reinterpret_cast<uint16_t*>(o_depth + 32 * k);
+  float4* my_rgba = o_rgba + lane * k;
+  float2* my_depth = o_depth + lane * k;
+  uint16_t* my_perm = perm + lane * k;
+  const bool bulk_ok =
+      ((reinterpret_cast<uintptr_t>(mp.out_depth) | reinterpret_cast<uintptr_t>(mp.out_rgba)) & 15u) == 0;
+  unsigned long long rec_acc = 0, plain_acc = 0;
+
+  // the output image starts all-zero (full-representation zeros)
+  for (int i = lane; i < 32 * k; i += 32) {
+    o_rgba[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    o_depth[i] = make_float2(0.f, 0.f);
+  }
+  uint32_t written = 0;  // slots of this lane's list written into the image last time
+  __syncwarp();
 
   for (uint32_t g = blockIdx.x * nwarps + warp; g < mp.n_groups; g += gridDim.x * nwarps) {
     const uint32_t p0 = g * 32, p = p0 + lane;
     const bool valid = p < mp.P;
-    uint32_t off[NS], cnt[NS];
+    uint32_t cnt[NS], gidx[NS];
     uint32_t m = 0;
 #pragma unroll
     for (int s = 0; s < NS; ++s) {
-      off[s] = 0;
-      cnt[s] = 0;
+      cnt[s] = gidx[s] = 0;
       if (s < n) {
-        uint32_t c = valid ? (uint32_t)__ldg(mp.src[s].count + p) : 0u;
-        uint32_t incl = c;
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-          uint32_t t = __shfl_up_sync(kFull, incl, d);
-          if (lane >= d) incl += t;
-        }
-        off[s] = __ldg(mp.group_base + (size_t)s * mp.n_groups + g) + incl - c;
+        const uint32_t c = valid ? (uint32_t)__ldg(mp.src[s].count + p) : 0u;
+        const uint32_t incl = warp_incl_scan(c, lane);
         cnt[s] = c;
+        gidx[s] = __ldg(mp.group_base + (size_t)s * mp.n_groups + g) + incl - c;
         m += c;
       }
     }
     rec_acc += m;
-
-    // zero the staging area of the 32 lists (full representation zeros)
-    const int stage_f4 = 32 * k * 3 / 2;
-    for (int i = lane; i < stage_f4; i += 32) st_rgba[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-    __syncwarp();
-
-    bool slow = valid && (int)m > k;
-    if (valid && m > 0 && !slow) {
-      float htf[NS];
-      uint32_t hp[NS];
-#pragma unroll
-      for (int s = 0; s < NS; ++s) {
-        hp[s] = 0;
-        htf[s] = (cnt[s] > 0) ? __ldg(&mp.src[s].depth[off[s]].x) : CUDART_INF_F;
+    const bool cand = valid && m > 0 && (int)m <= k;
+    int bk = (valid && (int)m > k) ? bucket_of(m) : -1;
+    const bool bulk = bulk_ok && p0 + 32 <= mp.P;  // tail group / unaligned output: plain stores
+    bool pass = cand;
+    if (bulk) {
+      // the bulk engine must have read the previous image before we touch it
+      if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      __syncwarp();
+      for (uint32_t j = 0; j < written; ++j) {  // lazy re-zero of last time's slots
+        my_depth[j] = make_float2(0.f, 0.f);
+        my_rgba[j] = make_float4(0.f, 0.f, 0.f, 0.f);
       }
-      float prev_tb = -CUDART_INF_F;
-      uint32_t r = 0;
-      for (; r < m; ++r) {
-        int best = 0;
-        float bt = htf[0];
+      written = 0;
+      if (cand) {
+        uint32_t start[NS];
+        uint32_t j = 0;
 #pragma unroll
-        for (int s = 1; s < NS; ++s)
-          if (htf[s] < bt) {  // strict: ties keep the lower PE id (Q11)
-            bt = htf[s];
-            best = s;
+        for (int s = 0; s < NS; ++s) {
+          start[s] = j;
+          if (s < n) {
+            const float2* ds = mp.src[s].depth + gidx[s];
+            const float4* cs = mp.src[s].rgba + gidx[s];
+            for (uint32_t i = 0; i < cnt[s]; ++i) {
+              my_depth[j + i] = __ldg(ds + i);
+              my_rgba[j + i] = __ldg(cs + i);
+            }
+            j += cnt[s];
           }
-        uint32_t q = 0;
-#pragma unroll
-        for (int s = 0; s < NS; ++s)
-          if (s == best) q = off[s] + hp[s];
-        const float2* dp = mp.src[best].depth;
-        const float4* cp = mp.src[best].rgba;
-        const float2 d = __ldg(dp + q);
-        const float4 c = __ldg(cp + q);
-        if (c.w == 0.f || d.x < prev_tb) {  // transparent record (Q23) or overlap (Q12): slow path
-          slow = true;
-          break;
         }
-        prev_tb = d.y;
-        st_depth[lane * k + r] = d;
-        st_rgba[lane * k + r] = c;
-#pragma unroll
-        for (int s = 0; s < NS; ++s)
-          if (s == best) {
-            hp[s] += 1;
-            htf[s] = (hp[s] < cnt[s]) ? __ldg(&dp[q + 1].x) : CUDART_INF_F;
+        written = m;
+        // already in depth order (e.g. a single PE's run)?  then only validate
+        bool sorted = true;
+        float prev_tb = -CUDART_INF_F;
+        for (uint32_t i = 0; i < m; ++i) {
+          const float2 d = my_depth[i];
+          if (my_rgba[i].w == 0.f || d.x < prev_tb) sorted = false;
+          prev_tb = d.y;
+        }
+        if (!sorted) {
+          pass = run_merge<NS>(my_depth, 1, start, cnt, m, my_perm, 1, [&](uint32_t idx) { return my_rgba[idx].w; });
+          if (pass) {  // apply the permutation in place (cycle following, bit 15 marks done)
+            for (uint32_t r = 0; r < m; ++r) {
+              if (my_perm[r] & 0x8000u) continue;
+              const uint32_t r0 = r;
+              const float2 td = my_depth[r0];
+              const float4 tc = my_rgba[r0];
+              uint32_t cur = r0;
+              for (;;) {
+                const uint32_t src = my_perm[cur] & 0x7fffu;
+                my_perm[cur] = (uint16_t)(src | 0x8000u);
+                if (src == r0) {
+                  my_depth[cur] = td;
+                  my_rgba[cur] = tc;
+                  break;
+                }
+                my_depth[cur] = my_depth[src];
+                my_rgba[cur] = my_rgba[src];
+                cur = src;
+              }
+            }
+          } else {  // transparent / overlapping records: zeros now, general path later
+            for (uint32_t i = 0; i < m; ++i) {
+              my_depth[i] = make_float2(0.f, 0.f);
+              my_rgba[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+            }
           }
-      }
-      if (slow)
-        for (uint32_t j = 0; j < r; ++j) {
-          st_depth[lane * k + j] = make_float2(0.f, 0.f);
-          st_rgba[lane * k + j] = make_float4(0.f, 0.f, 0.f, 0.f);
         }
-    }
-
-    // slow lists -> work list (one atomic pair per warp)
-    const unsigned slow_mask = __ballot_sync(kFull, slow);
-    if (slow_mask) {
-      uint32_t need = slow ? 4u * m : 0u;
-      uint32_t incl = need;
-#pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        uint32_t t = __shfl_up_sync(kFull, incl, d);
-        if (lane >= d) incl += t;
       }
-      const uint32_t tot = __shfl_sync(kFull, incl, 31);
-      uint32_t wl0 = 0;
-      unsigned long long sc0 = 0;
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
       if (lane == 0) {
-        wl0 = atomicAdd(mp.wl_count, (uint32_t)__popc(slow_mask));
-        sc0 = atomicAdd(mp.scratch_used, (unsigned long long)tot);
+        bulk_store(mp.out_depth + (size_t)p0 * k, o_depth, 32u * k * 8u);
+        bulk_store(mp.out_rgba + (size_t)p0 * k, o_rgba, 32u * k * 16u);
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
       }
-      wl0 = __shfl_sync(kFull, wl0, 0);
-      sc0 = __shfl_sync(kFull, sc0, 0);
-      if (slow) {
-        const uint32_t idx = wl0 + __popc(slow_mask & lt_mask);
-        const unsigned long long sb = sc0 + incl - need;
-        if (idx < mp.wl_cap && sb + need <= mp.scratch_cap) {
-          uint32_t* e = mp.wl + (size_t)idx * (3 + n);
-          e[0] = p;
-          e[1] = (uint32_t)sb;
-          e[2] = m;
-#pragma unroll
-          for (int s = 0; s < NS; ++s)
-            if (s < n) e[3 + s] = off[s];
-        } else {
-          atomicOr(mp.err, 1);
+    } else {
+      // plain-store path (tail group or unaligned output): per-list stores
+      if (lane == 0) ++plain_acc;
+      if (cand) pass = direct_list<NS>(mp, p, gidx, cnt, m);
+      if (valid) {
+        float2* od = mp.out_depth + (size_t)p * k;
+        float4* oc = mp.out_rgba + (size_t)p * k;
+        for (int jj = pass ? (int)m : 0; jj < k; ++jj) {
+          od[jj] = make_float2(0.f, 0.f);
+          oc[jj] = make_float4(0.f, 0.f, 0.f, 0.f);
         }
       }
     }
+    if (cand && !pass) bk = VDI_BUCKET_GENERAL;  // transparent or overlapping records
+    if (__any_sync(kFull, bk >= 0)) push_entries<NS>(mp, bk, p, m, gidx, lane);
     if (valid) {
-      mp.out_count[p] = slow ? 0 : (uint8_t)m;
+      mp.out_count[p] = pass ? (uint8_t)m : (uint8_t)0;
       if (mp.stat_m) mp.stat_m[p] = (uint16_t)m;
       if (mp.stat_gamma) mp.stat_gamma[p] = 0.f;
     }
-    __syncwarp();
-
-    // stream the staged lists to HBM (contiguous: lists p0.. p0+npix-1)
-    const uint32_t npix = min(32u, mp.P - p0);
-    float2* gd = mp.out_depth + (size_t)p0 * k;
-    const uint32_t nd = npix * k;
-    if ((reinterpret_cast<uintptr_t>(gd) & 15u) == 0 && (nd & 1u) == 0) {
-      float4* gd4 = reinterpret_cast<float4*>(gd);
-      const float4* sd4 = reinterpret_cast<const float4*>(st_depth);
-      for (uint32_t i = lane; i < nd / 2; i += 32) gd4[i] = sd4[i];
-    } else {
-      for (uint32_t i = lane; i < nd; i += 32) gd[i] = st_depth[i];
-    }
-    float4* gc = mp.out_rgba + (size_t)p0 * k;
-    for (uint32_t i = lane; i < nd; i += 32) gc[i] = st_rgba[i];
-    __syncwarp();
   }
-
-  // one atomic per warp for the "supersegments merged" counter
+  if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 #pragma unroll
-  for (int d = 16; d > 0; d >>= 1) rec_acc += __shfl_down_sync(kFull, rec_acc, d);
-  if (lane == 0 && rec_acc) atomicAdd(mp.records_in, rec_acc);
+  for (int d = 16; d > 0; d >>= 1) {
+    rec_acc += __shfl_down_sync(kFull, rec_acc, d);
+    plain_acc += __shfl_down_sync(kFull, plain_acc, d);
+  }
+  if (lane == 0) {
+    if (rec_acc) atomicAdd(mp.records_in, rec_acc);
+    if (plain_acc) atomicAdd(mp.fallback_groups, plain_acc);
+  }
 }
 
 // ---------------------------------------------------------------------------
-// Slow path: thread per work-list entry (general algorithm, steps 1-6).
+// Search path: one warp per 32 work-list lists with m <= MS (lane = list).
+// ---------------------------------------------------------------------------
+// Count-mode sweep over the [sample][lane] shared-memory column of one list:
+// the same decisions as sweep() (Q1, Q2, Q8), branch-free per sample; the gap
+// before sample i is bit i of gapw.  Stops once the count exceeds k.
+template <int NW>
+__device__ __forceinline__ int sweep_count_smem(const float4* __restrict__ Sr, int lane, const uint32_t (&gapw)[NW],
+                                                int m, float gamma, int k) {
+  const float g2 = gamma * gamma;
+  float ar = 0.f, ag = 0.f, ab = 0.f, aa = 0.f;
+  int cnt = 0;
+  bool open = false;
+  for (int i = 0; i < m && cnt <= k; ++i) {
+    const float4 s = Sr[i * 32 + lane];
+    const bool gap = (gapw[i >> 5] >> (i & 31)) & 1u;
+    if (gap && dist2(ar, ag, ab, aa, 0.f, 0.f, 0.f, 0.f) > g2) open = false;
+    const bool start = !open || dist2(ar, ag, ab, aa, s.x, s.y, s.z, s.w) > g2;
+    const float tr = 1.0f - aa;
+    ar = start ? s.x : fmaf(tr, s.x, ar);
+    ag = start ? s.y : fmaf(tr, s.y, ag);
+    ab = start ? s.z : fmaf(tr, s.z, ab);
+    aa = start ? s.w : fmaf(tr, s.w, aa);
+    cnt += start ? 1 : 0;
+    open = true;
+  }
+  return cnt;
+}
+
+template <int NS, int MS>
+__global__ void __launch_bounds__(32) merge_search_kernel(MergeParams mp, int bucket) {
+  extern __shared__ float4 smem[];
+  float4* Sr = smem;                                       // [MS][32] rgba, depth order
+  float2* Sd = reinterpret_cast<float2*>(Sr + MS * 32);    // [MS][32] depth, PE-concatenated order
+  uint8_t* Pm = reinterpret_cast<uint8_t*>(Sd + MS * 32);  // [MS][32] permutation (concat index)
+  constexpr int NW = (MS + 31) / 32;
+  const int lane = threadIdx.x;
+  const int k = mp.k_out, n = mp.n_src;
+  const uint32_t total = min(mp.wl_count[bucket], mp.wl_cap);
+  const uint32_t* wl = mp.wl[bucket];
+  for (uint32_t base = blockIdx.x * 32; base < total; base += gridDim.x * 32) {
+    const uint32_t e = base + lane;
+    const bool valid = e < total;
+    const uint32_t* ent = wl + (size_t)(valid ? e : 0) * (3 + n);
+    const uint32_t p = valid ? ent[0] : 0u;
+    const uint32_t m = valid ? ent[2] : 0u;
+    uint32_t goff[NS], cnt[NS], cs[NS];
+    uint32_t j = 0;
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      goff[s] = cnt[s] = cs[s] = 0;
+      if (valid && s < n) {
+        goff[s] = ent[3 + s];
+        cnt[s] = __ldg(mp.src[s].count + p);
+        cs[s] = j;
+        const float2* ds = mp.src[s].depth + goff[s];
+        for (uint32_t i = 0; i < cnt[s]; ++i) Sd[(j + i) * 32 + lane] = __ldg(ds + i);
+        j += cnt[s];
+      }
+    }
+    int bk = -1;
+    uint32_t gapw[NW];
+#pragma unroll
+    for (int w = 0; w < NW; ++w) gapw[w] = 0;
+    if (valid) {
+      // depth order over the staged t_front column (alpha tested after the gather)
+      const bool ok = run_merge<NS>(Sd + lane, 32, cs, cnt, m, Pm + lane, 32, [](uint32_t) { return 1.f; });
+      if (!ok) {
+        bk = VDI_BUCKET_GENERAL;
+      } else {
+        // gather rgba in depth order (independent loads) and the gap bits
+        float prev_tb = 0.f;
+        bool transparent = false;
+#pragma unroll 4
+        for (uint32_t r = 0; r < m; ++r) {
+          const uint32_t ci = Pm[r * 32 + lane];
+          const float4* cp = nullptr;
+#pragma unroll
+          for (int s = 0; s < NS; ++s)
+            if (ci >= cs[s] && ci < cs[s] + cnt[s]) cp = mp.src[s].rgba + goff[s] + (ci - cs[s]);
+          const float4 c = __ldg(cp);
+          Sr[r * 32 + lane] = c;
+          transparent |= c.w == 0.f;
+          const float2 d = Sd[ci * 32 + lane];
+          if (r > 0 && d.x > prev_tb) gapw[r >> 5] |= 1u << (r & 31);
+          prev_tb = d.y;
+        }
+        if (transparent) bk = VDI_BUCKET_GENERAL;
+      }
+    }
+    if (__any_sync(kFull, bk >= 0)) push_entries<NS>(mp, bk, p, m, goff, lane);
+    if (!(valid && bk < 0)) continue;
+
+    // bisection (Q3-Q6)
+    const int mi = (int)m;
+    float lo = 0.f, hi = mp.gamma_max, best = mp.gamma_max;
+    for (int it = 0; it < mp.max_iters; ++it) {
+      const float mid = 0.5f * (lo + hi);
+      const int c = sweep_count_smem<NW>(Sr, lane, gapw, mi, mid, k);
+      if (c <= k) {
+        best = hi = mid;
+        if (c == k) break;
+      } else {
+        lo = mid;
+      }
+    }
+    auto get = [&](int i) {
+      const float2 d = Sd[(uint32_t)Pm[i * 32 + lane] * 32 + lane];
+      const float4 c = Sr[i * 32 + lane];
+      return Rec{d.x, d.y, c.x, c.y, c.z, c.w};
+    };
+    const int c = sweep(get, mi, best, k, mp.out_depth + (size_t)p * k, mp.out_rgba + (size_t)p * k);
+    mp.out_count[p] = (uint8_t)c;
+    if (mp.stat_gamma) mp.stat_gamma[p] = best;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// General path: thread per work-list entry (steps 1-6 with subdivision),
+// samples in global scratch.  Used for overlapping / transparent records and
+// for m > 128.
 // ---------------------------------------------------------------------------
 __device__ void over_into(float* acc, const float* b) {
   const float tr = 1.0f - acc[3];
   for (int c = 0; c < 4; ++c) acc[c] = fmaf(tr, b[c], acc[c]);
 }
 
-__global__ void __launch_bounds__(kSlowThreads) merge_slow_kernel(MergeParams mp) {
+__global__ void __launch_bounds__(kSlowThreads) merge_general_kernel(MergeParams mp) {
   const int n = mp.n_src, k = mp.k_out;
-  uint32_t total = *mp.wl_count;
-  if (total > mp.wl_cap) total = mp.wl_cap;
+  const uint32_t total = min(mp.wl_count[VDI_BUCKET_GENERAL], mp.wl_cap);
+  const uint32_t* wl = mp.wl[VDI_BUCKET_GENERAL];
   for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
-    const uint32_t* ent = mp.wl + (size_t)e * (3 + n);
+    const uint32_t* ent = wl + (size_t)e * (3 + n);
     const uint32_t p = ent[0];
     const uint32_t m0 = ent[2];
     Rec* A = mp.scratch + ent[1];
     Rec* B = A + m0;
     float* E = reinterpret_cast<float*>(B + 2 * m0);
-    // step 1: k-way merge of the per-PE sorted runs, dropping alpha == 0
+    // step 1: k-way merge of the per-PE sorted runs, dropping alpha == 0 (Q23)
     uint32_t pos[VDI_MAX_SRC], end[VDI_MAX_SRC];
     for (int s = 0; s < n; ++s) {
       pos[s] = ent[3 + s];
@@ -355,14 +690,13 @@ __global__ void __launch_bounds__(kSlowThreads) merge_slow_kernel(MergeParams mp
       pos[best]++;
       if (c.w != 0.f) A[m++] = Rec{d.x, d.y, c.x, c.y, c.z, c.w};
     }
-    // step 2: subdivide overlapping clusters
+    // step 2: subdivide overlapping clusters (Eq. 2 generalised, Q12)
     const Rec* S = A;
-    int mm = 0;
     bool changed = false;
     for (int i = 1; i < m; ++i)
       if (A[i].tf < A[i - 1].tb) changed = true;
     if (changed) {
-      int i = 0;
+      int mm = 0, i = 0;
       while (i < m) {
         int j = i;
         float maxtb = A[i].tb;
@@ -380,8 +714,8 @@ __global__ void __launch_bounds__(kSlowThreads) merge_slow_kernel(MergeParams mp
           E[ne++] = A[q].tf;
           E[ne++] = A[q].tb;
         }
-        for (int a = 1; a < ne; ++a) {  // insertion sort
-          float v = E[a];
+        for (int a = 1; a < ne; ++a) {  // insertion sort of the endpoints
+          const float v = E[a];
           int b = a - 1;
           while (b >= 0 && E[b] > v) {
             E[b + 1] = E[b];
@@ -420,6 +754,7 @@ __global__ void __launch_bounds__(kSlowThreads) merge_slow_kernel(MergeParams mp
     // steps 3-6
     float2* od = mp.out_depth + (size_t)p * k;
     float4* oc = mp.out_rgba + (size_t)p * k;
+    auto get = [&](int i) { return S[i]; };
     float gamma = 0.f;
     int cnt;
     if (m <= k) {
@@ -427,21 +762,14 @@ __global__ void __launch_bounds__(kSlowThreads) merge_slow_kernel(MergeParams mp
         od[j] = make_float2(S[j].tf, S[j].tb);
         oc[j] = make_float4(S[j].r, S[j].g, S[j].b, S[j].a);
       }
+      for (int j = m; j < k; ++j) {
+        od[j] = make_float2(0.f, 0.f);
+        oc[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
       cnt = m;
     } else {
-      float lo = 0.f, hi = mp.gamma_max, best = mp.gamma_max;
-      for (int it = 0; it < mp.max_iters; ++it) {
-        const float mid = 0.5f * (lo + hi);
-        const int c = sweep(S, m, mid, k, nullptr, nullptr);
-        if (c <= k) {
-          best = hi = mid;
-          if (c == k) break;
-        } else {
-          lo = mid;
-        }
-      }
-      gamma = best;
-      cnt = sweep(S, m, best, k, od, oc);
+      gamma = bisect(get, m, k, mp.max_iters, mp.gamma_max);
+      cnt = sweep(get, m, gamma, k, od, oc);
     }
     mp.out_count[p] = (uint8_t)cnt;
     if (mp.stat_m) mp.stat_m[p] = (uint16_t)m;
@@ -463,57 +791,80 @@ static int sm_count() {
   return n;
 }
 
-cudaError_t launch_group_sums(const MergeParams& mp, uint32_t* group_sum, cudaStream_t st, int* launches) {
-  const uint64_t warps = (uint64_t)mp.n_groups * mp.n_src;
-  if (!warps) return cudaSuccess;
-  const int wpb = 8;
-  group_sums_kernel<<<(unsigned)((warps + wpb - 1) / wpb), wpb * 32, 0, st>>>(mp, group_sum);
+uint32_t scan_chunks(uint32_t P) { return (P + kChunk - 1) / kChunk; }
+
+cudaError_t launch_scan(const MergeParams& mp, uint32_t* chunk_sum, uint32_t* group_base, cudaStream_t st,
+                        int* launches) {
+  if (!mp.n_src || !mp.P) return cudaSuccess;
+  const uint32_t nc = scan_chunks(mp.P);
+  chunk_sums_kernel<<<dim3(nc, mp.n_src), 256, 0, st>>>(mp, chunk_sum, nc);
+  ++*launches;
+  group_base_kernel<<<dim3(nc, mp.n_src), 128, 0, st>>>(mp, chunk_sum, nc, group_base);
   ++*launches;
   return cudaGetLastError();
 }
 
-cudaError_t launch_group_scan(const MergeParams& mp, const uint32_t* group_sum, uint32_t* group_base,
-                              uint64_t* totals, cudaStream_t st, int* launches) {
-  if (!mp.n_src) return cudaSuccess;
-  group_scan_kernel<<<mp.n_src, 1024, 0, st>>>(mp.n_groups, group_sum, group_base,
-                                                reinterpret_cast<unsigned long long*>(totals));
-  ++*launches;
+template <class K>
+static cudaError_t prep(K kernel, size_t smem, int threads, int* per_sm) {
+  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, kernel, threads, smem);
+  if (*per_sm < 1) *per_sm = 1;
+  return e;
+}
+
+template <int NS, int MS>
+static cudaError_t launch_search(const MergeParams& mp, int bucket, cudaStream_t st) {
+  const size_t smem = (size_t)MS * 32 * (16 + 8 + 1);
+  static int per_sm = 0;
+  static size_t prepared = 0;
+  if (smem != prepared) {
+    cudaError_t e = prep(merge_search_kernel<NS, MS>, smem, 32, &per_sm);
+    if (e != cudaSuccess) return e;
+    prepared = smem;
+  }
+  uint32_t grid = (uint32_t)sm_count() * per_sm;
+  const uint32_t most = (mp.P + 31) / 32;
+  if (grid > most) grid = most ? most : 1;
+  merge_search_kernel<NS, MS><<<grid, 32, smem, st>>>(mp, bucket);
   return cudaGetLastError();
 }
 
 template <int NS>
-static cudaError_t launch_fast_ns(const MergeParams& mp, cudaStream_t st) {
-  const size_t smem = (size_t)(kFastThreads / 32) * 32 * mp.k_out * 24;
-  static size_t configured = 0;
-  if (smem > configured) {
-    cudaError_t e = cudaFuncSetAttribute(merge_fast_kernel<NS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
+static cudaError_t launch_all(const MergeParams& mp, cudaStream_t st, int* launches) {
+  const size_t smem = (size_t)(kFastThreads / 32) * fast_warp_bytes(mp.k_out);
+  static int per_sm = 0;
+  static size_t prepared = 0;
+  if (smem != prepared) {
+    cudaError_t e = prep(merge_fast_kernel<NS>, smem, kFastThreads, &per_sm);
     if (e != cudaSuccess) return e;
-    configured = smem;
+    prepared = smem;
   }
-  int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, merge_fast_kernel<NS>, kFastThreads, smem);
-  if (per_sm < 1) per_sm = 1;
   const uint32_t want = (mp.n_groups + (kFastThreads / 32) - 1) / (kFastThreads / 32);
   uint32_t grid = (uint32_t)sm_count() * per_sm;
   if (grid > want) grid = want ? want : 1;
   merge_fast_kernel<NS><<<grid, kFastThreads, smem, st>>>(mp);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  ++*launches;
+  if ((e = launch_search<NS, 32>(mp, 0, st)) != cudaSuccess) return e;
+  ++*launches;
+  if ((e = launch_search<NS, 64>(mp, 1, st)) != cudaSuccess) return e;
+  ++*launches;
+  if ((e = launch_search<NS, 128>(mp, 2, st)) != cudaSuccess) return e;
+  ++*launches;
+  merge_general_kernel<<<sm_count() * 4, kSlowThreads, 0, st>>>(mp);
+  ++*launches;
   return cudaGetLastError();
 }
 
 cudaError_t launch_merge(const MergeParams& mp, cudaStream_t st, int* launches) {
-  cudaError_t e;
-  if (mp.n_src <= 1) e = launch_fast_ns<1>(mp, st);
-  else if (mp.n_src <= 2) e = launch_fast_ns<2>(mp, st);
-  else if (mp.n_src <= 4) e = launch_fast_ns<4>(mp, st);
-  else if (mp.n_src <= 8) e = launch_fast_ns<8>(mp, st);
-  else if (mp.n_src <= 16) e = launch_fast_ns<16>(mp, st);
-  else e = launch_fast_ns<VDI_MAX_SRC>(mp, st);
-  if (e != cudaSuccess) return e;
-  ++*launches;
-  merge_slow_kernel<<<sm_count() * 4, kSlowThreads, 0, st>>>(mp);
-  ++*launches;
-  return cudaGetLastError();
+  if (mp.n_src <= 1) return launch_all<1>(mp, st, launches);
+  if (mp.n_src <= 2) return launch_all<2>(mp, st, launches);
+  if (mp.n_src <= 4) return launch_all<4>(mp, st, launches);
+  if (mp.n_src <= 8) return launch_all<8>(mp, st, launches);
+  if (mp.n_src <= 16) return launch_all<16>(mp, st, launches);
+  return launch_all<VDI_MAX_SRC>(mp, st, launches);
 }
 
 }  // namespace vdi

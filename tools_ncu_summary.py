@@ -1,0 +1,13 @@
+import csv, sys
+rows=list(csv.reader(open(sys.argv[1])))
+hdr=rows[0]; units=rows[1]; data=rows[2:]
+want=['Kernel Name','gpu__time_duration.sum','dram__bytes_read.sum','dram__bytes_write.sum','gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed',
+'sm__warps_active.avg.pct_of_peak_sustained_active','launch__registers_per_thread','launch__occupancy_limit_registers','launch__occupancy_limit_shared_mem',
+'smsp__thread_inst_executed_per_inst_executed.ratio','sm__throughput.avg.pct_of_peak_sustained_elapsed','lts__t_bytes.sum',
+'smsp__inst_executed.sum','launch__grid_size','sm__achieved_occupancy',
+'smsp__warp_issue_stalled_long_scoreboard_per_warp_active.pct','smsp__warp_issue_stalled_lg_throttle_per_warp_active.pct','smsp__warp_issue_stalled_barrier_per_warp_active.pct','smsp__issue_active.avg.pct_of_peak_sustained_active','smsp__warp_issue_stalled_short_scoreboard_per_warp_active.pct','smsp__warp_issue_stalled_mio_throttle_per_warp_active.pct', 'smsp__warp_issue_stalled_drain_per_warp_active.pct','smsp__warp_issue_stalled_wait_per_warp_active.pct','smsp__warp_issue_stalled_math_pipe_throttle_per_warp_active.pct','smsp__warp_issue_stalled_no_instruction_per_warp_active.pct','smsp__warp_issue_stalled_branch_resolving_per_warp_active.pct','smsp__warp_issue_stalled_dispatch_stall_per_warp_active.pct','smsp__warp_issue_stalled_not_selected_per_warp_active.pct','smsp__warp_issue_stalled_selected_per_warp_active.pct']
+idx={h:i for i,h in enumerate(hdr)}
+for d in data:
+    print('-----')
+    for w in want:
+        if w in idx: print(f"  {w:70s} {d[idx[w]]} {units[idx[w]]}")
