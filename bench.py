@@ -89,7 +89,7 @@ class ClockSampler:
 
     def summary(self):
         rows = self.rows[max(0, getattr(self, "start", 1) - 1):getattr(self, "end", len(self.rows))]
-        self.rows = rows
+        self.rows = [r for r in rows if len(r) >= 8]
         if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
         sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]

@@ -403,19 +403,40 @@ __global__ void __launch_bounds__(kFastThreads) merge_fast_kernel(MergeParams mp
   uint32_t written = 0;  // slots of this lane's list written into the image last time
   __syncwarp();
 
-  for (uint32_t g = blockIdx.x * nwarps + warp; g < mp.n_groups; g += gridDim.x * nwarps) {
+  // counts and group bases of the next group are loaded one iteration ahead
+  const uint32_t gstride = gridDim.x * nwarps;
+  uint32_t nc[NS], nb[NS];
+  auto prefetch = [&](uint32_t gg) {
+    const uint32_t pp = gg * 32 + lane;
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      nc[s] = 0;
+      nb[s] = 0;
+      if (s < n && gg < mp.n_groups) {
+        if (pp < mp.P) nc[s] = __ldg(mp.src[s].count + pp);
+        nb[s] = __ldg(mp.group_base + (size_t)s * mp.n_groups + gg);
+      }
+    }
+  };
+  prefetch(blockIdx.x * nwarps + warp);
+
+  for (uint32_t g = blockIdx.x * nwarps + warp; g < mp.n_groups; g += gstride) {
     const uint32_t p0 = g * 32, p = p0 + lane;
     const bool valid = p < mp.P;
     uint32_t cnt[NS], gidx[NS];
     uint32_t m = 0;
 #pragma unroll
     for (int s = 0; s < NS; ++s) {
-      cnt[s] = gidx[s] = 0;
+      cnt[s] = nc[s];
+      gidx[s] = nb[s];
+    }
+    prefetch(g + gstride);
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
       if (s < n) {
-        const uint32_t c = valid ? (uint32_t)__ldg(mp.src[s].count + p) : 0u;
+        const uint32_t c = cnt[s];
         const uint32_t incl = warp_incl_scan(c, lane);
-        cnt[s] = c;
-        gidx[s] = __ldg(mp.group_base + (size_t)s * mp.n_groups + g) + incl - c;
+        gidx[s] += incl - c;
         m += c;
       }
     }

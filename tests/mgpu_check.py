@@ -1,0 +1,110 @@
+"""Multi-GPU parity check, run under torchrun (one process per GPU):
+
+  torchrun --nproc-per-node N --master-addr 127.0.0.1 tests/mgpu_check.py [--config synthetic|C1|C3]
+
+Every rank builds the same seeded inputs (neutral synth/ generators), keeps
+the PEs homed on it (PAPER.md:218 block placement), composites its strip
+through vdi_composite (NCCL size exchange + all-to-allv) and
+gathers to rank 0 (vdi_gather).  Rank 0 checks the gathered
+image bit-for-bit against a 1-GPU composite of the same inputs (the result
+must not depend on G) and against the CPU oracle on sampled lists.
+Prints one JSON line on rank 0; exit code 0 iff all checks pass."""
+import argparse
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+import paper_2206_14503_b200 as vdi  # noqa: E402
+import synth  # noqa: E402
+from parity import compare, dense_to_device  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="synthetic")
+    ap.add_argument("--W", type=int, default=640)
+    ap.add_argument("--H", type=int, default=360)
+    ap.add_argument("--n", type=int, default=8)
+    ap.add_argument("--k", type=int, default=12)
+    ap.add_argument("--lam", type=float, default=9.0)
+    args = ap.parse_args()
+    world, rank, local = int(os.environ["WORLD_SIZE"]), int(os.environ["RANK"]), int(os.environ["LOCAL_RANK"])
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    obj = [vdi.get_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+
+    if args.config == "synthetic":
+        W, H, n, k_in, k_out = args.W, args.H, args.n, args.k, args.k
+        pes_np = synth.random_subvdis(n, W, H, k_in, lam=args.lam, seed=31)
+        comp = vdi.Compositor(W, H, k_in, k_out, n, n_ranks=world, rank=rank, unique_id=obj[0])
+        local_pes = [dense_to_device(pes_np[pe], pe) for pe in range(n) if vdi.pe_home(n, world, pe) == rank]
+    else:
+        cfg = synth.config_by_name(args.config)
+        W, H, n, k_in, k_out = cfg.W, cfg.H, cfg.n_pes, cfg.k_in, cfg.k_out
+        comp = vdi.Compositor(W, H, k_in, k_out, n, n_ranks=world, rank=rank, unique_id=obj[0])
+        vol = synth.make_volume(cfg, device="cuda")
+        tf = torch.from_numpy(synth.tf_table(cfg.tf, cfg.tf_scale)).cuda()
+        cam = synth.make_camera(W, H)
+        dec = cfg.decomposition()
+        local_pes = [comp.generate_subvdi(vol, tf, cam, dec, pe) for pe in range(n)
+                     if vdi.pe_home(n, world, pe) == rank]
+        pes_np = None
+
+    strip = comp.empty_strip()
+    image = vdi.FullVDI.empty(W, 0, H, k_out) if rank == 0 else None
+    comp.composite(local_pes, strip)
+    comp.gather(strip, image)
+    cnt = comp.counters()
+    torch.cuda.synchronize()
+    ok = True
+    res = {"world": world, "config": args.config, "bytes_sent_rank": cnt["bytes_sent"],
+           "bytes_received_rank": cnt["bytes_received"]}
+    # byte conservation over ranks
+    t = torch.tensor([cnt["bytes_sent"], cnt["bytes_received"]], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t)
+    res["sent_total"], res["received_total"] = int(t[0]), int(t[1])
+    ok &= int(t[0]) == int(t[1])
+
+    # single-GPU reference composite on rank 0 (all PEs, G = 1)
+    if args.config != "synthetic":
+        # every rank regenerates all PEs so rank 0 can run the G = 1 composite
+        allp = [comp.generate_subvdi(vol, tf, cam, dec, pe) for pe in range(n)] if rank == 0 else []
+    dist.barrier()
+    if rank == 0:
+        one = vdi.Compositor(W, H, k_in, k_out, n)
+        if args.config == "synthetic":
+            allp = [dense_to_device(p, i) for i, p in enumerate(pes_np)]
+        ref = one.empty_strip()
+        one.composite(allp, ref)
+        torch.cuda.synchronize()
+        same = all(torch.equal(a, b) for a, b in ((image.count, ref.count), (image.depth, ref.depth),
+                                                     (image.rgba, ref.rgba)))
+        res["bit_identical_to_1gpu"] = bool(same)
+        ok &= same
+        if pes_np is not None:
+            import oracle
+            rng = np.random.default_rng(3)
+            pix = np.unique(rng.choice(W * H, min(6000, W * H), replace=False))
+            o = oracle.composite_pixels(pes_np, pix, k_out)
+            gc, gd, gr = image.count.cpu().numpy(), image.depth.cpu().numpy(), image.rgba.cpu().numpy()
+            nl, ties = compare(gc[pix], gd[pix], gr[pix], o["count"], o["depth"], o["rgba"], o["stats"]["margin"],
+                               "mgpu")
+            res["oracle_lists_checked"] = nl
+            res["oracle_ties"] = len(ties)
+        print(json.dumps(res), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+    sys.exit(0 if ok else 1)
+
+
+if __name__ == "__main__":
+    main()

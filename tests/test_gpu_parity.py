@@ -164,3 +164,19 @@ def test_full_size_synthetic_sampled(vdi, orc):
     gc, gd, gr = full_to_numpy(strip)
     compare(gc[pix], gd[pix], gr[pix], ref["count"], ref["depth"], ref["rgba"], ref["stats"]["margin"], "1080p")
     assert cnt["records_in"] == sum(int(p["count"].sum()) for p in pes)
+
+
+def test_multi_gpu_strip_invariance(vdi):
+    """G = 2 (or all visible GPUs): NCCL exchange + gather give the 1-GPU result
+    bit-for-bit and match the oracle (tests/mgpu_check.py under torchrun)."""
+    import os
+    import subprocess
+    import sys
+    n = torch.cuda.device_count()
+    if n < 2:
+        pytest.skip("needs >= 2 GPUs")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={min(n, 4)}",
+           "--master-addr", "127.0.0.1", "--master-port", "29533", os.path.join(root, "tests", "mgpu_check.py")]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
