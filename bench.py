@@ -349,7 +349,10 @@ def run_ours(args, world, rank, local):
                          "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                          "algorithmic_bytes": int(B_merge), "ms": ms_merge, "ms_max_over_ranks": ms_merge_max},
-            "stages_ms": {"exchange": ms_ex, "merge": ms_merge, "gather": ms_ga},
+            "stages_ms": {"exchange": ms_ex, "merge": ms_merge, "gather": ms_ga,
+                          "merge_scan": statistics.mean(c["ms_scan"] for c in stage),
+                          "merge_fast": statistics.mean(c["ms_fast"] for c in stage),
+                          "merge_search": statistics.mean(c["ms_search"] for c in stage)},
             "supersegments_merged_per_s": rec * G / (ms_per_step * 1e-3),
             "searched_lists": stage[-1]["searched_lists"],
             "search_buckets": stage[-1]["bucket_lists"], "fast_fallback_groups": stage[-1]["fallback_groups"],

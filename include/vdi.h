@@ -190,8 +190,10 @@ typedef struct {
   uint64_t bytes_received;  /* all-to-allv payload bytes received */
   uint32_t kernel_launches; /* libvdi kernels launched by the call */
   float ms_exchange, ms_merge, ms_gather; /* VDI_FLAG_STAGE_TIMING, else 0 */
-  uint64_t bucket_lists[4];  /* lists sent to search buckets m<=32, <=64, <=128, and the general path */
-  uint64_t fallback_groups;  /* 32-list groups whose records exceeded the fast kernel's staging buffer */
+  uint64_t bucket_lists[4];  /* lists sent to the search buckets m <= 32, <= 40, <= 64, <= 128 */
+  uint64_t general_lists;    /* lists sent to the general path (overlaps, alpha == 0, m > 128) */
+  uint64_t fallback_groups;  /* 32-list groups written with plain stores (tail group / unaligned output) */
+  float ms_scan, ms_fast, ms_search; /* VDI_FLAG_STAGE_TIMING: receive scan, pass-through kernel, search kernels */
 } vdi_counters;
 vdi_status vdi_get_counters(vdi_ctx* ctx, vdi_counters* out);
 

@@ -60,7 +60,7 @@ struct GenOut {
 struct DevCounters {
   uint32_t wl_count[VDI_N_BUCKETS];
   int err;
-  int pad;
+  uint32_t search_ticket[VDI_N_BUCKETS];
   unsigned long long scratch_used;
   unsigned long long records_in;
   unsigned long long fallback_groups;
@@ -77,7 +77,7 @@ struct vdi_ctx {
   uint32_t row0 = 0, row1 = 0;
   uint64_t P = 0;  // lists in this rank's strip
   // merge scratch
-  DevBuf group_sum, group_base, wl, scratch, dcnt, stat_gamma, stat_m, bounds;
+  DevBuf group_sum, group_base, wl, scratch, dcnt, stat_gamma, stat_m, bounds, srch;
   // exchange receive buffers per source
   std::vector<DevBuf> rcount, rdepth, rrgba;
   // generator outputs per pe
@@ -91,7 +91,7 @@ struct vdi_ctx {
   // counters
   vdi_counters last{};
   bool have_stats = false;
-  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  cudaEvent_t ev[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
   bool timing_pending = false;
   bool gather_timing_pending = false;
   cudaEvent_t gev[2] = {nullptr, nullptr};
@@ -494,6 +494,26 @@ vdi_status vdi_composite(vdi_ctx* ctx, const vdi_dense_view* local, uint32_t n_l
     CUDA_TRY(ctx, ctx->stat_gamma.grow(ctx->P * 4));
     CUDA_TRY(ctx, ctx->stat_m.grow(ctx->P * 2));
   }
+  // short-list search scratch: a list in bucket b has m > k_out samples, so
+  // at most S_here / (k_out + 1) lists (and at most P) land there
+  const uint64_t sl = std::min<uint64_t>(ctx->P, S_here / (k + 1) + 1);
+  const uint64_t sb = (sl + 31) / 32;  // batches
+  const size_t srch_bytes = sb * 32 * (32 + 40) * 24 + 2 * sb * 64 * 4 + 1024;
+  CUDA_TRY(ctx, ctx->srch.grow(srch_bytes));
+  {
+    char* q = ctx->srch.as<char>();
+    mp.srch_rgba[0] = reinterpret_cast<float4*>(q);
+    q += sb * 32 * 32 * 16;
+    mp.srch_rgba[1] = reinterpret_cast<float4*>(q);
+    q += sb * 32 * 40 * 16;
+    mp.srch_depth[0] = reinterpret_cast<float2*>(q);
+    q += sb * 32 * 32 * 8;
+    mp.srch_depth[1] = reinterpret_cast<float2*>(q);
+    q += sb * 32 * 40 * 8;
+    mp.srch_gap[0] = reinterpret_cast<uint32_t*>(q);
+    q += sb * 64 * 4;
+    mp.srch_gap[1] = reinterpret_cast<uint32_t*>(q);
+  }
   DevCounters* dc = ctx->dcnt.as<DevCounters>();
   CUDA_TRY(ctx, cudaMemsetAsync(dc, 0, sizeof(DevCounters), st));
   mp.group_base = ctx->group_base.as<uint32_t>();
@@ -503,6 +523,7 @@ vdi_status vdi_composite(vdi_ctx* ctx, const vdi_dense_view* local, uint32_t n_l
   for (int b = 0; b < VDI_N_BUCKETS; ++b) mp.wl[b] = ctx->wl.as<uint32_t>() + wl_bucket * b;
   mp.wl_count = dc->wl_count;
   mp.fallback_groups = &dc->fallback_groups;
+  mp.search_ticket = dc->search_ticket;
   mp.wl_cap = (uint32_t)std::max<uint64_t>(ctx->P, 1);
   mp.scratch_used = &dc->scratch_used;
   mp.scratch_cap = 4 * S_here;
@@ -514,7 +535,8 @@ vdi_status vdi_composite(vdi_ctx* ctx, const vdi_dense_view* local, uint32_t n_l
   mp.validate = (cf.flags & VDI_FLAG_VALIDATE) ? 1 : 0;
   if (ctx->P) {
     CUDA_TRY(ctx, launch_scan(mp, ctx->group_sum.as<uint32_t>(), ctx->group_base.as<uint32_t>(), st, &launches));
-    CUDA_TRY(ctx, launch_merge(mp, st, &launches));
+    if (timing) CUDA_TRY(ctx, cudaEventRecord(ctx->ev[3], st));
+    CUDA_TRY(ctx, launch_merge(mp, st, &launches, timing ? ctx->ev + 4 : nullptr));
   }
   if (timing) {
     CUDA_TRY(ctx, cudaEventRecord(ctx->ev[2], st));
@@ -651,14 +673,20 @@ vdi_status vdi_get_counters(vdi_ctx* ctx, vdi_counters* out) {
   if (h.err & 1) return fail(VDI_ERR_INTERNAL, "merge work list / scratch overflow");
   ctx->last.records_in = h.records_in;
   ctx->last.searched_lists = 0;
+  ctx->last.general_lists = h.wl_count[VDI_BUCKET_GENERAL];
   for (int b = 0; b < VDI_N_BUCKETS; ++b) {
     ctx->last.searched_lists += h.wl_count[b];
-    ctx->last.bucket_lists[b] = h.wl_count[b];
+    if (b < 4) ctx->last.bucket_lists[b] = h.wl_count[b];
   }
   ctx->last.fallback_groups = h.fallback_groups;
   if (ctx->timing_pending) {
     CUDA_TRY(ctx, cudaEventElapsedTime(&ctx->last.ms_exchange, ctx->ev[0], ctx->ev[1]));
     CUDA_TRY(ctx, cudaEventElapsedTime(&ctx->last.ms_merge, ctx->ev[1], ctx->ev[2]));
+    if (ctx->P) {
+      CUDA_TRY(ctx, cudaEventElapsedTime(&ctx->last.ms_scan, ctx->ev[1], ctx->ev[3]));
+      CUDA_TRY(ctx, cudaEventElapsedTime(&ctx->last.ms_fast, ctx->ev[3], ctx->ev[4]));
+      CUDA_TRY(ctx, cudaEventElapsedTime(&ctx->last.ms_search, ctx->ev[4], ctx->ev[5]));
+    }
     ctx->timing_pending = false;
   }
   if (ctx->gather_timing_pending) {

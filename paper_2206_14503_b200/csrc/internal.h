@@ -30,11 +30,12 @@ struct SrcDesc {
 };
 
 // Work-list buckets of lists that need more than the pass-through:
-// 0..2 = gamma search with m <= 32 / 64 / 128 samples (warp-per-32-lists,
-// samples in shared memory); 3 = general path (overlap subdivision, alpha==0
-// records, or m > 128; thread per list, global scratch).
-#define VDI_N_BUCKETS 4
-#define VDI_BUCKET_GENERAL 3
+// 0, 1 = gamma search with m <= 32 / 40 samples (samples in registers);
+// 2, 3 = gamma search with m <= 64 / 128 samples (samples in shared memory);
+// 4 = general path (overlap subdivision, alpha==0 records, or m > 128;
+// thread per list, global scratch).
+#define VDI_N_BUCKETS 5
+#define VDI_BUCKET_GENERAL 4
 
 struct MergeParams {
   SrcDesc src[VDI_MAX_SRC];
@@ -58,7 +59,12 @@ struct MergeParams {
   float* stat_gamma;   // optional [P]
   uint16_t* stat_m;    // optional [P]
   unsigned long long* records_in;
-  unsigned long long* fallback_groups;  // groups whose records did not fit the warp's staging buffer
+  unsigned long long* fallback_groups;  // groups written with plain stores
+  uint32_t* search_ticket;              // [VDI_N_BUCKETS] per-bucket claim tickets of the search kernels
+  // short-list search scratch (buckets 0, 1: MS = 32, 40): [batch][MS][32] samples, [batch][2][32] gap bits
+  float4* srch_rgba[2];
+  float2* srch_depth[2];
+  uint32_t* srch_gap[2];
   int* err;            // bit 0: work list / scratch overflow
   int validate;
 };
@@ -67,7 +73,8 @@ struct MergeParams {
 uint32_t scan_chunks(uint32_t P);  // chunks of the receive-side scan
 cudaError_t launch_scan(const MergeParams& mp, uint32_t* chunk_sum, uint32_t* group_base, cudaStream_t st,
                         int* launches);
-cudaError_t launch_merge(const MergeParams& mp, cudaStream_t st, int* launches);
+// ev (optional, 2 entries): recorded after the fast kernel and after the search kernels
+cudaError_t launch_merge(const MergeParams& mp, cudaStream_t st, int* launches, cudaEvent_t* ev);
 
 // Generator (generate.cu)
 struct GenParams {

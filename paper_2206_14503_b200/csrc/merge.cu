@@ -239,7 +239,9 @@ __device__ __forceinline__ void push_entries(const MergeParams& mp, int bk, uint
   }
 }
 
-__device__ __forceinline__ int bucket_of(uint32_t m) { return m <= 32 ? 0 : m <= 64 ? 1 : m <= 128 ? 2 : 3; }
+__device__ __forceinline__ int bucket_of(uint32_t m) {
+  return m <= 32 ? 0 : m <= 40 ? 1 : m <= 64 ? 2 : m <= 128 ? 3 : VDI_BUCKET_GENERAL;
+}
 
 // Run-based k-way merge of NS sorted runs held in shared memory (PAPER.md:168:
 // repeatedly take the run with the lowest starting depth; ties -> lower PE id,
@@ -343,6 +345,62 @@ __device__ __forceinline__ bool direct_list(const MergeParams& mp, uint32_t p, c
     mp.out_rgba[(size_t)p * k + r] = c;
   }
   return true;
+}
+
+// global address of the record with PE-concatenated index ci of one list
+template <int NS>
+__device__ __forceinline__ uint32_t concat_src(const uint32_t (&cs)[NS], const uint32_t (&cnt)[NS],
+                                               const uint32_t (&goff)[NS], uint32_t ci, int* src) {
+  uint32_t gi = 0;
+  int sb = 0;
+#pragma unroll
+  for (int s = 0; s < NS; ++s)
+    if (ci >= cs[s] && ci < cs[s] + cnt[s]) {
+      gi = goff[s] + (ci - cs[s]);
+      sb = s;
+    }
+  *src = sb;
+  return gi;
+}
+
+// Load the records of one list in PE-concatenated order (PE s's run at
+// [cs[s], cs[s] + cnt[s])) with CH loads in flight per trip, instead of one
+// dependent round trip per record.  dst_d[q * stride], dst_c[q * stride]
+// (dst_c may be null).
+template <int NS, int CH>
+__device__ __forceinline__ void load_concat(const MergeParams& mp, const uint32_t (&goff)[NS],
+                                            const uint32_t (&cnt)[NS], const uint32_t (&cs)[NS], uint32_t m,
+                                            float2* dst_d, float4* dst_c, int stride) {
+  for (uint32_t q0 = 0; q0 < m; q0 += CH) {
+    float2 dv[CH];
+    float4 cv[CH];
+#pragma unroll
+    for (int u = 0; u < CH; ++u) {
+      const uint32_t q = q0 + u;
+      if (q < m) {
+        const float2* dp = nullptr;
+        const float4* cp = nullptr;
+        uint32_t gi = 0;
+#pragma unroll
+        for (int s = 0; s < NS; ++s)
+          if (q >= cs[s] && q < cs[s] + cnt[s]) {
+            gi = goff[s] + (q - cs[s]);
+            dp = mp.src[s].depth;
+            cp = mp.src[s].rgba;
+          }
+        dv[u] = __ldg(dp + gi);
+        if (dst_c) cv[u] = __ldg(cp + gi);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < CH; ++u) {
+      const uint32_t q = q0 + u;
+      if (q < m) {
+        dst_d[q * stride] = dv[u];
+        if (dst_c) dst_c[q * stride] = cv[u];
+      }
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -460,16 +518,9 @@ __global__ void __launch_bounds__(kFastThreads) merge_fast_kernel(MergeParams mp
 #pragma unroll
         for (int s = 0; s < NS; ++s) {
           start[s] = j;
-          if (s < n) {
-            const float2* ds = mp.src[s].depth + gidx[s];
-            const float4* cs = mp.src[s].rgba + gidx[s];
-            for (uint32_t i = 0; i < cnt[s]; ++i) {
-              my_depth[j + i] = __ldg(ds + i);
-              my_rgba[j + i] = __ldg(cs + i);
-            }
-            j += cnt[s];
-          }
+          j += cnt[s];
         }
+        load_concat<NS, 4>(mp, gidx, cnt, start, m, my_depth, my_rgba, 1);
         written = m;
         // already in depth order (e.g. a single PE's run)?  then only validate
         bool sorted = true;
@@ -550,119 +601,419 @@ __global__ void __launch_bounds__(kFastThreads) merge_fast_kernel(MergeParams mp
 }
 
 // ---------------------------------------------------------------------------
-// Search path: one warp per 32 work-list lists with m <= MS (lane = list).
+// Search path: one warp per 32 work-list lists (lane = list) of one m-bucket.
+//   * depth order: run-based k-way merge over the lists' t_front values read
+//     through L1 -> permutation (concat index per position);
+//   * the rgba of every sample is gathered in depth order into a PACKED
+//     per-warp shared buffer (17 B per sample: rgba + permutation byte; lanes'
+//     regions are laid end to end by a warp scan of m), the gap bits live in
+//     registers, t_front / t_back are re-read through L1 only by the final
+//     write sweep -- so ~16 warps fit per SM;
+//   * per-list bisection (Q3-Q6) with branch-free
+//     count sweeps (the decisions of sweep(), Q1/Q2/Q8), then the write sweep.
+// Lists with transparent or overlapping records go to the general path.
 // ---------------------------------------------------------------------------
-// Count-mode sweep over the [sample][lane] shared-memory column of one list:
-// the same decisions as sweep() (Q1, Q2, Q8), branch-free per sample; the gap
-// before sample i is bit i of gapw.  Stops once the count exceeds k.
-template <int NW>
-__device__ __forceinline__ int sweep_count_smem(const float4* __restrict__ Sr, int lane, const uint32_t (&gapw)[NW],
-                                                int m, float gamma, int k) {
-  const float g2 = gamma * gamma;
-  float ar = 0.f, ag = 0.f, ab = 0.f, aa = 0.f;
-  int cnt = 0;
-  bool open = false;
-  for (int i = 0; i < m && cnt <= k; ++i) {
-    const float4 s = Sr[i * 32 + lane];
-    const bool gap = (gapw[i >> 5] >> (i & 31)) & 1u;
-    if (gap && dist2(ar, ag, ab, aa, 0.f, 0.f, 0.f, 0.f) > g2) open = false;
-    const bool start = !open || dist2(ar, ag, ab, aa, s.x, s.y, s.z, s.w) > g2;
-    const float tr = 1.0f - aa;
-    ar = start ? s.x : fmaf(tr, s.x, ar);
-    ag = start ? s.y : fmaf(tr, s.y, ag);
-    ab = start ? s.z : fmaf(tr, s.z, ab);
-    aa = start ? s.w : fmaf(tr, s.w, aa);
-    cnt += start ? 1 : 0;
-    open = true;
-  }
-  return cnt;
-}
+static constexpr int kRefill = 8;  // lanes that must be free before the warp refills them together
 
 template <int NS, int MS>
 __global__ void __launch_bounds__(32) merge_search_kernel(MergeParams mp, int bucket) {
   extern __shared__ float4 smem[];
-  float4* Sr = smem;                                       // [MS][32] rgba, depth order
-  float2* Sd = reinterpret_cast<float2*>(Sr + MS * 32);    // [MS][32] depth, PE-concatenated order
-  uint8_t* Pm = reinterpret_cast<uint8_t*>(Sd + MS * 32);  // [MS][32] permutation (concat index)
+  float4* Sr = smem;                                             // [MS][32] rgba, depth order
+  float2* Sd = reinterpret_cast<float2*>(Sr + MS * 32);          // [MS][32] depth, PE-concatenated order
+  uint8_t* Pm = reinterpret_cast<uint8_t*>(Sd + MS * 32);        // [MS][32] concat index
   constexpr int NW = (MS + 31) / 32;
   const int lane = threadIdx.x;
   const int k = mp.k_out, n = mp.n_src;
   const uint32_t total = min(mp.wl_count[bucket], mp.wl_cap);
   const uint32_t* wl = mp.wl[bucket];
-  for (uint32_t base = blockIdx.x * 32; base < total; base += gridDim.x * 32) {
-    const uint32_t e = base + lane;
-    const bool valid = e < total;
-    const uint32_t* ent = wl + (size_t)(valid ? e : 0) * (3 + n);
-    const uint32_t p = valid ? ent[0] : 0u;
-    const uint32_t m = valid ? ent[2] : 0u;
-    uint32_t goff[NS], cnt[NS], cs[NS];
-    uint32_t j = 0;
+  uint32_t* ticket = mp.search_ticket + bucket;
+  const unsigned lt = (1u << lane) - 1u;
+
+  // this lane's list
+  bool has = false;     // a list is loaded
+  bool done = false;    // its bisection finished (write pending)
+  uint32_t p = 0, m = 0, goff[NS], cnt[NS], cs[NS], gapw[NW];
+#pragma unroll
+  for (int s = 0; s < NS; ++s) goff[s] = cnt[s] = cs[s] = 0;
+#pragma unroll
+  for (int w = 0; w < NW; ++w) gapw[w] = 0;
+  float lo = 0.f, hi = 0.f, best = 0.f, mid = 0.f, g2 = 0.f, ar = 0.f, ag = 0.f, ab = 0.f, aa = 0.f;
+  int it = 0, i = 0, sc = 0;
+  uint32_t gw = 0;
+  bool drained = false;  // warp-uniform: the bucket's queue is empty
+
+  for (;;) {
+    // ---- completion + refill, once enough lanes are free --------------------
+    const unsigned busy = __ballot_sync(kFull, has && !done);
+    const unsigned freel = ~busy;
+    if (__popc(freel) >= kRefill || busy == 0) {
+      if (done) {  // final write sweep, then the lane is free
+        auto get = [&](int q) {
+          const float2 d = Sd[(uint32_t)Pm[q * 32 + lane] * 32 + lane];
+          const float4 c = Sr[q * 32 + lane];
+          return Rec{d.x, d.y, c.x, c.y, c.z, c.w};
+        };
+        const int c = sweep(get, (int)m, best, k, mp.out_depth + (size_t)p * k, mp.out_rgba + (size_t)p * k);
+        mp.out_count[p] = (uint8_t)c;
+        if (mp.stat_gamma) mp.stat_gamma[p] = best;
+        has = done = false;
+      }
+      if (!drained) {
+        const unsigned idle = __ballot_sync(kFull, !has);
+        const uint32_t nidle = __popc(idle);
+        uint32_t t0 = 0;
+        if (lane == 0) t0 = atomicAdd(ticket, nidle);
+        t0 = __shfl_sync(kFull, t0, 0);
+        if (t0 + nidle >= total) drained = true;
+        const uint32_t e = t0 + __popc(idle & lt);
+        const bool take = !has && e < total;
+        int bk = -1;
+        if (take) {
+          const uint32_t* ent = wl + (size_t)e * (3 + n);
+          p = ent[0];
+          m = ent[2];
+          uint32_t j = 0;
+#pragma unroll
+          for (int s = 0; s < NS; ++s) {
+            goff[s] = cnt[s] = cs[s] = 0;
+            if (s < n) {
+              goff[s] = ent[3 + s];
+              cnt[s] = __ldg(mp.src[s].count + p);
+              cs[s] = j;
+              j += cnt[s];
+            }
+          }
+          load_concat<NS, 8>(mp, goff, cnt, cs, m, Sd + lane, nullptr, 32);
+          // depth order: run-based k-way merge over the staged t_front column
+          // (PAPER.md:168); gap bits and the overlap test (Q12) on the way
+#pragma unroll
+          for (int w = 0; w < NW; ++w) gapw[w] = 0;
+          bool bad = false;
+          float prev_tb = -CUDART_INF_F;
+          uint32_t hp[NS];
+#pragma unroll
+          for (int s = 0; s < NS; ++s) hp[s] = 0;
+          uint32_t r = 0;
+          while (r < m) {
+            int b = -1, b2 = NS;
+            float bt = CUDART_INF_F, b2t = CUDART_INF_F;
+#pragma unroll
+            for (int s = 0; s < NS; ++s)
+              if (hp[s] < cnt[s]) {
+                const float t = Sd[(cs[s] + hp[s]) * 32 + lane].x;
+                if (b < 0 || t < bt) {
+                  if (b >= 0) {
+                    b2t = bt;
+                    b2 = b;
+                  }
+                  bt = t;
+                  b = s;
+                } else if (t < b2t) {
+                  b2t = t;
+                  b2 = s;
+                }
+              }
+            uint32_t ii = 0, cb = 0, c0 = 0;
+#pragma unroll
+            for (int s = 0; s < NS; ++s)
+              if (s == b) {
+                ii = hp[s];
+                cb = cnt[s];
+                c0 = cs[s];
+              }
+            for (;;) {
+              const float2 d = Sd[(c0 + ii) * 32 + lane];
+              bad |= d.x < prev_tb;
+              if (r > 0 && d.x > prev_tb) gapw[r >> 5] |= 1u << (r & 31);
+              prev_tb = d.y;
+              Pm[r * 32 + lane] = (uint8_t)(c0 + ii);
+              ++r;
+              ++ii;
+              if (ii >= cb) break;
+              const float tn = Sd[(c0 + ii) * 32 + lane].x;
+              if (!(tn < b2t || (tn == b2t && b < b2))) break;
+            }
+#pragma unroll
+            for (int s = 0; s < NS; ++s)
+              if (s == b) hp[s] = ii;
+          }
+          // gather rgba in depth order (independent loads); transparent test (Q23)
+#pragma unroll 4
+          for (uint32_t q = 0; q < m; ++q) {
+            int sb;
+            const uint32_t gi = concat_src<NS>(cs, cnt, goff, Pm[q * 32 + lane], &sb);
+            const float4* cp = nullptr;
+#pragma unroll
+            for (int s = 0; s < NS; ++s)
+              if (s == sb) cp = mp.src[s].rgba;
+            const float4 c = __ldg(cp + gi);
+            Sr[q * 32 + lane] = c;
+            bad |= c.w == 0.f;
+          }
+          if (bad) {
+            bk = VDI_BUCKET_GENERAL;
+          } else {
+            has = true;
+            done = mp.max_iters <= 0;
+            lo = 0.f;
+            hi = best = mp.gamma_max;
+            mid = 0.5f * (lo + hi);
+            g2 = mid * mid;
+            it = i = sc = 0;
+            ar = ag = ab = aa = 0.f;
+            gw = gapw[0];
+          }
+        }
+        if (__any_sync(kFull, bk >= 0)) push_entries<NS>(mp, bk, p, m, goff, lane);
+      }
+      if (!__any_sync(kFull, has)) {
+        if (drained) break;
+        continue;
+      }
+    }
+    // ---- sweeps: every lane advances its own (iteration, sample) state ------
+    // (flattened bisection, an exact replay of bisect(): PAPER.md:100-101, :176)
+    for (;;) {
+      if (has && !done) {
+        const float4 sv = Sr[i * 32 + lane];
+        const uint32_t gapb = (gw >> (i & 31)) & 1u;
+        const float n2 = fmaf(aa, aa, fmaf(ab, ab, fmaf(ag, ag, ar * ar)));  // dist2(acc, 0), Q8
+        const float d2 = dist2(ar, ag, ab, aa, sv.x, sv.y, sv.z, sv.w);
+        // open before sample i is (i > 0); a gap closes iff |acc| > gamma (Q1, Q2, Q8)
+        const uint32_t st = (uint32_t)(i == 0) | (gapb & (uint32_t)(n2 > g2)) | (uint32_t)(d2 > g2);
+        const float tr = 1.0f - aa;
+        ar = st ? sv.x : fmaf(tr, sv.x, ar);
+        ag = st ? sv.y : fmaf(tr, sv.y, ag);
+        ab = st ? sv.z : fmaf(tr, sv.z, ab);
+        aa = st ? sv.w : fmaf(tr, sv.w, aa);
+        sc += (int)st;
+        ++i;
+        const bool end = (i >= (int)m) | (sc > k);
+        const bool feas = sc <= k;
+        const bool stop = end & ((feas & (sc == k)) | (it + 1 >= mp.max_iters));
+        best = (end & feas) ? mid : best;
+        hi = (end & feas) ? mid : hi;
+        lo = (end & !feas) ? mid : lo;
+        it += end ? 1 : 0;
+        const float nmid = 0.5f * (lo + hi);
+        mid = end ? nmid : mid;
+        g2 = end ? nmid * nmid : g2;
+        i = end ? 0 : i;
+        sc = end ? 0 : sc;
+        if ((i & 31) == 0) gw = gapw[i >> 5];
+        done = stop;
+      }
+      const unsigned run = __ballot_sync(kFull, has && !done);
+      if (run == 0 || (!drained && __popc(~run) >= kRefill)) break;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Search path for short lists (m <= 40), in two kernels:
+//   search_gather : thread per list (high occupancy hides the latency): the
+//                   run-based k-way merge over the per-PE runs,
+//                   then the samples are written in depth order to a scratch
+//                   in [batch][sample][lane] layout, plus the gap bits;
+//                   transparent / overlapping records -> general path;
+//   search_sweep  : warp per batch of 32 lists: one coalesced, independent
+//                   load of each lane's samples into a statically indexed
+//                   register array, the bisection as
+//                   fully unrolled predicated sweeps, and the final write
+//                   sweep -- no loads inside the sweeps.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int short_ms(int b) { return b == 0 ? 32 : 40; }
+
+template <int NS>
+__global__ void __launch_bounds__(128) search_gather_kernel(MergeParams mp) {
+  const int n = mp.n_src;
+  const uint32_t c0 = min(mp.wl_count[0], mp.wl_cap), c1 = min(mp.wl_count[1], mp.wl_cap);
+  const uint32_t tot = ((c0 + 31) & ~31u) + c1;  // bucket 1 starts at a warp boundary
+  const uint32_t lane = threadIdx.x & 31;
+  for (uint32_t v0 = blockIdx.x * blockDim.x; v0 < tot; v0 += gridDim.x * blockDim.x) {
+    const uint32_t v = v0 + threadIdx.x;
+    const uint32_t c0r = (c0 + 31) & ~31u;
+    const int bucket = v < c0r ? 0 : 1;
+    const uint32_t i = bucket == 0 ? v : v - c0r;
+    const bool valid = i < (bucket == 0 ? c0 : c1);
+    const int MS = short_ms(bucket);
+    const uint32_t* ent = mp.wl[bucket] + (size_t)(valid ? i : 0) * (3 + n);
+    const uint32_t p = valid ? ent[0] : 0u, m = valid ? ent[2] : 0u;
+    uint32_t goff[NS], cnt[NS];
 #pragma unroll
     for (int s = 0; s < NS; ++s) {
-      goff[s] = cnt[s] = cs[s] = 0;
+      goff[s] = cnt[s] = 0;
       if (valid && s < n) {
         goff[s] = ent[3 + s];
         cnt[s] = __ldg(mp.src[s].count + p);
-        cs[s] = j;
-        const float2* ds = mp.src[s].depth + goff[s];
-        for (uint32_t i = 0; i < cnt[s]; ++i) Sd[(j + i) * 32 + lane] = __ldg(ds + i);
-        j += cnt[s];
       }
     }
-    int bk = -1;
-    uint32_t gapw[NW];
-#pragma unroll
-    for (int w = 0; w < NW; ++w) gapw[w] = 0;
+    float4* orgba = mp.srch_rgba[bucket] + (size_t)(i >> 5) * MS * 32 + lane;
+    float2* odep = mp.srch_depth[bucket] + (size_t)(i >> 5) * MS * 32 + lane;
+    uint32_t g0 = 0, g1 = 0;
+    bool bad = false;
     if (valid) {
-      // depth order over the staged t_front column (alpha tested after the gather)
-      const bool ok = run_merge<NS>(Sd + lane, 32, cs, cnt, m, Pm + lane, 32, [](uint32_t) { return 1.f; });
-      if (!ok) {
-        bk = VDI_BUCKET_GENERAL;
-      } else {
-        // gather rgba in depth order (independent loads) and the gap bits
-        float prev_tb = 0.f;
-        bool transparent = false;
-#pragma unroll 4
-        for (uint32_t r = 0; r < m; ++r) {
-          const uint32_t ci = Pm[r * 32 + lane];
-          const float4* cp = nullptr;
+      uint32_t hp[NS];
 #pragma unroll
-          for (int s = 0; s < NS; ++s)
-            if (ci >= cs[s] && ci < cs[s] + cnt[s]) cp = mp.src[s].rgba + goff[s] + (ci - cs[s]);
-          const float4 c = __ldg(cp);
-          Sr[r * 32 + lane] = c;
-          transparent |= c.w == 0.f;
-          const float2 d = Sd[ci * 32 + lane];
-          if (r > 0 && d.x > prev_tb) gapw[r >> 5] |= 1u << (r & 31);
+      for (int s = 0; s < NS; ++s) hp[s] = 0;
+      float prev_tb = -CUDART_INF_F;
+      uint32_t r = 0;
+      while (r < m) {
+        int b = -1, b2 = NS;
+        float bt = CUDART_INF_F, b2t = CUDART_INF_F;
+#pragma unroll
+        for (int s = 0; s < NS; ++s)
+          if (hp[s] < cnt[s]) {
+            const float t = __ldg(&mp.src[s].depth[goff[s] + hp[s]].x);
+            if (b < 0 || t < bt) {
+              if (b >= 0) {
+                b2t = bt;
+                b2 = b;
+              }
+              bt = t;
+              b = s;
+            } else if (t < b2t) {
+              b2t = t;
+              b2 = s;
+            }
+          }
+        uint32_t ii = 0, cb = 0, gb = 0;
+        const float2* dp = nullptr;
+        const float4* cp = nullptr;
+#pragma unroll
+        for (int s = 0; s < NS; ++s)
+          if (s == b) {
+            ii = hp[s];
+            cb = cnt[s];
+            gb = goff[s];
+            dp = mp.src[s].depth;
+            cp = mp.src[s].rgba;
+          }
+        for (;;) {
+          const float2 d = __ldg(dp + gb + ii);
+          const float4 c = __ldg(cp + gb + ii);
+          bad |= c.w == 0.f || d.x < prev_tb;  // Q23 / Q12
+          if (r > 0 && d.x > prev_tb) {
+            if (r < 32) g0 |= 1u << r;
+            else g1 |= 1u << (r - 32);
+          }
           prev_tb = d.y;
+          orgba[r * 32] = c;
+          odep[r * 32] = d;
+          ++r;
+          ++ii;
+          if (ii >= cb) break;
+          const float tn = __ldg(&dp[gb + ii].x);
+          if (!(tn < b2t || (tn == b2t && b < b2))) break;
         }
-        if (transparent) bk = VDI_BUCKET_GENERAL;
+#pragma unroll
+        for (int s = 0; s < NS; ++s)
+          if (s == b) hp[s] = ii;
       }
+      uint32_t* og = mp.srch_gap[bucket] + (size_t)(i >> 5) * 64 + lane;
+      og[0] = g0;
+      og[32] = g1;
     }
+    const int bk = (valid && bad) ? VDI_BUCKET_GENERAL : -1;
     if (__any_sync(kFull, bk >= 0)) push_entries<NS>(mp, bk, p, m, goff, lane);
-    if (!(valid && bk < 0)) continue;
+    if (valid && bad) mp.srch_gap[bucket][(size_t)(i >> 5) * 64 + lane] = 0xffffffffu;  // skip marker
+    if (valid && bad) mp.srch_gap[bucket][(size_t)(i >> 5) * 64 + 32 + lane] = 0xffffffffu;
+  }
+}
 
-    // bisection (Q3-Q6)
-    const int mi = (int)m;
+template <int MS>
+__global__ void __launch_bounds__(32, 8) search_sweep_kernel(MergeParams mp, int bucket) {
+  const int lane = threadIdx.x;
+  const int k = mp.k_out, n = mp.n_src;
+  const uint32_t total = min(mp.wl_count[bucket], mp.wl_cap);
+  const uint32_t* wl = mp.wl[bucket];
+  for (uint32_t batch = blockIdx.x; batch * 32 < total; batch += gridDim.x) {
+    const uint32_t e = batch * 32 + lane;
+    const bool valid = e < total;
+    const uint32_t* ent = wl + (size_t)(valid ? e : 0) * (3 + n);
+    const uint32_t p = valid ? ent[0] : 0u;
+    const int mi = valid ? (int)ent[2] : 0;
+    const uint32_t* gp = mp.srch_gap[bucket] + (size_t)batch * 64 + lane;
+    const uint32_t gw0 = valid ? gp[0] : 0u, gw1 = valid ? gp[32] : 0u;
+    const bool bad = valid && gw0 == 0xffffffffu && gw1 == 0xffffffffu;  // sent to the general path
+    const float4* col = mp.srch_rgba[bucket] + (size_t)batch * MS * 32 + lane;
+    const float2* dcol = mp.srch_depth[bucket] + (size_t)batch * MS * 32 + lane;
+    float4 S[MS];
+#pragma unroll
+    for (int q = 0; q < MS; ++q) S[q] = (q < mi && !bad) ? col[q * 32] : make_float4(0.f, 0.f, 0.f, 0.f);
+    const uint32_t gapw[2] = {gw0, gw1};
+    bool active = valid && !bad && mp.max_iters > 0;
     float lo = 0.f, hi = mp.gamma_max, best = mp.gamma_max;
     for (int it = 0; it < mp.max_iters; ++it) {
+      if (!__any_sync(kFull, active)) break;
       const float mid = 0.5f * (lo + hi);
-      const int c = sweep_count_smem<NW>(Sr, lane, gapw, mi, mid, k);
-      if (c <= k) {
-        best = hi = mid;
-        if (c == k) break;
-      } else {
-        lo = mid;
+      const float g2 = mid * mid;
+      float ar = 0.f, ag = 0.f, ab = 0.f, aa = 0.f;
+      int sc = 0;
+#pragma unroll
+      for (int q = 0; q < MS; ++q) {
+        if ((q & 7) == 0 && q > 0 && !__any_sync(kFull, active && q < mi && sc <= k)) break;
+        const bool live = active && q < mi && sc <= k;
+        const float4 sv = S[q];
+        const bool gap = ((gapw[q >> 5] >> (q & 31)) & 1u) != 0u;
+        const float n2 = fmaf(aa, aa, fmaf(ab, ab, fmaf(ag, ag, ar * ar)));  // dist2(acc, 0), Q8
+        const float d2 = dist2(ar, ag, ab, aa, sv.x, sv.y, sv.z, sv.w);
+        const bool st = (q == 0) | (gap & (n2 > g2)) | (d2 > g2);  // open before q is (q > 0)
+        const float tr = 1.0f - aa;
+        const float nr = st ? sv.x : fmaf(tr, sv.x, ar), ng = st ? sv.y : fmaf(tr, sv.y, ag);
+        const float nb = st ? sv.z : fmaf(tr, sv.z, ab), na = st ? sv.w : fmaf(tr, sv.w, aa);
+        ar = live ? nr : ar;
+        ag = live ? ng : ag;
+        ab = live ? nb : ab;
+        aa = live ? na : aa;
+        sc += (live && st) ? 1 : 0;
+      }
+      if (active) {
+        if (sc <= k) {
+          best = hi = mid;
+          if (sc == k) active = false;
+        } else {
+          lo = mid;
+        }
+        if (it + 1 >= mp.max_iters) active = false;
       }
     }
-    auto get = [&](int i) {
-      const float2 d = Sd[(uint32_t)Pm[i * 32 + lane] * 32 + lane];
-      const float4 c = Sr[i * 32 + lane];
-      return Rec{d.x, d.y, c.x, c.y, c.z, c.w};
-    };
-    const int c = sweep(get, mi, best, k, mp.out_depth + (size_t)p * k, mp.out_rgba + (size_t)p * k);
-    mp.out_count[p] = (uint8_t)c;
-    if (mp.stat_gamma) mp.stat_gamma[p] = best;
+    if (valid && !bad) {  // final write sweep, unrolled: static sample indices
+      const float gg = best * best;
+      float2* od = mp.out_depth + (size_t)p * k;
+      float4* oc = mp.out_rgba + (size_t)p * k;
+      float ar = 0.f, ag = 0.f, ab = 0.f, aa = 0.f, tf = 0.f, tb = 0.f;
+      int c = 0;
+#pragma unroll
+      for (int q = 0; q < MS; ++q) {
+        if (q < mi) {
+          const float4 sv = S[q];
+          const float2 d = dcol[q * 32];
+          const bool gap = ((gapw[q >> 5] >> (q & 31)) & 1u) != 0u;
+          const float n2 = fmaf(aa, aa, fmaf(ab, ab, fmaf(ag, ag, ar * ar)));
+          const float d2 = dist2(ar, ag, ab, aa, sv.x, sv.y, sv.z, sv.w);
+          const bool st = (q == 0) | (gap & (n2 > gg)) | (d2 > gg);
+          if (st && q > 0 && c <= k) {  // close the open segment (ends at its last content sample)
+            od[c - 1] = make_float2(tf, tb);
+            oc[c - 1] = make_float4(ar, ag, ab, aa);
+          }
+          const float tr = 1.0f - aa;
+          ar = st ? sv.x : fmaf(tr, sv.x, ar);
+          ag = st ? sv.y : fmaf(tr, sv.y, ag);
+          ab = st ? sv.z : fmaf(tr, sv.z, ab);
+          aa = st ? sv.w : fmaf(tr, sv.w, aa);
+          tf = st ? d.x : tf;
+          tb = d.y;
+          c += st ? 1 : 0;
+        }
+      }
+      if (mi > 0 && c <= k) {
+        od[c - 1] = make_float2(tf, tb);
+        oc[c - 1] = make_float4(ar, ag, ab, aa);
+      }
+      mp.out_count[p] = (uint8_t)c;
+      if (mp.stat_gamma) mp.stat_gamma[p] = best;
+    }
   }
 }
 
@@ -851,8 +1202,23 @@ static cudaError_t launch_search(const MergeParams& mp, int bucket, cudaStream_t
   return cudaGetLastError();
 }
 
+template <int MS>
+static cudaError_t launch_sweep(const MergeParams& mp, int bucket, cudaStream_t st) {
+  static int per_sm = 0;
+  if (!per_sm) {
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, search_sweep_kernel<MS>, 32, 0);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 1) per_sm = 1;
+  }
+  uint32_t grid = (uint32_t)sm_count() * per_sm;
+  const uint32_t most = (mp.P + 31) / 32;
+  if (grid > most) grid = most ? most : 1;
+  search_sweep_kernel<MS><<<grid, 32, 0, st>>>(mp, bucket);
+  return cudaGetLastError();
+}
+
 template <int NS>
-static cudaError_t launch_all(const MergeParams& mp, cudaStream_t st, int* launches) {
+static cudaError_t launch_all(const MergeParams& mp, cudaStream_t st, int* launches, cudaEvent_t* ev) {
   const size_t smem = (size_t)(kFastThreads / 32) * fast_warp_bytes(mp.k_out);
   static int per_sm = 0;
   static size_t prepared = 0;
@@ -868,24 +1234,31 @@ static cudaError_t launch_all(const MergeParams& mp, cudaStream_t st, int* launc
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   ++*launches;
-  if ((e = launch_search<NS, 32>(mp, 0, st)) != cudaSuccess) return e;
+  if (ev) cudaEventRecord(ev[0], st);
+  search_gather_kernel<NS><<<sm_count() * 8, 128, 0, st>>>(mp);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
   ++*launches;
-  if ((e = launch_search<NS, 64>(mp, 1, st)) != cudaSuccess) return e;
+  if ((e = launch_sweep<32>(mp, 0, st)) != cudaSuccess) return e;
   ++*launches;
-  if ((e = launch_search<NS, 128>(mp, 2, st)) != cudaSuccess) return e;
+  if ((e = launch_sweep<40>(mp, 1, st)) != cudaSuccess) return e;
   ++*launches;
+  if ((e = launch_search<NS, 64>(mp, 2, st)) != cudaSuccess) return e;
+  ++*launches;
+  if ((e = launch_search<NS, 128>(mp, 3, st)) != cudaSuccess) return e;
+  ++*launches;
+  if (ev) cudaEventRecord(ev[1], st);
   merge_general_kernel<<<sm_count() * 4, kSlowThreads, 0, st>>>(mp);
   ++*launches;
   return cudaGetLastError();
 }
 
-cudaError_t launch_merge(const MergeParams& mp, cudaStream_t st, int* launches) {
-  if (mp.n_src <= 1) return launch_all<1>(mp, st, launches);
-  if (mp.n_src <= 2) return launch_all<2>(mp, st, launches);
-  if (mp.n_src <= 4) return launch_all<4>(mp, st, launches);
-  if (mp.n_src <= 8) return launch_all<8>(mp, st, launches);
-  if (mp.n_src <= 16) return launch_all<16>(mp, st, launches);
-  return launch_all<VDI_MAX_SRC>(mp, st, launches);
+cudaError_t launch_merge(const MergeParams& mp, cudaStream_t st, int* launches, cudaEvent_t* ev) {
+  if (mp.n_src <= 1) return launch_all<1>(mp, st, launches, ev);
+  if (mp.n_src <= 2) return launch_all<2>(mp, st, launches, ev);
+  if (mp.n_src <= 4) return launch_all<4>(mp, st, launches, ev);
+  if (mp.n_src <= 8) return launch_all<8>(mp, st, launches, ev);
+  if (mp.n_src <= 16) return launch_all<16>(mp, st, launches, ev);
+  return launch_all<VDI_MAX_SRC>(mp, st, launches, ev);
 }
 
 }  // namespace vdi
