@@ -57,10 +57,12 @@ struct GenOut {
 };
 
 // device-side counters of one composite
+#define VDI_MAX_CHUNKS 8
 struct DevCounters {
-  uint32_t wl_count[VDI_N_BUCKETS];
+  uint32_t wl_count[VDI_MAX_CHUNKS][VDI_N_BUCKETS];
+  uint32_t search_ticket[VDI_MAX_CHUNKS][VDI_N_BUCKETS];
   int err;
-  uint32_t search_ticket[VDI_N_BUCKETS];
+  uint32_t pool_next;
   unsigned long long scratch_used;
   unsigned long long records_in;
   unsigned long long fallback_groups;
@@ -77,7 +79,10 @@ struct vdi_ctx {
   uint32_t row0 = 0, row1 = 0;
   uint64_t P = 0;  // lists in this rank's strip
   // merge scratch
-  DevBuf group_sum, group_base, wl, scratch, dcnt, stat_gamma, stat_m, bounds, srch;
+  DevBuf group_sum, group_base, wl, scratch, dcnt, stat_gamma, stat_m, bounds, srch, slots;
+  cudaStream_t side = nullptr;  // search kernels of chunk c overlap the pass-through kernel of chunk c+1
+  cudaEvent_t evc[VDI_MAX_CHUNKS + 1] = {};
+  int n_chunks = 1;
   // exchange receive buffers per source
   std::vector<DevBuf> rcount, rdepth, rrgba;
   // generator outputs per pe
@@ -97,6 +102,9 @@ struct vdi_ctx {
   cudaEvent_t gev[2] = {nullptr, nullptr};
   ~vdi_ctx() {
     if (cub_tmp) cudaFree(cub_tmp);
+    for (auto& e : evc)
+      if (e) cudaEventDestroy(e);
+    if (side) cudaStreamDestroy(side);
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
     for (auto& e : gev)
@@ -229,6 +237,16 @@ vdi_status vdi_composite_init(const vdi_config* cfg, vdi_ctx** out) {
   ctx->hrgba.resize(cfg->n_pes);
   for (auto& ev : ctx->ev) cudaEventCreate(&ev);
   for (auto& ev : ctx->gev) cudaEventCreate(&ev);
+  for (auto& ev : ctx->evc) cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+  {
+    int lo_prio = 0, hi_prio = 0;
+    cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio);
+    cudaError_t e2 = cudaStreamCreateWithPriority(&ctx->side, cudaStreamNonBlocking, lo_prio);
+    if (e2 != cudaSuccess) {
+      delete ctx;
+      return fail(VDI_ERR_CUDA, "cudaStreamCreate: %s", cudaGetErrorString(e2));
+    }
+  }
   if (cfg->n_ranks > 1) {
     ncclUniqueId id;
     memcpy(&id, cfg->nccl_unique_id, sizeof id);
@@ -485,8 +503,19 @@ vdi_status vdi_composite(vdi_ctx* ctx, const vdi_dense_view* local, uint32_t n_l
   const size_t ng = mp.n_groups;
   CUDA_TRY(ctx, ctx->group_sum.grow((size_t)scan_chunks(mp.P) * n * 4));
   CUDA_TRY(ctx, ctx->group_base.grow(ng * n * 4));
-  const size_t wl_bucket = std::max<size_t>(ctx->P, 1) * (3 + n);  // u32 per bucket
-  CUDA_TRY(ctx, ctx->wl.grow(wl_bucket * 4 * VDI_N_BUCKETS));
+  // The strip can be processed in C chunks of 32-list groups, the search
+  // kernels of chunk c (side stream) overlapping the pass-through kernel of
+  // chunk c+1.  Measured on C3 (profiles/README.md): C = 8 -> 973 VDIs/s,
+  // C = 2 -> 1495, C = 1 -> 1976 (co-resident search blocks starve the
+  // persistent pass-through grid), so one chunk is used; the mechanism stays
+  // for a future fused scheduler.
+  const uint32_t C = ctx->cfg.flags & 0x100u ? 2u : 1u;
+  ctx->n_chunks = (int)C;
+  std::vector<uint32_t> gb(C + 1);
+  for (uint32_t c = 0; c <= C; ++c) gb[c] = (uint32_t)((uint64_t)ng * c / C);
+  const size_t wl_words = std::max<size_t>(ctx->P, 1) * (3 + n) * VDI_N_BUCKETS + 64;
+  CUDA_TRY(ctx, ctx->wl.grow(wl_words * 4));
+  CUDA_TRY(ctx, ctx->slots.grow((2 * ng + 2 * C + 64) * 4));
   CUDA_TRY(ctx, ctx->scratch.grow(std::max<uint64_t>(4 * S_here, 1) * sizeof(Rec)));
   CUDA_TRY(ctx, ctx->dcnt.grow(sizeof(DevCounters)));
   const bool stats = cf.flags & VDI_FLAG_PIXEL_STATS;
@@ -494,25 +523,19 @@ vdi_status vdi_composite(vdi_ctx* ctx, const vdi_dense_view* local, uint32_t n_l
     CUDA_TRY(ctx, ctx->stat_gamma.grow(ctx->P * 4));
     CUDA_TRY(ctx, ctx->stat_m.grow(ctx->P * 2));
   }
-  // short-list search scratch: a list in bucket b has m > k_out samples, so
-  // at most S_here / (k_out + 1) lists (and at most P) land there
-  const uint64_t sl = std::min<uint64_t>(ctx->P, S_here / (k + 1) + 1);
-  const uint64_t sb = (sl + 31) / 32;  // batches
-  const size_t srch_bytes = sb * 32 * (32 + 40) * 24 + 2 * sb * 64 * 4 + 1024;
-  CUDA_TRY(ctx, ctx->srch.grow(srch_bytes));
+  // short-list search pool: a list in bucket 0/1 has m > k_out samples, so at
+  // most S_here / (k_out + 1) such lists exist; + one partial batch per chunk and bucket
+  const uint64_t pool_cap = (S_here / (k + 1) + 31) / 32 + 2 * C + 2;
+  const size_t slot_bytes = 40 * 32 * 16 + 40 * 32 * 8 + 64 * 4;
+  CUDA_TRY(ctx, ctx->srch.grow(pool_cap * slot_bytes + 256));
   {
     char* q = ctx->srch.as<char>();
-    mp.srch_rgba[0] = reinterpret_cast<float4*>(q);
-    q += sb * 32 * 32 * 16;
-    mp.srch_rgba[1] = reinterpret_cast<float4*>(q);
-    q += sb * 32 * 40 * 16;
-    mp.srch_depth[0] = reinterpret_cast<float2*>(q);
-    q += sb * 32 * 32 * 8;
-    mp.srch_depth[1] = reinterpret_cast<float2*>(q);
-    q += sb * 32 * 40 * 8;
-    mp.srch_gap[0] = reinterpret_cast<uint32_t*>(q);
-    q += sb * 64 * 4;
-    mp.srch_gap[1] = reinterpret_cast<uint32_t*>(q);
+    mp.pool_rgba = reinterpret_cast<float4*>(q);
+    q += pool_cap * 40 * 32 * 16;
+    mp.pool_depth = reinterpret_cast<float2*>(q);
+    q += pool_cap * 40 * 32 * 8;
+    mp.pool_gap = reinterpret_cast<uint32_t*>(q);
+    mp.pool_cap = (uint32_t)pool_cap;
   }
   DevCounters* dc = ctx->dcnt.as<DevCounters>();
   CUDA_TRY(ctx, cudaMemsetAsync(dc, 0, sizeof(DevCounters), st));
@@ -520,11 +543,8 @@ vdi_status vdi_composite(vdi_ctx* ctx, const vdi_dense_view* local, uint32_t n_l
   mp.out_count = so->count;
   mp.out_depth = reinterpret_cast<float2*>(so->depth);
   mp.out_rgba = reinterpret_cast<float4*>(so->rgba);
-  for (int b = 0; b < VDI_N_BUCKETS; ++b) mp.wl[b] = ctx->wl.as<uint32_t>() + wl_bucket * b;
-  mp.wl_count = dc->wl_count;
   mp.fallback_groups = &dc->fallback_groups;
-  mp.search_ticket = dc->search_ticket;
-  mp.wl_cap = (uint32_t)std::max<uint64_t>(ctx->P, 1);
+  mp.pool_next = &dc->pool_next;
   mp.scratch_used = &dc->scratch_used;
   mp.scratch_cap = 4 * S_here;
   mp.scratch = ctx->scratch.as<Rec>();
@@ -536,7 +556,33 @@ vdi_status vdi_composite(vdi_ctx* ctx, const vdi_dense_view* local, uint32_t n_l
   if (ctx->P) {
     CUDA_TRY(ctx, launch_scan(mp, ctx->group_sum.as<uint32_t>(), ctx->group_base.as<uint32_t>(), st, &launches));
     if (timing) CUDA_TRY(ctx, cudaEventRecord(ctx->ev[3], st));
-    CUDA_TRY(ctx, launch_merge(mp, st, &launches, timing ? ctx->ev + 4 : nullptr));
+    uint32_t* wlp = ctx->wl.as<uint32_t>();
+    uint32_t* slp = ctx->slots.as<uint32_t>();
+    for (uint32_t c = 0; c < C; ++c) {
+      MergeParams mc = mp;
+      mc.g_begin = gb[c];
+      mc.g_end = gb[c + 1];
+      const uint64_t Pc = std::min<uint64_t>((uint64_t)gb[c + 1] * 32, ctx->P) - (uint64_t)gb[c] * 32;
+      mc.wl_cap = (uint32_t)std::max<uint64_t>(Pc, 1);
+      for (int b = 0; b < VDI_N_BUCKETS; ++b) {
+        mc.wl[b] = wlp;
+        wlp += (size_t)mc.wl_cap * (3 + n);
+      }
+      for (int b = 0; b < 2; ++b) {
+        mc.batch_slot[b] = slp;
+        slp += (mc.wl_cap + 31) / 32 + 1;
+      }
+      mc.wl_count = dc->wl_count[c];
+      mc.search_ticket = dc->search_ticket[c];
+      CUDA_TRY(ctx, launch_fast(mc, st, &launches));
+      CUDA_TRY(ctx, cudaEventRecord(ctx->evc[c], st));
+      CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->side, ctx->evc[c], 0));
+      CUDA_TRY(ctx, launch_search_all(mc, ctx->side, &launches));
+    }
+    if (timing) CUDA_TRY(ctx, cudaEventRecord(ctx->ev[4], st));
+    CUDA_TRY(ctx, cudaEventRecord(ctx->evc[VDI_MAX_CHUNKS], ctx->side));
+    CUDA_TRY(ctx, cudaStreamWaitEvent(st, ctx->evc[VDI_MAX_CHUNKS], 0));
+    if (timing) CUDA_TRY(ctx, cudaEventRecord(ctx->ev[5], st));
   }
   if (timing) {
     CUDA_TRY(ctx, cudaEventRecord(ctx->ev[2], st));
@@ -670,13 +716,17 @@ vdi_status vdi_get_counters(vdi_ctx* ctx, vdi_counters* out) {
     CUDA_TRY(ctx, cudaMemcpyAsync(&h, ctx->dcnt.p, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
     CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
   }
-  if (h.err & 1) return fail(VDI_ERR_INTERNAL, "merge work list / scratch overflow");
+  if (h.err & 1) return fail(VDI_ERR_INTERNAL, "merge work list / scratch / search pool overflow");
   ctx->last.records_in = h.records_in;
   ctx->last.searched_lists = 0;
-  ctx->last.general_lists = h.wl_count[VDI_BUCKET_GENERAL];
-  for (int b = 0; b < VDI_N_BUCKETS; ++b) {
-    ctx->last.searched_lists += h.wl_count[b];
-    if (b < 4) ctx->last.bucket_lists[b] = h.wl_count[b];
+  ctx->last.general_lists = 0;
+  for (int b = 0; b < 4; ++b) ctx->last.bucket_lists[b] = 0;
+  for (int c = 0; c < ctx->n_chunks; ++c) {
+    ctx->last.general_lists += h.wl_count[c][VDI_BUCKET_GENERAL];
+    for (int b = 0; b < VDI_N_BUCKETS; ++b) {
+      ctx->last.searched_lists += h.wl_count[c][b];
+      if (b < 4) ctx->last.bucket_lists[b] += h.wl_count[c][b];
+    }
   }
   ctx->last.fallback_groups = h.fallback_groups;
   if (ctx->timing_pending) {

@@ -45,6 +45,7 @@ struct MergeParams {
   float gamma_max;
   uint32_t P;          // lists in the strip
   uint32_t n_groups;   // ceil(P / 32)
+  uint32_t g_begin, g_end;  // 32-list groups of this launch's chunk of the strip
   const uint32_t* group_base;  // [n_src][n_groups] exclusive scan of 32-list group sums
   uint8_t* out_count;          // [P]
   float2* out_depth;           // [P][k_out]
@@ -61,10 +62,15 @@ struct MergeParams {
   unsigned long long* records_in;
   unsigned long long* fallback_groups;  // groups written with plain stores
   uint32_t* search_ticket;              // [VDI_N_BUCKETS] per-bucket claim tickets of the search kernels
-  // short-list search scratch (buckets 0, 1: MS = 32, 40): [batch][MS][32] samples, [batch][2][32] gap bits
-  float4* srch_rgba[2];
-  float2* srch_depth[2];
-  uint32_t* srch_gap[2];
+  // short-list search scratch (buckets 0, 1), a pool of batch slots shared by
+  // all chunks: slot = [40][32] rgba + [40][32] depth + [2][32] gap words;
+  // batch_slot[b][i] = slot of batch i (32 entries) of bucket b of this chunk
+  float4* pool_rgba;
+  float2* pool_depth;
+  uint32_t* pool_gap;
+  uint32_t* pool_next;
+  uint32_t pool_cap;
+  uint32_t* batch_slot[2];
   int* err;            // bit 0: work list / scratch overflow
   int validate;
 };
@@ -73,8 +79,10 @@ struct MergeParams {
 uint32_t scan_chunks(uint32_t P);  // chunks of the receive-side scan
 cudaError_t launch_scan(const MergeParams& mp, uint32_t* chunk_sum, uint32_t* group_base, cudaStream_t st,
                         int* launches);
-// ev (optional, 2 entries): recorded after the fast kernel and after the search kernels
-cudaError_t launch_merge(const MergeParams& mp, cudaStream_t st, int* launches, cudaEvent_t* ev);
+// pass-through kernel over groups [mp.g_begin, mp.g_end) (stream st)
+cudaError_t launch_fast(const MergeParams& mp, cudaStream_t st, int* launches);
+// search + general kernels over the work lists in mp (stream st)
+cudaError_t launch_search_all(const MergeParams& mp, cudaStream_t st, int* launches);
 
 // Generator (generate.cu)
 struct GenParams {

@@ -470,15 +470,15 @@ __global__ void __launch_bounds__(kFastThreads) merge_fast_kernel(MergeParams mp
     for (int s = 0; s < NS; ++s) {
       nc[s] = 0;
       nb[s] = 0;
-      if (s < n && gg < mp.n_groups) {
+      if (s < n && gg < mp.g_end) {
         if (pp < mp.P) nc[s] = __ldg(mp.src[s].count + pp);
         nb[s] = __ldg(mp.group_base + (size_t)s * mp.n_groups + gg);
       }
     }
   };
-  prefetch(blockIdx.x * nwarps + warp);
+  prefetch(mp.g_begin + blockIdx.x * nwarps + warp);
 
-  for (uint32_t g = blockIdx.x * nwarps + warp; g < mp.n_groups; g += gstride) {
+  for (uint32_t g = mp.g_begin + blockIdx.x * nwarps + warp; g < mp.g_end; g += gstride) {
     const uint32_t p0 = g * 32, p = p0 + lane;
     const bool valid = p < mp.P;
     uint32_t cnt[NS], gidx[NS];
@@ -848,8 +848,17 @@ __global__ void __launch_bounds__(128) search_gather_kernel(MergeParams mp) {
         cnt[s] = __ldg(mp.src[s].count + p);
       }
     }
-    float4* orgba = mp.srch_rgba[bucket] + (size_t)(i >> 5) * MS * 32 + lane;
-    float2* odep = mp.srch_depth[bucket] + (size_t)(i >> 5) * MS * 32 + lane;
+    // one pool slot per batch of 32 entries (a warp here = one batch)
+    uint32_t slot = 0;
+    if (lane == 0) {
+      slot = atomicAdd(mp.pool_next, 1u);
+      if (slot < mp.pool_cap) mp.batch_slot[bucket][i >> 5] = slot;
+      else atomicOr(mp.err, 1);
+    }
+    slot = __shfl_sync(kFull, slot, 0);
+    if (slot >= mp.pool_cap) continue;
+    float4* orgba = mp.pool_rgba + (size_t)slot * 40 * 32 + lane;
+    float2* odep = mp.pool_depth + (size_t)slot * 40 * 32 + lane;
     uint32_t g0 = 0, g1 = 0;
     bool bad = false;
     if (valid) {
@@ -910,14 +919,16 @@ __global__ void __launch_bounds__(128) search_gather_kernel(MergeParams mp) {
         for (int s = 0; s < NS; ++s)
           if (s == b) hp[s] = ii;
       }
-      uint32_t* og = mp.srch_gap[bucket] + (size_t)(i >> 5) * 64 + lane;
+      uint32_t* og = mp.pool_gap + (size_t)slot * 64 + lane;
       og[0] = g0;
       og[32] = g1;
     }
     const int bk = (valid && bad) ? VDI_BUCKET_GENERAL : -1;
     if (__any_sync(kFull, bk >= 0)) push_entries<NS>(mp, bk, p, m, goff, lane);
-    if (valid && bad) mp.srch_gap[bucket][(size_t)(i >> 5) * 64 + lane] = 0xffffffffu;  // skip marker
-    if (valid && bad) mp.srch_gap[bucket][(size_t)(i >> 5) * 64 + 32 + lane] = 0xffffffffu;
+    if (valid && bad) {  // skip marker (bit 0 of a real gap word is never set)
+      mp.pool_gap[(size_t)slot * 64 + lane] = 0xffffffffu;
+      mp.pool_gap[(size_t)slot * 64 + 32 + lane] = 0xffffffffu;
+    }
   }
 }
 
@@ -933,11 +944,13 @@ __global__ void __launch_bounds__(32, 8) search_sweep_kernel(MergeParams mp, int
     const uint32_t* ent = wl + (size_t)(valid ? e : 0) * (3 + n);
     const uint32_t p = valid ? ent[0] : 0u;
     const int mi = valid ? (int)ent[2] : 0;
-    const uint32_t* gp = mp.srch_gap[bucket] + (size_t)batch * 64 + lane;
+    const uint32_t slot = mp.batch_slot[bucket][batch];
+    if (slot >= mp.pool_cap) continue;
+    const uint32_t* gp = mp.pool_gap + (size_t)slot * 64 + lane;
     const uint32_t gw0 = valid ? gp[0] : 0u, gw1 = valid ? gp[32] : 0u;
     const bool bad = valid && gw0 == 0xffffffffu && gw1 == 0xffffffffu;  // sent to the general path
-    const float4* col = mp.srch_rgba[bucket] + (size_t)batch * MS * 32 + lane;
-    const float2* dcol = mp.srch_depth[bucket] + (size_t)batch * MS * 32 + lane;
+    const float4* col = mp.pool_rgba + (size_t)slot * 40 * 32 + lane;
+    const float2* dcol = mp.pool_depth + (size_t)slot * 40 * 32 + lane;
     float4 S[MS];
 #pragma unroll
     for (int q = 0; q < MS; ++q) S[q] = (q < mi && !bad) ? col[q * 32] : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -1218,7 +1231,7 @@ static cudaError_t launch_sweep(const MergeParams& mp, int bucket, cudaStream_t 
 }
 
 template <int NS>
-static cudaError_t launch_all(const MergeParams& mp, cudaStream_t st, int* launches, cudaEvent_t* ev) {
+static cudaError_t launch_fast_ns(const MergeParams& mp, cudaStream_t st, int* launches) {
   const size_t smem = (size_t)(kFastThreads / 32) * fast_warp_bytes(mp.k_out);
   static int per_sm = 0;
   static size_t prepared = 0;
@@ -1227,14 +1240,19 @@ static cudaError_t launch_all(const MergeParams& mp, cudaStream_t st, int* launc
     if (e != cudaSuccess) return e;
     prepared = smem;
   }
-  const uint32_t want = (mp.n_groups + (kFastThreads / 32) - 1) / (kFastThreads / 32);
+  const uint32_t groups = mp.g_end - mp.g_begin;
+  if (!groups) return cudaSuccess;
+  const uint32_t want = (groups + (kFastThreads / 32) - 1) / (kFastThreads / 32);
   uint32_t grid = (uint32_t)sm_count() * per_sm;
-  if (grid > want) grid = want ? want : 1;
+  if (grid > want) grid = want;
   merge_fast_kernel<NS><<<grid, kFastThreads, smem, st>>>(mp);
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
   ++*launches;
-  if (ev) cudaEventRecord(ev[0], st);
+  return cudaGetLastError();
+}
+
+template <int NS>
+static cudaError_t launch_search_ns(const MergeParams& mp, cudaStream_t st, int* launches) {
+  cudaError_t e;
   search_gather_kernel<NS><<<sm_count() * 8, 128, 0, st>>>(mp);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   ++*launches;
@@ -1246,19 +1264,25 @@ static cudaError_t launch_all(const MergeParams& mp, cudaStream_t st, int* launc
   ++*launches;
   if ((e = launch_search<NS, 128>(mp, 3, st)) != cudaSuccess) return e;
   ++*launches;
-  if (ev) cudaEventRecord(ev[1], st);
   merge_general_kernel<<<sm_count() * 4, kSlowThreads, 0, st>>>(mp);
   ++*launches;
   return cudaGetLastError();
 }
 
-cudaError_t launch_merge(const MergeParams& mp, cudaStream_t st, int* launches, cudaEvent_t* ev) {
-  if (mp.n_src <= 1) return launch_all<1>(mp, st, launches, ev);
-  if (mp.n_src <= 2) return launch_all<2>(mp, st, launches, ev);
-  if (mp.n_src <= 4) return launch_all<4>(mp, st, launches, ev);
-  if (mp.n_src <= 8) return launch_all<8>(mp, st, launches, ev);
-  if (mp.n_src <= 16) return launch_all<16>(mp, st, launches, ev);
-  return launch_all<VDI_MAX_SRC>(mp, st, launches, ev);
+#define VDI_DISPATCH_NS(F, ...)                                  \
+  if (mp.n_src <= 1) return F<1>(__VA_ARGS__);                   \
+  if (mp.n_src <= 2) return F<2>(__VA_ARGS__);                   \
+  if (mp.n_src <= 4) return F<4>(__VA_ARGS__);                   \
+  if (mp.n_src <= 8) return F<8>(__VA_ARGS__);                   \
+  if (mp.n_src <= 16) return F<16>(__VA_ARGS__);                 \
+  return F<VDI_MAX_SRC>(__VA_ARGS__);
+
+cudaError_t launch_fast(const MergeParams& mp, cudaStream_t st, int* launches) {
+  VDI_DISPATCH_NS(launch_fast_ns, mp, st, launches)
+}
+
+cudaError_t launch_search_all(const MergeParams& mp, cudaStream_t st, int* launches) {
+  VDI_DISPATCH_NS(launch_search_ns, mp, st, launches)
 }
 
 }  // namespace vdi
