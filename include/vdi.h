@@ -41,6 +41,7 @@ typedef enum {
 #define VDI_FLAG_PIXEL_STATS 0x1u  /* keep per-pixel gamma* and m of the last composite (vdi_pixel_stats) */
 #define VDI_FLAG_VALIDATE 0x2u     /* check inputs: count <= k_in, tf < tb, 0 < alpha <= 1, sorted runs */
 #define VDI_FLAG_STAGE_TIMING 0x4u /* record CUDA-event times of the exchange / merge / gather stages */
+#define VDI_FLAG_FULL_GATHER 0x8u  /* gather the full representation as in PAPER.md:185 (default: dense gather + root inflate, identical image) */
 
 typedef struct vdi_ctx vdi_ctx; /* opaque */
 
@@ -131,7 +132,7 @@ vdi_status vdi_get_unique_id(uint8_t out[128]);
 /* Validates cfg (VDI_ERR_INVALID_ARG), binds the current CUDA device, and for
  * n_ranks > 1 creates the NCCL communicator (collective over all ranks). */
 vdi_status vdi_composite_init(const vdi_config* cfg, vdi_ctx** out);
-void vdi_composite_destroy(vdi_ctx* ctx); /* NULL-safe; frees ctx-owned device memory */
+void vdi_composite_destroy(vdi_ctx* ctx); /* NULL-safe; waits for the ctx's stream, frees ctx-owned memory; local (no collective) */
 
 /* ---- Phase 1 (SUPPORT): sub-VDI of PE pe_id --------------------------------
  * Two passes per ray: pass 1 finds gamma and the count it
@@ -172,8 +173,12 @@ vdi_status vdi_composite_host(vdi_ctx* ctx, const vdi_dense_view* local_pes, uin
 
 /* Gather of the composited strips onto rank 0 (PAPER.md:185 MPI_Gather; Q14):
  * image_out (rows [0, H), root only; ignored elsewhere) receives every rank's
- * strip in rank order.  For n_ranks == 1 it copies the strip if the buffers
- * differ. */
+ * strip in rank order.  Default: each rank sends its counts + packed records
+ * (dense) and the root re-inflates the full representation -- the image is
+ * identical to gathering the full representation (VDI_FLAG_FULL_GATHER).
+ * Synchronises the stream once when n_ranks > 1 (payload sizes).  For
+ * n_ranks == 1 it copies the strip if the buffers differ (none if strip_out
+ * aliases the image rows). */
 vdi_status vdi_gather(vdi_ctx* ctx, const vdi_full_view* strip, vdi_full_view* image_out);
 
 /* ---- introspection ---------------------------------------------------------- */
@@ -185,6 +190,7 @@ vdi_status vdi_pixel_stats(vdi_ctx* ctx, float* gamma, uint16_t* m);
 /* Counters of the last vdi_composite on this rank. */
 typedef struct {
   uint64_t records_in;      /* sum over local strip lists of m before subdivision (supersegments merged) */
+  uint64_t records_search;  /* the part of records_in that belongs to lists needing the gamma search / general path */
   uint64_t searched_lists;  /* lists that needed the gamma search or subdivision */
   uint64_t bytes_sent;      /* all-to-allv payload bytes sent to other ranks */
   uint64_t bytes_received;  /* all-to-allv payload bytes received */
@@ -192,6 +198,7 @@ typedef struct {
   float ms_exchange, ms_merge, ms_gather; /* VDI_FLAG_STAGE_TIMING, else 0 */
   uint64_t bucket_lists[4];  /* lists sent to the search buckets m <= 32, <= 40, <= 64, <= 128 */
   uint64_t general_lists;    /* lists sent to the general path (overlaps, alpha == 0, m > 128) */
+  uint64_t bytes_gather;     /* bytes that crossed into the root in the last vdi_gather (G > 1) */
   uint64_t fallback_groups;  /* 32-list groups written with plain stores (tail group / unaligned output) */
   float ms_scan, ms_fast, ms_search; /* VDI_FLAG_STAGE_TIMING: receive scan, pass-through kernel, search kernels */
 } vdi_counters;

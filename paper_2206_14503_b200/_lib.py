@@ -17,6 +17,7 @@ VDI_OK = 0
 VDI_FLAG_PIXEL_STATS = 0x1
 VDI_FLAG_VALIDATE = 0x2
 VDI_FLAG_STAGE_TIMING = 0x4
+VDI_FLAG_FULL_GATHER = 0x8
 
 
 class vdi_config(C.Structure):
@@ -55,10 +56,10 @@ class vdi_decomp_desc(C.Structure):
 
 
 class vdi_counters(C.Structure):
-    _fields_ = [("records_in", C.c_uint64), ("searched_lists", C.c_uint64), ("bytes_sent", C.c_uint64),
+    _fields_ = [("records_in", C.c_uint64), ("records_search", C.c_uint64), ("searched_lists", C.c_uint64), ("bytes_sent", C.c_uint64),
                 ("bytes_received", C.c_uint64), ("kernel_launches", C.c_uint32), ("ms_exchange", C.c_float),
                 ("ms_merge", C.c_float), ("ms_gather", C.c_float), ("bucket_lists", C.c_uint64 * 4),
-                ("general_lists", C.c_uint64), ("fallback_groups", C.c_uint64), ("ms_scan", C.c_float), ("ms_fast", C.c_float),
+                ("general_lists", C.c_uint64), ("bytes_gather", C.c_uint64), ("fallback_groups", C.c_uint64), ("ms_scan", C.c_float), ("ms_fast", C.c_float),
                 ("ms_search", C.c_float)]
 
 

@@ -66,6 +66,7 @@ struct DevCounters {
   unsigned long long scratch_used;
   unsigned long long records_in;
   unsigned long long fallback_groups;
+  unsigned long long records_search;
 };
 
 }  // namespace
@@ -80,6 +81,7 @@ struct vdi_ctx {
   uint64_t P = 0;  // lists in this rank's strip
   // merge scratch
   DevBuf group_sum, group_base, wl, scratch, dcnt, stat_gamma, stat_m, bounds, srch, slots;
+  DevBuf g_sum, g_base, g_tot, g_dense, g_rcount, g_rpay, g_misc;  // dense gather
   cudaStream_t side = nullptr;  // search kernels of chunk c overlap the pass-through kernel of chunk c+1
   cudaEvent_t evc[VDI_MAX_CHUNKS + 1] = {};
   int n_chunks = 1;
@@ -109,7 +111,10 @@ struct vdi_ctx {
       if (e) cudaEventDestroy(e);
     for (auto& e : gev)
       if (e) cudaEventDestroy(e);
-    if (comm) ncclCommDestroy(comm);
+    // local teardown: drain our stream, then abort (not finalize) the
+    // communicator so destroying contexts never waits on other ranks
+    if (stream || comm) cudaStreamSynchronize(stream);
+    if (comm) ncclCommAbort(comm);
   }
 };
 
@@ -551,6 +556,7 @@ vdi_status vdi_composite(vdi_ctx* ctx, const vdi_dense_view* local, uint32_t n_l
   mp.stat_gamma = stats ? ctx->stat_gamma.as<float>() : nullptr;
   mp.stat_m = stats ? ctx->stat_m.as<uint16_t>() : nullptr;
   mp.records_in = &dc->records_in;
+  mp.records_search = &dc->records_search;
   mp.err = &dc->err;
   mp.validate = (cf.flags & VDI_FLAG_VALIDATE) ? 1 : 0;
   if (ctx->P) {
@@ -625,6 +631,99 @@ vdi_status vdi_gather(vdi_ctx* ctx, const vdi_full_view* strip, vdi_full_view* i
   };
   if (G == 1) {
     CUDA_TRY(ctx, copy_strip(0, strip));
+  } else if (!(cf.flags & VDI_FLAG_FULL_GATHER)) {
+    // Dense gather: every rank compacts its composited lists
+    // (counts + packed records) and the root re-inflates the
+    // full representation with the pass-through kernel; the image
+    // is bit-identical to the full-representation gather.
+    int launches = 0;
+    const size_t Pg = ctx->P, ng = (Pg + 31) / 32;
+    CUDA_TRY(ctx, ctx->g_sum.grow(((size_t)scan_chunks((uint32_t)std::max<size_t>(Pg, (size_t)cf.width * cf.height)) + 8) * 4));
+    CUDA_TRY(ctx, ctx->g_base.grow(((size_t)cf.width * cf.height / 32 + 8) * 4));
+    CUDA_TRY(ctx, ctx->g_tot.grow((G + 2) * 8));
+    unsigned long long* dtot = ctx->g_tot.as<unsigned long long>();
+    MergeParams ms{};
+    ms.n_src = 1;
+    ms.P = (uint32_t)Pg;
+    ms.n_groups = (uint32_t)ng;
+    ms.src[0].count = strip->count;
+    CUDA_TRY(ctx, launch_scan(ms, ctx->g_sum.as<uint32_t>(), ctx->g_base.as<uint32_t>(), st, &launches));
+    CUDA_TRY(ctx, launch_total(ms, ctx->g_sum.as<uint32_t>(), dtot + G, st, &launches));
+    NCCL_TRY(ctx, ncclAllGather(dtot + G, dtot, 1, ncclUint64, ctx->comm, st));
+    std::vector<unsigned long long> tot(G);
+    CUDA_TRY(ctx, cudaMemcpyAsync(tot.data(), dtot, G * 8, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(ctx, cudaStreamSynchronize(st));
+    if (!root) {
+      const uint64_t T = tot[me];
+      CUDA_TRY(ctx, ctx->g_dense.grow(std::max<uint64_t>(T, 1) * 24));
+      float4* dc4 = ctx->g_dense.as<float4>();
+      float2* dd2 = reinterpret_cast<float2*>(dc4 + std::max<uint64_t>(T, 1));
+      CUDA_TRY(ctx, launch_compact(strip->count, reinterpret_cast<const float2*>(strip->depth),
+                                   reinterpret_cast<const float4*>(strip->rgba), (uint32_t)Pg, (int)k,
+                                   ctx->g_base.as<uint32_t>(), dd2, dc4, st, &launches));
+      NCCL_TRY(ctx, ncclGroupStart());
+      NCCL_TRY(ctx, ncclSend(strip->count, Pg, ncclUint8, 0, ctx->comm, st));
+      if (T) {
+        NCCL_TRY(ctx, ncclSend(dd2, T * 2, ncclFloat32, 0, ctx->comm, st));
+        NCCL_TRY(ctx, ncclSend(dc4, T * 4, ncclFloat32, 0, ctx->comm, st));
+      }
+      NCCL_TRY(ctx, ncclGroupEnd());
+    } else {
+      const uint32_t r1 = strip_row(cf.height, G, 1);
+      const size_t Prem = (size_t)(cf.height - r1) * W;
+      uint64_t Trem = 0;
+      for (uint32_t g = 1; g < G; ++g) Trem += tot[g];
+      CUDA_TRY(ctx, ctx->g_rcount.grow(Prem + 64));
+      CUDA_TRY(ctx, ctx->g_rpay.grow(std::max<uint64_t>(Trem, 1) * 24 + 64));
+      float4* rc4 = ctx->g_rpay.as<float4>();
+      float2* rd2 = reinterpret_cast<float2*>(rc4 + std::max<uint64_t>(Trem, 1));
+      uint8_t* rcnt = ctx->g_rcount.as<uint8_t>();
+      NCCL_TRY(ctx, ncclGroupStart());
+      uint64_t off = 0;
+      for (uint32_t g = 1; g < G; ++g) {
+        const uint32_t a = strip_row(cf.height, G, g), b = strip_row(cf.height, G, g + 1);
+        NCCL_TRY(ctx, ncclRecv(rcnt + (size_t)(a - r1) * W, (size_t)(b - a) * W, ncclUint8, (int)g, ctx->comm, st));
+        if (tot[g]) {
+          NCCL_TRY(ctx, ncclRecv(rd2 + off, tot[g] * 2, ncclFloat32, (int)g, ctx->comm, st));
+          NCCL_TRY(ctx, ncclRecv(rc4 + off, tot[g] * 4, ncclFloat32, (int)g, ctx->comm, st));
+        }
+        off += tot[g];
+      }
+      NCCL_TRY(ctx, ncclGroupEnd());
+      // inflate rows [r1, H) of the image: one pass-through launch over the
+      // received (already depth-ordered, m <= k_out) lists
+      MergeParams mi{};
+      mi.n_src = 1;
+      mi.k_out = (int)k;
+      mi.max_iters = (int)cf.max_iters;
+      mi.gamma_max = cf.gamma_max;
+      mi.P = (uint32_t)Prem;
+      mi.n_groups = (uint32_t)((Prem + 31) / 32);
+      mi.g_begin = 0;
+      mi.g_end = mi.n_groups;
+      mi.src[0] = SrcDesc{rcnt, rd2, rc4};
+      CUDA_TRY(ctx, ctx->g_misc.grow(sizeof(DevCounters) + 256));
+      DevCounters* gc = ctx->g_misc.as<DevCounters>();
+      CUDA_TRY(ctx, cudaMemsetAsync(gc, 0, sizeof(DevCounters), st));
+      CUDA_TRY(ctx, launch_scan(mi, ctx->g_sum.as<uint32_t>(), ctx->g_base.as<uint32_t>(), st, &launches));
+      mi.group_base = ctx->g_base.as<uint32_t>();
+      mi.out_count = image->count + (size_t)r1 * W;
+      mi.out_depth = reinterpret_cast<float2*>(image->depth) + (size_t)r1 * W * k;
+      mi.out_rgba = reinterpret_cast<float4*>(image->rgba) + (size_t)r1 * W * k;
+      for (int b = 0; b < VDI_N_BUCKETS; ++b) mi.wl[b] = reinterpret_cast<uint32_t*>(gc);  // never written: wl_cap = 0
+      mi.wl_count = gc->wl_count[0];
+      mi.wl_cap = 0;
+      mi.scratch_used = &gc->scratch_used;
+      mi.records_in = &gc->records_in;
+      mi.fallback_groups = &gc->fallback_groups;
+      mi.err = &gc->err;
+      CUDA_TRY(ctx, launch_fast(mi, st, &launches));
+      CUDA_TRY(ctx, copy_strip(0, strip));
+    }
+    ctx->last.bytes_gather = 0;
+    for (uint32_t g = 1; g < G; ++g)
+      ctx->last.bytes_gather += (uint64_t)(strip_row(cf.height, G, g + 1) - strip_row(cf.height, G, g)) * W + 24 * tot[g];
+    ctx->last.kernel_launches += (uint32_t)launches;
   } else {
     // MPI_Gather of the full-representation strips as grouped send/recv
     NCCL_TRY(ctx, ncclGroupStart());
@@ -644,6 +743,7 @@ vdi_status vdi_gather(vdi_ctx* ctx, const vdi_full_view* strip, vdi_full_view* i
     }
     NCCL_TRY(ctx, ncclGroupEnd());
     if (root) CUDA_TRY(ctx, copy_strip(0, strip));
+    ctx->last.bytes_gather = (uint64_t)(cf.height - strip_row(cf.height, G, 1)) * W * (1 + 24ull * k);
   }
   if (timing) {
     CUDA_TRY(ctx, cudaEventRecord(ctx->gev[1], st));
@@ -718,6 +818,7 @@ vdi_status vdi_get_counters(vdi_ctx* ctx, vdi_counters* out) {
   }
   if (h.err & 1) return fail(VDI_ERR_INTERNAL, "merge work list / scratch / search pool overflow");
   ctx->last.records_in = h.records_in;
+  ctx->last.records_search = h.records_search;
   ctx->last.searched_lists = 0;
   ctx->last.general_lists = 0;
   for (int b = 0; b < 4; ++b) ctx->last.bucket_lists[b] = 0;

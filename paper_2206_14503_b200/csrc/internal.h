@@ -60,6 +60,7 @@ struct MergeParams {
   float* stat_gamma;   // optional [P]
   uint16_t* stat_m;    // optional [P]
   unsigned long long* records_in;
+  unsigned long long* records_search;   // records of lists sent to the search / general paths
   unsigned long long* fallback_groups;  // groups written with plain stores
   uint32_t* search_ticket;              // [VDI_N_BUCKETS] per-bucket claim tickets of the search kernels
   // short-list search scratch (buckets 0, 1), a pool of batch slots shared by
@@ -81,6 +82,11 @@ cudaError_t launch_scan(const MergeParams& mp, uint32_t* chunk_sum, uint32_t* gr
                         int* launches);
 // pass-through kernel over groups [mp.g_begin, mp.g_end) (stream st)
 cudaError_t launch_fast(const MergeParams& mp, cudaStream_t st, int* launches);
+// dense gather: total of the scanned counts (chunk sums) and compaction of a full-representation strip
+cudaError_t launch_total(const MergeParams& mp, const uint32_t* chunk_sum, unsigned long long* out, cudaStream_t st,
+                         int* launches);
+cudaError_t launch_compact(const uint8_t* count, const float2* depth, const float4* rgba, uint32_t P, int k,
+                           const uint32_t* group_base, float2* od, float4* oc, cudaStream_t st, int* launches);
 // search + general kernels over the work lists in mp (stream st)
 cudaError_t launch_search_all(const MergeParams& mp, cudaStream_t st, int* launches);
 

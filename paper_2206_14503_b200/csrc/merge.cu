@@ -451,7 +451,7 @@ __global__ void __launch_bounds__(kFastThreads) merge_fast_kernel(MergeParams mp
   uint16_t* my_perm = perm + lane * k;
   const bool bulk_ok =
       ((reinterpret_cast<uintptr_t>(mp.out_depth) | reinterpret_cast<uintptr_t>(mp.out_rgba)) & 15u) == 0;
-  unsigned long long rec_acc = 0, plain_acc = 0;
+  unsigned long long rec_acc = 0, plain_acc = 0, srch_acc = 0;
 
   // the output image starts all-zero (full-representation zeros)
   for (int i = lane; i < 32 * k; i += 32) {
@@ -582,6 +582,7 @@ __global__ void __launch_bounds__(kFastThreads) merge_fast_kernel(MergeParams mp
     }
     if (cand && !pass) bk = VDI_BUCKET_GENERAL;  // transparent or overlapping records
     if (__any_sync(kFull, bk >= 0)) push_entries<NS>(mp, bk, p, m, gidx, lane);
+    if (bk >= 0) srch_acc += m;
     if (valid) {
       mp.out_count[p] = pass ? (uint8_t)m : (uint8_t)0;
       if (mp.stat_m) mp.stat_m[p] = (uint16_t)m;
@@ -593,10 +594,12 @@ __global__ void __launch_bounds__(kFastThreads) merge_fast_kernel(MergeParams mp
   for (int d = 16; d > 0; d >>= 1) {
     rec_acc += __shfl_down_sync(kFull, rec_acc, d);
     plain_acc += __shfl_down_sync(kFull, plain_acc, d);
+    srch_acc += __shfl_down_sync(kFull, srch_acc, d);
   }
   if (lane == 0) {
     if (rec_acc) atomicAdd(mp.records_in, rec_acc);
     if (plain_acc) atomicAdd(mp.fallback_groups, plain_acc);
+    if (srch_acc && mp.records_search) atomicAdd(mp.records_search, srch_acc);
   }
 }
 
@@ -1185,6 +1188,64 @@ cudaError_t launch_scan(const MergeParams& mp, uint32_t* chunk_sum, uint32_t* gr
   chunk_sums_kernel<<<dim3(nc, mp.n_src), 256, 0, st>>>(mp, chunk_sum, nc);
   ++*launches;
   group_base_kernel<<<dim3(nc, mp.n_src), 128, 0, st>>>(mp, chunk_sum, nc, group_base);
+  ++*launches;
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// Dense gather support: compaction of a composited
+// full-representation strip into the dense layout before
+// it crosses NVLink; the root re-inflates with the pass-through kernel.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) sum_u32_kernel(const uint32_t* __restrict__ a, uint32_t n,
+                                                      unsigned long long* __restrict__ out) {
+  __shared__ unsigned long long red[8];
+  unsigned long long acc = 0;
+  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) acc += a[i];
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) acc += __shfl_down_sync(kFull, acc, d);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long t = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+    *out = t;
+  }
+}
+
+__global__ void __launch_bounds__(128) compact_kernel(const uint8_t* __restrict__ count, const float2* __restrict__ depth,
+                                                      const float4* __restrict__ rgba, uint32_t P, int k,
+                                                      const uint32_t* __restrict__ group_base, float2* __restrict__ od,
+                                                      float4* __restrict__ oc) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t ng = (P + 31) / 32;
+  for (uint32_t g = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); g < ng; g += gridDim.x * (blockDim.x >> 5)) {
+    const uint32_t p = g * 32 + lane;
+    const uint32_t c = p < P ? count[p] : 0u;
+    const uint32_t off = group_base[g] + warp_incl_scan(c, lane) - c;
+    const float2* sd = depth + (size_t)p * k;
+    const float4* sc = rgba + (size_t)p * k;
+#pragma unroll 4
+    for (uint32_t j = 0; j < c; ++j) {
+      od[off + j] = __ldg(sd + j);
+      oc[off + j] = __ldg(sc + j);
+    }
+  }
+}
+
+cudaError_t launch_total(const MergeParams& mp, const uint32_t* chunk_sum, unsigned long long* out, cudaStream_t st,
+                         int* launches) {
+  sum_u32_kernel<<<1, 256, 0, st>>>(chunk_sum, scan_chunks(mp.P) * mp.n_src, out);
+  ++*launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_compact(const uint8_t* count, const float2* depth, const float4* rgba, uint32_t P, int k,
+                           const uint32_t* group_base, float2* od, float4* oc, cudaStream_t st, int* launches) {
+  const uint32_t ng = (P + 31) / 32;
+  if (!ng) return cudaSuccess;
+  compact_kernel<<<std::min<uint32_t>((ng + 3) / 4, (uint32_t)sm_count() * 16), 128, 0, st>>>(count, depth, rgba, P, k,
+                                                                                             group_base, od, oc);
   ++*launches;
   return cudaGetLastError();
 }

@@ -41,6 +41,8 @@ def main():
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     obj = [vdi.get_unique_id() if rank == 0 else None]
     dist.broadcast_object_list(obj, src=0)
+    obj2 = [vdi.get_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj2, src=0)
 
     if args.config == "synthetic":
         W, H, n, k_in, k_out = args.W, args.H, args.n, args.k, args.k
@@ -64,6 +66,13 @@ def main():
     comp.composite(local_pes, strip)
     comp.gather(strip, image)
     cnt = comp.counters()
+    # the paper's full-representation gather must give the same image
+    comp2 = vdi.Compositor(W, H, k_in, k_out, n, n_ranks=world, rank=rank, unique_id=obj2[0],
+                           flags=vdi._lib.VDI_FLAG_FULL_GATHER)
+    image2 = vdi.FullVDI.empty(W, 0, H, k_out) if rank == 0 else None
+    strip2 = comp2.empty_strip()
+    comp2.composite(local_pes, strip2)
+    comp2.gather(strip2, image2)
     torch.cuda.synchronize()
     ok = True
     res = {"world": world, "config": args.config, "bytes_sent_rank": cnt["bytes_sent"],
@@ -88,8 +97,12 @@ def main():
         torch.cuda.synchronize()
         same = all(torch.equal(a, b) for a, b in ((image.count, ref.count), (image.depth, ref.depth),
                                                      (image.rgba, ref.rgba)))
+        same2 = all(torch.equal(a, b) for a, b in ((image2.count, ref.count), (image2.depth, ref.depth),
+                                                      (image2.rgba, ref.rgba)))
         res["bit_identical_to_1gpu"] = bool(same)
-        ok &= same
+        res["full_gather_identical"] = bool(same2)
+        res["gather_bytes_dense"] = cnt["bytes_gather"]
+        ok &= same and same2
         if pes_np is not None:
             import oracle
             rng = np.random.default_rng(3)
