@@ -217,7 +217,9 @@ def run_ours(args, world, rank, local):
         obj = [vdi.get_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         uid = obj[0]
-    flags = L.VDI_FLAG_STAGE_TIMING | (L.VDI_FLAG_FULL_GATHER if args.full_gather else 0)
+    flags = (L.VDI_FLAG_STAGE_TIMING | (L.VDI_FLAG_FULL_GATHER if args.full_gather else 0)
+             | (L.VDI_FLAG_NCCL_EXCHANGE if args.nccl_exchange else 0)
+             | (L.VDI_FLAG_PEER_READS if args.peer_reads else 0))
     comp = vdi.Compositor(W, H, cfg.k_in, k, n, n_ranks=G, rank=rank, flags=flags, unique_id=uid, stream=stream)
 
     # ---- inputs (untimed): synthetic volume -> per-PE dense sub-VDIs in HBM
@@ -374,6 +376,9 @@ def run_ours(args, world, rank, local):
             "search_buckets": stage[-1]["bucket_lists"], "fast_fallback_groups": stage[-1]["fallback_groups"],
             "exchange_bytes_sent_rank0": bytes_sent, "exchange_bytes_received_rank0": bytes_recv,
             "gather": "full representation (PAPER.md:185)" if args.full_gather else "dense + root inflate (f1)",
+            "exchange": ("NCCL send/recv" if args.nccl_exchange else
+                         "peer reads: merge kernels load peers' sub-VDIs over NVLink (CUDA IPC)" if args.peer_reads else
+                         "peer copies: copy engines pull peers' strip slices over NVLink (CUDA IPC)"),
             "gather_bytes_into_root": stage[-1]["bytes_gather"],
             "gpu_launches": launches,
             "clocks": clk.summary(),
@@ -398,6 +403,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--full-gather", action="store_true", help="gather the full representation (PAPER.md:185)")
+    ap.add_argument("--nccl-exchange", action="store_true", help="NCCL send/recv exchange instead of peer copies")
+    ap.add_argument("--peer-reads", action="store_true", help="merge kernels read peers' slices over NVLink")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     world, rank, local = dist_setup()

@@ -41,6 +41,8 @@ typedef enum {
 #define VDI_FLAG_PIXEL_STATS 0x1u  /* keep per-pixel gamma* and m of the last composite (vdi_pixel_stats) */
 #define VDI_FLAG_VALIDATE 0x2u     /* check inputs: count <= k_in, tf < tb, 0 < alpha <= 1, sorted runs */
 #define VDI_FLAG_STAGE_TIMING 0x4u /* record CUDA-event times of the exchange / merge / gather stages */
+#define VDI_FLAG_PEER_READS 0x20u    /* peer exchange without copies: the merge kernels load peers' slices over NVLink */
+#define VDI_FLAG_NCCL_EXCHANGE 0x10u /* exchange through NCCL send/recv into receive buffers (default: the merge reads peers' sub-VDIs over NVLink via CUDA IPC) */
 #define VDI_FLAG_FULL_GATHER 0x8u  /* gather the full representation as in PAPER.md:185 (default: dense gather + root inflate, identical image) */
 
 typedef struct vdi_ctx vdi_ctx; /* opaque */
@@ -160,7 +162,12 @@ vdi_status vdi_generate_subvdi(vdi_ctx* ctx, const vdi_volume_desc* vol, const v
  * local_pes: the n_local sub-VDIs homed on this rank, any order, each with a
  * distinct pe_id.  strip_out: caller-owned, rows of this rank's strip
  * (VDI_ERR_CAPACITY if the row range does not match).  Synchronises the
- * stream once when n_ranks > 1 (sizes of the all-to-allv). */
+ * stream once when n_ranks > 1 (sizes of the all-to-allv).  Exchange: by
+ * default the remote PEs' strip slices are pulled over NVLink by the copy
+ * engines from CUDA IPC mappings of the peers' buffers (input arrays must
+ * then be cudaMalloc memory, e.g. torch tensors); VDI_FLAG_PEER_READS lets
+ * the merge kernels read peer memory directly (no copies);
+ * VDI_FLAG_NCCL_EXCHANGE uses NCCL send/recv. */
 vdi_status vdi_composite(vdi_ctx* ctx, const vdi_dense_view* local_pes, uint32_t n_local,
                          vdi_full_view* strip_out);
 

@@ -18,6 +18,8 @@ VDI_FLAG_PIXEL_STATS = 0x1
 VDI_FLAG_VALIDATE = 0x2
 VDI_FLAG_STAGE_TIMING = 0x4
 VDI_FLAG_FULL_GATHER = 0x8
+VDI_FLAG_NCCL_EXCHANGE = 0x10
+VDI_FLAG_PEER_READS = 0x20
 
 
 class vdi_config(C.Structure):

@@ -1,8 +1,12 @@
 // api.cu — libvdi C ABI (include/vdi.h): context, validation, the Phase-2
 // orchestration (strip partition, size exchange, all-to-allv over NCCL,
 // receive-side scan, merge) and the gather to the root.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <nccl.h>
+
+#include <map>
 
 #include <algorithm>
 #include <cstdarg>
@@ -82,6 +86,11 @@ struct vdi_ctx {
   // merge scratch
   DevBuf group_sum, group_base, wl, scratch, dcnt, stat_gamma, stat_m, bounds, srch, slots;
   DevBuf g_sum, g_base, g_tot, g_dense, g_rcount, g_rpay, g_misc;  // dense gather
+  std::map<std::string, void*> ipc_cache;  // IPC handle bytes -> mapped base of a peer allocation
+  static constexpr int kXStreams = 4;      // copy-engine streams of the peer exchange
+  cudaStream_t xs[4] = {};
+  cudaEvent_t evx[5] = {};
+  bool peer_reads = false;
   cudaStream_t side = nullptr;  // search kernels of chunk c overlap the pass-through kernel of chunk c+1
   cudaEvent_t evc[VDI_MAX_CHUNKS + 1] = {};
   int n_chunks = 1;
@@ -107,6 +116,10 @@ struct vdi_ctx {
     for (auto& e : evc)
       if (e) cudaEventDestroy(e);
     if (side) cudaStreamDestroy(side);
+    for (auto& x : xs)
+      if (x) cudaStreamDestroy(x);
+    for (auto& e : evx)
+      if (e) cudaEventDestroy(e);
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
     for (auto& e : gev)
@@ -114,6 +127,7 @@ struct vdi_ctx {
     // local teardown: drain our stream, then abort (not finalize) the
     // communicator so destroying contexts never waits on other ranks
     if (stream || comm) cudaStreamSynchronize(stream);
+    for (auto& kv : ipc_cache) cudaIpcCloseMemHandle(kv.second);
     if (comm) ncclCommAbort(comm);
   }
 };
@@ -147,6 +161,56 @@ __global__ void gather_bounds_kernel(const uint32_t* const* offs, const uint32_t
     const int l = i / (G + 1), g = i % (G + 1);
     bnd[(size_t)pes[l] * (G + 1) + g] = offs[l][(size_t)rows[g] * W];
   }
+}
+
+// ---- CUDA IPC references to (sub-ranges of) cudaMalloc allocations ---------
+struct IpcRef {
+  cudaIpcMemHandle_t h;  // handle of the allocation's base
+  uint64_t off;          // byte offset of the pointer inside the allocation
+};
+static_assert(sizeof(IpcRef) == 72, "IpcRef layout");
+
+PFN_cuMemGetAddressRange_v3020 get_range_fn() {
+  static PFN_cuMemGetAddressRange_v3020 fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", reinterpret_cast<void**>(&fn), cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      fn = nullptr;
+  }
+  return fn;
+}
+
+bool ipc_export(const void* p, IpcRef* r) {
+  PFN_cuMemGetAddressRange_v3020 fn = get_range_fn();
+  if (!fn) return false;
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (fn(&base, &size, reinterpret_cast<CUdeviceptr>(p)) != CUDA_SUCCESS) return false;
+  if (cudaIpcGetMemHandle(&r->h, reinterpret_cast<void*>(base)) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  r->off = reinterpret_cast<uint64_t>(p) - base;
+  return true;
+}
+
+cudaError_t ipc_import(vdi_ctx* ctx, const IpcRef& r, void** out) {
+  const std::string key(reinterpret_cast<const char*>(&r.h), sizeof r.h);
+  auto it = ctx->ipc_cache.find(key);
+  void* base = nullptr;
+  if (it == ctx->ipc_cache.end()) {
+    cudaError_t e = cudaIpcOpenMemHandle(&base, r.h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) return e;
+    ctx->ipc_cache.emplace(key, base);
+  } else {
+    base = it->second;
+  }
+  *out = static_cast<char*>(base) + r.off;
+  return cudaSuccess;
 }
 
 vdi_status check_ctx(vdi_ctx* ctx) {
@@ -243,6 +307,8 @@ vdi_status vdi_composite_init(const vdi_config* cfg, vdi_ctx** out) {
   for (auto& ev : ctx->ev) cudaEventCreate(&ev);
   for (auto& ev : ctx->gev) cudaEventCreate(&ev);
   for (auto& ev : ctx->evc) cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+  for (auto& ev : ctx->evx) cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+  for (auto& x : ctx->xs) cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking);
   {
     int lo_prio = 0, hi_prio = 0;
     cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio);
@@ -429,7 +495,11 @@ vdi_status vdi_composite(vdi_ctx* ctx, const vdi_dense_view* local, uint32_t n_l
     for (uint32_t g = 0; g <= G; ++g) rows[g] = strip_row(cf.height, G, g);
     const size_t nb = (size_t)n * (G + 1);
     const size_t hdr = 64 * 8 + 64 * 4 + 64 * 4;  // ptrs, pes, rows
-    CUDA_TRY(ctx, ctx->bounds.grow(nb * 8 + hdr));
+    // exchange blob: bnd (u64) | IPC references of every PE's count/depth/rgba
+    const bool peer = !(cf.flags & VDI_FLAG_NCCL_EXCHANGE);
+    const size_t refs_bytes = peer ? (size_t)n * 3 * sizeof(IpcRef) : 0;
+    const size_t blob = nb * 8 + refs_bytes;
+    CUDA_TRY(ctx, ctx->bounds.grow(blob + hdr));
     std::vector<uint8_t> h(hdr, 0);
     const uint32_t** hp = reinterpret_cast<const uint32_t**>(h.data());
     uint32_t* hpes = reinterpret_cast<uint32_t*>(h.data() + 64 * 8);
@@ -439,67 +509,139 @@ vdi_status vdi_composite(vdi_ctx* ctx, const vdi_dense_view* local, uint32_t n_l
       hpes[l] = local[l].pe_id;
     }
     for (uint32_t g = 0; g <= G; ++g) hrows[g] = rows[g];
-    uint8_t* dh = ctx->bounds.as<uint8_t>() + nb * 8;
+    uint8_t* dh = ctx->bounds.as<uint8_t>() + blob;
     unsigned long long* dbnd = ctx->bounds.as<unsigned long long>();
+    std::vector<IpcRef> myrefs;
+    if (peer) {  // this rank's PEs, exported for the peers (zeros elsewhere: the sum is a gather)
+      myrefs.assign((size_t)n * 3, IpcRef{});
+      for (uint32_t l = 0; l < n_local; ++l) {
+        const vdi_dense_view& v = local[l];
+        const void* ptrs[3] = {v.count, v.depth, v.rgba};
+        for (int a2 = 0; a2 < 3; ++a2) {
+          if (!ptrs[a2]) continue;
+          if (!ipc_export(ptrs[a2], &myrefs[(size_t)v.pe_id * 3 + a2]))
+            return fail(VDI_ERR_INVALID_ARG, "PE %u: buffer is not IPC-exportable device memory (use "
+                        "VDI_FLAG_NCCL_EXCHANGE)", v.pe_id);
+        }
+      }
+    }
     CUDA_TRY(ctx, cudaMemcpyAsync(dh, h.data(), hdr, cudaMemcpyHostToDevice, st));
     CUDA_TRY(ctx, cudaMemsetAsync(dbnd, 0, nb * 8, st));
+    if (peer)
+      CUDA_TRY(ctx, cudaMemcpyAsync(reinterpret_cast<uint8_t*>(dbnd) + nb * 8, myrefs.data(), refs_bytes,
+                                    cudaMemcpyHostToDevice, st));
     gather_bounds_kernel<<<1, 256, 0, st>>>(reinterpret_cast<const uint32_t* const*>(dh),
                                             reinterpret_cast<const uint32_t*>(dh + 64 * 8), (int)n_local,
                                             reinterpret_cast<const uint32_t*>(dh + 64 * 8 + 64 * 4), (int)G, W,
                                             (int)n, dbnd);
     ++launches;
     CUDA_TRY(ctx, cudaGetLastError());
-    // size exchange (every rank contributes the rows of its PEs; sum = gather)
-    NCCL_TRY(ctx, ncclAllReduce(dbnd, dbnd, nb, ncclUint64, ncclSum, ctx->comm, st));
+    // size (+ IPC reference) exchange: every rank contributes its PEs' rows and
+    // zeros elsewhere, so a byte-wise sum is a gather.  It is also the start
+    // barrier of the peer reads: every rank's inputs are complete in its
+    // stream order before it joins.
+    NCCL_TRY(ctx, ncclAllReduce(dbnd, dbnd, blob, ncclUint8, ncclSum, ctx->comm, st));
     std::vector<unsigned long long> bnd(nb);
+    std::vector<IpcRef> refs(peer ? (size_t)n * 3 : 0);
     CUDA_TRY(ctx, cudaMemcpyAsync(bnd.data(), dbnd, nb * 8, cudaMemcpyDeviceToHost, st));
+    if (peer)
+      CUDA_TRY(ctx, cudaMemcpyAsync(refs.data(), reinterpret_cast<uint8_t*>(dbnd) + nb * 8, refs_bytes,
+                                    cudaMemcpyDeviceToHost, st));
     CUDA_TRY(ctx, cudaStreamSynchronize(st));
     auto T = [&](uint32_t s, uint32_t g) { return bnd[(size_t)s * (G + 1) + g + 1] - bnd[(size_t)s * (G + 1) + g]; };
-    for (uint32_t s = 0; s < n; ++s) {
-      if (slot[s] >= 0) continue;
-      CUDA_TRY(ctx, ctx->rcount[s].grow(ctx->P));
-      CUDA_TRY(ctx, ctx->rdepth[s].grow(std::max<uint64_t>(T(s, me), 1) * 8));
-      CUDA_TRY(ctx, ctx->rrgba[s].grow(std::max<uint64_t>(T(s, me), 1) * 16));
-    }
-    // all-to-allv of count slices and dense payload slices
-    NCCL_TRY(ctx, ncclGroupStart());
-    for (uint32_t g = 0; g < G; ++g) {
-      if (g == me) continue;
-      const uint64_t Pg = (uint64_t)(rows[g + 1] - rows[g]) * W;
-      for (uint32_t s = 0; s < n; ++s) {  // our PEs -> g
-        if (slot[s] < 0) continue;
-        const vdi_dense_view& v = local[slot[s]];
-        const uint64_t b = bnd[(size_t)s * (G + 1) + g], t = T(s, g);
-        NCCL_TRY(ctx, ncclSend(v.count + (size_t)rows[g] * W, Pg, ncclUint8, (int)g, ctx->comm, st));
-        if (t) {
-          NCCL_TRY(ctx, ncclSend(v.depth + b * 2, t * 2, ncclFloat32, (int)g, ctx->comm, st));
-          NCCL_TRY(ctx, ncclSend(v.rgba + b * 4, t * 4, ncclFloat32, (int)g, ctx->comm, st));
-        }
-        sent += Pg + 24 * t;
-      }
-      for (uint32_t s = 0; s < n; ++s) {  // g's PEs -> us
-        if (vdi_pe_home(n, G, s) != g) continue;
-        const uint64_t t = T(s, me);
-        NCCL_TRY(ctx, ncclRecv(ctx->rcount[s].p, ctx->P, ncclUint8, (int)g, ctx->comm, st));
-        if (t) {
-          NCCL_TRY(ctx, ncclRecv(ctx->rdepth[s].p, t * 2, ncclFloat32, (int)g, ctx->comm, st));
-          NCCL_TRY(ctx, ncclRecv(ctx->rrgba[s].p, t * 4, ncclFloat32, (int)g, ctx->comm, st));
+    if (peer) {
+      // Exchange over NVLink through CUDA IPC mappings of the peers' sub-VDIs:
+      // default, the strip slices are pulled by the copy engines (peer
+      // cudaMemcpyAsync on side streams) into local buffers; with
+      // VDI_FLAG_PEER_READS the merge kernels read peer memory directly.
+      const bool zero_copy = cf.flags & VDI_FLAG_PEER_READS;
+      int q = 0;
+      if (!zero_copy) CUDA_TRY(ctx, cudaEventRecord(ctx->evx[0], st));
+      for (uint32_t s = 0; s < n; ++s) {
+        if (slot[s] >= 0) continue;
+        void* pc = nullptr;
+        void* pd = nullptr;
+        void* pr = nullptr;
+        CUDA_TRY(ctx, ipc_import(ctx, refs[(size_t)s * 3 + 0], &pc));
+        CUDA_TRY(ctx, ipc_import(ctx, refs[(size_t)s * 3 + 1], &pd));
+        CUDA_TRY(ctx, ipc_import(ctx, refs[(size_t)s * 3 + 2], &pr));
+        const uint64_t b0 = bnd[(size_t)s * (G + 1) + me], t = T(s, me);
+        const uint8_t* rc = static_cast<const uint8_t*>(pc) + (size_t)ctx->row0 * W;
+        const float2* rd = static_cast<const float2*>(pd) + b0;
+        const float4* rr = static_cast<const float4*>(pr) + b0;
+        if (zero_copy) {
+          mp.src[s] = SrcDesc{rc, rd, rr};
+        } else {
+          CUDA_TRY(ctx, ctx->rcount[s].grow(ctx->P));
+          CUDA_TRY(ctx, ctx->rdepth[s].grow(std::max<uint64_t>(t, 1) * 8));
+          CUDA_TRY(ctx, ctx->rrgba[s].grow(std::max<uint64_t>(t, 1) * 16));
+          cudaStream_t cs = ctx->xs[q % vdi_ctx::kXStreams];
+          if (q < vdi_ctx::kXStreams) CUDA_TRY(ctx, cudaStreamWaitEvent(cs, ctx->evx[0], 0));
+          CUDA_TRY(ctx, cudaMemcpyAsync(ctx->rcount[s].p, rc, ctx->P, cudaMemcpyDeviceToDevice, cs));
+          if (t) {
+            CUDA_TRY(ctx, cudaMemcpyAsync(ctx->rdepth[s].p, rd, t * 8, cudaMemcpyDeviceToDevice, cs));
+            CUDA_TRY(ctx, cudaMemcpyAsync(ctx->rrgba[s].p, rr, t * 16, cudaMemcpyDeviceToDevice, cs));
+          }
+          mp.src[s] = SrcDesc{ctx->rcount[s].as<uint8_t>(), ctx->rdepth[s].as<float2>(), ctx->rrgba[s].as<float4>()};
+          ++q;
         }
         recvd += ctx->P + 24 * t;
       }
+      for (int i = 0; i < std::min<int>(q, vdi_ctx::kXStreams); ++i) {  // join the copy streams
+        CUDA_TRY(ctx, cudaEventRecord(ctx->evx[1 + i], ctx->xs[i]));
+        CUDA_TRY(ctx, cudaStreamWaitEvent(st, ctx->evx[1 + i], 0));
+      }
+      for (uint32_t s = 0; s < n; ++s)
+        if (slot[s] >= 0)
+          for (uint32_t g = 0; g < G; ++g)
+            if (g != me) sent += (uint64_t)(rows[g + 1] - rows[g]) * W + 24 * T(s, g);
+      ctx->peer_reads = true;
+    } else {
+      for (uint32_t s = 0; s < n; ++s) {
+        if (slot[s] >= 0) continue;
+        CUDA_TRY(ctx, ctx->rcount[s].grow(ctx->P));
+        CUDA_TRY(ctx, ctx->rdepth[s].grow(std::max<uint64_t>(T(s, me), 1) * 8));
+        CUDA_TRY(ctx, ctx->rrgba[s].grow(std::max<uint64_t>(T(s, me), 1) * 16));
+      }
+      // all-to-allv of count slices and dense payload slices
+      NCCL_TRY(ctx, ncclGroupStart());
+      for (uint32_t g = 0; g < G; ++g) {
+        if (g == me) continue;
+        const uint64_t Pg = (uint64_t)(rows[g + 1] - rows[g]) * W;
+        for (uint32_t s = 0; s < n; ++s) {  // our PEs -> g
+          if (slot[s] < 0) continue;
+          const vdi_dense_view& v = local[slot[s]];
+          const uint64_t b = bnd[(size_t)s * (G + 1) + g], t = T(s, g);
+          NCCL_TRY(ctx, ncclSend(v.count + (size_t)rows[g] * W, Pg, ncclUint8, (int)g, ctx->comm, st));
+          if (t) {
+            NCCL_TRY(ctx, ncclSend(v.depth + b * 2, t * 2, ncclFloat32, (int)g, ctx->comm, st));
+            NCCL_TRY(ctx, ncclSend(v.rgba + b * 4, t * 4, ncclFloat32, (int)g, ctx->comm, st));
+          }
+          sent += Pg + 24 * t;
+        }
+        for (uint32_t s = 0; s < n; ++s) {  // g's PEs -> us
+          if (vdi_pe_home(n, G, s) != g) continue;
+          const uint64_t t = T(s, me);
+          NCCL_TRY(ctx, ncclRecv(ctx->rcount[s].p, ctx->P, ncclUint8, (int)g, ctx->comm, st));
+          if (t) {
+            NCCL_TRY(ctx, ncclRecv(ctx->rdepth[s].p, t * 2, ncclFloat32, (int)g, ctx->comm, st));
+            NCCL_TRY(ctx, ncclRecv(ctx->rrgba[s].p, t * 4, ncclFloat32, (int)g, ctx->comm, st));
+          }
+          recvd += ctx->P + 24 * t;
+        }
+      }
+      NCCL_TRY(ctx, ncclGroupEnd());
     }
-    NCCL_TRY(ctx, ncclGroupEnd());
     for (uint32_t s = 0; s < n; ++s) {
-      const uint64_t t = T(s, me);
-      S_here += t;
+      S_here += T(s, me);
       if (slot[s] >= 0) {
         const vdi_dense_view& v = local[slot[s]];
         const uint64_t b = bnd[(size_t)s * (G + 1) + me];
         mp.src[s] = SrcDesc{v.count + (size_t)ctx->row0 * W, reinterpret_cast<const float2*>(v.depth) + b,
                             reinterpret_cast<const float4*>(v.rgba) + b};
-      } else {
+      } else if (!peer) {
         mp.src[s] = SrcDesc{ctx->rcount[s].as<uint8_t>(), ctx->rdepth[s].as<float2>(), ctx->rrgba[s].as<float4>()};
-      }
+      }  // peer: set above
     }
   }
   if (timing) CUDA_TRY(ctx, cudaEventRecord(ctx->ev[1], st));
@@ -589,6 +731,12 @@ vdi_status vdi_composite(vdi_ctx* ctx, const vdi_dense_view* local, uint32_t n_l
     CUDA_TRY(ctx, cudaEventRecord(ctx->evc[VDI_MAX_CHUNKS], ctx->side));
     CUDA_TRY(ctx, cudaStreamWaitEvent(st, ctx->evc[VDI_MAX_CHUNKS], 0));
     if (timing) CUDA_TRY(ctx, cudaEventRecord(ctx->ev[5], st));
+  }
+  if (ctx->peer_reads) {
+    // end barrier: no rank reuses its inputs before every peer finished reading them
+    CUDA_TRY(ctx, ctx->bounds.grow(16));
+    NCCL_TRY(ctx, ncclAllReduce(ctx->bounds.p, ctx->bounds.p, 1, ncclUint8, ncclSum, ctx->comm, st));
+    ctx->peer_reads = false;
   }
   if (timing) {
     CUDA_TRY(ctx, cudaEventRecord(ctx->ev[2], st));

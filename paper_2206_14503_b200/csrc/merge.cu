@@ -829,26 +829,35 @@ __device__ __forceinline__ int short_ms(int b) { return b == 0 ? 32 : 40; }
 
 template <int NS>
 __global__ void __launch_bounds__(128) search_gather_kernel(MergeParams mp) {
+  // per thread: depth column (PE-concatenated order) and the depth-order
+  // permutation in shared memory, [q][thread] layout (conflict-free)
+  __shared__ float2 sd[40 * 128];
+  __shared__ uint8_t sp[40 * 128];
   const int n = mp.n_src;
+  const int tid = threadIdx.x;
   const uint32_t c0 = min(mp.wl_count[0], mp.wl_cap), c1 = min(mp.wl_count[1], mp.wl_cap);
-  const uint32_t tot = ((c0 + 31) & ~31u) + c1;  // bucket 1 starts at a warp boundary
+  const uint32_t c0r = (c0 + 31) & ~31u;  // bucket 1 starts at a warp boundary
+  const uint32_t tot = c0r + c1;
   const uint32_t lane = threadIdx.x & 31;
+  float2* my_d = sd + tid;
+  uint8_t* my_p = sp + tid;
   for (uint32_t v0 = blockIdx.x * blockDim.x; v0 < tot; v0 += gridDim.x * blockDim.x) {
     const uint32_t v = v0 + threadIdx.x;
-    const uint32_t c0r = (c0 + 31) & ~31u;
     const int bucket = v < c0r ? 0 : 1;
     const uint32_t i = bucket == 0 ? v : v - c0r;
     const bool valid = i < (bucket == 0 ? c0 : c1);
-    const int MS = short_ms(bucket);
     const uint32_t* ent = mp.wl[bucket] + (size_t)(valid ? i : 0) * (3 + n);
     const uint32_t p = valid ? ent[0] : 0u, m = valid ? ent[2] : 0u;
-    uint32_t goff[NS], cnt[NS];
+    uint32_t goff[NS], cnt[NS], cs[NS];
+    uint32_t j = 0;
 #pragma unroll
     for (int s = 0; s < NS; ++s) {
-      goff[s] = cnt[s] = 0;
+      goff[s] = cnt[s] = cs[s] = 0;
       if (valid && s < n) {
         goff[s] = ent[3 + s];
         cnt[s] = __ldg(mp.src[s].count + p);
+        cs[s] = j;
+        j += cnt[s];
       }
     }
     // one pool slot per batch of 32 entries (a warp here = one batch)
@@ -862,76 +871,58 @@ __global__ void __launch_bounds__(128) search_gather_kernel(MergeParams mp) {
     if (slot >= mp.pool_cap) continue;
     float4* orgba = mp.pool_rgba + (size_t)slot * 40 * 32 + lane;
     float2* odep = mp.pool_depth + (size_t)slot * 40 * 32 + lane;
+    // depth column in PE order (independent loads), then the depth order
+    load_concat<NS, 8>(mp, goff, cnt, cs, m, my_d, nullptr, 128);
     uint32_t g0 = 0, g1 = 0;
     bool bad = false;
     if (valid) {
-      uint32_t hp[NS];
-#pragma unroll
-      for (int s = 0; s < NS; ++s) hp[s] = 0;
-      float prev_tb = -CUDART_INF_F;
-      uint32_t r = 0;
-      while (r < m) {
-        int b = -1, b2 = NS;
-        float bt = CUDART_INF_F, b2t = CUDART_INF_F;
-#pragma unroll
-        for (int s = 0; s < NS; ++s)
-          if (hp[s] < cnt[s]) {
-            const float t = __ldg(&mp.src[s].depth[goff[s] + hp[s]].x);
-            if (b < 0 || t < bt) {
-              if (b >= 0) {
-                b2t = bt;
-                b2 = b;
-              }
-              bt = t;
-              b = s;
-            } else if (t < b2t) {
-              b2t = t;
-              b2 = s;
-            }
-          }
-        uint32_t ii = 0, cb = 0, gb = 0;
-        const float2* dp = nullptr;
-        const float4* cp = nullptr;
-#pragma unroll
-        for (int s = 0; s < NS; ++s)
-          if (s == b) {
-            ii = hp[s];
-            cb = cnt[s];
-            gb = goff[s];
-            dp = mp.src[s].depth;
-            cp = mp.src[s].rgba;
-          }
-        for (;;) {
-          const float2 d = __ldg(dp + gb + ii);
-          const float4 c = __ldg(cp + gb + ii);
-          bad |= c.w == 0.f || d.x < prev_tb;  // Q23 / Q12
+      bad = !run_merge<NS>(my_d, 128, cs, cnt, m, my_p, 128, [](uint32_t) { return 1.f; });  // overlap, Q12
+      if (!bad) {
+        float prev_tb = 0.f;
+        for (uint32_t r = 0; r < m; ++r) {  // gap bits from the staged depths
+          const float2 d = my_d[(uint32_t)my_p[r * 128] * 128];
           if (r > 0 && d.x > prev_tb) {
             if (r < 32) g0 |= 1u << r;
             else g1 |= 1u << (r - 32);
           }
           prev_tb = d.y;
-          orgba[r * 32] = c;
-          odep[r * 32] = d;
-          ++r;
-          ++ii;
-          if (ii >= cb) break;
-          const float tn = __ldg(&dp[gb + ii].x);
-          if (!(tn < b2t || (tn == b2t && b < b2))) break;
         }
+        // records in depth order, 8 loads in flight per trip, to the scratch
+        for (uint32_t r0 = 0; r0 < m; r0 += 8) {
+          float4 cv[8];
 #pragma unroll
-        for (int s = 0; s < NS; ++s)
-          if (s == b) hp[s] = ii;
+          for (int u = 0; u < 8; ++u) {
+            const uint32_t r = r0 + u;
+            if (r < m) {
+              const uint32_t ci = my_p[r * 128];
+              const float4* cp = nullptr;
+              uint32_t gi = 0;
+#pragma unroll
+              for (int s = 0; s < NS; ++s)
+                if (ci >= cs[s] && ci < cs[s] + cnt[s]) {
+                  gi = goff[s] + (ci - cs[s]);
+                  cp = mp.src[s].rgba;
+                }
+              cv[u] = __ldg(cp + gi);
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const uint32_t r = r0 + u;
+            if (r < m) {
+              bad |= cv[u].w == 0.f;  // Q23
+              orgba[r * 32] = cv[u];
+              odep[r * 32] = my_d[(uint32_t)my_p[r * 128] * 128];
+            }
+          }
+        }
       }
       uint32_t* og = mp.pool_gap + (size_t)slot * 64 + lane;
-      og[0] = g0;
-      og[32] = g1;
+      og[0] = bad ? 0xffffffffu : g0;  // skip marker (bit 0 of a real gap word is never set)
+      og[32] = bad ? 0xffffffffu : g1;
     }
     const int bk = (valid && bad) ? VDI_BUCKET_GENERAL : -1;
     if (__any_sync(kFull, bk >= 0)) push_entries<NS>(mp, bk, p, m, goff, lane);
-    if (valid && bad) {  // skip marker (bit 0 of a real gap word is never set)
-      mp.pool_gap[(size_t)slot * 64 + lane] = 0xffffffffu;
-      mp.pool_gap[(size_t)slot * 64 + 32 + lane] = 0xffffffffu;
-    }
   }
 }
 
@@ -966,23 +957,25 @@ __global__ void __launch_bounds__(32, 8) search_sweep_kernel(MergeParams mp, int
       const float g2 = mid * mid;
       float ar = 0.f, ag = 0.f, ab = 0.f, aa = 0.f;
       int sc = 0;
+      // The count only grows, so "count > k at the end" == "the sequential
+      // sweep stopped early"; after that (or past m, or once the lane's
+      // bisection has ended) the accumulator is never read, so only the count
+      // increment is predicated: the recurrence acc -> D^2 -> split -> acc is
+      // the whole critical path.
 #pragma unroll
       for (int q = 0; q < MS; ++q) {
         if ((q & 7) == 0 && q > 0 && !__any_sync(kFull, active && q < mi && sc <= k)) break;
-        const bool live = active && q < mi && sc <= k;
         const float4 sv = S[q];
-        const bool gap = ((gapw[q >> 5] >> (q & 31)) & 1u) != 0u;
+        const bool gap = (gapw[q >> 5] & (1u << (q & 31))) != 0u;
         const float n2 = fmaf(aa, aa, fmaf(ab, ab, fmaf(ag, ag, ar * ar)));  // dist2(acc, 0), Q8
         const float d2 = dist2(ar, ag, ab, aa, sv.x, sv.y, sv.z, sv.w);
         const bool st = (q == 0) | (gap & (n2 > g2)) | (d2 > g2);  // open before q is (q > 0)
         const float tr = 1.0f - aa;
-        const float nr = st ? sv.x : fmaf(tr, sv.x, ar), ng = st ? sv.y : fmaf(tr, sv.y, ag);
-        const float nb = st ? sv.z : fmaf(tr, sv.z, ab), na = st ? sv.w : fmaf(tr, sv.w, aa);
-        ar = live ? nr : ar;
-        ag = live ? ng : ag;
-        ab = live ? nb : ab;
-        aa = live ? na : aa;
-        sc += (live && st) ? 1 : 0;
+        ar = st ? sv.x : fmaf(tr, sv.x, ar);
+        ag = st ? sv.y : fmaf(tr, sv.y, ag);
+        ab = st ? sv.z : fmaf(tr, sv.z, ab);
+        aa = st ? sv.w : fmaf(tr, sv.w, aa);
+        sc += (st && q < mi) ? 1 : 0;
       }
       if (active) {
         if (sc <= k) {
@@ -1000,11 +993,17 @@ __global__ void __launch_bounds__(32, 8) search_sweep_kernel(MergeParams mp, int
       float4* oc = mp.out_rgba + (size_t)p * k;
       float ar = 0.f, ag = 0.f, ab = 0.f, aa = 0.f, tf = 0.f, tb = 0.f;
       int c = 0;
+      float2 dq[8];
 #pragma unroll
       for (int q = 0; q < MS; ++q) {
+        if ((q & 7) == 0) {  // depth of the next 8 samples: loads issued together, before the stores
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            if (q + u < MS && q + u < mi) dq[u] = dcol[(q + u) * 32];
+        }
         if (q < mi) {
           const float4 sv = S[q];
-          const float2 d = dcol[q * 32];
+          const float2 d = dq[q & 7];
           const bool gap = ((gapw[q >> 5] >> (q & 31)) & 1u) != 0u;
           const float n2 = fmaf(aa, aa, fmaf(ab, ab, fmaf(ag, ag, ar * ar)));
           const float d2 = dist2(ar, ag, ab, aa, sv.x, sv.y, sv.z, sv.w);
@@ -1314,7 +1313,7 @@ static cudaError_t launch_fast_ns(const MergeParams& mp, cudaStream_t st, int* l
 template <int NS>
 static cudaError_t launch_search_ns(const MergeParams& mp, cudaStream_t st, int* launches) {
   cudaError_t e;
-  search_gather_kernel<NS><<<sm_count() * 8, 128, 0, st>>>(mp);
+  search_gather_kernel<NS><<<sm_count() * 4, 128, 0, st>>>(mp);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   ++*launches;
   if ((e = launch_sweep<32>(mp, 0, st)) != cudaSuccess) return e;
