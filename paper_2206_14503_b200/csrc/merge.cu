@@ -25,10 +25,13 @@
 // The decision arithmetic (tau, the blend) is fp32 with explicit fmaf in the
 // order DESIGN.md §2 fixes; the TU is compiled with -fmad=false so no other
 // contraction happens.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <math_constants.h>
 
 #include "internal.h"
+
+namespace cg = cooperative_groups;
 
 namespace vdi {
 
@@ -619,8 +622,7 @@ __global__ void __launch_bounds__(kFastThreads) merge_fast_kernel(MergeParams mp
 static constexpr int kRefill = 8;  // lanes that must be free before the warp refills them together
 
 template <int NS, int MS>
-__global__ void __launch_bounds__(32) merge_search_kernel(MergeParams mp, int bucket) {
-  extern __shared__ float4 smem[];
+__device__ __forceinline__ void search_smem_body(const MergeParams& mp, int bucket, float4* smem) {
   float4* Sr = smem;                                             // [MS][32] rgba, depth order
   float2* Sd = reinterpret_cast<float2*>(Sr + MS * 32);          // [MS][32] depth, PE-concatenated order
   uint8_t* Pm = reinterpret_cast<uint8_t*>(Sd + MS * 32);        // [MS][32] concat index
@@ -927,19 +929,19 @@ __global__ void __launch_bounds__(128) search_gather_kernel(MergeParams mp) {
 }
 
 template <int MS>
-__global__ void __launch_bounds__(32, 8) search_sweep_kernel(MergeParams mp, int bucket) {
+__device__ __forceinline__ void sweep_batch(const MergeParams& mp, int bucket, uint32_t batch) {
   const int lane = threadIdx.x;
   const int k = mp.k_out, n = mp.n_src;
   const uint32_t total = min(mp.wl_count[bucket], mp.wl_cap);
   const uint32_t* wl = mp.wl[bucket];
-  for (uint32_t batch = blockIdx.x; batch * 32 < total; batch += gridDim.x) {
+  {
     const uint32_t e = batch * 32 + lane;
     const bool valid = e < total;
     const uint32_t* ent = wl + (size_t)(valid ? e : 0) * (3 + n);
     const uint32_t p = valid ? ent[0] : 0u;
     const int mi = valid ? (int)ent[2] : 0;
     const uint32_t slot = mp.batch_slot[bucket][batch];
-    if (slot >= mp.pool_cap) continue;
+    if (slot >= mp.pool_cap) return;
     const uint32_t* gp = mp.pool_gap + (size_t)slot * 64 + lane;
     const uint32_t gw0 = valid ? gp[0] : 0u, gw1 = valid ? gp[32] : 0u;
     const bool bad = valid && gw0 == 0xffffffffu && gw1 == 0xffffffffu;  // sent to the general path
@@ -1032,6 +1034,16 @@ __global__ void __launch_bounds__(32, 8) search_sweep_kernel(MergeParams mp, int
   }
 }
 
+// both short-list buckets in one launch: batches of bucket 0 (m <= 32) first
+__global__ void __launch_bounds__(32, 8) search_sweep_kernel(MergeParams mp) {
+  const uint32_t nb0 = (min(mp.wl_count[0], mp.wl_cap) + 31) / 32;
+  const uint32_t nb1 = (min(mp.wl_count[1], mp.wl_cap) + 31) / 32;
+  for (uint32_t v = blockIdx.x; v < nb0 + nb1; v += gridDim.x) {
+    if (v < nb0) sweep_batch<32>(mp, 0, v);
+    else sweep_batch<40>(mp, 1, v - nb0);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // General path: thread per work-list entry (steps 1-6 with subdivision),
 // samples in global scratch.  Used for overlapping / transparent records and
@@ -1042,11 +1054,11 @@ __device__ void over_into(float* acc, const float* b) {
   for (int c = 0; c < 4; ++c) acc[c] = fmaf(tr, b[c], acc[c]);
 }
 
-__global__ void __launch_bounds__(kSlowThreads) merge_general_kernel(MergeParams mp) {
+__device__ __forceinline__ void general_body(const MergeParams& mp, uint32_t tid, uint32_t nthreads) {
   const int n = mp.n_src, k = mp.k_out;
   const uint32_t total = min(mp.wl_count[VDI_BUCKET_GENERAL], mp.wl_cap);
   const uint32_t* wl = mp.wl[VDI_BUCKET_GENERAL];
-  for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
+  for (uint32_t e = tid; e < total; e += nthreads) {
     const uint32_t* ent = wl + (size_t)e * (3 + n);
     const uint32_t p = ent[0];
     const uint32_t m0 = ent[2];
@@ -1164,6 +1176,18 @@ __global__ void __launch_bounds__(kSlowThreads) merge_general_kernel(MergeParams
   }
 }
 
+// Lists with 40 < m <= 128 (samples in shared memory) and then, after a
+// grid-wide barrier (every push to the general work list is complete), the
+// general path -- one cooperative launch.
+template <int NS>
+__global__ void __launch_bounds__(32) merge_tail_kernel(MergeParams mp) {
+  extern __shared__ float4 smem[];
+  search_smem_body<NS, 128>(mp, 2, smem);
+  search_smem_body<NS, 128>(mp, 3, smem);
+  cg::this_grid().sync();
+  general_body(mp, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x);
+}
+
 // ---------------------------------------------------------------------------
 // Launchers
 // ---------------------------------------------------------------------------
@@ -1258,35 +1282,34 @@ static cudaError_t prep(K kernel, size_t smem, int threads, int* per_sm) {
   return e;
 }
 
-template <int NS, int MS>
-static cudaError_t launch_search(const MergeParams& mp, int bucket, cudaStream_t st) {
-  const size_t smem = (size_t)MS * 32 * (16 + 8 + 1);
+template <int NS>
+static cudaError_t launch_tail(const MergeParams& mp, cudaStream_t st) {
+  const size_t smem = (size_t)128 * 32 * (16 + 8 + 1);
   static int per_sm = 0;
   static size_t prepared = 0;
   if (smem != prepared) {
-    cudaError_t e = prep(merge_search_kernel<NS, MS>, smem, 32, &per_sm);
+    cudaError_t e = prep(merge_tail_kernel<NS>, smem, 32, &per_sm);
     if (e != cudaSuccess) return e;
     prepared = smem;
   }
-  uint32_t grid = (uint32_t)sm_count() * per_sm;
-  const uint32_t most = (mp.P + 31) / 32;
-  if (grid > most) grid = most ? most : 1;
-  merge_search_kernel<NS, MS><<<grid, 32, smem, st>>>(mp, bucket);
-  return cudaGetLastError();
+  const unsigned grid = (unsigned)(sm_count() * per_sm);  // co-resident: cooperative launch
+  MergeParams copy = mp;
+  void* args[] = {&copy};
+  return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(merge_tail_kernel<NS>), dim3(grid), dim3(32), args,
+                                     smem, st);
 }
 
-template <int MS>
-static cudaError_t launch_sweep(const MergeParams& mp, int bucket, cudaStream_t st) {
+static cudaError_t launch_sweep(const MergeParams& mp, cudaStream_t st) {
   static int per_sm = 0;
   if (!per_sm) {
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, search_sweep_kernel<MS>, 32, 0);
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, search_sweep_kernel, 32, 0);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) per_sm = 1;
   }
   uint32_t grid = (uint32_t)sm_count() * per_sm;
   const uint32_t most = (mp.P + 31) / 32;
   if (grid > most) grid = most ? most : 1;
-  search_sweep_kernel<MS><<<grid, 32, 0, st>>>(mp, bucket);
+  search_sweep_kernel<<<grid, 32, 0, st>>>(mp);
   return cudaGetLastError();
 }
 
@@ -1316,17 +1339,11 @@ static cudaError_t launch_search_ns(const MergeParams& mp, cudaStream_t st, int*
   search_gather_kernel<NS><<<sm_count() * 4, 128, 0, st>>>(mp);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   ++*launches;
-  if ((e = launch_sweep<32>(mp, 0, st)) != cudaSuccess) return e;
+  if ((e = launch_sweep(mp, st)) != cudaSuccess) return e;
   ++*launches;
-  if ((e = launch_sweep<40>(mp, 1, st)) != cudaSuccess) return e;
+  if ((e = launch_tail<NS>(mp, st)) != cudaSuccess) return e;
   ++*launches;
-  if ((e = launch_search<NS, 64>(mp, 2, st)) != cudaSuccess) return e;
-  ++*launches;
-  if ((e = launch_search<NS, 128>(mp, 3, st)) != cudaSuccess) return e;
-  ++*launches;
-  merge_general_kernel<<<sm_count() * 4, kSlowThreads, 0, st>>>(mp);
-  ++*launches;
-  return cudaGetLastError();
+  return cudaSuccess;
 }
 
 #define VDI_DISPATCH_NS(F, ...)                                  \
