@@ -71,6 +71,7 @@ struct DevCounters {
   unsigned long long records_in;
   unsigned long long fallback_groups;
   unsigned long long records_search;
+  unsigned long long long_used;
 };
 
 }  // namespace
@@ -86,6 +87,7 @@ struct vdi_ctx {
   // merge scratch
   DevBuf group_sum, group_base, wl, scratch, dcnt, stat_gamma, stat_m, bounds, srch, slots;
   DevBuf g_sum, g_base, g_tot, g_dense, g_rcount, g_rpay, g_misc;  // dense gather
+  DevBuf lpool, lbatch;  // long-list search pool
   std::map<std::string, void*> ipc_cache;  // IPC handle bytes -> mapped base of a peer allocation
   static constexpr int kXStreams = 4;      // copy-engine streams of the peer exchange
   cudaStream_t xs[4] = {};
@@ -684,8 +686,20 @@ vdi_status vdi_composite(vdi_ctx* ctx, const vdi_dense_view* local, uint32_t n_l
     mp.pool_gap = reinterpret_cast<uint32_t*>(q);
     mp.pool_cap = (uint32_t)pool_cap;
   }
+  // long-list pool: slots of stride maxm per 32-list batch; a list of bucket
+  // 2/3 has m > 40, so the pool needs at most 24 B x (S_here + 32 x batches
+  // of padding); batches <= S_here / 41 / 32 + 1 per bucket
+  const uint64_t lb = S_here / 41 / 32 + 2;
+  const unsigned long long lcap = 24ull * S_here * 2 + lb * 2 * (128 + 24 * 32) + 4096;
+  CUDA_TRY(ctx, ctx->lpool.grow(lcap));
+  CUDA_TRY(ctx, ctx->lbatch.grow((size_t)(ctx->P / 32 + 2) * 2 * 16));
+  mp.long_pool = ctx->lpool.as<char>();
+  mp.long_cap = lcap;
+  mp.long_batch[0] = ctx->lbatch.as<PoolBatch>();
+  mp.long_batch[1] = ctx->lbatch.as<PoolBatch>() + (ctx->P / 32 + 2);
   DevCounters* dc = ctx->dcnt.as<DevCounters>();
   CUDA_TRY(ctx, cudaMemsetAsync(dc, 0, sizeof(DevCounters), st));
+  mp.long_used = &dc->long_used;
   mp.group_base = ctx->group_base.as<uint32_t>();
   mp.out_count = so->count;
   mp.out_depth = reinterpret_cast<float2*>(so->depth);

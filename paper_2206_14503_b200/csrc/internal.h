@@ -14,6 +14,12 @@
 #define VDI_MAX_GRID_AXIS 16  // bricks per axis in a decomposition
 
 namespace vdi {
+// one 32-list batch of the long-list search pool
+struct PoolBatch {
+  unsigned long long off;  // byte offset in the pool
+  uint32_t maxm;           // longest list of the batch (slot stride)
+  uint32_t ok;             // 1 if the slot was allocated
+};
 
 // 24-byte record of the sub-supersegment scratch (AoS).
 struct Rec {
@@ -31,8 +37,8 @@ struct SrcDesc {
 
 // Work-list buckets of lists that need more than the pass-through:
 // 0, 1 = gamma search with m <= 32 / 40 samples (samples in registers);
-// 2, 3 = gamma search with m <= 64 / 128 samples (samples in shared memory);
-// 4 = general path (overlap subdivision, alpha==0 records, or m > 128;
+// 2, 3 = gamma search with m <= 64 / 255 samples (samples streamed from a pool);
+// 4 = general path (overlap subdivision, alpha==0 records, or m > 255;
 // thread per list, global scratch).
 #define VDI_N_BUCKETS 5
 #define VDI_BUCKET_GENERAL 4
@@ -72,6 +78,11 @@ struct MergeParams {
   uint32_t* pool_next;
   uint32_t pool_cap;
   uint32_t* batch_slot[2];
+  // long-list pool (buckets 2, 3): byte pool + per-batch {offset, stride, ok}
+  char* long_pool;
+  unsigned long long long_cap;
+  unsigned long long* long_used;
+  PoolBatch* long_batch[2];
   int* err;            // bit 0: work list / scratch overflow
   int validate;
 };

@@ -243,7 +243,7 @@ __device__ __forceinline__ void push_entries(const MergeParams& mp, int bk, uint
 }
 
 __device__ __forceinline__ int bucket_of(uint32_t m) {
-  return m <= 32 ? 0 : m <= 40 ? 1 : m <= 64 ? 2 : m <= 128 ? 3 : VDI_BUCKET_GENERAL;
+  return m <= 32 ? 0 : m <= 40 ? 1 : m <= 64 ? 2 : m <= 255 ? 3 : VDI_BUCKET_GENERAL;
 }
 
 // Run-based k-way merge of NS sorted runs held in shared memory (PAPER.md:168:
@@ -1045,6 +1045,195 @@ __global__ void __launch_bounds__(32, 8) search_sweep_kernel(MergeParams mp) {
 }
 
 // ---------------------------------------------------------------------------
+// Search path for long lists (40 < m <= 255): the lists of a warp (one batch
+// of 32 work-list entries) are written in depth order to a slot of a global
+// pool in [sample][lane] layout (rgba with the gap flag in the sign of alpha,
+// then depth), sized by the batch's longest list; the sweeps stream each
+// lane's column through a register double buffer (coalesced, independent of
+// the accumulator, and L2-resident across the bisection's sweeps).
+// ---------------------------------------------------------------------------
+template <int NS>
+__global__ void __launch_bounds__(128) long_gather_kernel(MergeParams mp) {
+  const int n = mp.n_src;
+  const uint32_t c2 = min(mp.wl_count[2], mp.wl_cap), c3 = min(mp.wl_count[3], mp.wl_cap);
+  const uint32_t c2r = (c2 + 31) & ~31u;
+  const uint32_t tot = c2r + c3;
+  const uint32_t lane = threadIdx.x & 31;
+  for (uint32_t v0 = blockIdx.x * blockDim.x; v0 < tot; v0 += gridDim.x * blockDim.x) {
+    const uint32_t v = v0 + threadIdx.x;
+    const int bucket = v < c2r ? 2 : 3;
+    const uint32_t i = bucket == 2 ? v : v - c2r;
+    const bool valid = i < (bucket == 2 ? c2 : c3);
+    const uint32_t* ent = mp.wl[bucket] + (size_t)(valid ? i : 0) * (3 + n);
+    const uint32_t p = valid ? ent[0] : 0u, m = valid ? ent[2] : 0u;
+    uint32_t goff[NS], cnt[NS];
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      goff[s] = cnt[s] = 0;
+      if (valid && s < n) {
+        goff[s] = ent[3 + s];
+        cnt[s] = __ldg(mp.src[s].count + p);
+      }
+    }
+    const uint32_t maxm = __reduce_max_sync(kFull, m);
+    PoolBatch* pbt = mp.long_batch[bucket - 2] + (i >> 5);
+    unsigned long long off = 0;
+    if (lane == 0) {
+      const unsigned long long bytes = (unsigned long long)maxm * 32 * 24 + 128;
+      off = atomicAdd(mp.long_used, bytes);
+      const bool fits = off + bytes <= mp.long_cap;
+      *pbt = PoolBatch{off, maxm, fits ? 1u : 0u};
+    }
+    off = __shfl_sync(kFull, off, 0);
+    const bool fits = off + (unsigned long long)maxm * 32 * 24 + 128 <= mp.long_cap;
+    char* base = mp.long_pool + off;
+    float4* orgba = reinterpret_cast<float4*>(base) + lane;
+    float2* odep = reinterpret_cast<float2*>(base + (size_t)maxm * 32 * 16) + lane;
+    uint32_t* obad = reinterpret_cast<uint32_t*>(base + (size_t)maxm * 32 * 24) + lane;
+    bool bad = !fits;
+    if (valid && fits) {
+      uint32_t hp[NS];
+#pragma unroll
+      for (int s = 0; s < NS; ++s) hp[s] = 0;
+      float prev_tb = -CUDART_INF_F;
+      uint32_t r = 0;
+      while (r < m) {  // run-based k-way merge over the t_front values (L1)
+        int b = -1, b2 = NS;
+        float bt = CUDART_INF_F, b2t = CUDART_INF_F;
+#pragma unroll
+        for (int s = 0; s < NS; ++s)
+          if (hp[s] < cnt[s]) {
+            const float t = __ldg(&mp.src[s].depth[goff[s] + hp[s]].x);
+            if (b < 0 || t < bt) {
+              if (b >= 0) {
+                b2t = bt;
+                b2 = b;
+              }
+              bt = t;
+              b = s;
+            } else if (t < b2t) {
+              b2t = t;
+              b2 = s;
+            }
+          }
+        uint32_t ii = 0, cb = 0, gb = 0;
+        const float2* dp = nullptr;
+        const float4* cp = nullptr;
+#pragma unroll
+        for (int s = 0; s < NS; ++s)
+          if (s == b) {
+            ii = hp[s];
+            cb = cnt[s];
+            gb = goff[s];
+            dp = mp.src[s].depth;
+            cp = mp.src[s].rgba;
+          }
+        for (;;) {
+          const float2 d = __ldg(dp + gb + ii);
+          float4 c = __ldg(cp + gb + ii);
+          bad |= c.w == 0.f || d.x < prev_tb;  // Q23 / Q12
+          if (r > 0 && d.x > prev_tb) c.w = -c.w;  // gap before this sample: sign of alpha
+          prev_tb = d.y;
+          orgba[r * 32] = c;
+          odep[r * 32] = d;
+          ++r;
+          ++ii;
+          if (ii >= cb) break;
+          const float tn = __ldg(&dp[gb + ii].x);
+          if (!(tn < b2t || (tn == b2t && b < b2))) break;
+        }
+#pragma unroll
+        for (int s = 0; s < NS; ++s)
+          if (s == b) hp[s] = ii;
+      }
+    }
+    if (fits) *obad = bad ? 1u : 0u;
+    if (!fits && valid) atomicOr(mp.err, 1);
+    const int bk = (valid && bad && fits) ? VDI_BUCKET_GENERAL : -1;
+    if (__any_sync(kFull, bk >= 0)) push_entries<NS>(mp, bk, p, m, goff, lane);
+  }
+}
+
+// One count-mode sweep over a pool column (same decisions as sweep()).
+__device__ __forceinline__ int long_count(const float4* __restrict__ col, int m, float g2, int k) {
+  float ar = 0.f, ag = 0.f, ab = 0.f, aa = 0.f;
+  int sc = 0;
+  float4 cur[8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u)
+    if (u < m) cur[u] = col[u * 32];
+  for (int q0 = 0; q0 < m && sc <= k; q0 += 8) {
+    float4 nxt[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u)  // next chunk in flight while this one is swept
+      if (q0 + 8 + u < m) nxt[u] = col[(q0 + 8 + u) * 32];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int q = q0 + u;
+      const float4 sv = cur[u];
+      const bool gap = signbit(sv.w);
+      const float sa = fabsf(sv.w);
+      const float n2 = fmaf(aa, aa, fmaf(ab, ab, fmaf(ag, ag, ar * ar)));
+      const float d2 = dist2(ar, ag, ab, aa, sv.x, sv.y, sv.z, sa);
+      const bool st = (q == 0) | (gap & (n2 > g2)) | (d2 > g2);
+      const float tr = 1.0f - aa;
+      ar = st ? sv.x : fmaf(tr, sv.x, ar);
+      ag = st ? sv.y : fmaf(tr, sv.y, ag);
+      ab = st ? sv.z : fmaf(tr, sv.z, ab);
+      aa = st ? sa : fmaf(tr, sa, aa);
+      sc += (st && q < m) ? 1 : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) cur[u] = nxt[u];
+  }
+  return sc;
+}
+
+__global__ void __launch_bounds__(32) long_sweep_kernel(MergeParams mp) {
+  const int lane = threadIdx.x;
+  const int k = mp.k_out, n = mp.n_src;
+  const uint32_t c2 = min(mp.wl_count[2], mp.wl_cap), c3 = min(mp.wl_count[3], mp.wl_cap);
+  const uint32_t nb2 = (c2 + 31) / 32, nb3 = (c3 + 31) / 32;
+  for (uint32_t v = blockIdx.x; v < nb2 + nb3; v += gridDim.x) {
+    const int bucket = v < nb2 ? 2 : 3;
+    const uint32_t batch = bucket == 2 ? v : v - nb2;
+    const uint32_t total = bucket == 2 ? c2 : c3;
+    const PoolBatch pb = mp.long_batch[bucket - 2][batch];
+    if (!pb.ok) continue;
+    const uint32_t e = batch * 32 + lane;
+    const bool valid = e < total;
+    const uint32_t* ent = mp.wl[bucket] + (size_t)(valid ? e : 0) * (3 + n);
+    const uint32_t p = valid ? ent[0] : 0u;
+    const int m = valid ? (int)ent[2] : 0;
+    const char* base = mp.long_pool + pb.off;
+    const float4* col = reinterpret_cast<const float4*>(base) + lane;
+    const float2* dcol = reinterpret_cast<const float2*>(base + (size_t)pb.maxm * 32 * 16) + lane;
+    const bool bad = reinterpret_cast<const uint32_t*>(base + (size_t)pb.maxm * 32 * 24)[lane] != 0u;
+    if (!valid || bad) continue;  // lanes diverge freely: no warp collectives below
+    // bisection (Q3-Q6)
+    float lo = 0.f, hi = mp.gamma_max, best = mp.gamma_max;
+    for (int it = 0; it < mp.max_iters; ++it) {
+      const float mid = 0.5f * (lo + hi);
+      const int c = long_count(col, m, mid * mid, k);
+      if (c <= k) {
+        best = hi = mid;
+        if (c == k) break;
+      } else {
+        lo = mid;
+      }
+    }
+    auto get = [&](int q) {
+      const float4 c = col[q * 32];
+      const float2 d = dcol[q * 32];
+      return Rec{d.x, d.y, c.x, c.y, c.z, fabsf(c.w)};
+    };
+    const int c = sweep(get, m, best, k, mp.out_depth + (size_t)p * k, mp.out_rgba + (size_t)p * k);
+    mp.out_count[p] = (uint8_t)c;
+    if (mp.stat_gamma) mp.stat_gamma[p] = best;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // General path: thread per work-list entry (steps 1-6 with subdivision),
 // samples in global scratch.  Used for overlapping / transparent records and
 // for m > 128.
@@ -1179,12 +1368,7 @@ __device__ __forceinline__ void general_body(const MergeParams& mp, uint32_t tid
 // Lists with 40 < m <= 128 (samples in shared memory) and then, after a
 // grid-wide barrier (every push to the general work list is complete), the
 // general path -- one cooperative launch.
-template <int NS>
-__global__ void __launch_bounds__(32) merge_tail_kernel(MergeParams mp) {
-  extern __shared__ float4 smem[];
-  search_smem_body<NS, 128>(mp, 2, smem);
-  search_smem_body<NS, 128>(mp, 3, smem);
-  cg::this_grid().sync();
+__global__ void __launch_bounds__(kSlowThreads) merge_general_kernel(MergeParams mp) {
   general_body(mp, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x);
 }
 
@@ -1282,23 +1466,6 @@ static cudaError_t prep(K kernel, size_t smem, int threads, int* per_sm) {
   return e;
 }
 
-template <int NS>
-static cudaError_t launch_tail(const MergeParams& mp, cudaStream_t st) {
-  const size_t smem = (size_t)128 * 32 * (16 + 8 + 1);
-  static int per_sm = 0;
-  static size_t prepared = 0;
-  if (smem != prepared) {
-    cudaError_t e = prep(merge_tail_kernel<NS>, smem, 32, &per_sm);
-    if (e != cudaSuccess) return e;
-    prepared = smem;
-  }
-  const unsigned grid = (unsigned)(sm_count() * per_sm);  // co-resident: cooperative launch
-  MergeParams copy = mp;
-  void* args[] = {&copy};
-  return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(merge_tail_kernel<NS>), dim3(grid), dim3(32), args,
-                                     smem, st);
-}
-
 static cudaError_t launch_sweep(const MergeParams& mp, cudaStream_t st) {
   static int per_sm = 0;
   if (!per_sm) {
@@ -1341,9 +1508,15 @@ static cudaError_t launch_search_ns(const MergeParams& mp, cudaStream_t st, int*
   ++*launches;
   if ((e = launch_sweep(mp, st)) != cudaSuccess) return e;
   ++*launches;
-  if ((e = launch_tail<NS>(mp, st)) != cudaSuccess) return e;
+  long_gather_kernel<NS><<<sm_count() * 8, 128, 0, st>>>(mp);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
   ++*launches;
-  return cudaSuccess;
+  long_sweep_kernel<<<sm_count() * 16, 32, 0, st>>>(mp);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  ++*launches;
+  merge_general_kernel<<<sm_count() * 4, kSlowThreads, 0, st>>>(mp);
+  ++*launches;
+  return cudaGetLastError();
 }
 
 #define VDI_DISPATCH_NS(F, ...)                                  \
