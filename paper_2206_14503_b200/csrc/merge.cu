@@ -607,214 +607,6 @@ __global__ void __launch_bounds__(kFastThreads) merge_fast_kernel(MergeParams mp
 }
 
 // ---------------------------------------------------------------------------
-// Search path: one warp per 32 work-list lists (lane = list) of one m-bucket.
-//   * depth order: run-based k-way merge over the lists' t_front values read
-//     through L1 -> permutation (concat index per position);
-//   * the rgba of every sample is gathered in depth order into a PACKED
-//     per-warp shared buffer (17 B per sample: rgba + permutation byte; lanes'
-//     regions are laid end to end by a warp scan of m), the gap bits live in
-//     registers, t_front / t_back are re-read through L1 only by the final
-//     write sweep -- so ~16 warps fit per SM;
-//   * per-list bisection (Q3-Q6) with branch-free
-//     count sweeps (the decisions of sweep(), Q1/Q2/Q8), then the write sweep.
-// Lists with transparent or overlapping records go to the general path.
-// ---------------------------------------------------------------------------
-static constexpr int kRefill = 8;  // lanes that must be free before the warp refills them together
-
-template <int NS, int MS>
-__device__ __forceinline__ void search_smem_body(const MergeParams& mp, int bucket, float4* smem) {
-  float4* Sr = smem;                                             // [MS][32] rgba, depth order
-  float2* Sd = reinterpret_cast<float2*>(Sr + MS * 32);          // [MS][32] depth, PE-concatenated order
-  uint8_t* Pm = reinterpret_cast<uint8_t*>(Sd + MS * 32);        // [MS][32] concat index
-  constexpr int NW = (MS + 31) / 32;
-  const int lane = threadIdx.x;
-  const int k = mp.k_out, n = mp.n_src;
-  const uint32_t total = min(mp.wl_count[bucket], mp.wl_cap);
-  const uint32_t* wl = mp.wl[bucket];
-  uint32_t* ticket = mp.search_ticket + bucket;
-  const unsigned lt = (1u << lane) - 1u;
-
-  // this lane's list
-  bool has = false;     // a list is loaded
-  bool done = false;    // its bisection finished (write pending)
-  uint32_t p = 0, m = 0, goff[NS], cnt[NS], cs[NS], gapw[NW];
-#pragma unroll
-  for (int s = 0; s < NS; ++s) goff[s] = cnt[s] = cs[s] = 0;
-#pragma unroll
-  for (int w = 0; w < NW; ++w) gapw[w] = 0;
-  float lo = 0.f, hi = 0.f, best = 0.f, mid = 0.f, g2 = 0.f, ar = 0.f, ag = 0.f, ab = 0.f, aa = 0.f;
-  int it = 0, i = 0, sc = 0;
-  uint32_t gw = 0;
-  bool drained = false;  // warp-uniform: the bucket's queue is empty
-
-  for (;;) {
-    // ---- completion + refill, once enough lanes are free --------------------
-    const unsigned busy = __ballot_sync(kFull, has && !done);
-    const unsigned freel = ~busy;
-    if (__popc(freel) >= kRefill || busy == 0) {
-      if (done) {  // final write sweep, then the lane is free
-        auto get = [&](int q) {
-          const float2 d = Sd[(uint32_t)Pm[q * 32 + lane] * 32 + lane];
-          const float4 c = Sr[q * 32 + lane];
-          return Rec{d.x, d.y, c.x, c.y, c.z, c.w};
-        };
-        const int c = sweep(get, (int)m, best, k, mp.out_depth + (size_t)p * k, mp.out_rgba + (size_t)p * k);
-        mp.out_count[p] = (uint8_t)c;
-        if (mp.stat_gamma) mp.stat_gamma[p] = best;
-        has = done = false;
-      }
-      if (!drained) {
-        const unsigned idle = __ballot_sync(kFull, !has);
-        const uint32_t nidle = __popc(idle);
-        uint32_t t0 = 0;
-        if (lane == 0) t0 = atomicAdd(ticket, nidle);
-        t0 = __shfl_sync(kFull, t0, 0);
-        if (t0 + nidle >= total) drained = true;
-        const uint32_t e = t0 + __popc(idle & lt);
-        const bool take = !has && e < total;
-        int bk = -1;
-        if (take) {
-          const uint32_t* ent = wl + (size_t)e * (3 + n);
-          p = ent[0];
-          m = ent[2];
-          uint32_t j = 0;
-#pragma unroll
-          for (int s = 0; s < NS; ++s) {
-            goff[s] = cnt[s] = cs[s] = 0;
-            if (s < n) {
-              goff[s] = ent[3 + s];
-              cnt[s] = __ldg(mp.src[s].count + p);
-              cs[s] = j;
-              j += cnt[s];
-            }
-          }
-          load_concat<NS, 8>(mp, goff, cnt, cs, m, Sd + lane, nullptr, 32);
-          // depth order: run-based k-way merge over the staged t_front column
-          // (PAPER.md:168); gap bits and the overlap test (Q12) on the way
-#pragma unroll
-          for (int w = 0; w < NW; ++w) gapw[w] = 0;
-          bool bad = false;
-          float prev_tb = -CUDART_INF_F;
-          uint32_t hp[NS];
-#pragma unroll
-          for (int s = 0; s < NS; ++s) hp[s] = 0;
-          uint32_t r = 0;
-          while (r < m) {
-            int b = -1, b2 = NS;
-            float bt = CUDART_INF_F, b2t = CUDART_INF_F;
-#pragma unroll
-            for (int s = 0; s < NS; ++s)
-              if (hp[s] < cnt[s]) {
-                const float t = Sd[(cs[s] + hp[s]) * 32 + lane].x;
-                if (b < 0 || t < bt) {
-                  if (b >= 0) {
-                    b2t = bt;
-                    b2 = b;
-                  }
-                  bt = t;
-                  b = s;
-                } else if (t < b2t) {
-                  b2t = t;
-                  b2 = s;
-                }
-              }
-            uint32_t ii = 0, cb = 0, c0 = 0;
-#pragma unroll
-            for (int s = 0; s < NS; ++s)
-              if (s == b) {
-                ii = hp[s];
-                cb = cnt[s];
-                c0 = cs[s];
-              }
-            for (;;) {
-              const float2 d = Sd[(c0 + ii) * 32 + lane];
-              bad |= d.x < prev_tb;
-              if (r > 0 && d.x > prev_tb) gapw[r >> 5] |= 1u << (r & 31);
-              prev_tb = d.y;
-              Pm[r * 32 + lane] = (uint8_t)(c0 + ii);
-              ++r;
-              ++ii;
-              if (ii >= cb) break;
-              const float tn = Sd[(c0 + ii) * 32 + lane].x;
-              if (!(tn < b2t || (tn == b2t && b < b2))) break;
-            }
-#pragma unroll
-            for (int s = 0; s < NS; ++s)
-              if (s == b) hp[s] = ii;
-          }
-          // gather rgba in depth order (independent loads); transparent test (Q23)
-#pragma unroll 4
-          for (uint32_t q = 0; q < m; ++q) {
-            int sb;
-            const uint32_t gi = concat_src<NS>(cs, cnt, goff, Pm[q * 32 + lane], &sb);
-            const float4* cp = nullptr;
-#pragma unroll
-            for (int s = 0; s < NS; ++s)
-              if (s == sb) cp = mp.src[s].rgba;
-            const float4 c = __ldg(cp + gi);
-            Sr[q * 32 + lane] = c;
-            bad |= c.w == 0.f;
-          }
-          if (bad) {
-            bk = VDI_BUCKET_GENERAL;
-          } else {
-            has = true;
-            done = mp.max_iters <= 0;
-            lo = 0.f;
-            hi = best = mp.gamma_max;
-            mid = 0.5f * (lo + hi);
-            g2 = mid * mid;
-            it = i = sc = 0;
-            ar = ag = ab = aa = 0.f;
-            gw = gapw[0];
-          }
-        }
-        if (__any_sync(kFull, bk >= 0)) push_entries<NS>(mp, bk, p, m, goff, lane);
-      }
-      if (!__any_sync(kFull, has)) {
-        if (drained) break;
-        continue;
-      }
-    }
-    // ---- sweeps: every lane advances its own (iteration, sample) state ------
-    // (flattened bisection, an exact replay of bisect(): PAPER.md:100-101, :176)
-    for (;;) {
-      if (has && !done) {
-        const float4 sv = Sr[i * 32 + lane];
-        const uint32_t gapb = (gw >> (i & 31)) & 1u;
-        const float n2 = fmaf(aa, aa, fmaf(ab, ab, fmaf(ag, ag, ar * ar)));  // dist2(acc, 0), Q8
-        const float d2 = dist2(ar, ag, ab, aa, sv.x, sv.y, sv.z, sv.w);
-        // open before sample i is (i > 0); a gap closes iff |acc| > gamma (Q1, Q2, Q8)
-        const uint32_t st = (uint32_t)(i == 0) | (gapb & (uint32_t)(n2 > g2)) | (uint32_t)(d2 > g2);
-        const float tr = 1.0f - aa;
-        ar = st ? sv.x : fmaf(tr, sv.x, ar);
-        ag = st ? sv.y : fmaf(tr, sv.y, ag);
-        ab = st ? sv.z : fmaf(tr, sv.z, ab);
-        aa = st ? sv.w : fmaf(tr, sv.w, aa);
-        sc += (int)st;
-        ++i;
-        const bool end = (i >= (int)m) | (sc > k);
-        const bool feas = sc <= k;
-        const bool stop = end & ((feas & (sc == k)) | (it + 1 >= mp.max_iters));
-        best = (end & feas) ? mid : best;
-        hi = (end & feas) ? mid : hi;
-        lo = (end & !feas) ? mid : lo;
-        it += end ? 1 : 0;
-        const float nmid = 0.5f * (lo + hi);
-        mid = end ? nmid : mid;
-        g2 = end ? nmid * nmid : g2;
-        i = end ? 0 : i;
-        sc = end ? 0 : sc;
-        if ((i & 31) == 0) gw = gapw[i >> 5];
-        done = stop;
-      }
-      const unsigned run = __ballot_sync(kFull, has && !done);
-      if (run == 0 || (!drained && __popc(~run) >= kRefill)) break;
-    }
-  }
-}
-
-// ---------------------------------------------------------------------------
 // Search path for short lists (m <= 40), in two kernels:
 //   search_gather : thread per list (high occupancy hides the latency): the
 //                   run-based k-way merge over the per-PE runs,
