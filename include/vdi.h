@@ -42,7 +42,7 @@ typedef enum {
 #define VDI_FLAG_VALIDATE 0x2u     /* check inputs: count <= k_in, tf < tb, 0 < alpha <= 1, sorted runs */
 #define VDI_FLAG_STAGE_TIMING 0x4u /* record CUDA-event times of the exchange / merge / gather stages */
 #define VDI_FLAG_PEER_READS 0x20u    /* peer exchange without copies: the merge kernels load peers' slices over NVLink */
-#define VDI_FLAG_NCCL_EXCHANGE 0x10u /* exchange through NCCL send/recv into receive buffers (default: the merge reads peers' sub-VDIs over NVLink via CUDA IPC) */
+#define VDI_FLAG_NCCL_EXCHANGE 0x10u /* exchange through NCCL send/recv into receive buffers (default: copy engines pull peers' slices over NVLink from CUDA IPC mappings) */
 #define VDI_FLAG_FULL_GATHER 0x8u  /* gather the full representation as in PAPER.md:185 (default: dense gather + root inflate, identical image) */
 
 typedef struct vdi_ctx vdi_ctx; /* opaque */
@@ -203,7 +203,7 @@ typedef struct {
   uint64_t bytes_received;  /* all-to-allv payload bytes received */
   uint32_t kernel_launches; /* libvdi kernels launched by the call */
   float ms_exchange, ms_merge, ms_gather; /* VDI_FLAG_STAGE_TIMING, else 0 */
-  uint64_t bucket_lists[4];  /* lists sent to the search buckets m <= 32, <= 40, <= 64, <= 128 */
+  uint64_t bucket_lists[4];  /* lists sent to the search buckets m <= 32, <= 40, <= 64, <= 255 */
   uint64_t general_lists;    /* lists sent to the general path (overlaps, alpha == 0, m > 128) */
   uint64_t bytes_gather;     /* bytes that crossed into the root in the last vdi_gather (G > 1) */
   uint64_t fallback_groups;  /* 32-list groups written with plain stores (tail group / unaligned output) */

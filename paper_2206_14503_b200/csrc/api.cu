@@ -93,8 +93,6 @@ struct vdi_ctx {
   cudaStream_t xs[4] = {};
   cudaEvent_t evx[5] = {};
   bool peer_reads = false;
-  cudaStream_t side = nullptr;  // search kernels of chunk c overlap the pass-through kernel of chunk c+1
-  cudaEvent_t evc[VDI_MAX_CHUNKS + 1] = {};
   int n_chunks = 1;
   // exchange receive buffers per source
   std::vector<DevBuf> rcount, rdepth, rrgba;
@@ -115,9 +113,6 @@ struct vdi_ctx {
   cudaEvent_t gev[2] = {nullptr, nullptr};
   ~vdi_ctx() {
     if (cub_tmp) cudaFree(cub_tmp);
-    for (auto& e : evc)
-      if (e) cudaEventDestroy(e);
-    if (side) cudaStreamDestroy(side);
     for (auto& x : xs)
       if (x) cudaStreamDestroy(x);
     for (auto& e : evx)
@@ -308,18 +303,8 @@ vdi_status vdi_composite_init(const vdi_config* cfg, vdi_ctx** out) {
   ctx->hrgba.resize(cfg->n_pes);
   for (auto& ev : ctx->ev) cudaEventCreate(&ev);
   for (auto& ev : ctx->gev) cudaEventCreate(&ev);
-  for (auto& ev : ctx->evc) cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
   for (auto& ev : ctx->evx) cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
   for (auto& x : ctx->xs) cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking);
-  {
-    int lo_prio = 0, hi_prio = 0;
-    cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio);
-    cudaError_t e2 = cudaStreamCreateWithPriority(&ctx->side, cudaStreamNonBlocking, lo_prio);
-    if (e2 != cudaSuccess) {
-      delete ctx;
-      return fail(VDI_ERR_CUDA, "cudaStreamCreate: %s", cudaGetErrorString(e2));
-    }
-  }
   if (cfg->n_ranks > 1) {
     ncclUniqueId id;
     memcpy(&id, cfg->nccl_unique_id, sizeof id);
@@ -652,13 +637,13 @@ vdi_status vdi_composite(vdi_ctx* ctx, const vdi_dense_view* local, uint32_t n_l
   const size_t ng = mp.n_groups;
   CUDA_TRY(ctx, ctx->group_sum.grow((size_t)scan_chunks(mp.P) * n * 4));
   CUDA_TRY(ctx, ctx->group_base.grow(ng * n * 4));
-  // The strip can be processed in C chunks of 32-list groups, the search
-  // kernels of chunk c (side stream) overlapping the pass-through kernel of
-  // chunk c+1.  Measured on C3 (profiles/README.md): C = 8 -> 973 VDIs/s,
-  // C = 2 -> 1495, C = 1 -> 1976 (co-resident search blocks starve the
-  // persistent pass-through grid), so one chunk is used; the mechanism stays
-  // for a future fused scheduler.
-  const uint32_t C = ctx->cfg.flags & 0x100u ? 2u : 1u;
+  // One chunk of 32-list groups, search kernels after the pass-through on
+  // the same stream.  Measured on C3 (profiles/README.md): overlapping them
+  // is slower -- chunked overlap on a second stream (C = 2: 1495 VDIs/s,
+  // C = 8: 973, vs 1976) and a classify kernel + search concurrent with the
+  // whole pass-through (2069-2124 vs 2120): the latency-bound search kernels
+  // run ~2x slower beside the HBM-bound pass-through.
+  const uint32_t C = 1;
   ctx->n_chunks = (int)C;
   std::vector<uint32_t> gb(C + 1);
   for (uint32_t c = 0; c <= C; ++c) gb[c] = (uint32_t)((uint64_t)ng * c / C);
@@ -736,15 +721,13 @@ vdi_status vdi_composite(vdi_ctx* ctx, const vdi_dense_view* local, uint32_t n_l
       }
       mc.wl_count = dc->wl_count[c];
       mc.search_ticket = dc->search_ticket[c];
+      // pass-through (writes every slot of the strip) -> search kernels -> general path
       CUDA_TRY(ctx, launch_fast(mc, st, &launches));
-      CUDA_TRY(ctx, cudaEventRecord(ctx->evc[c], st));
-      CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->side, ctx->evc[c], 0));
-      CUDA_TRY(ctx, launch_search_all(mc, ctx->side, &launches));
+      if (timing) CUDA_TRY(ctx, cudaEventRecord(ctx->ev[4], st));
+      CUDA_TRY(ctx, launch_search(mc, st, &launches));
+      if (timing) CUDA_TRY(ctx, cudaEventRecord(ctx->ev[5], st));
+      CUDA_TRY(ctx, launch_general(mc, st, &launches));
     }
-    if (timing) CUDA_TRY(ctx, cudaEventRecord(ctx->ev[4], st));
-    CUDA_TRY(ctx, cudaEventRecord(ctx->evc[VDI_MAX_CHUNKS], ctx->side));
-    CUDA_TRY(ctx, cudaStreamWaitEvent(st, ctx->evc[VDI_MAX_CHUNKS], 0));
-    if (timing) CUDA_TRY(ctx, cudaEventRecord(ctx->ev[5], st));
   }
   if (ctx->peer_reads) {
     // end barrier: no rank reuses its inputs before every peer finished reading them

@@ -99,7 +99,10 @@ cudaError_t launch_total(const MergeParams& mp, const uint32_t* chunk_sum, unsig
 cudaError_t launch_compact(const uint8_t* count, const float2* depth, const float4* rgba, uint32_t P, int k,
                            const uint32_t* group_base, float2* od, float4* oc, cudaStream_t st, int* launches);
 // search + general kernels over the work lists in mp (stream st)
-cudaError_t launch_search_all(const MergeParams& mp, cudaStream_t st, int* launches);
+// search kernels (buckets 0-3); after launch_fast (it zeroes their lists' slots)
+cudaError_t launch_search(const MergeParams& mp, cudaStream_t st, int* launches);
+// general path (bucket 4); after launch_fast and launch_search
+cudaError_t launch_general(const MergeParams& mp, cudaStream_t st, int* launches);
 
 // Generator (generate.cu)
 struct GenParams {

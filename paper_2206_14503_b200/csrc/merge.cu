@@ -202,6 +202,74 @@ __device__ __forceinline__ float bisect(Get get, int m, int k, int iters, float 
   return best;
 }
 
+// Per-list gamma bisection state (Q3-Q6) with
+// memoised sweep paths.  A count sweep at g2 = fl(mid * mid) takes the same
+// split/merge decisions -- hence returns the same count -- for every g2' with
+// L <= g2' < U, where L is the largest D^2 it merged on (D^2 <= g2) and U the
+// smallest D^2 it split on (D^2 > g2), both over the decisions it evaluated
+// (a sweep that stopped early at count > k_out constrains only its prefix).
+// A level whose midpoint falls inside the interval of the latest sweep on
+// either side of the bracket is resolved without sweeping; the sequence of
+// midpoints and counts is exactly the sequential procedure's.
+struct Bisection {
+  float lo, hi, best, mid, g2;
+  float hL, hU, lL, lU;  // validity intervals (in g2) of the latest count <= k / count > k sweeps
+  int hc, it;
+  bool active;
+  __device__ __forceinline__ void init(float gmax, bool act) {
+    lo = 0.f;
+    hi = best = gmax;
+    hL = lL = 1.f;  // empty
+    hU = lU = 0.f;
+    hc = 0;
+    it = 0;
+    active = act;
+    mid = g2 = 0.f;
+  }
+  __device__ __forceinline__ void step(int c, int k, int iters) {
+    if (c <= k) {
+      best = hi = mid;
+      if (c == k) active = false;
+    } else {
+      lo = mid;
+    }
+    if (++it >= iters) active = false;
+  }
+  // resolve the levels whose count is known; leaves mid / g2 at the next level to sweep
+  __device__ __forceinline__ void advance(int k, int iters) {
+    while (active) {
+      mid = 0.5f * (lo + hi);
+      g2 = mid * mid;
+      if (g2 >= hL && g2 < hU) step(hc, k, iters);
+      else if (g2 >= lL && g2 < lU) step(k + 1, k, iters);
+      else break;
+    }
+  }
+  // record a sweep at g2 (count c, validity [L, U)) and take its level
+  __device__ __forceinline__ void swept(int c, float L, float U, int k, int iters) {
+    if (c <= k) {
+      hL = L;
+      hU = U;
+      hc = c;
+    } else {
+      lL = L;
+      lU = U;
+    }
+    step(c, k, iters);
+  }
+};
+
+// One evaluated decision step of a count sweep: the interval bookkeeping of
+// Bisection for the gap test (n2 vs g2, Q8) and the Eq. 1 test (d2 vs g2).
+__device__ __forceinline__ void track(bool ev, bool gap, float n2, float d2, float g2, float& L, float& U) {
+  const bool gcl = gap & (n2 > g2);  // the gap closed the segment: d2 not consulted
+  const bool dsp = d2 > g2;
+  const float up = gcl ? n2 : (dsp ? d2 : CUDART_INF_F);
+  const float lw = fmaxf((gap & !gcl) ? n2 : -1.f, (!gcl & !dsp) ? d2 : -1.f);
+  U = ev ? fminf(U, up) : U;
+  L = ev ? fmaxf(L, lw) : L;
+}
+
 // Append the lanes with bk >= 0 to work-list bucket bk (one atomic per warp and
 // bucket).  goff[s] = index of the list's first record in source s's payload.
 // General-path entries also reserve 4 m scratch records.
@@ -947,9 +1015,12 @@ __global__ void __launch_bounds__(128) long_gather_kernel(MergeParams mp) {
 }
 
 // One count-mode sweep over a pool column (same decisions as sweep()).
-__device__ __forceinline__ int long_count(const float4* __restrict__ col, int m, float g2, int k) {
+__device__ __forceinline__ int long_count(const float4* __restrict__ col, int m, float g2, int k, float& L,
+                                          float& U) {
   float ar = 0.f, ag = 0.f, ab = 0.f, aa = 0.f;
   int sc = 0;
+  L = -1.f;
+  U = CUDART_INF_F;
   float4 cur[8];
 #pragma unroll
   for (int u = 0; u < 8; ++u)
@@ -968,6 +1039,7 @@ __device__ __forceinline__ int long_count(const float4* __restrict__ col, int m,
       const float n2 = fmaf(aa, aa, fmaf(ab, ab, fmaf(ag, ag, ar * ar)));
       const float d2 = dist2(ar, ag, ab, aa, sv.x, sv.y, sv.z, sa);
       const bool st = (q == 0) | (gap & (n2 > g2)) | (d2 > g2);
+      track(q > 0 && q < m && sc <= k, gap, n2, d2, g2, L, U);
       const float tr = 1.0f - aa;
       ar = st ? sv.x : fmaf(tr, sv.x, ar);
       ag = st ? sv.y : fmaf(tr, sv.y, ag);
@@ -1003,17 +1075,16 @@ __global__ void __launch_bounds__(32) long_sweep_kernel(MergeParams mp) {
     const bool bad = reinterpret_cast<const uint32_t*>(base + (size_t)pb.maxm * 32 * 24)[lane] != 0u;
     if (!valid || bad) continue;  // lanes diverge freely: no warp collectives below
     // bisection (Q3-Q6)
-    float lo = 0.f, hi = mp.gamma_max, best = mp.gamma_max;
-    for (int it = 0; it < mp.max_iters; ++it) {
-      const float mid = 0.5f * (lo + hi);
-      const int c = long_count(col, m, mid * mid, k);
-      if (c <= k) {
-        best = hi = mid;
-        if (c == k) break;
-      } else {
-        lo = mid;
-      }
+    Bisection bs;
+    bs.init(mp.gamma_max, mp.max_iters > 0);
+    for (;;) {
+      bs.advance(k, mp.max_iters);
+      if (!bs.active) break;
+      float L, U;
+      const int c = long_count(col, m, bs.g2, k, L, U);
+      bs.swept(c, L, U, k, mp.max_iters);
     }
+    const float best = bs.best;
     auto get = [&](int q) {
       const float4 c = col[q * 32];
       const float2 d = dcol[q * 32];
@@ -1304,8 +1375,11 @@ static cudaError_t launch_search_ns(const MergeParams& mp, cudaStream_t st, int*
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   ++*launches;
   long_sweep_kernel<<<sm_count() * 16, 32, 0, st>>>(mp);
-  if ((e = cudaGetLastError()) != cudaSuccess) return e;
   ++*launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_general(const MergeParams& mp, cudaStream_t st, int* launches) {
   merge_general_kernel<<<sm_count() * 4, kSlowThreads, 0, st>>>(mp);
   ++*launches;
   return cudaGetLastError();
@@ -1323,7 +1397,7 @@ cudaError_t launch_fast(const MergeParams& mp, cudaStream_t st, int* launches) {
   VDI_DISPATCH_NS(launch_fast_ns, mp, st, launches)
 }
 
-cudaError_t launch_search_all(const MergeParams& mp, cudaStream_t st, int* launches) {
+cudaError_t launch_search(const MergeParams& mp, cudaStream_t st, int* launches) {
   VDI_DISPATCH_NS(launch_search_ns, mp, st, launches)
 }
 
