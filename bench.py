@@ -25,7 +25,16 @@ import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
-os.environ.setdefault("NCCL_DEBUG", "WARN")  # keep stdout to the single JSON line
+os.environ.setdefault("NCCL_DEBUG", "WARN")
+# stdout carries exactly one JSON line: everything else written to fd 1 (the
+# NCCL banner, library chatter) is sent to stderr; emit() writes the line.
+_JSON_FD = os.dup(1)
+os.dup2(2, 1)
+
+
+def emit(obj):
+    os.write(_JSON_FD, (json.dumps(obj) + "\n").encode())
+
 
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
@@ -46,39 +55,57 @@ def _peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons during the timed region."""
+    """nvidia-smi clocks / throttle reasons during the timed region: samples
+    every 20 ms, line-buffered, selected by their own timestamps."""
 
-    Q = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+    Q = ("timestamp,clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
 
     def __init__(self, index):
         self.index = index
-        self.rows = []
+        self.rows = []  # (unix time, fields)
         self.proc = None
+        self.t0 = self.t1 = None
 
     def __enter__(self):
+        cmd = ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+               "-lms", "20"]
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "50"],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            try:
+                self.proc = subprocess.Popen(["stdbuf", "-oL"] + cmd, stdout=subprocess.PIPE,
+                                             stderr=subprocess.DEVNULL, text=True)
+            except FileNotFoundError:
+                self.proc = subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
             t0 = time.time()
             while not self.rows and time.time() - t0 < 5.0:  # sampling is live before timing starts
                 time.sleep(0.01)
-            self.start = len(self.rows)
         except Exception:
             self.proc = None
         return self
 
-    def mark_end(self):
-        time.sleep(0.06)  # one more sample after the timed region
-        self.end = len(self.rows)
-
     def _read(self):
+        import datetime
         for line in self.proc.stdout:
-            self.rows.append([x.strip() for x in line.split(",")])
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                ts = datetime.datetime.strptime(f[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+            except ValueError:
+                ts = time.time()
+            self.rows.append((ts, f))
+
+    def mark_start(self):
+        self.t0 = time.time()
+
+    def mark_end(self):
+        self.t1 = time.time()
+        t = time.time()
+        while self.proc and time.time() - t < 0.5 and not any(ts >= self.t1 for ts, _ in self.rows[-3:]):
+            time.sleep(0.005)
 
     def __exit__(self, *a):
         if self.proc:
@@ -89,16 +116,22 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
-        rows = self.rows[max(0, getattr(self, "start", 1) - 1):getattr(self, "end", len(self.rows))]
-        self.rows = [r for r in rows if len(r) >= 8]
-        if not self.rows:
+        if self.t0 is None or self.t1 is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        rows = [f for ts, f in self.rows if self.t0 - 0.01 <= ts <= self.t1 + 0.01]
+        if not rows:  # region shorter than the sampling period: the first sample after its start
+            after = [f for ts, f in self.rows if ts >= self.t0]
+            rows = after[:1]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"],
+                    "diag": {"rows": len(self.rows), "t0": self.t0, "t1": self.t1,
+                             "last": self.rows[-1][0] if self.rows else None}}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({n for r in self.rows for n, v in zip(names, r[4:8]) if v.lower() == "active"})
+        reasons = sorted({n for r in rows for n, v in zip(names, r[4:8]) if v.lower() == "active"})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+                "reasons": reasons, "samples": len(rows)}
 
 
 def dist_setup():
@@ -194,17 +227,24 @@ def run_reference(args, world, rank):
     per_vdi = statistics.mean(ts) / frac
     v = 1.0 / per_vdi
     sample = f"rows [{pix[0] // cfg.W}, {pix[-1] // cfg.W + 1}) of {cfg.H} ({len(pix)} lists, {frac:.4f} of the image)"
-    print(json.dumps({
+    emit({
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": per_vdi * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": workload_name(cfg, args.view), "sample": sample},
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": sample},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-    }))
+    })
 
 
 def run_ours(args, world, rank, local):
+    # clock sampling starts now, well before the timed region (nvidia-smi can
+    # take seconds to deliver its first sample on a busy box)
+    with ClockSampler(local) as clk:
+        return _run_ours(args, world, rank, local, clk)
+
+
+def _run_ours(args, world, rank, local, clk):
     import paper_2206_14503_b200 as vdi
     from paper_2206_14503_b200 import _lib as L
 
@@ -258,20 +298,20 @@ def run_ours(args, world, rank, local):
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     stage = []
     launches = 0
-    with ClockSampler(local) as clk:
-        torch.cuda.synchronize()
-        barrier(G)
-        for i in range(args.steps):
-            flush.zero_()
-            evs[i][0].record(stream)
-            step()
-            evs[i][1].record(stream)
-            c = comp.counters()  # syncs the stream; outside the events
-            stage.append(c)
-            launches += c["kernel_launches"]
-        torch.cuda.synchronize()
-        barrier(G)
-        clk.mark_end()
+    torch.cuda.synchronize()
+    barrier(G)
+    clk.mark_start()
+    for i in range(args.steps):
+        flush.zero_()
+        evs[i][0].record(stream)
+        step()
+        evs[i][1].record(stream)
+        c = comp.counters()  # syncs the stream; outside the events
+        stage.append(c)
+        launches += c["kernel_launches"]
+    torch.cuda.synchronize()
+    barrier(G)
+    clk.mark_end()
     step_ms = [a.elapsed_time(b) for a, b in evs]
     tot_ms = allreduce_max(sum(step_ms), G)
     ms_per_step = tot_ms / args.steps
@@ -386,7 +426,7 @@ def run_ours(args, world, rank, local):
             "cpu_baseline": cpu,
             "parity_sample": parity,
         }
-        print(json.dumps(res))
+        emit(res)
 
 
 def main():
