@@ -250,72 +250,122 @@ def _run_ours(args, world, rank, local, clk):
 
     cfg = synth.config_by_name(args.config)
     G, n, W, H, k = world, cfg.n_pes, cfg.W, cfg.H, cfg.k_out
-    stream = torch.cuda.current_stream()
-    uid = None
-    if G > 1:
-        import torch.distributed as dist
-        obj = [vdi.get_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        uid = obj[0]
+    F = args.frames if args.frames > 0 else G  # frames in flight per step
     flags = (L.VDI_FLAG_STAGE_TIMING | (L.VDI_FLAG_FULL_GATHER if args.full_gather else 0)
              | (L.VDI_FLAG_NCCL_EXCHANGE if args.nccl_exchange else 0)
              | (L.VDI_FLAG_PEER_READS if args.peer_reads else 0))
-    comp = vdi.Compositor(W, H, cfg.k_in, k, n, n_ranks=G, rank=rank, flags=flags, unique_id=uid, stream=stream)
+    main_stream = torch.cuda.current_stream()
+    # one libvdi context per frame in flight, each on its own stream with its
+    # own communicator; frame f is gathered onto rank f mod G (Q14)
+    comps = []
+    for f in range(F):
+        uid = None
+        if G > 1:
+            import torch.distributed as dist
+            obj = [vdi.get_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            uid = obj[0]
+        st = main_stream if F == 1 else torch.cuda.Stream()
+        comps.append(vdi.Compositor(W, H, cfg.k_in, k, n, n_ranks=G, rank=rank, flags=flags, unique_id=uid,
+                                    stream=st, root=f % G))
+    comp = comps[0]
+    stream = comp.stream
 
-    # ---- inputs (untimed): synthetic volume -> per-PE dense sub-VDIs in HBM
+    # ---- inputs (untimed): synthetic volume -> per-PE dense sub-VDIs in HBM,
+    # one private copy per frame context (same view: every frame is the C3 VDI)
     t0 = time.time()
     vol = synth.make_volume(cfg, device="cuda")
     tf = synth.tf_table(cfg.tf, cfg.tf_scale)
     tft = torch.from_numpy(tf).cuda()
     cam = synth.make_camera(W, H, view=args.view)
     dec = cfg.decomposition()
+    torch.cuda.synchronize()  # the frame streams read the volume
     local_ids = [pe for pe in range(n) if vdi.pe_home(n, G, pe) == rank]
-    local = [comp.generate_subvdi(vol, tft, cam, dec, pe) for pe in local_ids]
+    locals_ = []
+    for c in comps:
+        with torch.cuda.stream(c.stream):
+            locals_.append([c.generate_subvdi(vol, tft, cam, dec, pe) for pe in local_ids])
     torch.cuda.synchronize()
+    local = locals_[0]
     t_gen = time.time() - t0
     S_local = sum(p.total for p in local)
     S_total = int(allreduce_sum(S_local, G))
 
-    if G > 1 and rank == 0:  # rank 0's strip aliases the first rows of the image (no copy in the gather)
-        image = vdi.FullVDI.empty(W, 0, H, k)
-        P0 = (comp.row_end - comp.row_begin) * W
-        strip = vdi.FullVDI(comp.row_begin, comp.row_end, image.count[:P0], image.depth[:P0], image.rgba[:P0])
-    else:
-        strip = comp.empty_strip()
-        image = strip if G == 1 else None
+    strips, images = [], []
+    for c in comps:
+        if G > 1 and rank == c.root:  # the root's strip aliases its rows of the image (no copy in the gather)
+            image = vdi.FullVDI.empty(W, 0, H, k)
+            a0, a1 = c.row_begin * W, c.row_end * W
+            strip = vdi.FullVDI(c.row_begin, c.row_end, image.count[a0:a1], image.depth[a0:a1], image.rgba[a0:a1])
+        else:
+            strip = c.empty_strip()
+            image = strip if G == 1 else None
+        strips.append(strip)
+        images.append(image)
+    strip = strips[0]
     flush = torch.empty(args.flush_mb << 20, dtype=torch.uint8, device="cuda")
 
     def step():
-        comp.composite(local, strip)
-        comp.gather(strip, image)
+        # every composite first (host syncs only on its own frame's size
+        # exchange), then every gather: frame f+1's exchange and merge overlap
+        # frame f's merge and gather
+        for c, lp, sp in zip(comps, locals_, strips):
+            c.composite(lp, sp)
+        for c, sp, im in zip(comps, strips, images):
+            c.gather(sp, im)
+
+    def timed_steps(K, fn, frames):
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+        done = [torch.cuda.Event() for _ in frames]
+        stats, nl = [], 0
+        torch.cuda.synchronize()
+        barrier(G)
+        for i in range(K):
+            flush.zero_()
+            evs[i][0].record(main_stream)
+            for c in frames:
+                if c.stream != main_stream:
+                    c.stream.wait_event(evs[i][0])
+            fn()
+            for c, d in zip(frames, done):
+                if c.stream != main_stream:
+                    d.record(c.stream)
+                    main_stream.wait_event(d)
+            evs[i][1].record(main_stream)
+            cs = [c.counters() for c in frames]  # syncs the frame streams; outside the events
+            stats.append(cs[0])
+            nl += sum(x["kernel_launches"] for x in cs)
+        torch.cuda.synchronize()
+        barrier(G)
+        return [a.elapsed_time(b) for a, b in evs], stats, nl
 
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
     barrier(G)
 
-    # ---- timed region: exactly K steps, L2 flushed between steps (untimed)
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    stage = []
-    launches = 0
-    torch.cuda.synchronize()
-    barrier(G)
+    # ---- timed region: exactly K steps of F frames, L2 flushed between steps (untimed)
     clk.mark_start()
-    for i in range(args.steps):
-        flush.zero_()
-        evs[i][0].record(stream)
-        step()
-        evs[i][1].record(stream)
-        c = comp.counters()  # syncs the stream; outside the events
-        stage.append(c)
-        launches += c["kernel_launches"]
-    torch.cuda.synchronize()
-    barrier(G)
+    step_ms, stage, launches = timed_steps(args.steps, step, comps)
     clk.mark_end()
-    step_ms = [a.elapsed_time(b) for a, b in evs]
     tot_ms = allreduce_max(sum(step_ms), G)
     ms_per_step = tot_ms / args.steps
-    value = args.steps / (tot_ms / 1e3)  # whole VDIs composited by all ranks per second
+    value = F * args.steps / (tot_ms / 1e3)  # whole VDIs composited by all ranks per second
+
+    # ---- latency mode (paper-style): one VDI per step onto rank 0
+    latency = None
+    if F > 1:
+        def one():
+            comps[0].composite(locals_[0], strips[0])
+            comps[0].gather(strips[0], images[0])
+        for _ in range(3):
+            one()
+        K1 = max(10, args.steps // 4)
+        lat_ms, lat_stage, _ = timed_steps(K1, one, comps[:1])
+        l_ms = allreduce_max(sum(lat_ms), G) / K1
+        latency = {"ms_per_vdi": l_ms, "value": 1e3 / l_ms, "steps": K1,
+                   "stages_ms": {s_: statistics.mean(c[f"ms_{s_}"] for c in lat_stage)
+                                 for s_ in ("exchange", "merge", "gather")}}
 
     # ---- rooflines, per rank.  The dominant HBM-bound kernel is
     # merge_fast: it reads the counts, the group bases and the records of the
@@ -391,11 +441,14 @@ def _run_ours(args, world, rank, local, clk):
     if rank == 0:
         res = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": G, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "weak" if F == G else "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": workload_name(cfg, args.view), "n_pes": n, "image": f"{W}x{H}",
                        "k_in": cfg.k_in, "k_out": k, "supersegments_total": S_total,
-                       "parallelism": f"image-space strips x{G} (direct send)",
+                       "parallelism": (f"image-space strips x{G} (direct send); {F} frame(s) in flight per step, "
+                                       f"frame f gathered onto rank f mod {G}"),
+                       "frames_per_step": F,
                        "l2": f"flushed between steps ({args.flush_mb} MiB memset, untimed)",
                        "inputs": "sub-VDIs raycast by vdi_generate_subvdi (untimed), resident in HBM",
                        "gen_seconds": round(t_gen, 2)},
@@ -411,7 +464,8 @@ def _run_ours(args, world, rank, local, clk):
                           "merge_scan": statistics.mean(c["ms_scan"] for c in stage),
                           "merge_fast": statistics.mean(c["ms_fast"] for c in stage),
                           "merge_search": statistics.mean(c["ms_search"] for c in stage)},
-            "supersegments_merged_per_s": rec * G / (ms_per_step * 1e-3),
+            "latency_mode": latency,
+            "supersegments_merged_per_s": S_total * F / (ms_per_step * 1e-3),
             "searched_lists": stage[-1]["searched_lists"],
             "search_buckets": stage[-1]["bucket_lists"], "fast_fallback_groups": stage[-1]["fallback_groups"],
             "exchange_bytes_sent_rank0": bytes_sent, "exchange_bytes_received_rank0": bytes_recv,
@@ -445,6 +499,8 @@ def main():
     ap.add_argument("--full-gather", action="store_true", help="gather the full representation (PAPER.md:185)")
     ap.add_argument("--nccl-exchange", action="store_true", help="NCCL send/recv exchange instead of peer copies")
     ap.add_argument("--peer-reads", action="store_true", help="merge kernels read peers' slices over NVLink")
+    ap.add_argument("--frames", type=int, default=0,
+                    help="frames in flight per step (default: one per GPU, frame f gathered onto rank f mod G)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     world, rank, local = dist_setup()

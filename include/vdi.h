@@ -58,6 +58,8 @@ typedef struct {
   uint32_t k_out;          /* budget of the composited lists, 1..255 (N_s) */
   uint32_t n_pes;          /* number of PEs (sources), >= 1 */
   uint32_t n_ranks, rank;  /* GPUs (one process per GPU) and this process's index */
+  uint32_t root;           /* rank that receives the gathered image (Q14: 0 unless several
+                              frames are in flight, when frame f may be gathered on rank f mod G) */
   uint32_t max_iters;      /* bisection iterations I; 0 -> 16 (Q5) */
   float gamma_max;         /* upper end of the gamma search; 0 -> 2.0 (Q5) */
   uint32_t flags;          /* VDI_FLAG_* */
@@ -178,9 +180,9 @@ vdi_status vdi_composite(vdi_ctx* ctx, const vdi_dense_view* local_pes, uint32_t
 vdi_status vdi_composite_host(vdi_ctx* ctx, const vdi_dense_view* local_pes, uint32_t n_local,
                               vdi_full_view* strip_out);
 
-/* Gather of the composited strips onto rank 0 (PAPER.md:185 MPI_Gather; Q14):
- * image_out (rows [0, H), root only; ignored elsewhere) receives every rank's
- * strip in rank order.  Default: each rank sends its counts + packed records
+/* Gather of the composited strips onto vdi_config.root (PAPER.md:185
+ * MPI_Gather; Q14): image_out (rows [0, H), root only; ignored elsewhere)
+ * receives every rank's strip at its rows.  Default: each rank sends its counts + packed records
  * (dense) and the root re-inflates the full representation -- the image is
  * identical to gathering the full representation (VDI_FLAG_FULL_GATHER).
  * Synchronises the stream once when n_ranks > 1 (payload sizes).  For

@@ -24,7 +24,7 @@ VDI_FLAG_PEER_READS = 0x20
 
 class vdi_config(C.Structure):
     _fields_ = [("width", C.c_uint32), ("height", C.c_uint32), ("k_in", C.c_uint32), ("k_out", C.c_uint32),
-                ("n_pes", C.c_uint32), ("n_ranks", C.c_uint32), ("rank", C.c_uint32),
+                ("n_pes", C.c_uint32), ("n_ranks", C.c_uint32), ("rank", C.c_uint32), ("root", C.c_uint32),
                 ("max_iters", C.c_uint32), ("gamma_max", C.c_float), ("flags", C.c_uint32),
                 ("nccl_unique_id", C.c_void_p), ("cuda_stream", C.c_void_p)]
 

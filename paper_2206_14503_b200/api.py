@@ -109,13 +109,13 @@ class Compositor:
     """One libvdi context (vdi_composite_init ... vdi_composite_destroy)."""
 
     def __init__(self, width, height, k_in, k_out, n_pes, n_ranks=1, rank=0, max_iters=16, gamma_max=2.0,
-                 flags=0, unique_id: bytes | None = None, stream: torch.cuda.Stream | None = None):
+                 flags=0, unique_id: bytes | None = None, stream: torch.cuda.Stream | None = None, root=0):
         self.lib = L.lib()
         self.width, self.height, self.k_in, self.k_out, self.n_pes = width, height, k_in, k_out, n_pes
-        self.n_ranks, self.rank = n_ranks, rank
+        self.n_ranks, self.rank, self.root = n_ranks, rank, root
         self.stream = stream if stream is not None else torch.cuda.current_stream()
         self._uid = (C.c_uint8 * 128).from_buffer_copy(unique_id) if unique_id else None
-        cfg = L.vdi_config(width, height, k_in, k_out, n_pes, n_ranks, rank, max_iters, gamma_max, flags,
+        cfg = L.vdi_config(width, height, k_in, k_out, n_pes, n_ranks, rank, root, max_iters, gamma_max, flags,
                            C.cast(self._uid, C.c_void_p) if self._uid is not None else None,
                            self.stream.cuda_stream)
         h = C.c_void_p()
@@ -180,7 +180,7 @@ class Compositor:
         return strip
 
     def gather(self, strip: FullVDI, image: FullVDI | None):
-        """vdi_gather: strips -> rank 0 (image ignored on other ranks)."""
+        """vdi_gather: strips -> the root rank (image ignored on other ranks)."""
         sv = strip.view()
         iv = image.view() if image is not None else None
         L.check(self.lib.vdi_gather(self.ctx, C.byref(sv), C.byref(iv) if iv is not None else None), "vdi_gather")

@@ -276,6 +276,7 @@ vdi_status vdi_composite_init(const vdi_config* cfg, vdi_ctx** out) {
   if (cfg->n_pes < 1 || cfg->n_pes > VDI_MAX_SRC)
     return fail(VDI_ERR_INVALID_ARG, "n_pes must be in 1..%d", VDI_MAX_SRC);
   if (cfg->n_ranks < 1 || cfg->rank >= cfg->n_ranks) return fail(VDI_ERR_INVALID_ARG, "bad rank/n_ranks");
+  if (cfg->root >= cfg->n_ranks) return fail(VDI_ERR_INVALID_ARG, "root %u >= n_ranks %u", cfg->root, cfg->n_ranks);
   if (cfg->n_ranks > cfg->height) return fail(VDI_ERR_INVALID_ARG, "more ranks than image rows");
   if (cfg->n_ranks > 1 && !cfg->nccl_unique_id) return fail(VDI_ERR_INVALID_ARG, "nccl_unique_id required");
   if ((uint64_t)cfg->width * cfg->height > (1ull << 31)) return fail(VDI_ERR_INVALID_ARG, "image too large");
@@ -755,7 +756,8 @@ vdi_status vdi_gather(vdi_ctx* ctx, const vdi_full_view* strip, vdi_full_view* i
     return fail(VDI_ERR_INVALID_ARG, "strip is NULL");
   if (strip->row_begin != ctx->row0 || strip->row_end != ctx->row1)
     return fail(VDI_ERR_CAPACITY, "strip rows do not match this rank");
-  const bool root = me == 0;
+  const uint32_t R = cf.root;
+  const bool root = me == R;
   if (root && (!image || !image->count || !image->depth || !image->rgba || image->row_begin != 0 ||
                image->row_end != cf.height))
     return fail(VDI_ERR_INVALID_ARG, "root image_out must cover rows [0, H)");
@@ -807,27 +809,33 @@ vdi_status vdi_gather(vdi_ctx* ctx, const vdi_full_view* strip, vdi_full_view* i
                                    reinterpret_cast<const float4*>(strip->rgba), (uint32_t)Pg, (int)k,
                                    ctx->g_base.as<uint32_t>(), dd2, dc4, st, &launches));
       NCCL_TRY(ctx, ncclGroupStart());
-      NCCL_TRY(ctx, ncclSend(strip->count, Pg, ncclUint8, 0, ctx->comm, st));
+      NCCL_TRY(ctx, ncclSend(strip->count, Pg, ncclUint8, (int)R, ctx->comm, st));
       if (T) {
-        NCCL_TRY(ctx, ncclSend(dd2, T * 2, ncclFloat32, 0, ctx->comm, st));
-        NCCL_TRY(ctx, ncclSend(dc4, T * 4, ncclFloat32, 0, ctx->comm, st));
+        NCCL_TRY(ctx, ncclSend(dd2, T * 2, ncclFloat32, (int)R, ctx->comm, st));
+        NCCL_TRY(ctx, ncclSend(dc4, T * 4, ncclFloat32, (int)R, ctx->comm, st));
       }
       NCCL_TRY(ctx, ncclGroupEnd());
     } else {
-      const uint32_t r1 = strip_row(cf.height, G, 1);
-      const size_t Prem = (size_t)(cf.height - r1) * W;
+      // receive every other strip: counts at their image rows (the root's own
+      // rows stay unused), payloads concatenated in rank order
+      const size_t Pimg = (size_t)cf.height * W;
       uint64_t Trem = 0;
-      for (uint32_t g = 1; g < G; ++g) Trem += tot[g];
-      CUDA_TRY(ctx, ctx->g_rcount.grow(Prem + 64));
+      for (uint32_t g = 0; g < G; ++g)
+        if (g != R) Trem += tot[g];
+      CUDA_TRY(ctx, ctx->g_rcount.grow(Pimg + 64));
       CUDA_TRY(ctx, ctx->g_rpay.grow(std::max<uint64_t>(Trem, 1) * 24 + 64));
       float4* rc4 = ctx->g_rpay.as<float4>();
       float2* rd2 = reinterpret_cast<float2*>(rc4 + std::max<uint64_t>(Trem, 1));
       uint8_t* rcnt = ctx->g_rcount.as<uint8_t>();
       NCCL_TRY(ctx, ncclGroupStart());
-      uint64_t off = 0;
-      for (uint32_t g = 1; g < G; ++g) {
+      uint64_t off = 0, off_after = 0;
+      for (uint32_t g = 0; g < G; ++g) {
+        if (g == R) {
+          off_after = off;
+          continue;
+        }
         const uint32_t a = strip_row(cf.height, G, g), b = strip_row(cf.height, G, g + 1);
-        NCCL_TRY(ctx, ncclRecv(rcnt + (size_t)(a - r1) * W, (size_t)(b - a) * W, ncclUint8, (int)g, ctx->comm, st));
+        NCCL_TRY(ctx, ncclRecv(rcnt + (size_t)a * W, (size_t)(b - a) * W, ncclUint8, (int)g, ctx->comm, st));
         if (tot[g]) {
           NCCL_TRY(ctx, ncclRecv(rd2 + off, tot[g] * 2, ncclFloat32, (int)g, ctx->comm, st));
           NCCL_TRY(ctx, ncclRecv(rc4 + off, tot[g] * 4, ncclFloat32, (int)g, ctx->comm, st));
@@ -835,45 +843,55 @@ vdi_status vdi_gather(vdi_ctx* ctx, const vdi_full_view* strip, vdi_full_view* i
         off += tot[g];
       }
       NCCL_TRY(ctx, ncclGroupEnd());
-      // inflate rows [r1, H) of the image: one pass-through launch over the
-      // received (already depth-ordered, m <= k_out) lists
-      MergeParams mi{};
-      mi.n_src = 1;
-      mi.k_out = (int)k;
-      mi.max_iters = (int)cf.max_iters;
-      mi.gamma_max = cf.gamma_max;
-      mi.P = (uint32_t)Prem;
-      mi.n_groups = (uint32_t)((Prem + 31) / 32);
-      mi.g_begin = 0;
-      mi.g_end = mi.n_groups;
-      mi.src[0] = SrcDesc{rcnt, rd2, rc4};
       CUDA_TRY(ctx, ctx->g_misc.grow(sizeof(DevCounters) + 256));
       DevCounters* gc = ctx->g_misc.as<DevCounters>();
       CUDA_TRY(ctx, cudaMemsetAsync(gc, 0, sizeof(DevCounters), st));
-      CUDA_TRY(ctx, launch_scan(mi, ctx->g_sum.as<uint32_t>(), ctx->g_base.as<uint32_t>(), st, &launches));
-      mi.group_base = ctx->g_base.as<uint32_t>();
-      mi.out_count = image->count + (size_t)r1 * W;
-      mi.out_depth = reinterpret_cast<float2*>(image->depth) + (size_t)r1 * W * k;
-      mi.out_rgba = reinterpret_cast<float4*>(image->rgba) + (size_t)r1 * W * k;
-      for (int b = 0; b < VDI_N_BUCKETS; ++b) mi.wl[b] = reinterpret_cast<uint32_t*>(gc);  // never written: wl_cap = 0
-      mi.wl_count = gc->wl_count[0];
-      mi.wl_cap = 0;
-      mi.scratch_used = &gc->scratch_used;
-      mi.records_in = &gc->records_in;
-      mi.fallback_groups = &gc->fallback_groups;
-      mi.err = &gc->err;
-      CUDA_TRY(ctx, launch_fast(mi, st, &launches));
-      CUDA_TRY(ctx, copy_strip(0, strip));
+      // inflate the received rows (already depth-ordered, m <= k_out): one
+      // pass-through launch per contiguous row range, [0, root rows) and
+      // [after root rows, H)
+      auto inflate = [&](uint32_t ra, uint32_t rb, uint64_t poff) -> vdi_status {
+        const size_t Pr = (size_t)(rb - ra) * W;
+        if (!Pr) return VDI_OK;
+        MergeParams mi{};
+        mi.n_src = 1;
+        mi.k_out = (int)k;
+        mi.max_iters = (int)cf.max_iters;
+        mi.gamma_max = cf.gamma_max;
+        mi.P = (uint32_t)Pr;
+        mi.n_groups = (uint32_t)((Pr + 31) / 32);
+        mi.g_begin = 0;
+        mi.g_end = mi.n_groups;
+        mi.src[0] = SrcDesc{rcnt + (size_t)ra * W, rd2 + poff, rc4 + poff};
+        CUDA_TRY(ctx, launch_scan(mi, ctx->g_sum.as<uint32_t>(), ctx->g_base.as<uint32_t>(), st, &launches));
+        mi.group_base = ctx->g_base.as<uint32_t>();
+        mi.out_count = image->count + (size_t)ra * W;
+        mi.out_depth = reinterpret_cast<float2*>(image->depth) + (size_t)ra * W * k;
+        mi.out_rgba = reinterpret_cast<float4*>(image->rgba) + (size_t)ra * W * k;
+        for (int b = 0; b < VDI_N_BUCKETS; ++b) mi.wl[b] = reinterpret_cast<uint32_t*>(gc);  // never written: wl_cap = 0
+        mi.wl_count = gc->wl_count[0];
+        mi.wl_cap = 0;
+        mi.scratch_used = &gc->scratch_used;
+        mi.records_in = &gc->records_in;
+        mi.fallback_groups = &gc->fallback_groups;
+        mi.err = &gc->err;
+        CUDA_TRY(ctx, launch_fast(mi, st, &launches));
+        return VDI_OK;
+      };
+      if (vdi_status s = inflate(0, ctx->row0, 0)) return s;
+      if (vdi_status s = inflate(ctx->row1, cf.height, off_after)) return s;
+      CUDA_TRY(ctx, copy_strip(ctx->row0, strip));
     }
     ctx->last.bytes_gather = 0;
-    for (uint32_t g = 1; g < G; ++g)
-      ctx->last.bytes_gather += (uint64_t)(strip_row(cf.height, G, g + 1) - strip_row(cf.height, G, g)) * W + 24 * tot[g];
+    for (uint32_t g = 0; g < G; ++g)
+      if (g != R)
+        ctx->last.bytes_gather += (uint64_t)(strip_row(cf.height, G, g + 1) - strip_row(cf.height, G, g)) * W + 24 * tot[g];
     ctx->last.kernel_launches += (uint32_t)launches;
   } else {
     // MPI_Gather of the full-representation strips as grouped send/recv
     NCCL_TRY(ctx, ncclGroupStart());
     if (root) {
-      for (uint32_t g = 1; g < G; ++g) {
+      for (uint32_t g = 0; g < G; ++g) {
+        if (g == R) continue;
         const uint32_t r0 = strip_row(cf.height, G, g), r1 = strip_row(cf.height, G, g + 1);
         const size_t P = (size_t)(r1 - r0) * W, o = (size_t)r0 * W;
         NCCL_TRY(ctx, ncclRecv(image->count + o, P, ncclUint8, (int)g, ctx->comm, st));
@@ -882,13 +900,14 @@ vdi_status vdi_gather(vdi_ctx* ctx, const vdi_full_view* strip, vdi_full_view* i
       }
     } else {
       const size_t P = ctx->P;
-      NCCL_TRY(ctx, ncclSend(strip->count, P, ncclUint8, 0, ctx->comm, st));
-      NCCL_TRY(ctx, ncclSend(strip->depth, P * k * 2, ncclFloat32, 0, ctx->comm, st));
-      NCCL_TRY(ctx, ncclSend(strip->rgba, P * k * 4, ncclFloat32, 0, ctx->comm, st));
+      NCCL_TRY(ctx, ncclSend(strip->count, P, ncclUint8, (int)R, ctx->comm, st));
+      NCCL_TRY(ctx, ncclSend(strip->depth, P * k * 2, ncclFloat32, (int)R, ctx->comm, st));
+      NCCL_TRY(ctx, ncclSend(strip->rgba, P * k * 4, ncclFloat32, (int)R, ctx->comm, st));
     }
     NCCL_TRY(ctx, ncclGroupEnd());
-    if (root) CUDA_TRY(ctx, copy_strip(0, strip));
-    ctx->last.bytes_gather = (uint64_t)(cf.height - strip_row(cf.height, G, 1)) * W * (1 + 24ull * k);
+    if (root) CUDA_TRY(ctx, copy_strip(ctx->row0, strip));
+    ctx->last.bytes_gather =
+        (uint64_t)(cf.height - (strip_row(cf.height, G, R + 1) - strip_row(cf.height, G, R))) * W * (1 + 24ull * k);
   }
   if (timing) {
     CUDA_TRY(ctx, cudaEventRecord(ctx->gev[1], st));

@@ -82,6 +82,25 @@ def main():
         torch.cuda.synchronize()
         variants[name] = im2
         c2.close()
+    # the gather onto another root (frames in flight are gathered round-robin,
+    # Q14): dense and full-representation gathers onto the last and a middle
+    # rank; the root ships its image to rank 0 for the comparison
+    for R in sorted({world - 1, world // 2}):
+        for name, fl in (("dense", 0), ("full", vdi._lib.VDI_FLAG_FULL_GATHER)):
+            u = [vdi.get_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(u, src=0)
+            c2 = vdi.Compositor(W, H, k_in, k_out, n, n_ranks=world, rank=rank, unique_id=u[0], flags=fl, root=R)
+            st2 = c2.empty_strip()
+            im2 = vdi.FullVDI.empty(W, 0, H, k_out) if rank in (R, 0) else None
+            c2.composite(local_pes, st2)
+            c2.gather(st2, im2 if rank == R else None)
+            torch.cuda.synchronize()
+            if R != 0:
+                for t_ in (im2.count, im2.depth, im2.rgba) if rank in (R, 0) else ():
+                    (dist.send if rank == R else dist.recv)(t_, R if rank == 0 else 0)
+            torch.cuda.synchronize()
+            variants[f"root{R}_{name}"] = im2
+            c2.close()
     torch.cuda.synchronize()
     ok = True
     res = {"world": world, "config": args.config, "bytes_sent_rank": cnt["bytes_sent"],

@@ -69,13 +69,13 @@ def test_init_rejects_bad_config(L):
     h = C.c_void_p()
 
     def cfg(**kw):
-        d = dict(width=64, height=64, k_in=4, k_out=4, n_pes=2, n_ranks=1, rank=0, max_iters=0, gamma_max=0.0,
+        d = dict(width=64, height=64, k_in=4, k_out=4, n_pes=2, n_ranks=1, rank=0, root=0, max_iters=0, gamma_max=0.0,
                  flags=0, nccl_unique_id=None, cuda_stream=None)
         d.update(kw)
         return L.vdi_config(**d)
 
     for bad in (dict(k_out=0), dict(k_in=256), dict(n_pes=0), dict(n_pes=65), dict(rank=1),
-                dict(n_ranks=2, rank=1), dict(width=0), dict(n_ranks=100, height=64)):
+                dict(n_ranks=2, rank=1), dict(root=1), dict(width=0), dict(n_ranks=100, height=64)):
         c = cfg(**bad)
         assert lib.vdi_composite_init(C.byref(c), C.byref(h)) == 1, bad  # VDI_ERR_INVALID_ARG
         assert lib.vdi_last_error(None)
