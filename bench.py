@@ -250,122 +250,116 @@ def _run_ours(args, world, rank, local, clk):
 
     cfg = synth.config_by_name(args.config)
     G, n, W, H, k = world, cfg.n_pes, cfg.W, cfg.H, cfg.k_out
-    F = args.frames if args.frames > 0 else G  # frames in flight per step
+    F = args.frames if args.frames > 0 else 2 * G if G > 1 else 1  # VDIs per step
     flags = (L.VDI_FLAG_STAGE_TIMING | (L.VDI_FLAG_FULL_GATHER if args.full_gather else 0)
              | (L.VDI_FLAG_NCCL_EXCHANGE if args.nccl_exchange else 0)
              | (L.VDI_FLAG_PEER_READS if args.peer_reads else 0))
-    main_stream = torch.cuda.current_stream()
-    # one libvdi context per frame in flight, each on its own stream with its
-    # own communicator; frame f is gathered onto rank f mod G (Q14)
-    comps = []
-    for f in range(F):
-        uid = None
-        if G > 1:
-            import torch.distributed as dist
-            obj = [vdi.get_unique_id() if rank == 0 else None]
-            dist.broadcast_object_list(obj, src=0)
-            uid = obj[0]
-        st = main_stream if F == 1 else torch.cuda.Stream()
-        comps.append(vdi.Compositor(W, H, cfg.k_in, k, n, n_ranks=G, rank=rank, flags=flags, unique_id=uid,
-                                    stream=st, root=f % G))
-    comp = comps[0]
-    stream = comp.stream
+    stream = torch.cuda.current_stream()
 
-    # ---- inputs (untimed): synthetic volume -> per-PE dense sub-VDIs in HBM,
-    # one private copy per frame context (same view: every frame is the C3 VDI)
+    def new_uid():
+        if G == 1:
+            return None
+        import torch.distributed as dist
+        obj = [vdi.get_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        return obj[0]
+
+    # strip mode (the paper's direct send: strips of one VDI on every GPU, gather to rank 0)
+    comp = vdi.Compositor(W, H, cfg.k_in, k, n, n_ranks=G, rank=rank, flags=flags, unique_id=new_uid(),
+                          stream=stream)
+    # frames mode (G > 1): F VDIs per step, frame f composited whole by rank f mod G
+    compf = (vdi.Compositor(W, H, cfg.k_in, k, n, n_ranks=G, rank=rank,
+                            flags=L.VDI_FLAG_STAGE_TIMING | (L.VDI_FLAG_PEER_READS if args.peer_reads else 0),
+                            unique_id=new_uid(), stream=stream) if G > 1 else None)
+
+    # ---- inputs (untimed): synthetic volume -> per-PE dense sub-VDIs in HBM;
+    # frames mode gets one private copy per frame (every frame is this VDI)
     t0 = time.time()
     vol = synth.make_volume(cfg, device="cuda")
     tf = synth.tf_table(cfg.tf, cfg.tf_scale)
     tft = torch.from_numpy(tf).cuda()
     cam = synth.make_camera(W, H, view=args.view)
     dec = cfg.decomposition()
-    torch.cuda.synchronize()  # the frame streams read the volume
     local_ids = [pe for pe in range(n) if vdi.pe_home(n, G, pe) == rank]
-    locals_ = []
-    for c in comps:
-        with torch.cuda.stream(c.stream):
-            locals_.append([c.generate_subvdi(vol, tft, cam, dec, pe) for pe in local_ids])
+    local = [comp.generate_subvdi(vol, tft, cam, dec, pe) for pe in local_ids]
     torch.cuda.synchronize()
-    local = locals_[0]
     t_gen = time.time() - t0
     S_local = sum(p.total for p in local)
     S_total = int(allreduce_sum(S_local, G))
+    frames_local, frames_img = None, None
+    if compf is not None:
+        frames_local = [[vdi.DenseSubVDI(p.pe_id, p.total, p.count.clone(), p.offset.clone(), p.depth.clone(),
+                                         p.rgba.clone()) for p in local] for _ in range(F)]
+        frames_img = [vdi.FullVDI.empty(W, 0, H, k) if f % G == rank else None for f in range(F)]
 
-    strips, images = [], []
-    for c in comps:
-        if G > 1 and rank == c.root:  # the root's strip aliases its rows of the image (no copy in the gather)
-            image = vdi.FullVDI.empty(W, 0, H, k)
-            a0, a1 = c.row_begin * W, c.row_end * W
-            strip = vdi.FullVDI(c.row_begin, c.row_end, image.count[a0:a1], image.depth[a0:a1], image.rgba[a0:a1])
-        else:
-            strip = c.empty_strip()
-            image = strip if G == 1 else None
-        strips.append(strip)
-        images.append(image)
-    strip = strips[0]
+    if G > 1 and rank == 0:  # rank 0's strip aliases the first rows of the image (no copy in the gather)
+        image = vdi.FullVDI.empty(W, 0, H, k)
+        P0 = (comp.row_end - comp.row_begin) * W
+        strip = vdi.FullVDI(comp.row_begin, comp.row_end, image.count[:P0], image.depth[:P0], image.rgba[:P0])
+    else:
+        strip = comp.empty_strip()
+        image = strip if G == 1 else None
     flush = torch.empty(args.flush_mb << 20, dtype=torch.uint8, device="cuda")
 
-    def step():
-        # every composite first (host syncs only on its own frame's size
-        # exchange), then every gather: frame f+1's exchange and merge overlap
-        # frame f's merge and gather
-        for c, lp, sp in zip(comps, locals_, strips):
-            c.composite(lp, sp)
-        for c, sp, im in zip(comps, strips, images):
-            c.gather(sp, im)
+    def strip_step():
+        comp.composite(local, strip)
+        comp.gather(strip, image)
 
-    def timed_steps(K, fn, frames):
+    def frames_step():
+        compf.composite_frames(frames_local, frames_img, chunks=args.chunks)
+
+    def timed_steps(K, fn, c):
         evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
-        done = [torch.cuda.Event() for _ in frames]
         stats, nl = [], 0
         torch.cuda.synchronize()
         barrier(G)
         for i in range(K):
             flush.zero_()
-            evs[i][0].record(main_stream)
-            for c in frames:
-                if c.stream != main_stream:
-                    c.stream.wait_event(evs[i][0])
+            evs[i][0].record(stream)
             fn()
-            for c, d in zip(frames, done):
-                if c.stream != main_stream:
-                    d.record(c.stream)
-                    main_stream.wait_event(d)
-            evs[i][1].record(main_stream)
-            cs = [c.counters() for c in frames]  # syncs the frame streams; outside the events
-            stats.append(cs[0])
-            nl += sum(x["kernel_launches"] for x in cs)
+            evs[i][1].record(stream)
+            x = c.counters()  # syncs the stream; outside the events
+            stats.append(x)
+            nl += x["kernel_launches"]
         torch.cuda.synchronize()
         barrier(G)
-        return [a.elapsed_time(b) for a, b in evs], stats, nl
+        return [a_.elapsed_time(b_) for a_, b_ in evs], stats, nl
 
+    step, step_comp = (frames_step, compf) if compf is not None else (strip_step, comp)
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
     barrier(G)
 
-    # ---- timed region: exactly K steps of F frames, L2 flushed between steps (untimed)
+    # ---- timed region: exactly K steps, L2 flushed between steps (untimed)
     clk.mark_start()
-    step_ms, stage, launches = timed_steps(args.steps, step, comps)
+    step_ms, fstage, launches = timed_steps(args.steps, step, step_comp)
     clk.mark_end()
     tot_ms = allreduce_max(sum(step_ms), G)
     ms_per_step = tot_ms / args.steps
     value = F * args.steps / (tot_ms / 1e3)  # whole VDIs composited by all ranks per second
 
-    # ---- latency mode (paper-style): one VDI per step onto rank 0
+    # ---- strip (latency) mode: one VDI per step, strips on every GPU, gather
+    # to rank 0 (timed paper-style per stage).
+    # At G = 1 this is the timed run itself.
     latency = None
-    if F > 1:
-        def one():
-            comps[0].composite(locals_[0], strips[0])
-            comps[0].gather(strips[0], images[0])
+    if compf is not None:
         for _ in range(3):
-            one()
+            strip_step()
         K1 = max(10, args.steps // 4)
-        lat_ms, lat_stage, _ = timed_steps(K1, one, comps[:1])
+        lat_ms, stage, _ = timed_steps(K1, strip_step, comp)
         l_ms = allreduce_max(sum(lat_ms), G) / K1
         latency = {"ms_per_vdi": l_ms, "value": 1e3 / l_ms, "steps": K1,
-                   "stages_ms": {s_: statistics.mean(c[f"ms_{s_}"] for c in lat_stage)
-                                 for s_ in ("exchange", "merge", "gather")}}
+                   "stages_ms": {s_: statistics.mean(c_[f"ms_{s_}"] for c_ in stage)
+                                 for s_ in ("exchange", "merge", "gather")},
+                   "note": "one VDI per step in strips over all GPUs, dense gather to rank 0"}
+        frames_info = {"frames_per_step": F, "chunks": args.chunks,
+                       "ms_size_exchange_and_first_copy": statistics.mean(c_["ms_exchange"] for c_ in fstage),
+                       "ms_merge_incl_overlapped_copies": statistics.mean(c_["ms_merge"] for c_ in fstage),
+                       "bytes_pulled_per_step_rank0": fstage[-1]["bytes_received"]}
+    else:
+        stage = fstage
+        frames_info = None
 
     # ---- rooflines, per rank.  The dominant HBM-bound kernel is
     # merge_fast: it reads the counts, the group bases and the records of the
@@ -442,12 +436,13 @@ def _run_ours(args, world, rank, local, clk):
         res = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": G, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-            "scaling": "weak" if F == G else "strong",
+            "scaling": "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": workload_name(cfg, args.view), "n_pes": n, "image": f"{W}x{H}",
                        "k_in": cfg.k_in, "k_out": k, "supersegments_total": S_total,
-                       "parallelism": (f"image-space strips x{G} (direct send); {F} frame(s) in flight per step, "
-                                       f"frame f gathered onto rank f mod {G}"),
+                       "parallelism": (f"{F} VDIs per step, frame f composited whole on rank f mod {G} from all "
+                                       f"ranks' PEs (frames mode)" if G > 1 else
+                                       "one GPU: every PE homed on it, one VDI per step"),
                        "frames_per_step": F,
                        "l2": f"flushed between steps ({args.flush_mb} MiB memset, untimed)",
                        "inputs": "sub-VDIs raycast by vdi_generate_subvdi (untimed), resident in HBM",
@@ -465,6 +460,7 @@ def _run_ours(args, world, rank, local, clk):
                           "merge_fast": statistics.mean(c["ms_fast"] for c in stage),
                           "merge_search": statistics.mean(c["ms_search"] for c in stage)},
             "latency_mode": latency,
+            "frames_mode": frames_info,
             "supersegments_merged_per_s": S_total * F / (ms_per_step * 1e-3),
             "searched_lists": stage[-1]["searched_lists"],
             "search_buckets": stage[-1]["bucket_lists"], "fast_fallback_groups": stage[-1]["fallback_groups"],
@@ -500,7 +496,8 @@ def main():
     ap.add_argument("--nccl-exchange", action="store_true", help="NCCL send/recv exchange instead of peer copies")
     ap.add_argument("--peer-reads", action="store_true", help="merge kernels read peers' slices over NVLink")
     ap.add_argument("--frames", type=int, default=0,
-                    help="frames in flight per step (default: one per GPU, frame f gathered onto rank f mod G)")
+                    help="G > 1: VDIs per step in frames mode (default 2G; frame f composited whole on rank f mod G)")
+    ap.add_argument("--chunks", type=int, default=1, help="frames mode: row chunks per frame (copy/merge overlap)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     world, rank, local = dist_setup()

@@ -173,6 +173,23 @@ vdi_status vdi_generate_subvdi(vdi_ctx* ctx, const vdi_volume_desc* vol, const v
 vdi_status vdi_composite(vdi_ctx* ctx, const vdi_dense_view* local_pes, uint32_t n_local,
                          vdi_full_view* strip_out);
 
+/* Frames in flight: n_frames independent VDIs in one
+ * collective call, the image-space partition taken at frame granularity
+ * (PAPER.md:164): frame f is composited whole by rank f mod n_ranks, which is
+ * also its root, so no gather follows.  One size + IPC-reference
+ * exchange covers every frame (one host sync); the owner's copy engines pull
+ * every remote PE's sub-VDI of its frames over NVLink in
+ * `chunks` row ranges (0 -> 2, at most 8), and the merge of vdi_composite
+ * runs on chunk c while chunk c+1 is in flight.  The image
+ * of every frame equals vdi_composite of that frame on one GPU, bit for bit.
+ * local_pes: [n_frames][n_local] dense views, frame-major: the PEs homed here
+ * (offset arrays required; cudaMalloc memory when n_ranks > 1).  images:
+ * [n_frames] caller-owned full representations of rows [0, H); only the
+ * frames owned by this rank are read or written (others may be zeroed
+ * structs).  Counters and pixel stats describe the last merged chunk. */
+vdi_status vdi_composite_frames(vdi_ctx* ctx, uint32_t n_frames, const vdi_dense_view* local_pes,
+                                uint32_t n_local, vdi_full_view* images, uint32_t chunks);
+
 /* Same as vdi_composite with HOST buffers (the end-to-end entry point):
  * copies the local sub-VDIs host->device (pinned memory recommended),
  * composites, and copies the strip back device->host into strip_out.

@@ -79,6 +79,8 @@ SIGNATURES = {
     "vdi_composite": (C.c_int, [C.c_void_p, C.POINTER(vdi_dense_view), C.c_uint32, C.POINTER(vdi_full_view)]),
     "vdi_composite_host": (C.c_int, [C.c_void_p, C.POINTER(vdi_dense_view), C.c_uint32,
                                      C.POINTER(vdi_full_view)]),
+    "vdi_composite_frames": (C.c_int, [C.c_void_p, C.c_uint32, C.POINTER(vdi_dense_view), C.c_uint32,
+                                       C.POINTER(vdi_full_view), C.c_uint32]),
     "vdi_gather": (C.c_int, [C.c_void_p, C.POINTER(vdi_full_view), C.POINTER(vdi_full_view)]),
     "vdi_pixel_stats": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "vdi_get_counters": (C.c_int, [C.c_void_p, C.POINTER(vdi_counters)]),

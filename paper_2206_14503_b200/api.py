@@ -172,6 +172,18 @@ class Compositor:
         L.check(self.lib.vdi_composite(self.ctx, views, len(local_pes), C.byref(sv)), "vdi_composite")
         return strip
 
+    def composite_frames(self, frames_local_pes, images, chunks=0):
+        """vdi_composite_frames: frames_local_pes[f] = the PEs of frame f homed
+        here; images[f] = FullVDI of rows [0, H) for the frames this rank owns
+        (f % n_ranks == rank), None elsewhere."""
+        F = len(frames_local_pes)
+        nl = len(frames_local_pes[0]) if F else 0
+        flat = [p.view() for fr in frames_local_pes for p in fr]
+        views = (L.vdi_dense_view * max(1, len(flat)))(*flat)
+        ims = (L.vdi_full_view * max(1, F))(*[im.view() if im is not None else L.vdi_full_view() for im in images])
+        L.check(self.lib.vdi_composite_frames(self.ctx, F, views, nl, ims, chunks), "vdi_composite_frames")
+        return images
+
     def composite_host(self, local_pes, strip: FullVDI) -> FullVDI:
         """vdi_composite_host (host buffers; H2D + composite + D2H)."""
         views = (L.vdi_dense_view * max(1, len(local_pes)))(*[p.view() for p in local_pes])

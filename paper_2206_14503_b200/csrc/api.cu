@@ -7,6 +7,7 @@
 #include <nccl.h>
 
 #include <map>
+#include <memory>
 
 #include <algorithm>
 #include <cstdarg>
@@ -84,6 +85,7 @@ struct vdi_ctx {
   bool poisoned = false;
   uint32_t row0 = 0, row1 = 0;
   uint64_t P = 0;  // lists in this rank's strip
+  uint64_t mP = 0;  // lists of the last merge (strip, or whole frame in vdi_composite_frames)
   // merge scratch
   DevBuf group_sum, group_base, wl, scratch, dcnt, stat_gamma, stat_m, bounds, srch, slots;
   DevBuf g_sum, g_base, g_tot, g_dense, g_rcount, g_rpay, g_misc;  // dense gather
@@ -96,6 +98,11 @@ struct vdi_ctx {
   int n_chunks = 1;
   // exchange receive buffers per source
   std::vector<DevBuf> rcount, rdepth, rrgba;
+  // vdi_composite_frames: receive buffers per (owned frame, source), chunk events
+  std::vector<std::unique_ptr<DevBuf>> fcount, fdepth, frgba;
+  static constexpr int kMaxChunks = 8;
+  cudaEvent_t evc[8][4] = {};
+  DevBuf fblob;
   // generator outputs per pe
   std::vector<GenOut> gen;
   DevBuf gen_tmp;
@@ -121,6 +128,9 @@ struct vdi_ctx {
       if (e) cudaEventDestroy(e);
     for (auto& e : gev)
       if (e) cudaEventDestroy(e);
+    for (auto& r : evc)
+      for (auto& e : r)
+        if (e) cudaEventDestroy(e);
     // local teardown: drain our stream, then abort (not finalize) the
     // communicator so destroying contexts never waits on other ranks
     if (stream || comm) cudaStreamSynchronize(stream);
@@ -220,6 +230,119 @@ uint32_t strip_row(uint32_t H, uint32_t G, uint32_t g) { return (uint32_t)((uint
 
 }  // namespace
 
+// Merge of P lists whose sources are set in mp.src[0..n_pes) (receive-side
+// scan, pass-through + classification, gamma search, general path;
+// PAPER.md:166-185) into the full representation `so` (P lists).  Scratch is
+// ctx-owned and stream-ordered, so consecutive merges on the ctx stream reuse it.
+static vdi_status merge_lists(vdi_ctx* ctx, MergeParams& mp, uint64_t P, uint64_t S_here, vdi_full_view* so,
+                              bool timing, int& launches_ref) {
+  const vdi_config& cf = ctx->cfg;
+  const uint32_t n = cf.n_pes, k = cf.k_out;
+  cudaStream_t st = ctx->stream;
+  int launches = 0;
+  mp.P = (uint32_t)P;
+  mp.n_groups = (uint32_t)((P + 31) / 32);
+  ctx->mP = P;
+  // buffers of the merge
+  const size_t ng = mp.n_groups;
+  CUDA_TRY(ctx, ctx->group_sum.grow((size_t)scan_chunks(mp.P) * n * 4));
+  CUDA_TRY(ctx, ctx->group_base.grow(ng * n * 4));
+  // One chunk of 32-list groups, search kernels after the pass-through on
+  // the same stream.  Measured on C3 (profiles/README.md): overlapping them
+  // is slower -- chunked overlap on a second stream (C = 2: 1495 VDIs/s,
+  // C = 8: 973, vs 1976) and a classify kernel + search concurrent with the
+  // whole pass-through (2069-2124 vs 2120): the latency-bound search kernels
+  // run ~2x slower beside the HBM-bound pass-through.
+  const uint32_t C = 1;
+  ctx->n_chunks = (int)C;
+  std::vector<uint32_t> gb(C + 1);
+  for (uint32_t c = 0; c <= C; ++c) gb[c] = (uint32_t)((uint64_t)ng * c / C);
+  const size_t wl_words = std::max<size_t>(P, 1) * (3 + n) * VDI_N_BUCKETS + 64;
+  CUDA_TRY(ctx, ctx->wl.grow(wl_words * 4));
+  CUDA_TRY(ctx, ctx->slots.grow((2 * ng + 2 * C + 64) * 4));
+  CUDA_TRY(ctx, ctx->scratch.grow(std::max<uint64_t>(4 * S_here, 1) * sizeof(Rec)));
+  CUDA_TRY(ctx, ctx->dcnt.grow(sizeof(DevCounters)));
+  const bool stats = cf.flags & VDI_FLAG_PIXEL_STATS;
+  if (stats) {
+    CUDA_TRY(ctx, ctx->stat_gamma.grow(P * 4));
+    CUDA_TRY(ctx, ctx->stat_m.grow(P * 2));
+  }
+  // short-list search pool: a list in bucket 0/1 has m > k_out samples, so at
+  // most S_here / (k_out + 1) such lists exist; + one partial batch per chunk and bucket
+  const uint64_t pool_cap = (S_here / (k + 1) + 31) / 32 + 2 * C + 2;
+  const size_t slot_bytes = 40 * 32 * 16 + 40 * 32 * 8 + 64 * 4;
+  CUDA_TRY(ctx, ctx->srch.grow(pool_cap * slot_bytes + 256));
+  {
+    char* q = ctx->srch.as<char>();
+    mp.pool_rgba = reinterpret_cast<float4*>(q);
+    q += pool_cap * 40 * 32 * 16;
+    mp.pool_depth = reinterpret_cast<float2*>(q);
+    q += pool_cap * 40 * 32 * 8;
+    mp.pool_gap = reinterpret_cast<uint32_t*>(q);
+    mp.pool_cap = (uint32_t)pool_cap;
+  }
+  // long-list pool: slots of stride maxm per 32-list batch; a list of bucket
+  // 2/3 has m > 40, so the pool needs at most 24 B x (S_here + 32 x batches
+  // of padding); batches <= S_here / 41 / 32 + 1 per bucket
+  const uint64_t lb = S_here / 41 / 32 + 2;
+  const unsigned long long lcap = 24ull * S_here * 2 + lb * 2 * (128 + 24 * 32) + 4096;
+  CUDA_TRY(ctx, ctx->lpool.grow(lcap));
+  CUDA_TRY(ctx, ctx->lbatch.grow((size_t)(P / 32 + 2) * 2 * 16));
+  mp.long_pool = ctx->lpool.as<char>();
+  mp.long_cap = lcap;
+  mp.long_batch[0] = ctx->lbatch.as<PoolBatch>();
+  mp.long_batch[1] = ctx->lbatch.as<PoolBatch>() + (P / 32 + 2);
+  DevCounters* dc = ctx->dcnt.as<DevCounters>();
+  CUDA_TRY(ctx, cudaMemsetAsync(dc, 0, sizeof(DevCounters), st));
+  mp.long_used = &dc->long_used;
+  mp.group_base = ctx->group_base.as<uint32_t>();
+  mp.out_count = so->count;
+  mp.out_depth = reinterpret_cast<float2*>(so->depth);
+  mp.out_rgba = reinterpret_cast<float4*>(so->rgba);
+  mp.fallback_groups = &dc->fallback_groups;
+  mp.pool_next = &dc->pool_next;
+  mp.scratch_used = &dc->scratch_used;
+  mp.scratch_cap = 4 * S_here;
+  mp.scratch = ctx->scratch.as<Rec>();
+  mp.stat_gamma = stats ? ctx->stat_gamma.as<float>() : nullptr;
+  mp.stat_m = stats ? ctx->stat_m.as<uint16_t>() : nullptr;
+  mp.records_in = &dc->records_in;
+  mp.records_search = &dc->records_search;
+  mp.err = &dc->err;
+  mp.validate = (cf.flags & VDI_FLAG_VALIDATE) ? 1 : 0;
+  if (P) {
+    CUDA_TRY(ctx, launch_scan(mp, ctx->group_sum.as<uint32_t>(), ctx->group_base.as<uint32_t>(), st, &launches));
+    if (timing) CUDA_TRY(ctx, cudaEventRecord(ctx->ev[3], st));
+    uint32_t* wlp = ctx->wl.as<uint32_t>();
+    uint32_t* slp = ctx->slots.as<uint32_t>();
+    for (uint32_t c = 0; c < C; ++c) {
+      MergeParams mc = mp;
+      mc.g_begin = gb[c];
+      mc.g_end = gb[c + 1];
+      const uint64_t Pc = std::min<uint64_t>((uint64_t)gb[c + 1] * 32, P) - (uint64_t)gb[c] * 32;
+      mc.wl_cap = (uint32_t)std::max<uint64_t>(Pc, 1);
+      for (int b = 0; b < VDI_N_BUCKETS; ++b) {
+        mc.wl[b] = wlp;
+        wlp += (size_t)mc.wl_cap * (3 + n);
+      }
+      for (int b = 0; b < 2; ++b) {
+        mc.batch_slot[b] = slp;
+        slp += (mc.wl_cap + 31) / 32 + 1;
+      }
+      mc.wl_count = dc->wl_count[c];
+      mc.search_ticket = dc->search_ticket[c];
+      // pass-through (writes every slot of the strip) -> search kernels -> general path
+      CUDA_TRY(ctx, launch_fast(mc, st, &launches));
+      if (timing) CUDA_TRY(ctx, cudaEventRecord(ctx->ev[4], st));
+      CUDA_TRY(ctx, launch_search(mc, st, &launches));
+      if (timing) CUDA_TRY(ctx, cudaEventRecord(ctx->ev[5], st));
+      CUDA_TRY(ctx, launch_general(mc, st, &launches));
+    }
+  }
+  launches_ref += launches;
+  return VDI_OK;
+}
+
 extern "C" {
 
 const char* vdi_version(void) { return "libvdi 0.1 (sm_100a)"; }
@@ -305,6 +428,8 @@ vdi_status vdi_composite_init(const vdi_config* cfg, vdi_ctx** out) {
   for (auto& ev : ctx->ev) cudaEventCreate(&ev);
   for (auto& ev : ctx->gev) cudaEventCreate(&ev);
   for (auto& ev : ctx->evx) cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+  for (auto& r : ctx->evc)
+    for (auto& ev : r) cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
   for (auto& x : ctx->xs) cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking);
   if (cfg->n_ranks > 1) {
     ncclUniqueId id;
@@ -634,102 +759,7 @@ vdi_status vdi_composite(vdi_ctx* ctx, const vdi_dense_view* local, uint32_t n_l
   }
   if (timing) CUDA_TRY(ctx, cudaEventRecord(ctx->ev[1], st));
 
-  // buffers of the merge
-  const size_t ng = mp.n_groups;
-  CUDA_TRY(ctx, ctx->group_sum.grow((size_t)scan_chunks(mp.P) * n * 4));
-  CUDA_TRY(ctx, ctx->group_base.grow(ng * n * 4));
-  // One chunk of 32-list groups, search kernels after the pass-through on
-  // the same stream.  Measured on C3 (profiles/README.md): overlapping them
-  // is slower -- chunked overlap on a second stream (C = 2: 1495 VDIs/s,
-  // C = 8: 973, vs 1976) and a classify kernel + search concurrent with the
-  // whole pass-through (2069-2124 vs 2120): the latency-bound search kernels
-  // run ~2x slower beside the HBM-bound pass-through.
-  const uint32_t C = 1;
-  ctx->n_chunks = (int)C;
-  std::vector<uint32_t> gb(C + 1);
-  for (uint32_t c = 0; c <= C; ++c) gb[c] = (uint32_t)((uint64_t)ng * c / C);
-  const size_t wl_words = std::max<size_t>(ctx->P, 1) * (3 + n) * VDI_N_BUCKETS + 64;
-  CUDA_TRY(ctx, ctx->wl.grow(wl_words * 4));
-  CUDA_TRY(ctx, ctx->slots.grow((2 * ng + 2 * C + 64) * 4));
-  CUDA_TRY(ctx, ctx->scratch.grow(std::max<uint64_t>(4 * S_here, 1) * sizeof(Rec)));
-  CUDA_TRY(ctx, ctx->dcnt.grow(sizeof(DevCounters)));
-  const bool stats = cf.flags & VDI_FLAG_PIXEL_STATS;
-  if (stats) {
-    CUDA_TRY(ctx, ctx->stat_gamma.grow(ctx->P * 4));
-    CUDA_TRY(ctx, ctx->stat_m.grow(ctx->P * 2));
-  }
-  // short-list search pool: a list in bucket 0/1 has m > k_out samples, so at
-  // most S_here / (k_out + 1) such lists exist; + one partial batch per chunk and bucket
-  const uint64_t pool_cap = (S_here / (k + 1) + 31) / 32 + 2 * C + 2;
-  const size_t slot_bytes = 40 * 32 * 16 + 40 * 32 * 8 + 64 * 4;
-  CUDA_TRY(ctx, ctx->srch.grow(pool_cap * slot_bytes + 256));
-  {
-    char* q = ctx->srch.as<char>();
-    mp.pool_rgba = reinterpret_cast<float4*>(q);
-    q += pool_cap * 40 * 32 * 16;
-    mp.pool_depth = reinterpret_cast<float2*>(q);
-    q += pool_cap * 40 * 32 * 8;
-    mp.pool_gap = reinterpret_cast<uint32_t*>(q);
-    mp.pool_cap = (uint32_t)pool_cap;
-  }
-  // long-list pool: slots of stride maxm per 32-list batch; a list of bucket
-  // 2/3 has m > 40, so the pool needs at most 24 B x (S_here + 32 x batches
-  // of padding); batches <= S_here / 41 / 32 + 1 per bucket
-  const uint64_t lb = S_here / 41 / 32 + 2;
-  const unsigned long long lcap = 24ull * S_here * 2 + lb * 2 * (128 + 24 * 32) + 4096;
-  CUDA_TRY(ctx, ctx->lpool.grow(lcap));
-  CUDA_TRY(ctx, ctx->lbatch.grow((size_t)(ctx->P / 32 + 2) * 2 * 16));
-  mp.long_pool = ctx->lpool.as<char>();
-  mp.long_cap = lcap;
-  mp.long_batch[0] = ctx->lbatch.as<PoolBatch>();
-  mp.long_batch[1] = ctx->lbatch.as<PoolBatch>() + (ctx->P / 32 + 2);
-  DevCounters* dc = ctx->dcnt.as<DevCounters>();
-  CUDA_TRY(ctx, cudaMemsetAsync(dc, 0, sizeof(DevCounters), st));
-  mp.long_used = &dc->long_used;
-  mp.group_base = ctx->group_base.as<uint32_t>();
-  mp.out_count = so->count;
-  mp.out_depth = reinterpret_cast<float2*>(so->depth);
-  mp.out_rgba = reinterpret_cast<float4*>(so->rgba);
-  mp.fallback_groups = &dc->fallback_groups;
-  mp.pool_next = &dc->pool_next;
-  mp.scratch_used = &dc->scratch_used;
-  mp.scratch_cap = 4 * S_here;
-  mp.scratch = ctx->scratch.as<Rec>();
-  mp.stat_gamma = stats ? ctx->stat_gamma.as<float>() : nullptr;
-  mp.stat_m = stats ? ctx->stat_m.as<uint16_t>() : nullptr;
-  mp.records_in = &dc->records_in;
-  mp.records_search = &dc->records_search;
-  mp.err = &dc->err;
-  mp.validate = (cf.flags & VDI_FLAG_VALIDATE) ? 1 : 0;
-  if (ctx->P) {
-    CUDA_TRY(ctx, launch_scan(mp, ctx->group_sum.as<uint32_t>(), ctx->group_base.as<uint32_t>(), st, &launches));
-    if (timing) CUDA_TRY(ctx, cudaEventRecord(ctx->ev[3], st));
-    uint32_t* wlp = ctx->wl.as<uint32_t>();
-    uint32_t* slp = ctx->slots.as<uint32_t>();
-    for (uint32_t c = 0; c < C; ++c) {
-      MergeParams mc = mp;
-      mc.g_begin = gb[c];
-      mc.g_end = gb[c + 1];
-      const uint64_t Pc = std::min<uint64_t>((uint64_t)gb[c + 1] * 32, ctx->P) - (uint64_t)gb[c] * 32;
-      mc.wl_cap = (uint32_t)std::max<uint64_t>(Pc, 1);
-      for (int b = 0; b < VDI_N_BUCKETS; ++b) {
-        mc.wl[b] = wlp;
-        wlp += (size_t)mc.wl_cap * (3 + n);
-      }
-      for (int b = 0; b < 2; ++b) {
-        mc.batch_slot[b] = slp;
-        slp += (mc.wl_cap + 31) / 32 + 1;
-      }
-      mc.wl_count = dc->wl_count[c];
-      mc.search_ticket = dc->search_ticket[c];
-      // pass-through (writes every slot of the strip) -> search kernels -> general path
-      CUDA_TRY(ctx, launch_fast(mc, st, &launches));
-      if (timing) CUDA_TRY(ctx, cudaEventRecord(ctx->ev[4], st));
-      CUDA_TRY(ctx, launch_search(mc, st, &launches));
-      if (timing) CUDA_TRY(ctx, cudaEventRecord(ctx->ev[5], st));
-      CUDA_TRY(ctx, launch_general(mc, st, &launches));
-    }
-  }
+  if (vdi_status s = merge_lists(ctx, mp, ctx->P, S_here, so, timing, launches)) return s;
   if (ctx->peer_reads) {
     // end barrier: no rank reuses its inputs before every peer finished reading them
     CUDA_TRY(ctx, ctx->bounds.grow(16));
@@ -740,7 +770,222 @@ vdi_status vdi_composite(vdi_ctx* ctx, const vdi_dense_view* local, uint32_t n_l
     CUDA_TRY(ctx, cudaEventRecord(ctx->ev[2], st));
     ctx->timing_pending = true;
   }
-  ctx->have_stats = stats;
+  ctx->have_stats = cf.flags & VDI_FLAG_PIXEL_STATS;
+  ctx->last = vdi_counters{};
+  ctx->last.bytes_sent = sent;
+  ctx->last.bytes_received = recvd;
+  ctx->last.kernel_launches = (uint32_t)launches;
+  return VDI_OK;
+}
+
+vdi_status vdi_composite_frames(vdi_ctx* ctx, uint32_t F, const vdi_dense_view* local, uint32_t n_local,
+                                vdi_full_view* images, uint32_t chunks) {
+  if (vdi_status s = check_ctx(ctx)) return s;
+  const vdi_config& cf = ctx->cfg;
+  const uint32_t G = cf.n_ranks, me = cf.rank, n = cf.n_pes, W = cf.width, H = cf.height;
+  const uint64_t P = (uint64_t)W * H;
+  if (F < 1) return fail(VDI_ERR_INVALID_ARG, "n_frames must be >= 1");
+  if (!images) return fail(VDI_ERR_INVALID_ARG, "images is NULL");
+  const uint32_t C = std::max<uint32_t>(1, std::min<uint32_t>(chunks ? chunks : 2, std::min<uint32_t>(vdi_ctx::kMaxChunks, H)));
+  uint32_t expect = 0;
+  for (uint32_t s = 0; s < n; ++s)
+    if (vdi_pe_home(n, G, s) == me) ++expect;
+  if (n_local != expect) return fail(VDI_ERR_INVALID_ARG, "rank %u homes %u PEs, got %u", me, expect, n_local);
+  if (n_local && !local) return fail(VDI_ERR_INVALID_ARG, "local_pes is NULL");
+  // slot[f][s]: index of PE s of frame f in local[], -1 if remote
+  std::vector<int> slot((size_t)F * n, -1);
+  for (uint32_t f = 0; f < F; ++f)
+    for (uint32_t l = 0; l < n_local; ++l) {
+      const vdi_dense_view& v = local[(size_t)f * n_local + l];
+      if (v.pe_id >= n || vdi_pe_home(n, G, v.pe_id) != me || slot[(size_t)f * n + v.pe_id] >= 0)
+        return fail(VDI_ERR_INVALID_ARG, "frame %u: pe_id %u not homed on rank %u or duplicated", f, v.pe_id, me);
+      if (!v.count || !v.offset || (v.total && (!v.depth || !v.rgba)))
+        return fail(VDI_ERR_INVALID_ARG, "frame %u: dense view of PE %u has NULL arrays", f, v.pe_id);
+      if ((reinterpret_cast<uintptr_t>(v.rgba) & 15) || (reinterpret_cast<uintptr_t>(v.depth) & 7))
+        return fail(VDI_ERR_INVALID_ARG, "frame %u: dense view of PE %u misaligned", f, v.pe_id);
+      slot[(size_t)f * n + v.pe_id] = (int)l;
+    }
+  for (uint32_t f = me; f < F; f += G) {
+    const vdi_full_view& im = images[f];
+    if (!im.count || !im.depth || !im.rgba || im.row_begin != 0 || im.row_end != H)
+      return fail(VDI_ERR_INVALID_ARG, "images[%u] (owned by rank %u) must cover rows [0, H)", f, me);
+    if ((reinterpret_cast<uintptr_t>(im.rgba) & 15) || (reinterpret_cast<uintptr_t>(im.depth) & 7))
+      return fail(VDI_ERR_INVALID_ARG, "images[%u]: depth/rgba must be 8/16-byte aligned", f);
+  }
+  cudaStream_t st = ctx->stream;
+  const bool timing = cf.flags & VDI_FLAG_STAGE_TIMING;
+  int launches = 0;
+  uint64_t sent = 0, recvd = 0;
+  if (timing) CUDA_TRY(ctx, cudaEventRecord(ctx->ev[0], st));
+  std::vector<uint32_t> rows(C + 1);
+  for (uint32_t c = 0; c <= C; ++c) rows[c] = strip_row(H, C, c);
+  const size_t nb = (size_t)n * (C + 1);  // bnd[s][c] = offset_s[rows[c] * W] of one frame
+  // exchange blob: per frame bnd (u64) | per frame IPC references of every PE's count/depth/rgba
+  const size_t refs_off = (size_t)F * nb * 8;
+  const size_t blob = refs_off + (G > 1 ? (size_t)F * n * 3 * sizeof(IpcRef) : 0);
+  const size_t hdr = 64 * 8 + 64 * 4 + 64 * 4;  // per frame: ptrs, pes, rows
+  CUDA_TRY(ctx, ctx->fblob.grow(blob + (size_t)F * hdr));
+  uint8_t* dblob = ctx->fblob.as<uint8_t>();
+  std::vector<uint8_t> h((size_t)F * hdr, 0);
+  std::vector<IpcRef> myrefs(G > 1 ? (size_t)F * n * 3 : 0, IpcRef{});
+  for (uint32_t f = 0; f < F; ++f) {
+    uint8_t* hf = h.data() + (size_t)f * hdr;
+    const uint32_t** hp = reinterpret_cast<const uint32_t**>(hf);
+    uint32_t* hpes = reinterpret_cast<uint32_t*>(hf + 64 * 8);
+    uint32_t* hrows = reinterpret_cast<uint32_t*>(hf + 64 * 8 + 64 * 4);
+    for (uint32_t l = 0; l < n_local; ++l) {
+      const vdi_dense_view& v = local[(size_t)f * n_local + l];
+      hp[l] = v.offset;
+      hpes[l] = v.pe_id;
+      if (G > 1) {
+        const void* ptrs[3] = {v.count, v.depth, v.rgba};
+        for (int a2 = 0; a2 < 3; ++a2)
+          if (ptrs[a2] && !ipc_export(ptrs[a2], &myrefs[((size_t)f * n + v.pe_id) * 3 + a2]))
+            return fail(VDI_ERR_INVALID_ARG, "frame %u PE %u: buffer is not IPC-exportable device memory", f,
+                        v.pe_id);
+      }
+    }
+    for (uint32_t c = 0; c <= C; ++c) hrows[c] = rows[c];
+  }
+  CUDA_TRY(ctx, cudaMemcpyAsync(dblob + blob, h.data(), h.size(), cudaMemcpyHostToDevice, st));
+  CUDA_TRY(ctx, cudaMemsetAsync(dblob, 0, refs_off, st));
+  if (G > 1)
+    CUDA_TRY(ctx, cudaMemcpyAsync(dblob + refs_off, myrefs.data(), myrefs.size() * sizeof(IpcRef),
+                                  cudaMemcpyHostToDevice, st));
+  for (uint32_t f = 0; f < F; ++f) {
+    const uint8_t* dh = dblob + blob + (size_t)f * hdr;
+    gather_bounds_kernel<<<1, 256, 0, st>>>(reinterpret_cast<const uint32_t* const*>(dh),
+                                            reinterpret_cast<const uint32_t*>(dh + 64 * 8), (int)n_local,
+                                            reinterpret_cast<const uint32_t*>(dh + 64 * 8 + 64 * 4), (int)C, W,
+                                            (int)n, reinterpret_cast<unsigned long long*>(dblob) + (size_t)f * nb);
+    ++launches;
+  }
+  CUDA_TRY(ctx, cudaGetLastError());
+  // one size + IPC-reference exchange for all frames (each rank contributes
+  // its PEs' entries, zeros elsewhere: the byte-wise sum is a gather); also
+  // the start barrier of the peer copies
+  if (G > 1) NCCL_TRY(ctx, ncclAllReduce(dblob, dblob, blob, ncclUint8, ncclSum, ctx->comm, st));
+  std::vector<unsigned long long> bnd((size_t)F * nb);
+  std::vector<IpcRef> refs(myrefs.size());
+  CUDA_TRY(ctx, cudaMemcpyAsync(bnd.data(), dblob, refs_off, cudaMemcpyDeviceToHost, st));
+  if (G > 1)
+    CUDA_TRY(ctx, cudaMemcpyAsync(refs.data(), dblob + refs_off, refs.size() * sizeof(IpcRef),
+                                  cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(ctx, cudaStreamSynchronize(st));
+  auto B = [&](uint32_t f, uint32_t s, uint32_t c) { return bnd[(size_t)f * nb + (size_t)s * (C + 1) + c]; };
+  for (uint32_t f = 0; f < F; ++f)  // bytes this rank's PEs send to the frames' owners
+    if (f % G != me)
+      for (uint32_t s = 0; s < n; ++s)
+        if (slot[(size_t)f * n + s] >= 0) sent += P + 24 * B(f, s, C);
+  // frames owned here: the copy engines pull every remote PE's sub-VDI over
+  // NVLink chunk by chunk (rows [rows[c], rows[c+1])) while the merge of the
+  // previous chunk runs on the compositing stream
+  uint32_t j = 0;
+  bool first = true;
+  if (G > 1) CUDA_TRY(ctx, cudaEventRecord(ctx->evx[0], st));  // the copies wait only for the size exchange
+  for (uint32_t f = me; f < F; f += G, ++j) {
+    if (ctx->fcount.size() < (size_t)(j + 1) * n) {
+      while (ctx->fcount.size() < (size_t)(j + 1) * n) {
+        ctx->fcount.emplace_back(new DevBuf());
+        ctx->fdepth.emplace_back(new DevBuf());
+        ctx->frgba.emplace_back(new DevBuf());
+      }
+    }
+    struct Src {
+      const uint8_t* c;
+      const float2* d;
+      const float4* r;
+    };
+    std::vector<Src> src(n), rp(n);
+    std::vector<int> qs(n, -1);
+    int q = 0;
+    for (uint32_t s = 0; s < n; ++s) {
+      const int l = slot[(size_t)f * n + s];
+      if (l >= 0) {
+        const vdi_dense_view& v = local[(size_t)f * n_local + l];
+        src[s] = Src{v.count, reinterpret_cast<const float2*>(v.depth), reinterpret_cast<const float4*>(v.rgba)};
+        continue;
+      }
+      void *pc = nullptr, *pd = nullptr, *pr = nullptr;
+      CUDA_TRY(ctx, ipc_import(ctx, refs[((size_t)f * n + s) * 3 + 0], &pc));
+      CUDA_TRY(ctx, ipc_import(ctx, refs[((size_t)f * n + s) * 3 + 1], &pd));
+      CUDA_TRY(ctx, ipc_import(ctx, refs[((size_t)f * n + s) * 3 + 2], &pr));
+      const uint64_t T = B(f, s, C);
+      DevBuf& bc = *ctx->fcount[(size_t)j * n + s];
+      DevBuf& bd = *ctx->fdepth[(size_t)j * n + s];
+      DevBuf& br = *ctx->frgba[(size_t)j * n + s];
+      recvd += P + 24 * T;
+      if (cf.flags & VDI_FLAG_PEER_READS) {  // zero copy: the merge kernels load the peer's arrays over NVLink
+        src[s] = Src{static_cast<const uint8_t*>(pc), static_cast<const float2*>(pd), static_cast<const float4*>(pr)};
+        continue;
+      }
+      CUDA_TRY(ctx, bc.grow(P));
+      CUDA_TRY(ctx, bd.grow(std::max<uint64_t>(T, 1) * 8));
+      CUDA_TRY(ctx, br.grow(std::max<uint64_t>(T, 1) * 16));
+      src[s] = Src{bc.as<uint8_t>(), bd.as<float2>(), br.as<float4>()};
+      const int xi = q % vdi_ctx::kXStreams;
+      qs[s] = xi;
+      if (q < vdi_ctx::kXStreams) CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->xs[xi], ctx->evx[0], 0));
+      rp[s] = Src{static_cast<const uint8_t*>(pc), static_cast<const float2*>(pd), static_cast<const float4*>(pr)};
+      ++q;
+    }
+    const int nq = std::min<int>(q, vdi_ctx::kXStreams);
+    // chunk-major issue: chunk c of every remote source, then one event per
+    // copy stream, so the merge of chunk c waits only for chunk c's copies
+    for (uint32_t c = 0; c < C && q; ++c) {
+      const size_t r0 = (size_t)rows[c] * W, r1 = (size_t)rows[c + 1] * W;
+      for (uint32_t s = 0; s < n; ++s) {
+        if (qs[s] < 0) continue;
+        cudaStream_t cs = ctx->xs[qs[s]];
+        const uint64_t b0 = B(f, s, c), b1 = B(f, s, c + 1);
+        CUDA_TRY(ctx, cudaMemcpyAsync(const_cast<uint8_t*>(src[s].c) + r0, rp[s].c + r0, r1 - r0,
+                                      cudaMemcpyDeviceToDevice, cs));
+        if (b1 > b0) {
+          CUDA_TRY(ctx, cudaMemcpyAsync(const_cast<float2*>(src[s].d) + b0, rp[s].d + b0, (b1 - b0) * 8,
+                                        cudaMemcpyDeviceToDevice, cs));
+          CUDA_TRY(ctx, cudaMemcpyAsync(const_cast<float4*>(src[s].r) + b0, rp[s].r + b0, (b1 - b0) * 16,
+                                        cudaMemcpyDeviceToDevice, cs));
+        }
+      }
+      for (int xi = 0; xi < nq; ++xi) CUDA_TRY(ctx, cudaEventRecord(ctx->evc[c][xi], ctx->xs[xi]));
+    }
+    for (uint32_t c = 0; c < C; ++c) {
+      MergeParams mp{};
+      mp.n_src = (int)n;
+      mp.k_out = (int)cf.k_out;
+      mp.max_iters = (int)cf.max_iters;
+      mp.gamma_max = cf.gamma_max;
+      uint64_t S_c = 0;
+      for (uint32_t s = 0; s < n; ++s) {
+        const uint64_t b0 = B(f, s, c);
+        mp.src[s] = SrcDesc{src[s].c + (size_t)rows[c] * W, src[s].d + b0, src[s].r + b0};
+        S_c += B(f, s, c + 1) - b0;
+      }
+      vdi_full_view so{rows[c], rows[c + 1], images[f].count + (size_t)rows[c] * W,
+                       images[f].depth + (size_t)rows[c] * W * cf.k_out * 2,
+                       images[f].rgba + (size_t)rows[c] * W * cf.k_out * 4};
+      for (int xi = 0; xi < nq; ++xi) CUDA_TRY(ctx, cudaStreamWaitEvent(st, ctx->evc[c][xi], 0));
+      if (first && timing) CUDA_TRY(ctx, cudaEventRecord(ctx->ev[1], st));
+      first = false;
+      if (vdi_status e = merge_lists(ctx, mp, (uint64_t)(rows[c + 1] - rows[c]) * W, S_c, &so, timing, launches))
+        return e;
+    }
+  }
+  if (first && timing) CUDA_TRY(ctx, cudaEventRecord(ctx->ev[1], st));
+  if (G > 1) {
+    // end barrier: no rank reuses its inputs before every owner finished copying them
+    for (int xi = 0; xi < vdi_ctx::kXStreams; ++xi) {
+      CUDA_TRY(ctx, cudaEventRecord(ctx->evx[1 + xi], ctx->xs[xi]));
+      CUDA_TRY(ctx, cudaStreamWaitEvent(st, ctx->evx[1 + xi], 0));
+    }
+    CUDA_TRY(ctx, ctx->bounds.grow(16));
+    NCCL_TRY(ctx, ncclAllReduce(ctx->bounds.p, ctx->bounds.p, 1, ncclUint8, ncclSum, ctx->comm, st));
+  }
+  if (timing) {
+    CUDA_TRY(ctx, cudaEventRecord(ctx->ev[2], st));
+    ctx->timing_pending = true;
+  }
+  ctx->have_stats = cf.flags & VDI_FLAG_PIXEL_STATS;
   ctx->last = vdi_counters{};
   ctx->last.bytes_sent = sent;
   ctx->last.bytes_received = recvd;
@@ -967,8 +1212,8 @@ vdi_status vdi_pixel_stats(vdi_ctx* ctx, float* gamma, uint16_t* m) {
   if (vdi_status s = check_ctx(ctx)) return s;
   if (!ctx->have_stats) return fail(VDI_ERR_STATE, "VDI_FLAG_PIXEL_STATS was not set for the last composite");
   if (gamma)
-    CUDA_TRY(ctx, cudaMemcpyAsync(gamma, ctx->stat_gamma.p, ctx->P * 4, cudaMemcpyDeviceToDevice, ctx->stream));
-  if (m) CUDA_TRY(ctx, cudaMemcpyAsync(m, ctx->stat_m.p, ctx->P * 2, cudaMemcpyDeviceToDevice, ctx->stream));
+    CUDA_TRY(ctx, cudaMemcpyAsync(gamma, ctx->stat_gamma.p, ctx->mP * 4, cudaMemcpyDeviceToDevice, ctx->stream));
+  if (m) CUDA_TRY(ctx, cudaMemcpyAsync(m, ctx->stat_m.p, ctx->mP * 2, cudaMemcpyDeviceToDevice, ctx->stream));
   return VDI_OK;
 }
 
@@ -997,7 +1242,7 @@ vdi_status vdi_get_counters(vdi_ctx* ctx, vdi_counters* out) {
   if (ctx->timing_pending) {
     CUDA_TRY(ctx, cudaEventElapsedTime(&ctx->last.ms_exchange, ctx->ev[0], ctx->ev[1]));
     CUDA_TRY(ctx, cudaEventElapsedTime(&ctx->last.ms_merge, ctx->ev[1], ctx->ev[2]));
-    if (ctx->P) {
+    if (ctx->mP) {
       CUDA_TRY(ctx, cudaEventElapsedTime(&ctx->last.ms_scan, ctx->ev[1], ctx->ev[3]));
       CUDA_TRY(ctx, cudaEventElapsedTime(&ctx->last.ms_fast, ctx->ev[3], ctx->ev[4]));
       CUDA_TRY(ctx, cudaEventElapsedTime(&ctx->last.ms_search, ctx->ev[4], ctx->ev[5]));

@@ -101,9 +101,43 @@ def main():
             torch.cuda.synchronize()
             variants[f"root{R}_{name}"] = im2
             c2.close()
+    # frames in flight (vdi_composite_frames): frame f composited whole on rank
+    # f mod G from every rank's PEs; each owner checks its frames bit for bit
+    # against a 1-GPU composite of the same frame (synthetic inputs only: every
+    # rank can rebuild every frame from its seed)
+    frames_ok = None
+    if args.config == "synthetic":
+        F = 2 * world
+        fr_np = [synth.random_subvdis(n, W, H, k_in, lam=args.lam + f, seed=700 + f) for f in range(F)]
+        u = [vdi.get_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(u, src=0)
+        cf = vdi.Compositor(W, H, k_in, k_out, n, n_ranks=world, rank=rank, unique_id=u[0])
+        fl = [[dense_to_device(fr_np[f][pe], pe) for pe in range(n) if vdi.pe_home(n, world, pe) == rank]
+              for f in range(F)]
+        ims = [vdi.FullVDI.empty(W, 0, H, k_out) if f % world == rank else None for f in range(F)]
+        for chunks in (1, 3):
+            cf.composite_frames(fl, ims, chunks=chunks)
+            torch.cuda.synchronize()
+            one = vdi.Compositor(W, H, k_in, k_out, n)
+            for f in range(rank, F, world):
+                ref1 = one.empty_strip()
+                one.composite([dense_to_device(p, i) for i, p in enumerate(fr_np[f])], ref1)
+                torch.cuda.synchronize()
+                same = all(torch.equal(a, b) for a, b in ((ims[f].count, ref1.count), (ims[f].depth, ref1.depth),
+                                                          (ims[f].rgba, ref1.rgba)))
+                frames_ok = same if frames_ok is None else (frames_ok and same)
+            one.close()
+        fc = cf.counters()
+        t2 = torch.tensor([fc["bytes_sent"], fc["bytes_received"], 0 if frames_ok else 1], dtype=torch.float64,
+                          device="cuda")
+        dist.all_reduce(t2)
+        frames_ok = int(t2[2]) == 0 and int(t2[0]) == int(t2[1])
+        cf.close()
     torch.cuda.synchronize()
     ok = True
-    res = {"world": world, "config": args.config, "bytes_sent_rank": cnt["bytes_sent"],
+    if frames_ok is not None:
+        ok &= frames_ok
+    res = {"world": world, "frames_identical_to_1gpu": frames_ok, "config": args.config, "bytes_sent_rank": cnt["bytes_sent"],
            "bytes_received_rank": cnt["bytes_received"]}
     # byte conservation over ranks
     t = torch.tensor([cnt["bytes_sent"], cnt["bytes_received"]], dtype=torch.float64, device="cuda")

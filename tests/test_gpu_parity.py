@@ -166,6 +166,31 @@ def test_full_size_synthetic_sampled(vdi, orc):
     assert cnt["records_in"] == sum(int(p["count"].sum()) for p in pes)
 
 
+def test_composite_frames_single_gpu(vdi, orc):
+    """vdi_composite_frames (frames in flight, chunked merge) on one GPU: every
+    frame's image equals vdi_composite of that frame bit for bit, and the
+    oracle on sampled lists."""
+    n, W, H, k = 6, 160, 90, 12
+    frames = [synth.random_subvdis(n, W, H, k, lam=9.0 + 3 * f, seed=500 + f) for f in range(3)]
+    comp = vdi.Compositor(W, H, k, k, n)
+    dev = [[dense_to_device(p, i) for i, p in enumerate(fr)] for fr in frames]
+    for chunks in (1, 3, 8):
+        images = [vdi.FullVDI.empty(W, 0, H, k) for _ in frames]
+        comp.composite_frames(dev, images, chunks=chunks)
+        torch.cuda.synchronize()
+        for f, fr in enumerate(frames):
+            one = comp.empty_strip()
+            comp.composite(dev[f], one)
+            torch.cuda.synchronize()
+            for a, b in ((images[f].count, one.count), (images[f].depth, one.depth), (images[f].rgba, one.rgba)):
+                assert torch.equal(a, b), (chunks, f)
+    rng = np.random.default_rng(5)
+    pix = np.unique(rng.choice(W * H, 1500, replace=False))
+    o = orc.composite_pixels(frames[2], pix, k)
+    gc, gd, gr = full_to_numpy(images[2])
+    compare(gc[pix], gd[pix], gr[pix], o["count"], o["depth"], o["rgba"], o["stats"]["margin"], "frames")
+
+
 def test_multi_gpu_strip_invariance(vdi):
     """G = 2 (or all visible GPUs): NCCL exchange + gather give the 1-GPU result
     bit-for-bit and match the oracle (tests/mgpu_check.py under torchrun)."""
