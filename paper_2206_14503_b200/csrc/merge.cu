@@ -698,15 +698,19 @@ __global__ void __launch_bounds__(128) search_gather_kernel(MergeParams mp) {
   const int n = mp.n_src;
   const int tid = threadIdx.x;
   const uint32_t c0 = min(mp.wl_count[0], mp.wl_cap), c1 = min(mp.wl_count[1], mp.wl_cap);
-  const uint32_t c0r = (c0 + 31) & ~31u;  // bucket 1 starts at a warp boundary
-  const uint32_t tot = c0r + c1;
+  const uint32_t nb0 = (c0 + 31) / 32, nb1 = (c1 + 31) / 32;
   const uint32_t lane = threadIdx.x & 31;
   float2* my_d = sd + tid;
   uint8_t* my_p = sp + tid;
-  for (uint32_t v0 = blockIdx.x * blockDim.x; v0 < tot; v0 += gridDim.x * blockDim.x) {
-    const uint32_t v = v0 + threadIdx.x;
-    const int bucket = v < c0r ? 0 : 1;
-    const uint32_t i = bucket == 0 ? v : v - c0r;
+  // a warp claims one batch of 32 work-list entries at a time, the longer
+  // lists (bucket 1) first, so the last claims are the short ones
+  for (;;) {
+    uint32_t b = 0;
+    if (lane == 0) b = atomicAdd(&mp.search_ticket[1], 1u);
+    b = __shfl_sync(kFull, b, 0);
+    if (b >= nb0 + nb1) break;
+    const int bucket = b < nb1 ? 1 : 0;
+    const uint32_t i = (bucket == 1 ? b : b - nb1) * 32 + lane;
     const bool valid = i < (bucket == 0 ? c0 : c1);
     const uint32_t* ent = mp.wl[bucket] + (size_t)(valid ? i : 0) * (3 + n);
     const uint32_t p = valid ? ent[0] : 0u, m = valid ? ent[2] : 0u;
@@ -773,6 +777,10 @@ __global__ void __launch_bounds__(128) search_gather_kernel(MergeParams mp) {
             const uint32_t r = r0 + u;
             if (r < m) {
               bad |= cv[u].w == 0.f;  // Q23
+              // gap before sample r: flagged in the sign of alpha (alpha > 0
+              // for every stored sample), tested by the sweeps with one FSETP
+              const bool gp = r < 32 ? ((g0 >> r) & 1u) : ((g1 >> (r - 32)) & 1u);
+              if (gp) cv[u].w = -cv[u].w;
               orgba[r * 32] = cv[u];
               odep[r * 32] = my_d[(uint32_t)my_p[r * 128] * 128];
             }
@@ -807,10 +815,12 @@ __device__ __forceinline__ void sweep_batch(const MergeParams& mp, int bucket, u
     const bool bad = valid && gw0 == 0xffffffffu && gw1 == 0xffffffffu;  // sent to the general path
     const float4* col = mp.pool_rgba + (size_t)slot * 40 * 32 + lane;
     const float2* dcol = mp.pool_depth + (size_t)slot * 40 * 32 + lane;
+    // samples past m are NaN: D^2 = NaN never exceeds g^2 and their gap bits
+    // are 0, so they never split and the count sweeps need no "q < m" test
     float4 S[MS];
+    const float qnan = __int_as_float(0x7fc00000);
 #pragma unroll
-    for (int q = 0; q < MS; ++q) S[q] = (q < mi && !bad) ? col[q * 32] : make_float4(0.f, 0.f, 0.f, 0.f);
-    const uint32_t gapw[2] = {gw0, gw1};
+    for (int q = 0; q < MS; ++q) S[q] = (q < mi && !bad) ? col[q * 32] : make_float4(qnan, qnan, qnan, qnan);
     bool active = valid && !bad && mp.max_iters > 0;
     float lo = 0.f, hi = mp.gamma_max, best = mp.gamma_max;
     for (int it = 0; it < mp.max_iters; ++it) {
@@ -828,16 +838,17 @@ __device__ __forceinline__ void sweep_batch(const MergeParams& mp, int bucket, u
       for (int q = 0; q < MS; ++q) {
         if ((q & 7) == 0 && q > 0 && !__any_sync(kFull, active && q < mi && sc <= k)) break;
         const float4 sv = S[q];
-        const bool gap = (gapw[q >> 5] & (1u << (q & 31))) != 0u;
+        const bool gap = sv.w < 0.f;  // NaN padding: false
+        const float sa = fabsf(sv.w);
         const float n2 = fmaf(aa, aa, fmaf(ab, ab, fmaf(ag, ag, ar * ar)));  // dist2(acc, 0), Q8
-        const float d2 = dist2(ar, ag, ab, aa, sv.x, sv.y, sv.z, sv.w);
+        const float d2 = dist2(ar, ag, ab, aa, sv.x, sv.y, sv.z, sa);
         const bool st = (q == 0) | (gap & (n2 > g2)) | (d2 > g2);  // open before q is (q > 0)
         const float tr = 1.0f - aa;
         ar = st ? sv.x : fmaf(tr, sv.x, ar);
         ag = st ? sv.y : fmaf(tr, sv.y, ag);
         ab = st ? sv.z : fmaf(tr, sv.z, ab);
-        aa = st ? sv.w : fmaf(tr, sv.w, aa);
-        sc += (st && q < mi) ? 1 : 0;
+        aa = st ? sa : fmaf(tr, sa, aa);
+        sc += st ? 1 : 0;
       }
       if (active) {
         if (sc <= k) {
@@ -866,9 +877,10 @@ __device__ __forceinline__ void sweep_batch(const MergeParams& mp, int bucket, u
         if (q < mi) {
           const float4 sv = S[q];
           const float2 d = dq[q & 7];
-          const bool gap = ((gapw[q >> 5] >> (q & 31)) & 1u) != 0u;
+          const bool gap = sv.w < 0.f;
+          const float sa = fabsf(sv.w);
           const float n2 = fmaf(aa, aa, fmaf(ab, ab, fmaf(ag, ag, ar * ar)));
-          const float d2 = dist2(ar, ag, ab, aa, sv.x, sv.y, sv.z, sv.w);
+          const float d2 = dist2(ar, ag, ab, aa, sv.x, sv.y, sv.z, sa);
           const bool st = (q == 0) | (gap & (n2 > gg)) | (d2 > gg);
           if (st && q > 0 && c <= k) {  // close the open segment (ends at its last content sample)
             od[c - 1] = make_float2(tf, tb);
@@ -878,7 +890,7 @@ __device__ __forceinline__ void sweep_batch(const MergeParams& mp, int bucket, u
           ar = st ? sv.x : fmaf(tr, sv.x, ar);
           ag = st ? sv.y : fmaf(tr, sv.y, ag);
           ab = st ? sv.z : fmaf(tr, sv.z, ab);
-          aa = st ? sv.w : fmaf(tr, sv.w, aa);
+          aa = st ? sa : fmaf(tr, sa, aa);
           tf = st ? d.x : tf;
           tb = d.y;
           c += st ? 1 : 0;
@@ -898,9 +910,18 @@ __device__ __forceinline__ void sweep_batch(const MergeParams& mp, int bucket, u
 __global__ void __launch_bounds__(32, 8) search_sweep_kernel(MergeParams mp) {
   const uint32_t nb0 = (min(mp.wl_count[0], mp.wl_cap) + 31) / 32;
   const uint32_t nb1 = (min(mp.wl_count[1], mp.wl_cap) + 31) / 32;
-  for (uint32_t v = blockIdx.x; v < nb0 + nb1; v += gridDim.x) {
-    if (v < nb0) sweep_batch<32>(mp, 0, v);
-    else sweep_batch<40>(mp, 1, v - nb0);
+  // dynamic claims, longest lists first (bucket 1, then bucket 0): a warp
+  // takes the next batch when it finishes one, so the makespan is set by the
+  // total work, not by the batches a static stride happens to give a warp
+  for (;;) {
+    uint32_t v = 0;
+    if (threadIdx.x == 0) v = atomicAdd(&mp.search_ticket[0], 1u);
+    v = __shfl_sync(kFull, v, 0);
+    if (v >= nb0 + nb1) break;
+    // one instantiation for both buckets (half the code: the unrolled sweeps
+    // otherwise miss in the instruction cache); bucket-0 batches leave the
+    // sweeps at sample 32 through the every-8-samples warp vote
+    sweep_batch<40>(mp, v < nb1 ? 1 : 0, v < nb1 ? v : v - nb1);
   }
 }
 
