@@ -35,7 +35,7 @@ namespace cg = cooperative_groups;
 
 namespace vdi {
 
-static constexpr int kFastThreads = 128;  // 4 warps
+static constexpr int kFastThreads = 32;  // 1 warp per block: 13 resident per SM at k = 20 (smem-bound)
 static constexpr int kSlowThreads = 128;
 static constexpr unsigned kFull = 0xffffffffu;
 static constexpr int kChunk = 4096;       // lists per scan chunk (128 groups of 32)
