@@ -357,9 +357,34 @@ def _run_ours(args, world, rank, local, clk):
                        "ms_size_exchange_and_first_copy": statistics.mean(c_["ms_exchange"] for c_ in fstage),
                        "ms_merge_incl_overlapped_copies": statistics.mean(c_["ms_merge"] for c_ in fstage),
                        "bytes_pulled_per_step_rank0": fstage[-1]["bytes_received"]}
+        # the full-representation pipeline of Fig. 6: sub-VDIs in
+        # the full representation (converted untimed), fixed-size exchange,
+        # full-representation gather -- same image, the paper's A/B
+        compx = vdi.Compositor(W, H, cfg.k_in, k, n, n_ranks=G, rank=rank, unique_id=new_uid(), stream=stream,
+                               flags=L.VDI_FLAG_STAGE_TIMING | L.VDI_FLAG_FULL_GATHER)
+        fulls = [compx.dense_to_full(p) for p in local]
+        ids = [p.pe_id for p in local]
+
+        def full_step():
+            compx.composite_fullrep(fulls, ids, strip)
+            compx.gather(strip, image)
+        for _ in range(3):
+            full_step()
+        Kx = max(5, args.steps // 10)
+        x_ms, x_stage, _ = timed_steps(Kx, full_step, compx)
+        xm = allreduce_max(sum(x_ms), G) / Kx
+        full_rep = {"ms_per_vdi": xm, "value": 1e3 / xm, "steps": Kx,
+                    "stages_ms": {s_: statistics.mean(c_[f"ms_{s_}"] for c_ in x_stage)
+                                  for s_ in ("exchange", "merge", "gather")},
+                    "exchange_bytes_sent_rank0": x_stage[-1]["bytes_sent"],
+                    "note": "sub-VDIs in the full representation: fixed-size exchange, compositing from full "
+                            "slices, full-representation gather (Fig. 6 'full'); latency mode"}
+        compx.close()
+        del fulls
     else:
         stage = fstage
         frames_info = None
+        full_rep = None
 
     # ---- rooflines, per rank.  The dominant HBM-bound kernel is
     # merge_fast: it reads the counts, the group bases and the records of the
@@ -461,6 +486,7 @@ def _run_ours(args, world, rank, local, clk):
                           "merge_search": statistics.mean(c["ms_search"] for c in stage)},
             "latency_mode": latency,
             "frames_mode": frames_info,
+            "full_representation_mode": full_rep,
             "supersegments_merged_per_s": S_total * F / (ms_per_step * 1e-3),
             "searched_lists": stage[-1]["searched_lists"],
             "search_buckets": stage[-1]["bucket_lists"], "fast_fallback_groups": stage[-1]["fallback_groups"],

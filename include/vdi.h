@@ -190,6 +190,22 @@ vdi_status vdi_composite(vdi_ctx* ctx, const vdi_dense_view* local_pes, uint32_t
 vdi_status vdi_composite_frames(vdi_ctx* ctx, uint32_t n_frames, const vdi_dense_view* local_pes,
                                 uint32_t n_local, vdi_full_view* images, uint32_t chunks);
 
+/* The full-representation variant of the compositing (Fig. 6
+ * "full"): every local PE's sub-VDI is given in the full
+ * representation (rows [0, H), k_in slots per list, unused slots zero,
+ * PAPER.md:111), the strips are exchanged as fixed-size slices (NCCL
+ * send/recv, no size exchange: P_g (1 + 24 k_in) bytes per PE and strip),
+ * and each source is compacted to the dense layout on the receiver before
+ * the same merge as vdi_composite -- so the image is identical.  pe_ids[l]
+ * names the PE of local_pes[l].  Collective; synchronises the stream once. */
+vdi_status vdi_composite_fullrep(vdi_ctx* ctx, const vdi_full_view* local_pes, const uint32_t* pe_ids,
+                                 uint32_t n_local, vdi_full_view* strip_out);
+
+/* Dense -> full representation of one sub-VDI:
+ * out (rows [0, H), k_in slots per list) receives each list's records in its
+ * first count slots and zeros elsewhere.  Local (no collective). */
+vdi_status vdi_dense_to_full(vdi_ctx* ctx, const vdi_dense_view* in, vdi_full_view* out);
+
 /* Same as vdi_composite with HOST buffers (the end-to-end entry point):
  * copies the local sub-VDIs host->device (pinned memory recommended),
  * composites, and copies the strip back device->host into strip_out.

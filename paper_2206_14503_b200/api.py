@@ -184,6 +184,23 @@ class Compositor:
         L.check(self.lib.vdi_composite_frames(self.ctx, F, views, nl, ims, chunks), "vdi_composite_frames")
         return images
 
+    def dense_to_full(self, pe: DenseSubVDI) -> FullVDI:
+        """vdi_dense_to_full: the sub-VDI in the full representation (k_in slots)."""
+        out = FullVDI.empty(self.width, 0, self.height, self.k_in)
+        dv, fv = pe.view(), out.view()
+        L.check(self.lib.vdi_dense_to_full(self.ctx, C.byref(dv), C.byref(fv)), "vdi_dense_to_full")
+        return out
+
+    def composite_fullrep(self, local_full, pe_ids, strip: FullVDI) -> FullVDI:
+        """vdi_composite_fullrep: local_full[l] = full representation (rows
+        [0, H), k_in slots) of PE pe_ids[l]."""
+        views = (L.vdi_full_view * max(1, len(local_full)))(*[f.view() for f in local_full])
+        ids = (C.c_uint32 * max(1, len(pe_ids)))(*pe_ids)
+        sv = strip.view()
+        L.check(self.lib.vdi_composite_fullrep(self.ctx, views, C.cast(ids, C.c_void_p), len(local_full),
+                                               C.byref(sv)), "vdi_composite_fullrep")
+        return strip
+
     def composite_host(self, local_pes, strip: FullVDI) -> FullVDI:
         """vdi_composite_host (host buffers; H2D + composite + D2H)."""
         views = (L.vdi_dense_view * max(1, len(local_pes)))(*[p.view() for p in local_pes])

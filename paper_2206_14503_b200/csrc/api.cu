@@ -103,6 +103,9 @@ struct vdi_ctx {
   static constexpr int kMaxChunks = 8;
   cudaEvent_t evc[8][4] = {};
   DevBuf fblob;
+  // vdi_composite_fullrep: per-source dense scratch of the compaction + its scan
+  std::vector<std::unique_ptr<DevBuf>> xdense;
+  DevBuf xsum, xbase, xtot;
   // generator outputs per pe
   std::vector<GenOut> gen;
   DevBuf gen_tmp;
@@ -981,6 +984,178 @@ vdi_status vdi_composite_frames(vdi_ctx* ctx, uint32_t F, const vdi_dense_view* 
     CUDA_TRY(ctx, ctx->bounds.grow(16));
     NCCL_TRY(ctx, ncclAllReduce(ctx->bounds.p, ctx->bounds.p, 1, ncclUint8, ncclSum, ctx->comm, st));
   }
+  if (timing) {
+    CUDA_TRY(ctx, cudaEventRecord(ctx->ev[2], st));
+    ctx->timing_pending = true;
+  }
+  ctx->have_stats = cf.flags & VDI_FLAG_PIXEL_STATS;
+  ctx->last = vdi_counters{};
+  ctx->last.bytes_sent = sent;
+  ctx->last.bytes_received = recvd;
+  ctx->last.kernel_launches = (uint32_t)launches;
+  return VDI_OK;
+}
+
+vdi_status vdi_dense_to_full(vdi_ctx* ctx, const vdi_dense_view* in, vdi_full_view* out) {
+  if (vdi_status s = check_ctx(ctx)) return s;
+  const vdi_config& cf = ctx->cfg;
+  if (!in || !out || !in->count || (in->total && (!in->depth || !in->rgba)))
+    return fail(VDI_ERR_INVALID_ARG, "in/out is NULL");
+  if (!out->count || !out->depth || !out->rgba || out->row_begin != 0 || out->row_end != cf.height)
+    return fail(VDI_ERR_INVALID_ARG, "out must cover rows [0, H)");
+  if ((reinterpret_cast<uintptr_t>(out->rgba) & 15) || (reinterpret_cast<uintptr_t>(out->depth) & 7) ||
+      (reinterpret_cast<uintptr_t>(in->rgba) & 15) || (reinterpret_cast<uintptr_t>(in->depth) & 7))
+    return fail(VDI_ERR_INVALID_ARG, "depth/rgba misaligned");
+  cudaStream_t st = ctx->stream;
+  const size_t P = (size_t)cf.width * cf.height;
+  int launches = 0;
+  CUDA_TRY(ctx, ctx->g_sum.grow(((size_t)scan_chunks((uint32_t)P) + 8) * 4));
+  CUDA_TRY(ctx, ctx->g_base.grow((P / 32 + 8) * 4));
+  CUDA_TRY(ctx, ctx->g_misc.grow(sizeof(DevCounters) + 256));
+  DevCounters* gc = ctx->g_misc.as<DevCounters>();
+  CUDA_TRY(ctx, cudaMemsetAsync(gc, 0, sizeof(DevCounters), st));
+  MergeParams mi{};
+  mi.n_src = 1;
+  mi.k_out = (int)cf.k_in;  // k_in slots per list: every list passes through verbatim (m <= k_in)
+  mi.max_iters = (int)cf.max_iters;
+  mi.gamma_max = cf.gamma_max;
+  mi.P = (uint32_t)P;
+  mi.n_groups = (uint32_t)((P + 31) / 32);
+  mi.g_begin = 0;
+  mi.g_end = mi.n_groups;
+  mi.src[0] = SrcDesc{in->count, reinterpret_cast<const float2*>(in->depth), reinterpret_cast<const float4*>(in->rgba)};
+  CUDA_TRY(ctx, launch_scan(mi, ctx->g_sum.as<uint32_t>(), ctx->g_base.as<uint32_t>(), st, &launches));
+  mi.group_base = ctx->g_base.as<uint32_t>();
+  mi.out_count = out->count;
+  mi.out_depth = reinterpret_cast<float2*>(out->depth);
+  mi.out_rgba = reinterpret_cast<float4*>(out->rgba);
+  for (int b = 0; b < VDI_N_BUCKETS; ++b) mi.wl[b] = reinterpret_cast<uint32_t*>(gc);  // never written: wl_cap = 0
+  mi.wl_count = gc->wl_count[0];
+  mi.wl_cap = 0;
+  mi.scratch_used = &gc->scratch_used;
+  mi.records_in = &gc->records_in;
+  mi.fallback_groups = &gc->fallback_groups;
+  mi.err = &gc->err;
+  CUDA_TRY(ctx, launch_fast(mi, st, &launches));
+  return VDI_OK;
+}
+
+vdi_status vdi_composite_fullrep(vdi_ctx* ctx, const vdi_full_view* local, const uint32_t* pe_ids, uint32_t n_local,
+                                 vdi_full_view* so) {
+  if (vdi_status s = check_ctx(ctx)) return s;
+  const vdi_config& cf = ctx->cfg;
+  const uint32_t G = cf.n_ranks, me = cf.rank, n = cf.n_pes, W = cf.width, K = cf.k_in;
+  if (!so || !so->count || !so->depth || !so->rgba) return fail(VDI_ERR_INVALID_ARG, "strip_out is NULL");
+  if (so->row_begin != ctx->row0 || so->row_end != ctx->row1)
+    return fail(VDI_ERR_CAPACITY, "strip_out rows do not match this rank's strip");
+  std::vector<int> slot(n, -1);
+  uint32_t expect = 0;
+  for (uint32_t s = 0; s < n; ++s)
+    if (vdi_pe_home(n, G, s) == me) ++expect;
+  if (n_local != expect) return fail(VDI_ERR_INVALID_ARG, "rank %u homes %u PEs, got %u", me, expect, n_local);
+  if (n_local && (!local || !pe_ids)) return fail(VDI_ERR_INVALID_ARG, "local_pes / pe_ids is NULL");
+  for (uint32_t l = 0; l < n_local; ++l) {
+    const uint32_t pe = pe_ids[l];
+    if (pe >= n || vdi_pe_home(n, G, pe) != me || slot[pe] >= 0)
+      return fail(VDI_ERR_INVALID_ARG, "pe_id %u not homed on rank %u or duplicated", pe, me);
+    const vdi_full_view& v = local[l];
+    if (!v.count || !v.depth || !v.rgba || v.row_begin != 0 || v.row_end != cf.height)
+      return fail(VDI_ERR_INVALID_ARG, "full sub-VDI of PE %u must cover rows [0, H)", pe);
+    if ((reinterpret_cast<uintptr_t>(v.rgba) & 15) || (reinterpret_cast<uintptr_t>(v.depth) & 7))
+      return fail(VDI_ERR_INVALID_ARG, "full sub-VDI of PE %u misaligned", pe);
+    slot[pe] = (int)l;
+  }
+  cudaStream_t st = ctx->stream;
+  const bool timing = cf.flags & VDI_FLAG_STAGE_TIMING;
+  int launches = 0;
+  uint64_t sent = 0, recvd = 0;
+  const uint64_t Pg = ctx->P;
+  if (timing) CUDA_TRY(ctx, cudaEventRecord(ctx->ev[0], st));
+  // sources: this strip's rows of every PE's full representation (k_in slots per list)
+  std::vector<const uint8_t*> sc(n);
+  std::vector<const float*> sd(n), sr(n);
+  for (uint32_t s = 0; s < n; ++s) {
+    if (slot[s] < 0) continue;
+    const vdi_full_view& v = local[slot[s]];
+    const size_t o = (size_t)ctx->row0 * W;
+    sc[s] = v.count + o;
+    sd[s] = v.depth + o * K * 2;
+    sr[s] = v.rgba + o * K * 4;
+  }
+  if (G > 1) {
+    // fixed-size all-to-all of the full-representation slices (no size exchange)
+    for (uint32_t s = 0; s < n; ++s) {
+      if (slot[s] >= 0) continue;
+      CUDA_TRY(ctx, ctx->rcount[s].grow(Pg));
+      CUDA_TRY(ctx, ctx->rdepth[s].grow(Pg * K * 8));
+      CUDA_TRY(ctx, ctx->rrgba[s].grow(Pg * K * 16));
+      sc[s] = ctx->rcount[s].as<uint8_t>();
+      sd[s] = ctx->rdepth[s].as<float>();
+      sr[s] = ctx->rrgba[s].as<float>();
+    }
+    NCCL_TRY(ctx, ncclGroupStart());
+    for (uint32_t g = 0; g < G; ++g) {
+      if (g == me) continue;
+      const uint32_t a = strip_row(cf.height, G, g), b = strip_row(cf.height, G, g + 1);
+      const size_t P2 = (size_t)(b - a) * W, o = (size_t)a * W;
+      for (uint32_t s = 0; s < n; ++s) {
+        if (slot[s] < 0) continue;
+        const vdi_full_view& v = local[slot[s]];
+        NCCL_TRY(ctx, ncclSend(v.count + o, P2, ncclUint8, (int)g, ctx->comm, st));
+        NCCL_TRY(ctx, ncclSend(v.depth + o * K * 2, P2 * K * 2, ncclFloat32, (int)g, ctx->comm, st));
+        NCCL_TRY(ctx, ncclSend(v.rgba + o * K * 4, P2 * K * 4, ncclFloat32, (int)g, ctx->comm, st));
+        sent += P2 * (1 + 24ull * K);
+      }
+      for (uint32_t s = 0; s < n; ++s) {
+        if (vdi_pe_home(n, G, s) != g) continue;
+        NCCL_TRY(ctx, ncclRecv(ctx->rcount[s].p, Pg, ncclUint8, (int)g, ctx->comm, st));
+        NCCL_TRY(ctx, ncclRecv(ctx->rdepth[s].p, Pg * K * 2, ncclFloat32, (int)g, ctx->comm, st));
+        NCCL_TRY(ctx, ncclRecv(ctx->rrgba[s].p, Pg * K * 4, ncclFloat32, (int)g, ctx->comm, st));
+        recvd += Pg * (1 + 24ull * K);
+      }
+    }
+    NCCL_TRY(ctx, ncclGroupEnd());
+  }
+  if (timing) CUDA_TRY(ctx, cudaEventRecord(ctx->ev[1], st));
+  // compositing from the full representation: each source is compacted to
+  // the dense layout (scan of its counts, packed copy of its records), then
+  // merged like vdi_composite -- the same lists, so the same image
+  const size_t ng = (Pg + 31) / 32;
+  MergeParams ms{};
+  ms.n_src = (int)n;
+  ms.P = (uint32_t)Pg;
+  ms.n_groups = (uint32_t)ng;
+  for (uint32_t s = 0; s < n; ++s) ms.src[s].count = sc[s];
+  CUDA_TRY(ctx, ctx->xsum.grow(((size_t)scan_chunks(ms.P) * n + 8) * 4));
+  CUDA_TRY(ctx, ctx->xbase.grow((ng * n + 8) * 4));
+  CUDA_TRY(ctx, ctx->xtot.grow(64));
+  unsigned long long* dtot = ctx->xtot.as<unsigned long long>();
+  if (Pg) {
+    CUDA_TRY(ctx, launch_scan(ms, ctx->xsum.as<uint32_t>(), ctx->xbase.as<uint32_t>(), st, &launches));
+    CUDA_TRY(ctx, launch_total(ms, ctx->xsum.as<uint32_t>(), dtot, st, &launches));
+  } else {
+    CUDA_TRY(ctx, cudaMemsetAsync(dtot, 0, 8, st));
+  }
+  while (ctx->xdense.size() < n) ctx->xdense.emplace_back(new DevBuf());
+  MergeParams mp{};
+  mp.n_src = (int)n;
+  mp.k_out = (int)cf.k_out;
+  mp.max_iters = (int)cf.max_iters;
+  mp.gamma_max = cf.gamma_max;
+  for (uint32_t s = 0; s < n; ++s) {
+    DevBuf& xd = *ctx->xdense[s];
+    CUDA_TRY(ctx, xd.grow(std::max<uint64_t>(Pg * K, 1) * 24));
+    float4* dc = xd.as<float4>();
+    float2* dd = reinterpret_cast<float2*>(dc + std::max<uint64_t>(Pg * K, 1));
+    CUDA_TRY(ctx, launch_compact(sc[s], reinterpret_cast<const float2*>(sd[s]), reinterpret_cast<const float4*>(sr[s]),
+                                 (uint32_t)Pg, (int)K, ctx->xbase.as<uint32_t>() + (size_t)s * ng, dd, dc, st,
+                                 &launches));
+    mp.src[s] = SrcDesc{sc[s], dd, dc};
+  }
+  unsigned long long S_here = 0;
+  CUDA_TRY(ctx, cudaMemcpyAsync(&S_here, dtot, 8, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(ctx, cudaStreamSynchronize(st));
+  if (vdi_status e = merge_lists(ctx, mp, Pg, S_here, so, timing, launches)) return e;
   if (timing) {
     CUDA_TRY(ctx, cudaEventRecord(ctx->ev[2], st));
     ctx->timing_pending = true;

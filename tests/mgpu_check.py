@@ -82,6 +82,20 @@ def main():
         torch.cuda.synchronize()
         variants[name] = im2
         c2.close()
+    # compositing in the full representation (Fig. 6 "full"):
+    # fixed-size exchange of full-representation slices + full gather
+    u = [vdi.get_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(u, src=0)
+    c2 = vdi.Compositor(W, H, k_in, k_out, n, n_ranks=world, rank=rank, unique_id=u[0],
+                        flags=vdi._lib.VDI_FLAG_FULL_GATHER)
+    fulls = [c2.dense_to_full(p) for p in local_pes]
+    st2 = c2.empty_strip()
+    im2 = vdi.FullVDI.empty(W, 0, H, k_out) if rank == 0 else None
+    c2.composite_fullrep(fulls, [p.pe_id for p in local_pes], st2)
+    c2.gather(st2, im2)
+    torch.cuda.synchronize()
+    variants["fullrep_exchange"] = im2
+    c2.close()
     # the gather onto another root (frames in flight are gathered round-robin,
     # Q14): dense and full-representation gathers onto the last and a middle
     # rank; the root ships its image to rank 0 for the comparison

@@ -191,6 +191,38 @@ def test_composite_frames_single_gpu(vdi, orc):
     compare(gc[pix], gd[pix], gr[pix], o["count"], o["depth"], o["rgba"], o["stats"]["margin"], "frames")
 
 
+def test_dense_to_full_and_fullrep_composite(vdi, orc):
+    """vdi_dense_to_full gives the full representation of a sub-VDI (records in
+    the first count slots, zeros elsewhere); compositing from the
+    full representation (vdi_composite_fullrep, Fig. 6 "full") gives the same
+    image as the dense path."""
+    n, W, H, k_in, k_out = 5, 120, 70, 10, 8
+    pes = synth.random_subvdis(n, W, H, k_in, lam=8.0, seed=611)
+    comp = vdi.Compositor(W, H, k_in, k_out, n)
+    dev = [dense_to_device(p, i) for i, p in enumerate(pes)]
+    fulls = [comp.dense_to_full(d) for d in dev]
+    torch.cuda.synchronize()
+    for p, f in zip(pes, fulls):  # layout law, checked on the host from the seeded inputs
+        c = np.asarray(p["count"], np.int64)
+        off = np.concatenate([[0], np.cumsum(c)])
+        fc, fd, fr = full_to_numpy(f)
+        assert np.array_equal(fc, p["count"])
+        slot = np.arange(k_in)[None, :] < c[:, None]
+        idx = (off[:-1, None] + np.arange(k_in)[None, :])[slot]
+        assert np.array_equal(fd[slot], p["depth"][idx]) and np.array_equal(fr[slot], p["rgba"][idx])
+        assert not fd[~slot].any() and not fr[~slot].any()
+    a = comp.empty_strip()
+    comp.composite(dev, a)
+    b = comp.empty_strip()
+    comp.composite_fullrep(fulls, list(range(n)), b)
+    torch.cuda.synchronize()
+    for x, y in ((a.count, b.count), (a.depth, b.depth), (a.rgba, b.rgba)):
+        assert torch.equal(x, y)
+    ref = orc.composite(pes, W, H, 1, k_out)
+    gc, gd, gr = full_to_numpy(b)
+    compare(gc, gd, gr, ref["count"], ref["depth"], ref["rgba"], ref["stats"]["margin"], "fullrep")
+
+
 def test_multi_gpu_strip_invariance(vdi):
     """G = 2 (or all visible GPUs): NCCL exchange + gather give the 1-GPU result
     bit-for-bit and match the oracle (tests/mgpu_check.py under torchrun)."""
