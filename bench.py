@@ -253,7 +253,7 @@ def _run_ours(args, world, rank, local, clk):
     F = args.frames if args.frames > 0 else 2 * G if G > 1 else 1  # VDIs per step
     flags = (L.VDI_FLAG_STAGE_TIMING | (L.VDI_FLAG_FULL_GATHER if args.full_gather else 0)
              | (L.VDI_FLAG_NCCL_EXCHANGE if args.nccl_exchange else 0)
-             | (L.VDI_FLAG_PEER_READS if args.peer_reads else 0))
+             | (L.VDI_FLAG_PEER_READS if args.peer_reads else 0) | (L.VDI_FLAG_CE_COPIES if args.ce_copies else 0))
     stream = torch.cuda.current_stream()
 
     def new_uid():
@@ -269,7 +269,8 @@ def _run_ours(args, world, rank, local, clk):
                           stream=stream)
     # frames mode (G > 1): F VDIs per step, frame f composited whole by rank f mod G
     compf = (vdi.Compositor(W, H, cfg.k_in, k, n, n_ranks=G, rank=rank,
-                            flags=L.VDI_FLAG_STAGE_TIMING | (L.VDI_FLAG_PEER_READS if args.peer_reads else 0),
+                            flags=L.VDI_FLAG_STAGE_TIMING | (L.VDI_FLAG_PEER_READS if args.peer_reads else 0)
+                            | (L.VDI_FLAG_CE_COPIES if args.ce_copies else 0),
                             unique_id=new_uid(), stream=stream) if G > 1 else None)
 
     # ---- inputs (untimed): synthetic volume -> per-PE dense sub-VDIs in HBM;
@@ -494,7 +495,8 @@ def _run_ours(args, world, rank, local, clk):
             "gather": "full representation (PAPER.md:185)" if args.full_gather else "dense + root inflate (f1)",
             "exchange": ("NCCL send/recv" if args.nccl_exchange else
                          "peer reads: merge kernels load peers' sub-VDIs over NVLink (CUDA IPC)" if args.peer_reads else
-                         "peer copies: copy engines pull peers' strip slices over NVLink (CUDA IPC)"),
+                         "peer copies: copy engines pull peers' strip slices over NVLink (CUDA IPC)" if args.ce_copies else
+                         "peer copies: one SM kernel pulls peers' strip slices over NVLink (CUDA IPC)"),
             "gather_bytes_into_root": stage[-1]["bytes_gather"],
             "gpu_launches": launches,
             "clocks": clk.summary(),
@@ -523,6 +525,7 @@ def main():
     ap.add_argument("--peer-reads", action="store_true", help="merge kernels read peers' slices over NVLink")
     ap.add_argument("--frames", type=int, default=0,
                     help="G > 1: VDIs per step in frames mode (default 2G; frame f composited whole on rank f mod G)")
+    ap.add_argument("--ce-copies", action="store_true", help="exchange copies on the copy engines, not the SM copy kernel")
     ap.add_argument("--chunks", type=int, default=1, help="frames mode: row chunks per frame (copy/merge overlap)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup

@@ -43,6 +43,7 @@ typedef enum {
 #define VDI_FLAG_STAGE_TIMING 0x4u /* record CUDA-event times of the exchange / merge / gather stages */
 #define VDI_FLAG_PEER_READS 0x20u    /* peer exchange without copies: the merge kernels load peers' slices over NVLink */
 #define VDI_FLAG_NCCL_EXCHANGE 0x10u /* exchange through NCCL send/recv into receive buffers (default: copy engines pull peers' slices over NVLink from CUDA IPC mappings) */
+#define VDI_FLAG_CE_COPIES 0x40u     /* peer exchange copies on the copy engines (default: one SM kernel pulls the slices over NVLink -- strip mode, and the first owned frame of vdi_composite_frames; later frames always use the copy engines, overlapping the merges) */
 #define VDI_FLAG_FULL_GATHER 0x8u  /* gather the full representation as in PAPER.md:185 (default: dense gather + root inflate, identical image) */
 
 typedef struct vdi_ctx vdi_ctx; /* opaque */

@@ -20,6 +20,7 @@ VDI_FLAG_STAGE_TIMING = 0x4
 VDI_FLAG_FULL_GATHER = 0x8
 VDI_FLAG_NCCL_EXCHANGE = 0x10
 VDI_FLAG_PEER_READS = 0x20
+VDI_FLAG_CE_COPIES = 0x40
 
 
 class vdi_config(C.Structure):

@@ -106,6 +106,8 @@ struct vdi_ctx {
   // vdi_composite_fullrep: per-source dense scratch of the compaction + its scan
   std::vector<std::unique_ptr<DevBuf>> xdense;
   DevBuf xsum, xbase, xtot;
+  DevBuf segbuf;  // peer_copy_kernel segment tables (grow-only, stream-ordered)
+  size_t seg_used = 0;
   // generator outputs per pe
   std::vector<GenOut> gen;
   DevBuf gen_tmp;
@@ -162,6 +164,38 @@ struct vdi_ctx {
   } while (0)
 
 namespace {
+
+// SM-driven copy of many segments (peer slices over NVLink through CUDA IPC
+// mappings into local receive buffers): blockIdx.y = segment, 16/8/4/1-byte
+// vectors by the common alignment of the segment, 4 loads in flight per thread.
+struct CopySeg {
+  const void* src;
+  void* dst;
+  unsigned long long bytes;
+};
+
+template <class V>
+__device__ __forceinline__ void copy_vec(const V* __restrict__ s, V* __restrict__ d, unsigned long long n) {
+  const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+  unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+  for (; i + 3 * stride < n; i += 4 * stride) {
+    const V a = s[i], b = s[i + stride], c = s[i + 2 * stride], e = s[i + 3 * stride];
+    d[i] = a;
+    d[i + stride] = b;
+    d[i + 2 * stride] = c;
+    d[i + 3 * stride] = e;
+  }
+  for (; i < n; i += stride) d[i] = s[i];
+}
+
+__global__ void __launch_bounds__(256) peer_copy_kernel(const CopySeg* __restrict__ segs) {
+  const CopySeg sg = segs[blockIdx.y];
+  const uintptr_t al = reinterpret_cast<uintptr_t>(sg.src) | reinterpret_cast<uintptr_t>(sg.dst) | sg.bytes;
+  if (!(al & 15)) copy_vec(static_cast<const uint4*>(sg.src), static_cast<uint4*>(sg.dst), sg.bytes / 16);
+  else if (!(al & 7)) copy_vec(static_cast<const uint2*>(sg.src), static_cast<uint2*>(sg.dst), sg.bytes / 8);
+  else if (!(al & 3)) copy_vec(static_cast<const uint32_t*>(sg.src), static_cast<uint32_t*>(sg.dst), sg.bytes / 4);
+  else copy_vec(static_cast<const uint8_t*>(sg.src), static_cast<uint8_t*>(sg.dst), sg.bytes);
+}
 
 __global__ void gather_bounds_kernel(const uint32_t* const* offs, const uint32_t* pes, int n_local,
                                      const uint32_t* rows, int G, uint32_t W, int n_pes,
@@ -232,6 +266,32 @@ vdi_status check_ctx(vdi_ctx* ctx) {
 uint32_t strip_row(uint32_t H, uint32_t G, uint32_t g) { return (uint32_t)((uint64_t)g * H / G); }
 
 }  // namespace
+
+// Enqueue one peer_copy_kernel over `segs` on st.  The segment table goes
+// through a pinned-less H2D copy into a ctx-owned slice (stream-ordered).
+static int api_sm_count() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n < 1) n = 1;
+  }
+  return n;
+}
+
+static cudaError_t sm_copy(vdi_ctx* ctx, const std::vector<CopySeg>& segs, cudaStream_t st, int& launches) {
+  if (segs.empty()) return cudaSuccess;
+  const size_t bytes = segs.size() * sizeof(CopySeg);
+  cudaError_t e = ctx->segbuf.grow(std::max<size_t>(bytes, 64 * sizeof(CopySeg)));
+  if (e != cudaSuccess) return e;
+  if ((e = cudaMemcpyAsync(ctx->segbuf.p, segs.data(), bytes, cudaMemcpyHostToDevice, st)) != cudaSuccess) return e;
+  // ~4 blocks of 256 threads per SM over all segments
+  const unsigned gx = std::max<unsigned>(1u, (unsigned)(api_sm_count() * 4 / (int)segs.size()));
+  peer_copy_kernel<<<dim3(gx, (unsigned)segs.size()), 256, 0, st>>>(ctx->segbuf.as<CopySeg>());
+  ++launches;
+  return cudaGetLastError();
+}
 
 // Merge of P lists whose sources are set in mp.src[0..n_pes) (receive-side
 // scan, pass-through + classification, gamma search, general path;
@@ -671,6 +731,8 @@ vdi_status vdi_composite(vdi_ctx* ctx, const vdi_dense_view* local, uint32_t n_l
       // cudaMemcpyAsync on side streams) into local buffers; with
       // VDI_FLAG_PEER_READS the merge kernels read peer memory directly.
       const bool zero_copy = cf.flags & VDI_FLAG_PEER_READS;
+      const bool sm_copies = !(cf.flags & VDI_FLAG_CE_COPIES) && !zero_copy;
+      std::vector<CopySeg> segs;
       int q = 0;
       if (!zero_copy) CUDA_TRY(ctx, cudaEventRecord(ctx->evx[0], st));
       for (uint32_t s = 0; s < n; ++s) {
@@ -691,19 +753,28 @@ vdi_status vdi_composite(vdi_ctx* ctx, const vdi_dense_view* local, uint32_t n_l
           CUDA_TRY(ctx, ctx->rcount[s].grow(ctx->P));
           CUDA_TRY(ctx, ctx->rdepth[s].grow(std::max<uint64_t>(t, 1) * 8));
           CUDA_TRY(ctx, ctx->rrgba[s].grow(std::max<uint64_t>(t, 1) * 16));
-          cudaStream_t cs = ctx->xs[q % vdi_ctx::kXStreams];
-          if (q < vdi_ctx::kXStreams) CUDA_TRY(ctx, cudaStreamWaitEvent(cs, ctx->evx[0], 0));
-          CUDA_TRY(ctx, cudaMemcpyAsync(ctx->rcount[s].p, rc, ctx->P, cudaMemcpyDeviceToDevice, cs));
-          if (t) {
-            CUDA_TRY(ctx, cudaMemcpyAsync(ctx->rdepth[s].p, rd, t * 8, cudaMemcpyDeviceToDevice, cs));
-            CUDA_TRY(ctx, cudaMemcpyAsync(ctx->rrgba[s].p, rr, t * 16, cudaMemcpyDeviceToDevice, cs));
+          if (sm_copies) {
+            segs.push_back(CopySeg{rc, ctx->rcount[s].p, ctx->P});
+            if (t) {
+              segs.push_back(CopySeg{rd, ctx->rdepth[s].p, t * 8});
+              segs.push_back(CopySeg{rr, ctx->rrgba[s].p, t * 16});
+            }
+          } else {
+            cudaStream_t cs = ctx->xs[q % vdi_ctx::kXStreams];
+            if (q < vdi_ctx::kXStreams) CUDA_TRY(ctx, cudaStreamWaitEvent(cs, ctx->evx[0], 0));
+            CUDA_TRY(ctx, cudaMemcpyAsync(ctx->rcount[s].p, rc, ctx->P, cudaMemcpyDeviceToDevice, cs));
+            if (t) {
+              CUDA_TRY(ctx, cudaMemcpyAsync(ctx->rdepth[s].p, rd, t * 8, cudaMemcpyDeviceToDevice, cs));
+              CUDA_TRY(ctx, cudaMemcpyAsync(ctx->rrgba[s].p, rr, t * 16, cudaMemcpyDeviceToDevice, cs));
+            }
           }
           mp.src[s] = SrcDesc{ctx->rcount[s].as<uint8_t>(), ctx->rdepth[s].as<float2>(), ctx->rrgba[s].as<float4>()};
           ++q;
         }
         recvd += ctx->P + 24 * t;
       }
-      for (int i = 0; i < std::min<int>(q, vdi_ctx::kXStreams); ++i) {  // join the copy streams
+      if (sm_copies) CUDA_TRY(ctx, sm_copy(ctx, segs, st, launches));
+      for (int i = 0; i < (sm_copies ? 0 : std::min<int>(q, vdi_ctx::kXStreams)); ++i) {  // join the copy streams
         CUDA_TRY(ctx, cudaEventRecord(ctx->evx[1 + i], ctx->xs[i]));
         CUDA_TRY(ctx, cudaStreamWaitEvent(st, ctx->evx[1 + i], 0));
       }
@@ -928,14 +999,32 @@ vdi_status vdi_composite_frames(vdi_ctx* ctx, uint32_t F, const vdi_dense_view* 
       src[s] = Src{bc.as<uint8_t>(), bd.as<float2>(), br.as<float4>()};
       const int xi = q % vdi_ctx::kXStreams;
       qs[s] = xi;
-      if (q < vdi_ctx::kXStreams) CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->xs[xi], ctx->evx[0], 0));
       rp[s] = Src{static_cast<const uint8_t*>(pc), static_cast<const float2*>(pd), static_cast<const float4*>(pr)};
       ++q;
     }
     const int nq = std::min<int>(q, vdi_ctx::kXStreams);
+    for (int xi = 0; xi < nq; ++xi) CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->xs[xi], ctx->evx[0], 0));
+    const bool smc = !(cf.flags & VDI_FLAG_CE_COPIES) && j == 0 && q;
+    if (smc) {
+      // the first owned frame: nothing else runs yet, so the SMs pull its
+      // remote sources (faster than the copy engines); later frames' copies
+      // go to the copy engines after it, overlapping the merges
+      std::vector<CopySeg> segs;
+      for (uint32_t s = 0; s < n; ++s) {
+        if (qs[s] < 0) continue;
+        const uint64_t T = B(f, s, C);
+        segs.push_back(CopySeg{rp[s].c, const_cast<uint8_t*>(src[s].c), P});
+        if (T) {
+          segs.push_back(CopySeg{rp[s].d, const_cast<float2*>(src[s].d), T * 8});
+          segs.push_back(CopySeg{rp[s].r, const_cast<float4*>(src[s].r), T * 16});
+        }
+      }
+      CUDA_TRY(ctx, sm_copy(ctx, segs, st, launches));
+      CUDA_TRY(ctx, cudaEventRecord(ctx->evx[0], st));  // later frames' copies start after it
+    }
     // chunk-major issue: chunk c of every remote source, then one event per
     // copy stream, so the merge of chunk c waits only for chunk c's copies
-    for (uint32_t c = 0; c < C && q; ++c) {
+    for (uint32_t c = 0; c < C && q && !smc; ++c) {
       const size_t r0 = (size_t)rows[c] * W, r1 = (size_t)rows[c + 1] * W;
       for (uint32_t s = 0; s < n; ++s) {
         if (qs[s] < 0) continue;
@@ -967,7 +1056,8 @@ vdi_status vdi_composite_frames(vdi_ctx* ctx, uint32_t F, const vdi_dense_view* 
       vdi_full_view so{rows[c], rows[c + 1], images[f].count + (size_t)rows[c] * W,
                        images[f].depth + (size_t)rows[c] * W * cf.k_out * 2,
                        images[f].rgba + (size_t)rows[c] * W * cf.k_out * 4};
-      for (int xi = 0; xi < nq; ++xi) CUDA_TRY(ctx, cudaStreamWaitEvent(st, ctx->evc[c][xi], 0));
+      if (!smc)
+        for (int xi = 0; xi < nq; ++xi) CUDA_TRY(ctx, cudaStreamWaitEvent(st, ctx->evc[c][xi], 0));
       if (first && timing) CUDA_TRY(ctx, cudaEventRecord(ctx->ev[1], st));
       first = false;
       if (vdi_status e = merge_lists(ctx, mp, (uint64_t)(rows[c + 1] - rows[c]) * W, S_c, &so, timing, launches))

@@ -71,7 +71,8 @@ def main():
     variants = {}
     for name, fl in (("full_gather", vdi._lib.VDI_FLAG_FULL_GATHER),
                      ("nccl_exchange", vdi._lib.VDI_FLAG_NCCL_EXCHANGE),
-                     ("peer_reads", vdi._lib.VDI_FLAG_PEER_READS)):
+                     ("peer_reads", vdi._lib.VDI_FLAG_PEER_READS),
+                     ("ce_copies", vdi._lib.VDI_FLAG_CE_COPIES)):
         u = [vdi.get_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(u, src=0)
         c2 = vdi.Compositor(W, H, k_in, k_out, n, n_ranks=world, rank=rank, unique_id=u[0], flags=fl)
