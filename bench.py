@@ -287,6 +287,21 @@ def _run_ours(args, world, rank, local, clk):
     t_gen = time.time() - t0
     S_local = sum(p.total for p in local)
     S_total = int(allreduce_sum(S_local, G))
+    # Phase 1 as a measured stage (untimed w.r.t. `value`):
+    # vdi_generate_subvdi of one local PE (two-pass raycast, device scan, write)
+    # timed with CUDA events; deterministic, so the regenerated output is the same
+    g_ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    g_ms = []
+    for _ in range(2):
+        g_ev[0].record(stream)
+        p0 = comp.generate_subvdi(vol, tft, cam, dec, local_ids[0])
+        g_ev[1].record(stream)
+        torch.cuda.synchronize()
+        g_ms.append(g_ev[0].elapsed_time(g_ev[1]))
+    assert p0.total == local[0].total
+    phase1 = {"ms_per_subvdi": min(g_ms), "pe": local_ids[0], "supersegments": int(p0.total),
+              "note": "vdi_generate_subvdi: gamma search + count pass, scan, write pass (PAPER.md:113-118, "
+                      ":150-157); not part of the timed step"}
     frames_local, frames_img = None, None
     if compf is not None:
         frames_local = [[vdi.DenseSubVDI(p.pe_id, p.total, p.count.clone(), p.offset.clone(), p.depth.clone(),
@@ -485,6 +500,7 @@ def _run_ours(args, world, rank, local, clk):
                           "merge_scan": statistics.mean(c["ms_scan"] for c in stage),
                           "merge_fast": statistics.mean(c["ms_fast"] for c in stage),
                           "merge_search": statistics.mean(c["ms_search"] for c in stage)},
+            "phase1_generate": phase1,
             "latency_mode": latency,
             "frames_mode": frames_info,
             "full_representation_mode": full_rep,

@@ -907,7 +907,10 @@ __device__ __forceinline__ void sweep_batch(const MergeParams& mp, int bucket, u
 }
 
 // both short-list buckets in one launch: batches of bucket 0 (m <= 32) first
-__global__ void __launch_bounds__(32, 8) search_sweep_kernel(MergeParams mp) {
+#ifndef VDI_SWEEP_MINB
+#define VDI_SWEEP_MINB 8
+#endif
+__global__ void __launch_bounds__(32, VDI_SWEEP_MINB) search_sweep_kernel(MergeParams mp) {
   const uint32_t nb0 = (min(mp.wl_count[0], mp.wl_cap) + 31) / 32;
   const uint32_t nb1 = (min(mp.wl_count[1], mp.wl_cap) + 31) / 32;
   // dynamic claims, longest lists first (bucket 1, then bucket 0): a warp
