@@ -977,17 +977,21 @@ __global__ void __launch_bounds__(128) long_gather_kernel(MergeParams mp) {
     bool bad = !fits;
     if (valid && fits) {
       uint32_t hp[NS];
+      float ht[NS];  // t_front of each run's head, kept in registers (one load per record)
 #pragma unroll
-      for (int s = 0; s < NS; ++s) hp[s] = 0;
+      for (int s = 0; s < NS; ++s) {
+        hp[s] = 0;
+        ht[s] = cnt[s] ? __ldg(&mp.src[s].depth[goff[s]].x) : CUDART_INF_F;
+      }
       float prev_tb = -CUDART_INF_F;
       uint32_t r = 0;
-      while (r < m) {  // run-based k-way merge over the t_front values (L1)
+      while (r < m) {  // run-based k-way merge over the runs' head t_front values
         int b = -1, b2 = NS;
         float bt = CUDART_INF_F, b2t = CUDART_INF_F;
 #pragma unroll
         for (int s = 0; s < NS; ++s)
           if (hp[s] < cnt[s]) {
-            const float t = __ldg(&mp.src[s].depth[goff[s] + hp[s]].x);
+            const float t = ht[s];
             if (b < 0 || t < bt) {
               if (b >= 0) {
                 b2t = bt;
@@ -1012,6 +1016,7 @@ __global__ void __launch_bounds__(128) long_gather_kernel(MergeParams mp) {
             dp = mp.src[s].depth;
             cp = mp.src[s].rgba;
           }
+        float tn = CUDART_INF_F;
         for (;;) {
           const float2 d = __ldg(dp + gb + ii);
           float4 c = __ldg(cp + gb + ii);
@@ -1022,13 +1027,17 @@ __global__ void __launch_bounds__(128) long_gather_kernel(MergeParams mp) {
           odep[r * 32] = d;
           ++r;
           ++ii;
+          tn = CUDART_INF_F;
           if (ii >= cb) break;
-          const float tn = __ldg(&dp[gb + ii].x);
+          tn = __ldg(&dp[gb + ii].x);
           if (!(tn < b2t || (tn == b2t && b < b2))) break;
         }
 #pragma unroll
         for (int s = 0; s < NS; ++s)
-          if (s == b) hp[s] = ii;
+          if (s == b) {
+            hp[s] = ii;
+            ht[s] = tn;
+          }
       }
     }
     if (fits) *obad = bad ? 1u : 0u;
@@ -1078,26 +1087,27 @@ __device__ __forceinline__ int long_count(const float4* __restrict__ col, int m,
 }
 
 __global__ void __launch_bounds__(32) long_sweep_kernel(MergeParams mp) {
-  const int lane = threadIdx.x;
   const int k = mp.k_out, n = mp.n_src;
   const uint32_t c2 = min(mp.wl_count[2], mp.wl_cap), c3 = min(mp.wl_count[3], mp.wl_cap);
-  const uint32_t nb2 = (c2 + 31) / 32, nb3 = (c3 + 31) / 32;
-  for (uint32_t v = blockIdx.x; v < nb2 + nb3; v += gridDim.x) {
-    const int bucket = v < nb2 ? 2 : 3;
-    const uint32_t batch = bucket == 2 ? v : v - nb2;
-    const uint32_t total = bucket == 2 ? c2 : c3;
-    const PoolBatch pb = mp.long_batch[bucket - 2][batch];
+  // every lane claims its own lists (lanes diverge freely here: no warp
+  // collectives), the longest bucket first, so a lane that finishes early
+  // takes the next list instead of idling until the warp's longest list ends
+  for (;;) {
+    const uint32_t t = atomicAdd(&mp.search_ticket[2], 1u);
+    if (t >= c2 + c3) break;
+    const int bucket = t < c3 ? 3 : 2;
+    const uint32_t e = t < c3 ? t : t - c3;
+    const PoolBatch pb = mp.long_batch[bucket - 2][e >> 5];
     if (!pb.ok) continue;
-    const uint32_t e = batch * 32 + lane;
-    const bool valid = e < total;
-    const uint32_t* ent = mp.wl[bucket] + (size_t)(valid ? e : 0) * (3 + n);
-    const uint32_t p = valid ? ent[0] : 0u;
-    const int m = valid ? (int)ent[2] : 0;
+    const uint32_t* ent = mp.wl[bucket] + (size_t)e * (3 + n);
+    const uint32_t p = ent[0];
+    const int m = (int)ent[2];
     const char* base = mp.long_pool + pb.off;
-    const float4* col = reinterpret_cast<const float4*>(base) + lane;
-    const float2* dcol = reinterpret_cast<const float2*>(base + (size_t)pb.maxm * 32 * 16) + lane;
-    const bool bad = reinterpret_cast<const uint32_t*>(base + (size_t)pb.maxm * 32 * 24)[lane] != 0u;
-    if (!valid || bad) continue;  // lanes diverge freely: no warp collectives below
+    const uint32_t l = e & 31;
+    const float4* col = reinterpret_cast<const float4*>(base) + l;
+    const float2* dcol = reinterpret_cast<const float2*>(base + (size_t)pb.maxm * 32 * 16) + l;
+    const bool bad = reinterpret_cast<const uint32_t*>(base + (size_t)pb.maxm * 32 * 24)[l] != 0u;
+    if (bad) continue;
     // bisection (Q3-Q6)
     Bisection bs;
     bs.init(mp.gamma_max, mp.max_iters > 0);
