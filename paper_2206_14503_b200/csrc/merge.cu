@@ -1047,41 +1047,66 @@ __global__ void __launch_bounds__(128) long_gather_kernel(MergeParams mp) {
   }
 }
 
-// One count-mode sweep over a pool column (same decisions as sweep()).
+// Eight steps of a count-mode sweep over a pool column (same decisions as
+// sweep()) with the validity-interval bookkeeping of Bisection: a comparison
+// that split tightens U, one that merged raises L; comparisons that did not
+// happen contribute NaN, which fminf / fmaxf ignore.  Samples past m (rows of
+// longer lists of the batch, or the pool's slack) may be evaluated: their
+// splits are not counted and their extra constraints only shrink [L, U),
+// which keeps it valid.
+__device__ __forceinline__ void long_step8(const float4 (&v)[8], int q0, int m, float g2, float& ar, float& ag,
+                                           float& ab, float& aa, int& sc, float& L, float& U) {
+  const float qn = __int_as_float(0x7fc00000);
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    const float4 sv = v[u];
+    const bool first = u == 0 && q0 == 0;  // the first sample opens without a comparison
+    const bool gap = sv.w < 0.f;
+    const float sa = fabsf(sv.w);
+    const float n2 = fmaf(aa, aa, fmaf(ab, ab, fmaf(ag, ag, ar * ar)));
+    const float d2 = dist2(ar, ag, ab, aa, sv.x, sv.y, sv.z, sa);
+    const bool gcl = gap & (n2 > g2);  // the gap closed the segment: d2 not consulted (Q8)
+    const bool dsp = d2 > g2;
+    const bool dev = !gcl & !first;
+    U = fminf(U, fminf(gcl ? n2 : qn, (dev & dsp) ? d2 : qn));
+    L = fmaxf(L, fmaxf((gap & !gcl) ? n2 : qn, (dev & !dsp) ? d2 : qn));
+    const bool st = first | gcl | dsp;
+    const float tr = 1.0f - aa;
+    ar = st ? sv.x : fmaf(tr, sv.x, ar);
+    ag = st ? sv.y : fmaf(tr, sv.y, ag);
+    ab = st ? sv.z : fmaf(tr, sv.z, ab);
+    aa = st ? sa : fmaf(tr, sa, aa);
+    sc += (st & (q0 + u < m)) ? 1 : 0;
+  }
+}
+
+// One count-mode sweep over a pool column: chunks of 8 samples in two register
+// buffers (the next chunk's loads are in flight while one is swept; ping-pong,
+// no copies), leaving as soon as the count exceeds k.  Reads up to 16 rows past
+// m (the pool has slack for that).
 __device__ __forceinline__ int long_count(const float4* __restrict__ col, int m, float g2, int k, float& L,
                                           float& U) {
   float ar = 0.f, ag = 0.f, ab = 0.f, aa = 0.f;
   int sc = 0;
   L = -1.f;
   U = CUDART_INF_F;
-  float4 cur[8];
+  float4 A[8], B[8];
 #pragma unroll
-  for (int u = 0; u < 8; ++u)
-    if (u < m) cur[u] = col[u * 32];
-  for (int q0 = 0; q0 < m && sc <= k; q0 += 8) {
-    float4 nxt[8];
+  for (int u = 0; u < 8; ++u) A[u] = col[u * 32];
+  const float4* pp = col + 8 * 32;
+  for (int q0 = 0;;) {
 #pragma unroll
-    for (int u = 0; u < 8; ++u)  // next chunk in flight while this one is swept
-      if (q0 + 8 + u < m) nxt[u] = col[(q0 + 8 + u) * 32];
+    for (int u = 0; u < 8; ++u) B[u] = pp[u * 32];
+    pp += 8 * 32;
+    long_step8(A, q0, m, g2, ar, ag, ab, aa, sc, L, U);
+    q0 += 8;
+    if (q0 >= m || sc > k) break;
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int q = q0 + u;
-      const float4 sv = cur[u];
-      const bool gap = signbit(sv.w);
-      const float sa = fabsf(sv.w);
-      const float n2 = fmaf(aa, aa, fmaf(ab, ab, fmaf(ag, ag, ar * ar)));
-      const float d2 = dist2(ar, ag, ab, aa, sv.x, sv.y, sv.z, sa);
-      const bool st = (q == 0) | (gap & (n2 > g2)) | (d2 > g2);
-      track(q > 0 && q < m && sc <= k, gap, n2, d2, g2, L, U);
-      const float tr = 1.0f - aa;
-      ar = st ? sv.x : fmaf(tr, sv.x, ar);
-      ag = st ? sv.y : fmaf(tr, sv.y, ag);
-      ab = st ? sv.z : fmaf(tr, sv.z, ab);
-      aa = st ? sa : fmaf(tr, sa, aa);
-      sc += (st && q < m) ? 1 : 0;
-    }
-#pragma unroll
-    for (int u = 0; u < 8; ++u) cur[u] = nxt[u];
+    for (int u = 0; u < 8; ++u) A[u] = pp[u * 32];
+    pp += 8 * 32;
+    long_step8(B, q0, m, g2, ar, ag, ab, aa, sc, L, U);
+    q0 += 8;
+    if (q0 >= m || sc > k) break;
   }
   return sc;
 }
