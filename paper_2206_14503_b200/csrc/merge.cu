@@ -689,111 +689,99 @@ __global__ void __launch_bounds__(kFastThreads) merge_fast_kernel(MergeParams mp
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ int short_ms(int b) { return b == 0 ? 32 : 40; }
 
-template <int NS>
-__global__ void __launch_bounds__(128) search_gather_kernel(MergeParams mp) {
-  // per thread: depth column (PE-concatenated order) and the depth-order
-  // permutation in shared memory, [q][thread] layout (conflict-free)
-  __shared__ float2 sd[40 * 128];
-  __shared__ uint8_t sp[40 * 128];
+// Gather of one batch of short search lists (k_out < m <= 40), thread per
+// list: the run-based k-way merge over the per-PE runs staged
+// in shared memory ([q][thread], stride ST), then the samples are written in
+// depth order to the batch's pool slot in [sample][lane] layout with the gap
+// flag in the sign of alpha; transparent / overlapping records -> general path.
+template <int NS, int ST>
+__device__ __forceinline__ void gather_short_batch(const MergeParams& mp, uint32_t b, uint32_t nb1, uint32_t c0,
+                                                   uint32_t c1, float2* my_d, uint8_t* my_p, uint32_t lane) {
   const int n = mp.n_src;
-  const int tid = threadIdx.x;
-  const uint32_t c0 = min(mp.wl_count[0], mp.wl_cap), c1 = min(mp.wl_count[1], mp.wl_cap);
-  const uint32_t nb0 = (c0 + 31) / 32, nb1 = (c1 + 31) / 32;
-  const uint32_t lane = threadIdx.x & 31;
-  float2* my_d = sd + tid;
-  uint8_t* my_p = sp + tid;
-  // a warp claims one batch of 32 work-list entries at a time, the longer
-  // lists (bucket 1) first, so the last claims are the short ones
-  for (;;) {
-    uint32_t b = 0;
-    if (lane == 0) b = atomicAdd(&mp.search_ticket[1], 1u);
-    b = __shfl_sync(kFull, b, 0);
-    if (b >= nb0 + nb1) break;
-    const int bucket = b < nb1 ? 1 : 0;
-    const uint32_t i = (bucket == 1 ? b : b - nb1) * 32 + lane;
-    const bool valid = i < (bucket == 0 ? c0 : c1);
-    const uint32_t* ent = mp.wl[bucket] + (size_t)(valid ? i : 0) * (3 + n);
-    const uint32_t p = valid ? ent[0] : 0u, m = valid ? ent[2] : 0u;
-    uint32_t goff[NS], cnt[NS], cs[NS];
-    uint32_t j = 0;
+  const int bucket = b < nb1 ? 1 : 0;
+  const uint32_t i = (bucket == 1 ? b : b - nb1) * 32 + lane;
+  const bool valid = i < (bucket == 0 ? c0 : c1);
+  const uint32_t* ent = mp.wl[bucket] + (size_t)(valid ? i : 0) * (3 + n);
+  const uint32_t p = valid ? ent[0] : 0u, m = valid ? ent[2] : 0u;
+  uint32_t goff[NS], cnt[NS], cs[NS];
+  uint32_t j = 0;
 #pragma unroll
-    for (int s = 0; s < NS; ++s) {
-      goff[s] = cnt[s] = cs[s] = 0;
-      if (valid && s < n) {
-        goff[s] = ent[3 + s];
-        cnt[s] = __ldg(mp.src[s].count + p);
-        cs[s] = j;
-        j += cnt[s];
-      }
+  for (int s = 0; s < NS; ++s) {
+    goff[s] = cnt[s] = cs[s] = 0;
+    if (valid && s < n) {
+      goff[s] = ent[3 + s];
+      cnt[s] = __ldg(mp.src[s].count + p);
+      cs[s] = j;
+      j += cnt[s];
     }
-    // one pool slot per batch of 32 entries (a warp here = one batch)
-    uint32_t slot = 0;
-    if (lane == 0) {
-      slot = atomicAdd(mp.pool_next, 1u);
-      if (slot < mp.pool_cap) mp.batch_slot[bucket][i >> 5] = slot;
-      else atomicOr(mp.err, 1);
-    }
-    slot = __shfl_sync(kFull, slot, 0);
-    if (slot >= mp.pool_cap) continue;
-    float4* orgba = mp.pool_rgba + (size_t)slot * 40 * 32 + lane;
-    float2* odep = mp.pool_depth + (size_t)slot * 40 * 32 + lane;
-    // depth column in PE order (independent loads), then the depth order
-    load_concat<NS, 8>(mp, goff, cnt, cs, m, my_d, nullptr, 128);
-    uint32_t g0 = 0, g1 = 0;
-    bool bad = false;
-    if (valid) {
-      bad = !run_merge<NS>(my_d, 128, cs, cnt, m, my_p, 128, [](uint32_t) { return 1.f; });  // overlap, Q12
-      if (!bad) {
-        float prev_tb = 0.f;
-        for (uint32_t r = 0; r < m; ++r) {  // gap bits from the staged depths
-          const float2 d = my_d[(uint32_t)my_p[r * 128] * 128];
-          if (r > 0 && d.x > prev_tb) {
-            if (r < 32) g0 |= 1u << r;
-            else g1 |= 1u << (r - 32);
-          }
-          prev_tb = d.y;
-        }
-        // records in depth order, 8 loads in flight per trip, to the scratch
-        for (uint32_t r0 = 0; r0 < m; r0 += 8) {
-          float4 cv[8];
-#pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            const uint32_t r = r0 + u;
-            if (r < m) {
-              const uint32_t ci = my_p[r * 128];
-              const float4* cp = nullptr;
-              uint32_t gi = 0;
-#pragma unroll
-              for (int s = 0; s < NS; ++s)
-                if (ci >= cs[s] && ci < cs[s] + cnt[s]) {
-                  gi = goff[s] + (ci - cs[s]);
-                  cp = mp.src[s].rgba;
-                }
-              cv[u] = __ldg(cp + gi);
-            }
-          }
-#pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            const uint32_t r = r0 + u;
-            if (r < m) {
-              bad |= cv[u].w == 0.f;  // Q23
-              // gap before sample r: flagged in the sign of alpha (alpha > 0
-              // for every stored sample), tested by the sweeps with one FSETP
-              const bool gp = r < 32 ? ((g0 >> r) & 1u) : ((g1 >> (r - 32)) & 1u);
-              if (gp) cv[u].w = -cv[u].w;
-              orgba[r * 32] = cv[u];
-              odep[r * 32] = my_d[(uint32_t)my_p[r * 128] * 128];
-            }
-          }
-        }
-      }
-      uint32_t* og = mp.pool_gap + (size_t)slot * 64 + lane;
-      og[0] = bad ? 0xffffffffu : g0;  // skip marker (bit 0 of a real gap word is never set)
-      og[32] = bad ? 0xffffffffu : g1;
-    }
-    const int bk = (valid && bad) ? VDI_BUCKET_GENERAL : -1;
-    if (__any_sync(kFull, bk >= 0)) push_entries<NS>(mp, bk, p, m, goff, lane);
   }
+  // one pool slot per batch of 32 entries (a warp here = one batch)
+  uint32_t slot = 0;
+  if (lane == 0) {
+    slot = atomicAdd(mp.pool_next, 1u);
+    if (slot < mp.pool_cap) mp.batch_slot[bucket][i >> 5] = slot;
+    else atomicOr(mp.err, 1);
+  }
+  slot = __shfl_sync(kFull, slot, 0);
+  if (slot >= mp.pool_cap) return;
+  float4* orgba = mp.pool_rgba + (size_t)slot * 40 * 32 + lane;
+  float2* odep = mp.pool_depth + (size_t)slot * 40 * 32 + lane;
+  // depth column in PE order (independent loads), then the depth order
+  load_concat<NS, 8>(mp, goff, cnt, cs, m, my_d, nullptr, ST);
+  uint32_t g0 = 0, g1 = 0;
+  bool bad = false;
+  if (valid) {
+    bad = !run_merge<NS>(my_d, ST, cs, cnt, m, my_p, ST, [](uint32_t) { return 1.f; });  // overlap, Q12
+    if (!bad) {
+      float prev_tb = 0.f;
+      for (uint32_t r = 0; r < m; ++r) {  // gap bits from the staged depths
+        const float2 d = my_d[(uint32_t)my_p[r * ST] * ST];
+        if (r > 0 && d.x > prev_tb) {
+          if (r < 32) g0 |= 1u << r;
+          else g1 |= 1u << (r - 32);
+        }
+        prev_tb = d.y;
+      }
+      // records in depth order, 8 loads in flight per trip, to the scratch
+      for (uint32_t r0 = 0; r0 < m; r0 += 8) {
+        float4 cv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const uint32_t r = r0 + u;
+          if (r < m) {
+            const uint32_t ci = my_p[r * ST];
+            const float4* cp = nullptr;
+            uint32_t gi = 0;
+#pragma unroll
+            for (int s = 0; s < NS; ++s)
+              if (ci >= cs[s] && ci < cs[s] + cnt[s]) {
+                gi = goff[s] + (ci - cs[s]);
+                cp = mp.src[s].rgba;
+              }
+            cv[u] = __ldg(cp + gi);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const uint32_t r = r0 + u;
+          if (r < m) {
+            bad |= cv[u].w == 0.f;  // Q23
+            // gap before sample r: flagged in the sign of alpha (alpha > 0
+            // for every stored sample), tested by the sweeps with one FSETP
+            const bool gp = r < 32 ? ((g0 >> r) & 1u) : ((g1 >> (r - 32)) & 1u);
+            if (gp) cv[u].w = -cv[u].w;
+            orgba[r * 32] = cv[u];
+            odep[r * 32] = my_d[(uint32_t)my_p[r * ST] * ST];
+          }
+        }
+      }
+    }
+    uint32_t* og = mp.pool_gap + (size_t)slot * 64 + lane;
+    og[0] = bad ? 0xffffffffu : g0;  // skip marker (bit 0 of a real gap word is never set)
+    og[32] = bad ? 0xffffffffu : g1;
+  }
+  const int bk = (valid && bad) ? VDI_BUCKET_GENERAL : -1;
+  if (__any_sync(kFull, bk >= 0)) push_entries<NS>(mp, bk, p, m, goff, lane);
 }
 
 template <int MS>
@@ -910,17 +898,26 @@ __device__ __forceinline__ void sweep_batch(const MergeParams& mp, int bucket, u
 #ifndef VDI_SWEEP_MINB
 #define VDI_SWEEP_MINB 8
 #endif
-__global__ void __launch_bounds__(32, VDI_SWEEP_MINB) search_sweep_kernel(MergeParams mp) {
-  const uint32_t nb0 = (min(mp.wl_count[0], mp.wl_cap) + 31) / 32;
-  const uint32_t nb1 = (min(mp.wl_count[1], mp.wl_cap) + 31) / 32;
+// Short-list search (k_out < m <= 40), one warp per batch of 32 lists: the
+// gather (thread per list, memory-latency bound) and then the bisection
+// sweeps (register-resident, ALU bound) of the same batch.  Fused, the warps
+// of an SM overlap one batch's gather latency with other batches' sweeps.
+template <int NS>
+__global__ void __launch_bounds__(32, VDI_SWEEP_MINB) search_short_kernel(MergeParams mp) {
+  __shared__ float2 sd[40 * 32];
+  __shared__ uint8_t sp[40 * 32];
+  const uint32_t lane = threadIdx.x;
+  const uint32_t c0 = min(mp.wl_count[0], mp.wl_cap), c1 = min(mp.wl_count[1], mp.wl_cap);
+  const uint32_t nb0 = (c0 + 31) / 32, nb1 = (c1 + 31) / 32;
   // dynamic claims, longest lists first (bucket 1, then bucket 0): a warp
-  // takes the next batch when it finishes one, so the makespan is set by the
-  // total work, not by the batches a static stride happens to give a warp
+  // takes the next batch when it finishes one
   for (;;) {
     uint32_t v = 0;
-    if (threadIdx.x == 0) v = atomicAdd(&mp.search_ticket[0], 1u);
+    if (lane == 0) v = atomicAdd(&mp.search_ticket[0], 1u);
     v = __shfl_sync(kFull, v, 0);
     if (v >= nb0 + nb1) break;
+    gather_short_batch<NS, 32>(mp, v, nb1, c0, c1, sd + lane, sp + lane, lane);
+    __syncwarp();  // batch_slot written by lane 0; pool rows are read back by the lanes that wrote them
     // one instantiation for both buckets (half the code: the unrolled sweeps
     // otherwise miss in the instruction cache); bucket-0 batches leave the
     // sweeps at sample 32 through the every-8-samples warp vote
@@ -1388,17 +1385,18 @@ static cudaError_t prep(K kernel, size_t smem, int threads, int* per_sm) {
   return e;
 }
 
-static cudaError_t launch_sweep(const MergeParams& mp, cudaStream_t st) {
+template <int NS>
+static cudaError_t launch_short(const MergeParams& mp, cudaStream_t st) {
   static int per_sm = 0;
   if (!per_sm) {
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, search_sweep_kernel, 32, 0);
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, search_short_kernel<NS>, 32, 0);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) per_sm = 1;
   }
   uint32_t grid = (uint32_t)sm_count() * per_sm;
   const uint32_t most = (mp.P + 31) / 32;
   if (grid > most) grid = most ? most : 1;
-  search_sweep_kernel<<<grid, 32, 0, st>>>(mp);
+  search_short_kernel<NS><<<grid, 32, 0, st>>>(mp);
   return cudaGetLastError();
 }
 
@@ -1425,10 +1423,7 @@ static cudaError_t launch_fast_ns(const MergeParams& mp, cudaStream_t st, int* l
 template <int NS>
 static cudaError_t launch_search_ns(const MergeParams& mp, cudaStream_t st, int* launches) {
   cudaError_t e;
-  search_gather_kernel<NS><<<sm_count() * 4, 128, 0, st>>>(mp);
-  if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  ++*launches;
-  if ((e = launch_sweep(mp, st)) != cudaSuccess) return e;
+  if ((e = launch_short<NS>(mp, st)) != cudaSuccess) return e;
   ++*launches;
   long_gather_kernel<NS><<<sm_count() * 8, 128, 0, st>>>(mp);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
