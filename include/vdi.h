@@ -163,7 +163,9 @@ vdi_status vdi_generate_subvdi(vdi_ctx* ctx, const vdi_volume_desc* vol, const v
  * sub-supersegments and the final greedy sweep, written in the
  * full representation.
  * local_pes: the n_local sub-VDIs homed on this rank, any order, each with a
- * distinct pe_id.  strip_out: caller-owned, rows of this rank's strip
+ * distinct pe_id (offset arrays are required when n_ranks > 1; with one rank,
+ * when every view carries its offsets they supply the group bases and the
+ * receive-side scan is skipped -- they must then be the exclusive scan of count).  strip_out: caller-owned, rows of this rank's strip
  * (VDI_ERR_CAPACITY if the row range does not match).  Synchronises the
  * stream once when n_ranks > 1 (sizes of the all-to-allv).  Exchange: by
  * default the remote PEs' strip slices are pulled over NVLink by the copy

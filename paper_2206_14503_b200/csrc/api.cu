@@ -375,7 +375,8 @@ static vdi_status merge_lists(vdi_ctx* ctx, MergeParams& mp, uint64_t P, uint64_
   mp.err = &dc->err;
   mp.validate = (cf.flags & VDI_FLAG_VALIDATE) ? 1 : 0;
   if (P) {
-    CUDA_TRY(ctx, launch_scan(mp, ctx->group_sum.as<uint32_t>(), ctx->group_base.as<uint32_t>(), st, &launches));
+    if (!mp.src[0].offset)
+      CUDA_TRY(ctx, launch_scan(mp, ctx->group_sum.as<uint32_t>(), ctx->group_base.as<uint32_t>(), st, &launches));
     if (timing) CUDA_TRY(ctx, cudaEventRecord(ctx->ev[3], st));
     uint32_t* wlp = ctx->wl.as<uint32_t>();
     uint32_t* slp = ctx->slots.as<uint32_t>();
@@ -661,9 +662,15 @@ vdi_status vdi_composite(vdi_ctx* ctx, const vdi_dense_view* local, uint32_t n_l
   uint64_t S_here = 0, sent = 0, recvd = 0;
 
   if (G == 1) {
+    // every source is whole and local: when all carry their offset arrays
+    // (Fig. 2) the group bases are read from them and the
+    // receive-side scan is skipped
+    bool all_off = true;
+    for (uint32_t s = 0; s < n; ++s) all_off &= local[slot[s]].offset != nullptr;
     for (uint32_t s = 0; s < n; ++s) {
       const vdi_dense_view& v = local[slot[s]];
-      mp.src[s] = SrcDesc{v.count, reinterpret_cast<const float2*>(v.depth), reinterpret_cast<const float4*>(v.rgba)};
+      mp.src[s] = SrcDesc{v.count, reinterpret_cast<const float2*>(v.depth), reinterpret_cast<const float4*>(v.rgba),
+                          all_off ? v.offset : nullptr};
       S_here += v.total;
     }
   } else {

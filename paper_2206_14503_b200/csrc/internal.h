@@ -33,6 +33,8 @@ struct SrcDesc {
   const uint8_t* count;
   const float2* depth;
   const float4* rgba;
+  const uint32_t* offset;  // the source's exclusive scan of count (indexed by list), or null: then the
+                           // merge scans the counts itself (receive-side scan)
 };
 
 // Work-list buckets of lists that need more than the pass-through:

@@ -543,7 +543,8 @@ __global__ void __launch_bounds__(kFastThreads) merge_fast_kernel(MergeParams mp
       nb[s] = 0;
       if (s < n && gg < mp.g_end) {
         if (pp < mp.P) nc[s] = __ldg(mp.src[s].count + pp);
-        nb[s] = __ldg(mp.group_base + (size_t)s * mp.n_groups + gg);
+        nb[s] = mp.src[s].offset ? __ldg(mp.src[s].offset + (size_t)gg * 32)
+                                 : __ldg(mp.group_base + (size_t)s * mp.n_groups + gg);
       }
     }
   };

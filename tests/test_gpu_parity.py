@@ -223,6 +223,24 @@ def test_dense_to_full_and_fullrep_composite(vdi, orc):
     compare(gc, gd, gr, ref["count"], ref["depth"], ref["rgba"], ref["stats"]["margin"], "fullrep")
 
 
+def test_offsets_or_receive_scan_same_image(vdi):
+    """One GPU: with every source's offset array the merge reads the group
+    bases from it; without, it scans the counts (receive-side scan,
+    PAPER.md:166).  Same image."""
+    n, W, H, k = 7, 131, 53, 9
+    pes = synth.random_subvdis(n, W, H, k, lam=7.0, seed=77)
+    comp = vdi.Compositor(W, H, k, k, n)
+    dev = [dense_to_device(p, i) for i, p in enumerate(pes)]
+    a = comp.empty_strip()
+    comp.composite(dev, a)
+    no_off = [vdi.DenseSubVDI(d.pe_id, d.total, d.count, None, d.depth, d.rgba) for d in dev]
+    b = comp.empty_strip()
+    comp.composite(no_off, b)
+    torch.cuda.synchronize()
+    for x, y in ((a.count, b.count), (a.depth, b.depth), (a.rgba, b.rgba)):
+        assert torch.equal(x, y)
+
+
 def test_multi_gpu_strip_invariance(vdi):
     """G = 2 (or all visible GPUs): NCCL exchange + gather give the 1-GPU result
     bit-for-bit and match the oracle (tests/mgpu_check.py under torchrun)."""
