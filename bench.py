@@ -428,26 +428,33 @@ def _run_ours(args, world, rank, local, clk):
     bytes_sent = stage[-1]["bytes_sent"]
     bytes_recv = stage[-1]["bytes_received"]
 
-    # ---- end to end through the C ABI with host buffers (pinned)
+    # ---- end to end through the C ABI with host buffers (pinned): host
+    # sub-VDIs in, the composited strip back in the dense representation
+    # (vdi_composite_host_dense)
     e2e = None
     if not args.no_e2e:
         host_pes = [vdi.DenseSubVDI(p.pe_id, p.total, p.count.cpu().pin_memory(),
                                     p.offset.cpu().pin_memory() if G > 1 else None,
                                     p.depth.cpu().pin_memory(), p.rgba.cpu().pin_memory()) for p in local]
-        hstrip = comp.empty_strip(device="cpu", pin=True)
+        P_g = strip.count.numel()
+        cap = max(1, min(P_g * k, S_total))  # a list never gains supersegments: output <= input records
+        h_cnt = torch.empty(P_g, dtype=torch.uint8).pin_memory()
+        h_dep = torch.empty((cap, 2), dtype=torch.float32).pin_memory()
+        h_rgb = torch.empty((cap, 4), dtype=torch.float32).pin_memory()
         for _ in range(2):
-            comp.composite_host(host_pes, hstrip)
+            T_out = comp.composite_host_dense(host_pes, h_cnt, h_dep, h_rgb)
         barrier(G)
         t0 = time.perf_counter()
         for _ in range(args.e2e_steps):
-            comp.composite_host(host_pes, hstrip)
+            T_out = comp.composite_host_dense(host_pes, h_cnt, h_dep, h_rgb)
         dt = allreduce_max(time.perf_counter() - t0, G)
         P_full = W * H
         h2d = sum(P_full + 24 * p.total + (4 * (P_full + 1) if G > 1 else 0) for p in host_pes)
-        d2h = P_g * (1 + 24 * k)
+        d2h = P_g + 24 * T_out
         e2e = {"value": args.e2e_steps / dt, "unit": UNIT, "h2d_bytes_per_step": int(allreduce_sum(h2d, G)),
                "d2h_bytes_per_step": int(allreduce_sum(d2h, G)),
-               "note": "vdi_composite_host: pinned host sub-VDIs -> H2D -> composite -> strip D2H on every rank"}
+               "note": "vdi_composite_host_dense: pinned host sub-VDIs -> H2D -> composite (strip mode) -> "
+                       "on-device compaction -> counts + packed supersegments D2H, every rank"}
 
     # ---- CPU oracle baseline (rank 0, N = 1 only) + a parity spot check
     cpu = None

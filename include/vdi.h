@@ -216,6 +216,26 @@ vdi_status vdi_dense_to_full(vdi_ctx* ctx, const vdi_dense_view* in, vdi_full_vi
 vdi_status vdi_composite_host(vdi_ctx* ctx, const vdi_dense_view* local_pes, uint32_t n_local,
                               vdi_full_view* strip_out);
 
+/* Composited strip in the dense representation: per-list
+ * counts and the packed supersegments, list-major, slots in depth order. */
+typedef struct {
+  uint32_t row_begin, row_end; /* must be this rank's strip */
+  uint64_t capacity;           /* supersegments depth/rgba can hold */
+  uint64_t total;              /* out: supersegments written (set even on VDI_ERR_CAPACITY) */
+  uint8_t* count;              /* [rows*W] */
+  float* depth;                /* [capacity][2] */
+  float* rgba;                 /* [capacity][4] */
+} vdi_dense_strip;
+
+/* vdi_composite_host with the result returned in the dense representation:
+ * host sub-VDIs -> device -> composite -> compaction on the device -> only
+ * the counts and the packed supersegments cross back to the host buffers of
+ * out (vdi_dense_to_full re-inflates on a device when the full
+ * representation is needed).  VDI_ERR_CAPACITY if out->capacity < total.
+ * Synchronises. */
+vdi_status vdi_composite_host_dense(vdi_ctx* ctx, const vdi_dense_view* local_pes, uint32_t n_local,
+                                    vdi_dense_strip* out);
+
 /* Gather of the composited strips onto vdi_config.root (PAPER.md:185
  * MPI_Gather; Q14): image_out (rows [0, H), root only; ignored elsewhere)
  * receives every rank's strip at its rows.  Default: each rank sends its counts + packed records

@@ -11,7 +11,8 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libvdi.so")
+# VDI_LIB_PATH selects another in-tree build (A/B experiments); default lib/libvdi.so
+LIB_PATH = os.environ.get("VDI_LIB_PATH") or os.path.join(_HERE, "lib", "libvdi.so")
 
 VDI_OK = 0
 VDI_FLAG_PIXEL_STATS = 0x1
@@ -28,6 +29,11 @@ class vdi_config(C.Structure):
                 ("n_pes", C.c_uint32), ("n_ranks", C.c_uint32), ("rank", C.c_uint32), ("root", C.c_uint32),
                 ("max_iters", C.c_uint32), ("gamma_max", C.c_float), ("flags", C.c_uint32),
                 ("nccl_unique_id", C.c_void_p), ("cuda_stream", C.c_void_p)]
+
+
+class vdi_dense_strip(C.Structure):
+    _fields_ = [("row_begin", C.c_uint32), ("row_end", C.c_uint32), ("capacity", C.c_uint64), ("total", C.c_uint64),
+                ("count", C.c_void_p), ("depth", C.c_void_p), ("rgba", C.c_void_p)]
 
 
 class vdi_dense_view(C.Structure):
@@ -85,6 +91,8 @@ SIGNATURES = {
     "vdi_composite_fullrep": (C.c_int, [C.c_void_p, C.POINTER(vdi_full_view), C.c_void_p, C.c_uint32,
                                         C.POINTER(vdi_full_view)]),
     "vdi_dense_to_full": (C.c_int, [C.c_void_p, C.POINTER(vdi_dense_view), C.POINTER(vdi_full_view)]),
+    "vdi_composite_host_dense": (C.c_int, [C.c_void_p, C.POINTER(vdi_dense_view), C.c_uint32,
+                                           C.POINTER(vdi_dense_strip)]),
     "vdi_gather": (C.c_int, [C.c_void_p, C.POINTER(vdi_full_view), C.POINTER(vdi_full_view)]),
     "vdi_pixel_stats": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "vdi_get_counters": (C.c_int, [C.c_void_p, C.POINTER(vdi_counters)]),

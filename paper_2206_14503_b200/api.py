@@ -208,6 +208,16 @@ class Compositor:
         L.check(self.lib.vdi_composite_host(self.ctx, views, len(local_pes), C.byref(sv)), "vdi_composite_host")
         return strip
 
+    def composite_host_dense(self, local_pes, count, depth, rgba) -> int:
+        """vdi_composite_host_dense: host sub-VDIs in, the composited strip out
+        in the dense representation into host tensors count u8[rows*W],
+        depth f32[cap,2], rgba f32[cap,4].  Returns the supersegment total."""
+        views = (L.vdi_dense_view * max(1, len(local_pes)))(*[p.view() for p in local_pes])
+        out = L.vdi_dense_strip(self.row_begin, self.row_end, depth.shape[0], 0, _ptr(count), _ptr(depth), _ptr(rgba))
+        L.check(self.lib.vdi_composite_host_dense(self.ctx, views, len(local_pes), C.byref(out)),
+                "vdi_composite_host_dense")
+        return int(out.total)
+
     def gather(self, strip: FullVDI, image: FullVDI | None):
         """vdi_gather: strips -> the root rank (image ignored on other ranks)."""
         sv = strip.view()

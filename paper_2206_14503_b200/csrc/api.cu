@@ -1434,15 +1434,15 @@ vdi_status vdi_gather(vdi_ctx* ctx, const vdi_full_view* strip, vdi_full_view* i
   return VDI_OK;
 }
 
-vdi_status vdi_composite_host(vdi_ctx* ctx, const vdi_dense_view* local, uint32_t n_local, vdi_full_view* so) {
-  if (vdi_status s = check_ctx(ctx)) return s;
+// host sub-VDIs -> ctx-owned device copies (H2D on the ctx stream); dv gets device views
+static vdi_status upload_host_pes(vdi_ctx* ctx, const vdi_dense_view* local, uint32_t n_local,
+                                  std::vector<vdi_dense_view>& dv) {
   const vdi_config& cf = ctx->cfg;
-  if (!so || !so->count || !so->depth || !so->rgba) return fail(VDI_ERR_INVALID_ARG, "strip_out is NULL");
   if (n_local && !local) return fail(VDI_ERR_INVALID_ARG, "local_pes is NULL");
   if (n_local > cf.n_pes) return fail(VDI_ERR_INVALID_ARG, "too many local PEs");
   cudaStream_t st = ctx->stream;
   const size_t P = (size_t)cf.width * cf.height;
-  std::vector<vdi_dense_view> dv(n_local);
+  dv.assign(n_local, vdi_dense_view{});
   for (uint32_t l = 0; l < n_local; ++l) {
     const vdi_dense_view& v = local[l];
     if (!v.count || (v.total && (!v.depth || !v.rgba)) || (cf.n_ranks > 1 && !v.offset))
@@ -1467,6 +1467,16 @@ vdi_status vdi_composite_host(vdi_ctx* ctx, const vdi_dense_view* local, uint32_
       dv[l].offset = nullptr;
     }
   }
+  return VDI_OK;
+}
+
+vdi_status vdi_composite_host(vdi_ctx* ctx, const vdi_dense_view* local, uint32_t n_local, vdi_full_view* so) {
+  if (vdi_status s = check_ctx(ctx)) return s;
+  const vdi_config& cf = ctx->cfg;
+  if (!so || !so->count || !so->depth || !so->rgba) return fail(VDI_ERR_INVALID_ARG, "strip_out is NULL");
+  cudaStream_t st = ctx->stream;
+  std::vector<vdi_dense_view> dv;
+  if (vdi_status s = upload_host_pes(ctx, local, n_local, dv)) return s;
   const size_t Ps = ctx->P, k = cf.k_out;
   CUDA_TRY(ctx, ctx->hstrip_count.grow(Ps));
   CUDA_TRY(ctx, ctx->hstrip_depth.grow(Ps * k * 8));
@@ -1478,6 +1488,65 @@ vdi_status vdi_composite_host(vdi_ctx* ctx, const vdi_dense_view* local, uint32_
   CUDA_TRY(ctx, cudaMemcpyAsync(so->depth, ds.depth, Ps * k * 8, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(ctx, cudaMemcpyAsync(so->rgba, ds.rgba, Ps * k * 16, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(ctx, cudaStreamSynchronize(st));
+  return VDI_OK;
+}
+
+vdi_status vdi_composite_host_dense(vdi_ctx* ctx, const vdi_dense_view* local, uint32_t n_local,
+                                    vdi_dense_strip* out) {
+  if (vdi_status s = check_ctx(ctx)) return s;
+  const vdi_config& cf = ctx->cfg;
+  if (!out || !out->count || (out->capacity && (!out->depth || !out->rgba)))
+    return fail(VDI_ERR_INVALID_ARG, "out is NULL");
+  if (out->row_begin != ctx->row0 || out->row_end != ctx->row1)
+    return fail(VDI_ERR_CAPACITY, "out rows do not match this rank's strip");
+  cudaStream_t st = ctx->stream;
+  std::vector<vdi_dense_view> dv;
+  if (vdi_status s = upload_host_pes(ctx, local, n_local, dv)) return s;
+  const size_t Ps = ctx->P, k = cf.k_out;
+  CUDA_TRY(ctx, ctx->hstrip_count.grow(Ps));
+  CUDA_TRY(ctx, ctx->hstrip_depth.grow(Ps * k * 8));
+  CUDA_TRY(ctx, ctx->hstrip_rgba.grow(Ps * k * 16));
+  vdi_full_view ds{ctx->row0, ctx->row1, ctx->hstrip_count.as<uint8_t>(), ctx->hstrip_depth.as<float>(),
+                   ctx->hstrip_rgba.as<float>()};
+  if (vdi_status s = vdi_composite(ctx, dv.data(), n_local, &ds)) return s;
+  // the composited strip in the dense representation:
+  // scan of its counts, packed copy of its records, then only those bytes
+  // cross PCIe
+  int launches = 0;
+  const size_t ng = (Ps + 31) / 32;
+  CUDA_TRY(ctx, ctx->xsum.grow(((size_t)scan_chunks((uint32_t)std::max<size_t>(Ps, 1)) + 8) * 4));
+  CUDA_TRY(ctx, ctx->xbase.grow((ng + 8) * 4));
+  CUDA_TRY(ctx, ctx->xtot.grow(64));
+  unsigned long long* dtot = ctx->xtot.as<unsigned long long>();
+  MergeParams ms{};
+  ms.n_src = 1;
+  ms.P = (uint32_t)Ps;
+  ms.n_groups = (uint32_t)ng;
+  ms.src[0].count = ds.count;
+  unsigned long long T = 0;
+  if (Ps) {
+    CUDA_TRY(ctx, launch_scan(ms, ctx->xsum.as<uint32_t>(), ctx->xbase.as<uint32_t>(), st, &launches));
+    CUDA_TRY(ctx, launch_total(ms, ctx->xsum.as<uint32_t>(), dtot, st, &launches));
+    CUDA_TRY(ctx, cudaMemcpyAsync(&T, dtot, 8, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(ctx, cudaStreamSynchronize(st));
+  }
+  out->total = T;
+  if (T > out->capacity) return fail(VDI_ERR_CAPACITY, "dense strip needs %llu supersegments, capacity %llu", T,
+                                     (unsigned long long)out->capacity);
+  CUDA_TRY(ctx, ctx->g_dense.grow(std::max<uint64_t>(T, 1) * 24));
+  float4* dc4 = ctx->g_dense.as<float4>();
+  float2* dd2 = reinterpret_cast<float2*>(dc4 + std::max<uint64_t>(T, 1));
+  if (Ps)
+    CUDA_TRY(ctx, launch_compact(ds.count, reinterpret_cast<const float2*>(ds.depth),
+                                 reinterpret_cast<const float4*>(ds.rgba), (uint32_t)Ps, (int)k,
+                                 ctx->xbase.as<uint32_t>(), dd2, dc4, st, &launches));
+  CUDA_TRY(ctx, cudaMemcpyAsync(out->count, ds.count, Ps, cudaMemcpyDeviceToHost, st));
+  if (T) {
+    CUDA_TRY(ctx, cudaMemcpyAsync(out->depth, dd2, T * 8, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(ctx, cudaMemcpyAsync(out->rgba, dc4, T * 16, cudaMemcpyDeviceToHost, st));
+  }
+  CUDA_TRY(ctx, cudaStreamSynchronize(st));
+  ctx->last.kernel_launches += (uint32_t)launches;
   return VDI_OK;
 }
 

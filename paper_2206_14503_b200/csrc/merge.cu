@@ -508,6 +508,9 @@ __host__ __device__ constexpr size_t fast_warp_bytes(int k) {
          & ~(size_t)15;
 }
 
+#ifndef VDI_FAST_RUN
+#define VDI_FAST_RUN 4
+#endif
 template <int NS>
 __global__ void __launch_bounds__(kFastThreads) merge_fast_kernel(MergeParams mp) {
   extern __shared__ float4 smem[];
@@ -533,24 +536,39 @@ __global__ void __launch_bounds__(kFastThreads) merge_fast_kernel(MergeParams mp
   __syncwarp();
 
   // counts and group bases of the next group are loaded one iteration ahead
-  const uint32_t gstride = gridDim.x * nwarps;
+  // groups are taken in runs of kRun consecutive groups, the runs interleaved
+  // over the warps (all warps write one window of the output at a time: DRAM
+  // page locality); counts are loaded one group ahead.  Group bases: from
+  // the receive-side scan, or -- when the sources carry their offset arrays --
+  // read at the start of a run and carried along as base + the group's count
+  // total (one offset sector per source and run instead of per group)
+  constexpr uint32_t kRun = VDI_FAST_RUN;
+  const uint32_t nw_all = gridDim.x * nwarps, w_id = blockIdx.x * nwarps + warp;
+  const bool carry = mp.src[0].offset != nullptr;  // all sources or none (api.cu)
+  auto next_group = [&](uint32_t gg) -> uint32_t {  // the group after gg in this warp's sequence
+    const uint32_t r = (gg - mp.g_begin) % kRun;
+    return r + 1 < kRun ? gg + 1 : gg + 1 + (nw_all - 1) * kRun;
+  };
   uint32_t nc[NS], nb[NS];
+#pragma unroll
+  for (int s = 0; s < NS; ++s) nb[s] = 0;
   auto prefetch = [&](uint32_t gg) {
     const uint32_t pp = gg * 32 + lane;
+    const bool run_start = (gg - mp.g_begin) % kRun == 0;
 #pragma unroll
     for (int s = 0; s < NS; ++s) {
       nc[s] = 0;
-      nb[s] = 0;
       if (s < n && gg < mp.g_end) {
         if (pp < mp.P) nc[s] = __ldg(mp.src[s].count + pp);
-        nb[s] = mp.src[s].offset ? __ldg(mp.src[s].offset + (size_t)gg * 32)
-                                 : __ldg(mp.group_base + (size_t)s * mp.n_groups + gg);
+        if (!carry) nb[s] = __ldg(mp.group_base + (size_t)s * mp.n_groups + gg);
+        else if (run_start) nb[s] = __ldg(mp.src[s].offset + (size_t)gg * 32);
       }
     }
   };
-  prefetch(mp.g_begin + blockIdx.x * nwarps + warp);
+  const uint32_t g_first = mp.g_begin + w_id * kRun;
+  prefetch(g_first);
 
-  for (uint32_t g = mp.g_begin + blockIdx.x * nwarps + warp; g < mp.g_end; g += gstride) {
+  for (uint32_t g = g_first; g < mp.g_end; g = next_group(g)) {
     const uint32_t p0 = g * 32, p = p0 + lane;
     const bool valid = p < mp.P;
     uint32_t cnt[NS], gidx[NS];
@@ -560,12 +578,14 @@ __global__ void __launch_bounds__(kFastThreads) merge_fast_kernel(MergeParams mp
       cnt[s] = nc[s];
       gidx[s] = nb[s];
     }
-    prefetch(g + gstride);
+    prefetch(next_group(g));
 #pragma unroll
     for (int s = 0; s < NS; ++s) {
       if (s < n) {
         const uint32_t c = cnt[s];
         const uint32_t incl = warp_incl_scan(c, lane);
+        if (carry && (g - mp.g_begin) % kRun + 1 < kRun)
+          nb[s] = gidx[s] + __shfl_sync(kFull, incl, 31);  // base of group g + 1 (same run)
         gidx[s] += incl - c;
         m += c;
       }

@@ -241,6 +241,33 @@ def test_offsets_or_receive_scan_same_image(vdi):
         assert torch.equal(x, y)
 
 
+def test_host_dense_output(vdi):
+    """vdi_composite_host_dense: host sub-VDIs in, the composited strip back
+    in the dense representation -- the counts of the device composite and its
+    non-empty slots packed in list order."""
+    n, W, H, k = 5, 97, 61, 10
+    pes = synth.random_subvdis(n, W, H, k, lam=8.0, seed=91)
+    comp = vdi.Compositor(W, H, k, k, n)
+    dev = [dense_to_device(p, i) for i, p in enumerate(pes)]
+    full = comp.empty_strip()
+    comp.composite(dev, full)
+    torch.cuda.synchronize()
+    host = [dense_to_device(p, i, device="cpu") for i, p in enumerate(pes)]
+    cap = W * H * k
+    hc = torch.empty(W * H, dtype=torch.uint8)
+    hd = torch.empty((cap, 2), dtype=torch.float32)
+    hr = torch.empty((cap, 4), dtype=torch.float32)
+    T = comp.composite_host_dense(host, hc, hd, hr)
+    fc, fd, fr = full_to_numpy(full)
+    assert np.array_equal(hc.numpy(), fc)
+    sel = np.arange(k)[None, :] < fc[:, None].astype(np.int64)
+    assert T == int(sel.sum())
+    assert np.array_equal(hd.numpy()[:T], fd[sel]) and np.array_equal(hr.numpy()[:T], fr[sel])
+    small = torch.empty((max(T - 1, 1), 2), dtype=torch.float32), torch.empty((max(T - 1, 1), 4), dtype=torch.float32)
+    with pytest.raises(Exception):
+        comp.composite_host_dense(host, hc, small[0], small[1])  # VDI_ERR_CAPACITY
+
+
 def test_multi_gpu_strip_invariance(vdi):
     """G = 2 (or all visible GPUs): NCCL exchange + gather give the 1-GPU result
     bit-for-bit and match the oracle (tests/mgpu_check.py under torchrun)."""
