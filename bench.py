@@ -371,6 +371,10 @@ def _run_ours(args, world, rank, local, clk):
                    "note": "one VDI per step in strips over all GPUs, dense gather to rank 0"}
         frames_info = {"frames_per_step": F, "chunks": args.chunks,
                        "ms_size_exchange_and_first_copy": statistics.mean(c_["ms_exchange"] for c_ in fstage),
+                       "ms_size_exchange": statistics.mean(c_["ms_sizes"] for c_ in fstage),
+                       "ms_first_pull": statistics.mean(c_["ms_pull"] for c_ in fstage),
+                       "first_pull_GBs": (fstage[-1]["bytes_received"] / max(1, F // G)) / 1e6
+                                         / max(1e-6, statistics.mean(c_["ms_pull"] for c_ in fstage)),
                        "ms_merge_incl_overlapped_copies": statistics.mean(c_["ms_merge"] for c_ in fstage),
                        "bytes_pulled_per_step_rank0": fstage[-1]["bytes_received"]}
         # the full-representation pipeline of Fig. 6: sub-VDIs in

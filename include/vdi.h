@@ -266,6 +266,7 @@ typedef struct {
   uint64_t bytes_gather;     /* bytes that crossed into the root in the last vdi_gather (G > 1) */
   uint64_t fallback_groups;  /* 32-list groups written with plain stores (tail group / unaligned output) */
   float ms_scan, ms_fast, ms_search; /* VDI_FLAG_STAGE_TIMING: receive scan, pass-through kernel, search kernels */
+  float ms_sizes, ms_pull;           /* VDI_FLAG_STAGE_TIMING, vdi_composite_frames: size exchange (+ host sync), SM pull of the first owned frame */
 } vdi_counters;
 vdi_status vdi_get_counters(vdi_ctx* ctx, vdi_counters* out);
 

@@ -123,6 +123,8 @@ struct vdi_ctx {
   bool timing_pending = false;
   bool gather_timing_pending = false;
   cudaEvent_t gev[2] = {nullptr, nullptr};
+  cudaEvent_t fev[2] = {nullptr, nullptr};  // frames mode: pull start / end
+  bool frames_timing_pending = false;
   ~vdi_ctx() {
     if (cub_tmp) cudaFree(cub_tmp);
     for (auto& x : xs)
@@ -132,6 +134,8 @@ struct vdi_ctx {
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
     for (auto& e : gev)
+      if (e) cudaEventDestroy(e);
+    for (auto& e : fev)
       if (e) cudaEventDestroy(e);
     for (auto& r : evc)
       for (auto& e : r)
@@ -168,6 +172,9 @@ namespace {
 // SM-driven copy of many segments (peer slices over NVLink through CUDA IPC
 // mappings into local receive buffers): blockIdx.y = segment, 16/8/4/1-byte
 // vectors by the common alignment of the segment, 4 loads in flight per thread.
+#ifndef VDI_COPY_BPS
+#define VDI_COPY_BPS 4
+#endif
 struct CopySeg {
   const void* src;
   void* dst;
@@ -286,8 +293,8 @@ static cudaError_t sm_copy(vdi_ctx* ctx, const std::vector<CopySeg>& segs, cudaS
   cudaError_t e = ctx->segbuf.grow(std::max<size_t>(bytes, 64 * sizeof(CopySeg)));
   if (e != cudaSuccess) return e;
   if ((e = cudaMemcpyAsync(ctx->segbuf.p, segs.data(), bytes, cudaMemcpyHostToDevice, st)) != cudaSuccess) return e;
-  // ~4 blocks of 256 threads per SM over all segments
-  const unsigned gx = std::max<unsigned>(1u, (unsigned)(api_sm_count() * 4 / (int)segs.size()));
+  // VDI_COPY_BPS blocks of 256 threads per SM over all segments
+  const unsigned gx = std::max<unsigned>(1u, (unsigned)(api_sm_count() * VDI_COPY_BPS / (int)segs.size()));
   peer_copy_kernel<<<dim3(gx, (unsigned)segs.size()), 256, 0, st>>>(ctx->segbuf.as<CopySeg>());
   ++launches;
   return cudaGetLastError();
@@ -492,6 +499,7 @@ vdi_status vdi_composite_init(const vdi_config* cfg, vdi_ctx** out) {
   ctx->hrgba.resize(cfg->n_pes);
   for (auto& ev : ctx->ev) cudaEventCreate(&ev);
   for (auto& ev : ctx->gev) cudaEventCreate(&ev);
+  for (auto& ev : ctx->fev) cudaEventCreate(&ev);
   for (auto& ev : ctx->evx) cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
   for (auto& r : ctx->evc)
     for (auto& ev : r) cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
@@ -1027,7 +1035,12 @@ vdi_status vdi_composite_frames(vdi_ctx* ctx, uint32_t F, const vdi_dense_view* 
           segs.push_back(CopySeg{rp[s].r, const_cast<float4*>(src[s].r), T * 16});
         }
       }
+      if (timing) CUDA_TRY(ctx, cudaEventRecord(ctx->fev[0], st));
       CUDA_TRY(ctx, sm_copy(ctx, segs, st, launches));
+      if (timing) {
+        CUDA_TRY(ctx, cudaEventRecord(ctx->fev[1], st));
+        ctx->frames_timing_pending = true;
+      }
       CUDA_TRY(ctx, cudaEventRecord(ctx->evx[0], st));  // later frames' copies start after it
     }
     // chunk-major issue: chunk c of every remote source, then one event per
@@ -1590,6 +1603,11 @@ vdi_status vdi_get_counters(vdi_ctx* ctx, vdi_counters* out) {
       CUDA_TRY(ctx, cudaEventElapsedTime(&ctx->last.ms_search, ctx->ev[4], ctx->ev[5]));
     }
     ctx->timing_pending = false;
+  }
+  if (ctx->frames_timing_pending) {
+    CUDA_TRY(ctx, cudaEventElapsedTime(&ctx->last.ms_sizes, ctx->ev[0], ctx->fev[0]));
+    CUDA_TRY(ctx, cudaEventElapsedTime(&ctx->last.ms_pull, ctx->fev[0], ctx->fev[1]));
+    ctx->frames_timing_pending = false;
   }
   if (ctx->gather_timing_pending) {
     CUDA_TRY(ctx, cudaEventElapsedTime(&ctx->last.ms_gather, ctx->gev[0], ctx->gev[1]));
