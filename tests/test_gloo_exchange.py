@@ -124,3 +124,62 @@ def test_two_rank_exchange_matches_single_process():
     assert res["pes_received"] == N_PES      # every PE contributes to every strip
     assert res["conserved"]
     assert res["identical"]
+
+
+def _frames_worker(rank, world, port, q):
+    """Frames mode (vdi_composite_frames): frame f is composited whole by rank
+    f mod G from every rank's PEs; each rank sends the whole sub-VDIs of its
+    PEs for frame f to f's owner (sizes first, then payload)."""
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import oracle
+        import synth
+        from paper_2206_14503_b200 import api
+        F = 2 * world
+        frames = [synth.random_subvdis(N_PES, W, H, K_IN, lam=4.0 + f, seed=40 + f) for f in range(F)]
+        home = [pe for pe in range(N_PES) if api.pe_home(N_PES, world, pe) == rank]
+        send = [b"".join(_pack(f * N_PES + pe, _slice(frames[f][pe], 0, H)) for f in range(g, F, world)
+                         for pe in home) for g in range(world)]
+        ssz = torch.tensor([len(b) for b in send], dtype=torch.int64)
+        rsz = torch.empty(world, dtype=torch.int64)
+        dist.all_to_all_single(rsz, ssz)
+        sbuf = torch.frombuffer(bytearray(b"".join(send)), dtype=torch.uint8)
+        rbuf = torch.empty(int(rsz.sum()), dtype=torch.uint8)
+        dist.all_to_all_single(rbuf, sbuf, rsz.tolist(), ssz.tolist())
+        got = sorted(_unpack(rbuf.numpy().tobytes()))
+        ok, owned = True, []
+        for f in range(rank, F, world):
+            pes_f = [p for key, p in got if key // N_PES == f]
+            assert [key % N_PES for key, _ in got if key // N_PES == f] == list(range(N_PES))
+            img = oracle.composite(pes_f, W, H, 1, K_OUT, with_stats=False)
+            ref = oracle.composite(frames[f], W, H, 1, K_OUT, with_stats=False)
+            ok &= all(np.array_equal(img[k], ref[k]) for k in ("count", "depth", "rgba"))
+            owned.append(f)
+        res = [None] * world if rank == 0 else None
+        dist.gather_object((owned, ok), res, dst=0)
+        if rank == 0:
+            q.put(res)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_frames_mode_matches_single_process():
+    try:
+        import oracle
+        oracle.lib()
+    except Exception as e:   # pragma: no cover
+        pytest.skip(f"oracle not built: {e}")
+    world, port = 2, _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_frames_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = q.get(timeout=240)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert [o for o, _ in res] == [[0, 2], [1, 3]]   # frame f owned by rank f mod G
+    assert all(ok for _, ok in res)
