@@ -1129,6 +1129,9 @@ __device__ __forceinline__ int long_count(const float4* __restrict__ col, int m,
   return sc;
 }
 
+#ifndef VDI_LONG_WPS
+#define VDI_LONG_WPS 16  // resident long-sweep warps per SM
+#endif
 __global__ void __launch_bounds__(32) long_sweep_kernel(MergeParams mp) {
   const int k = mp.k_out, n = mp.n_src;
   const uint32_t c2 = min(mp.wl_count[2], mp.wl_cap), c3 = min(mp.wl_count[3], mp.wl_cap);
@@ -1449,7 +1452,7 @@ static cudaError_t launch_search_ns(const MergeParams& mp, cudaStream_t st, int*
   long_gather_kernel<NS><<<sm_count() * 8, 128, 0, st>>>(mp);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   ++*launches;
-  long_sweep_kernel<<<sm_count() * 16, 32, 0, st>>>(mp);
+  long_sweep_kernel<<<sm_count() * VDI_LONG_WPS, 32, 0, st>>>(mp);
   ++*launches;
   return cudaGetLastError();
 }
