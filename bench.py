@@ -525,6 +525,17 @@ def _run_ours(args, world, rank, local, clk):
                          "peer copies: copy engines pull peers' strip slices over NVLink (CUDA IPC)" if args.ce_copies else
                          "peer copies: one SM kernel pulls peers' strip slices over NVLink (CUDA IPC)"),
             "gather_bytes_into_root": stage[-1]["bytes_gather"],
+            "nvlink_roofline": None if G == 1 else {
+                "peak_GBs_per_direction": 900.0, "peak_source": "NVLink 5 nominal per GPU per direction",
+                "strip_exchange_GBs_rank0": bytes_recv / max(ms_ex, 1e-6) / 1e6,
+                "strip_exchange_frac": bytes_recv / max(ms_ex, 1e-6) / 1e6 / 900.0,
+                "strip_exchange_note": "peer slices pulled into rank 0 / (size exchange + host sync + pull) time",
+                "gather_into_root_GBs": stage[-1]["bytes_gather"] / max(ms_ga, 1e-6) / 1e6,
+                "gather_into_root_frac": stage[-1]["bytes_gather"] / max(ms_ga, 1e-6) / 1e6 / 900.0,
+                "gather_note": "dense bytes into the root / gather stage time (includes compaction, host sync and "
+                               "the root's 1 GB inflate)",
+                "frames_first_pull_GBs": frames_info["first_pull_GBs"] if frames_info else None,
+                "frames_first_pull_frac": frames_info["first_pull_GBs"] / 900.0 if frames_info else None},
             "gpu_launches": launches,
             "clocks": clk.summary(),
             "e2e": e2e,

@@ -287,14 +287,15 @@ static int api_sm_count() {
   return n;
 }
 
-static cudaError_t sm_copy(vdi_ctx* ctx, const std::vector<CopySeg>& segs, cudaStream_t st, int& launches) {
+static cudaError_t sm_copy(vdi_ctx* ctx, const std::vector<CopySeg>& segs, cudaStream_t st, int& launches,
+                           int bps = VDI_COPY_BPS) {
   if (segs.empty()) return cudaSuccess;
   const size_t bytes = segs.size() * sizeof(CopySeg);
   cudaError_t e = ctx->segbuf.grow(std::max<size_t>(bytes, 64 * sizeof(CopySeg)));
   if (e != cudaSuccess) return e;
   if ((e = cudaMemcpyAsync(ctx->segbuf.p, segs.data(), bytes, cudaMemcpyHostToDevice, st)) != cudaSuccess) return e;
-  // VDI_COPY_BPS blocks of 256 threads per SM over all segments
-  const unsigned gx = std::max<unsigned>(1u, (unsigned)(api_sm_count() * VDI_COPY_BPS / (int)segs.size()));
+  // bps blocks of 256 threads per SM over all segments
+  const unsigned gx = std::max<unsigned>(1u, (unsigned)(api_sm_count() * bps / (int)segs.size()));
   peer_copy_kernel<<<dim3(gx, (unsigned)segs.size()), 256, 0, st>>>(ctx->segbuf.as<CopySeg>());
   ++launches;
   return cudaGetLastError();
@@ -789,7 +790,8 @@ vdi_status vdi_composite(vdi_ctx* ctx, const vdi_dense_view* local, uint32_t n_l
         }
         recvd += ctx->P + 24 * t;
       }
-      if (sm_copies) CUDA_TRY(ctx, sm_copy(ctx, segs, st, launches));
+      // nothing overlaps the strip exchange: the whole GPU pulls (16 blocks per SM)
+      if (sm_copies) CUDA_TRY(ctx, sm_copy(ctx, segs, st, launches, 16));
       for (int i = 0; i < (sm_copies ? 0 : std::min<int>(q, vdi_ctx::kXStreams)); ++i) {  // join the copy streams
         CUDA_TRY(ctx, cudaEventRecord(ctx->evx[1 + i], ctx->xs[i]));
         CUDA_TRY(ctx, cudaStreamWaitEvent(st, ctx->evx[1 + i], 0));
