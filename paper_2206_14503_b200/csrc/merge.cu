@@ -1037,21 +1037,47 @@ __global__ void __launch_bounds__(128) long_gather_kernel(MergeParams mp) {
             dp = mp.src[s].depth;
             cp = mp.src[s].rgba;
           }
+        // take records of run b while they precede the next run's head
+        // (ties: lower PE first, Q11), 8 of them loaded per trip (the ones
+        // past the cut are reloaded, from L1/L2, when b is chosen again)
         float tn = CUDART_INF_F;
-        for (;;) {
-          const float2 d = __ldg(dp + gb + ii);
-          float4 c = __ldg(cp + gb + ii);
-          bad |= c.w == 0.f || d.x < prev_tb;  // Q23 / Q12
-          if (r > 0 && d.x > prev_tb) c.w = -c.w;  // gap before this sample: sign of alpha
-          prev_tb = d.y;
-          orgba[r * 32] = c;
-          odep[r * 32] = d;
-          ++r;
-          ++ii;
-          tn = CUDART_INF_F;
-          if (ii >= cb) break;
-          tn = __ldg(&dp[gb + ii].x);
-          if (!(tn < b2t || (tn == b2t && b < b2))) break;
+        for (bool first = true;;) {
+          const uint32_t nch = min(8u, cb - ii);
+          float2 dv[8];
+          float4 cv[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            if ((uint32_t)u < nch) {
+              dv[u] = __ldg(dp + gb + ii + u);
+              cv[u] = __ldg(cp + gb + ii + u);
+            }
+          uint32_t taken = 0;
+          bool stop = false;
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            if (!stop && (uint32_t)u < nch) {
+              const float2 d = dv[u];
+              if (!(first && u == 0) && !(d.x < b2t || (d.x == b2t && b < b2))) {
+                stop = true;
+                tn = d.x;
+              } else {
+                float4 c = cv[u];
+                bad |= c.w == 0.f || d.x < prev_tb;  // Q23 / Q12
+                if (r > 0 && d.x > prev_tb) c.w = -c.w;  // gap before this sample: sign of alpha
+                prev_tb = d.y;
+                orgba[r * 32] = c;
+                odep[r * 32] = d;
+                ++r;
+                ++taken;
+              }
+            }
+          ii += taken;
+          first = false;
+          if (stop) break;  // tn = head of run b
+          if (ii >= cb) {
+            tn = CUDART_INF_F;
+            break;
+          }
         }
 #pragma unroll
         for (int s = 0; s < NS; ++s)
