@@ -961,13 +961,17 @@ template <int NS>
 __global__ void __launch_bounds__(128) long_gather_kernel(MergeParams mp) {
   const int n = mp.n_src;
   const uint32_t c2 = min(mp.wl_count[2], mp.wl_cap), c3 = min(mp.wl_count[3], mp.wl_cap);
-  const uint32_t c2r = (c2 + 31) & ~31u;
-  const uint32_t tot = c2r + c3;
+  const uint32_t nb2 = (c2 + 31) / 32, nb3 = (c3 + 31) / 32;
   const uint32_t lane = threadIdx.x & 31;
-  for (uint32_t v0 = blockIdx.x * blockDim.x; v0 < tot; v0 += gridDim.x * blockDim.x) {
-    const uint32_t v = v0 + threadIdx.x;
-    const int bucket = v < c2r ? 2 : 3;
-    const uint32_t i = bucket == 2 ? v : v - c2r;
+  // a warp claims one batch of 32 work-list entries at a time, the longest
+  // bucket (3) first
+  for (;;) {
+    uint32_t bt0 = 0;
+    if (lane == 0) bt0 = atomicAdd(&mp.search_ticket[3], 1u);
+    bt0 = __shfl_sync(kFull, bt0, 0);
+    if (bt0 >= nb2 + nb3) break;
+    const int bucket = bt0 < nb3 ? 3 : 2;
+    const uint32_t i = (bucket == 3 ? bt0 : bt0 - nb3) * 32 + lane;
     const bool valid = i < (bucket == 2 ? c2 : c3);
     const uint32_t* ent = mp.wl[bucket] + (size_t)(valid ? i : 0) * (3 + n);
     const uint32_t p = valid ? ent[0] : 0u, m = valid ? ent[2] : 0u;
@@ -1530,7 +1534,15 @@ static cudaError_t launch_search_ns(const MergeParams& mp, cudaStream_t st, int*
   if ((e = launch_short<NS>(mp, st)) != cudaSuccess) return e;
 #endif
   ++*launches;
-  long_gather_kernel<NS><<<sm_count() * 8, 128, 0, st>>>(mp);
+  {
+    static int per_sm = 0;  // resident blocks: the warps claim batches dynamically
+    if (!per_sm) {
+      if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, long_gather_kernel<NS>, 128, 0)) != cudaSuccess)
+        return e;
+      if (per_sm < 1) per_sm = 1;
+    }
+    long_gather_kernel<NS><<<sm_count() * per_sm, 128, 0, st>>>(mp);
+  }
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   ++*launches;
   long_sweep_kernel<<<sm_count() * VDI_LONG_WPS, 32, 0, st>>>(mp);
