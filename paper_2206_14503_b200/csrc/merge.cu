@@ -511,6 +511,9 @@ __host__ __device__ constexpr size_t fast_warp_bytes(int k) {
 #ifndef VDI_FAST_RUN
 #define VDI_FAST_RUN 4
 #endif
+#ifndef VDI_FAST_LDGSTS
+#define VDI_FAST_LDGSTS 1
+#endif
 template <int NS>
 __global__ void __launch_bounds__(kFastThreads) merge_fast_kernel(MergeParams mp) {
   extern __shared__ float4 smem[];
@@ -612,7 +615,26 @@ __global__ void __launch_bounds__(kFastThreads) merge_fast_kernel(MergeParams mp
           start[s] = j;
           j += cnt[s];
         }
+#if VDI_FAST_LDGSTS
+        // every record straight into its slot of the image with async copies
+        // (LDGSTS): all of the list's loads in flight at once, no registers,
+        // no per-record source selection
+#pragma unroll
+        for (int s = 0; s < NS; ++s) {
+          if (s < n) {
+            const float2* dp = mp.src[s].depth + gidx[s];
+            const float4* cp = mp.src[s].rgba + gidx[s];
+            const uint32_t sd0 = smem_u32(my_depth + start[s]), sc0 = smem_u32(my_rgba + start[s]);
+            for (uint32_t jj = 0; jj < cnt[s]; ++jj) {
+              asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sd0 + jj * 8), "l"(dp + jj) : "memory");
+              asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sc0 + jj * 16), "l"(cp + jj) : "memory");
+            }
+          }
+        }
+        asm volatile("cp.async.wait_all;" ::: "memory");
+#else
         load_concat<NS, 4>(mp, gidx, cnt, start, m, my_depth, my_rgba, 1);
+#endif
         written = m;
         // already in depth order (e.g. a single PE's run)?  then only validate
         bool sorted = true;
