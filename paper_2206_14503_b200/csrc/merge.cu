@@ -830,6 +830,9 @@ __device__ __forceinline__ void gather_short_batch(const MergeParams& mp, uint32
   if (__any_sync(kFull, bk >= 0)) push_entries<NS>(mp, bk, p, m, goff, lane);
 }
 
+#ifndef VDI_SHORT_MEMO
+#define VDI_SHORT_MEMO 0  // measured slower on C3 (search 0.173 vs 0.166 ms): +6 instructions per sample, 255 registers
+#endif
 template <int MS>
 __device__ __forceinline__ void sweep_batch(const MergeParams& mp, int bucket, uint32_t batch) {
   const int lane = threadIdx.x;
@@ -855,6 +858,46 @@ __device__ __forceinline__ void sweep_batch(const MergeParams& mp, int bucket, u
     const float qnan = __int_as_float(0x7fc00000);
 #pragma unroll
     for (int q = 0; q < MS; ++q) S[q] = (q < mi && !bad) ? col[q * 32] : make_float4(qnan, qnan, qnan, qnan);
+#if VDI_SHORT_MEMO
+    // memoised bisection (as in the long-list sweep): a count sweep at g2
+    // takes the same decisions for every g2' in [L, U), so a later midpoint
+    // inside the interval of the latest sweep on either side of the bracket
+    // reuses its count; each lane resolves such levels on its own and the
+    // warp sweeps while any lane still needs a sweep
+    Bisection bs;
+    bs.init(mp.gamma_max, valid && !bad && mp.max_iters > 0);
+    for (;;) {
+      bs.advance(k, mp.max_iters);
+      if (!__any_sync(kFull, bs.active)) break;
+      const float g2 = bs.g2;
+      float ar = 0.f, ag = 0.f, ab = 0.f, aa = 0.f, L = -1.f, U = CUDART_INF_F;
+      int sc = 0;
+#pragma unroll
+      for (int q = 0; q < MS; ++q) {
+        if ((q & 7) == 0 && q > 0 && !__any_sync(kFull, bs.active && q < mi && sc <= k)) break;
+        const float4 sv = S[q];
+        const bool gap = sv.w < 0.f;  // NaN padding: false
+        const float sa = fabsf(sv.w);
+        const float n2 = fmaf(aa, aa, fmaf(ab, ab, fmaf(ag, ag, ar * ar)));  // dist2(acc, 0), Q8
+        const float d2 = dist2(ar, ag, ab, aa, sv.x, sv.y, sv.z, sa);
+        const bool gcl = gap & (n2 > g2);
+        const bool dsp = d2 > g2;
+        if (q > 0) {  // comparisons that did not happen contribute NaN (ignored by fminf / fmaxf)
+          U = fminf(U, fminf(gcl ? n2 : qnan, (!gcl & dsp) ? d2 : qnan));
+          L = fmaxf(L, fmaxf((gap & !gcl) ? n2 : qnan, (!gcl & !dsp) ? d2 : qnan));
+        }
+        const bool st = (q == 0) | gcl | dsp;
+        const float tr = 1.0f - aa;
+        ar = st ? sv.x : fmaf(tr, sv.x, ar);
+        ag = st ? sv.y : fmaf(tr, sv.y, ag);
+        ab = st ? sv.z : fmaf(tr, sv.z, ab);
+        aa = st ? sa : fmaf(tr, sa, aa);
+        sc += st ? 1 : 0;
+      }
+      if (bs.active) bs.swept(sc, L, U, k, mp.max_iters);
+    }
+    const float best = bs.best;
+#else
     bool active = valid && !bad && mp.max_iters > 0;
     float lo = 0.f, hi = mp.gamma_max, best = mp.gamma_max;
     for (int it = 0; it < mp.max_iters; ++it) {
@@ -894,6 +937,7 @@ __device__ __forceinline__ void sweep_batch(const MergeParams& mp, int bucket, u
         if (it + 1 >= mp.max_iters) active = false;
       }
     }
+#endif
     if (valid && !bad) {  // final write sweep, unrolled: static sample indices
       const float gg = best * best;
       float2* od = mp.out_depth + (size_t)p * k;
