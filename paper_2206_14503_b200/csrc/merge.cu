@@ -127,6 +127,22 @@ __device__ __forceinline__ float dist2(float ar, float ag, float ab, float aa, f
   return fmaf(da, da, fmaf(db, db, fmaf(dg, dg, dr * dr)));
 }
 
+// (|acc|^2, |acc - s|^2) as one packed f32x2 chain: the same four rounded
+// steps as dist2 on each half (FMUL2 + 3 FFMA2 instead of 8 scalar ops).
+__device__ __forceinline__ void n2d2_packed(float ar, float ag, float ab, float aa, float sr, float sg, float sb,
+                                            float sa, float& n2, float& d2) {
+  unsigned long long pr, pg, pb, pa, t;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(pr) : "f"(ar), "f"(ar - sr));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(pg) : "f"(ag), "f"(ag - sg));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(pb) : "f"(ab), "f"(ab - sb));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(pa) : "f"(aa), "f"(aa - sa));
+  asm("mul.rn.f32x2 %0, %1, %1;" : "=l"(t) : "l"(pr));
+  asm("fma.rn.f32x2 %0, %1, %1, %2;" : "=l"(t) : "l"(pg), "l"(t));
+  asm("fma.rn.f32x2 %0, %1, %1, %2;" : "=l"(t) : "l"(pb), "l"(t));
+  asm("fma.rn.f32x2 %0, %1, %1, %2;" : "=l"(t) : "l"(pa), "l"(t));
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(n2), "=f"(d2) : "l"(t));
+}
+
 // One greedy sweep over depth-ordered samples (
 // Q1, Q2, Q8).  get(i) returns sample i.  Count mode (od == nullptr) returns
 // early once cnt > k.  Write mode writes the closed segments to od/oc[0..cnt).
@@ -830,8 +846,11 @@ __device__ __forceinline__ void gather_short_batch(const MergeParams& mp, uint32
   if (__any_sync(kFull, bk >= 0)) push_entries<NS>(mp, bk, p, m, goff, lane);
 }
 
+#ifndef VDI_PACKED_D2
+#define VDI_PACKED_D2 1  // alone: 0.173 vs 0.166 ms (the packed chain is longer); with the memo it frees the registers
+#endif
 #ifndef VDI_SHORT_MEMO
-#define VDI_SHORT_MEMO 0  // measured slower on C3 (search 0.173 vs 0.166 ms): +6 instructions per sample, 255 registers
+#define VDI_SHORT_MEMO 1  // with VDI_PACKED_D2: search 0.1637 vs 0.1658 ms (alone: 0.173, slower)
 #endif
 template <int MS>
 __device__ __forceinline__ void sweep_batch(const MergeParams& mp, int bucket, uint32_t batch) {
@@ -878,8 +897,13 @@ __device__ __forceinline__ void sweep_batch(const MergeParams& mp, int bucket, u
         const float4 sv = S[q];
         const bool gap = sv.w < 0.f;  // NaN padding: false
         const float sa = fabsf(sv.w);
+#if VDI_PACKED_D2
+        float n2, d2;
+        n2d2_packed(ar, ag, ab, aa, sv.x, sv.y, sv.z, sa, n2, d2);
+#else
         const float n2 = fmaf(aa, aa, fmaf(ab, ab, fmaf(ag, ag, ar * ar)));  // dist2(acc, 0), Q8
         const float d2 = dist2(ar, ag, ab, aa, sv.x, sv.y, sv.z, sa);
+#endif
         const bool gcl = gap & (n2 > g2);
         const bool dsp = d2 > g2;
         if (q > 0) {  // comparisons that did not happen contribute NaN (ignored by fminf / fmaxf)
@@ -917,8 +941,13 @@ __device__ __forceinline__ void sweep_batch(const MergeParams& mp, int bucket, u
         const float4 sv = S[q];
         const bool gap = sv.w < 0.f;  // NaN padding: false
         const float sa = fabsf(sv.w);
+#if VDI_PACKED_D2
+        float n2, d2;  // dist2(acc, 0) (Q8) and dist2(acc, s), packed
+        n2d2_packed(ar, ag, ab, aa, sv.x, sv.y, sv.z, sa, n2, d2);
+#else
         const float n2 = fmaf(aa, aa, fmaf(ab, ab, fmaf(ag, ag, ar * ar)));  // dist2(acc, 0), Q8
         const float d2 = dist2(ar, ag, ab, aa, sv.x, sv.y, sv.z, sa);
+#endif
         const bool st = (q == 0) | (gap & (n2 > g2)) | (d2 > g2);  // open before q is (q > 0)
         const float tr = 1.0f - aa;
         ar = st ? sv.x : fmaf(tr, sv.x, ar);
