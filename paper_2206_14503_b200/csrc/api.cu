@@ -356,8 +356,8 @@ static vdi_status merge_lists(vdi_ctx* ctx, MergeParams& mp, uint64_t P, uint64_
   // 2/3 has m > 40, so the pool needs at most 24 B x (S_here + 32 x batches
   // of padding); batches <= S_here / 41 / 32 + 1 per bucket
   const uint64_t lb = S_here / 41 / 32 + 2;
-  // + 16 rows x 32 lanes x 16 B of slack: the long sweeps read up to 16 rows past a list's end
-  const unsigned long long lcap = 24ull * S_here * 2 + lb * 2 * (128 + 24 * 32) + 4096 + 16 * 32 * 16;
+  // + 32 rows x 32 lanes x 16 B of slack: the long sweeps read up to 24 rows past a list's end
+  const unsigned long long lcap = 24ull * S_here * 2 + lb * 2 * (128 + 24 * 32) + 4096 + 32 * 32 * 16;
   CUDA_TRY(ctx, ctx->lpool.grow(lcap));
   CUDA_TRY(ctx, ctx->lbatch.grow((size_t)(P / 32 + 2) * 2 * 16));
   mp.long_pool = ctx->lpool.as<char>();

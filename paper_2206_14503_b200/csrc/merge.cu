@@ -1228,7 +1228,7 @@ __device__ __forceinline__ void long_step8(const float4 (&v)[8], int q0, int m, 
 
 // One count-mode sweep over a pool column: chunks of 8 samples in two register
 // buffers (the next chunk's loads are in flight while one is swept; ping-pong,
-// no copies), leaving as soon as the count exceeds k.  Reads up to 16 rows past
+// no copies), leaving as soon as the count exceeds k.  Reads up to 24 rows past
 // m (the pool has slack for that).
 __device__ __forceinline__ int long_count(const float4* __restrict__ col, int m, float g2, int k, float& L,
                                           float& U) {
@@ -1236,13 +1236,18 @@ __device__ __forceinline__ int long_count(const float4* __restrict__ col, int m,
   int sc = 0;
   L = -1.f;
   U = CUDART_INF_F;
-  float4 A[8], B[8];
+  // three register chunks in rotation: the loads run two chunks (16 samples)
+  // ahead of the sweep, which covers the L2 latency of the pool
+  float4 A[8], B[8], C[8];
 #pragma unroll
-  for (int u = 0; u < 8; ++u) A[u] = col[u * 32];
-  const float4* pp = col + 8 * 32;
+  for (int u = 0; u < 8; ++u) {
+    A[u] = col[u * 32];
+    B[u] = col[(8 + u) * 32];
+  }
+  const float4* pp = col + 16 * 32;
   for (int q0 = 0;;) {
 #pragma unroll
-    for (int u = 0; u < 8; ++u) B[u] = pp[u * 32];
+    for (int u = 0; u < 8; ++u) C[u] = pp[u * 32];
     pp += 8 * 32;
     long_step8(A, q0, m, g2, ar, ag, ab, aa, sc, L, U);
     q0 += 8;
@@ -1251,6 +1256,12 @@ __device__ __forceinline__ int long_count(const float4* __restrict__ col, int m,
     for (int u = 0; u < 8; ++u) A[u] = pp[u * 32];
     pp += 8 * 32;
     long_step8(B, q0, m, g2, ar, ag, ab, aa, sc, L, U);
+    q0 += 8;
+    if (q0 >= m || sc > k) break;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) B[u] = pp[u * 32];
+    pp += 8 * 32;
+    long_step8(C, q0, m, g2, ar, ag, ab, aa, sc, L, U);
     q0 += 8;
     if (q0 >= m || sc > k) break;
   }
