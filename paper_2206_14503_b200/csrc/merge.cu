@@ -1268,6 +1268,66 @@ __device__ __forceinline__ int long_count(const float4* __restrict__ col, int m,
   return sc;
 }
 
+// The final write sweep over a pool column (same decisions and output as
+// sweep(), the gap taken from the sign of alpha): rgba and depth in chunks of
+// 8 with the next chunk's loads in flight, so the sweep does not wait on one
+// L2 round trip per sample.
+__device__ __forceinline__ int long_write(const float4* __restrict__ col, const float2* __restrict__ dcol, int m,
+                                          float gamma, int k, float2* od, float4* oc) {
+  const float gg = gamma * gamma;
+  float ar = 0.f, ag = 0.f, ab = 0.f, aa = 0.f, tf = 0.f, tb = 0.f;
+  int c = 0;
+  float4 cv[8], cn[8];
+  float2 dv[8], dn[8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    cv[u] = col[u * 32];
+    dv[u] = dcol[u * 32];
+  }
+  for (int q0 = 0; q0 < m; q0 += 8) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      cn[u] = col[(q0 + 8 + u) * 32];
+      dn[u] = dcol[(q0 + 8 + u) * 32];
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int q = q0 + u;
+      if (q < m) {
+        const float4 sv = cv[u];
+        const float2 d = dv[u];
+        const bool gap = sv.w < 0.f;
+        const float sa = fabsf(sv.w);
+        const float n2 = fmaf(aa, aa, fmaf(ab, ab, fmaf(ag, ag, ar * ar)));
+        const float d2 = dist2(ar, ag, ab, aa, sv.x, sv.y, sv.z, sa);
+        const bool st = (q == 0) | (gap & (n2 > gg)) | (d2 > gg);
+        if (st && q > 0 && c <= k) {  // close the open segment (ends at its last content sample)
+          od[c - 1] = make_float2(tf, tb);
+          oc[c - 1] = make_float4(ar, ag, ab, aa);
+        }
+        const float tr = 1.0f - aa;
+        ar = st ? sv.x : fmaf(tr, sv.x, ar);
+        ag = st ? sv.y : fmaf(tr, sv.y, ag);
+        ab = st ? sv.z : fmaf(tr, sv.z, ab);
+        aa = st ? sa : fmaf(tr, sa, aa);
+        tf = st ? d.x : tf;
+        tb = d.y;
+        c += st ? 1 : 0;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      cv[u] = cn[u];
+      dv[u] = dn[u];
+    }
+  }
+  if (m > 0 && c <= k) {
+    od[c - 1] = make_float2(tf, tb);
+    oc[c - 1] = make_float4(ar, ag, ab, aa);
+  }
+  return c;
+}
+
 #ifndef VDI_LONG_WPS
 #define VDI_LONG_WPS 16  // resident long-sweep warps per SM
 #endif
@@ -1304,12 +1364,7 @@ __global__ void __launch_bounds__(32) long_sweep_kernel(MergeParams mp) {
       bs.swept(c, L, U, k, mp.max_iters);
     }
     const float best = bs.best;
-    auto get = [&](int q) {
-      const float4 c = col[q * 32];
-      const float2 d = dcol[q * 32];
-      return Rec{d.x, d.y, c.x, c.y, c.z, fabsf(c.w)};
-    };
-    const int c = sweep(get, m, best, k, mp.out_depth + (size_t)p * k, mp.out_rgba + (size_t)p * k);
+    const int c = long_write(col, dcol, m, best, k, mp.out_depth + (size_t)p * k, mp.out_rgba + (size_t)p * k);
     mp.out_count[p] = (uint8_t)c;
     if (mp.stat_gamma) mp.stat_gamma[p] = best;
   }
