@@ -1328,12 +1328,84 @@ __device__ __forceinline__ int long_write(const float4* __restrict__ col, const 
   return c;
 }
 
+// Few long lists (C4: ~1000 at 1080p) leave the lane-per-list sweep latency
+// bound: ~34 warps on the whole GPU, each lane running ~10 dependent sweeps.
+// Then every list gets a warp: lane j (heap node j + 1 of the next five
+// bisection levels) evaluates the midpoint the sequential procedure would
+// reach along that path (the same fp32 mid = 0.5 (lo + hi) recurrence), all
+// lanes sweep the same samples (broadcast loads), and the warp walks the five
+// levels with the counts, stopping where the procedure stops (count == k_out,
+// or I iterations).  Same gamma*, same output.
+#ifndef VDI_SPEC_MAX
+#define VDI_SPEC_MAX 8192
+#endif
+__global__ void __launch_bounds__(32) long_spec_kernel(MergeParams mp) {
+  const int lane = threadIdx.x;
+  const int k = mp.k_out, n = mp.n_src;
+  const uint32_t c2 = min(mp.wl_count[2], mp.wl_cap), c3 = min(mp.wl_count[3], mp.wl_cap);
+  if (c2 + c3 > VDI_SPEC_MAX) return;  // long_sweep_kernel takes them (lane per list)
+  const uint32_t jn = lane < 31 ? (uint32_t)lane + 1 : 1u;  // heap node of this lane
+  const int depth = 31 - __clz(jn);
+  for (;;) {
+    uint32_t t = 0;
+    if (lane == 0) t = atomicAdd(&mp.search_ticket[4], 1u);
+    t = __shfl_sync(kFull, t, 0);
+    if (t >= c2 + c3) break;
+    const int bucket = t < c3 ? 3 : 2;
+    const uint32_t e = t < c3 ? t : t - c3;
+    const PoolBatch pb = mp.long_batch[bucket - 2][e >> 5];
+    if (!pb.ok) continue;
+    const uint32_t* ent = mp.wl[bucket] + (size_t)e * (3 + n);
+    const uint32_t p = ent[0];
+    const int m = (int)ent[2];
+    const char* base = mp.long_pool + pb.off;
+    const uint32_t l = e & 31;
+    const float4* col = reinterpret_cast<const float4*>(base) + l;
+    const float2* dcol = reinterpret_cast<const float2*>(base + (size_t)pb.maxm * 32 * 16) + l;
+    const bool bad = reinterpret_cast<const uint32_t*>(base + (size_t)pb.maxm * 32 * 24)[l] != 0u;
+    if (bad) continue;
+    float lo = 0.f, hi = mp.gamma_max, best = mp.gamma_max;
+    int it = 0;
+    bool done = mp.max_iters <= 0;
+    while (!done) {
+      float lw = lo, hg = hi, md = 0.5f * (lw + hg);
+      for (int b = depth - 1; b >= 0; --b) {  // bit 1: count > k (lo = mid), bit 0: count <= k (hi = mid)
+        if ((jn >> b) & 1u) lw = md;
+        else hg = md;
+        md = 0.5f * (lw + hg);
+      }
+      float L, U;
+      const int c = long_count(col, m, md * md, k, L, U);
+      uint32_t node = 1;
+      for (int lev = 0; lev < 5 && !done; ++lev) {
+        const int cn = __shfl_sync(kFull, c, (int)node - 1);
+        const float mid = __shfl_sync(kFull, md, (int)node - 1);
+        if (cn <= k) {
+          best = hi = mid;
+          if (cn == k) done = true;
+          node = 2 * node;
+        } else {
+          lo = mid;
+          node = 2 * node + 1;
+        }
+        if (++it >= mp.max_iters) done = true;
+      }
+    }
+    if (lane == 0) {
+      const int c = long_write(col, dcol, m, best, k, mp.out_depth + (size_t)p * k, mp.out_rgba + (size_t)p * k);
+      mp.out_count[p] = (uint8_t)c;
+      if (mp.stat_gamma) mp.stat_gamma[p] = best;
+    }
+  }
+}
+
 #ifndef VDI_LONG_WPS
 #define VDI_LONG_WPS 16  // resident long-sweep warps per SM
 #endif
 __global__ void __launch_bounds__(32) long_sweep_kernel(MergeParams mp) {
   const int k = mp.k_out, n = mp.n_src;
   const uint32_t c2 = min(mp.wl_count[2], mp.wl_cap), c3 = min(mp.wl_count[3], mp.wl_cap);
+  if (c2 + c3 <= VDI_SPEC_MAX) return;  // long_spec_kernel took them (warp per list)
   // every lane claims its own lists (lanes diverge freely here: no warp
   // collectives), the longest bucket first, so a lane that finishes early
   // takes the next list instead of idling until the warp's longest list ends
@@ -1707,6 +1779,9 @@ static cudaError_t launch_search_ns(const MergeParams& mp, cudaStream_t st, int*
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   ++*launches;
   long_sweep_kernel<<<sm_count() * VDI_LONG_WPS, 32, 0, st>>>(mp);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  ++*launches;
+  long_spec_kernel<<<sm_count() * 16, 32, 0, st>>>(mp);
   ++*launches;
   return cudaGetLastError();
 }
