@@ -1339,11 +1339,10 @@ __device__ __forceinline__ int long_write(const float4* __restrict__ col, const 
 #ifndef VDI_SPEC_MAX
 #define VDI_SPEC_MAX 8192
 #endif
-__global__ void __launch_bounds__(32) long_spec_kernel(MergeParams mp) {
+__device__ __forceinline__ void long_spec_body(const MergeParams& mp) {
   const int lane = threadIdx.x;
   const int k = mp.k_out, n = mp.n_src;
   const uint32_t c2 = min(mp.wl_count[2], mp.wl_cap), c3 = min(mp.wl_count[3], mp.wl_cap);
-  if (c2 + c3 > VDI_SPEC_MAX) return;  // long_sweep_kernel takes them (lane per list)
   const uint32_t jn = lane < 31 ? (uint32_t)lane + 1 : 1u;  // heap node of this lane
   const int depth = 31 - __clz(jn);
   for (;;) {
@@ -1405,7 +1404,10 @@ __global__ void __launch_bounds__(32) long_spec_kernel(MergeParams mp) {
 __global__ void __launch_bounds__(32) long_sweep_kernel(MergeParams mp) {
   const int k = mp.k_out, n = mp.n_src;
   const uint32_t c2 = min(mp.wl_count[2], mp.wl_cap), c3 = min(mp.wl_count[3], mp.wl_cap);
-  if (c2 + c3 <= VDI_SPEC_MAX) return;  // long_spec_kernel took them (warp per list)
+  if (c2 + c3 <= VDI_SPEC_MAX) {  // few lists: a warp per list
+    long_spec_body(mp);
+    return;
+  }
   // every lane claims its own lists (lanes diverge freely here: no warp
   // collectives), the longest bucket first, so a lane that finishes early
   // takes the next list instead of idling until the warp's longest list ends
@@ -1779,9 +1781,6 @@ static cudaError_t launch_search_ns(const MergeParams& mp, cudaStream_t st, int*
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   ++*launches;
   long_sweep_kernel<<<sm_count() * VDI_LONG_WPS, 32, 0, st>>>(mp);
-  if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  ++*launches;
-  long_spec_kernel<<<sm_count() * 16, 32, 0, st>>>(mp);
   ++*launches;
   return cudaGetLastError();
 }
