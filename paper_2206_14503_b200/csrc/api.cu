@@ -206,8 +206,13 @@ __global__ void __launch_bounds__(256) peer_copy_kernel(const CopySeg* __restric
 
 __global__ void gather_bounds_kernel(const uint32_t* const* offs, const uint32_t* pes, int n_local,
                                      const uint32_t* rows, int G, uint32_t W, int n_pes,
-                                     unsigned long long* bnd) {
-  // bnd[pe][g] = offset_pe[rows[g] * W]  (g = 0..G)
+                                     unsigned long long* bnd, size_t hdr_stride = 0, size_t bnd_stride = 0) {
+  // bnd[pe][g] = offset_pe[rows[g] * W]  (g = 0..G); block b handles frame b
+  // (headers hdr_stride bytes apart, bnd blocks bnd_stride entries apart)
+  offs = reinterpret_cast<const uint32_t* const*>(reinterpret_cast<const char*>(offs) + blockIdx.x * hdr_stride);
+  pes = reinterpret_cast<const uint32_t*>(reinterpret_cast<const char*>(pes) + blockIdx.x * hdr_stride);
+  rows = reinterpret_cast<const uint32_t*>(reinterpret_cast<const char*>(rows) + blockIdx.x * hdr_stride);
+  bnd += blockIdx.x * bnd_stride;
   for (int i = threadIdx.x; i < n_local * (G + 1); i += blockDim.x) {
     const int l = i / (G + 1), g = i % (G + 1);
     bnd[(size_t)pes[l] * (G + 1) + g] = offs[l][(size_t)rows[g] * W];
@@ -944,12 +949,12 @@ vdi_status vdi_composite_frames(vdi_ctx* ctx, uint32_t F, const vdi_dense_view* 
   if (G > 1)
     CUDA_TRY(ctx, cudaMemcpyAsync(dblob + refs_off, myrefs.data(), myrefs.size() * sizeof(IpcRef),
                                   cudaMemcpyHostToDevice, st));
-  for (uint32_t f = 0; f < F; ++f) {
-    const uint8_t* dh = dblob + blob + (size_t)f * hdr;
-    gather_bounds_kernel<<<1, 256, 0, st>>>(reinterpret_cast<const uint32_t* const*>(dh),
+  {  // one launch for every frame
+    const uint8_t* dh = dblob + blob;
+    gather_bounds_kernel<<<F, 256, 0, st>>>(reinterpret_cast<const uint32_t* const*>(dh),
                                             reinterpret_cast<const uint32_t*>(dh + 64 * 8), (int)n_local,
                                             reinterpret_cast<const uint32_t*>(dh + 64 * 8 + 64 * 4), (int)C, W,
-                                            (int)n, reinterpret_cast<unsigned long long*>(dblob) + (size_t)f * nb);
+                                            (int)n, reinterpret_cast<unsigned long long*>(dblob), hdr, nb);
     ++launches;
   }
   CUDA_TRY(ctx, cudaGetLastError());
