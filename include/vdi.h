@@ -236,6 +236,22 @@ typedef struct {
 vdi_status vdi_composite_host_dense(vdi_ctx* ctx, const vdi_dense_view* local_pes, uint32_t n_local,
                                     vdi_dense_strip* out);
 
+/* vdi_composite_host_dense over n_frames independent frames (the serving
+ * loop: a new set of host sub-VDIs per frame), pipelined: frame f's
+ * host->device copies overlap frame f-1's compositing and frame f-2's
+ * device->host copies (two copy streams, double-buffered device inputs and
+ * dense outputs).  local_pes is frame-major [n_frames][n_local] (host
+ * pointers, read until the call returns); outs[n_frames] as for
+ * vdi_composite_host_dense (host buffers; one buffer may serve several
+ * frames only if the caller accepts that the last frame wins).  Each frame's
+ * result is identical to a vdi_composite_host_dense call on its inputs
+ * (PAPER.md:113-115, :164-185).  Device scratch: two input slots and two
+ * output slots of the strip's full capacity (rows*W*k_out*24 B each), grow-only.
+ * VDI_ERR_CAPACITY (after every frame ran) if a frame's total exceeds its
+ * outs[f].capacity; outs[f].total is set for every frame.  Synchronises. */
+vdi_status vdi_composite_host_dense_frames(vdi_ctx* ctx, uint32_t n_frames, const vdi_dense_view* local_pes,
+                                           uint32_t n_local, vdi_dense_strip* outs);
+
 /* Gather of the composited strips onto vdi_config.root (PAPER.md:185
  * MPI_Gather; Q14): image_out (rows [0, H), root only; ignored elsewhere)
  * receives every rank's strip at its rows.  Default: each rank sends its counts + packed records

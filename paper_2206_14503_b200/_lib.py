@@ -93,6 +93,8 @@ SIGNATURES = {
     "vdi_dense_to_full": (C.c_int, [C.c_void_p, C.POINTER(vdi_dense_view), C.POINTER(vdi_full_view)]),
     "vdi_composite_host_dense": (C.c_int, [C.c_void_p, C.POINTER(vdi_dense_view), C.c_uint32,
                                            C.POINTER(vdi_dense_strip)]),
+    "vdi_composite_host_dense_frames": (C.c_int, [C.c_void_p, C.c_uint32, C.POINTER(vdi_dense_view), C.c_uint32,
+                                                  C.POINTER(vdi_dense_strip)]),
     "vdi_gather": (C.c_int, [C.c_void_p, C.POINTER(vdi_full_view), C.POINTER(vdi_full_view)]),
     "vdi_pixel_stats": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "vdi_get_counters": (C.c_int, [C.c_void_p, C.POINTER(vdi_counters)]),

@@ -218,6 +218,24 @@ class Compositor:
                 "vdi_composite_host_dense")
         return int(out.total)
 
+    def composite_host_dense_frames(self, frames, outs) -> list:
+        """vdi_composite_host_dense_frames: frames = [[host DenseSubVDI per local PE]
+        per frame], outs = [(count, depth, rgba) host tensors per frame]; H2D,
+        compositing and D2H of consecutive frames overlap.  Returns the
+        supersegment total of every frame."""
+        F = len(frames)
+        n_local = len(frames[0]) if F else 0
+        if any(len(fr) != n_local for fr in frames) or len(outs) != F:
+            raise ValueError("every frame needs the same number of local PEs and one output")
+        flat = [p.view() for fr in frames for p in fr]
+        views = (L.vdi_dense_view * max(1, len(flat)))(*flat)
+        ov = (L.vdi_dense_strip * max(1, F))(*[
+            L.vdi_dense_strip(self.row_begin, self.row_end, d.shape[0], 0, _ptr(c), _ptr(d), _ptr(r))
+            for c, d, r in outs])
+        L.check(self.lib.vdi_composite_host_dense_frames(self.ctx, F, views, n_local, ov),
+                "vdi_composite_host_dense_frames")
+        return [int(ov[f].total) for f in range(F)]
+
     def gather(self, strip: FullVDI, image: FullVDI | None):
         """vdi_gather: strips -> the root rank (image ignored on other ranks)."""
         sv = strip.view()

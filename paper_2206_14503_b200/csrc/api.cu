@@ -116,6 +116,13 @@ struct vdi_ctx {
   // host e2e staging
   std::vector<DevBuf> hcount, hoffset, hdepth, hrgba;
   DevBuf hstrip_count, hstrip_depth, hstrip_rgba;
+  // vdi_composite_host_dense_frames: the second input slot, per-slot dense
+  // outputs, the H2D / D2H streams and their slot events
+  std::vector<DevBuf> hcount1, hoffset1, hdepth1, hrgba1;
+  DevBuf pcount[2], pdense[2];
+  cudaStream_t pin_st = nullptr, pout_st = nullptr;
+  cudaEvent_t pev_in[2] = {}, pev_used[2] = {}, pev_tot[2] = {}, pev_comp[2] = {}, pev_out[2] = {};
+  unsigned long long* ptot = nullptr;  // pinned host [2]
   // counters
   vdi_counters last{};
   bool have_stats = false;
@@ -126,6 +133,14 @@ struct vdi_ctx {
   cudaEvent_t fev[2] = {nullptr, nullptr};  // frames mode: pull start / end
   bool frames_timing_pending = false;
   ~vdi_ctx() {
+    if (pin_st) cudaStreamSynchronize(pin_st);
+    if (pout_st) cudaStreamSynchronize(pout_st);
+    if (pin_st) cudaStreamDestroy(pin_st);
+    if (pout_st) cudaStreamDestroy(pout_st);
+    for (cudaEvent_t* a : {pev_in, pev_used, pev_tot, pev_comp, pev_out})
+      for (int i = 0; i < 2; ++i)
+        if (a[i]) cudaEventDestroy(a[i]);
+    if (ptot) cudaFreeHost(ptot);
     if (cub_tmp) cudaFree(cub_tmp);
     for (auto& x : xs)
       if (x) cudaStreamDestroy(x);
@@ -503,6 +518,10 @@ vdi_status vdi_composite_init(const vdi_config* cfg, vdi_ctx** out) {
   ctx->hoffset.resize(cfg->n_pes);
   ctx->hdepth.resize(cfg->n_pes);
   ctx->hrgba.resize(cfg->n_pes);
+  ctx->hcount1.resize(cfg->n_pes);
+  ctx->hoffset1.resize(cfg->n_pes);
+  ctx->hdepth1.resize(cfg->n_pes);
+  ctx->hrgba1.resize(cfg->n_pes);
   for (auto& ev : ctx->ev) cudaEventCreate(&ev);
   for (auto& ev : ctx->gev) cudaEventCreate(&ev);
   for (auto& ev : ctx->fev) cudaEventCreate(&ev);
@@ -1455,34 +1474,40 @@ vdi_status vdi_gather(vdi_ctx* ctx, const vdi_full_view* strip, vdi_full_view* i
 }
 
 // host sub-VDIs -> ctx-owned device copies (H2D on the ctx stream); dv gets device views
+// H2D of the host sub-VDIs into input slot `set` (0: the single-frame
+// entries; 0/1: the double-buffered frames pipeline), on stream st
 static vdi_status upload_host_pes(vdi_ctx* ctx, const vdi_dense_view* local, uint32_t n_local,
-                                  std::vector<vdi_dense_view>& dv) {
+                                  std::vector<vdi_dense_view>& dv, int set = 0, cudaStream_t st = nullptr) {
   const vdi_config& cf = ctx->cfg;
   if (n_local && !local) return fail(VDI_ERR_INVALID_ARG, "local_pes is NULL");
   if (n_local > cf.n_pes) return fail(VDI_ERR_INVALID_ARG, "too many local PEs");
-  cudaStream_t st = ctx->stream;
+  if (!st) st = ctx->stream;
+  std::vector<DevBuf>& hcount = set ? ctx->hcount1 : ctx->hcount;
+  std::vector<DevBuf>& hoffset = set ? ctx->hoffset1 : ctx->hoffset;
+  std::vector<DevBuf>& hdepth = set ? ctx->hdepth1 : ctx->hdepth;
+  std::vector<DevBuf>& hrgba = set ? ctx->hrgba1 : ctx->hrgba;
   const size_t P = (size_t)cf.width * cf.height;
   dv.assign(n_local, vdi_dense_view{});
   for (uint32_t l = 0; l < n_local; ++l) {
     const vdi_dense_view& v = local[l];
     if (!v.count || (v.total && (!v.depth || !v.rgba)) || (cf.n_ranks > 1 && !v.offset))
       return fail(VDI_ERR_INVALID_ARG, "host view %u has NULL arrays", l);
-    CUDA_TRY(ctx, ctx->hcount[l].grow(P));
-    CUDA_TRY(ctx, ctx->hdepth[l].grow(std::max<uint64_t>(v.total, 1) * 8));
-    CUDA_TRY(ctx, ctx->hrgba[l].grow(std::max<uint64_t>(v.total, 1) * 16));
-    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->hcount[l].p, v.count, P, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(ctx, hcount[l].grow(P));
+    CUDA_TRY(ctx, hdepth[l].grow(std::max<uint64_t>(v.total, 1) * 8));
+    CUDA_TRY(ctx, hrgba[l].grow(std::max<uint64_t>(v.total, 1) * 16));
+    CUDA_TRY(ctx, cudaMemcpyAsync(hcount[l].p, v.count, P, cudaMemcpyHostToDevice, st));
     if (v.total) {
-      CUDA_TRY(ctx, cudaMemcpyAsync(ctx->hdepth[l].p, v.depth, v.total * 8, cudaMemcpyHostToDevice, st));
-      CUDA_TRY(ctx, cudaMemcpyAsync(ctx->hrgba[l].p, v.rgba, v.total * 16, cudaMemcpyHostToDevice, st));
+      CUDA_TRY(ctx, cudaMemcpyAsync(hdepth[l].p, v.depth, v.total * 8, cudaMemcpyHostToDevice, st));
+      CUDA_TRY(ctx, cudaMemcpyAsync(hrgba[l].p, v.rgba, v.total * 16, cudaMemcpyHostToDevice, st));
     }
     dv[l] = v;
-    dv[l].count = ctx->hcount[l].as<uint8_t>();
-    dv[l].depth = ctx->hdepth[l].as<float>();
-    dv[l].rgba = ctx->hrgba[l].as<float>();
+    dv[l].count = hcount[l].as<uint8_t>();
+    dv[l].depth = hdepth[l].as<float>();
+    dv[l].rgba = hrgba[l].as<float>();
     if (cf.n_ranks > 1) {
-      CUDA_TRY(ctx, ctx->hoffset[l].grow((P + 1) * 4));
-      CUDA_TRY(ctx, cudaMemcpyAsync(ctx->hoffset[l].p, v.offset, (P + 1) * 4, cudaMemcpyHostToDevice, st));
-      dv[l].offset = ctx->hoffset[l].as<uint32_t>();
+      CUDA_TRY(ctx, hoffset[l].grow((P + 1) * 4));
+      CUDA_TRY(ctx, cudaMemcpyAsync(hoffset[l].p, v.offset, (P + 1) * 4, cudaMemcpyHostToDevice, st));
+      dv[l].offset = hoffset[l].as<uint32_t>();
     } else {
       dv[l].offset = nullptr;
     }
@@ -1568,6 +1593,131 @@ vdi_status vdi_composite_host_dense(vdi_ctx* ctx, const vdi_dense_view* local, u
   CUDA_TRY(ctx, cudaStreamSynchronize(st));
   ctx->last.kernel_launches += (uint32_t)launches;
   return VDI_OK;
+}
+
+// Pipelined vdi_composite_host_dense over independent frames: frame f's H2D
+// (stream pin_st, input slot f&1) overlaps frame f-1's compositing (ctx
+// stream) and frame f-2's D2H (stream pout_st, output slot f&1).  Each frame
+// is exactly one vdi_composite + dense compaction, as in the single call.
+vdi_status vdi_composite_host_dense_frames(vdi_ctx* ctx, uint32_t F, const vdi_dense_view* local, uint32_t n_local,
+                                           vdi_dense_strip* outs) {
+  if (vdi_status s = check_ctx(ctx)) return s;
+  const vdi_config& cf = ctx->cfg;
+  if (F == 0) return VDI_OK;
+  if (!outs || (n_local && !local)) return fail(VDI_ERR_INVALID_ARG, "outs / local_pes is NULL");
+  for (uint32_t f = 0; f < F; ++f) {
+    const vdi_dense_strip& o = outs[f];
+    if (!o.count || (o.capacity && (!o.depth || !o.rgba))) return fail(VDI_ERR_INVALID_ARG, "outs[%u] is NULL", f);
+    if (o.row_begin != ctx->row0 || o.row_end != ctx->row1)
+      return fail(VDI_ERR_CAPACITY, "outs[%u] rows do not match this rank's strip", f);
+  }
+  cudaStream_t st = ctx->stream;
+  if (!ctx->pin_st) {
+    CUDA_TRY(ctx, cudaStreamCreateWithFlags(&ctx->pin_st, cudaStreamNonBlocking));
+    CUDA_TRY(ctx, cudaStreamCreateWithFlags(&ctx->pout_st, cudaStreamNonBlocking));
+    for (cudaEvent_t* a : {ctx->pev_in, ctx->pev_used, ctx->pev_tot, ctx->pev_comp, ctx->pev_out})
+      for (int i = 0; i < 2; ++i) CUDA_TRY(ctx, cudaEventCreateWithFlags(&a[i], cudaEventDisableTiming));
+    CUDA_TRY(ctx, cudaHostAlloc(reinterpret_cast<void**>(&ctx->ptot), 2 * sizeof(unsigned long long),
+                                cudaHostAllocDefault));
+  }
+  const size_t Ps = ctx->P, k = cf.k_out, Tmax = std::max<size_t>(Ps * k, 1);  // a strip holds <= Ps*k
+  CUDA_TRY(ctx, ctx->hstrip_count.grow(Ps));
+  CUDA_TRY(ctx, ctx->hstrip_depth.grow(Ps * k * 8));
+  CUDA_TRY(ctx, ctx->hstrip_rgba.grow(Ps * k * 16));
+  const size_t ng = (Ps + 31) / 32;
+  CUDA_TRY(ctx, ctx->xsum.grow(((size_t)scan_chunks((uint32_t)std::max<size_t>(Ps, 1)) + 8) * 4));
+  CUDA_TRY(ctx, ctx->xbase.grow((ng + 8) * 4));
+  CUDA_TRY(ctx, ctx->xtot.grow(64));
+  for (int i = 0; i < 2; ++i) {
+    CUDA_TRY(ctx, ctx->pcount[i].grow(std::max<size_t>(Ps, 1)));
+    CUDA_TRY(ctx, ctx->pdense[i].grow(Tmax * 24));
+  }
+  vdi_full_view ds{ctx->row0, ctx->row1, ctx->hstrip_count.as<uint8_t>(), ctx->hstrip_depth.as<float>(),
+                   ctx->hstrip_rgba.as<float>()};
+  std::vector<vdi_dense_view> dv[2];
+  int launches = 0;
+  // H2D of frame f into slot f&1, once the compositing of frame f-2 has read it
+  auto h2d = [&](uint32_t f) -> vdi_status {
+    const int sl = f & 1;
+    CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->pin_st, ctx->pev_used[sl], 0));
+    if (vdi_status s = upload_host_pes(ctx, local + (size_t)f * n_local, n_local, dv[sl], sl, ctx->pin_st)) return s;
+    CUDA_TRY(ctx, cudaEventRecord(ctx->pev_in[sl], ctx->pin_st));
+    return VDI_OK;
+  };
+  // composite + dense compaction of frame f into output slot f&1
+  auto compute = [&](uint32_t f) -> vdi_status {
+    const int sl = f & 1;
+    CUDA_TRY(ctx, cudaStreamWaitEvent(st, ctx->pev_in[sl], 0));
+    if (vdi_status s = vdi_composite(ctx, dv[sl].data(), n_local, &ds)) return s;
+    CUDA_TRY(ctx, cudaEventRecord(ctx->pev_used[sl], st));
+    MergeParams ms{};
+    ms.n_src = 1;
+    ms.P = (uint32_t)Ps;
+    ms.n_groups = (uint32_t)ng;
+    ms.src[0].count = ds.count;
+    unsigned long long* dtot = ctx->xtot.as<unsigned long long>();
+    if (Ps) {
+      CUDA_TRY(ctx, launch_scan(ms, ctx->xsum.as<uint32_t>(), ctx->xbase.as<uint32_t>(), st, &launches));
+      CUDA_TRY(ctx, launch_total(ms, ctx->xsum.as<uint32_t>(), dtot, st, &launches));
+      CUDA_TRY(ctx, cudaMemcpyAsync(ctx->ptot + sl, dtot, 8, cudaMemcpyDeviceToHost, st));
+    } else {
+      ctx->ptot[sl] = 0;
+    }
+    CUDA_TRY(ctx, cudaEventRecord(ctx->pev_tot[sl], st));
+    CUDA_TRY(ctx, cudaStreamWaitEvent(st, ctx->pev_out[sl], 0));  // frame f-2's D2H has read the slot
+    float4* dc4 = ctx->pdense[sl].as<float4>();
+    float2* dd2 = reinterpret_cast<float2*>(dc4 + Tmax);
+    if (Ps) {
+      CUDA_TRY(ctx, launch_compact(ds.count, reinterpret_cast<const float2*>(ds.depth),
+                                   reinterpret_cast<const float4*>(ds.rgba), (uint32_t)Ps, (int)k,
+                                   ctx->xbase.as<uint32_t>(), dd2, dc4, st, &launches));
+      CUDA_TRY(ctx, cudaMemcpyAsync(ctx->pcount[sl].p, ds.count, Ps, cudaMemcpyDeviceToDevice, st));
+    }
+    CUDA_TRY(ctx, cudaEventRecord(ctx->pev_comp[sl], st));
+    return VDI_OK;
+  };
+  // D2H of frame f once its total is known on the host
+  vdi_status first_err = VDI_OK;
+  auto d2h = [&](uint32_t f) -> vdi_status {
+    const int sl = f & 1;
+    CUDA_TRY(ctx, cudaEventSynchronize(ctx->pev_tot[sl]));
+    const unsigned long long T = ctx->ptot[sl];
+    vdi_dense_strip& o = outs[f];
+    o.total = T;
+    CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->pout_st, ctx->pev_comp[sl], 0));
+    if (T > o.capacity) {
+      if (first_err == VDI_OK)
+        first_err = fail(VDI_ERR_CAPACITY, "frame %u: dense strip needs %llu supersegments, capacity %llu", f, T,
+                         (unsigned long long)o.capacity);
+    } else {
+      const float4* dc4 = ctx->pdense[sl].as<float4>();
+      const float2* dd2 = reinterpret_cast<const float2*>(dc4 + Tmax);
+      CUDA_TRY(ctx, cudaMemcpyAsync(o.count, ctx->pcount[sl].p, Ps, cudaMemcpyDeviceToHost, ctx->pout_st));
+      if (T) {
+        CUDA_TRY(ctx, cudaMemcpyAsync(o.depth, dd2, T * 8, cudaMemcpyDeviceToHost, ctx->pout_st));
+        CUDA_TRY(ctx, cudaMemcpyAsync(o.rgba, dc4, T * 16, cudaMemcpyDeviceToHost, ctx->pout_st));
+      }
+    }
+    CUDA_TRY(ctx, cudaEventRecord(ctx->pev_out[sl], ctx->pout_st));
+    return VDI_OK;
+  };
+  // order: H2D(f+1) is queued before the host waits for frame f's total, and
+  // compute(f+1) after D2H(f) is queued (vdi_composite may wait on the host
+  // for the size exchange when n_ranks > 1)
+  if (vdi_status s = h2d(0)) return s;
+  if (vdi_status s = compute(0)) return s;
+  for (uint32_t f = 0; f < F; ++f) {
+    if (f + 1 < F)
+      if (vdi_status s = h2d(f + 1)) return s;
+    if (vdi_status s = d2h(f)) return s;
+    if (f + 1 < F)
+      if (vdi_status s = compute(f + 1)) return s;
+  }
+  CUDA_TRY(ctx, cudaStreamSynchronize(ctx->pout_st));
+  CUDA_TRY(ctx, cudaStreamSynchronize(ctx->pin_st));
+  CUDA_TRY(ctx, cudaStreamSynchronize(st));
+  ctx->last.kernel_launches += (uint32_t)launches;
+  return first_err;
 }
 
 vdi_status vdi_pixel_stats(vdi_ctx* ctx, float* gamma, uint16_t* m) {

@@ -268,6 +268,37 @@ def test_host_dense_output(vdi):
         comp.composite_host_dense(host, hc, small[0], small[1])  # VDI_ERR_CAPACITY
 
 
+def test_host_dense_frames_pipeline(vdi):
+    """vdi_composite_host_dense_frames: each frame of the pipelined call (H2D /
+    compositing / D2H of consecutive frames overlapped, double-buffered slots)
+    equals vdi_composite_host_dense on that frame's inputs, bit for bit; frames
+    differ (three input sets, five frames: every slot is reused)."""
+    n, W, H, k = 4, 83, 47, 8
+    sets = [synth.random_subvdis(n, W, H, k, lam=7.0 + s, seed=300 + s) for s in range(3)]
+    comp = vdi.Compositor(W, H, k, k, n)
+    host = [[dense_to_device(p, i, device="cpu") for i, p in enumerate(pes)] for pes in sets]
+    cap = W * H * k
+    mk = lambda c: (torch.empty(W * H, dtype=torch.uint8), torch.empty((c, 2), dtype=torch.float32),
+                    torch.empty((c, 4), dtype=torch.float32))
+    want = []
+    for hs in host:
+        o = mk(cap)
+        T = comp.composite_host_dense(hs, *o)
+        want.append((T, o))
+    order = [0, 1, 2, 1, 0]
+    outs = [mk(cap) for _ in order]
+    Ts = comp.composite_host_dense_frames([host[i] for i in order], outs)
+    for f, i in enumerate(order):
+        T, (wc, wd, wr) = want[i]
+        assert Ts[f] == T
+        assert torch.equal(outs[f][0], wc)
+        assert torch.equal(outs[f][1][:T], wd[:T]) and torch.equal(outs[f][2][:T], wr[:T])
+    # capacity error is reported after every frame ran; totals are still set
+    small = [mk(max(want[i][0] - 1, 1)) for i in order[:2]]
+    with pytest.raises(Exception):
+        comp.composite_host_dense_frames([host[i] for i in order[:2]], small)
+
+
 def test_multi_gpu_strip_invariance(vdi):
     """G = 2 (or all visible GPUs): NCCL exchange + gather give the 1-GPU result
     bit-for-bit and match the oracle (tests/mgpu_check.py under torchrun)."""
