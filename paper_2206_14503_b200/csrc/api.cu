@@ -122,7 +122,8 @@ struct vdi_ctx {
   DevBuf pcount[2], pdense[2];
   cudaStream_t pin_st = nullptr, pout_st = nullptr;
   cudaEvent_t pev_in[2] = {}, pev_used[2] = {}, pev_tot[2] = {}, pev_comp[2] = {}, pev_out[2] = {};
-  unsigned long long* ptot = nullptr;  // pinned host [2]
+  unsigned long long* ptot = nullptr;      // pinned, mapped host [2]: frame totals written by the kernel
+  unsigned long long* ptot_dev = nullptr;  // its device alias
   // counters
   vdi_counters last{};
   bool have_stats = false;
@@ -1595,6 +1596,9 @@ vdi_status vdi_composite_host_dense(vdi_ctx* ctx, const vdi_dense_view* local, u
   return VDI_OK;
 }
 
+#ifndef VDI_E2E_MAPPED
+#define VDI_E2E_MAPPED 1  // frame totals stored by the kernel into mapped host memory (else an 8-byte D2H)
+#endif
 // Pipelined vdi_composite_host_dense over independent frames: frame f's H2D
 // (stream pin_st, input slot f&1) overlaps frame f-1's compositing (ctx
 // stream) and frame f-2's D2H (stream pout_st, output slot f&1).  Each frame
@@ -1618,7 +1622,8 @@ vdi_status vdi_composite_host_dense_frames(vdi_ctx* ctx, uint32_t F, const vdi_d
     for (cudaEvent_t* a : {ctx->pev_in, ctx->pev_used, ctx->pev_tot, ctx->pev_comp, ctx->pev_out})
       for (int i = 0; i < 2; ++i) CUDA_TRY(ctx, cudaEventCreateWithFlags(&a[i], cudaEventDisableTiming));
     CUDA_TRY(ctx, cudaHostAlloc(reinterpret_cast<void**>(&ctx->ptot), 2 * sizeof(unsigned long long),
-                                cudaHostAllocDefault));
+                                cudaHostAllocMapped));
+    CUDA_TRY(ctx, cudaHostGetDevicePointer(reinterpret_cast<void**>(&ctx->ptot_dev), ctx->ptot, 0));
   }
   const size_t Ps = ctx->P, k = cf.k_out, Tmax = std::max<size_t>(Ps * k, 1);  // a strip holds <= Ps*k
   CUDA_TRY(ctx, ctx->hstrip_count.grow(Ps));
@@ -1632,8 +1637,9 @@ vdi_status vdi_composite_host_dense_frames(vdi_ctx* ctx, uint32_t F, const vdi_d
     CUDA_TRY(ctx, ctx->pcount[i].grow(std::max<size_t>(Ps, 1)));
     CUDA_TRY(ctx, ctx->pdense[i].grow(Tmax * 24));
   }
-  vdi_full_view ds{ctx->row0, ctx->row1, ctx->hstrip_count.as<uint8_t>(), ctx->hstrip_depth.as<float>(),
-                   ctx->hstrip_rgba.as<float>()};
+  // the strip's counts go straight to the output slot (read by the D2H);
+  // its records to the shared full-representation scratch (read by the compaction)
+  vdi_full_view ds{ctx->row0, ctx->row1, nullptr, ctx->hstrip_depth.as<float>(), ctx->hstrip_rgba.as<float>()};
   std::vector<vdi_dense_view> dv[2];
   int launches = 0;
   // H2D of frame f into slot f&1, once the compositing of frame f-2 has read it
@@ -1647,7 +1653,9 @@ vdi_status vdi_composite_host_dense_frames(vdi_ctx* ctx, uint32_t F, const vdi_d
   // composite + dense compaction of frame f into output slot f&1
   auto compute = [&](uint32_t f) -> vdi_status {
     const int sl = f & 1;
+    CUDA_TRY(ctx, cudaStreamWaitEvent(st, ctx->pev_out[sl], 0));  // frame f-2's D2H has read the slot
     CUDA_TRY(ctx, cudaStreamWaitEvent(st, ctx->pev_in[sl], 0));
+    ds.count = ctx->pcount[sl].as<uint8_t>();
     if (vdi_status s = vdi_composite(ctx, dv[sl].data(), n_local, &ds)) return s;
     CUDA_TRY(ctx, cudaEventRecord(ctx->pev_used[sl], st));
     MergeParams ms{};
@@ -1655,23 +1663,24 @@ vdi_status vdi_composite_host_dense_frames(vdi_ctx* ctx, uint32_t F, const vdi_d
     ms.P = (uint32_t)Ps;
     ms.n_groups = (uint32_t)ng;
     ms.src[0].count = ds.count;
-    unsigned long long* dtot = ctx->xtot.as<unsigned long long>();
-    if (Ps) {
+    if (Ps) {  // the total is stored by the kernel into mapped host memory (no copy-engine hop)
       CUDA_TRY(ctx, launch_scan(ms, ctx->xsum.as<uint32_t>(), ctx->xbase.as<uint32_t>(), st, &launches));
-      CUDA_TRY(ctx, launch_total(ms, ctx->xsum.as<uint32_t>(), dtot, st, &launches));
-      CUDA_TRY(ctx, cudaMemcpyAsync(ctx->ptot + sl, dtot, 8, cudaMemcpyDeviceToHost, st));
+#if VDI_E2E_MAPPED
+      CUDA_TRY(ctx, launch_total(ms, ctx->xsum.as<uint32_t>(), ctx->ptot_dev + sl, st, &launches));
+#else
+      CUDA_TRY(ctx, launch_total(ms, ctx->xsum.as<uint32_t>(), ctx->xtot.as<unsigned long long>(), st, &launches));
+      CUDA_TRY(ctx, cudaMemcpyAsync(ctx->ptot + sl, ctx->xtot.p, 8, cudaMemcpyDeviceToHost, st));
+#endif
     } else {
       ctx->ptot[sl] = 0;
     }
     CUDA_TRY(ctx, cudaEventRecord(ctx->pev_tot[sl], st));
-    CUDA_TRY(ctx, cudaStreamWaitEvent(st, ctx->pev_out[sl], 0));  // frame f-2's D2H has read the slot
     float4* dc4 = ctx->pdense[sl].as<float4>();
     float2* dd2 = reinterpret_cast<float2*>(dc4 + Tmax);
     if (Ps) {
       CUDA_TRY(ctx, launch_compact(ds.count, reinterpret_cast<const float2*>(ds.depth),
                                    reinterpret_cast<const float4*>(ds.rgba), (uint32_t)Ps, (int)k,
                                    ctx->xbase.as<uint32_t>(), dd2, dc4, st, &launches));
-      CUDA_TRY(ctx, cudaMemcpyAsync(ctx->pcount[sl].p, ds.count, Ps, cudaMemcpyDeviceToDevice, st));
     }
     CUDA_TRY(ctx, cudaEventRecord(ctx->pev_comp[sl], st));
     return VDI_OK;
@@ -1681,7 +1690,7 @@ vdi_status vdi_composite_host_dense_frames(vdi_ctx* ctx, uint32_t F, const vdi_d
   auto d2h = [&](uint32_t f) -> vdi_status {
     const int sl = f & 1;
     CUDA_TRY(ctx, cudaEventSynchronize(ctx->pev_tot[sl]));
-    const unsigned long long T = ctx->ptot[sl];
+    const unsigned long long T = *static_cast<volatile unsigned long long*>(ctx->ptot + sl);
     vdi_dense_strip& o = outs[f];
     o.total = T;
     CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->pout_st, ctx->pev_comp[sl], 0));

@@ -852,8 +852,15 @@ __device__ __forceinline__ void gather_short_batch(const MergeParams& mp, uint32
 #ifndef VDI_SHORT_MEMO
 #define VDI_SHORT_MEMO 1  // with VDI_PACKED_D2: search 0.1637 vs 0.1658 ms (alone: 0.173, slower)
 #endif
-template <int MS>
-__device__ __forceinline__ void sweep_batch(const MergeParams& mp, int bucket, uint32_t batch) {
+struct NoOp {
+  __device__ __forceinline__ void operator()() const {}
+};
+// sbuf: the batch's samples already in shared memory ([sample][lane]); after()
+// runs once they are in registers (the prefetching sweep kernel claims the
+// next batch and starts its copy into the same buffer there)
+template <int MS, class After = NoOp>
+__device__ __forceinline__ void sweep_batch(const MergeParams& mp, int bucket, uint32_t batch,
+                                            const float4* sbuf = nullptr, After after = After()) {
   const int lane = threadIdx.x;
   const int k = mp.k_out, n = mp.n_src;
   const uint32_t total = min(mp.wl_count[bucket], mp.wl_cap);
@@ -876,7 +883,15 @@ __device__ __forceinline__ void sweep_batch(const MergeParams& mp, int bucket, u
     float4 S[MS];
     const float qnan = __int_as_float(0x7fc00000);
 #pragma unroll
-    for (int q = 0; q < MS; ++q) S[q] = (q < mi && !bad) ? col[q * 32] : make_float4(qnan, qnan, qnan, qnan);
+    for (int q = 0; q < MS; ++q)
+      S[q] = (q < mi && !bad) ? (sbuf ? sbuf[q * 32 + lane] : col[q * 32]) : make_float4(qnan, qnan, qnan, qnan);
+    if (sbuf) {
+      // the samples are in registers: the buffer may take the next batch
+      // (generic-proxy reads ordered before the async-proxy bulk write)
+      __syncwarp();
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      after();
+    }
 #if VDI_SHORT_MEMO
     // memoised bisection (as in the long-list sweep): a count sweep at g2
     // takes the same decisions for every g2' in [L, U), so a later midpoint
@@ -1685,8 +1700,11 @@ static cudaError_t prep(K kernel, size_t smem, int threads, int* per_sm) {
 #ifndef VDI_SPLIT_CH
 #define VDI_SPLIT_CH 16
 #endif
+#ifndef VDI_GATHER_MINB
+#define VDI_GATHER_MINB 1  // resident 128-thread blocks per SM asked of ptxas (3 at 167 registers)
+#endif
 template <int NS>
-__global__ void __launch_bounds__(128) search_gather_kernel(MergeParams mp) {
+__global__ void __launch_bounds__(128, VDI_GATHER_MINB) search_gather_kernel(MergeParams mp) {
   __shared__ float2 sd[40 * 128];
   __shared__ uint8_t sp[40 * 128];
   const uint32_t lane = threadIdx.x & 31;
@@ -1701,9 +1719,80 @@ __global__ void __launch_bounds__(128) search_gather_kernel(MergeParams mp) {
   }
 }
 
+#ifndef VDI_SWEEP_PREFETCH
+#define VDI_SWEEP_PREFETCH 0  // measured: search 0.1662 vs 0.1654 ms without (C3), C2 equal
+#endif
+// Short-list sweeps, warp per batch (dynamic claims, longest bucket first).
+// With VDI_SWEEP_PREFETCH the next claimed batch's samples (its pool rows,
+// [sample][lane] float4, 16 or 20 KB) are pulled into shared memory by one
+// bulk copy (cp.async.bulk, mbarrier completion) while the current batch is
+// swept from registers, so a batch starts on shared-memory loads instead of
+// a pool read from L2/HBM.
 __global__ void __launch_bounds__(32, VDI_SWEEP_MINB) search_sweep_kernel(MergeParams mp) {
   const uint32_t c0 = min(mp.wl_count[0], mp.wl_cap), c1 = min(mp.wl_count[1], mp.wl_cap);
   const uint32_t nb0 = (c0 + 31) / 32, nb1 = (c1 + 31) / 32;
+#if VDI_SWEEP_PREFETCH
+  __shared__ __align__(128) float4 sbuf[40 * 32];
+  __shared__ __align__(8) unsigned long long bar;
+  const uint32_t lane = threadIdx.x;
+  const uint32_t sb = smem_u32(sbuf), bb = smem_u32(&bar);
+  if (lane == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bb) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  uint32_t phase = 0;
+  // claim a batch; lane 0 starts its bulk copy; returns the batch (>= total: none)
+  auto claim = [&]() -> uint32_t {
+    uint32_t v = 0;
+    bool issued = false;
+    if (lane == 0) {
+      v = atomicAdd(&mp.search_ticket[0], 1u);
+      if (v < nb0 + nb1) {
+        const int bucket = v < nb1 ? 1 : 0;
+        const uint32_t slot = mp.batch_slot[bucket][bucket ? v : v - nb1];
+        if (slot < mp.pool_cap) {
+          const uint32_t bytes = (bucket ? 40u : 32u) * 32u * 16u;
+          const float4* src = mp.pool_rgba + (size_t)slot * 40 * 32;
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bb), "r"(bytes) : "memory");
+          asm volatile(
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(sb),
+              "l"(src), "r"(bytes), "r"(bb)
+              : "memory");
+          issued = true;
+        }
+      }
+    }
+    v = __shfl_sync(kFull, v, 0);
+    return __shfl_sync(kFull, issued ? 1u : 0u, 0) ? v : v | 0x80000000u;  // top bit: nothing in flight
+  };
+  uint32_t cur = claim();
+  while ((cur & 0x7fffffffu) < nb0 + nb1) {
+    if (!(cur & 0x80000000u)) {  // wait for its bulk copy
+      uint32_t done = 0;
+      while (!done)
+        asm volatile(
+            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+            : "=r"(done)
+            : "r"(bb), "r"(phase)
+            : "memory");
+      phase ^= 1u;
+    }
+    const uint32_t v = cur & 0x7fffffffu;
+    // sweep_batch reads the samples into registers, then releases the buffer;
+    // the next claim (and its copy) is issued from inside via the callback
+    // ordering below: registers first, then claim
+    const int bucket = v < nb1 ? 1 : 0;
+    const uint32_t b = bucket ? v : v - nb1;
+    const uint32_t slot = mp.batch_slot[bucket][b];
+    if (slot < mp.pool_cap && !(cur & 0x80000000u)) {
+      sweep_batch<40>(mp, bucket, b, sbuf, [&]() { cur = claim(); });
+    } else {
+      cur = claim();
+      if (slot < mp.pool_cap) sweep_batch<40>(mp, bucket, b);
+    }
+  }
+#else
   for (;;) {
     uint32_t v = 0;
     if (threadIdx.x == 0) v = atomicAdd(&mp.search_ticket[0], 1u);
@@ -1711,6 +1800,7 @@ __global__ void __launch_bounds__(32, VDI_SWEEP_MINB) search_sweep_kernel(MergeP
     if (v >= nb0 + nb1) break;
     sweep_batch<40>(mp, v < nb1 ? 1 : 0, v < nb1 ? v : v - nb1);
   }
+#endif
 }
 
 template <int NS>
@@ -1758,6 +1848,10 @@ static cudaError_t launch_search_ns(const MergeParams& mp, cudaStream_t st, int*
   {
     static int per_sm = 0;
     if (!per_sm) {
+      // 8 warps x 20 KB prefetch buffers: ask for the largest shared-memory carveout
+      if ((e = cudaFuncSetAttribute(search_sweep_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100)) !=
+          cudaSuccess)
+        return e;
       if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, search_sweep_kernel, 32, 0)) != cudaSuccess)
         return e;
       if (per_sm < 1) per_sm = 1;
