@@ -432,6 +432,29 @@ def _run_ours(args, world, rank, local, clk):
     bytes_sent = stage[-1]["bytes_sent"]
     bytes_recv = stage[-1]["bytes_received"]
 
+    # ---- Phase 1 + Phase 2 of one VDI: every local PE's
+    # sub-VDI raycast from the resident volume (vdi_generate_subvdi), then the
+    # strip-mode exchange + merge + gather; CUDA events on the stream, min over
+    # 3 repetitions, max over ranks; deterministic, so `local` is regenerated
+    # in place with identical contents
+    v2r = []
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for _ in range(3):
+        torch.cuda.synchronize()
+        barrier(G)
+        ev0.record(stream)
+        regen = [comp.generate_subvdi(vol, tft, cam, dec, pe) for pe in local_ids]
+        strip_step()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        v2r.append(ev0.elapsed_time(ev1))
+    assert [p.total for p in regen] == [p.total for p in local]
+    ms_v2r = allreduce_max(min(v2r), G)
+    volume_to_root = {"ms": ms_v2r, "vdis_per_s": 1e3 / ms_v2r, "pes_generated_per_rank": len(local_ids),
+                      "note": "Phase 1 (vdi_generate_subvdi of every local PE: gamma search + count pass, scan, "
+                              "write pass; PAPER.md:113-118, :150-157) + strip-mode exchange, merge and gather of "
+                              "one VDI (PAPER.md:164-185), one stream, max over ranks"}
+
     # ---- end to end through the C ABI with host buffers (pinned): host
     # sub-VDIs in, the composited strip back in the dense representation
     # (vdi_composite_host_dense)
@@ -519,6 +542,7 @@ def _run_ours(args, world, rank, local, clk):
                           "merge_fast": statistics.mean(c["ms_fast"] for c in stage),
                           "merge_search": statistics.mean(c["ms_search"] for c in stage)},
             "phase1_generate": phase1,
+            "volume_to_root_vdi": volume_to_root,
             "latency_mode": latency,
             "frames_mode": frames_info,
             "full_representation_mode": full_rep,
