@@ -1799,8 +1799,31 @@ __global__ void __launch_bounds__(32, VDI_SWEEP_MINB) search_sweep_kernel(MergeP
     v = __shfl_sync(kFull, v, 0);
     if (v >= nb0 + nb1) break;
     sweep_batch<40>(mp, v < nb1 ? 1 : 0, v < nb1 ? v : v - nb1);
+#if VDI_SWEEP_SPLIT
+    if (v >= nb1) break;  // at most one bucket-0 batch here; the rest go to search_sweep32_kernel
+#endif
   }
 #endif
+}
+
+#ifndef VDI_SWEEP_SPLIT
+#define VDI_SWEEP_SPLIT 0
+#endif
+#ifndef VDI_SWEEP32_MINB
+#define VDI_SWEEP32_MINB 10
+#endif
+// Bucket-0 batches (m <= 32) left by search_sweep_kernel, swept with a
+// 32-sample register file (fewer registers: more resident warps)
+__global__ void __launch_bounds__(32, VDI_SWEEP32_MINB) search_sweep32_kernel(MergeParams mp) {
+  const uint32_t c0 = min(mp.wl_count[0], mp.wl_cap), c1 = min(mp.wl_count[1], mp.wl_cap);
+  const uint32_t nb0 = (c0 + 31) / 32, nb1 = (c1 + 31) / 32;
+  for (;;) {
+    uint32_t v = 0;
+    if (threadIdx.x == 0) v = atomicAdd(&mp.search_ticket[0], 1u);
+    v = __shfl_sync(kFull, v, 0);
+    if (v >= nb0 + nb1) break;
+    sweep_batch<32>(mp, 0, v - nb1);  // v >= nb1: bucket 1 is exhausted before this kernel starts
+  }
 }
 
 template <int NS>
@@ -1858,6 +1881,17 @@ static cudaError_t launch_search_ns(const MergeParams& mp, cudaStream_t st, int*
     }
     search_sweep_kernel<<<sm_count() * per_sm, 32, 0, st>>>(mp);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
+#if VDI_SWEEP_SPLIT
+    static int per_sm32 = 0;
+    if (!per_sm32) {
+      if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm32, search_sweep32_kernel, 32, 0)) != cudaSuccess)
+        return e;
+      if (per_sm32 < 1) per_sm32 = 1;
+    }
+    search_sweep32_kernel<<<sm_count() * per_sm32, 32, 0, st>>>(mp);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    ++*launches;
+#endif
   }
 #else
   if ((e = launch_short<NS>(mp, st)) != cudaSuccess) return e;
