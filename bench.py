@@ -460,9 +460,21 @@ def _run_ours(args, world, rank, local, clk):
     # (vdi_composite_host_dense)
     e2e = None
     if not args.no_e2e:
-        host_pes = [vdi.DenseSubVDI(p.pe_id, p.total, p.count.cpu().pin_memory(),
-                                    p.offset.cpu().pin_memory() if G > 1 else None,
-                                    p.depth.cpu().pin_memory(), p.rgba.cpu().pin_memory()) for p in local]
+        # the local sub-VDIs packed in one pinned host arena (256-B aligned
+        # arrays): libvdi then moves a frame's inputs with one H2D copy
+        parts = [[p.count] + ([p.offset] if G > 1 else []) + [p.depth, p.rgba] for p in local]
+        sizes = [[(t.numel() * t.element_size() + 255) // 256 * 256 for t in ts] for ts in parts]
+        arena = torch.empty(sum(map(sum, sizes)), dtype=torch.uint8).pin_memory()
+        host_pes, off = [], 0
+        for p, ts, ss in zip(local, parts, sizes):
+            hv = []
+            for t, sz in zip(ts, ss):
+                nb = t.numel() * t.element_size()
+                h = arena[off:off + nb].view(t.dtype).view(t.shape)
+                h.copy_(t)
+                hv.append(h)
+                off += sz
+            host_pes.append(vdi.DenseSubVDI(p.pe_id, p.total, hv[0], hv[1] if G > 1 else None, hv[-2], hv[-1]))
         P_g = strip.count.numel()
         cap = max(1, min(P_g * k, S_total))  # a list never gains supersegments: output <= input records
         outs = [(torch.empty(P_g, dtype=torch.uint8).pin_memory(), torch.empty((cap, 2), dtype=torch.float32).pin_memory(),
@@ -486,6 +498,7 @@ def _run_ours(args, world, rank, local, clk):
         e2e = {"value": args.e2e_steps / dt, "unit": UNIT, "h2d_bytes_per_step": int(allreduce_sum(h2d, G)),
                "d2h_bytes_per_step": int(allreduce_sum(d2h, G)),
                "frames": args.e2e_steps,
+               "host_link_GBs": (h2d + d2h) * args.e2e_steps / dt / 1e9,  # this rank's H2D + D2H bytes / time
                "note": "vdi_composite_host_dense_frames: per frame, pinned host sub-VDIs -> H2D -> composite "
                        "(strip mode) -> on-device compaction -> counts + packed supersegments D2H, every rank; "
                        "frame f's H2D overlaps frame f-1's compositing and frame f-2's D2H"}

@@ -119,6 +119,7 @@ struct vdi_ctx {
   // vdi_composite_host_dense_frames: the second input slot, per-slot dense
   // outputs, the H2D / D2H streams and their slot events
   std::vector<DevBuf> hcount1, hoffset1, hdepth1, hrgba1;
+  DevBuf harena[2];  // input slots when the host arrays are packed in one span
   DevBuf pcount[2], pdense[2];
   cudaStream_t pin_st = nullptr, pout_st = nullptr;
   cudaEvent_t pev_in[2] = {}, pev_used[2] = {}, pev_tot[2] = {}, pev_comp[2] = {}, pev_out[2] = {};
@@ -1493,6 +1494,54 @@ static vdi_status upload_host_pes(vdi_ctx* ctx, const vdi_dense_view* local, uin
     const vdi_dense_view& v = local[l];
     if (!v.count || (v.total && (!v.depth || !v.rgba)) || (cf.n_ranks > 1 && !v.offset))
       return fail(VDI_ERR_INVALID_ARG, "host view %u has NULL arrays", l);
+  }
+  // Host arrays packed in one span (e.g. one pinned arena per frame): ONE
+  // copy of the span instead of 3-4 per PE -- many mid-sized H2D copies run
+  // the host link at ~80 % of one large copy (profiles/pipeline_probe.py).
+  // Device views keep the host arrays' offsets inside the span (alignment
+  // mod 256 preserved); a gap-ridden span falls back to per-array copies.
+  {
+    uintptr_t lo = UINTPTR_MAX, hi = 0;
+    size_t sum = 0;
+    bool aligned = true;
+    auto add = [&](const void* p, size_t n, size_t al) {
+      if (!n) return;
+      const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+      lo = std::min(lo, a);
+      hi = std::max(hi, a + n);
+      sum += n;
+      aligned &= (a % al) == 0;
+    };
+    for (uint32_t l = 0; l < n_local; ++l) {
+      const vdi_dense_view& v = local[l];
+      add(v.count, P, 1);
+      add(v.depth, v.total * 8, 8);
+      add(v.rgba, v.total * 16, 16);
+      if (cf.n_ranks > 1) add(v.offset, (P + 1) * 4, 4);
+    }
+    if (sum && aligned) {
+      lo &= ~(uintptr_t)255;
+      const size_t span = hi - lo;
+      if (span <= sum + std::max<size_t>(sum / 16, (size_t)1 << 20)) {
+        DevBuf& ar = ctx->harena[set];
+        CUDA_TRY(ctx, ar.grow(span));
+        CUDA_TRY(ctx, cudaMemcpyAsync(ar.p, reinterpret_cast<const void*>(lo), span, cudaMemcpyHostToDevice, st));
+        uint8_t* base = ar.as<uint8_t>();
+        auto dev = [&](const void* p) { return base + (reinterpret_cast<uintptr_t>(p) - lo); };
+        for (uint32_t l = 0; l < n_local; ++l) {
+          const vdi_dense_view& v = local[l];
+          dv[l] = v;
+          dv[l].count = dev(v.count);
+          dv[l].depth = reinterpret_cast<float*>(v.total ? dev(v.depth) : base);  // base: never read
+          dv[l].rgba = reinterpret_cast<float*>(v.total ? dev(v.rgba) : base);
+          dv[l].offset = cf.n_ranks > 1 ? reinterpret_cast<uint32_t*>(dev(v.offset)) : nullptr;
+        }
+        return VDI_OK;
+      }
+    }
+  }
+  for (uint32_t l = 0; l < n_local; ++l) {
+    const vdi_dense_view& v = local[l];
     CUDA_TRY(ctx, hcount[l].grow(P));
     CUDA_TRY(ctx, hdepth[l].grow(std::max<uint64_t>(v.total, 1) * 8));
     CUDA_TRY(ctx, hrgba[l].grow(std::max<uint64_t>(v.total, 1) * 16));

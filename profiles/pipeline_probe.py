@@ -14,10 +14,13 @@ din = [[[torch.empty(n, dtype=torch.uint8, device="cuda") for n in (P, 8 * S, 16
 dout = [torch.empty(OUT, dtype=torch.uint8, device="cuda") for _ in range(2)]
 hout = [torch.empty(OUT, dtype=torch.uint8).pin_memory() for _ in range(2)]
 sin, scomp, sout = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
+tot_in = 8 * (P + 24 * S)
+hflat = torch.empty(tot_in, dtype=torch.uint8).pin_memory()
+dflat = [torch.empty(tot_in, dtype=torch.uint8, device="cuda") for _ in range(2)]
 work = torch.empty(1 << 30, dtype=torch.uint8, device="cuda")
 
 
-def run(frames):
+def run(frames, one_copy=False):
     ev_in = [torch.cuda.Event() for _ in range(frames)]
     ev_c = [torch.cuda.Event() for _ in range(frames)]
     ev_o = [torch.cuda.Event() for _ in range(frames)]
@@ -26,9 +29,12 @@ def run(frames):
         with torch.cuda.stream(sin):
             if f >= 2:
                 sin.wait_event(ev_c[f - 2])
-            for l in range(8):
-                for a in range(3):
-                    din[sl][l][a].copy_(hin[l][a], non_blocking=True)
+            if one_copy:
+                dflat[sl].copy_(hflat, non_blocking=True)
+            else:
+                for l in range(8):
+                    for a in range(3):
+                        din[sl][l][a].copy_(hin[l][a], non_blocking=True)
             ev_in[f].record(sin)
         with torch.cuda.stream(scomp):
             scomp.wait_event(ev_in[f])
@@ -44,8 +50,11 @@ def run(frames):
     torch.cuda.synchronize()
 
 
-run(2)
-t0 = time.perf_counter()
-run(F)
-dt = time.perf_counter() - t0
-print(json.dumps({"frames": F, "frames_per_s": F / dt, "ms_per_frame": dt / F * 1e3}))
+res = {}
+for one in (False, True, False, True):
+    run(2, one)
+    t0 = time.perf_counter()
+    run(F, one)
+    dt = time.perf_counter() - t0
+    res.setdefault("one_h2d_copy" if one else "24_h2d_copies", []).append(F / dt)
+print(json.dumps({"frames": F, "frames_per_s": res}))

@@ -293,6 +293,33 @@ def test_host_dense_frames_pipeline(vdi):
         assert Ts[f] == T
         assert torch.equal(outs[f][0], wc)
         assert torch.equal(outs[f][1][:T], wd[:T]) and torch.equal(outs[f][2][:T], wr[:T])
+    # the same inputs packed in one pinned arena (libvdi's one-copy span path)
+    # give the same bits, single-frame and pipelined
+    packed = []
+    for hs in host:
+        parts = [[p.count, p.depth, p.rgba] for p in hs]
+        sizes = [[(t.numel() * t.element_size() + 255) // 256 * 256 for t in ts] for ts in parts]
+        arena = torch.empty(sum(map(sum, sizes)), dtype=torch.uint8).pin_memory()
+        pk, off = [], 0
+        for p, ts, ss in zip(hs, parts, sizes):
+            hv = []
+            for t, sz in zip(ts, ss):
+                nb = t.numel() * t.element_size()
+                h = arena[off:off + nb].view(t.dtype).view(t.shape)
+                h.copy_(t)
+                hv.append(h)
+                off += sz
+            pk.append(vdi.DenseSubVDI(p.pe_id, p.total, hv[0], None, hv[1], hv[2]))
+        packed.append((arena, pk))
+    o = mk(cap)
+    assert comp.composite_host_dense(packed[1][1], *o) == want[1][0]
+    assert torch.equal(o[0], want[1][1][0]) and torch.equal(o[2][:want[1][0]], want[1][1][2][:want[1][0]])
+    outs = [mk(cap) for _ in order]
+    Ts = comp.composite_host_dense_frames([packed[i][1] for i in order], outs)
+    for f, i in enumerate(order):
+        T, (wc, wd, wr) = want[i]
+        assert Ts[f] == T and torch.equal(outs[f][0], wc)
+        assert torch.equal(outs[f][1][:T], wd[:T]) and torch.equal(outs[f][2][:T], wr[:T])
     # capacity error is reported after every frame ran; totals are still set
     small = [mk(max(want[i][0] - 1, 1)) for i in order[:2]]
     with pytest.raises(Exception):
