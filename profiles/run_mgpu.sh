@@ -1,10 +1,7 @@
 #!/bin/bash
-# Multi-GPU bench lines (driver's torchrun launch) + the multi-GPU parity test; outputs in gpurun_out/.
+# Multi-GPU bench lines (driver's torchrun launch); outputs in gpurun_out/.
 set -x
-make -s >/dev/null 2>&1
 R="python -m torch.distributed.run --nnodes=1 --master-addr 127.0.0.1"
-python profiles/pipeline_probe.py > gpurun_out/pipeline_probe.json 2>&1
-timeout 600 python -m pytest tests -m gpu -x -q -k multi_gpu > gpurun_out/pytest_mgpu.log 2>&1
-timeout 300 python bench.py > gpurun_out/bench_n1.json 2> gpurun_out/bench_n1.err
 timeout 400 $R --nproc-per-node 2 --master-port 29601 bench.py --gpus 2 > gpurun_out/bench_n2.json 2> gpurun_out/bench_n2.err
 timeout 400 $R --nproc-per-node 4 --master-port 29602 bench.py --gpus 4 > gpurun_out/bench_n4.json 2> gpurun_out/bench_n4.err
+timeout 600 python -m pytest tests -m gpu -x -q -k multi_gpu > gpurun_out/pytest_mgpu.log 2>&1
