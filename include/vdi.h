@@ -212,7 +212,11 @@ vdi_status vdi_dense_to_full(vdi_ctx* ctx, const vdi_dense_view* in, vdi_full_vi
 /* Same as vdi_composite with HOST buffers (the end-to-end entry point):
  * copies the local sub-VDIs host->device (pinned memory recommended),
  * composites, and copies the strip back device->host into strip_out.
- * Pointers in local_pes / strip_out are host pointers.  Synchronises. */
+ * Pointers in local_pes / strip_out are host pointers.  Synchronises.
+ * Host inputs of every _host entry: when all local arrays lie packed in one
+ * span (gaps <= 1/16 of the bytes or 1 MiB; depth 8-B, rgba 16-B, offset
+ * 4-B aligned), the span is copied with ONE host->device copy (the library
+ * reads the gap bytes too); otherwise each array is copied on its own. */
 vdi_status vdi_composite_host(vdi_ctx* ctx, const vdi_dense_view* local_pes, uint32_t n_local,
                               vdi_full_view* strip_out);
 
