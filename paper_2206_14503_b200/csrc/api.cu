@@ -1565,6 +1565,17 @@ static vdi_status upload_host_pes(vdi_ctx* ctx, const vdi_dense_view* local, uin
   return VDI_OK;
 }
 
+// n_ranks > 1: peers pull their strip slices out of this rank's staging
+// buffers during their own compositing; a one-byte allreduce on the stream
+// after the merge (every rank's pulls precede its merge) keeps the next host
+// call from overwriting a slot a peer is still reading
+static vdi_status peer_quiesce(vdi_ctx* ctx, cudaStream_t st) {
+  if (ctx->cfg.n_ranks <= 1) return VDI_OK;
+  CUDA_TRY(ctx, ctx->bounds.grow(16));
+  NCCL_TRY(ctx, ncclAllReduce(ctx->bounds.p, ctx->bounds.p, 1, ncclUint8, ncclSum, ctx->comm, st));
+  return VDI_OK;
+}
+
 vdi_status vdi_composite_host(vdi_ctx* ctx, const vdi_dense_view* local, uint32_t n_local, vdi_full_view* so) {
   if (vdi_status s = check_ctx(ctx)) return s;
   const vdi_config& cf = ctx->cfg;
@@ -1579,6 +1590,7 @@ vdi_status vdi_composite_host(vdi_ctx* ctx, const vdi_dense_view* local, uint32_
   vdi_full_view ds{ctx->row0, ctx->row1, ctx->hstrip_count.as<uint8_t>(), ctx->hstrip_depth.as<float>(),
                    ctx->hstrip_rgba.as<float>()};
   if (vdi_status s = vdi_composite(ctx, dv.data(), n_local, &ds)) return s;
+  if (vdi_status s = peer_quiesce(ctx, st)) return s;
   CUDA_TRY(ctx, cudaMemcpyAsync(so->count, ds.count, Ps, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(ctx, cudaMemcpyAsync(so->depth, ds.depth, Ps * k * 8, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(ctx, cudaMemcpyAsync(so->rgba, ds.rgba, Ps * k * 16, cudaMemcpyDeviceToHost, st));
@@ -1604,6 +1616,7 @@ vdi_status vdi_composite_host_dense(vdi_ctx* ctx, const vdi_dense_view* local, u
   vdi_full_view ds{ctx->row0, ctx->row1, ctx->hstrip_count.as<uint8_t>(), ctx->hstrip_depth.as<float>(),
                    ctx->hstrip_rgba.as<float>()};
   if (vdi_status s = vdi_composite(ctx, dv.data(), n_local, &ds)) return s;
+  if (vdi_status s = peer_quiesce(ctx, st)) return s;
   // the composited strip in the dense representation:
   // scan of its counts, packed copy of its records, then only those bytes
   // cross PCIe
@@ -1691,10 +1704,13 @@ vdi_status vdi_composite_host_dense_frames(vdi_ctx* ctx, uint32_t F, const vdi_d
   vdi_full_view ds{ctx->row0, ctx->row1, nullptr, ctx->hstrip_depth.as<float>(), ctx->hstrip_rgba.as<float>()};
   std::vector<vdi_dense_view> dv[2];
   int launches = 0;
-  // H2D of frame f into slot f&1, once the compositing of frame f-2 has read it
+  // H2D of frame f into slot f&1, once the compositing of frame f-2 has read
+  // it.  n_ranks > 1: peers pull their strip slices out of this rank's slot
+  // during THEIR compositing of f-2, which has ended once this rank's
+  // compositing of f-1 is past its size-exchange collective -- so wait for f-1
   auto h2d = [&](uint32_t f) -> vdi_status {
     const int sl = f & 1;
-    CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->pin_st, ctx->pev_used[sl], 0));
+    CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->pin_st, ctx->pev_used[cf.n_ranks > 1 ? sl ^ 1 : sl], 0));
     if (vdi_status s = upload_host_pes(ctx, local + (size_t)f * n_local, n_local, dv[sl], sl, ctx->pin_st)) return s;
     CUDA_TRY(ctx, cudaEventRecord(ctx->pev_in[sl], ctx->pin_st));
     return VDI_OK;
@@ -1771,6 +1787,7 @@ vdi_status vdi_composite_host_dense_frames(vdi_ctx* ctx, uint32_t F, const vdi_d
     if (f + 1 < F)
       if (vdi_status s = compute(f + 1)) return s;
   }
+  if (vdi_status s = peer_quiesce(ctx, st)) return s;  // the last frames' slots (next call)
   CUDA_TRY(ctx, cudaStreamSynchronize(ctx->pout_st));
   CUDA_TRY(ctx, cudaStreamSynchronize(ctx->pin_st));
   CUDA_TRY(ctx, cudaStreamSynchronize(st));
