@@ -38,13 +38,16 @@ typedef enum {
 } vdi_status;
 
 /* vdi_config.flags */
-#define VDI_FLAG_PIXEL_STATS 0x1u  /* keep per-pixel gamma* and m of the last composite (vdi_pixel_stats) */
+#define VDI_FLAG_PIXEL_STATS 0x1u  /* keep per-list gamma*, tie margin and m of the last composite (vdi_pixel_stats) */
 #define VDI_FLAG_VALIDATE 0x2u     /* check inputs: count <= k_in, tf < tb, 0 < alpha <= 1, sorted runs */
 #define VDI_FLAG_STAGE_TIMING 0x4u /* record CUDA-event times of the exchange / merge / gather stages */
-#define VDI_FLAG_PEER_READS 0x20u    /* peer exchange without copies: the merge kernels load peers' slices over NVLink */
-#define VDI_FLAG_NCCL_EXCHANGE 0x10u /* exchange through NCCL send/recv into receive buffers (default: copy engines pull peers' slices over NVLink from CUDA IPC mappings) */
-#define VDI_FLAG_CE_COPIES 0x40u     /* peer exchange copies on the copy engines (default: one SM kernel pulls the slices over NVLink -- strip mode, and the first owned frame of vdi_composite_frames; later frames always use the copy engines, overlapping the merges) */
-#define VDI_FLAG_FULL_GATHER 0x8u  /* gather the full representation as in PAPER.md:185 (default: dense gather + root inflate, identical image) */
+#define VDI_FLAG_LOOPBACK 0x10u    /* n_ranks > 1 contexts in ONE process (any devices, e.g. all on one GPU):
+                                      nccl_unique_id is only the group's key, the windows are exchanged
+                                      in-process instead of by NCCL + CUDA IPC; the device path is the same */
+#define VDI_FLAG_HOST_SPAN 0x20u   /* _host entries: the caller promises that the host arrays of one call lie
+                                      in ONE allocation (e.g. a pinned arena); libvdi then copies the span
+                                      [lowest array start, highest array end) with one host->device copy,
+                                      gap bytes included (default: one copy per array) */
 
 typedef struct vdi_ctx vdi_ctx; /* opaque */
 
@@ -52,19 +55,26 @@ typedef struct vdi_ctx vdi_ctx; /* opaque */
  * PEs (processing elements) are the sources of sub-VDIs; PE s
  * is homed on rank floor(s * n_ranks / n_pes) ("block manner").
  * Rank g composites image rows [floor(g H / G), floor((g+1) H / G)) with
- * G = n_ranks (direct send; Q13). */
+ * G = n_ranks (direct send; Q13).
+ * n_ranks > 1: vdi_composite_init allocates this rank's window (flag words,
+ * two parities of receive slots for the strip slices of every PE homed
+ * elsewhere -- rows*W*(1 + 24 k_in) bytes each -- and two parities of a
+ * root-side gather buffer of W*H*(1 + 24 k_out) bytes) and exchanges its
+ * CUDA IPC handle with all ranks (one NCCL all-gather, collective; with
+ * VDI_FLAG_LOOPBACK an in-process registry).  After init no call
+ * synchronises the host. */
 typedef struct {
   uint32_t width, height;  /* image = N_lists = w h lists */
   uint32_t k_in;           /* per-PE budget of the sub-VDIs, 1..255 */
   uint32_t k_out;          /* budget of the composited lists, 1..255 (N_s) */
   uint32_t n_pes;          /* number of PEs (sources), >= 1 */
-  uint32_t n_ranks, rank;  /* GPUs (one process per GPU) and this process's index */
-  uint32_t root;           /* rank that receives the gathered image (Q14: 0 unless several
-                              frames are in flight, when frame f may be gathered on rank f mod G) */
+  uint32_t n_ranks, rank;  /* GPUs (one process per GPU; 1..64) and this context's index */
+  uint32_t root;           /* rank that receives the gathered image of vdi_gather (Q14: 0) */
   uint32_t max_iters;      /* bisection iterations I; 0 -> 16 (Q5) */
   float gamma_max;         /* upper end of the gamma search; 0 -> 2.0 (Q5) */
   uint32_t flags;          /* VDI_FLAG_* */
-  const uint8_t* nccl_unique_id; /* 128 bytes from vdi_get_unique_id on rank 0; required iff n_ranks > 1 */
+  const uint8_t* nccl_unique_id; /* 128 bytes from vdi_get_unique_id on rank 0; required iff n_ranks > 1
+                                    (VDI_FLAG_LOOPBACK: any 128 bytes shared by the group's contexts) */
   void* cuda_stream;             /* cudaStream_t (borrowed); NULL = legacy default stream */
 } vdi_config;
 
@@ -135,9 +145,15 @@ const char* vdi_last_error(const vdi_ctx* ctx); /* NULL-safe; thread-local text 
 vdi_status vdi_get_unique_id(uint8_t out[128]);
 
 /* Validates cfg (VDI_ERR_INVALID_ARG), binds the current CUDA device, and for
- * n_ranks > 1 creates the NCCL communicator (collective over all ranks). */
+ * n_ranks > 1 allocates the window and exchanges it (collective over all
+ * ranks: NCCL communicator + all-gather of CUDA IPC handles; VDI_FLAG_LOOPBACK:
+ * registration in the process, the group is complete once all n_ranks
+ * contexts exist -- calls before that return VDI_ERR_STATE).
+ * VDI_ERR_OUT_OF_MEMORY if the window does not fit. */
 vdi_status vdi_composite_init(const vdi_config* cfg, vdi_ctx** out);
-void vdi_composite_destroy(vdi_ctx* ctx); /* NULL-safe; waits for the ctx's stream, frees ctx-owned memory; local (no collective) */
+void vdi_composite_destroy(vdi_ctx* ctx); /* NULL-safe; waits for the ctx's stream, frees ctx-owned memory; local
+                                             (no collective) -- destroy a group's contexts only once no rank
+                                             has calls in flight (peers write into this window) */
 
 /* ---- Phase 1 (SUPPORT): sub-VDI of PE pe_id --------------------------------
  * Two passes per ray: pass 1 finds gamma and the count it
@@ -155,52 +171,44 @@ vdi_status vdi_generate_subvdi(vdi_ctx* ctx, const vdi_volume_desc* vol, const v
 
 /* ---- Phase 2: the hot path -------------------------------------------------
  * Parallel compositing of the sub-VDIs, collective over
- * all ranks: strip totals, size exchange + all-to-allv of count slices and
- * dense payload slices (NCCL over NVLink, no-op for n_ranks
- * == 1), receive-side scans, then per list: depth ordering,
- * overlap subdivision (Eq. 2 generalised, Q12), verbatim pass-through when
- * m <= k_out (Q9), otherwise the per-ray gamma bisection over the
- * sub-supersegments and the final greedy sweep, written in the
- * full representation.
+ * all ranks (n_ranks == 1: local):
+ *   a2  strip bounds: each rank finds, ON THE DEVICE, where every strip g
+ *       starts in each of its PEs' payloads (offset[row_g W], or a scan of
+ *       the counts when a view has no offset array);
+ *   a3/a4 exchange: each rank pushes, for every local PE and
+ *       every other strip g, the count slice and the packed payload slice
+ *       into rank g's window over NVLink (one kernel, plain stores into CUDA
+ *       IPC mappings); every block then bumps a counter word at g, and rank
+ *       g proceeds once the counter of each sender reaches its block count
+ *       for this call -- sizes never cross the host;
+ *   a5  receive-side scan of every source's count slice (Q17);
+ *   a6-a10 per list: depth ordering, overlap subdivision
+ *       (Eq. 2 generalised, Q12), verbatim pass-through when m <= k_out (Q9),
+ *       otherwise the per-ray gamma bisection over the sub-supersegments
+ *        and the final greedy sweep, written in the full
+ *       representation.
  * local_pes: the n_local sub-VDIs homed on this rank, any order, each with a
- * distinct pe_id (offset arrays are required when n_ranks > 1; with one rank,
- * when every view carries its offsets they supply the group bases and the
- * receive-side scan is skipped -- they must then be the exclusive scan of count).  strip_out: caller-owned, rows of this rank's strip
- * (VDI_ERR_CAPACITY if the row range does not match).  Synchronises the
- * stream once when n_ranks > 1 (sizes of the all-to-allv).  Exchange: by
- * default the remote PEs' strip slices are pulled over NVLink by the copy
- * engines from CUDA IPC mappings of the peers' buffers (input arrays must
- * then be cudaMalloc memory, e.g. torch tensors); VDI_FLAG_PEER_READS lets
- * the merge kernels read peer memory directly (no copies);
- * VDI_FLAG_NCCL_EXCHANGE uses NCCL send/recv. */
+ * distinct pe_id; device memory (any allocation: only this rank reads it).
+ * Offset arrays are optional: with one rank, when every view carries its
+ * offsets they supply the group bases and the receive-side scan is skipped
+ * (they must then be the exclusive scan of count).  strip_out: caller-owned,
+ * rows of this rank's strip (VDI_ERR_CAPACITY if the row range does not
+ * match).  Never synchronises the host; the inputs are free once the stream
+ * passes the call (only this rank reads them).  The receive slots are
+ * double-buffered: a sender waits (on the device) until the receiver has
+ * merged the call before last. */
 vdi_status vdi_composite(vdi_ctx* ctx, const vdi_dense_view* local_pes, uint32_t n_local,
                          vdi_full_view* strip_out);
-
-/* Frames in flight: n_frames independent VDIs in one
- * collective call, the image-space partition taken at frame granularity
- * (PAPER.md:164): frame f is composited whole by rank f mod n_ranks, which is
- * also its root, so no gather follows.  One size + IPC-reference
- * exchange covers every frame (one host sync); the owner's copy engines pull
- * every remote PE's sub-VDI of its frames over NVLink in
- * `chunks` row ranges (0 -> 2, at most 8), and the merge of vdi_composite
- * runs on chunk c while chunk c+1 is in flight.  The image
- * of every frame equals vdi_composite of that frame on one GPU, bit for bit.
- * local_pes: [n_frames][n_local] dense views, frame-major: the PEs homed here
- * (offset arrays required; cudaMalloc memory when n_ranks > 1).  images:
- * [n_frames] caller-owned full representations of rows [0, H); only the
- * frames owned by this rank are read or written (others may be zeroed
- * structs).  Counters and pixel stats describe the last merged chunk. */
-vdi_status vdi_composite_frames(vdi_ctx* ctx, uint32_t n_frames, const vdi_dense_view* local_pes,
-                                uint32_t n_local, vdi_full_view* images, uint32_t chunks);
 
 /* The full-representation variant of the compositing (Fig. 6
  * "full"): every local PE's sub-VDI is given in the full
  * representation (rows [0, H), k_in slots per list, unused slots zero,
- * PAPER.md:111), the strips are exchanged as fixed-size slices (NCCL
- * send/recv, no size exchange: P_g (1 + 24 k_in) bytes per PE and strip),
- * and each source is compacted to the dense layout on the receiver before
- * the same merge as vdi_composite -- so the image is identical.  pe_ids[l]
- * names the PE of local_pes[l].  Collective; synchronises the stream once. */
+ * PAPER.md:111), the strips are exchanged as fixed-size slices (pushed into
+ * the same window slots, P_g (1 + 24 k_in) bytes per PE and strip), and each
+ * source is compacted to the dense layout on the receiver before the same
+ * merge as vdi_composite -- so the image is identical.  pe_ids[l] names the
+ * PE of local_pes[l].  Collective; synchronises the host once (the record
+ * total of the compaction sizes the merge, as in the paper's pipeline). */
 vdi_status vdi_composite_fullrep(vdi_ctx* ctx, const vdi_full_view* local_pes, const uint32_t* pe_ids,
                                  uint32_t n_local, vdi_full_view* strip_out);
 
@@ -213,10 +221,9 @@ vdi_status vdi_dense_to_full(vdi_ctx* ctx, const vdi_dense_view* in, vdi_full_vi
  * copies the local sub-VDIs host->device (pinned memory recommended),
  * composites, and copies the strip back device->host into strip_out.
  * Pointers in local_pes / strip_out are host pointers.  Synchronises.
- * Host inputs of every _host entry: when all local arrays lie packed in one
- * span (gaps <= 1/16 of the bytes or 1 MiB; depth 8-B, rgba 16-B, offset
- * 4-B aligned), the span is copied with ONE host->device copy (the library
- * reads the gap bytes too); otherwise each array is copied on its own. */
+ * Host inputs of every _host entry: count, depth and rgba are copied (offset
+ * arrays are ignored: the device re-derives what it needs from the counts),
+ * one copy per array, or one copy of their span with VDI_FLAG_HOST_SPAN. */
 vdi_status vdi_composite_host(vdi_ctx* ctx, const vdi_dense_view* local_pes, uint32_t n_local,
                               vdi_full_view* strip_out);
 
@@ -256,37 +263,49 @@ vdi_status vdi_composite_host_dense(vdi_ctx* ctx, const vdi_dense_view* local_pe
 vdi_status vdi_composite_host_dense_frames(vdi_ctx* ctx, uint32_t n_frames, const vdi_dense_view* local_pes,
                                            uint32_t n_local, vdi_dense_strip* outs);
 
-/* Gather of the composited strips onto vdi_config.root (PAPER.md:185
+/* Gather (a11) of the composited strips onto vdi_config.root (PAPER.md:185
  * MPI_Gather; Q14): image_out (rows [0, H), root only; ignored elsewhere)
- * receives every rank's strip at its rows.  Default: each rank sends its counts + packed records
- * (dense) and the root re-inflates the full representation -- the image is
- * identical to gathering the full representation (VDI_FLAG_FULL_GATHER).
- * Synchronises the stream once when n_ranks > 1 (payload sizes).  For
- * n_ranks == 1 it copies the strip if the buffers differ (none if strip_out
- * aliases the image rows). */
+ * receives every rank's strip at its rows.  Each non-root rank compacts its
+ * strip to counts + packed records (the dense representation,
+ * PAPER.md:113-115) straight into the root's window over NVLink and bumps a
+ * counter word there; the root waits for every rank's blocks, re-inflates the
+ * full representation with the pass-through kernel and copies its own strip
+ * (none if strip aliases the image rows).  The image is identical to gathering
+ * the full representation.  Never synchronises the host; the root's gather
+ * buffer is double-buffered (a rank waits on the device until the root has
+ * inflated the gather before last).  n_ranks == 1: copies the strip if the
+ * buffers differ. */
 vdi_status vdi_gather(vdi_ctx* ctx, const vdi_full_view* strip, vdi_full_view* image_out);
 
-/* ---- introspection ---------------------------------------------------------- */
-/* Per-pixel gamma* (0 for pass-through) and m (samples after sort/subdivision)
- * of this rank's strip for the last composite; device pointers [rows*W].
- * Requires VDI_FLAG_PIXEL_STATS. */
-vdi_status vdi_pixel_stats(vdi_ctx* ctx, float* gamma, uint16_t* m);
+/* vdi_gather onto rank `root` instead of vdi_config.root (e.g. a root that
+ * rotates over consecutive frames so that no GPU re-inflates every image);
+ * all ranks pass the same root. */
+vdi_status vdi_gather_root(vdi_ctx* ctx, uint32_t root, const vdi_full_view* strip, vdi_full_view* image_out);
 
-/* Counters of the last vdi_composite on this rank. */
+/* ---- introspection ---------------------------------------------------------- */
+/* Per-list gamma* (0 for pass-through), tie margin and m (samples after
+ * sort/subdivision) of this rank's strip for the last composite; device
+ * pointers [rows*W], each may be NULL.  The tie margin is the minimum over the
+ * executed comparisons of the bisection and the final sweep of
+ * |sqrt(D^2) - gamma| (double; +inf when no comparison ran) -- lists whose
+ * margin is < 1e-6 are the "ties" of the parity bar.  Requires
+ * VDI_FLAG_PIXEL_STATS (a replay kernel per composite computes the margins). */
+vdi_status vdi_pixel_stats(vdi_ctx* ctx, float* gamma, float* min_margin, uint16_t* m);
+
+/* Counters of the last vdi_composite / vdi_gather on this rank (synchronises the stream). */
 typedef struct {
   uint64_t records_in;      /* sum over local strip lists of m before subdivision (supersegments merged) */
   uint64_t records_search;  /* the part of records_in that belongs to lists needing the gamma search / general path */
   uint64_t searched_lists;  /* lists that needed the gamma search or subdivision */
-  uint64_t bytes_sent;      /* all-to-allv payload bytes sent to other ranks */
-  uint64_t bytes_received;  /* all-to-allv payload bytes received */
+  uint64_t bytes_sent;      /* exchange bytes this rank pushed to other ranks (counts + records) */
+  uint64_t bytes_received;  /* exchange bytes other ranks pushed into this rank's window */
   uint32_t kernel_launches; /* libvdi kernels launched by the call */
   float ms_exchange, ms_merge, ms_gather; /* VDI_FLAG_STAGE_TIMING, else 0 */
-  uint64_t bucket_lists[4];  /* lists sent to the search buckets m <= 32, <= 40, <= 64, <= 255 */
-  uint64_t general_lists;    /* lists sent to the general path (overlaps, alpha == 0, m > 128) */
-  uint64_t bytes_gather;     /* bytes that crossed into the root in the last vdi_gather (G > 1) */
+  uint64_t bucket_lists[4];  /* lists sent to the search buckets m <= 32, <= 40, <= 64, > 64 */
+  uint64_t general_lists;    /* lists sent to the general path (overlaps, alpha == 0, no search-pool room) */
+  uint64_t bytes_gather;     /* last vdi_gather: bytes that crossed into the root (root) / pushed (others) */
   uint64_t fallback_groups;  /* 32-list groups written with plain stores (tail group / unaligned output) */
   float ms_scan, ms_fast, ms_search; /* VDI_FLAG_STAGE_TIMING: receive scan, pass-through kernel, search kernels */
-  float ms_sizes, ms_pull;           /* VDI_FLAG_STAGE_TIMING, vdi_composite_frames: size exchange (+ host sync), SM pull of the first owned frame */
 } vdi_counters;
 vdi_status vdi_get_counters(vdi_ctx* ctx, vdi_counters* out);
 

@@ -18,10 +18,8 @@ VDI_OK = 0
 VDI_FLAG_PIXEL_STATS = 0x1
 VDI_FLAG_VALIDATE = 0x2
 VDI_FLAG_STAGE_TIMING = 0x4
-VDI_FLAG_FULL_GATHER = 0x8
-VDI_FLAG_NCCL_EXCHANGE = 0x10
-VDI_FLAG_PEER_READS = 0x20
-VDI_FLAG_CE_COPIES = 0x40
+VDI_FLAG_LOOPBACK = 0x10
+VDI_FLAG_HOST_SPAN = 0x20
 
 
 class vdi_config(C.Structure):
@@ -68,8 +66,8 @@ class vdi_counters(C.Structure):
     _fields_ = [("records_in", C.c_uint64), ("records_search", C.c_uint64), ("searched_lists", C.c_uint64), ("bytes_sent", C.c_uint64),
                 ("bytes_received", C.c_uint64), ("kernel_launches", C.c_uint32), ("ms_exchange", C.c_float),
                 ("ms_merge", C.c_float), ("ms_gather", C.c_float), ("bucket_lists", C.c_uint64 * 4),
-                ("general_lists", C.c_uint64), ("bytes_gather", C.c_uint64), ("fallback_groups", C.c_uint64), ("ms_scan", C.c_float), ("ms_fast", C.c_float),
-                ("ms_search", C.c_float), ("ms_sizes", C.c_float), ("ms_pull", C.c_float)]
+                ("general_lists", C.c_uint64), ("bytes_gather", C.c_uint64), ("fallback_groups", C.c_uint64),
+                ("ms_scan", C.c_float), ("ms_fast", C.c_float), ("ms_search", C.c_float)]
 
 
 # name -> (restype, argtypes) exactly as declared in include/vdi.h
@@ -86,8 +84,6 @@ SIGNATURES = {
     "vdi_composite": (C.c_int, [C.c_void_p, C.POINTER(vdi_dense_view), C.c_uint32, C.POINTER(vdi_full_view)]),
     "vdi_composite_host": (C.c_int, [C.c_void_p, C.POINTER(vdi_dense_view), C.c_uint32,
                                      C.POINTER(vdi_full_view)]),
-    "vdi_composite_frames": (C.c_int, [C.c_void_p, C.c_uint32, C.POINTER(vdi_dense_view), C.c_uint32,
-                                       C.POINTER(vdi_full_view), C.c_uint32]),
     "vdi_composite_fullrep": (C.c_int, [C.c_void_p, C.POINTER(vdi_full_view), C.c_void_p, C.c_uint32,
                                         C.POINTER(vdi_full_view)]),
     "vdi_dense_to_full": (C.c_int, [C.c_void_p, C.POINTER(vdi_dense_view), C.POINTER(vdi_full_view)]),
@@ -96,7 +92,8 @@ SIGNATURES = {
     "vdi_composite_host_dense_frames": (C.c_int, [C.c_void_p, C.c_uint32, C.POINTER(vdi_dense_view), C.c_uint32,
                                                   C.POINTER(vdi_dense_strip)]),
     "vdi_gather": (C.c_int, [C.c_void_p, C.POINTER(vdi_full_view), C.POINTER(vdi_full_view)]),
-    "vdi_pixel_stats": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
+    "vdi_gather_root": (C.c_int, [C.c_void_p, C.c_uint32, C.POINTER(vdi_full_view), C.POINTER(vdi_full_view)]),
+    "vdi_pixel_stats": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "vdi_get_counters": (C.c_int, [C.c_void_p, C.POINTER(vdi_counters)]),
     "vdi_strip_rows": (C.c_int, [C.c_uint32, C.c_uint32, C.c_uint32, C.POINTER(C.c_uint32),
                                  C.POINTER(C.c_uint32)]),

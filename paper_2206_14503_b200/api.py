@@ -172,18 +172,6 @@ class Compositor:
         L.check(self.lib.vdi_composite(self.ctx, views, len(local_pes), C.byref(sv)), "vdi_composite")
         return strip
 
-    def composite_frames(self, frames_local_pes, images, chunks=0):
-        """vdi_composite_frames: frames_local_pes[f] = the PEs of frame f homed
-        here; images[f] = FullVDI of rows [0, H) for the frames this rank owns
-        (f % n_ranks == rank), None elsewhere."""
-        F = len(frames_local_pes)
-        nl = len(frames_local_pes[0]) if F else 0
-        flat = [p.view() for fr in frames_local_pes for p in fr]
-        views = (L.vdi_dense_view * max(1, len(flat)))(*flat)
-        ims = (L.vdi_full_view * max(1, F))(*[im.view() if im is not None else L.vdi_full_view() for im in images])
-        L.check(self.lib.vdi_composite_frames(self.ctx, F, views, nl, ims, chunks), "vdi_composite_frames")
-        return images
-
     def dense_to_full(self, pe: DenseSubVDI) -> FullVDI:
         """vdi_dense_to_full: the sub-VDI in the full representation (k_in slots)."""
         out = FullVDI.empty(self.width, 0, self.height, self.k_in)
@@ -203,17 +191,37 @@ class Compositor:
 
     def composite_host(self, local_pes, strip: FullVDI) -> FullVDI:
         """vdi_composite_host (host buffers; H2D + composite + D2H)."""
-        views = (L.vdi_dense_view * max(1, len(local_pes)))(*[p.view() for p in local_pes])
+        views = self._host_views(local_pes)
         sv = strip.view()
         L.check(self.lib.vdi_composite_host(self.ctx, views, len(local_pes), C.byref(sv)), "vdi_composite_host")
         return strip
+
+    def _dense_out(self, count, depth, rgba) -> L.vdi_dense_strip:
+        P = (self.row_end - self.row_begin) * self.width
+        for t, dt, w in ((count, torch.uint8, None), (depth, torch.float32, 2), (rgba, torch.float32, 4)):
+            if t.device.type != "cpu" or t.dtype != dt or not t.is_contiguous():
+                raise ValueError("dense outputs must be contiguous host tensors (u8 counts, f32 depth/rgba)")
+            if w is not None and (t.dim() != 2 or t.shape[1] != w):
+                raise ValueError(f"depth/rgba must be [capacity, {w}]")
+        if count.numel() != P:
+            raise ValueError(f"count must hold rows*W = {P} entries")
+        cap = min(depth.shape[0], rgba.shape[0])
+        return L.vdi_dense_strip(self.row_begin, self.row_end, cap, 0, _ptr(count), _ptr(depth), _ptr(rgba))
+
+    @staticmethod
+    def _host_views(local_pes):
+        for p in local_pes:
+            for t in (p.count, p.depth, p.rgba):
+                if t.device.type != "cpu" or not t.is_contiguous():
+                    raise ValueError("host entry points take contiguous host tensors")
+        return (L.vdi_dense_view * max(1, len(local_pes)))(*[p.view() for p in local_pes])
 
     def composite_host_dense(self, local_pes, count, depth, rgba) -> int:
         """vdi_composite_host_dense: host sub-VDIs in, the composited strip out
         in the dense representation into host tensors count u8[rows*W],
         depth f32[cap,2], rgba f32[cap,4].  Returns the supersegment total."""
-        views = (L.vdi_dense_view * max(1, len(local_pes)))(*[p.view() for p in local_pes])
-        out = L.vdi_dense_strip(self.row_begin, self.row_end, depth.shape[0], 0, _ptr(count), _ptr(depth), _ptr(rgba))
+        views = self._host_views(local_pes)
+        out = self._dense_out(count, depth, rgba)
         L.check(self.lib.vdi_composite_host_dense(self.ctx, views, len(local_pes), C.byref(out)),
                 "vdi_composite_host_dense")
         return int(out.total)
@@ -227,28 +235,32 @@ class Compositor:
         n_local = len(frames[0]) if F else 0
         if any(len(fr) != n_local for fr in frames) or len(outs) != F:
             raise ValueError("every frame needs the same number of local PEs and one output")
-        flat = [p.view() for fr in frames for p in fr]
-        views = (L.vdi_dense_view * max(1, len(flat)))(*flat)
-        ov = (L.vdi_dense_strip * max(1, F))(*[
-            L.vdi_dense_strip(self.row_begin, self.row_end, d.shape[0], 0, _ptr(c), _ptr(d), _ptr(r))
-            for c, d, r in outs])
+        views = self._host_views([p for fr in frames for p in fr])
+        ov = (L.vdi_dense_strip * max(1, F))(*[self._dense_out(c, d, r) for c, d, r in outs])
         L.check(self.lib.vdi_composite_host_dense_frames(self.ctx, F, views, n_local, ov),
                 "vdi_composite_host_dense_frames")
         return [int(ov[f].total) for f in range(F)]
 
-    def gather(self, strip: FullVDI, image: FullVDI | None):
-        """vdi_gather: strips -> the root rank (image ignored on other ranks)."""
+    def gather(self, strip: FullVDI, image: FullVDI | None, root: int | None = None):
+        """vdi_gather (root=None: the config's root) / vdi_gather_root: strips ->
+        the root rank (image ignored on other ranks)."""
         sv = strip.view()
         iv = image.view() if image is not None else None
-        L.check(self.lib.vdi_gather(self.ctx, C.byref(sv), C.byref(iv) if iv is not None else None), "vdi_gather")
+        ip = C.byref(iv) if iv is not None else None
+        if root is None:
+            L.check(self.lib.vdi_gather(self.ctx, C.byref(sv), ip), "vdi_gather")
+        else:
+            L.check(self.lib.vdi_gather_root(self.ctx, root, C.byref(sv), ip), "vdi_gather_root")
         return image
 
-    def pixel_stats(self):
+    def pixel_stats(self, with_margin=False):
+        """vdi_pixel_stats: per-list gamma*, m (and the tie margin) of the last composite."""
         P = (self.row_end - self.row_begin) * self.width
         g = torch.empty(P, dtype=torch.float32, device="cuda")
+        mg = torch.empty(P, dtype=torch.float32, device="cuda")
         m = torch.empty(P, dtype=torch.int16, device="cuda")
-        L.check(self.lib.vdi_pixel_stats(self.ctx, g.data_ptr(), m.data_ptr()), "vdi_pixel_stats")
-        return g, m
+        L.check(self.lib.vdi_pixel_stats(self.ctx, g.data_ptr(), mg.data_ptr(), m.data_ptr()), "vdi_pixel_stats")
+        return (g, m, mg) if with_margin else (g, m)
 
     def counters(self) -> dict:
         c = L.vdi_counters()

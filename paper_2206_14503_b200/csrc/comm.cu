@@ -1,0 +1,234 @@
+// comm.cu — device-driven exchange and gather of libvdi (sm_100a).
+//
+// Every byte of the strip exchange (MPI_AllToAllv in the paper)
+// and of the gather to the root (MPI_Gather) is moved by these
+// kernels with plain stores into the receiving GPU's memory over NVLink 5 /
+// NVSwitch (CUDA IPC mappings of ctx-owned windows, opened once at init) --
+// no host round trip, no size exchange on the host:
+//   * a sender reads its strip bounds from its own offset arrays (or a scan
+//     of its counts) on the device and pushes the count slice and the packed
+//     payload slice of every (local PE, strip) pair into the owner's window;
+//   * every block, after its stores, bumps a per-sender counter word in the
+//     receiver's flag array (bar.sync + fence.sc.sys + atomic add at system
+//     scope), so the receiver knows its data has landed once the counter
+//     reaches (call index) x (blocks per call) -- both ends derive the block
+//     count from the config;
+//   * receivers wait with a one-CTA spin kernel (ld.acquire.sys) and release
+//     the sender's window slot with a one-CTA signal kernel after their merge.
+#include <cuda_runtime.h>
+
+#include "comm.h"
+
+namespace vdi {
+
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// all of this block's stores are performed (at system scope) before the
+// counter increment becomes visible
+__device__ __forceinline__ void block_arrive(uint32_t* flag) {
+  __syncthreads();
+  if (threadIdx.x == 0 && flag) {
+    __threadfence_system();
+    atomicAdd_system(flag, 1u);
+  }
+}
+
+template <class V>
+__device__ __forceinline__ void copy_span(const V* __restrict__ s, V* __restrict__ d, unsigned long long n,
+                                          unsigned long long i0, unsigned long long stride) {
+  unsigned long long i = i0;
+  for (; i + 3 * stride < n; i += 4 * stride) {
+    const V a = s[i], b = s[i + stride], c = s[i + 2 * stride], e = s[i + 3 * stride];
+    d[i] = a;
+    d[i + stride] = b;
+    d[i + 2 * stride] = c;
+    d[i + 3 * stride] = e;
+  }
+  for (; i < n; i += stride) d[i] = s[i];
+}
+
+// bytes [0, n) from s to d; the widest vector both addresses allow
+__device__ __forceinline__ void copy_bytes(const void* s, void* d, unsigned long long n, unsigned long long i0,
+                                           unsigned long long stride) {
+  const uintptr_t al = reinterpret_cast<uintptr_t>(s) | reinterpret_cast<uintptr_t>(d);
+  if (!(al & 15)) {
+    const unsigned long long n16 = n / 16;
+    copy_span(static_cast<const uint4*>(s), static_cast<uint4*>(d), n16, i0, stride);
+    for (unsigned long long i = n16 * 16 + i0; i < n; i += stride)
+      static_cast<uint8_t*>(d)[i] = static_cast<const uint8_t*>(s)[i];
+  } else if (!(al & 3)) {
+    const unsigned long long n4 = n / 4;
+    copy_span(static_cast<const uint32_t*>(s), static_cast<uint32_t*>(d), n4, i0, stride);
+    for (unsigned long long i = n4 * 4 + i0; i < n; i += stride)
+      static_cast<uint8_t*>(d)[i] = static_cast<const uint8_t*>(s)[i];
+  } else {
+    copy_span(static_cast<const uint8_t*>(s), static_cast<uint8_t*>(d), n, i0, stride);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Strip bounds of the local PEs (a2): bnd[l][g] = index of the first record of
+// strip g in PE l's payload, g = 0..G (bnd[l][G] = the PE's total).  From the
+// PE's offset array when given, else from the 32-list group
+// bases of a scan of its counts plus the partial group.
+// ---------------------------------------------------------------------------
+__global__ void bounds_kernel(BoundsArgs a) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= a.n_local * (a.G + 1)) return;
+  const int l = i / (a.G + 1), g = i % (a.G + 1);
+  const uint64_t p = (uint64_t)a.rows[g] * a.W;
+  uint64_t v;
+  if (a.offset[l]) {
+    v = a.offset[l][p];
+  } else {
+    const uint64_t g32 = p / 32;
+    v = g32 < a.n_groups ? a.gbase[(size_t)l * a.n_groups + g32] : a.total[l];
+    if (g32 < a.n_groups)
+      for (uint64_t q = g32 * 32; q < p; ++q) v += a.count[l][q];
+  }
+  a.bnd[(size_t)l * (a.G + 1) + g] = v;
+  if (g == a.me && a.srcbase) a.srcbase[a.pe[l]] = (uint32_t)v;
+}
+
+// ---------------------------------------------------------------------------
+// Push of (local PE, destination strip) slices into the destination windows
+// (a4): blockIdx.y = segment, blockIdx.x = share of it.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) push_kernel(const PushSeg* __restrict__ segs) {
+  const PushSeg sg = segs[blockIdx.y];
+  const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+  const unsigned long long i0 = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned long long r0, nrec;
+  if (sg.bnd) {  // dense slice [bnd[0], bnd[1]) of the payload
+    r0 = sg.bnd[0];
+    nrec = sg.bnd[1] - r0;
+  } else {       // fixed-size slice (full representation)
+    r0 = sg.rec0;
+    nrec = sg.nrec;
+  }
+  copy_bytes(sg.src_count, sg.dst_count, sg.n_count, i0, stride);
+  if (nrec) {
+    copy_bytes(sg.src_depth + r0, sg.dst_depth, nrec * 8, i0, stride);
+    copy_bytes(sg.src_rgba + r0, sg.dst_rgba, nrec * 16, i0, stride);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (sg.dst_hdr) *sg.dst_hdr = nrec;
+    if (sg.bytes) atomicAdd(sg.bytes, sg.n_count + 24ull * nrec);
+  }
+  block_arrive(sg.flag);
+}
+
+// ---------------------------------------------------------------------------
+// Gather (a11): compaction of a composited strip (full representation,
+// PAPER.md:185) into the root's window -- counts at their image rows, the
+// 32-list group bases of the packed records (+ region offset), the records
+// packed in list order -- then one counter bump per block at the root.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t warp_incl_scan_c(uint32_t v, int lane) {
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t t = __shfl_up_sync(0xffffffffu, v, d);
+    if (lane >= d) v += t;
+  }
+  return v;
+}
+
+__global__ void __launch_bounds__(128) compact_push_kernel(CompactPushArgs a) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t ng = (a.P + 31) / 32;
+  for (uint32_t g = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); g < ng;
+       g += gridDim.x * (blockDim.x >> 5)) {
+    const uint32_t p = g * 32 + lane;
+    const uint32_t c = p < a.P ? a.count[p] : 0u;
+    const uint32_t gb = a.group_base[g];
+    const size_t off = (size_t)a.region + gb + warp_incl_scan_c(c, lane) - c;  // record index in the root window
+    if (p < a.P) a.dst_count[p] = (uint8_t)c;
+    if (lane == 0) a.dst_gbase[g] = a.region + gb;
+    const float2* sd = a.depth + (size_t)p * a.k;
+    const float4* sc = a.rgba + (size_t)p * a.k;
+#pragma unroll 4
+    for (uint32_t j = 0; j < c; ++j) {
+      a.dst_depth[off + j] = __ldg(sd + j);
+      a.dst_rgba[off + j] = __ldg(sc + j);
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0 && a.total_out) {
+    // records of the strip = the base of the last group + its count sum
+    const uint32_t lg = ng ? ng - 1 : 0;
+    uint32_t t = ng ? a.group_base[lg] : 0u;
+    for (uint32_t q = lg * 32; q < a.P; ++q) t += a.count[q];
+    *a.total_out = t;
+    if (a.bytes) atomicAdd(a.bytes, (unsigned long long)a.P + 4ull * ng + 24ull * t);
+  }
+  block_arrive(a.flag);
+}
+
+// ---------------------------------------------------------------------------
+// Flags: one-CTA wait (thread t spins until flag t reaches its target, wrap-
+// aware) and one-CTA signal (release store of a value into peer flag words).
+// ---------------------------------------------------------------------------
+__global__ void wait_kernel(WaitArgs a) {
+  const int t = threadIdx.x;
+  if (t < a.n) {
+    while ((int32_t)(ld_acquire_sys(a.addr[t]) - a.target[t]) < 0) __nanosleep(64);
+  }
+  __syncthreads();
+}
+
+__global__ void signal_kernel(SignalArgs a) {
+  const int t = threadIdx.x;
+  if (t < a.n) {
+    __threadfence_system();
+    st_release_sys(a.addr[t], a.value[t]);
+  }
+}
+
+cudaError_t launch_bounds(const BoundsArgs& a, cudaStream_t st) {
+  const int n = a.n_local * (a.G + 1);
+  if (!n) return cudaSuccess;
+  bounds_kernel<<<(n + 127) / 128, 128, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_push(const PushSeg* dsegs, uint32_t n_segs, uint32_t blocks_per_seg, cudaStream_t st) {
+  if (!n_segs) return cudaSuccess;
+  push_kernel<<<dim3(blocks_per_seg, n_segs), 256, 0, st>>>(dsegs);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_compact_push(const CompactPushArgs& a, uint32_t blocks, cudaStream_t st) {
+  compact_push_kernel<<<blocks, 128, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_wait(const WaitArgs& a, cudaStream_t st) {
+  if (!a.n) return cudaSuccess;
+  wait_kernel<<<1, 64, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_signal(const SignalArgs& a, cudaStream_t st) {
+  if (!a.n) return cudaSuccess;
+  signal_kernel<<<1, 64, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t preload_comm() {
+  cudaFuncAttributes fa;
+  cudaFuncGetAttributes(&fa, bounds_kernel);
+  cudaFuncGetAttributes(&fa, push_kernel);
+  cudaFuncGetAttributes(&fa, compact_push_kernel);
+  cudaFuncGetAttributes(&fa, wait_kernel);
+  cudaFuncGetAttributes(&fa, signal_kernel);
+  return cudaGetLastError();
+}
+
+}  // namespace vdi

@@ -27,8 +27,9 @@ struct Rec {
 };
 
 // One composite source (PE) as seen by the merge kernels: the strip's count
-// slice and the payload slice, rebased so that the first record of the
-// strip's first list is at index 0.
+// slice and the source's payload array; record indices are absolute in the
+// payload array (the receive-side scan adds MergeParams::src_base[s], the
+// index of the strip's first record, which only the device knows).
 struct SrcDesc {
   const uint8_t* count;
   const float2* depth;
@@ -39,9 +40,9 @@ struct SrcDesc {
 
 // Work-list buckets of lists that need more than the pass-through:
 // 0, 1 = gamma search with m <= 32 / 40 samples (samples in registers);
-// 2, 3 = gamma search with m <= 64 / 255 samples (samples streamed from a pool);
-// 4 = general path (overlap subdivision, alpha==0 records, or m > 255;
-// thread per list, global scratch).
+// 2, 3 = gamma search with 40 < m <= 64 / m > 64 samples (samples in a pool);
+// 4 = general path (overlap subdivision, alpha==0 records, and lists whose
+// search-pool slot could not be allocated; thread per list, per-thread scratch).
 #define VDI_N_BUCKETS 5
 #define VDI_BUCKET_GENERAL 4
 
@@ -55,18 +56,20 @@ struct MergeParams {
   uint32_t n_groups;   // ceil(P / 32)
   uint32_t g_begin, g_end;  // 32-list groups of this launch's chunk of the strip
   const uint32_t* group_base;  // [n_src][n_groups] exclusive scan of 32-list group sums
+  const uint32_t* src_base;    // optional device [n_src]: added to the receive-side scan (strip start)
   uint8_t* out_count;          // [P]
   float2* out_depth;           // [P][k_out]
   float4* out_rgba;            // [P][k_out]
-  // work lists: entry i of bucket b = wl[b][i*(3+n_src) ...] = {p, scratch_base, m, off[0..n_src)}
+  // work lists: entry i of bucket b = wl[b][i*(3+n_src) ...] = {p, 0, m, off[0..n_src)}
   uint32_t* wl[VDI_N_BUCKETS];
   uint32_t* wl_count;          // [VDI_N_BUCKETS]
   uint32_t wl_cap;             // entries per bucket
-  unsigned long long* scratch_used;
-  unsigned long long scratch_cap;  // in records
-  Rec* scratch;
+  Rec* scratch;            // general path: gen_threads slices of gen_stride records
+  uint32_t gen_threads;    // threads of the general kernel (one scratch slice each)
+  uint32_t gen_stride;     // records per slice: 4 * (n_src * k_in)
   float* stat_gamma;   // optional [P]
   uint16_t* stat_m;    // optional [P]
+  float* stat_margin;  // optional [P]: min |sqrt(D^2) - gamma| over the executed comparisons
   unsigned long long* records_in;
   unsigned long long* records_search;   // records of lists sent to the search / general paths
   unsigned long long* fallback_groups;  // groups written with plain stores
@@ -85,7 +88,7 @@ struct MergeParams {
   unsigned long long long_cap;
   unsigned long long* long_used;
   PoolBatch* long_batch[2];
-  int* err;            // bit 0: work list / scratch overflow
+  int* err;            // bit 0: work-list overflow (cannot happen: capacity = lists)
   int validate;
 };
 
@@ -100,11 +103,14 @@ cudaError_t launch_total(const MergeParams& mp, const uint32_t* chunk_sum, unsig
                          int* launches);
 cudaError_t launch_compact(const uint8_t* count, const float2* depth, const float4* rgba, uint32_t P, int k,
                            const uint32_t* group_base, float2* od, float4* oc, cudaStream_t st, int* launches);
-// search + general kernels over the work lists in mp (stream st)
 // search kernels (buckets 0-3); after launch_fast (it zeroes their lists' slots)
 cudaError_t launch_search(const MergeParams& mp, cudaStream_t st, int* launches);
 // general path (bucket 4); after launch_fast and launch_search
 cudaError_t launch_general(const MergeParams& mp, cudaStream_t st, int* launches);
+// VDI_FLAG_PIXEL_STATS: tie margins of the searched lists (replays their bisection from the pools)
+cudaError_t launch_margins(const MergeParams& mp, cudaStream_t st, int* launches);
+uint32_t general_threads(uint32_t m_max);
+cudaError_t preload_merge();  // load every merge kernel now (loopback groups spin-wait across contexts)  // threads of the general kernel for lists of <= m_max records
 
 // Generator (generate.cu)
 struct GenParams {

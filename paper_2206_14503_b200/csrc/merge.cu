@@ -13,18 +13,19 @@
 //                             in unused slots) leaves with fully coalesced
 //                             streaming stores.  Lists with m > k_out go to a
 //                             search work list, bucketed by m;
-//   merge_search<MS>        : one warp per 32 work-list lists (lane = list),
-//                             m <= MS samples per list held in shared memory
-//                             in a [sample][lane] layout; gamma bisection
-//                              advanced two levels per
-//                             pass with three speculative sweeps (an exact
-//                             replay of the sequential procedure);
+//   search_gather/sweep     : lists with k_out < m <= 40: depth order into a
+//                             pool slot ([sample][lane]), then a warp per 32
+//                             lists sweeps register-resident samples through
+//                             the gamma bisection;
+//   long_gather/long_sweep  : lists with m > 40, the same from a byte pool;
 //   merge_general           : thread per list for overlapping records
 //                             (subdivision, Eq. 2 generalised, Q12), alpha==0
-//                             records (Q23) and m > 128.
+//                             records (Q23) and lists whose pool slot could not
+//                             be allocated.
 // The decision arithmetic (tau, the blend) is fp32 with explicit fmaf in the
 // order DESIGN.md §2 fixes; the TU is compiled with -fmad=false so no other
 // contraction happens.
+#include <algorithm>
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <math_constants.h>
@@ -115,7 +116,8 @@ __global__ void __launch_bounds__(128) group_base_kernel(MergeParams mp, const u
   const uint32_t base = red[0] + red[1] + red[2] + red[3];
   uint32_t woff = 0;
   for (int q = 0; q < w; ++q) woff += wtot[q];
-  if (g < mp.n_groups) group_base[(size_t)s * mp.n_groups + g] = base + woff + incl - gs;
+  const uint32_t sb = mp.src_base ? __ldg(mp.src_base + s) : 0u;  // index of the strip's first record
+  if (g < mp.n_groups) group_base[(size_t)s * mp.n_groups + g] = sb + base + woff + incl - gs;
 }
 
 // ---------------------------------------------------------------------------
@@ -143,11 +145,19 @@ __device__ __forceinline__ void n2d2_packed(float ar, float ag, float ab, float 
   asm("mov.b64 {%0, %1}, %2;" : "=f"(n2), "=f"(d2) : "l"(t));
 }
 
+// |sqrt(D^2) - gamma| in double (the tie margin of one executed comparison;
+// VDI_FLAG_PIXEL_STATS only)
+__device__ __forceinline__ void note_margin(double* mg, float d2, float gamma) {
+  if (mg) *mg = fmin(*mg, fabs(sqrt((double)d2) - (double)gamma));
+}
+
 // One greedy sweep over depth-ordered samples (
 // Q1, Q2, Q8).  get(i) returns sample i.  Count mode (od == nullptr) returns
 // early once cnt > k.  Write mode writes the closed segments to od/oc[0..cnt).
+// mg (optional) tracks the tie margin of the executed comparisons.
 template <class Get>
-__device__ __forceinline__ int sweep(Get get, int m, float gamma, int k, float2* od, float4* oc) {
+__device__ __forceinline__ int sweep(Get get, int m, float gamma, int k, float2* od, float4* oc,
+                                     double* mg = nullptr) {
   const float g2 = gamma * gamma;
   int cnt = 0;
   bool open = false;
@@ -155,7 +165,9 @@ __device__ __forceinline__ int sweep(Get get, int m, float gamma, int k, float2*
   for (int i = 0; i < m; ++i) {
     const Rec s = get(i);
     if (open && s.tf > prev_tb) {
-      if (dist2(ar, ag, ab, aa, 0.f, 0.f, 0.f, 0.f) > g2) {
+      const float n2 = dist2(ar, ag, ab, aa, 0.f, 0.f, 0.f, 0.f);
+      note_margin(mg, n2, gamma);
+      if (n2 > g2) {
         if (od && cnt <= k) {
           od[cnt - 1] = make_float2(tf, tb);
           oc[cnt - 1] = make_float4(ar, ag, ab, aa);
@@ -165,7 +177,9 @@ __device__ __forceinline__ int sweep(Get get, int m, float gamma, int k, float2*
     }
     bool start = !open;
     if (open) {
-      if (dist2(ar, ag, ab, aa, s.r, s.g, s.b, s.a) > g2) {
+      const float d2 = dist2(ar, ag, ab, aa, s.r, s.g, s.b, s.a);
+      note_margin(mg, d2, gamma);
+      if (d2 > g2) {
         if (od && cnt <= k) {
           od[cnt - 1] = make_float2(tf, tb);
           oc[cnt - 1] = make_float4(ar, ag, ab, aa);
@@ -203,11 +217,11 @@ __device__ __forceinline__ int sweep(Get get, int m, float gamma, int k, float2*
 // Per-list gamma bisection (PAPER.md:100-101 re-used at :176; Q3-Q6):
 // midpoints 0.5*(lo+hi) of [0, gamma_max], I iterations, stop at count == k.
 template <class Get>
-__device__ __forceinline__ float bisect(Get get, int m, int k, int iters, float gmax) {
+__device__ __forceinline__ float bisect(Get get, int m, int k, int iters, float gmax, double* mg = nullptr) {
   float lo = 0.f, hi = gmax, best = gmax;
   for (int it = 0; it < iters; ++it) {
     const float mid = 0.5f * (lo + hi);
-    const int c = sweep(get, m, mid, k, nullptr, nullptr);
+    const int c = sweep(get, m, mid, k, nullptr, nullptr, mg);
     if (c <= k) {
       best = hi = mid;
       if (c == k) break;
@@ -288,7 +302,6 @@ __device__ __forceinline__ void track(bool ev, bool gap, float n2, float d2, flo
 
 // Append the lanes with bk >= 0 to work-list bucket bk (one atomic per warp and
 // bucket).  goff[s] = index of the list's first record in source s's payload.
-// General-path entries also reserve 4 m scratch records.
 template <int NS>
 __device__ __forceinline__ void push_entries(const MergeParams& mp, int bk, uint32_t p, uint32_t m,
                                              const uint32_t (&goff)[NS], int lane) {
@@ -297,24 +310,15 @@ __device__ __forceinline__ void push_entries(const MergeParams& mp, int bk, uint
   for (int b = 0; b < VDI_N_BUCKETS; ++b) {
     const unsigned mask = __ballot_sync(kFull, bk == b);
     if (!mask) continue;
-    const uint32_t need = (bk == b && b == VDI_BUCKET_GENERAL) ? 4u * m : 0u;
-    const uint32_t incl = warp_incl_scan(need, lane);
-    const uint32_t tot = __shfl_sync(kFull, incl, 31);
     uint32_t w0 = 0;
-    unsigned long long s0 = 0;
-    if (lane == 0) {
-      w0 = atomicAdd(mp.wl_count + b, (uint32_t)__popc(mask));
-      if (tot) s0 = atomicAdd(mp.scratch_used, (unsigned long long)tot);
-    }
+    if (lane == 0) w0 = atomicAdd(mp.wl_count + b, (uint32_t)__popc(mask));
     w0 = __shfl_sync(kFull, w0, 0);
-    s0 = __shfl_sync(kFull, s0, 0);
     if (bk == b) {
       const uint32_t idx = w0 + __popc(mask & lt);
-      const unsigned long long sb = s0 + incl - need;
-      if (idx < mp.wl_cap && (b != VDI_BUCKET_GENERAL || sb + need <= mp.scratch_cap)) {
+      if (idx < mp.wl_cap) {
         uint32_t* e = mp.wl[b] + (size_t)idx * (3 + mp.n_src);
         e[0] = p;
-        e[1] = (uint32_t)sb;
+        e[1] = 0u;
         e[2] = m;
 #pragma unroll
         for (int s = 0; s < NS; ++s)
@@ -327,7 +331,7 @@ __device__ __forceinline__ void push_entries(const MergeParams& mp, int bk, uint
 }
 
 __device__ __forceinline__ int bucket_of(uint32_t m) {
-  return m <= 32 ? 0 : m <= 40 ? 1 : m <= 64 ? 2 : m <= 255 ? 3 : VDI_BUCKET_GENERAL;
+  return m <= 32 ? 0 : m <= 40 ? 1 : m <= 64 ? 2 : 3;
 }
 
 // Run-based k-way merge of NS sorted runs held in shared memory (PAPER.md:168:
@@ -527,9 +531,6 @@ __host__ __device__ constexpr size_t fast_warp_bytes(int k) {
 #ifndef VDI_FAST_RUN
 #define VDI_FAST_RUN 4
 #endif
-#ifndef VDI_FAST_LDGSTS
-#define VDI_FAST_LDGSTS 1
-#endif
 template <int NS>
 __global__ void __launch_bounds__(kFastThreads) merge_fast_kernel(MergeParams mp) {
   extern __shared__ float4 smem[];
@@ -631,7 +632,6 @@ __global__ void __launch_bounds__(kFastThreads) merge_fast_kernel(MergeParams mp
           start[s] = j;
           j += cnt[s];
         }
-#if VDI_FAST_LDGSTS
         // every record straight into its slot of the image with async copies
         // (LDGSTS): all of the list's loads in flight at once, no registers,
         // no per-record source selection
@@ -648,9 +648,6 @@ __global__ void __launch_bounds__(kFastThreads) merge_fast_kernel(MergeParams mp
           }
         }
         asm volatile("cp.async.wait_all;" ::: "memory");
-#else
-        load_concat<NS, 4>(mp, gidx, cnt, start, m, my_depth, my_rgba, 1);
-#endif
         written = m;
         // already in depth order (e.g. a single PE's run)?  then only validate
         bool sorted = true;
@@ -717,6 +714,7 @@ __global__ void __launch_bounds__(kFastThreads) merge_fast_kernel(MergeParams mp
       mp.out_count[p] = pass ? (uint8_t)m : (uint8_t)0;
       if (mp.stat_m) mp.stat_m[p] = (uint16_t)m;
       if (mp.stat_gamma) mp.stat_gamma[p] = 0.f;
+      if (mp.stat_margin) mp.stat_margin[p] = CUDART_INF_F;  // no comparison executed (overwritten if searched)
     }
   }
   if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
@@ -781,11 +779,13 @@ __device__ __forceinline__ void gather_short_batch(const MergeParams& mp, uint32
   uint32_t slot = 0;
   if (lane == 0) {
     slot = atomicAdd(mp.pool_next, 1u);
-    if (slot < mp.pool_cap) mp.batch_slot[bucket][i >> 5] = slot;
-    else atomicOr(mp.err, 1);
+    mp.batch_slot[bucket][i >> 5] = slot;  // >= pool_cap: the sweep skips the batch
   }
   slot = __shfl_sync(kFull, slot, 0);
-  if (slot >= mp.pool_cap) return;
+  if (slot >= mp.pool_cap) {  // pool exhausted: the batch's lists take the general path
+    if (__any_sync(kFull, valid)) push_entries<NS>(mp, valid ? VDI_BUCKET_GENERAL : -1, p, m, goff, lane);
+    return;
+  }
   float4* orgba = mp.pool_rgba + (size_t)slot * 40 * 32 + lane;
   float2* odep = mp.pool_depth + (size_t)slot * 40 * 32 + lane;
   // depth column in PE order (independent loads), then the depth order
@@ -846,21 +846,12 @@ __device__ __forceinline__ void gather_short_batch(const MergeParams& mp, uint32
   if (__any_sync(kFull, bk >= 0)) push_entries<NS>(mp, bk, p, m, goff, lane);
 }
 
-#ifndef VDI_PACKED_D2
-#define VDI_PACKED_D2 1  // alone: 0.173 vs 0.166 ms (the packed chain is longer); with the memo it frees the registers
-#endif
-#ifndef VDI_SHORT_MEMO
-#define VDI_SHORT_MEMO 1  // with VDI_PACKED_D2: search 0.1637 vs 0.1658 ms (alone: 0.173, slower)
-#endif
-struct NoOp {
-  __device__ __forceinline__ void operator()() const {}
-};
-// sbuf: the batch's samples already in shared memory ([sample][lane]); after()
-// runs once they are in registers (the prefetching sweep kernel claims the
-// next batch and starts its copy into the same buffer there)
-template <int MS, class After = NoOp>
-__device__ __forceinline__ void sweep_batch(const MergeParams& mp, int bucket, uint32_t batch,
-                                            const float4* sbuf = nullptr, After after = After()) {
+// Short-list sweep of one batch (32 work-list entries, lane = list): the
+// samples are loaded once into a statically indexed register file, then the
+// memoised bisection (see Bisection) sweeps while any lane still needs a
+// count; (|acc|^2, |acc - s|^2) are one packed f32x2 chain.
+template <int MS>
+__device__ __forceinline__ void sweep_batch(const MergeParams& mp, int bucket, uint32_t batch) {
   const int lane = threadIdx.x;
   const int k = mp.k_out, n = mp.n_src;
   const uint32_t total = min(mp.wl_count[bucket], mp.wl_cap);
@@ -883,21 +874,12 @@ __device__ __forceinline__ void sweep_batch(const MergeParams& mp, int bucket, u
     float4 S[MS];
     const float qnan = __int_as_float(0x7fc00000);
 #pragma unroll
-    for (int q = 0; q < MS; ++q)
-      S[q] = (q < mi && !bad) ? (sbuf ? sbuf[q * 32 + lane] : col[q * 32]) : make_float4(qnan, qnan, qnan, qnan);
-    if (sbuf) {
-      // the samples are in registers: the buffer may take the next batch
-      // (generic-proxy reads ordered before the async-proxy bulk write)
-      __syncwarp();
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      after();
-    }
-#if VDI_SHORT_MEMO
-    // memoised bisection (as in the long-list sweep): a count sweep at g2
-    // takes the same decisions for every g2' in [L, U), so a later midpoint
-    // inside the interval of the latest sweep on either side of the bracket
-    // reuses its count; each lane resolves such levels on its own and the
-    // warp sweeps while any lane still needs a sweep
+    for (int q = 0; q < MS; ++q) S[q] = (q < mi && !bad) ? col[q * 32] : make_float4(qnan, qnan, qnan, qnan);
+    // memoised bisection: a count sweep at g2 takes the same decisions for
+    // every g2' in [L, U), so a later midpoint inside the interval of the
+    // latest sweep on either side of the bracket reuses its count; each lane
+    // resolves such levels on its own and the warp sweeps while any lane
+    // still needs a sweep
     Bisection bs;
     bs.init(mp.gamma_max, valid && !bad && mp.max_iters > 0);
     for (;;) {
@@ -912,13 +894,8 @@ __device__ __forceinline__ void sweep_batch(const MergeParams& mp, int bucket, u
         const float4 sv = S[q];
         const bool gap = sv.w < 0.f;  // NaN padding: false
         const float sa = fabsf(sv.w);
-#if VDI_PACKED_D2
         float n2, d2;
         n2d2_packed(ar, ag, ab, aa, sv.x, sv.y, sv.z, sa, n2, d2);
-#else
-        const float n2 = fmaf(aa, aa, fmaf(ab, ab, fmaf(ag, ag, ar * ar)));  // dist2(acc, 0), Q8
-        const float d2 = dist2(ar, ag, ab, aa, sv.x, sv.y, sv.z, sa);
-#endif
         const bool gcl = gap & (n2 > g2);
         const bool dsp = d2 > g2;
         if (q > 0) {  // comparisons that did not happen contribute NaN (ignored by fminf / fmaxf)
@@ -936,52 +913,6 @@ __device__ __forceinline__ void sweep_batch(const MergeParams& mp, int bucket, u
       if (bs.active) bs.swept(sc, L, U, k, mp.max_iters);
     }
     const float best = bs.best;
-#else
-    bool active = valid && !bad && mp.max_iters > 0;
-    float lo = 0.f, hi = mp.gamma_max, best = mp.gamma_max;
-    for (int it = 0; it < mp.max_iters; ++it) {
-      if (!__any_sync(kFull, active)) break;
-      const float mid = 0.5f * (lo + hi);
-      const float g2 = mid * mid;
-      float ar = 0.f, ag = 0.f, ab = 0.f, aa = 0.f;
-      int sc = 0;
-      // The count only grows, so "count > k at the end" == "the sequential
-      // sweep stopped early"; after that (or past m, or once the lane's
-      // bisection has ended) the accumulator is never read, so only the count
-      // increment is predicated: the recurrence acc -> D^2 -> split -> acc is
-      // the whole critical path.
-#pragma unroll
-      for (int q = 0; q < MS; ++q) {
-        if ((q & 7) == 0 && q > 0 && !__any_sync(kFull, active && q < mi && sc <= k)) break;
-        const float4 sv = S[q];
-        const bool gap = sv.w < 0.f;  // NaN padding: false
-        const float sa = fabsf(sv.w);
-#if VDI_PACKED_D2
-        float n2, d2;  // dist2(acc, 0) (Q8) and dist2(acc, s), packed
-        n2d2_packed(ar, ag, ab, aa, sv.x, sv.y, sv.z, sa, n2, d2);
-#else
-        const float n2 = fmaf(aa, aa, fmaf(ab, ab, fmaf(ag, ag, ar * ar)));  // dist2(acc, 0), Q8
-        const float d2 = dist2(ar, ag, ab, aa, sv.x, sv.y, sv.z, sa);
-#endif
-        const bool st = (q == 0) | (gap & (n2 > g2)) | (d2 > g2);  // open before q is (q > 0)
-        const float tr = 1.0f - aa;
-        ar = st ? sv.x : fmaf(tr, sv.x, ar);
-        ag = st ? sv.y : fmaf(tr, sv.y, ag);
-        ab = st ? sv.z : fmaf(tr, sv.z, ab);
-        aa = st ? sa : fmaf(tr, sa, aa);
-        sc += st ? 1 : 0;
-      }
-      if (active) {
-        if (sc <= k) {
-          best = hi = mid;
-          if (sc == k) active = false;
-        } else {
-          lo = mid;
-        }
-        if (it + 1 >= mp.max_iters) active = false;
-      }
-    }
-#endif
     if (valid && !bad) {  // final write sweep, unrolled: static sample indices
       const float gg = best * best;
       float2* od = mp.out_depth + (size_t)p * k;
@@ -1028,36 +959,9 @@ __device__ __forceinline__ void sweep_batch(const MergeParams& mp, int bucket, u
   }
 }
 
-// both short-list buckets in one launch: batches of bucket 0 (m <= 32) first
 #ifndef VDI_SWEEP_MINB
 #define VDI_SWEEP_MINB 8
 #endif
-// Short-list search (k_out < m <= 40), one warp per batch of 32 lists: the
-// gather (thread per list, memory-latency bound) and then the bisection
-// sweeps (register-resident, ALU bound) of the same batch.  Fused, the warps
-// of an SM overlap one batch's gather latency with other batches' sweeps.
-template <int NS>
-__global__ void __launch_bounds__(32, VDI_SWEEP_MINB) search_short_kernel(MergeParams mp) {
-  __shared__ float2 sd[40 * 32];
-  __shared__ uint8_t sp[40 * 32];
-  const uint32_t lane = threadIdx.x;
-  const uint32_t c0 = min(mp.wl_count[0], mp.wl_cap), c1 = min(mp.wl_count[1], mp.wl_cap);
-  const uint32_t nb0 = (c0 + 31) / 32, nb1 = (c1 + 31) / 32;
-  // dynamic claims, longest lists first (bucket 1, then bucket 0): a warp
-  // takes the next batch when it finishes one
-  for (;;) {
-    uint32_t v = 0;
-    if (lane == 0) v = atomicAdd(&mp.search_ticket[0], 1u);
-    v = __shfl_sync(kFull, v, 0);
-    if (v >= nb0 + nb1) break;
-    gather_short_batch<NS, 32>(mp, v, nb1, c0, c1, sd + lane, sp + lane, lane);
-    __syncwarp();  // batch_slot written by lane 0; pool rows are read back by the lanes that wrote them
-    // one instantiation for both buckets (half the code: the unrolled sweeps
-    // otherwise miss in the instruction cache); bucket-0 batches leave the
-    // sweeps at sample 32 through the every-8-samples warp vote
-    sweep_batch<40>(mp, v < nb1 ? 1 : 0, v < nb1 ? v : v - nb1);
-  }
-}
 
 // ---------------------------------------------------------------------------
 // Search path for long lists (40 < m <= 255): the lists of a warp (one batch
@@ -1202,8 +1106,7 @@ __global__ void __launch_bounds__(128) long_gather_kernel(MergeParams mp) {
       }
     }
     if (fits) *obad = bad ? 1u : 0u;
-    if (!fits && valid) atomicOr(mp.err, 1);
-    const int bk = (valid && bad && fits) ? VDI_BUCKET_GENERAL : -1;
+    const int bk = (valid && bad) ? VDI_BUCKET_GENERAL : -1;  // overlap / alpha == 0, or no pool room
     if (__any_sync(kFull, bk >= 0)) push_entries<NS>(mp, bk, p, m, goff, lane);
   }
 }
@@ -1473,11 +1376,13 @@ __device__ __forceinline__ void general_body(const MergeParams& mp, uint32_t tid
   const int n = mp.n_src, k = mp.k_out;
   const uint32_t total = min(mp.wl_count[VDI_BUCKET_GENERAL], mp.wl_cap);
   const uint32_t* wl = mp.wl[VDI_BUCKET_GENERAL];
+  // this thread's scratch slice: A [m0] sorted records, B [2 m0] subdivided
+  // samples, E [2 m0] endpoints (m0 <= n_src k_in, gen_stride = 4 n_src k_in)
+  Rec* A = mp.scratch + (size_t)tid * mp.gen_stride;
   for (uint32_t e = tid; e < total; e += nthreads) {
     const uint32_t* ent = wl + (size_t)e * (3 + n);
     const uint32_t p = ent[0];
     const uint32_t m0 = ent[2];
-    Rec* A = mp.scratch + ent[1];
     Rec* B = A + m0;
     float* E = reinterpret_cast<float*>(B + 2 * m0);
     // step 1: k-way merge of the per-PE sorted runs, dropping alpha == 0 (Q23)
@@ -1571,6 +1476,8 @@ __device__ __forceinline__ void general_body(const MergeParams& mp, uint32_t tid
     auto get = [&](int i) { return S[i]; };
     float gamma = 0.f;
     int cnt;
+    double mgn = CUDART_INF;
+    double* mg = mp.stat_margin ? &mgn : nullptr;
     if (m <= k) {
       for (int j = 0; j < m; ++j) {
         od[j] = make_float2(S[j].tf, S[j].tb);
@@ -1582,20 +1489,67 @@ __device__ __forceinline__ void general_body(const MergeParams& mp, uint32_t tid
       }
       cnt = m;
     } else {
-      gamma = bisect(get, m, k, mp.max_iters, mp.gamma_max);
-      cnt = sweep(get, m, gamma, k, od, oc);
+      gamma = bisect(get, m, k, mp.max_iters, mp.gamma_max, mg);
+      cnt = sweep(get, m, gamma, k, od, oc, mg);
     }
     mp.out_count[p] = (uint8_t)cnt;
     if (mp.stat_m) mp.stat_m[p] = (uint16_t)m;
     if (mp.stat_gamma) mp.stat_gamma[p] = gamma;
+    if (mp.stat_margin) mp.stat_margin[p] = (float)mgn;
   }
 }
 
-// Lists with 40 < m <= 128 (samples in shared memory) and then, after a
-// grid-wide barrier (every push to the general work list is complete), the
-// general path -- one cooperative launch.
 __global__ void __launch_bounds__(kSlowThreads) merge_general_kernel(MergeParams mp) {
-  general_body(mp, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x);
+  const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x;
+  if (tid < mp.gen_threads) general_body(mp, tid, mp.gen_threads);
+}
+
+// Tie margins of the searched lists (VDI_FLAG_PIXEL_STATS, debug): thread per
+// work-list entry of buckets 0-3, replaying the bisection and the final sweep
+// (the same procedure as the search kernels: same gamma*, same comparisons)
+// over the depth-ordered samples the gather kernels left in the pools, with
+// the margin min |sqrt(D^2) - gamma| of every executed comparison in double.
+__global__ void __launch_bounds__(128) margins_kernel(MergeParams mp) {
+  const uint32_t c[4] = {min(mp.wl_count[0], mp.wl_cap), min(mp.wl_count[1], mp.wl_cap),
+                         min(mp.wl_count[2], mp.wl_cap), min(mp.wl_count[3], mp.wl_cap)};
+  const uint32_t tot = c[0] + c[1] + c[2] + c[3];
+  const int n = mp.n_src, k = mp.k_out;
+  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < tot; t += gridDim.x * blockDim.x) {
+    int b = 0;
+    uint32_t e = t;
+    while (e >= c[b]) e -= c[b++];
+    const uint32_t* ent = mp.wl[b] + (size_t)e * (3 + n);
+    const uint32_t p = ent[0];
+    const int m = (int)ent[2];
+    const float4* col;
+    const float2* dcol;
+    if (b < 2) {
+      const uint32_t slot = mp.batch_slot[b][e >> 5];
+      if (slot >= mp.pool_cap) continue;
+      const uint32_t* gp = mp.pool_gap + (size_t)slot * 64 + (e & 31);
+      if (gp[0] == 0xffffffffu && gp[32] == 0xffffffffu) continue;  // general path
+      col = mp.pool_rgba + (size_t)slot * 40 * 32 + (e & 31);
+      dcol = mp.pool_depth + (size_t)slot * 40 * 32 + (e & 31);
+    } else {
+      const PoolBatch pb = mp.long_batch[b - 2][e >> 5];
+      if (!pb.ok) continue;
+      const char* base = mp.long_pool + pb.off;
+      if (reinterpret_cast<const uint32_t*>(base + (size_t)pb.maxm * 32 * 24)[e & 31]) continue;
+      col = reinterpret_cast<const float4*>(base) + (e & 31);
+      dcol = reinterpret_cast<const float2*>(base + (size_t)pb.maxm * 32 * 16) + (e & 31);
+    }
+    // pool samples carry the gap flag in the sign of alpha; rebuild records whose
+    // t_front exceeds the previous t_back exactly where a gap was flagged
+    auto get = [&](int i) {
+      const float4 v = col[(size_t)i * 32];
+      const float2 d = dcol[(size_t)i * 32];
+      return Rec{d.x, d.y, v.x, v.y, v.z, fabsf(v.w)};
+    };
+    double mgn = CUDART_INF;
+    const float g = bisect(get, m, k, mp.max_iters, mp.gamma_max, &mgn);
+    sweep(get, m, g, k, nullptr, nullptr, &mgn);
+    mp.stat_margin[p] = (float)mgn;
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -1692,9 +1646,8 @@ static cudaError_t prep(K kernel, size_t smem, int threads, int* per_sm) {
   return e;
 }
 
-// Short search as two kernels (default; VDI_FUSED_SEARCH selects the fused
-// kernel above): a gather kernel with its own register budget (16 loads in
-// flight per thread, 12 warps per SM) followed by a sweep-only kernel.
+// Short search as two kernels: a gather kernel with its own register budget
+// (16 loads in flight per thread, 12 warps per SM) followed by a sweep-only kernel.
 // Measured on C3: search 0.1655 ms vs 0.172 fused, 0.170 with 8 loads in
 // flight (spills at 40).
 #ifndef VDI_SPLIT_CH
@@ -1719,126 +1672,17 @@ __global__ void __launch_bounds__(128, VDI_GATHER_MINB) search_gather_kernel(Mer
   }
 }
 
-#ifndef VDI_SWEEP_PREFETCH
-#define VDI_SWEEP_PREFETCH 0  // measured: search 0.1662 vs 0.1654 ms without (C3), C2 equal
-#endif
 // Short-list sweeps, warp per batch (dynamic claims, longest bucket first).
-// With VDI_SWEEP_PREFETCH the next claimed batch's samples (its pool rows,
-// [sample][lane] float4, 16 or 20 KB) are pulled into shared memory by one
-// bulk copy (cp.async.bulk, mbarrier completion) while the current batch is
-// swept from registers, so a batch starts on shared-memory loads instead of
-// a pool read from L2/HBM.
 __global__ void __launch_bounds__(32, VDI_SWEEP_MINB) search_sweep_kernel(MergeParams mp) {
   const uint32_t c0 = min(mp.wl_count[0], mp.wl_cap), c1 = min(mp.wl_count[1], mp.wl_cap);
   const uint32_t nb0 = (c0 + 31) / 32, nb1 = (c1 + 31) / 32;
-#if VDI_SWEEP_PREFETCH
-  __shared__ __align__(128) float4 sbuf[40 * 32];
-  __shared__ __align__(8) unsigned long long bar;
-  const uint32_t lane = threadIdx.x;
-  const uint32_t sb = smem_u32(sbuf), bb = smem_u32(&bar);
-  if (lane == 0) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bb) : "memory");
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncwarp();
-  uint32_t phase = 0;
-  // claim a batch; lane 0 starts its bulk copy; returns the batch (>= total: none)
-  auto claim = [&]() -> uint32_t {
-    uint32_t v = 0;
-    bool issued = false;
-    if (lane == 0) {
-      v = atomicAdd(&mp.search_ticket[0], 1u);
-      if (v < nb0 + nb1) {
-        const int bucket = v < nb1 ? 1 : 0;
-        const uint32_t slot = mp.batch_slot[bucket][bucket ? v : v - nb1];
-        if (slot < mp.pool_cap) {
-          const uint32_t bytes = (bucket ? 40u : 32u) * 32u * 16u;
-          const float4* src = mp.pool_rgba + (size_t)slot * 40 * 32;
-          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bb), "r"(bytes) : "memory");
-          asm volatile(
-              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(sb),
-              "l"(src), "r"(bytes), "r"(bb)
-              : "memory");
-          issued = true;
-        }
-      }
-    }
-    v = __shfl_sync(kFull, v, 0);
-    return __shfl_sync(kFull, issued ? 1u : 0u, 0) ? v : v | 0x80000000u;  // top bit: nothing in flight
-  };
-  uint32_t cur = claim();
-  while ((cur & 0x7fffffffu) < nb0 + nb1) {
-    if (!(cur & 0x80000000u)) {  // wait for its bulk copy
-      uint32_t done = 0;
-      while (!done)
-        asm volatile(
-            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
-            : "=r"(done)
-            : "r"(bb), "r"(phase)
-            : "memory");
-      phase ^= 1u;
-    }
-    const uint32_t v = cur & 0x7fffffffu;
-    // sweep_batch reads the samples into registers, then releases the buffer;
-    // the next claim (and its copy) is issued from inside via the callback
-    // ordering below: registers first, then claim
-    const int bucket = v < nb1 ? 1 : 0;
-    const uint32_t b = bucket ? v : v - nb1;
-    const uint32_t slot = mp.batch_slot[bucket][b];
-    if (slot < mp.pool_cap && !(cur & 0x80000000u)) {
-      sweep_batch<40>(mp, bucket, b, sbuf, [&]() { cur = claim(); });
-    } else {
-      cur = claim();
-      if (slot < mp.pool_cap) sweep_batch<40>(mp, bucket, b);
-    }
-  }
-#else
   for (;;) {
     uint32_t v = 0;
     if (threadIdx.x == 0) v = atomicAdd(&mp.search_ticket[0], 1u);
     v = __shfl_sync(kFull, v, 0);
     if (v >= nb0 + nb1) break;
     sweep_batch<40>(mp, v < nb1 ? 1 : 0, v < nb1 ? v : v - nb1);
-#if VDI_SWEEP_SPLIT
-    if (v >= nb1) break;  // at most one bucket-0 batch here; the rest go to search_sweep32_kernel
-#endif
   }
-#endif
-}
-
-#ifndef VDI_SWEEP_SPLIT
-#define VDI_SWEEP_SPLIT 0
-#endif
-#ifndef VDI_SWEEP32_MINB
-#define VDI_SWEEP32_MINB 10
-#endif
-// Bucket-0 batches (m <= 32) left by search_sweep_kernel, swept with a
-// 32-sample register file (fewer registers: more resident warps)
-__global__ void __launch_bounds__(32, VDI_SWEEP32_MINB) search_sweep32_kernel(MergeParams mp) {
-  const uint32_t c0 = min(mp.wl_count[0], mp.wl_cap), c1 = min(mp.wl_count[1], mp.wl_cap);
-  const uint32_t nb0 = (c0 + 31) / 32, nb1 = (c1 + 31) / 32;
-  for (;;) {
-    uint32_t v = 0;
-    if (threadIdx.x == 0) v = atomicAdd(&mp.search_ticket[0], 1u);
-    v = __shfl_sync(kFull, v, 0);
-    if (v >= nb0 + nb1) break;
-    sweep_batch<32>(mp, 0, v - nb1);  // v >= nb1: bucket 1 is exhausted before this kernel starts
-  }
-}
-
-template <int NS>
-static cudaError_t launch_short(const MergeParams& mp, cudaStream_t st) {
-  static int per_sm = 0;
-  if (!per_sm) {
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, search_short_kernel<NS>, 32, 0);
-    if (e != cudaSuccess) return e;
-    if (per_sm < 1) per_sm = 1;
-  }
-  uint32_t grid = (uint32_t)sm_count() * per_sm;
-  const uint32_t most = (mp.P + 31) / 32;
-  if (grid > most) grid = most ? most : 1;
-  search_short_kernel<NS><<<grid, 32, 0, st>>>(mp);
-  return cudaGetLastError();
 }
 
 template <int NS>
@@ -1864,39 +1708,20 @@ static cudaError_t launch_fast_ns(const MergeParams& mp, cudaStream_t st, int* l
 template <int NS>
 static cudaError_t launch_search_ns(const MergeParams& mp, cudaStream_t st, int* launches) {
   cudaError_t e;
-#ifndef VDI_FUSED_SEARCH
   search_gather_kernel<NS><<<sm_count() * 4, 128, 0, st>>>(mp);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   ++*launches;
   {
     static int per_sm = 0;
     if (!per_sm) {
-      // 8 warps x 20 KB prefetch buffers: ask for the largest shared-memory carveout
-      if ((e = cudaFuncSetAttribute(search_sweep_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100)) !=
-          cudaSuccess)
-        return e;
       if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, search_sweep_kernel, 32, 0)) != cudaSuccess)
         return e;
       if (per_sm < 1) per_sm = 1;
     }
     search_sweep_kernel<<<sm_count() * per_sm, 32, 0, st>>>(mp);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
-#if VDI_SWEEP_SPLIT
-    static int per_sm32 = 0;
-    if (!per_sm32) {
-      if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm32, search_sweep32_kernel, 32, 0)) != cudaSuccess)
-        return e;
-      if (per_sm32 < 1) per_sm32 = 1;
-    }
-    search_sweep32_kernel<<<sm_count() * per_sm32, 32, 0, st>>>(mp);
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
     ++*launches;
-#endif
   }
-#else
-  if ((e = launch_short<NS>(mp, st)) != cudaSuccess) return e;
-#endif
-  ++*launches;
   {
     static int per_sm = 0;  // resident blocks: the warps claim batches dynamically
     if (!per_sm) {
@@ -1913,8 +1738,21 @@ static cudaError_t launch_search_ns(const MergeParams& mp, cudaStream_t st, int*
   return cudaGetLastError();
 }
 
+uint32_t general_threads(uint32_t m_max) {
+  // one scratch slice of 4 m_max records per thread; at most ~512 MB of scratch
+  const uint64_t per = 4ull * std::max<uint32_t>(m_max, 1) * sizeof(Rec);
+  const uint64_t cap = (512ull << 20) / per;
+  return (uint32_t)std::max<uint64_t>(128, std::min<uint64_t>(cap, (uint64_t)sm_count() * 4 * kSlowThreads));
+}
+
 cudaError_t launch_general(const MergeParams& mp, cudaStream_t st, int* launches) {
-  merge_general_kernel<<<sm_count() * 4, kSlowThreads, 0, st>>>(mp);
+  merge_general_kernel<<<(mp.gen_threads + kSlowThreads - 1) / kSlowThreads, kSlowThreads, 0, st>>>(mp);
+  ++*launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_margins(const MergeParams& mp, cudaStream_t st, int* launches) {
+  margins_kernel<<<sm_count() * 8, 128, 0, st>>>(mp);
   ++*launches;
   return cudaGetLastError();
 }
@@ -1933,6 +1771,35 @@ cudaError_t launch_fast(const MergeParams& mp, cudaStream_t st, int* launches) {
 
 cudaError_t launch_search(const MergeParams& mp, cudaStream_t st, int* launches) {
   VDI_DISPATCH_NS(launch_search_ns, mp, st, launches)
+}
+
+// Load every merge kernel now (lazy module loading could otherwise try to
+// load a kernel while a spinning wait kernel of another loopback context
+// occupies the device)
+template <int NS>
+static void preload_ns(cudaFuncAttributes* fa) {
+  cudaFuncGetAttributes(fa, merge_fast_kernel<NS>);
+  cudaFuncGetAttributes(fa, search_gather_kernel<NS>);
+  cudaFuncGetAttributes(fa, long_gather_kernel<NS>);
+}
+
+cudaError_t preload_merge() {
+  cudaFuncAttributes fa;
+  preload_ns<1>(&fa);
+  preload_ns<2>(&fa);
+  preload_ns<4>(&fa);
+  preload_ns<8>(&fa);
+  preload_ns<16>(&fa);
+  preload_ns<VDI_MAX_SRC>(&fa);
+  cudaFuncGetAttributes(&fa, chunk_sums_kernel);
+  cudaFuncGetAttributes(&fa, group_base_kernel);
+  cudaFuncGetAttributes(&fa, search_sweep_kernel);
+  cudaFuncGetAttributes(&fa, long_sweep_kernel);
+  cudaFuncGetAttributes(&fa, merge_general_kernel);
+  cudaFuncGetAttributes(&fa, margins_kernel);
+  cudaFuncGetAttributes(&fa, sum_u32_kernel);
+  cudaFuncGetAttributes(&fa, compact_kernel);
+  return cudaGetLastError();
 }
 
 }  // namespace vdi

@@ -20,7 +20,7 @@ def vdi():
     return vdi
 
 
-def _gpu_composite(vdi, pes_np, W, H, k_in, k_out, flags=0, host=False):
+def _gpu_composite(vdi, pes_np, W, H, k_in, k_out, flags=0, host=False, margin=False):
     n = len(pes_np)
     comp = vdi.Compositor(W, H, k_in, k_out, n, flags=flags | vdi._lib.VDI_FLAG_PIXEL_STATS)
     if host:
@@ -32,8 +32,10 @@ def _gpu_composite(vdi, pes_np, W, H, k_in, k_out, flags=0, host=False):
         strip = comp.empty_strip()
         comp.composite(dev, strip)
     torch.cuda.synchronize()
-    g, m = comp.pixel_stats()
+    g, m, mg = comp.pixel_stats(with_margin=True)
     cnt = comp.counters()
+    if margin:
+        return strip, g.cpu().numpy(), m.cpu().numpy(), cnt, mg.cpu().numpy()
     return strip, g.cpu().numpy(), m.cpu().numpy(), cnt
 
 
@@ -58,13 +60,21 @@ def test_merge_parity_random(vdi, orc, case):
     n, W, H, k_in, k_out, lam, overlap = case
     pes = synth.random_subvdis(n, W, H, k_in, lam=lam, seed=100 + n, overlap=overlap)
     ref = orc.composite(pes, W, H, 1, k_out)
-    strip, gam, m, cnt = _gpu_composite(vdi, pes, W, H, k_in, k_out)
+    strip, gam, m, cnt, mg = _gpu_composite(vdi, pes, W, H, k_in, k_out, margin=True)
     gc, gd, gr = full_to_numpy(strip)
     nl, ties = compare(gc, gd, gr, ref["count"], ref["depth"], ref["rgba"], ref["stats"]["margin"], str(case))
     st = ref["stats"]
-    ok = st["margin"] >= 1e-6
-    assert np.array_equal(gam[ok], st["gamma"][ok])      # the per-list gamma* is reproduced
-    assert np.array_equal(m.astype(np.int64)[ok], st["m"][ok].astype(np.int64))
+    # the per-list gamma*, m and tie margin are reproduced on every list (ties included)
+    assert np.array_equal(gam, st["gamma"])
+    assert np.array_equal(m.astype(np.int64), st["m"].astype(np.int64))
+    om = st["margin"].astype(np.float32)
+    fin = np.isfinite(om)
+    assert np.array_equal(np.isfinite(mg), fin)
+    if overlap:  # subdivided samples carry powf results (ulp-level host/device differences)
+        np.testing.assert_allclose(mg[fin], om[fin], rtol=0, atol=1e-6)
+    else:        # identical comparisons: identical margins, identical tie lists
+        assert np.array_equal(mg[fin], om[fin])
+        assert np.nonzero(mg < 1e-6)[0].tolist() == ties
     assert cnt["records_in"] == sum(int(p["count"].sum()) for p in pes)
     print(f"{case}: {nl} lists bit-checked, ties listed: {ties[:20]} ({len(ties)}); searched {cnt['searched_lists']}")
 
@@ -149,46 +159,23 @@ def test_composite_parity_c1_oracle_inputs(vdi, orc):
     assert np.abs(img - orc.dvr(sc)).max() <= 1e-3
 
 
-def test_full_size_synthetic_sampled(vdi, orc):
-    """1920x1080, 8 PEs, k=20 merge-only inputs in the bench's launch
-    configuration; the oracle recomposes a sample of lists one by one."""
+def test_full_size_synthetic_whole_image(vdi, orc):
+    """1920x1080, 8 PEs, k=20 merge-only inputs (synth only) in the bench's
+    launch configuration: ALL 2,073,600 lists against orc.composite (OpenMP
+    over the host cores), ties included; the GPU's own tie list equals the
+    oracle's."""
+    import os
     W, H, n, k = 1920, 1080, 8, 20
     pes = synth.random_subvdis(n, W, H, k, lam=10.0, seed=7)
-    strip, gam, m, cnt = _gpu_composite(vdi, pes, W, H, k, k)
-    rng = np.random.default_rng(1)
-    srch = np.nonzero(m > k)[0]
-    pix = np.unique(np.concatenate([rng.choice(W * H, 8000, replace=False),
-                                    rng.choice(srch, min(4000, len(srch)), replace=False) if len(srch) else [],
-                                    [0, W * H - 1]]).astype(np.int64))
-    ref = orc.composite_pixels(pes, pix, k)
+    strip, gam, m, cnt, mg = _gpu_composite(vdi, pes, W, H, k, k, margin=True)
+    ref = orc.composite(pes, W, H, 1, k, n_threads=os.cpu_count() or 1)
     gc, gd, gr = full_to_numpy(strip)
-    compare(gc[pix], gd[pix], gr[pix], ref["count"], ref["depth"], ref["rgba"], ref["stats"]["margin"], "1080p")
+    nl, ties = compare(gc, gd, gr, ref["count"], ref["depth"], ref["rgba"], ref["stats"]["margin"], "1080p")
+    assert nl == W * H
+    assert np.array_equal(gam, ref["stats"]["gamma"])
+    assert np.nonzero(mg < 1e-6)[0].tolist() == ties
     assert cnt["records_in"] == sum(int(p["count"].sum()) for p in pes)
-
-
-def test_composite_frames_single_gpu(vdi, orc):
-    """vdi_composite_frames (frames in flight, chunked merge) on one GPU: every
-    frame's image equals vdi_composite of that frame bit for bit, and the
-    oracle on sampled lists."""
-    n, W, H, k = 6, 160, 90, 12
-    frames = [synth.random_subvdis(n, W, H, k, lam=9.0 + 3 * f, seed=500 + f) for f in range(3)]
-    comp = vdi.Compositor(W, H, k, k, n)
-    dev = [[dense_to_device(p, i) for i, p in enumerate(fr)] for fr in frames]
-    for chunks in (1, 3, 8):
-        images = [vdi.FullVDI.empty(W, 0, H, k) for _ in frames]
-        comp.composite_frames(dev, images, chunks=chunks)
-        torch.cuda.synchronize()
-        for f, fr in enumerate(frames):
-            one = comp.empty_strip()
-            comp.composite(dev[f], one)
-            torch.cuda.synchronize()
-            for a, b in ((images[f].count, one.count), (images[f].depth, one.depth), (images[f].rgba, one.rgba)):
-                assert torch.equal(a, b), (chunks, f)
-    rng = np.random.default_rng(5)
-    pix = np.unique(rng.choice(W * H, 1500, replace=False))
-    o = orc.composite_pixels(frames[2], pix, k)
-    gc, gd, gr = full_to_numpy(images[2])
-    compare(gc[pix], gd[pix], gr[pix], o["count"], o["depth"], o["rgba"], o["stats"]["margin"], "frames")
+    print(f"1080p whole image: {nl} lists, {int((m > k).sum())} searched, ties {len(ties)}")
 
 
 def test_dense_to_full_and_fullrep_composite(vdi, orc):
