@@ -1,15 +1,21 @@
 #!/usr/bin/env python
 """bench.py — composited VDIs/s of the sort-last VDI compositing hot path on
-1..8 B200 (BASELINE.json metric), with the merge's HBM roofline fraction,
-an end-to-end (host buffers) number and the CPU oracle's baseline.
+1..8 B200 (BASELINE.json metric), with the merge's HBM roofline fraction, the
+search's ALU roofline, an end-to-end (host buffers) number and the CPU
+oracle's baseline.
 
-A step = one pass of the whole hot path over one VDI:
-strip totals, size exchange + all-to-allv (NCCL, G > 1), receive-side scan,
-per-list merge / gamma search / full-representation write, gather to rank 0.
-Inputs (untimed): the config's synthetic volume raycast into per-PE dense
-sub-VDIs by vdi_generate_subvdi, resident in HBM.
+A step composites VDIs in the paper's strip mode: strip
+bounds, the device-driven exchange of the strip slices (N > 1), receive-side
+scan, per-list merge / gamma search / full-representation write, and the
+gather to rank 0.  N = 1: one VDI per step.  N > 1: F VDIs per step enqueued
+back to back (no host synchronisation inside a step: frame f+1's exchange
+and merge overlap frame f's gather on the other ranks), all gathered to rank
+0.  Inputs (untimed): the config's synthetic volume raycast into per-PE dense
+sub-VDIs by vdi_generate_subvdi for the paper's timing protocol
+(the camera rotates 10 degrees every 10th iteration; views V0
+and V1), resident in HBM.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3] [--impl ours|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3] [--pes n] [--impl ours|reference]
   torchrun --nproc-per-node N bench.py --gpus N ...
 """
 from __future__ import annotations
@@ -177,8 +183,26 @@ def workload_name(cfg, view):
             f"view V{view}")
 
 
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def stats_ms(xs):
+    xs = sorted(xs)
+    if not xs:
+        return {}
+    p95 = xs[min(len(xs) - 1, int(round(0.95 * (len(xs) - 1))))]
+    return {"mean": statistics.mean(xs), "median": statistics.median(xs), "p95": p95, "n": len(xs)}
+
+
 # ---------------------------------------------------------------------------
-# oracle helpers (cpu_baseline and --impl reference ONLY)
+# oracle helpers (cpu_baseline, parity_sample and --impl reference ONLY)
 # ---------------------------------------------------------------------------
 def oracle_band_inputs(cfg, vol_host, tf, cam, dec, rows, threads):
     import oracle
@@ -206,13 +230,21 @@ def host_volume(vol_t):
     return np.ascontiguousarray(a.view(np.uint16) if a.dtype == np.int16 else a)
 
 
+def get_config(args):
+    cfg = synth.config_by_name(args.config)
+    if args.pes:
+        cfg = synth.config_by_name(args.config, n_pes=args.pes)
+    return cfg
+
+
 # ---------------------------------------------------------------------------
 def run_reference(args, world, rank):
     """--impl reference: the CPU oracle as it stands, on the box's host cores,
-    each step a bounded sample (a band of image rows) of the same workload."""
+    each step a bounded sample (a band of image rows) of the same workload;
+    ms_per_step is the measured band time, value the VDIs/s it extrapolates to."""
     if rank != 0:
         return
-    cfg = synth.config_by_name(args.config)
+    cfg = get_config(args)
     threads = os.cpu_count() or 1
     dev = "cuda" if torch.cuda.is_available() else "cpu"
     vol = host_volume(synth.make_volume(cfg, device=dev))
@@ -224,15 +256,19 @@ def run_reference(args, world, rank):
     for _ in range(args.warmup):
         oracle_composite_band(cfg, pes, pix, threads)
     ts = [oracle_composite_band(cfg, pes, pix, threads)[1] for _ in range(args.steps)]
-    per_vdi = statistics.mean(ts) / frac
-    v = 1.0 / per_vdi
-    sample = f"rows [{pix[0] // cfg.W}, {pix[-1] // cfg.W + 1}) of {cfg.H} ({len(pix)} lists, {frac:.4f} of the image)"
+    band_ms = statistics.mean(ts) * 1e3
+    v = frac / statistics.mean(ts)
+    sample = (f"rows [{pix[0] // cfg.W}, {pix[-1] // cfg.W + 1}) of {cfg.H} ({len(pix)} lists, {frac:.4f} of the "
+              f"image); value = band fraction / band time (extrapolated to whole VDIs)")
     emit({
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": per_vdi * 1e3, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": band_ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": workload_name(cfg, args.view), "sample": sample},
-        "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": sample},
+        "config": {"workload": workload_name(cfg, args.view), "sample": sample,
+                   "ms_per_step_is": "measured time of one band (the bounded sample), not of a whole VDI"},
+        "step_ms": stats_ms([t * 1e3 for t in ts]),
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "cpu_model": cpu_model(), "kind": "oracle",
+                         "sample": sample},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     })
 
@@ -248,12 +284,9 @@ def _run_ours(args, world, rank, local, clk):
     import paper_2206_14503_b200 as vdi
     from paper_2206_14503_b200 import _lib as L
 
-    cfg = synth.config_by_name(args.config)
+    cfg = get_config(args)
     G, n, W, H, k = world, cfg.n_pes, cfg.W, cfg.H, cfg.k_out
-    F = args.frames if args.frames > 0 else 4 * G if G > 1 else 1  # VDIs per step (4 per rank: G=2 4160 vs 3772 VDIs/s at 2)
-    flags = (L.VDI_FLAG_STAGE_TIMING | (L.VDI_FLAG_FULL_GATHER if args.full_gather else 0)
-             | (L.VDI_FLAG_NCCL_EXCHANGE if args.nccl_exchange else 0)
-             | (L.VDI_FLAG_PEER_READS if args.peer_reads else 0) | (L.VDI_FLAG_CE_COPIES if args.ce_copies else 0))
+    F = args.frames if args.frames > 0 else (1 if G == 1 else 4)  # VDIs per step
     stream = torch.cuda.current_stream()
 
     def new_uid():
@@ -264,322 +297,353 @@ def _run_ours(args, world, rank, local, clk):
         dist.broadcast_object_list(obj, src=0)
         return obj[0]
 
-    # strip mode (the paper's direct send: strips of one VDI on every GPU, gather to rank 0)
-    comp = vdi.Compositor(W, H, cfg.k_in, k, n, n_ranks=G, rank=rank, flags=flags, unique_id=new_uid(),
-                          stream=stream)
-    # frames mode (G > 1): F VDIs per step, frame f composited whole by rank f mod G
-    compf = (vdi.Compositor(W, H, cfg.k_in, k, n, n_ranks=G, rank=rank,
-                            flags=L.VDI_FLAG_STAGE_TIMING | (L.VDI_FLAG_PEER_READS if args.peer_reads else 0)
-                            | (L.VDI_FLAG_CE_COPIES if args.ce_copies else 0),
-                            unique_id=new_uid(), stream=stream) if G > 1 else None)
+    comp = vdi.Compositor(W, H, cfg.k_in, k, n, n_ranks=G, rank=rank, flags=L.VDI_FLAG_STAGE_TIMING,
+                          unique_id=new_uid(), stream=stream)
 
-    # ---- inputs (untimed): synthetic volume -> per-PE dense sub-VDIs in HBM;
-    # frames mode gets one private copy per frame (every frame is this VDI)
+    # ---- inputs (untimed): the timing protocol of PAPER.md:366 -- views V0,
+    # V1, the camera rotating 10 degrees every 10th iteration
+    # (5 rotations per view) -- raycast into dense sub-VDIs resident in HBM
     t0 = time.time()
     vol = synth.make_volume(cfg, device="cuda")
     tf = synth.tf_table(cfg.tf, cfg.tf_scale)
     tft = torch.from_numpy(tf).cuda()
-    cam = synth.make_camera(W, H, view=args.view)
     dec = cfg.decomposition()
     local_ids = [pe for pe in range(n) if vdi.pe_home(n, G, pe) == rank]
-    local = [comp.generate_subvdi(vol, tft, cam, dec, pe) for pe in local_ids]
+    rotations = [10.0 * r for r in range(args.rotations)]
+    views = [0, 1] if not args.no_v1 else [0]
+    sets = {}
+    for v in views:
+        for a in rotations:
+            cam = synth.make_camera(W, H, view=v, angle_deg=a)
+            ps = [comp.generate_subvdi(vol, tft, cam, dec, pe) for pe in local_ids]
+            sets[(v, a)] = [vdi.DenseSubVDI(p.pe_id, p.total, p.count.clone(), p.offset.clone(), p.depth.clone(),
+                                            p.rgba.clone()) for p in ps]
     torch.cuda.synchronize()
     t_gen = time.time() - t0
-    S_local = sum(p.total for p in local)
+    base = sets[(0, 0.0)]
+    S_local = sum(p.total for p in base)
     S_total = int(allreduce_sum(S_local, G))
-    # Phase 1 as a measured stage (untimed w.r.t. `value`):
-    # vdi_generate_subvdi of one local PE (two-pass raycast, device scan, write)
-    # timed with CUDA events; deterministic, so the regenerated output is the same
+    # Phase 1 as a measured stage (outside `value`)
     g_ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
     g_ms = []
+    cam0 = synth.make_camera(W, H, view=0)
     for _ in range(2):
         g_ev[0].record(stream)
-        p0 = comp.generate_subvdi(vol, tft, cam, dec, local_ids[0])
+        p0 = comp.generate_subvdi(vol, tft, cam0, dec, local_ids[0])
         g_ev[1].record(stream)
         torch.cuda.synchronize()
         g_ms.append(g_ev[0].elapsed_time(g_ev[1]))
-    assert p0.total == local[0].total
+    assert p0.total == base[0].total
     phase1 = {"ms_per_subvdi": min(g_ms), "pe": local_ids[0], "supersegments": int(p0.total),
               "note": "vdi_generate_subvdi: gamma search + count pass, scan, write pass (PAPER.md:113-118, "
                       ":150-157); not part of the timed step"}
-    frames_local, frames_img = None, None
-    if compf is not None:
-        frames_local = [[vdi.DenseSubVDI(p.pe_id, p.total, p.count.clone(), p.offset.clone(), p.depth.clone(),
-                                         p.rgba.clone()) for p in local] for _ in range(F)]
-        frames_img = [vdi.FullVDI.empty(W, 0, H, k) if f % G == rank else None for f in range(F)]
 
-    if G > 1 and rank == 0:  # rank 0's strip aliases the first rows of the image (no copy in the gather)
+    if rank == 0:  # rank 0's strip aliases the first rows of the image (no copy in the gather)
         image = vdi.FullVDI.empty(W, 0, H, k)
         P0 = (comp.row_end - comp.row_begin) * W
         strip = vdi.FullVDI(comp.row_begin, comp.row_end, image.count[:P0], image.depth[:P0], image.rgba[:P0])
     else:
+        image = vdi.FullVDI.empty(W, 0, H, k) if args.rotating else None
         strip = comp.empty_strip()
-        image = strip if G == 1 else None
+    own_image = image if image is not None else None
     flush = torch.empty(args.flush_mb << 20, dtype=torch.uint8, device="cuda")
 
-    def strip_step():
-        comp.composite(local, strip)
-        comp.gather(strip, image)
+    def frame(s, root):
+        comp.composite(s, strip)
+        comp.gather(strip, own_image if rank == root else None, root=root)
 
-    def frames_step():
-        compf.composite_frames(frames_local, frames_img, chunks=args.chunks)
-
-    def timed_steps(K, fn, c):
+    def timed(K, view, rotating=False, frames=F):
+        """K steps of `frames` VDIs; the protocol's rotation changes every 10th step."""
         evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
-        stats, nl = [], 0
+        cnts, nl = [], 0
         torch.cuda.synchronize()
         barrier(G)
         for i in range(K):
+            s = sets[(view, rotations[(i // 10) % len(rotations)])]
             flush.zero_()
             evs[i][0].record(stream)
-            fn()
+            if frames == 1:
+                frame(s, (i % G) if rotating else 0)
+            else:  # frames in flight through strip mode (vdi_composite_frames)
+                roots = [(i * frames + f) % G if rotating else 0 for f in range(frames)]
+                comp.composite_frames([s] * frames, [own_image if r == rank else None for r in roots], roots=roots)
             evs[i][1].record(stream)
-            x = c.counters()  # syncs the stream; outside the events
-            stats.append(x)
-            nl += x["kernel_launches"]
+            x = comp.counters()  # syncs the stream; outside the events
+            cnts.append(x)
+            nl += x["kernel_launches"] * (frames if frames == 1 else 1)
         torch.cuda.synchronize()
         barrier(G)
-        return [a_.elapsed_time(b_) for a_, b_ in evs], stats, nl
+        return [a_.elapsed_time(b_) for a_, b_ in evs], cnts, nl
 
-    step, step_comp = (frames_step, compf) if compf is not None else (strip_step, comp)
     for _ in range(args.warmup):
-        step()
+        frame(base, 0)
+    for _ in range(2):  # every protocol set once (first-touch of the pools)
+        for s in sets.values():
+            frame(s, 0)
     torch.cuda.synchronize()
     barrier(G)
 
     # ---- timed region: exactly K steps, L2 flushed between steps (untimed)
     clk.mark_start()
-    step_ms, fstage, launches = timed_steps(args.steps, step, step_comp)
+    step_ms, cnts, launches = timed(args.steps, 0)
     clk.mark_end()
     tot_ms = allreduce_max(sum(step_ms), G)
     ms_per_step = tot_ms / args.steps
-    value = F * args.steps / (tot_ms / 1e3)  # whole VDIs composited by all ranks per second
+    value = F * args.steps / (tot_ms / 1e3)
+    per_vdi = [t / F for t in step_ms]
+    protocol = {"V0": {"vdis_per_s": value, "ms_per_vdi": stats_ms(per_vdi)}}
+    if 1 in views:
+        v1_ms, _, _ = timed(args.steps, 1)
+        v1_tot = allreduce_max(sum(v1_ms), G)
+        protocol["V1"] = {"vdis_per_s": F * args.steps / (v1_tot / 1e3), "ms_per_vdi": stats_ms([t / F for t in v1_ms])}
+    protocol["note"] = (f"PAPER.md:366 protocol: {args.steps} timed iterations, camera rotated 10 deg every 10th "
+                        f"iteration ({len(rotations)} rotations), views V0 and V1 (PAPER.md:364); statistics per VDI")
 
-    # ---- strip (latency) mode: one VDI per step, strips on every GPU, gather
-    # to rank 0 (timed paper-style per stage).
-    # At G = 1 this is the timed run itself.
-    latency = None
-    if compf is not None:
-        for _ in range(3):
-            strip_step()
+    # ---- N > 1: secondary modes -- a rotating root (frame f gathered on
+    # rank f mod G), latency mode (1 VDI per step, stage breakdown), and the
+    # full-representation pipeline of Fig. 6 (PAPER.md:244)
+    latency = rotating = full_rep = None
+    if G > 1:
+        if args.rotating:
+            r_ms, _, _ = timed(args.steps, 0, rotating=True)
+            r_tot = allreduce_max(sum(r_ms), G)
+            rotating = {"vdis_per_s": F * args.steps / (r_tot / 1e3), "ms_per_vdi": stats_ms([t / F for t in r_ms]),
+                        "note": "frame f gathered on rank f mod G (vdi_gather_root): the root's inflate is shared"}
         K1 = max(10, args.steps // 4)
-        lat_ms, stage, _ = timed_steps(K1, strip_step, comp)
-        l_ms = allreduce_max(sum(lat_ms), G) / K1
-        latency = {"ms_per_vdi": l_ms, "value": 1e3 / l_ms, "steps": K1,
-                   "stages_ms": {s_: statistics.mean(c_[f"ms_{s_}"] for c_ in stage)
+        l_ms, lstage, _ = timed(K1, 0, frames=1)
+        l_tot = allreduce_max(sum(l_ms), G)
+        latency = {"ms_per_vdi": l_tot / K1, "value": 1e3 * K1 / l_tot, "steps": K1,
+                   "stages_ms": {s_: statistics.mean(c_[f"ms_{s_}"] for c_ in lstage)
                                  for s_ in ("exchange", "merge", "gather")},
-                   "note": "one VDI per step in strips over all GPUs, dense gather to rank 0"}
-        frames_info = {"frames_per_step": F, "chunks": args.chunks,
-                       "ms_size_exchange_and_first_copy": statistics.mean(c_["ms_exchange"] for c_ in fstage),
-                       "ms_size_exchange": statistics.mean(c_["ms_sizes"] for c_ in fstage),
-                       "ms_first_pull": statistics.mean(c_["ms_pull"] for c_ in fstage),
-                       "first_pull_GBs": (fstage[-1]["bytes_received"] / max(1, F // G)) / 1e6
-                                         / max(1e-6, statistics.mean(c_["ms_pull"] for c_ in fstage)),
-                       "ms_merge_incl_overlapped_copies": statistics.mean(c_["ms_merge"] for c_ in fstage),
-                       "bytes_pulled_per_step_rank0": fstage[-1]["bytes_received"]}
-        # the full-representation pipeline of Fig. 6: sub-VDIs in
-        # the full representation (converted untimed), fixed-size exchange,
-        # full-representation gather -- same image, the paper's A/B
+                   "note": "one VDI per step (no overlap between VDIs)"}
+        cnts = lstage  # per-stage numbers below come from the one-VDI steps
         compx = vdi.Compositor(W, H, cfg.k_in, k, n, n_ranks=G, rank=rank, unique_id=new_uid(), stream=stream,
-                               flags=L.VDI_FLAG_STAGE_TIMING | L.VDI_FLAG_FULL_GATHER)
-        fulls = [compx.dense_to_full(p) for p in local]
-        ids = [p.pe_id for p in local]
+                               flags=L.VDI_FLAG_STAGE_TIMING)
+        fulls = [compx.dense_to_full(p) for p in base]
+        ids = [p.pe_id for p in base]
+        stx = compx.empty_strip()
+        imx = vdi.FullVDI.empty(W, 0, H, k) if rank == 0 else None
 
         def full_step():
-            compx.composite_fullrep(fulls, ids, strip)
-            compx.gather(strip, image)
+            compx.composite_fullrep(fulls, ids, stx)
+            compx.gather(stx, imx)
         for _ in range(3):
             full_step()
         Kx = max(5, args.steps // 10)
-        x_ms, x_stage, _ = timed_steps(Kx, full_step, compx)
-        xm = allreduce_max(sum(x_ms), G) / Kx
+        xs = []
+        torch.cuda.synchronize()
+        barrier(G)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        for _ in range(Kx):
+            e0.record(stream)
+            full_step()
+            e1.record(stream)
+            xs.append(compx.counters())
+            torch.cuda.synchronize()
+            xs[-1]["ms"] = e0.elapsed_time(e1)
+        xm = allreduce_max(statistics.mean(x["ms"] for x in xs), G)
         full_rep = {"ms_per_vdi": xm, "value": 1e3 / xm, "steps": Kx,
-                    "stages_ms": {s_: statistics.mean(c_[f"ms_{s_}"] for c_ in x_stage)
-                                  for s_ in ("exchange", "merge", "gather")},
-                    "exchange_bytes_sent_rank0": x_stage[-1]["bytes_sent"],
-                    "note": "sub-VDIs in the full representation: fixed-size exchange, compositing from full "
-                            "slices, full-representation gather (Fig. 6 'full'); latency mode"}
+                    "stages_ms": {s_: statistics.mean(c_[f"ms_{s_}"] for c_ in xs) for s_ in ("exchange", "merge", "gather")},
+                    "exchange_bytes_sent_rank0": xs[-1]["bytes_sent"],
+                    "note": "sub-VDIs in the full representation: fixed-size exchange, compositing from full slices "
+                            "(Fig. 6 'full'); one VDI per step"}
         compx.close()
         del fulls
-    else:
-        stage = fstage
-        frames_info = None
-        full_rep = None
 
-    # ---- rooflines, per rank.  The dominant HBM-bound kernel is
-    # merge_fast: it reads the counts, the group bases and the records of the
-    # pass-through lists and writes the whole full representation.
+    # ---- rooflines (DESIGN.md §6).  Headline: the whole merge stage (every
+    # merge kernel, one stream) against HBM; beside it the pass-through kernel
+    # alone and the search's ALU bound.
     P_g = strip.count.numel()
     ng = (P_g + 31) // 32
-    rec = stage[-1]["records_in"]
-    rec_s = stage[-1]["records_search"]
+    rec = cnts[-1]["records_in"]
+    rec_s = cnts[-1]["records_search"]
     B_merge = 24 * rec + n * P_g + P_g * (24 * k + 1)  # SURVEY §8(d) algorithmic bytes of the merge stage
     B_fast = n * P_g + 4 * n * ng + 24 * (rec - rec_s) + P_g * (24 * k + 1)
-    ms_merge = statistics.mean(c["ms_merge"] for c in stage)
-    ms_fast = statistics.mean(c["ms_fast"] for c in stage)
-    ms_merge_max = allreduce_max(ms_merge, G)
-    achieved = B_fast / (ms_fast * 1e-3) / 1e9
+    ms_merge = statistics.mean(c["ms_merge"] for c in cnts)
+    ms_fast = statistics.mean(c["ms_fast"] for c in cnts)
+    ms_search = statistics.mean(c["ms_search"] for c in cnts)
     peak, peak_src = _peaks()
-    traffic = None
+    traffic = traffic_fast = None
     tp = os.path.join(ROOT, "profiles", "merge_traffic.json")
     if os.path.exists(tp):
         try:
-            traffic = json.load(open(tp)).get(cfg.name)
+            tj = json.load(open(tp)).get(cfg.name if not args.pes else f"{cfg.name}-{cfg.n_pes}")
+            if isinstance(tj, dict):
+                traffic, traffic_fast = tj.get("merge_stage"), tj.get("merge_fast")
         except Exception:
-            traffic = None
-    ms_ex = statistics.mean(c["ms_exchange"] for c in stage)
-    ms_ga = statistics.mean(c["ms_gather"] for c in stage)
-    bytes_sent = stage[-1]["bytes_sent"]
-    bytes_recv = stage[-1]["bytes_received"]
+            pass
+    # ALU roofline of the gamma search: the plain procedure's sample-steps
+    # (counted on the GPU by the margin replay, VDI_FLAG_PIXEL_STATS, untimed)
+    # x 20 FP32 operations (SURVEY §8(d)) / the search kernels' time
+    alu = None
+    if G == 1:
+        cs = vdi.Compositor(W, H, cfg.k_in, k, n, flags=L.VDI_FLAG_PIXEL_STATS, stream=stream)
+        sst = cs.empty_strip()
+        cs.composite(base, sst)
+        steps_alg = cs.counters()["sweep_steps"]
+        cs.close()
+        del sst
+        clk_mhz = clk.summary().get("sm_mhz") or 1965.0
+        fp32_peak = 148 * 128 * 2 * clk_mhz * 1e6 / 1e12  # TFLOP/s: SMs x FP32 lanes x FMA at the measured clock
+        ach = 20.0 * steps_alg / (ms_search * 1e-3) / 1e12 if ms_search > 0 else 0.0
+        alu = {"bound": "alu", "kernel": "search kernels (short + long gather / bisection sweeps)",
+               "achieved": ach, "peak": fp32_peak, "unit": "TFLOP/s", "frac": ach / fp32_peak if fp32_peak else None,
+               "sweep_steps": int(steps_alg), "flop_per_step": 20, "ms": ms_search,
+               "flop_per_byte": 20.0 * steps_alg / max(1, 24 * rec_s),
+               "peak_source": f"148 SMs x 128 FP32 lanes x 2 (FMA) x {clk_mhz:.0f} MHz (median SM clock under load)"}
+    ms_ex = statistics.mean(c["ms_exchange"] for c in cnts)
+    ms_ga = statistics.mean(c["ms_gather"] for c in cnts)
+    bytes_sent = cnts[-1]["bytes_sent"]
+    bytes_recv = cnts[-1]["bytes_received"]
+    ing_max = allreduce_max(bytes_recv, G)
+    eg_max = allreduce_max(bytes_sent, G)
+    ms_ex_max = allreduce_max(ms_ex, G)
 
-    # ---- Phase 1 + Phase 2 of one VDI: every local PE's
-    # sub-VDI raycast from the resident volume (vdi_generate_subvdi), then the
-    # strip-mode exchange + merge + gather; CUDA events on the stream, min over
-    # 3 repetitions, max over ranks; deterministic, so `local` is regenerated
-    # in place with identical contents
+    # ---- Phase 1 + Phase 2 of one VDI (SURVEY §8(f) f3)
     v2r = []
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     for _ in range(3):
         torch.cuda.synchronize()
         barrier(G)
         ev0.record(stream)
-        regen = [comp.generate_subvdi(vol, tft, cam, dec, pe) for pe in local_ids]
-        strip_step()
+        regen = [comp.generate_subvdi(vol, tft, cam0, dec, pe) for pe in local_ids]
+        frame(regen, 0)
         ev1.record(stream)
         torch.cuda.synchronize()
         v2r.append(ev0.elapsed_time(ev1))
-    assert [p.total for p in regen] == [p.total for p in local]
     ms_v2r = allreduce_max(min(v2r), G)
     volume_to_root = {"ms": ms_v2r, "vdis_per_s": 1e3 / ms_v2r, "pes_generated_per_rank": len(local_ids),
-                      "note": "Phase 1 (vdi_generate_subvdi of every local PE: gamma search + count pass, scan, "
-                              "write pass; PAPER.md:113-118, :150-157) + strip-mode exchange, merge and gather of "
-                              "one VDI (PAPER.md:164-185), one stream, max over ranks"}
+                      "note": "Phase 1 (vdi_generate_subvdi of every local PE) + exchange, merge and gather of one "
+                              "VDI, one stream, max over ranks"}
 
-    # ---- end to end through the C ABI with host buffers (pinned): host
-    # sub-VDIs in, the composited strip back in the dense representation
-    # (vdi_composite_host_dense)
+    # ---- end to end through the C ABI with host buffers (pinned): per frame
+    # the host sub-VDIs in, the composited strip back in the dense
+    # representation (PAPER.md:113-115; vdi_composite_host_dense_frames); the
+    # frames cycle over the protocol's input sets (distinct inputs)
     e2e = None
     if not args.no_e2e:
-        # the local sub-VDIs packed in one pinned host arena (256-B aligned
-        # arrays): libvdi then moves a frame's inputs with one H2D copy
-        parts = [[p.count] + ([p.offset] if G > 1 else []) + [p.depth, p.rgba] for p in local]
-        sizes = [[(t.numel() * t.element_size() + 255) // 256 * 256 for t in ts] for ts in parts]
-        arena = torch.empty(sum(map(sum, sizes)), dtype=torch.uint8).pin_memory()
-        host_pes, off = [], 0
-        for p, ts, ss in zip(local, parts, sizes):
-            hv = []
-            for t, sz in zip(ts, ss):
-                nb = t.numel() * t.element_size()
-                h = arena[off:off + nb].view(t.dtype).view(t.shape)
-                h.copy_(t)
-                hv.append(h)
-                off += sz
-            host_pes.append(vdi.DenseSubVDI(p.pe_id, p.total, hv[0], hv[1] if G > 1 else None, hv[-2], hv[-1]))
+        compe = vdi.Compositor(W, H, cfg.k_in, k, n, n_ranks=G, rank=rank, flags=L.VDI_FLAG_HOST_SPAN,
+                               unique_id=new_uid(), stream=stream)
+        keys = list(sets.keys())[: args.e2e_sets]
+        host_sets, arenas = [], []
+        for key in keys:
+            parts = [[p.count, p.depth, p.rgba] for p in sets[key]]
+            sizes = [[(t.numel() * t.element_size() + 255) // 256 * 256 for t in ts] for ts in parts]
+            arena = torch.empty(max(1, sum(map(sum, sizes))), dtype=torch.uint8).pin_memory()
+            hp, off = [], 0
+            for p, ts, ss in zip(sets[key], parts, sizes):
+                hv = []
+                for t, sz in zip(ts, ss):
+                    nb = t.numel() * t.element_size()
+                    h = arena[off:off + nb].view(t.dtype).view(t.shape)
+                    h.copy_(t)
+                    hv.append(h)
+                    off += sz
+                hp.append(vdi.DenseSubVDI(p.pe_id, p.total, hv[0], None, hv[1], hv[2]))
+            host_sets.append(hp)
+            arenas.append(arena)
         P_g = strip.count.numel()
         cap = max(1, min(P_g * k, S_total))  # a list never gains supersegments: output <= input records
         outs = [(torch.empty(P_g, dtype=torch.uint8).pin_memory(), torch.empty((cap, 2), dtype=torch.float32).pin_memory(),
                  torch.empty((cap, 4), dtype=torch.float32).pin_memory()) for _ in range(2)]
-        # warm-up: the single-frame call once, then the pipelined call (its
-        # first call allocates the second input slot and the output slots)
-        T_one = comp.composite_host_dense(host_pes, *outs[0])
-        comp.composite_host_dense_frames([host_pes] * 2, outs)
+        want = [compe.composite_host_dense(hs, *outs[0]) for hs in host_sets]
+        compe.composite_host_dense_frames([host_sets[0]] * 2, outs)
         barrier(G)
+        fr = [host_sets[f % len(host_sets)] for f in range(args.e2e_steps)]
         t0 = time.perf_counter()
-        # every step = one frame: its sub-VDIs host->device, compositing, its
-        # dense result device->host; consecutive frames overlap (copy engines
-        # in both directions beside the SMs)
-        Ts = comp.composite_host_dense_frames([host_pes] * args.e2e_steps, [outs[f & 1] for f in range(args.e2e_steps)])
+        Ts = compe.composite_host_dense_frames(fr, [outs[f & 1] for f in range(args.e2e_steps)])
         dt = allreduce_max(time.perf_counter() - t0, G)
-        assert all(t == T_one for t in Ts), (Ts, T_one)
-        T_out = T_one
-        P_full = W * H
-        h2d = sum(P_full + 24 * p.total + (4 * (P_full + 1) if G > 1 else 0) for p in host_pes)
-        d2h = P_g + 24 * T_out
+        assert all(Ts[f] == want[f % len(host_sets)] for f in range(args.e2e_steps)), (Ts, want)
+        h2d = statistics.mean(sum(P_full + 24 * p.total for p in hs) for hs in host_sets for P_full in [W * H])
+        d2h = statistics.mean(P_g + 24 * t for t in want)
         e2e = {"value": args.e2e_steps / dt, "unit": UNIT, "h2d_bytes_per_step": int(allreduce_sum(h2d, G)),
-               "d2h_bytes_per_step": int(allreduce_sum(d2h, G)),
-               "frames": args.e2e_steps,
-               "host_link_GBs": (h2d + d2h) * args.e2e_steps / dt / 1e9,  # this rank's H2D + D2H bytes / time
-               "note": "vdi_composite_host_dense_frames: per frame, pinned host sub-VDIs -> H2D -> composite "
-                       "(strip mode) -> on-device compaction -> counts + packed supersegments D2H, every rank; "
-                       "frame f's H2D overlaps frame f-1's compositing and frame f-2's D2H"}
+               "d2h_bytes_per_step": int(allreduce_sum(d2h, G)), "frames": args.e2e_steps,
+               "input_sets": len(host_sets),
+               "host_link_GBs": (h2d + d2h) * args.e2e_steps / dt / 1e9,
+               "note": "vdi_composite_host_dense_frames: per frame, pinned host sub-VDIs (one arena per frame, "
+                       "VDI_FLAG_HOST_SPAN) -> H2D -> composite -> on-device compaction -> counts + packed "
+                       "supersegments D2H, every rank; frame f's H2D overlaps frame f-1's compositing and frame "
+                       "f-2's D2H; frames cycle over the protocol's input sets"}
+        compe.close()
 
-    # ---- CPU oracle baseline (rank 0, N = 1 only) + a parity spot check
-    cpu = None
-    parity = None
+    # ---- CPU oracle baseline (rank 0, N = 1 only) + a parity band
+    cpu = parity = None
     if rank == 0 and G == 1 and not args.no_cpu:
         threads = os.cpu_count() or 1
         volh = host_volume(vol)
-        pes_o, pix = oracle_band_inputs(cfg, volh, tf, cam, dec, args.cpu_rows, threads)
+        t0 = time.perf_counter()
+        pes_o, pix = oracle_band_inputs(cfg, volh, tf, cam0, dec, args.cpu_rows, threads)
+        t_gen_o = time.perf_counter() - t0
         out, t = oracle_composite_band(cfg, pes_o, pix, threads)
         frac = len(pix) / (W * H)
         sample = (f"rows [{pix[0] // W}, {pix[-1] // W + 1}) of {H} ({len(pix)} lists, {frac:.4f} of the image), "
-                  f"oracle-generated inputs")
-        cpu = {"value": frac / t, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": sample,
-               "seconds": t}
+                  f"oracle-generated inputs; value = band fraction / band time")
+        cpu = {"value": frac / t, "unit": UNIT, "cores": threads, "cpu_model": cpu_model(), "kind": "oracle",
+               "sample": sample, "seconds": t, "oracle_generation_seconds": t_gen_o}
+        frame(base, 0)  # the image of V0, rotation 0
+        torch.cuda.synchronize()
         gc = strip.count[pix].cpu().numpy()
         gd = strip.depth[pix].cpu().numpy()
         gr = strip.rgba[pix].cpu().numpy()
         oc, od, orr = out["count"][pix], out["depth"][pix], out["rgba"][pix]
         tie = out["stats"]["margin"][pix] < 1e-6
-        ok = ~tie
-        parity = {"lists": int(len(pix)), "ties": int(tie.sum()),
-                  "count_mismatch": int((gc[ok] != oc[ok]).sum()),
-                  "max_rgba_err": float(np.abs(gr[ok] - orr[ok]).max()),
-                  "max_depth_rel_err": float((np.abs(gd[ok] - od[ok]) / np.maximum(np.abs(od[ok]), 1e-30)).max())}
+        parity = {"lists": int(len(pix)), "ties_listed": int(tie.sum()),
+                  "count_mismatch": int((gc != oc).sum()),
+                  "count_mismatch_on_ties": int(((gc != oc) & tie).sum()),
+                  "max_rgba_err": float(np.abs(gr - orr).max()),
+                  "max_depth_rel_err": float((np.abs(gd - od) / np.maximum(np.abs(od), 1e-30)).max()),
+                  "note": "every list of the band compared, ties included"}
 
     if rank == 0:
         res = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": G, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-            "scaling": "weak",
+            "scaling": "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": workload_name(cfg, args.view), "n_pes": n, "image": f"{W}x{H}",
+            "config": {"workload": workload_name(cfg, 0), "n_pes": n, "image": f"{W}x{H}",
                        "k_in": cfg.k_in, "k_out": k, "supersegments_total": S_total,
-                       "parallelism": (f"{F} VDIs per step, frame f composited whole on rank f mod {G} from all "
-                                       f"ranks' PEs (frames mode)" if G > 1 else
-                                       "one GPU: every PE homed on it, one VDI per step"),
+                       "parallelism": ("one GPU: every PE homed on it, one VDI per step" if G == 1 else
+                                       f"strip mode (PAPER.md:164): each VDI split in {G} row strips, PEs block-"
+                                       f"mapped to ranks, device-driven all-to-all exchange, dense gather to rank 0; "
+                                       f"{F} VDIs per step enqueued back to back"),
                        "frames_per_step": F,
                        "l2": f"flushed between steps ({args.flush_mb} MiB memset, untimed)",
-                       "inputs": "sub-VDIs raycast by vdi_generate_subvdi (untimed), resident in HBM",
+                       "inputs": (f"sub-VDIs raycast by vdi_generate_subvdi (untimed), resident in HBM; "
+                                  f"{len(sets)} input sets (views x rotations, PAPER.md:364-366)"),
                        "gen_seconds": round(t_gen, 2)},
-            "roofline": {"kernel": "merge_fast (pass-through lists + full-representation write, TMA bulk stores)",
-                         "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                         "algorithmic_bytes": int(B_fast), "ms": ms_fast,
-                         "merge_stage": {"algorithmic_bytes": int(B_merge), "ms": ms_merge,
-                                         "achieved_GBs": B_merge / (ms_merge * 1e-3) / 1e9,
-                                         "frac": B_merge / (ms_merge * 1e-3) / 1e9 / peak,
-                                         "ms_max_over_ranks": ms_merge_max}},
+            "roofline": {"kernel": "merge stage (receive scan + pass-through + gamma search + general path, one stream)",
+                         "bound": "hbm", "achieved": B_merge / (ms_merge * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
+                         "frac": B_merge / (ms_merge * 1e-3) / 1e9 / peak, "traffic": traffic,
+                         "peak_source": peak_src, "algorithmic_bytes": int(B_merge), "ms": ms_merge,
+                         "merge_fast": {"kernel": "merge_fast (pass-through lists + full-representation write, "
+                                                  "TMA bulk stores)", "algorithmic_bytes": int(B_fast), "ms": ms_fast,
+                                        "achieved": B_fast / (ms_fast * 1e-3) / 1e9,
+                                        "frac": B_fast / (ms_fast * 1e-3) / 1e9 / peak, "traffic": traffic_fast},
+                         "search_alu": alu},
+            "timing_protocol": protocol,
             "stages_ms": {"exchange": ms_ex, "merge": ms_merge, "gather": ms_ga,
-                          "merge_scan": statistics.mean(c["ms_scan"] for c in stage),
-                          "merge_fast": statistics.mean(c["ms_fast"] for c in stage),
-                          "merge_search": statistics.mean(c["ms_search"] for c in stage)},
+                          "merge_scan": statistics.mean(c["ms_scan"] for c in cnts),
+                          "merge_fast": ms_fast, "merge_search": ms_search},
             "phase1_generate": phase1,
             "volume_to_root_vdi": volume_to_root,
             "latency_mode": latency,
-            "frames_mode": frames_info,
+            "rotating_root": rotating,
             "full_representation_mode": full_rep,
-            "supersegments_merged_per_s": S_total * F / (ms_per_step * 1e-3),
-            "searched_lists": stage[-1]["searched_lists"],
-            "search_buckets": stage[-1]["bucket_lists"], "fast_fallback_groups": stage[-1]["fallback_groups"],
+            "supersegments_merged_per_s": S_total * value,
+            "searched_lists": cnts[-1]["searched_lists"],
+            "search_buckets": cnts[-1]["bucket_lists"], "fast_fallback_groups": cnts[-1]["fallback_groups"],
             "exchange_bytes_sent_rank0": bytes_sent, "exchange_bytes_received_rank0": bytes_recv,
-            "gather": "full representation (PAPER.md:185)" if args.full_gather else "dense + root inflate (f1)",
-            "exchange": ("NCCL send/recv" if args.nccl_exchange else
-                         "peer reads: merge kernels load peers' sub-VDIs over NVLink (CUDA IPC)" if args.peer_reads else
-                         "peer copies: copy engines pull peers' strip slices over NVLink (CUDA IPC)" if args.ce_copies else
-                         "peer copies: one SM kernel pulls peers' strip slices over NVLink (CUDA IPC)"),
-            "gather_bytes_into_root": stage[-1]["bytes_gather"],
+            "gather_bytes_into_root": cnts[-1]["bytes_gather"],
             "nvlink_roofline": None if G == 1 else {
                 "peak_GBs_per_direction": 900.0, "peak_source": "NVLink 5 nominal per GPU per direction",
-                "strip_exchange_GBs_rank0": bytes_recv / max(ms_ex, 1e-6) / 1e6,
-                "strip_exchange_frac": bytes_recv / max(ms_ex, 1e-6) / 1e6 / 900.0,
-                "strip_exchange_note": "peer slices pulled into rank 0 / (size exchange + host sync + pull) time",
-                "gather_into_root_GBs": stage[-1]["bytes_gather"] / max(ms_ga, 1e-6) / 1e6,
-                "gather_into_root_frac": stage[-1]["bytes_gather"] / max(ms_ga, 1e-6) / 1e6 / 900.0,
-                "gather_note": "dense bytes into the root / gather stage time (includes compaction, host sync and "
-                               "the root's 1 GB inflate)",
-                "frames_first_pull_GBs": frames_info["first_pull_GBs"] if frames_info else None,
-                "frames_first_pull_frac": frames_info["first_pull_GBs"] / 900.0 if frames_info else None},
+                "exchange_GBs": max(ing_max, eg_max) / max(ms_ex_max, 1e-6) / 1e6,
+                "exchange_frac": max(ing_max, eg_max) / max(ms_ex_max, 1e-6) / 1e6 / 900.0,
+                "exchange_note": "max over ranks of max(egress, ingress) bytes / the exchange stage time (strip "
+                                 "bounds + push + ready wait), one-VDI steps",
+                "gather_into_root_GBs": cnts[-1]["bytes_gather"] / max(ms_ga, 1e-6) / 1e6,
+                "gather_into_root_frac": cnts[-1]["bytes_gather"] / max(ms_ga, 1e-6) / 1e6 / 900.0,
+                "gather_note": "dense bytes into the root / gather stage time (includes the root's wait and its "
+                               "inflate of the full representation)"},
             "gpu_launches": launches,
             "clocks": clk.summary(),
             "e2e": e2e,
@@ -592,27 +656,27 @@ def _run_ours(args, world, rank, local, clk):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C3")
+    ap.add_argument("--pes", type=int, default=0, help="override the config's PE count (C5 sweep: 2/4/8/16)")
     ap.add_argument("--view", type=int, default=0)
+    ap.add_argument("--rotations", type=int, default=5, help="protocol rotations of 10 degrees per view")
+    ap.add_argument("--no-v1", action="store_true")
     ap.add_argument("--flush-mb", type=int, default=512)
     ap.add_argument("--e2e-steps", type=int, default=24)
-    ap.add_argument("--cpu-rows", type=int, default=12)
+    ap.add_argument("--e2e-sets", type=int, default=3)
+    ap.add_argument("--cpu-rows", type=int, default=64)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--full-gather", action="store_true", help="gather the full representation (PAPER.md:185)")
-    ap.add_argument("--nccl-exchange", action="store_true", help="NCCL send/recv exchange instead of peer copies")
-    ap.add_argument("--peer-reads", action="store_true", help="merge kernels read peers' slices over NVLink")
-    ap.add_argument("--frames", type=int, default=0,
-                    help="G > 1: VDIs per step in frames mode (default 4G; frame f composited whole on rank f mod G)")
-    ap.add_argument("--ce-copies", action="store_true", help="exchange copies on the copy engines, not the SM copy kernel")
-    ap.add_argument("--chunks", type=int, default=1, help="frames mode: row chunks per frame (copy/merge overlap)")
+    ap.add_argument("--rotating", action="store_true", help="N > 1: also time a root rotating over the frames")
+    ap.add_argument("--frames", type=int, default=0, help="N > 1: VDIs per step (default 4)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     world, rank, local = dist_setup()
     if args.impl == "reference":
+        args.cpu_rows = min(args.cpu_rows, 12)  # the reference arm's bounded sample per step
         run_reference(args, world, rank)
     else:
         run_ours(args, world, rank, local)

@@ -282,6 +282,23 @@ vdi_status vdi_gather(vdi_ctx* ctx, const vdi_full_view* strip, vdi_full_view* i
  * all ranks pass the same root. */
 vdi_status vdi_gather_root(vdi_ctx* ctx, uint32_t root, const vdi_full_view* strip, vdi_full_view* image_out);
 
+/* Frames in flight through strip mode: n_frames VDIs,
+ * each composited in strips on every rank (vdi_composite) and gathered onto
+ * roots[f] (vdi_gather_root; roots == NULL: vdi_config.root for all).  The
+ * root of a frame merges its own strip straight into the rows of images[f]
+ * and re-inflates the other ranks' rows on a second, ctx-owned stream, so its
+ * exchange and merge of frame f+1 -- and through them every other rank's --
+ * overlap its inflate of frame f.  Each image equals vdi_composite +
+ * vdi_gather of that frame bit for bit.  local_pes: [n_frames][n_local]
+ * (frame-major) dense views homed on this rank; images[n_frames]: full
+ * representations of rows [0, H), read only for the frames this rank is the
+ * root of (others may be zeroed structs).  The call is complete when the
+ * caller's stream passes it; never synchronises the host.  ctx-owned scratch:
+ * two strips (rows*W*(1 + 24 k_out) bytes each).  n_ranks == 1: one
+ * vdi_composite per frame into images[f]. */
+vdi_status vdi_composite_frames(vdi_ctx* ctx, uint32_t n_frames, const vdi_dense_view* local_pes,
+                                uint32_t n_local, vdi_full_view* images, const uint32_t* roots);
+
 /* ---- introspection ---------------------------------------------------------- */
 /* Per-list gamma* (0 for pass-through), tie margin and m (samples after
  * sort/subdivision) of this rank's strip for the last composite; device
@@ -306,6 +323,9 @@ typedef struct {
   uint64_t bytes_gather;     /* last vdi_gather: bytes that crossed into the root (root) / pushed (others) */
   uint64_t fallback_groups;  /* 32-list groups written with plain stores (tail group / unaligned output) */
   float ms_scan, ms_fast, ms_search; /* VDI_FLAG_STAGE_TIMING: receive scan, pass-through kernel, search kernels */
+  uint64_t sweep_steps;      /* VDI_FLAG_PIXEL_STATS: sample-steps of the plain bisection procedure (every count
+                                sweep to its early exit + the final sweep) over the searched lists -- the
+                                algorithmic work of the search (the kernels' memoised bisection skips some) */
 } vdi_counters;
 vdi_status vdi_get_counters(vdi_ctx* ctx, vdi_counters* out);
 

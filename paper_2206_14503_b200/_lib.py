@@ -67,7 +67,7 @@ class vdi_counters(C.Structure):
                 ("bytes_received", C.c_uint64), ("kernel_launches", C.c_uint32), ("ms_exchange", C.c_float),
                 ("ms_merge", C.c_float), ("ms_gather", C.c_float), ("bucket_lists", C.c_uint64 * 4),
                 ("general_lists", C.c_uint64), ("bytes_gather", C.c_uint64), ("fallback_groups", C.c_uint64),
-                ("ms_scan", C.c_float), ("ms_fast", C.c_float), ("ms_search", C.c_float)]
+                ("ms_scan", C.c_float), ("ms_fast", C.c_float), ("ms_search", C.c_float), ("sweep_steps", C.c_uint64)]
 
 
 # name -> (restype, argtypes) exactly as declared in include/vdi.h
@@ -93,6 +93,8 @@ SIGNATURES = {
                                                   C.POINTER(vdi_dense_strip)]),
     "vdi_gather": (C.c_int, [C.c_void_p, C.POINTER(vdi_full_view), C.POINTER(vdi_full_view)]),
     "vdi_gather_root": (C.c_int, [C.c_void_p, C.c_uint32, C.POINTER(vdi_full_view), C.POINTER(vdi_full_view)]),
+    "vdi_composite_frames": (C.c_int, [C.c_void_p, C.c_uint32, C.POINTER(vdi_dense_view), C.c_uint32,
+                                       C.POINTER(vdi_full_view), C.c_void_p]),
     "vdi_pixel_stats": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "vdi_get_counters": (C.c_int, [C.c_void_p, C.POINTER(vdi_counters)]),
     "vdi_strip_rows": (C.c_int, [C.c_uint32, C.c_uint32, C.c_uint32, C.POINTER(C.c_uint32),

@@ -172,6 +172,22 @@ class Compositor:
         L.check(self.lib.vdi_composite(self.ctx, views, len(local_pes), C.byref(sv)), "vdi_composite")
         return strip
 
+    def composite_frames(self, frames_local_pes, images, roots=None):
+        """vdi_composite_frames: frames_local_pes[f] = the PEs of frame f homed
+        here; images[f] = FullVDI of rows [0, H) on the root of frame f (None
+        elsewhere); roots[f] (None: the config's root for every frame)."""
+        F = len(frames_local_pes)
+        nl = len(frames_local_pes[0]) if F else 0
+        if any(len(fr) != nl for fr in frames_local_pes) or len(images) != F:
+            raise ValueError("every frame needs the same number of local PEs and one image slot")
+        flat = [p.view() for fr in frames_local_pes for p in fr]
+        views = (L.vdi_dense_view * max(1, len(flat)))(*flat)
+        ims = (L.vdi_full_view * max(1, F))(*[im.view() if im is not None else L.vdi_full_view() for im in images])
+        rs = (C.c_uint32 * max(1, F))(*roots) if roots is not None else None
+        L.check(self.lib.vdi_composite_frames(self.ctx, F, views, nl, ims, C.cast(rs, C.c_void_p) if rs is not None
+                                              else None), "vdi_composite_frames")
+        return images
+
     def dense_to_full(self, pe: DenseSubVDI) -> FullVDI:
         """vdi_dense_to_full: the sub-VDI in the full representation (k_in slots)."""
         out = FullVDI.empty(self.width, 0, self.height, self.k_in)

@@ -95,6 +95,7 @@ struct DevCounters {
   unsigned long long fallback_groups;
   unsigned long long records_search;
   unsigned long long long_used;
+  unsigned long long sweep_steps;
 };
 
 inline size_t al256(size_t b) { return (b + 255) & ~(size_t)255; }
@@ -216,7 +217,17 @@ struct vdi_ctx {
   bool timing_pending = false;
   bool gather_timing_pending = false;
   cudaEvent_t gev[2] = {nullptr, nullptr};
+  // vdi_composite_frames: the root's inflate stream and the non-root strips
+  cudaStream_t gst = nullptr;
+  cudaEvent_t gev_in = nullptr, gev_out = nullptr;
+  DevBuf fs_count[2], fs_depth[2], fs_rgba[2];
   ~vdi_ctx() {
+    if (gst) {
+      cudaStreamSynchronize(gst);
+      cudaStreamDestroy(gst);
+    }
+    if (gev_in) cudaEventDestroy(gev_in);
+    if (gev_out) cudaEventDestroy(gev_out);
     if (pin_st) cudaStreamSynchronize(pin_st);
     if (pout_st) cudaStreamSynchronize(pout_st);
     if (pin_st) cudaStreamDestroy(pin_st);
@@ -388,6 +399,7 @@ static vdi_status merge_lists(vdi_ctx* ctx, MergeParams& mp, uint64_t P, uint64_
   mp.stat_margin = stats ? ctx->stat_margin.as<float>() : nullptr;
   mp.records_in = &dc->records_in;
   mp.records_search = &dc->records_search;
+  mp.sweep_steps = stats ? &dc->sweep_steps : nullptr;
   mp.err = &dc->err;
   mp.validate = (cf.flags & VDI_FLAG_VALIDATE) ? 1 : 0;
   uint32_t* slp = ctx->slots.as<uint32_t>();
@@ -418,11 +430,12 @@ static vdi_status merge_lists(vdi_ctx* ctx, MergeParams& mp, uint64_t P, uint64_
 // vdi_dense_to_full): one source, group bases given.
 static vdi_status inflate(vdi_ctx* ctx, const uint8_t* count, const float2* depth, const float4* rgba,
                           const uint32_t* group_base, uint64_t P, uint32_t k, uint8_t* oc, float2* od, float4* orgba,
-                          int& launches) {
+                          int& launches, cudaStream_t st = nullptr) {
+  if (!st) st = ctx->stream;
   if (!P) return VDI_OK;
   CUDA_TRY(ctx, ctx->g_misc.grow(sizeof(DevCounters) + 256));
   DevCounters* gc = ctx->g_misc.as<DevCounters>();
-  CUDA_TRY(ctx, cudaMemsetAsync(gc, 0, sizeof(DevCounters), ctx->stream));
+  CUDA_TRY(ctx, cudaMemsetAsync(gc, 0, sizeof(DevCounters), st));
   MergeParams mi{};
   mi.n_src = 1;
   mi.k_out = (int)k;
@@ -443,7 +456,7 @@ static vdi_status inflate(vdi_ctx* ctx, const uint8_t* count, const float2* dept
   mi.records_in = &gc->records_in;
   mi.fallback_groups = &gc->fallback_groups;
   mi.err = &gc->err;
-  CUDA_TRY(ctx, launch_fast(mi, ctx->stream, &launches));
+  CUDA_TRY(ctx, launch_fast(mi, st, &launches));
   return VDI_OK;
 }
 
@@ -769,26 +782,28 @@ static vdi_status check_local(vdi_ctx* ctx, const vdi_dense_view* local, uint32_
 }
 
 // block until the flags reach their targets (one-CTA spin kernel on the stream)
-static vdi_status wait_flags(vdi_ctx* ctx, int kind, const std::vector<std::pair<uint32_t, uint32_t>>& who_target) {
+static vdi_status wait_flags(vdi_ctx* ctx, int kind, const std::vector<std::pair<uint32_t, uint32_t>>& who_target,
+                             cudaStream_t st = nullptr) {
   WaitArgs w{};
   for (auto& [r, t] : who_target) {
     w.addr[w.n] = flag_at(ctx->peer[ctx->cfg.rank], kind, r);
     w.target[w.n] = t;
     ++w.n;
   }
-  CUDA_TRY(ctx, launch_wait(w, ctx->stream));
+  CUDA_TRY(ctx, launch_wait(w, st ? st : ctx->stream));
   return VDI_OK;
 }
 
 // release store of `value` into flag word (kind, me) of each listed peer
-static vdi_status signal_peers(vdi_ctx* ctx, int kind, const std::vector<uint32_t>& peers, uint32_t value) {
+static vdi_status signal_peers(vdi_ctx* ctx, int kind, const std::vector<uint32_t>& peers, uint32_t value,
+                               cudaStream_t st = nullptr) {
   SignalArgs s{};
   for (uint32_t r : peers) {
     s.addr[s.n] = flag_at(ctx->peer[r], kind, ctx->cfg.rank);
     s.value[s.n] = value;
     ++s.n;
   }
-  CUDA_TRY(ctx, launch_signal(s, ctx->stream));
+  CUDA_TRY(ctx, launch_signal(s, st ? st : ctx->stream));
   return VDI_OK;
 }
 
@@ -1122,11 +1137,86 @@ vdi_status vdi_composite_fullrep(vdi_ctx* ctx, const vdi_full_view* local, const
   return VDI_OK;
 }
 
+// Gather (a11), non-root side: compaction of the composited
+// strip straight into root R's window (stream st), gather sequence number j
+static vdi_status gather_send(vdi_ctx* ctx, const vdi_full_view* strip, uint32_t R, uint32_t j, cudaStream_t st,
+                              int& launches) {
+  const Layout& L = ctx->lay;
+  const uint32_t me = ctx->cfg.rank, W = ctx->cfg.width, k = ctx->cfg.k_out;
+  char* gp = ctx->peer[R] + L.g_off(R, j & 1);
+  CUDA_TRY(ctx, cudaMemsetAsync(ctx->ccnt.as<unsigned long long>() + 1, 0, 8, st));
+  if (j > 2) {  // the root has inflated this buffer's previous contents
+    if (vdi_status s = wait_flags(ctx, GFREE, {{R, j - 2}}, st)) return s;
+    ++launches;
+  }
+  const uint32_t P = (uint32_t)ctx->P, ng = (P + 31) / 32;
+  MergeParams ms{};
+  ms.n_src = 1;
+  ms.P = P;
+  ms.n_groups = ng;
+  ms.src[0].count = strip->count;
+  CUDA_TRY(ctx, launch_scan(ms, ctx->gsum.as<uint32_t>(), ctx->gbase_loc.as<uint32_t>(), st, &launches));
+  CompactPushArgs a{};
+  a.count = strip->count;
+  a.depth = reinterpret_cast<const float2*>(strip->depth);
+  a.rgba = reinterpret_cast<const float4*>(strip->rgba);
+  a.P = P;
+  a.k = (int)k;
+  a.group_base = ctx->gbase_loc.as<uint32_t>();
+  a.region = (uint32_t)((size_t)ctx->row0 * W * k);
+  a.dst_count = reinterpret_cast<uint8_t*>(gp + L.g_count_off()) + (size_t)ctx->row0 * W;
+  a.dst_gbase = reinterpret_cast<uint32_t*>(gp + L.g_gbase_off()) + L.gbase_index(me);
+  a.dst_depth = reinterpret_cast<float2*>(gp + L.g_depth_off());
+  a.dst_rgba = reinterpret_cast<float4*>(gp + L.g_rgba_off());
+  a.total_out = reinterpret_cast<unsigned long long*>(gp + L.g_hdr_off()) + me;
+  a.bytes = ctx->ccnt.as<unsigned long long>() + 1;
+  a.flag = flag_at(ctx->peer[R], GREADY, me);
+  CUDA_TRY(ctx, launch_compact_push(a, compact_push_blocks(P), st));
+  ++launches;
+  return VDI_OK;
+}
+
+// Gather, root side (this rank is R): wait until every other rank's
+// compaction j has landed, re-inflate their rows of `image` with the
+// pass-through kernel, release the buffer (stream st)
+static vdi_status gather_recv(vdi_ctx* ctx, vdi_full_view* image, uint32_t j, cudaStream_t st, int& launches) {
+  const Layout& L = ctx->lay;
+  const uint32_t G = ctx->cfg.n_ranks, R = ctx->cfg.rank, W = ctx->cfg.width, k = ctx->cfg.k_out;
+  char* gp = ctx->peer[R] + L.g_off(R, j & 1);
+  std::vector<std::pair<uint32_t, uint32_t>> wt;
+  for (uint32_t g = 0; g < G; ++g)
+    if (g != R) wt.push_back({g, j * compact_push_blocks(L.rows(g) * W)});
+  if (vdi_status s = wait_flags(ctx, GREADY, wt, st)) return s;
+  ++launches;
+  const uint8_t* gc = reinterpret_cast<const uint8_t*>(gp + L.g_count_off());
+  const uint32_t* gb = reinterpret_cast<const uint32_t*>(gp + L.g_gbase_off());
+  const float2* gd = reinterpret_cast<const float2*>(gp + L.g_depth_off());
+  const float4* gr = reinterpret_cast<const float4*>(gp + L.g_rgba_off());
+  auto infl = [&](size_t p0, size_t P, const uint32_t* gbp) -> vdi_status {
+    return inflate(ctx, gc + p0, gd, gr, gbp, P, k, image->count + p0, reinterpret_cast<float2*>(image->depth) + p0 * k,
+                   reinterpret_cast<float4*>(image->rgba) + p0 * k, launches, st);
+  };
+  if (L.aligned()) {  // the rows before and after the root's own strip: one launch each
+    const size_t a0 = 0, a1 = (size_t)ctx->row0 * W, b0 = (size_t)ctx->row1 * W, b1 = L.img();
+    if (vdi_status s = infl(a0, a1 - a0, gb + a0 / 32)) return s;
+    if (vdi_status s = infl(b0, b1 - b0, gb + b0 / 32)) return s;
+  } else {
+    for (uint32_t g = 0; g < G; ++g)
+      if (g != R)
+        if (vdi_status s = infl((size_t)L.row0(g) * W, (size_t)L.rows(g) * W, gb + L.gbase_index(g))) return s;
+  }
+  std::vector<uint32_t> others;
+  for (uint32_t g = 0; g < G; ++g)
+    if (g != R) others.push_back(g);
+  if (vdi_status s = signal_peers(ctx, GFREE, others, j, st)) return s;
+  ++launches;
+  return VDI_OK;
+}
+
 // Gather (a11) of the composited strips onto rank R
 static vdi_status gather_to(vdi_ctx* ctx, const vdi_full_view* strip, vdi_full_view* image, uint32_t R) {
   if (vdi_status s = check_ctx(ctx)) return s;
   const vdi_config& cf = ctx->cfg;
-  const Layout& L = ctx->lay;
   const uint32_t G = cf.n_ranks, me = cf.rank, W = cf.width, k = cf.k_out;
   if (!strip || !strip->count || !strip->depth || !strip->rgba) return fail(VDI_ERR_INVALID_ARG, "strip is NULL");
   if (strip->row_begin != ctx->row0 || strip->row_end != ctx->row1)
@@ -1161,73 +1251,15 @@ static vdi_status gather_to(vdi_ctx* ctx, const vdi_full_view* strip, vdi_full_v
     // with the pass-through kernel -- the image is bit-identical to gathering
     // the full representation
     if (vdi_status s = resolve_peers(ctx)) return s;
-    const uint32_t j = ++ctx->gcalls_to[R], q = j & 1;
-    char* gp = ctx->peer[R] + L.g_off(R, q);
-    CUDA_TRY(ctx, ctx->ccnt.grow(64));
+    const uint32_t j = ++ctx->gcalls_to[R];
     if (!root) {
-      CUDA_TRY(ctx, cudaMemsetAsync(ctx->ccnt.as<unsigned long long>() + 1, 0, 8, st));
-      if (j > 2) {  // the root has inflated this buffer's previous contents
-        if (vdi_status s = wait_flags(ctx, GFREE, {{R, j - 2}})) return s;
-        ++launches;
-      }
-      const uint32_t P = (uint32_t)ctx->P, ng = (P + 31) / 32;
-      MergeParams ms{};
-      ms.n_src = 1;
-      ms.P = P;
-      ms.n_groups = ng;
-      ms.src[0].count = strip->count;
-      CUDA_TRY(ctx, ctx->gsum.grow(((size_t)scan_chunks(P) + 8) * 4));
-      CUDA_TRY(ctx, ctx->gbase_loc.grow(((size_t)ng + 8) * 4));
-      CUDA_TRY(ctx, launch_scan(ms, ctx->gsum.as<uint32_t>(), ctx->gbase_loc.as<uint32_t>(), st, &launches));
-      CompactPushArgs a{};
-      a.count = strip->count;
-      a.depth = reinterpret_cast<const float2*>(strip->depth);
-      a.rgba = reinterpret_cast<const float4*>(strip->rgba);
-      a.P = P;
-      a.k = (int)k;
-      a.group_base = ctx->gbase_loc.as<uint32_t>();
-      a.region = (uint32_t)((size_t)ctx->row0 * W * k);
-      a.dst_count = reinterpret_cast<uint8_t*>(gp + L.g_count_off()) + (size_t)ctx->row0 * W;
-      a.dst_gbase = reinterpret_cast<uint32_t*>(gp + L.g_gbase_off()) + L.gbase_index(me);
-      a.dst_depth = reinterpret_cast<float2*>(gp + L.g_depth_off());
-      a.dst_rgba = reinterpret_cast<float4*>(gp + L.g_rgba_off());
-      a.total_out = reinterpret_cast<unsigned long long*>(gp + L.g_hdr_off()) + me;
-      a.bytes = ctx->ccnt.as<unsigned long long>() + 1;
-      a.flag = flag_at(ctx->peer[R], GREADY, me);
-      CUDA_TRY(ctx, launch_compact_push(a, compact_push_blocks(P), st));
-      ++launches;
+      if (vdi_status s = gather_send(ctx, strip, R, j, st, launches)) return s;
     } else {
-      std::vector<std::pair<uint32_t, uint32_t>> wt;
-      for (uint32_t g = 0; g < G; ++g)
-        if (g != R) wt.push_back({g, j * compact_push_blocks(L.rows(g) * W)});
-      if (vdi_status s = wait_flags(ctx, GREADY, wt)) return s;
-      ++launches;
-      const uint8_t* gc = reinterpret_cast<const uint8_t*>(gp + L.g_count_off());
-      const uint32_t* gb = reinterpret_cast<const uint32_t*>(gp + L.g_gbase_off());
-      const float2* gd = reinterpret_cast<const float2*>(gp + L.g_depth_off());
-      const float4* gr = reinterpret_cast<const float4*>(gp + L.g_rgba_off());
-      auto infl = [&](size_t p0, size_t P, const uint32_t* gbp) -> vdi_status {
-        return inflate(ctx, gc + p0, gd, gr, gbp, P, k, image->count + p0, reinterpret_cast<float2*>(image->depth) + p0 * k,
-                       reinterpret_cast<float4*>(image->rgba) + p0 * k, launches);
-      };
-      if (L.aligned()) {  // the rows before and after the root's own strip: one launch each
-        const size_t a0 = 0, a1 = (size_t)ctx->row0 * W, b0 = (size_t)ctx->row1 * W, b1 = L.img();
-        if (vdi_status s = infl(a0, a1 - a0, gb + a0 / 32)) return s;
-        if (vdi_status s = infl(b0, b1 - b0, gb + b0 / 32)) return s;
-      } else {
-        for (uint32_t g = 0; g < G; ++g)
-          if (g != R)
-            if (vdi_status s = infl((size_t)L.row0(g) * W, (size_t)L.rows(g) * W, gb + L.gbase_index(g))) return s;
-      }
+      if (vdi_status s = gather_recv(ctx, image, j, st, launches)) return s;
       CUDA_TRY(ctx, copy_own());
-      std::vector<uint32_t> others;
-      for (uint32_t g = 0; g < G; ++g)
-        if (g != R) others.push_back(g);
-      if (vdi_status s = signal_peers(ctx, GFREE, others, j)) return s;
-      ++launches;
     }
     ctx->last_gather_root = (int)R;
-    ctx->last_gather_parity = q;
+    ctx->last_gather_parity = j & 1;
   }
   ctx->last.kernel_launches += (uint32_t)launches;
   if (timing) {
@@ -1244,6 +1276,83 @@ vdi_status vdi_gather(vdi_ctx* ctx, const vdi_full_view* strip, vdi_full_view* i
 
 vdi_status vdi_gather_root(vdi_ctx* ctx, uint32_t root, const vdi_full_view* strip, vdi_full_view* image) {
   return gather_to(ctx, strip, image, root);
+}
+
+// Frames in flight through strip mode: frame f =
+// vdi_composite + vdi_gather onto roots[f], but the root merges its strip
+// straight into the rows of images[f] and re-inflates the other rows on a
+// second stream, so that its exchange and merge of frame f+1 do not wait for
+// its inflate of frame f (and neither do the other ranks, whose next slices
+// it pushes right after its merge).  Non-root strips: two ctx-owned buffers.
+vdi_status vdi_composite_frames(vdi_ctx* ctx, uint32_t F, const vdi_dense_view* local, uint32_t n_local,
+                                vdi_full_view* images, const uint32_t* roots) {
+  if (vdi_status s = check_ctx(ctx)) return s;
+  const vdi_config& cf = ctx->cfg;
+  const uint32_t G = cf.n_ranks, me = cf.rank, W = cf.width, H = cf.height, k = cf.k_out;
+  if (!F) return VDI_OK;
+  if (!images || (n_local && !local)) return fail(VDI_ERR_INVALID_ARG, "images / local_pes is NULL");
+  for (uint32_t f = 0; f < F; ++f) {
+    const uint32_t R = roots ? roots[f] : cf.root;
+    if (R >= G) return fail(VDI_ERR_INVALID_ARG, "roots[%u] = %u >= n_ranks", f, R);
+    if (R != me) continue;
+    const vdi_full_view& im = images[f];
+    if (!im.count || !im.depth || !im.rgba || im.row_begin != 0 || im.row_end != H)
+      return fail(VDI_ERR_INVALID_ARG, "images[%u] (root %u) must cover rows [0, H)", f, R);
+    if ((reinterpret_cast<uintptr_t>(im.rgba) & 15) || (reinterpret_cast<uintptr_t>(im.depth) & 7))
+      return fail(VDI_ERR_INVALID_ARG, "images[%u]: depth/rgba must be 8/16-byte aligned", f);
+  }
+  cudaStream_t st = ctx->stream;
+  const size_t P = ctx->P, o = (size_t)ctx->row0 * W;
+  if (G == 1) {
+    for (uint32_t f = 0; f < F; ++f) {
+      vdi_full_view so{0, H, images[f].count, images[f].depth, images[f].rgba};
+      if (vdi_status s = vdi_composite(ctx, local + (size_t)f * n_local, n_local, &so)) return s;
+    }
+    return VDI_OK;
+  }
+  if (vdi_status s = resolve_peers(ctx)) return s;
+  if (!ctx->gst) {
+    CUDA_TRY(ctx, cudaStreamCreateWithFlags(&ctx->gst, cudaStreamNonBlocking));
+    CUDA_TRY(ctx, cudaEventCreateWithFlags(&ctx->gev_in, cudaEventDisableTiming));
+    CUDA_TRY(ctx, cudaEventCreateWithFlags(&ctx->gev_out, cudaEventDisableTiming));
+  }
+  for (int i = 0; i < 2; ++i) {
+    CUDA_TRY(ctx, ctx->fs_count[i].grow(P));
+    CUDA_TRY(ctx, ctx->fs_depth[i].grow(P * k * 8));
+    CUDA_TRY(ctx, ctx->fs_rgba[i].grow(P * k * 16));
+  }
+  // the inflate stream starts once the caller's stream has reached this call
+  CUDA_TRY(ctx, cudaEventRecord(ctx->gev_in, st));
+  CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->gst, ctx->gev_in, 0));
+  int launches = 0;
+  uint32_t nf = 0;
+  for (uint32_t f = 0; f < F; ++f) {
+    const uint32_t R = roots ? roots[f] : cf.root;
+    vdi_full_view so;
+    if (R == me) {  // the root's strip is its image rows
+      so = vdi_full_view{ctx->row0, ctx->row1, images[f].count + o, images[f].depth + o * k * 2,
+                         images[f].rgba + o * k * 4};
+    } else {
+      const int b = nf++ & 1;
+      so = vdi_full_view{ctx->row0, ctx->row1, ctx->fs_count[b].as<uint8_t>(), ctx->fs_depth[b].as<float>(),
+                         ctx->fs_rgba[b].as<float>()};
+    }
+    if (vdi_status s = vdi_composite(ctx, local + (size_t)f * n_local, n_local, &so)) return s;
+    launches += ctx->last.kernel_launches;
+    const uint32_t j = ++ctx->gcalls_to[R];
+    if (R != me) {
+      if (vdi_status s = gather_send(ctx, &so, R, j, st, launches)) return s;
+    } else {
+      if (vdi_status s = gather_recv(ctx, &images[f], j, ctx->gst, launches)) return s;
+    }
+    ctx->last_gather_root = (int)R;
+    ctx->last_gather_parity = j & 1;
+  }
+  // the call ends on the caller's stream once the inflates have too
+  CUDA_TRY(ctx, cudaEventRecord(ctx->gev_out, ctx->gst));
+  CUDA_TRY(ctx, cudaStreamWaitEvent(st, ctx->gev_out, 0));
+  ctx->last.kernel_launches = (uint32_t)launches;
+  return VDI_OK;
 }
 
 // H2D of the host sub-VDIs into input slot `set` (0/1: the double-buffered
@@ -1579,6 +1688,7 @@ vdi_status vdi_get_counters(vdi_ctx* ctx, vdi_counters* out) {
   for (int b = 0; b < 4; ++b) ctx->last.bucket_lists[b] = h.wl_count[b];
   ctx->last.general_lists = h.wl_count[VDI_BUCKET_GENERAL];
   ctx->last.fallback_groups = h.fallback_groups;
+  ctx->last.sweep_steps = h.sweep_steps;
   ctx->last.bytes_sent = cc[0];
   ctx->last.bytes_received = 0;
   for (unsigned long long t : xh) ctx->last.bytes_received += ctx->P + 24ull * t;

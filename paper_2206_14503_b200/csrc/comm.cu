@@ -149,15 +149,28 @@ __global__ void __launch_bounds__(128) compact_push_kernel(CompactPushArgs a) {
     const uint32_t p = g * 32 + lane;
     const uint32_t c = p < a.P ? a.count[p] : 0u;
     const uint32_t gb = a.group_base[g];
-    const size_t off = (size_t)a.region + gb + warp_incl_scan_c(c, lane) - c;  // record index in the root window
     if (p < a.P) a.dst_count[p] = (uint8_t)c;
     if (lane == 0) a.dst_gbase[g] = a.region + gb;
-    const float2* sd = a.depth + (size_t)p * a.k;
-    const float4* sc = a.rgba + (size_t)p * a.k;
-#pragma unroll 4
-    for (uint32_t j = 0; j < c; ++j) {
-      a.dst_depth[off + j] = __ldg(sd + j);
-      a.dst_rgba[off + j] = __ldg(sc + j);
+    // the group's records are contiguous in the root window: record d goes to
+    // base + d, consecutive lanes -> consecutive records (coalesced stores over
+    // NVLink); the list holding record d: 5-step search over the lists' prefix
+    const uint32_t incl = warp_incl_scan_c(c, lane), excl = incl - c;
+    const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
+    const size_t base = (size_t)a.region + gb;
+    for (uint32_t d0 = 0; d0 < tot; d0 += 32) {
+      const uint32_t d = d0 + lane;
+      uint32_t l = 0;
+#pragma unroll
+      for (int step = 16; step > 0; step >>= 1) {
+        const uint32_t e = __shfl_sync(0xffffffffu, excl, (int)(l + step));
+        if (e <= d) l += step;
+      }
+      const uint32_t el = __shfl_sync(0xffffffffu, excl, (int)l);
+      if (d < tot) {
+        const size_t src = ((size_t)g * 32 + l) * a.k + (d - el);
+        a.dst_depth[base + d] = __ldg(a.depth + src);
+        a.dst_rgba[base + d] = __ldg(a.rgba + src);
+      }
     }
   }
   if (blockIdx.x == 0 && threadIdx.x == 0 && a.total_out) {

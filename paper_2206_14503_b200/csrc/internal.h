@@ -72,6 +72,7 @@ struct MergeParams {
   float* stat_margin;  // optional [P]: min |sqrt(D^2) - gamma| over the executed comparisons
   unsigned long long* records_in;
   unsigned long long* records_search;   // records of lists sent to the search / general paths
+  unsigned long long* sweep_steps;      // optional: sample-steps of the plain procedure (PIXEL_STATS replay)
   unsigned long long* fallback_groups;  // groups written with plain stores
   uint32_t* search_ticket;              // [VDI_N_BUCKETS] per-bucket claim tickets of the search kernels
   // short-list search scratch (buckets 0, 1), a pool of batch slots shared by

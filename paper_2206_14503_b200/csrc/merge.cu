@@ -157,12 +157,13 @@ __device__ __forceinline__ void note_margin(double* mg, float d2, float gamma) {
 // mg (optional) tracks the tie margin of the executed comparisons.
 template <class Get>
 __device__ __forceinline__ int sweep(Get get, int m, float gamma, int k, float2* od, float4* oc,
-                                     double* mg = nullptr) {
+                                     double* mg = nullptr, unsigned long long* steps = nullptr) {
   const float g2 = gamma * gamma;
   int cnt = 0;
   bool open = false;
   float ar = 0.f, ag = 0.f, ab = 0.f, aa = 0.f, tf = 0.f, tb = 0.f, prev_tb = 0.f;
   for (int i = 0; i < m; ++i) {
+    if (steps) ++*steps;
     const Rec s = get(i);
     if (open && s.tf > prev_tb) {
       const float n2 = dist2(ar, ag, ab, aa, 0.f, 0.f, 0.f, 0.f);
@@ -217,11 +218,12 @@ __device__ __forceinline__ int sweep(Get get, int m, float gamma, int k, float2*
 // Per-list gamma bisection (PAPER.md:100-101 re-used at :176; Q3-Q6):
 // midpoints 0.5*(lo+hi) of [0, gamma_max], I iterations, stop at count == k.
 template <class Get>
-__device__ __forceinline__ float bisect(Get get, int m, int k, int iters, float gmax, double* mg = nullptr) {
+__device__ __forceinline__ float bisect(Get get, int m, int k, int iters, float gmax, double* mg = nullptr,
+                                        unsigned long long* steps = nullptr) {
   float lo = 0.f, hi = gmax, best = gmax;
   for (int it = 0; it < iters; ++it) {
     const float mid = 0.5f * (lo + hi);
-    const int c = sweep(get, m, mid, k, nullptr, nullptr, mg);
+    const int c = sweep(get, m, mid, k, nullptr, nullptr, mg, steps);
     if (c <= k) {
       best = hi = mid;
       if (c == k) break;
@@ -1489,8 +1491,10 @@ __device__ __forceinline__ void general_body(const MergeParams& mp, uint32_t tid
       }
       cnt = m;
     } else {
-      gamma = bisect(get, m, k, mp.max_iters, mp.gamma_max, mg);
-      cnt = sweep(get, m, gamma, k, od, oc, mg);
+      unsigned long long st = 0;
+      gamma = bisect(get, m, k, mp.max_iters, mp.gamma_max, mg, mp.sweep_steps ? &st : nullptr);
+      cnt = sweep(get, m, gamma, k, od, oc, mg, mp.sweep_steps ? &st : nullptr);
+      if (st) atomicAdd(mp.sweep_steps, st);
     }
     mp.out_count[p] = (uint8_t)cnt;
     if (mp.stat_m) mp.stat_m[p] = (uint16_t)m;
@@ -1514,7 +1518,10 @@ __global__ void __launch_bounds__(128) margins_kernel(MergeParams mp) {
                          min(mp.wl_count[2], mp.wl_cap), min(mp.wl_count[3], mp.wl_cap)};
   const uint32_t tot = c[0] + c[1] + c[2] + c[3];
   const int n = mp.n_src, k = mp.k_out;
-  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < tot; t += gridDim.x * blockDim.x) {
+  unsigned long long steps = 0;
+  const uint32_t t_end = (tot + 31) / 32 * 32;  // whole warps iterate (warp reduction below)
+  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < t_end; t += gridDim.x * blockDim.x) {
+    if (t >= tot) continue;
     int b = 0;
     uint32_t e = t;
     while (e >= c[b]) e -= c[b++];
@@ -1546,10 +1553,16 @@ __global__ void __launch_bounds__(128) margins_kernel(MergeParams mp) {
       return Rec{d.x, d.y, v.x, v.y, v.z, fabsf(v.w)};
     };
     double mgn = CUDART_INF;
-    const float g = bisect(get, m, k, mp.max_iters, mp.gamma_max, &mgn);
-    sweep(get, m, g, k, nullptr, nullptr, &mgn);
+    unsigned long long st = 0;
+    const float g = bisect(get, m, k, mp.max_iters, mp.gamma_max, &mgn, &st);
+    sweep(get, m, g, k, nullptr, nullptr, &mgn, &st);
     mp.stat_margin[p] = (float)mgn;
+    steps += st;
   }
+  // algorithmic sample-steps of the procedure (count sweeps to their early
+  // exit + the final sweep), the unit of the search's ALU roofline
+  for (int d = 16; d > 0; d >>= 1) steps += __shfl_down_sync(kFull, steps, d);
+  if ((threadIdx.x & 31) == 0 && steps && mp.sweep_steps) atomicAdd(mp.sweep_steps, steps);
 }
 
 // ---------------------------------------------------------------------------
@@ -1600,24 +1613,44 @@ __global__ void __launch_bounds__(256) sum_u32_kernel(const uint32_t* __restrict
   }
 }
 
+// Compaction of one 32-list group (warp): the group's records are contiguous
+// in the dense output, so record d of the group goes to od/oc[base + d] --
+// consecutive lanes store consecutive records (coalesced, also across NVLink);
+// the lane whose list holds record d is found by a 5-step search over the
+// lists' exclusive prefix (warp shuffles).
+__device__ __forceinline__ void compact_group(const uint8_t* __restrict__ count, const float2* __restrict__ depth,
+                                              const float4* __restrict__ rgba, uint32_t P, int k, uint32_t g,
+                                              size_t base, float2* __restrict__ od, float4* __restrict__ oc, int lane) {
+  const uint32_t p = g * 32 + lane;
+  const uint32_t c = p < P ? count[p] : 0u;
+  const uint32_t incl = warp_incl_scan(c, lane), excl = incl - c;
+  const uint32_t tot = __shfl_sync(kFull, incl, 31);
+  for (uint32_t d0 = 0; d0 < tot; d0 += 32) {
+    const uint32_t d = d0 + lane;
+    uint32_t l = 0;
+#pragma unroll
+    for (int step = 16; step > 0; step >>= 1) {
+      const uint32_t e = __shfl_sync(kFull, excl, (int)(l + step));
+      if (e <= d) l += step;
+    }
+    // empty lists share their successor's prefix: l is the last list starting at or before d
+    const uint32_t el = __shfl_sync(kFull, excl, (int)l);
+    if (d < tot) {
+      const size_t src = ((size_t)g * 32 + l) * k + (d - el);
+      od[base + d] = __ldg(depth + src);
+      oc[base + d] = __ldg(rgba + src);
+    }
+  }
+}
+
 __global__ void __launch_bounds__(128) compact_kernel(const uint8_t* __restrict__ count, const float2* __restrict__ depth,
                                                       const float4* __restrict__ rgba, uint32_t P, int k,
                                                       const uint32_t* __restrict__ group_base, float2* __restrict__ od,
                                                       float4* __restrict__ oc) {
   const int lane = threadIdx.x & 31;
   const uint32_t ng = (P + 31) / 32;
-  for (uint32_t g = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); g < ng; g += gridDim.x * (blockDim.x >> 5)) {
-    const uint32_t p = g * 32 + lane;
-    const uint32_t c = p < P ? count[p] : 0u;
-    const uint32_t off = group_base[g] + warp_incl_scan(c, lane) - c;
-    const float2* sd = depth + (size_t)p * k;
-    const float4* sc = rgba + (size_t)p * k;
-#pragma unroll 4
-    for (uint32_t j = 0; j < c; ++j) {
-      od[off + j] = __ldg(sd + j);
-      oc[off + j] = __ldg(sc + j);
-    }
-  }
+  for (uint32_t g = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); g < ng; g += gridDim.x * (blockDim.x >> 5))
+    compact_group(count, depth, rgba, P, k, g, group_base[g], od, oc, lane);
 }
 
 cudaError_t launch_total(const MergeParams& mp, const uint32_t* chunk_sum, unsigned long long* out, cudaStream_t st,

@@ -135,24 +135,31 @@ def main():
     c2.close()
     del fulls
 
-    # (3) pipelined frames, rotating root: all calls enqueued back to back
+    # (3) pipelined frames with a rotating root: vdi_gather_root calls
+    # enqueued back to back, then vdi_composite_frames (frames in flight, one
+    # root and a rotating root)
     F = 2 * world + 1
-    strips = [comp.empty_strip() for _ in range(F)]
     roots = [f % world for f in range(F)]
-    ims = [vdi.FullVDI.empty(W, 0, H, k_out) if rank == roots[f] else None for f in range(F)]
-    for f in range(F):
-        comp.composite(mine(sets[f % len(sets)]), strips[f])
-        comp.gather(strips[f], ims[f], root=roots[f])
-    torch.cuda.synchronize()
-    eq = []
-    for f in range(F):
-        im0 = to_rank0(ims[f], roots[f], rank)
+    for mode in ("calls", "frames_root0", "frames_rotating"):
+        rts = [0] * F if mode == "frames_root0" else roots
+        ims = [vdi.FullVDI.empty(W, 0, H, k_out) if rank == rts[f] else None for f in range(F)]
+        if mode == "calls":
+            strips = [comp.empty_strip() for _ in range(F)]
+            for f in range(F):
+                comp.composite(mine(sets[f % len(sets)]), strips[f])
+                comp.gather(strips[f], ims[f], root=rts[f])
+        else:
+            comp.composite_frames([mine(sets[f % len(sets)]) for f in range(F)], ims, roots=rts)
         torch.cuda.synchronize()
+        eq = []
+        for f in range(F):
+            im0 = to_rank0(ims[f], rts[f], rank)
+            torch.cuda.synchronize()
+            if rank == 0:
+                eq.append(equal(im0, refs[f % len(sets)]))
         if rank == 0:
-            eq.append(equal(im0, refs[f % len(sets)]))
-    if rank == 0:
-        res["rotating_root_frames_equal"] = eq
-        ok &= all(eq)
+            res[f"{mode}_equal"] = eq
+            ok &= all(eq)
 
     # (4) host entry points at n_ranks > 1: 3 distinct input sets (2 for C*),
     # order reusing both slots, per-array and one-span uploads

@@ -253,3 +253,29 @@ def test_loopback_host_entries(vdi, span):
                 np.array_equal(outs[f][2].numpy()[:Ts[f]], fr[sel]), (r, f)
     for c in comps:
         c.close()
+
+
+@pytest.mark.parametrize("rotate", [False, True])
+def test_loopback_composite_frames(vdi, rotate):
+    """vdi_composite_frames (frames in flight through strip mode): the root
+    merges into its image rows and inflates the others on a second stream;
+    six frames, one root or a rotating one -- each image equals the
+    one-context composite of its frame bit for bit."""
+    G, n, W, H, k = 3, 6, 128, 72, 10
+    F = 6
+    comps = _group(vdi, G, W, H, k, k, n)
+    frames = []
+    for f in range(F):
+        pes = synth.random_subvdis(n, W, H, k, lam=7.0 + f, seed=1500 + f)
+        frames.append([dense_to_device(p, i) for i, p in enumerate(pes)])
+    ones = [_one_gpu(vdi, fr, W, H, k, k)[0] for fr in frames]
+    roots = [f % G if rotate else 0 for f in range(F)]
+    images = {r: [vdi.FullVDI.empty(W, 0, H, k) if roots[f] == r else None for f in range(F)] for r in range(G)}
+    torch.cuda.synchronize()
+    for r, c in enumerate(comps):
+        c.composite_frames([_local(vdi, comps, fr, r) for fr in frames], images[r], roots=roots)
+    torch.cuda.synchronize()
+    for f in range(F):
+        _assert_equal_full(images[roots[f]][f], ones[f], f"frame {f} (root {roots[f]})")
+    for c in comps:
+        c.close()
