@@ -15,6 +15,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <condition_variable>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -22,6 +23,7 @@
 #include <memory>
 #include <mutex>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include "comm.h"
@@ -159,12 +161,25 @@ struct Layout {
 };
 
 // VDI_FLAG_LOOPBACK: contexts of one process that form one group, keyed by
-// the 128-byte id; members publish their window base pointers here
+// the 128-byte id; members publish their window base pointers here.  The
+// ranks of a loopback group are threads of one process sharing a device, and
+// kernels that spin on each other must not share a device (nothing guarantees
+// they run concurrently): a loopback rank instead waits on the HOST until the
+// producer has enqueued its side (an event per (kind, producer, consumer,
+// sequence)), makes its stream wait on that event, and then only CHECKS the
+// flag words the device path would have spun on (a check kernel counts
+// shortfalls; vdi_get_counters reports them).
 struct LoopGroup {
   std::vector<char*> base;
+  std::mutex mu;
+  std::condition_variable cv;
+  std::map<std::tuple<int, uint32_t, uint32_t, uint32_t>, cudaEvent_t> posted;
+  ~LoopGroup() {
+    for (auto& kv : posted) cudaEventDestroy(kv.second);
+  }
 };
 std::mutex g_loop_mu;
-std::map<std::string, LoopGroup> g_loop;
+std::map<std::string, std::shared_ptr<LoopGroup>> g_loop;
 
 }  // namespace
 
@@ -183,6 +198,7 @@ struct vdi_ctx {
   std::vector<char*> peer;  // window base of every rank (own included)
   bool peers_ready = false;
   std::string loop_key;
+  std::shared_ptr<LoopGroup> grp;  // VDI_FLAG_LOOPBACK
   std::vector<void*> ipc_opened;
   uint32_t xcalls = 0;               // exchange calls so far (epoch)
   std::vector<uint32_t> gcalls_to;   // gathers to each root so far
@@ -249,9 +265,12 @@ struct vdi_ctx {
       std::lock_guard<std::mutex> lk(g_loop_mu);
       auto it = g_loop.find(loop_key);
       if (it != g_loop.end()) {
-        it->second.base[cfg.rank] = nullptr;
+        {
+          std::lock_guard<std::mutex> lk2(it->second->mu);
+          it->second->base[cfg.rank] = nullptr;
+        }
         bool any = false;
-        for (char* b : it->second.base) any |= b != nullptr;
+        for (char* b : it->second->base) any |= b != nullptr;
         if (!any) g_loop.erase(it);
       }
     }
@@ -297,9 +316,11 @@ vdi_status resolve_peers(vdi_ctx* ctx) {
   std::lock_guard<std::mutex> lk(g_loop_mu);
   auto it = g_loop.find(ctx->loop_key);
   if (it == g_loop.end()) return fail(VDI_ERR_STATE, "loopback group vanished");
+  std::lock_guard<std::mutex> lk2(it->second->mu);
   for (uint32_t r = 0; r < ctx->cfg.n_ranks; ++r)
-    if (!it->second.base[r]) return fail(VDI_ERR_STATE, "loopback group incomplete: rank %u not initialised", r);
-  ctx->peer = it->second.base;
+    if (!it->second->base[r]) return fail(VDI_ERR_STATE, "loopback group incomplete: rank %u not initialised", r);
+  ctx->peer = it->second->base;
+  ctx->grp = it->second;
   ctx->peers_ready = true;
   return VDI_OK;
 }
@@ -563,14 +584,16 @@ vdi_status vdi_composite_init(const vdi_config* cfg, vdi_ctx** out) {
       });
       ctx->loop_key.assign(reinterpret_cast<const char*>(cfg->nccl_unique_id), 128);
       std::lock_guard<std::mutex> lk(g_loop_mu);
-      LoopGroup& grp = g_loop[ctx->loop_key];
-      if (grp.base.empty()) grp.base.assign(G, nullptr);
-      if (grp.base.size() != G || grp.base[me]) {
+      std::shared_ptr<LoopGroup>& grp = g_loop[ctx->loop_key];
+      if (!grp) grp = std::make_shared<LoopGroup>();
+      std::lock_guard<std::mutex> lk2(grp->mu);
+      if (grp->base.empty()) grp->base.assign(G, nullptr);
+      if (grp->base.size() != G || grp->base[me]) {
         ctx->loop_key.clear();
         delete ctx;
         return fail(VDI_ERR_INVALID_ARG, "loopback group: rank %u registered twice or n_ranks differs", me);
       }
-      grp.base[me] = ctx->win.as<char>();
+      grp->base[me] = ctx->win.as<char>();
     } else {
       ncclUniqueId id;
       memcpy(&id, cfg->nccl_unique_id, sizeof id);
@@ -641,6 +664,7 @@ vdi_status vdi_composite_init(const vdi_config* cfg, vdi_ctx** out) {
     if (e2 == cudaSuccess)
       s = reserve_merge(ctx, ctx->P, std::min<uint64_t>((uint64_t)cfg->n_pes * ctx->P * cfg->k_in, (uint64_t)cfg->n_pes * ctx->P * 2),
                         cfg->n_pes * cfg->k_in);
+    if (e2 == cudaSuccess) e2 = cudaMemset(ctx->ccnt.p, 0, 64);  // [2]: loopback check shortfalls (never reset)
     if (e2 != cudaSuccess || s != VDI_OK) {
       delete ctx;
       return e2 != cudaSuccess ? fail(VDI_ERR_OUT_OF_MEMORY, "reserve: %s", cudaGetErrorString(e2)) : s;
@@ -781,29 +805,68 @@ static vdi_status check_local(vdi_ctx* ctx, const vdi_dense_view* local, uint32_
   return VDI_OK;
 }
 
-// block until the flags reach their targets (one-CTA spin kernel on the stream)
-static vdi_status wait_flags(vdi_ctx* ctx, int kind, const std::vector<std::pair<uint32_t, uint32_t>>& who_target,
-                             cudaStream_t st = nullptr) {
+// loopback: publish "this rank's side of (kind, seq) is enqueued" to each consumer
+static vdi_status loop_post(vdi_ctx* ctx, int kind, const std::vector<uint32_t>& consumers, uint32_t seq,
+                            cudaStream_t st) {
+  for (uint32_t c : consumers) {
+    cudaEvent_t ev;
+    CUDA_TRY(ctx, cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    CUDA_TRY(ctx, cudaEventRecord(ev, st));
+    std::lock_guard<std::mutex> lk(ctx->grp->mu);
+    ctx->grp->posted[std::make_tuple(kind, ctx->cfg.rank, c, seq)] = ev;
+  }
+  ctx->grp->cv.notify_all();
+  return VDI_OK;
+}
+
+// A wait of the device path: each entry = (peer rank, flag target, sequence).
+// Multi-GPU: one-CTA spin kernel until the flag words reach their targets.
+// Loopback: the host waits until each peer has posted (kind, seq), the
+// stream waits on the posted event, and a check kernel verifies the flags.
+struct WaitOn {
+  uint32_t rank, target, seq;
+};
+static vdi_status wait_flags(vdi_ctx* ctx, int kind, const std::vector<WaitOn>& who, cudaStream_t st = nullptr) {
+  if (!st) st = ctx->stream;
   WaitArgs w{};
-  for (auto& [r, t] : who_target) {
-    w.addr[w.n] = flag_at(ctx->peer[ctx->cfg.rank], kind, r);
-    w.target[w.n] = t;
+  for (const WaitOn& x : who) {
+    w.addr[w.n] = flag_at(ctx->peer[ctx->cfg.rank], kind, x.rank);
+    w.target[w.n] = x.target;
     ++w.n;
   }
-  CUDA_TRY(ctx, launch_wait(w, st ? st : ctx->stream));
+  if (!ctx->grp) {
+    CUDA_TRY(ctx, launch_wait(w, st));
+    return VDI_OK;
+  }
+  for (const WaitOn& x : who) {
+    cudaEvent_t ev;
+    {
+      std::unique_lock<std::mutex> lk(ctx->grp->mu);
+      const auto key = std::make_tuple(kind, x.rank, ctx->cfg.rank, x.seq);
+      ctx->grp->cv.wait(lk, [&] { return ctx->grp->posted.count(key) > 0; });
+      ev = ctx->grp->posted[key];
+      ctx->grp->posted.erase(key);
+    }
+    CUDA_TRY(ctx, cudaStreamWaitEvent(st, ev, 0));
+    CUDA_TRY(ctx, cudaEventDestroy(ev));
+  }
+  CUDA_TRY(ctx, launch_check(w, ctx->ccnt.as<unsigned long long>() + 2, st));
   return VDI_OK;
 }
 
 // release store of `value` into flag word (kind, me) of each listed peer
+// (loopback: and post (kind, seq) to them)
 static vdi_status signal_peers(vdi_ctx* ctx, int kind, const std::vector<uint32_t>& peers, uint32_t value,
-                               cudaStream_t st = nullptr) {
+                               cudaStream_t st = nullptr, uint32_t seq = 0) {
+  if (!st) st = ctx->stream;
   SignalArgs s{};
   for (uint32_t r : peers) {
     s.addr[s.n] = flag_at(ctx->peer[r], kind, ctx->cfg.rank);
     s.value[s.n] = value;
     ++s.n;
   }
-  CUDA_TRY(ctx, launch_signal(s, st ? st : ctx->stream));
+  CUDA_TRY(ctx, launch_signal(s, st));
+  if (ctx->grp) return loop_post(ctx, kind, peers, seq, st);
   return VDI_OK;
 }
 
@@ -871,9 +934,10 @@ static vdi_status exchange(vdi_ctx* ctx, const vdi_dense_view* local, const vdi_
       if (n_local) dests.push_back(g);
       if (L.n_local(g)) senders.push_back(g);
     }
-  if (n_local && e > 2) {
-    std::vector<std::pair<uint32_t, uint32_t>> wt;
-    for (uint32_t g : dests) wt.push_back({g, e - 2});
+  // (loopback: the receiver's merge of the previous call, posted as seq e - 1)
+  if (n_local && e > (ctx->grp ? 1u : 2u)) {
+    std::vector<WaitOn> wt;
+    for (uint32_t g : dests) wt.push_back({g, e - 2, e - 1});
     if (vdi_status s = wait_flags(ctx, XFREE, wt)) return s;
     ++launches;
   }
@@ -915,14 +979,16 @@ static vdi_status exchange(vdi_ctx* ctx, const vdi_dense_view* local, const vdi_
                                   st));
     CUDA_TRY(ctx, launch_push(ctx->segbuf.as<PushSeg>(), (uint32_t)segs.size(), push_blocks(n_local, G), st));
     ++launches;
+    if (ctx->grp)
+      if (vdi_status s = loop_post(ctx, XREADY, dests, e, st)) return s;
   }
   // a3/a5: the remote PEs' slices of this strip have landed once every
   // sender's counter reaches (calls) x (its blocks per call)
   if (!senders.empty()) {
-    std::vector<std::pair<uint32_t, uint32_t>> wt;
+    std::vector<WaitOn> wt;
     for (uint32_t s : senders) {
       const uint32_t nl = L.n_local(s);
-      wt.push_back({s, e * nl * push_blocks(nl, G)});
+      wt.push_back({s, e * nl * push_blocks(nl, G), e});
     }
     if (vdi_status s = wait_flags(ctx, XREADY, wt)) return s;
     ++launches;
@@ -958,7 +1024,7 @@ static vdi_status release_slots(vdi_ctx* ctx, int& launches) {
   for (uint32_t g = 0; g < ctx->cfg.n_ranks; ++g)
     if (g != ctx->cfg.rank && ctx->lay.n_local(g)) senders.push_back(g);
   if (senders.empty()) return VDI_OK;
-  if (vdi_status s = signal_peers(ctx, XFREE, senders, ctx->xcalls)) return s;
+  if (vdi_status s = signal_peers(ctx, XFREE, senders, ctx->xcalls, nullptr, ctx->xcalls)) return s;
   ++launches;
   return VDI_OK;
 }
@@ -1145,8 +1211,8 @@ static vdi_status gather_send(vdi_ctx* ctx, const vdi_full_view* strip, uint32_t
   const uint32_t me = ctx->cfg.rank, W = ctx->cfg.width, k = ctx->cfg.k_out;
   char* gp = ctx->peer[R] + L.g_off(R, j & 1);
   CUDA_TRY(ctx, cudaMemsetAsync(ctx->ccnt.as<unsigned long long>() + 1, 0, 8, st));
-  if (j > 2) {  // the root has inflated this buffer's previous contents
-    if (vdi_status s = wait_flags(ctx, GFREE, {{R, j - 2}}, st)) return s;
+  if (j > (ctx->grp ? 1u : 2u)) {  // the root has inflated this buffer's previous contents
+    if (vdi_status s = wait_flags(ctx, GFREE, {{R, j - 2, j - 1}}, st)) return s;
     ++launches;
   }
   const uint32_t P = (uint32_t)ctx->P, ng = (P + 31) / 32;
@@ -1173,6 +1239,7 @@ static vdi_status gather_send(vdi_ctx* ctx, const vdi_full_view* strip, uint32_t
   a.flag = flag_at(ctx->peer[R], GREADY, me);
   CUDA_TRY(ctx, launch_compact_push(a, compact_push_blocks(P), st));
   ++launches;
+  if (ctx->grp) return loop_post(ctx, GREADY, {R}, j, st);
   return VDI_OK;
 }
 
@@ -1183,9 +1250,9 @@ static vdi_status gather_recv(vdi_ctx* ctx, vdi_full_view* image, uint32_t j, cu
   const Layout& L = ctx->lay;
   const uint32_t G = ctx->cfg.n_ranks, R = ctx->cfg.rank, W = ctx->cfg.width, k = ctx->cfg.k_out;
   char* gp = ctx->peer[R] + L.g_off(R, j & 1);
-  std::vector<std::pair<uint32_t, uint32_t>> wt;
+  std::vector<WaitOn> wt;
   for (uint32_t g = 0; g < G; ++g)
-    if (g != R) wt.push_back({g, j * compact_push_blocks(L.rows(g) * W)});
+    if (g != R) wt.push_back({g, j * compact_push_blocks(L.rows(g) * W), j});
   if (vdi_status s = wait_flags(ctx, GREADY, wt, st)) return s;
   ++launches;
   const uint8_t* gc = reinterpret_cast<const uint8_t*>(gp + L.g_count_off());
@@ -1208,7 +1275,7 @@ static vdi_status gather_recv(vdi_ctx* ctx, vdi_full_view* image, uint32_t j, cu
   std::vector<uint32_t> others;
   for (uint32_t g = 0; g < G; ++g)
     if (g != R) others.push_back(g);
-  if (vdi_status s = signal_peers(ctx, GFREE, others, j, st)) return s;
+  if (vdi_status s = signal_peers(ctx, GFREE, others, j, st, j)) return s;
   ++launches;
   return VDI_OK;
 }
@@ -1659,8 +1726,8 @@ vdi_status vdi_get_counters(vdi_ctx* ctx, vdi_counters* out) {
   const Layout& L = ctx->lay;
   DevCounters h{};
   if (ctx->dcnt.p) CUDA_TRY(ctx, cudaMemcpyAsync(&h, ctx->dcnt.p, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
-  unsigned long long cc[2] = {0, 0};
-  if (ctx->ccnt.p) CUDA_TRY(ctx, cudaMemcpyAsync(cc, ctx->ccnt.p, 16, cudaMemcpyDeviceToHost, ctx->stream));
+  unsigned long long cc[3] = {0, 0, 0};
+  if (ctx->ccnt.p) CUDA_TRY(ctx, cudaMemcpyAsync(cc, ctx->ccnt.p, 24, cudaMemcpyDeviceToHost, ctx->stream));
   // records received in the last exchange (slot headers) and, at the root,
   // in the last gather (region headers)
   const uint32_t G = cf.n_ranks, me = cf.rank;
@@ -1681,6 +1748,7 @@ vdi_status vdi_get_counters(vdi_ctx* ctx, vdi_counters* out) {
   }
   CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
   if (h.err & 1) return fail(VDI_ERR_INTERNAL, "merge work-list overflow");
+  if (cc[2]) return fail(VDI_ERR_INTERNAL, "loopback: %llu flag words short of their targets", cc[2]);
   ctx->last.records_in = h.records_in;
   ctx->last.records_search = h.records_search;
   ctx->last.searched_lists = 0;

@@ -196,6 +196,13 @@ __global__ void wait_kernel(WaitArgs a) {
   __syncthreads();
 }
 
+// loopback: the flags must already be at their targets (the stream waited on
+// the producers' events); count the shortfalls
+__global__ void check_kernel(WaitArgs a, unsigned long long* fails) {
+  const int t = threadIdx.x;
+  if (t < a.n && (int32_t)(ld_acquire_sys(a.addr[t]) - a.target[t]) < 0) atomicAdd(fails, 1ull);
+}
+
 __global__ void signal_kernel(SignalArgs a) {
   const int t = threadIdx.x;
   if (t < a.n) {
@@ -228,6 +235,12 @@ cudaError_t launch_wait(const WaitArgs& a, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+cudaError_t launch_check(const WaitArgs& a, unsigned long long* fails, cudaStream_t st) {
+  if (!a.n) return cudaSuccess;
+  check_kernel<<<1, 64, 0, st>>>(a, fails);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_signal(const SignalArgs& a, cudaStream_t st) {
   if (!a.n) return cudaSuccess;
   signal_kernel<<<1, 64, 0, st>>>(a);
@@ -241,6 +254,7 @@ cudaError_t preload_comm() {
   cudaFuncGetAttributes(&fa, compact_push_kernel);
   cudaFuncGetAttributes(&fa, wait_kernel);
   cudaFuncGetAttributes(&fa, signal_kernel);
+  cudaFuncGetAttributes(&fa, check_kernel);
   return cudaGetLastError();
 }
 

@@ -76,6 +76,7 @@ cudaError_t launch_push(const PushSeg* dsegs, uint32_t n_segs, uint32_t blocks_p
 cudaError_t launch_compact_push(const CompactPushArgs& a, uint32_t blocks, cudaStream_t st);
 cudaError_t launch_wait(const WaitArgs& a, cudaStream_t st);
 cudaError_t launch_signal(const SignalArgs& a, cudaStream_t st);
+cudaError_t launch_check(const WaitArgs& a, unsigned long long* fails, cudaStream_t st);
 cudaError_t preload_comm();   // load the comm kernels now (see preload_merge)
 
 // blocks of the gather compaction of a P-list strip (both ends derive it)

@@ -1,15 +1,17 @@
 """The multi-GPU path (§8(e)) on ONE device.
 
-G contexts of one process form a VDI_FLAG_LOOPBACK group: the same device
-code as G processes on G GPUs -- strip bounds found on the device, the push of
-every (PE, strip) slice into the owner's window, block-counted ready flags,
-the receive-side scan and merge, the compaction of each strip into the root's
-window and the root's inflate -- with the window pointers exchanged in-process
-instead of by NCCL + CUDA IPC.  Each context has its own stream; the host
-enqueues all ranks' calls without blocking (the ranks wait for each other on
-the device).  Results are compared with the oracle's direct-send composite
-(orc.composite(..., G): strips, simulated exchange, gather) element by
-element and with the one-context image bit for bit; exchange bytes are
+G contexts of one process form a VDI_FLAG_LOOPBACK group, each rank driven by
+its own host thread with its own stream: the same device code as G processes
+on G GPUs -- strip bounds found on the device, the push of every (PE, strip)
+slice into the owner's window, block-counted ready flags, the receive-side
+scan and merge, the compaction of each strip into the root's window and the
+root's inflate -- with the window pointers exchanged in-process instead of by
+NCCL + CUDA IPC.  Kernels that spin on each other must not share a device
+(B200_PROFILING.md), so a loopback rank waits for its peers on the host
+(events) and only checks the flag words on the device (shortfalls fail
+vdi_get_counters).  Results are compared with the oracle's direct-send
+composite (orc.composite(..., G): strips, simulated exchange, gather) element
+by element and with the one-context image bit for bit; exchange bytes are
 checked for conservation against the seeded inputs."""
 import os
 import threading
@@ -55,12 +57,30 @@ def _local(vdi, comps, pes_dev, r):
     return [pes_dev[s] for s in range(n) if vdi.pe_home(n, len(comps), s) == r]
 
 
+def _threads(fns):
+    """Run fns[r] (rank r's calls) in one host thread per rank; re-raise errors."""
+    errors = []
+
+    def wrap(f):
+        try:
+            f()
+        except Exception as e:  # noqa: BLE001 -- surfaced below
+            errors.append(e)
+    th = [threading.Thread(target=wrap, args=(f,)) for f in fns]
+    [t.start() for t in th]
+    [t.join(timeout=300) for t in th]
+    assert not any(t.is_alive() for t in th), "a loopback rank did not finish"
+    assert not errors, errors
+
+
 def _run(vdi, comps, pes_dev, root, images, strips):
-    """All ranks' composite, then all ranks' gather; nothing blocks the host."""
-    for r, c in enumerate(comps):
-        c.composite(_local(vdi, comps, pes_dev, r), strips[r])
-    for r, c in enumerate(comps):
-        c.gather(strips[r], images if r == root else None, root=root)
+    """Every rank (thread): composite of its strip, then the gather to root."""
+    def rank(r, c):
+        def f():
+            c.composite(_local(vdi, comps, pes_dev, r), strips[r])
+            c.gather(strips[r], images if r == root else None, root=root)
+        return f
+    _threads([rank(r, c) for r, c in enumerate(comps)])
 
 
 def _assert_equal_full(a, b, what):
@@ -136,14 +156,16 @@ def test_loopback_frames_rotating_root(vdi, orc):
         dev = [dense_to_device(p, i) for i, p in enumerate(pes)]
         frames.append((pes, dev))
         ones.append(_one_gpu(vdi, dev, W, H, k, k)[0])
-    for f, (pes, dev) in enumerate(frames):
-        # a fresh strip per frame: a rank's next composite may start before
-        # the root has read its previous strip only through the gather
-        # window, never the strip buffer itself -- reuse is safe; fresh ones
-        # make the test independent of that
-        strips = [c.empty_strip() for c in comps]
-        images.append(vdi.FullVDI.empty(W, 0, H, k))
-        _run(vdi, comps, dev, f % G, images[-1], strips)
+    images = [vdi.FullVDI.empty(W, 0, H, k) for _ in frames]
+    torch.cuda.synchronize()
+
+    def rank(r, c):
+        def f():  # all five frames back to back, no host synchronisation between them
+            for fi, (pes, dev) in enumerate(frames):
+                c.composite(_local(vdi, comps, dev, r), strips[r])
+                c.gather(strips[r], images[fi] if r == fi % G else None, root=fi % G)
+        return f
+    _threads([rank(r, c) for r, c in enumerate(comps)])
     torch.cuda.synchronize()
     for f in range(5):
         _assert_equal_full(images[f], ones[f], f"frame {f}")
@@ -167,17 +189,13 @@ def test_loopback_fullrep(vdi, orc):
     torch.cuda.synchronize()
     strips = [c.empty_strip() for c in comps]
     image = vdi.FullVDI.empty(W, 0, H, k_out)
-    # composite_fullrep synchronises its host once (the compaction total), so
-    # the ranks run in threads
     def rank(r):
-        ids = [s for s in range(n) if vdi.pe_home(n, G, s) == r]
-        with torch.cuda.stream(comps[r].stream):
+        def f():
+            ids = [s for s in range(n) if vdi.pe_home(n, G, s) == r]
             comps[r].composite_fullrep([fulls[s] for s in ids], ids, strips[r])
-    th = [threading.Thread(target=rank, args=(r,)) for r in range(G)]
-    [t.start() for t in th]
-    [t.join() for t in th]
-    for r, c in enumerate(comps):
-        c.gather(strips[r], image if r == 0 else None)
+            comps[r].gather(strips[r], image if r == 0 else None)
+        return f
+    _threads([rank(r) for r in range(G)])
     torch.cuda.synchronize()
     _assert_equal_full(image, one, "fullrep G=2")
     for c in comps:
@@ -231,15 +249,12 @@ def test_loopback_host_entries(vdi, span):
             P = (comps[r].row_end - comps[r].row_begin) * W
             outs = [(torch.empty(P, dtype=torch.uint8), torch.empty((P * k, 2), dtype=torch.float32),
                      torch.empty((P * k, 4), dtype=torch.float32)) for _ in order]
-            with torch.cuda.stream(comps[r].stream):
-                Ts = comps[r].composite_host_dense_frames(frames, outs)
+            Ts = comps[r].composite_host_dense_frames(frames, outs)
             results[r] = (Ts, outs)
         except Exception as e:  # surfaced below
             errors.append(e)
 
-    th = [threading.Thread(target=rank, args=(r,)) for r in range(G)]
-    [t.start() for t in th]
-    [t.join() for t in th]
+    _threads([(lambda r=r: rank(r)) for r in range(G)])
     assert not errors, errors
     for r, c in enumerate(comps):
         Ts, outs = results[r]
@@ -272,8 +287,8 @@ def test_loopback_composite_frames(vdi, rotate):
     roots = [f % G if rotate else 0 for f in range(F)]
     images = {r: [vdi.FullVDI.empty(W, 0, H, k) if roots[f] == r else None for f in range(F)] for r in range(G)}
     torch.cuda.synchronize()
-    for r, c in enumerate(comps):
-        c.composite_frames([_local(vdi, comps, fr, r) for fr in frames], images[r], roots=roots)
+    _threads([(lambda r=r, c=c: c.composite_frames([_local(vdi, comps, fr, r) for fr in frames], images[r],
+                                                   roots=roots)) for r, c in enumerate(comps)])
     torch.cuda.synchronize()
     for f in range(F):
         _assert_equal_full(images[roots[f]][f], ones[f], f"frame {f} (root {roots[f]})")
