@@ -120,10 +120,11 @@ struct Layout {
     for (uint32_t s = 0; s < n; ++s) c += home(s) == r;
     return c;
   }
-  // receive slot of PE s at rank r: header | count [P_r] | depth [P_r k_in] | rgba [P_r k_in]
+  // receive slot of PE s at rank r: header | count [P_r] | group bases [P_r/32 + 1] |
+  // depth [P_r k_in] | rgba [P_r k_in]
   size_t slot_bytes(uint32_t r) const {
     const size_t P = (size_t)rows(r) * W;
-    return 256 + al256(P) + al256(P * k_in * 8) + al256(P * k_in * 16);
+    return 256 + al256(P) + al256(((P + 31) / 32 + 1) * 4) + al256(P * k_in * 8) + al256(P * k_in * 16);
   }
   uint32_t slot_index(uint32_t s, uint32_t r) const {  // PEs homed elsewhere, in PE order
     uint32_t j = 0;
@@ -159,6 +160,28 @@ struct Layout {
     return o;
   }
 };
+
+// the arrays of a receive slot of P lists (see Layout::slot_bytes)
+struct Slot {
+  unsigned long long* hdr;
+  uint8_t* count;
+  uint32_t* gbase;
+  float2* depth;
+  float4* rgba;
+};
+inline Slot slot_at(char* p, size_t P, uint32_t k_in) {
+  Slot sl;
+  sl.hdr = reinterpret_cast<unsigned long long*>(p);
+  p += 256;
+  sl.count = reinterpret_cast<uint8_t*>(p);
+  p += al256(P);
+  sl.gbase = reinterpret_cast<uint32_t*>(p);
+  p += al256(((P + 31) / 32 + 1) * 4);
+  sl.depth = reinterpret_cast<float2*>(p);
+  p += al256(P * k_in * 8);
+  sl.rgba = reinterpret_cast<float4*>(p);
+  return sl;
+}
 
 // VDI_FLAG_LOOPBACK: contexts of one process that form one group, keyed by
 // the 128-byte id; members publish their window base pointers here.  The
@@ -203,6 +226,11 @@ struct vdi_ctx {
   uint32_t xcalls = 0;               // exchange calls so far (epoch)
   std::vector<uint32_t> gcalls_to;   // gathers to each root so far
   DevBuf bnd, srcbase, segbuf, ccnt, gsum, gbase_loc;
+  DevBuf gsum_x, gbase_x;                // exchange: scan of the local PEs' counts (2 parities)
+  cudaEvent_t xev_bounds[2] = {}, xev_merged[2] = {};
+  cudaStream_t xst = nullptr;            // vdi_composite_frames: the push stream
+  cudaStream_t xpst = nullptr;           // push stream of the current call (null: the ctx stream)
+  int xpar = 0;                          // parity of the exchange buffers of the current call
   // merge scratch
   DevBuf group_sum, group_base, wl, scratch, dcnt, stat_gamma, stat_m, stat_margin, srch, slots;
   DevBuf lpool, lbatch;
@@ -238,6 +266,14 @@ struct vdi_ctx {
   cudaEvent_t gev_in = nullptr, gev_out = nullptr;
   DevBuf fs_count[2], fs_depth[2], fs_rgba[2];
   ~vdi_ctx() {
+    if (xst) {
+      cudaStreamSynchronize(xst);
+      cudaStreamDestroy(xst);
+    }
+    for (int i = 0; i < 2; ++i) {
+      if (xev_bounds[i]) cudaEventDestroy(xev_bounds[i]);
+      if (xev_merged[i]) cudaEventDestroy(xev_merged[i]);
+    }
     if (gst) {
       cudaStreamSynchronize(gst);
       cudaStreamDestroy(gst);
@@ -431,7 +467,9 @@ static vdi_status merge_lists(vdi_ctx* ctx, MergeParams& mp, uint64_t P, uint64_
   mp.wl_count = dc->wl_count;
   mp.search_ticket = dc->search_ticket;
   if (P) {
-    if (!mp.src[0].offset)
+    bool scan = false;  // some source has neither an offset array nor group bases: receive-side scan
+    for (uint32_t s = 0; s < n; ++s) scan |= !mp.src[s].offset && !mp.src[s].gbase;
+    if (scan)
       CUDA_TRY(ctx, launch_scan(mp, ctx->group_sum.as<uint32_t>(), ctx->group_base.as<uint32_t>(), st, &launches));
     if (timing) CUDA_TRY(ctx, cudaEventRecord(ctx->ev[3], st));
     // pass-through (writes every slot of the strip) -> search kernels -> general path
@@ -654,13 +692,18 @@ vdi_status vdi_composite_init(const vdi_config* cfg, vdi_ctx** out) {
     cudaError_t e2 = cudaSuccess;
     for (auto [b, need] : std::initializer_list<std::pair<DevBuf*, size_t>>{
              {&ctx->ccnt, 64},
-             {&ctx->srcbase, (size_t)cfg->n_pes * 4 + 64},
+             {&ctx->srcbase, 2 * VDI_MAX_SRC * 4 + 64},
              {&ctx->bnd, (size_t)std::max<uint32_t>(nl, 1) * (G + 1) * 8 + 64},
-             {&ctx->segbuf, (size_t)std::max<uint32_t>(nl, 1) * G * sizeof(PushSeg)},
-             {&ctx->gsum, std::max<size_t>((size_t)scan_chunks((uint32_t)Pimg) * std::max<uint32_t>(nl, 1),
-                                           scan_chunks((uint32_t)ctx->P) + 8) * 4 + 64},
-             {&ctx->gbase_loc, std::max<size_t>((Pimg + 31) / 32 * std::max<uint32_t>(nl, 1), ngs + 8) * 4 + 64}})
+             {&ctx->segbuf, (size_t)2 * VDI_MAX_SRC * VDI_MAX_RANKS * sizeof(PushSeg)},
+             {&ctx->gsum, ((size_t)scan_chunks((uint32_t)ctx->P) + 8) * 4 + 64},
+             {&ctx->gbase_loc, (ngs + 8) * 4 + 64},
+             {&ctx->gsum_x, (size_t)scan_chunks((uint32_t)Pimg) * std::max<uint32_t>(nl, 1) * 4 + 64},
+             {&ctx->gbase_x, 2 * ((Pimg + 31) / 32) * std::max<uint32_t>(nl, 1) * 4 + 64}})
       if (e2 == cudaSuccess) e2 = b->grow(need);
+    for (int i = 0; i < 2 && e2 == cudaSuccess; ++i) {
+      e2 = cudaEventCreateWithFlags(&ctx->xev_bounds[i], cudaEventDisableTiming);
+      if (e2 == cudaSuccess) e2 = cudaEventCreateWithFlags(&ctx->xev_merged[i], cudaEventDisableTiming);
+    }
     if (e2 == cudaSuccess)
       s = reserve_merge(ctx, ctx->P, std::min<uint64_t>((uint64_t)cfg->n_pes * ctx->P * cfg->k_in, (uint64_t)cfg->n_pes * ctx->P * 2),
                         cfg->n_pes * cfg->k_in);
@@ -870,75 +913,76 @@ static vdi_status signal_peers(vdi_ctx* ctx, int kind, const std::vector<uint32_
   return VDI_OK;
 }
 
-// Exchange (a2-a5) of the sub-VDIs of this rank's PEs: the
-// (PE, strip) slices are pushed into the strip owners' windows and the
-// remote PEs' slices of this rank's strip are awaited.  dense: `local` are
-// dense views (slices [offset[row_g W], offset[row_{g+1} W]) found on the
-// device); full (vdi_composite_fullrep): `flocal` are full representations
-// (fixed-size slices).  Sets mp.src / mp.src_base for every PE.
-static vdi_status exchange(vdi_ctx* ctx, const vdi_dense_view* local, const vdi_full_view* flocal, uint32_t n_local,
-                           const std::vector<int>& slot, const uint32_t* full_ids, MergeParams& mp, int& launches) {
+// Exchange (a2-a5), sending half: the strip bounds of this
+// rank's PEs (on the device) and the push of every (local PE, strip g != me)
+// slice -- counts, the 32-list group bases of the slice (so the receiver
+// needs no scan; strips starting on 32-list boundaries) and the packed
+// records -- into g's window, once g has released the slot of the same
+// parity.  dense: `local` are dense views (slices [offset[row_g W],
+// offset[row_{g+1} W]) found on the device); full (vdi_composite_fullrep):
+// `flocal` are full representations (fixed-size slices).  Runs on stream pst;
+// the device arrays the merge will read (local group bases / strip starts)
+// are double-buffered by `par` and ready at event ctx->xev_bounds[par].
+// Returns the call's epoch in *epoch.
+static vdi_status exchange_push(vdi_ctx* ctx, const vdi_dense_view* local, const vdi_full_view* flocal,
+                                uint32_t n_local, const uint32_t* full_ids, int& launches, cudaStream_t pst, int par,
+                                uint32_t* epoch) {
   const vdi_config& cf = ctx->cfg;
   const Layout& L = ctx->lay;
   const uint32_t G = cf.n_ranks, me = cf.rank, n = cf.n_pes, W = cf.width, K = cf.k_in;
-  cudaStream_t st = ctx->stream;
   if (vdi_status s = resolve_peers(ctx)) return s;
   const uint32_t e = ++ctx->xcalls, q = e & 1;
-  CUDA_TRY(ctx, ctx->ccnt.grow(64));
-  CUDA_TRY(ctx, cudaMemsetAsync(ctx->ccnt.p, 0, 8, st));
-  CUDA_TRY(ctx, ctx->srcbase.grow((size_t)n * 4 + 64));
-  CUDA_TRY(ctx, cudaMemsetAsync(ctx->srcbase.p, 0, (size_t)n * 4, st));
-  unsigned long long* bnd = nullptr;
+  *epoch = e;
+  const uint64_t Pimg = (uint64_t)W * cf.height;
+  const uint32_t ngimg = (uint32_t)((Pimg + 31) / 32);
+  const bool aligned = L.aligned();
+  CUDA_TRY(ctx, cudaMemsetAsync(ctx->ccnt.p, 0, 8, pst));
+  CUDA_TRY(ctx, cudaMemsetAsync(ctx->srcbase.as<uint32_t>() + (size_t)par * VDI_MAX_SRC, 0, (size_t)n * 4, pst));
+  unsigned long long* bnd = ctx->bnd.as<unsigned long long>();
+  const uint32_t* gb32 = nullptr;  // the local PEs' 32-list group bases from the image start (no offset arrays)
   if (!flocal && n_local) {
     // a2: strip bounds of the local PEs on the device
     BoundsArgs ba{};
-    const uint64_t Pimg = (uint64_t)W * cf.height;
     bool all_off = true;
     for (uint32_t l = 0; l < n_local; ++l) all_off &= local[l].offset != nullptr;
     if (!all_off) {  // scan of the counts (no offset arrays, e.g. the host entry points)
       MergeParams ms{};
       ms.n_src = (int)n_local;
       ms.P = (uint32_t)Pimg;
-      ms.n_groups = (uint32_t)((Pimg + 31) / 32);
+      ms.n_groups = ngimg;
       for (uint32_t l = 0; l < n_local; ++l) ms.src[l].count = local[l].count;
-      CUDA_TRY(ctx, ctx->gsum.grow((size_t)scan_chunks(ms.P) * n_local * 4 + 64));
-      CUDA_TRY(ctx, ctx->gbase_loc.grow((size_t)ms.n_groups * n_local * 4 + 64));
-      CUDA_TRY(ctx, launch_scan(ms, ctx->gsum.as<uint32_t>(), ctx->gbase_loc.as<uint32_t>(), st, &launches));
-      ba.gbase = ctx->gbase_loc.as<uint32_t>();
+      uint32_t* gbx = ctx->gbase_x.as<uint32_t>() + (size_t)par * n_local * ngimg;
+      CUDA_TRY(ctx, launch_scan(ms, ctx->gsum_x.as<uint32_t>(), gbx, pst, &launches));
+      ba.gbase = gbx;
+      gb32 = gbx;
     }
     for (uint32_t l = 0; l < n_local; ++l) {
       ba.offset[l] = local[l].offset;
       ba.count[l] = local[l].count;
       ba.total[l] = local[l].total;
+      ba.pe[l] = local[l].pe_id;
     }
     for (uint32_t g = 0; g <= G; ++g) ba.rows[g] = strip_row(cf.height, G, g);
-    ba.n_groups = (uint32_t)((Pimg + 31) / 32);
+    ba.n_groups = ngimg;
     ba.W = W;
     ba.n_local = (int)n_local;
     ba.G = (int)G;
-    CUDA_TRY(ctx, ctx->bnd.grow((size_t)n_local * (G + 1) * 8 + 64));
-    bnd = ctx->bnd.as<unsigned long long>();
     ba.bnd = bnd;
     // the merge reads its own strip of the local PEs in place: src_base = bnd[l][me]
-    ba.srcbase = ctx->srcbase.as<uint32_t>();
-    for (uint32_t l = 0; l < n_local; ++l) ba.pe[l] = local[l].pe_id;
+    ba.srcbase = ctx->srcbase.as<uint32_t>() + (size_t)par * VDI_MAX_SRC;
     ba.me = (int)me;
-    CUDA_TRY(ctx, launch_bounds(ba, st));
+    CUDA_TRY(ctx, launch_bounds(ba, pst));
     ++launches;
   }
-  // a4: push every (local PE, strip g != me) slice into g's window, once g has
-  // released the slot of the same parity (its merge two calls ago)
-  std::vector<uint32_t> dests, senders;
+  CUDA_TRY(ctx, cudaEventRecord(ctx->xev_bounds[par], pst));
+  std::vector<uint32_t> dests;
   for (uint32_t g = 0; g < G; ++g)
-    if (g != me) {
-      if (n_local) dests.push_back(g);
-      if (L.n_local(g)) senders.push_back(g);
-    }
+    if (g != me && n_local) dests.push_back(g);
   // (loopback: the receiver's merge of the previous call, posted as seq e - 1)
   if (n_local && e > (ctx->grp ? 1u : 2u)) {
     std::vector<WaitOn> wt;
     for (uint32_t g : dests) wt.push_back({g, e - 2, e - 1});
-    if (vdi_status s = wait_flags(ctx, XFREE, wt)) return s;
+    if (vdi_status s = wait_flags(ctx, XFREE, wt, pst)) return s;
     ++launches;
   }
   std::vector<PushSeg> segs;
@@ -947,7 +991,7 @@ static vdi_status exchange(vdi_ctx* ctx, const vdi_dense_view* local, const vdi_
     for (uint32_t g : dests) {
       const uint32_t a = strip_row(cf.height, G, g), b = strip_row(cf.height, G, g + 1);
       const size_t Pg = (size_t)(b - a) * W;
-      char* slotp = ctx->peer[g] + L.x_off(g, q, pe);
+      const Slot sl = slot_at(ctx->peer[g] + L.x_off(g, q, pe), Pg, K);
       PushSeg sg{};
       if (flocal) {
         const vdi_full_view& v = flocal[l];
@@ -962,59 +1006,85 @@ static vdi_status exchange(vdi_ctx* ctx, const vdi_dense_view* local, const vdi_
         sg.src_depth = reinterpret_cast<const float2*>(v.depth);
         sg.src_rgba = reinterpret_cast<const float4*>(v.rgba);
         sg.bnd = bnd + (size_t)l * (G + 1) + g;
+        if (aligned) {  // the slice's group bases, relative to its first record
+          sg.src_offset = v.offset ? v.offset + (size_t)a * W : nullptr;
+          sg.src_gb32 = v.offset ? nullptr : gb32 + (size_t)l * ngimg + (size_t)a * W / 32;
+          sg.n_groups = (uint32_t)((Pg + 31) / 32);
+          sg.dst_gbase = sl.gbase;
+        }
       }
       sg.n_count = Pg;
-      sg.dst_hdr = reinterpret_cast<unsigned long long*>(slotp);
-      sg.dst_count = reinterpret_cast<uint8_t*>(slotp + 256);
-      sg.dst_depth = reinterpret_cast<float2*>(slotp + 256 + al256(Pg));
-      sg.dst_rgba = reinterpret_cast<float4*>(slotp + 256 + al256(Pg) + al256(Pg * K * 8));
+      sg.dst_hdr = sl.hdr;
+      sg.dst_count = sl.count;
+      sg.dst_depth = sl.depth;
+      sg.dst_rgba = sl.rgba;
       sg.bytes = ctx->ccnt.as<unsigned long long>();
       sg.flag = flag_at(ctx->peer[g], XREADY, me);
       segs.push_back(sg);
     }
   }
   if (!segs.empty()) {
-    CUDA_TRY(ctx, ctx->segbuf.grow(segs.size() * sizeof(PushSeg)));
-    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->segbuf.p, segs.data(), segs.size() * sizeof(PushSeg), cudaMemcpyHostToDevice,
-                                  st));
-    CUDA_TRY(ctx, launch_push(ctx->segbuf.as<PushSeg>(), (uint32_t)segs.size(), push_blocks(n_local, G), st));
+    PushSeg* dsegs = ctx->segbuf.as<PushSeg>() + (size_t)par * VDI_MAX_SRC * VDI_MAX_RANKS;
+    CUDA_TRY(ctx, cudaMemcpyAsync(dsegs, segs.data(), segs.size() * sizeof(PushSeg), cudaMemcpyHostToDevice, pst));
+    CUDA_TRY(ctx, launch_push(dsegs, (uint32_t)segs.size(), push_blocks(n_local, G), pst));
     ++launches;
     if (ctx->grp)
-      if (vdi_status s = loop_post(ctx, XREADY, dests, e, st)) return s;
+      if (vdi_status s = loop_post(ctx, XREADY, dests, e, pst)) return s;
   }
-  // a3/a5: the remote PEs' slices of this strip have landed once every
-  // sender's counter reaches (calls) x (its blocks per call)
-  if (!senders.empty()) {
-    std::vector<WaitOn> wt;
-    for (uint32_t s : senders) {
+  return VDI_OK;
+}
+
+// Exchange, receiving half (stream = the ctx stream): wait until every
+// sender's slices of epoch e have landed, then point the merge's sources at
+// the own PEs (read in place) and the receive slots.  With 32-list aligned
+// strips every source comes with its group bases (offsets, the sender's
+// pushed bases, or the local scan) and the receive-side scan is skipped.
+static vdi_status exchange_recv(vdi_ctx* ctx, const vdi_dense_view* local, const vdi_full_view* flocal,
+                                const std::vector<int>& slot, uint32_t e, int par, MergeParams& mp, int& launches) {
+  const vdi_config& cf = ctx->cfg;
+  const Layout& L = ctx->lay;
+  const uint32_t G = cf.n_ranks, me = cf.rank, n = cf.n_pes, W = cf.width, K = cf.k_in;
+  const uint32_t q = e & 1;
+  const uint64_t Pimg = (uint64_t)W * cf.height;
+  const uint32_t ngimg = (uint32_t)((Pimg + 31) / 32);
+  const bool direct = !flocal && L.aligned();
+  CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->stream, ctx->xev_bounds[par], 0));
+  std::vector<WaitOn> wt;
+  for (uint32_t s = 0; s < G; ++s)
+    if (s != me && L.n_local(s)) {
       const uint32_t nl = L.n_local(s);
       wt.push_back({s, e * nl * push_blocks(nl, G), e});
     }
-    if (vdi_status s = wait_flags(ctx, XREADY, wt)) return s;
+  if (!wt.empty()) {
+    if (vdi_status st = wait_flags(ctx, XREADY, wt)) return st;
     ++launches;
   }
-  // sources of the merge: own PEs in place, remote PEs from the window slots
   const size_t Pm = ctx->P;
+  uint32_t l_of[VDI_MAX_SRC];
+  for (uint32_t s = 0; s < n; ++s) l_of[s] = slot[s] >= 0 ? (uint32_t)slot[s] : 0u;
   for (uint32_t s = 0; s < n; ++s) {
     if (slot[s] >= 0) {
       if (flocal) {
         const vdi_full_view& v = flocal[slot[s]];
         const size_t o = (size_t)ctx->row0 * W;
         mp.src[s] = SrcDesc{v.count + o, reinterpret_cast<const float2*>(v.depth) + o * K,
-                            reinterpret_cast<const float4*>(v.rgba) + o * K, nullptr};
+                            reinterpret_cast<const float4*>(v.rgba) + o * K, nullptr, nullptr};
       } else {
         const vdi_dense_view& v = local[slot[s]];
-        mp.src[s] = SrcDesc{v.count + (size_t)ctx->row0 * W, reinterpret_cast<const float2*>(v.depth),
-                            reinterpret_cast<const float4*>(v.rgba), nullptr};
+        const size_t o = (size_t)ctx->row0 * W;
+        mp.src[s] = SrcDesc{v.count + o, reinterpret_cast<const float2*>(v.depth),
+                            reinterpret_cast<const float4*>(v.rgba), nullptr, nullptr};
+        if (direct) {
+          if (v.offset) mp.src[s].offset = v.offset + o;  // absolute record indices
+          else mp.src[s].gbase = ctx->gbase_x.as<uint32_t>() + ((size_t)par * L.n_local(me) + l_of[s]) * ngimg + o / 32;
+        }
       }
     } else {
-      char* slotp = ctx->peer[me] + L.x_off(me, q, s);
-      mp.src[s] = SrcDesc{reinterpret_cast<const uint8_t*>(slotp + 256),
-                          reinterpret_cast<const float2*>(slotp + 256 + al256(Pm)),
-                          reinterpret_cast<const float4*>(slotp + 256 + al256(Pm) + al256(Pm * K * 8)), nullptr};
+      const Slot sl = slot_at(ctx->peer[me] + L.x_off(me, q, s), Pm, K);
+      mp.src[s] = SrcDesc{sl.count, sl.depth, sl.rgba, nullptr, direct ? sl.gbase : nullptr};
     }
   }
-  mp.src_base = flocal ? nullptr : ctx->srcbase.as<uint32_t>();
+  mp.src_base = flocal ? nullptr : ctx->srcbase.as<uint32_t>() + (size_t)par * VDI_MAX_SRC;
   return VDI_OK;
 }
 
@@ -1066,7 +1136,11 @@ vdi_status vdi_composite(vdi_ctx* ctx, const vdi_dense_view* local, uint32_t n_l
     }
     S_est = S_loc;
   } else {
-    if (vdi_status s = exchange(ctx, local, nullptr, n_local, slot, nullptr, mp, launches)) return s;
+    uint32_t e = 0;
+    if (vdi_status s = exchange_push(ctx, local, nullptr, n_local, nullptr, launches, ctx->xpst ? ctx->xpst : st,
+                                     ctx->xpar, &e))
+      return s;
+    if (vdi_status s = exchange_recv(ctx, local, nullptr, slot, e, ctx->xpar, mp, launches)) return s;
     // the strip's records are known only on the device: size the pools for
     // twice this rank's share of the whole VDI (estimated from the local PEs)
     const uint64_t cap = (uint64_t)n * ctx->P * cf.k_in;
@@ -1074,8 +1148,10 @@ vdi_status vdi_composite(vdi_ctx* ctx, const vdi_dense_view* local, uint32_t n_l
   }
   if (timing) CUDA_TRY(ctx, cudaEventRecord(ctx->ev[1], st));
   if (vdi_status s = merge_lists(ctx, mp, ctx->P, S_est, n * cf.k_in, so, timing, launches)) return s;
-  if (G > 1)
+  if (G > 1) {
+    CUDA_TRY(ctx, cudaEventRecord(ctx->xev_merged[ctx->xpar], st));  // the exchange buffers of this parity are read
     if (vdi_status s = release_slots(ctx, launches)) return s;
+  }
   if (timing) {
     CUDA_TRY(ctx, cudaEventRecord(ctx->ev[2], st));
     ctx->timing_pending = true;
@@ -1144,7 +1220,9 @@ vdi_status vdi_composite_fullrep(vdi_ctx* ctx, const vdi_full_view* local, const
   if (G > 1) {
     // fixed-size slices of the full representation (no size exchange): pushed
     // into the same window slots as the dense exchange
-    if (vdi_status s = exchange(ctx, nullptr, local, n_local, slot, pe_ids, mx, launches)) return s;
+    uint32_t e = 0;
+    if (vdi_status s = exchange_push(ctx, nullptr, local, n_local, pe_ids, launches, st, 0, &e)) return s;
+    if (vdi_status s = exchange_recv(ctx, nullptr, local, slot, e, 0, mx, launches)) return s;
   } else {
     for (uint32_t s = 0; s < n; ++s) {
       const vdi_full_view& v = local[slot[s]];
@@ -1191,8 +1269,10 @@ vdi_status vdi_composite_fullrep(vdi_ctx* ctx, const vdi_full_view* local, const
   CUDA_TRY(ctx, cudaMemcpyAsync(&S_here, dtot, 8, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(ctx, cudaStreamSynchronize(st));
   if (vdi_status e = merge_lists(ctx, mp, Pg, S_here, n * K, so, timing, launches)) return e;
-  if (G > 1)
+  if (G > 1) {
+    CUDA_TRY(ctx, cudaEventRecord(ctx->xev_merged[0], st));
     if (vdi_status s = release_slots(ctx, launches)) return s;
+  }
   if (timing) {
     CUDA_TRY(ctx, cudaEventRecord(ctx->ev[2], st));
     ctx->timing_pending = true;
@@ -1379,6 +1459,7 @@ vdi_status vdi_composite_frames(vdi_ctx* ctx, uint32_t F, const vdi_dense_view* 
   }
   if (vdi_status s = resolve_peers(ctx)) return s;
   if (!ctx->gst) {
+    CUDA_TRY(ctx, cudaStreamCreateWithFlags(&ctx->xst, cudaStreamNonBlocking));
     CUDA_TRY(ctx, cudaStreamCreateWithFlags(&ctx->gst, cudaStreamNonBlocking));
     CUDA_TRY(ctx, cudaEventCreateWithFlags(&ctx->gev_in, cudaEventDisableTiming));
     CUDA_TRY(ctx, cudaEventCreateWithFlags(&ctx->gev_out, cudaEventDisableTiming));
@@ -1388,9 +1469,10 @@ vdi_status vdi_composite_frames(vdi_ctx* ctx, uint32_t F, const vdi_dense_view* 
     CUDA_TRY(ctx, ctx->fs_depth[i].grow(P * k * 8));
     CUDA_TRY(ctx, ctx->fs_rgba[i].grow(P * k * 16));
   }
-  // the inflate stream starts once the caller's stream has reached this call
+  // the push and inflate streams start once the caller's stream has reached this call
   CUDA_TRY(ctx, cudaEventRecord(ctx->gev_in, st));
   CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->gst, ctx->gev_in, 0));
+  CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->xst, ctx->gev_in, 0));
   int launches = 0;
   uint32_t nf = 0;
   for (uint32_t f = 0; f < F; ++f) {
@@ -1404,7 +1486,15 @@ vdi_status vdi_composite_frames(vdi_ctx* ctx, uint32_t F, const vdi_dense_view* 
       so = vdi_full_view{ctx->row0, ctx->row1, ctx->fs_count[b].as<uint8_t>(), ctx->fs_depth[b].as<float>(),
                          ctx->fs_rgba[b].as<float>()};
     }
-    if (vdi_status s = vdi_composite(ctx, local + (size_t)f * n_local, n_local, &so)) return s;
+    // frame f's push runs on the push stream beside frame f-1's merge; its
+    // double-buffered exchange arrays wait for the merge of frame f-2
+    ctx->xpst = ctx->xst;
+    ctx->xpar = (int)(f & 1);
+    if (f >= 2) CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->xst, ctx->xev_merged[f & 1], 0));
+    const vdi_status cs = vdi_composite(ctx, local + (size_t)f * n_local, n_local, &so);
+    ctx->xpst = nullptr;
+    ctx->xpar = 0;
+    if (cs != VDI_OK) return cs;
     launches += ctx->last.kernel_launches;
     const uint32_t j = ++ctx->gcalls_to[R];
     if (R != me) {
@@ -1415,8 +1505,10 @@ vdi_status vdi_composite_frames(vdi_ctx* ctx, uint32_t F, const vdi_dense_view* 
     ctx->last_gather_root = (int)R;
     ctx->last_gather_parity = j & 1;
   }
-  // the call ends on the caller's stream once the inflates have too
+  // the call ends on the caller's stream once the pushes and inflates have too
   CUDA_TRY(ctx, cudaEventRecord(ctx->gev_out, ctx->gst));
+  CUDA_TRY(ctx, cudaStreamWaitEvent(st, ctx->gev_out, 0));
+  CUDA_TRY(ctx, cudaEventRecord(ctx->gev_out, ctx->xst));
   CUDA_TRY(ctx, cudaStreamWaitEvent(st, ctx->gev_out, 0));
   ctx->last.kernel_launches = (uint32_t)launches;
   return VDI_OK;

@@ -115,6 +115,15 @@ __global__ void __launch_bounds__(256) push_kernel(const PushSeg* __restrict__ s
     nrec = sg.nrec;
   }
   copy_bytes(sg.src_count, sg.dst_count, sg.n_count, i0, stride);
+  if (sg.dst_gbase) {  // group bases relative to the slice's first record: the receiver needs no scan
+    if (sg.src_offset) {
+      const uint32_t b0 = sg.src_offset[0];
+      for (unsigned long long i = i0; i < sg.n_groups; i += stride) sg.dst_gbase[i] = sg.src_offset[i * 32] - b0;
+    } else if (sg.src_gb32) {
+      const uint32_t b0 = sg.src_gb32[0];
+      for (unsigned long long i = i0; i < sg.n_groups; i += stride) sg.dst_gbase[i] = sg.src_gb32[i] - b0;
+    }
+  }
   if (nrec) {
     copy_bytes(sg.src_depth + r0, sg.dst_depth, nrec * 8, i0, stride);
     copy_bytes(sg.src_rgba + r0, sg.dst_rgba, nrec * 16, i0, stride);

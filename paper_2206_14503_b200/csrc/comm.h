@@ -33,6 +33,10 @@ struct PushSeg {
   const unsigned long long* bnd;  // &bnd[l][g]: records [bnd[0], bnd[1]); null -> [rec0, rec0 + nrec)
   unsigned long long rec0, nrec;
   unsigned long long n_count;   // bytes of the count slice
+  const uint32_t* src_offset;   // group bases of the slice from the PE's offsets (at the slice start), or
+  const uint32_t* src_gb32;     // from its 32-list scan (at the slice's first group); neither: none pushed
+  uint32_t n_groups;            // 32-list groups of the destination strip
+  uint32_t* dst_gbase;          // [n_groups]: index of each group's first record in the slice
   uint8_t* dst_count;           // destination window slot (peer memory)
   float2* dst_depth;
   float4* dst_rgba;

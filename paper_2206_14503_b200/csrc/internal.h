@@ -34,8 +34,10 @@ struct SrcDesc {
   const uint8_t* count;
   const float2* depth;
   const float4* rgba;
-  const uint32_t* offset;  // the source's exclusive scan of count (indexed by list), or null: then the
-                           // merge scans the counts itself (receive-side scan)
+  const uint32_t* offset;  // the source's exclusive scan of count (indexed by list), or null
+  const uint32_t* gbase;   // or: the index of the first record of each 32-list group of the strip (pushed by
+                           // the sender / from its scan); neither: the merge scans the counts itself
+                           // (receive-side scan)
 };
 
 // Work-list buckets of lists that need more than the pass-through:

@@ -566,7 +566,8 @@ __global__ void __launch_bounds__(kFastThreads) merge_fast_kernel(MergeParams mp
   // total (one offset sector per source and run instead of per group)
   constexpr uint32_t kRun = VDI_FAST_RUN;
   const uint32_t nw_all = gridDim.x * nwarps, w_id = blockIdx.x * nwarps + warp;
-  const bool carry = mp.src[0].offset != nullptr;  // all sources or none (api.cu)
+  // per source: offset array (bases read at run starts and carried), pushed
+  // group bases (read per group), or the receive-side scan (mp.group_base)
   auto next_group = [&](uint32_t gg) -> uint32_t {  // the group after gg in this warp's sequence
     const uint32_t r = (gg - mp.g_begin) % kRun;
     return r + 1 < kRun ? gg + 1 : gg + 1 + (nw_all - 1) * kRun;
@@ -582,8 +583,13 @@ __global__ void __launch_bounds__(kFastThreads) merge_fast_kernel(MergeParams mp
       nc[s] = 0;
       if (s < n && gg < mp.g_end) {
         if (pp < mp.P) nc[s] = __ldg(mp.src[s].count + pp);
-        if (!carry) nb[s] = __ldg(mp.group_base + (size_t)s * mp.n_groups + gg);
-        else if (run_start) nb[s] = __ldg(mp.src[s].offset + (size_t)gg * 32);
+        if (mp.src[s].offset) {
+          if (run_start) nb[s] = __ldg(mp.src[s].offset + (size_t)gg * 32);
+        } else if (mp.src[s].gbase) {
+          nb[s] = __ldg(mp.src[s].gbase + gg);
+        } else {
+          nb[s] = __ldg(mp.group_base + (size_t)s * mp.n_groups + gg);
+        }
       }
     }
   };
@@ -606,7 +612,7 @@ __global__ void __launch_bounds__(kFastThreads) merge_fast_kernel(MergeParams mp
       if (s < n) {
         const uint32_t c = cnt[s];
         const uint32_t incl = warp_incl_scan(c, lane);
-        if (carry && (g - mp.g_begin) % kRun + 1 < kRun)
+        if (mp.src[s].offset && (g - mp.g_begin) % kRun + 1 < kRun)
           nb[s] = gidx[s] + __shfl_sync(kFull, incl, 31);  // base of group g + 1 (same run)
         gidx[s] += incl - c;
         m += c;
