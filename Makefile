@@ -6,13 +6,13 @@ ARCH    := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := -std=c++17 -O3 $(ARCH) -lineinfo -fmad=false -Xcompiler -fPIC -Xcompiler -fvisibility=hidden \
            -Iinclude -I$(NCCL)/include -Xptxas -v
 PKG     := paper_2206_14503_b200
-SRCS    := $(PKG)/csrc/api.cu $(PKG)/csrc/merge.cu $(PKG)/csrc/generate.cu $(PKG)/csrc/comm.cu
+SRCS    := $(PKG)/csrc/api.cu $(PKG)/csrc/merge.cu $(PKG)/csrc/generate.cu $(PKG)/csrc/comm.cu $(PKG)/csrc/render.cu
 OBJS    := $(patsubst $(PKG)/csrc/%.cu,build/%.o,$(SRCS))
 LIB     := $(PKG)/lib/libvdi.so
 
 all: $(LIB) oracle/liboracle.so
 
-build/%.o: $(PKG)/csrc/%.cu $(PKG)/csrc/internal.h $(PKG)/csrc/comm.h include/vdi.h
+build/%.o: $(PKG)/csrc/%.cu $(PKG)/csrc/internal.h $(PKG)/csrc/comm.h $(PKG)/csrc/render.h include/vdi.h
 	@mkdir -p build
 	$(NVCC) $(NVFLAGS) -dc -o $@ $< 2> build/$*.ptxas.log || (cat build/$*.ptxas.log; false)
 

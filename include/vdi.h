@@ -169,6 +169,15 @@ vdi_status vdi_generate_subvdi(vdi_ctx* ctx, const vdi_volume_desc* vol, const v
                                const vdi_camera* cam, const vdi_decomp_desc* decomp, uint32_t pe_id,
                                vdi_dense_view* out);
 
+/* Limit case: the sub-VDI of PE pe_id with a
+ * single S~ per sub-domain intersection -- the sweep of vdi_generate_subvdi
+ * at gamma = infinity, so only leaving the PE's domain ends a supersegment
+ * (PAPER.md:196).  k_in must cover the most domain intervals with content on
+ * a ray (VDI_ERR_CAPACITY otherwise).  Output as vdi_generate_subvdi. */
+vdi_status vdi_generate_limit(vdi_ctx* ctx, const vdi_volume_desc* vol, const vdi_tf_desc* tf,
+                              const vdi_camera* cam, const vdi_decomp_desc* decomp, uint32_t pe_id,
+                              vdi_dense_view* out);
+
 /* ---- Phase 2: the hot path -------------------------------------------------
  * Parallel compositing of the sub-VDIs, collective over
  * all ranks (n_ranks == 1: local):
@@ -298,6 +307,48 @@ vdi_status vdi_gather_root(vdi_ctx* ctx, uint32_t root, const vdi_full_view* str
  * vdi_composite per frame into images[f]. */
 vdi_status vdi_composite_frames(vdi_ctx* ctx, uint32_t n_frames, const vdi_dense_view* local_pes,
                                 uint32_t n_local, vdi_full_view* images, const uint32_t* roots);
+
+/* ---- limit case and rendering ------------------------------ */
+/* The limit case of the compositing: the exchange of
+ * vdi_composite, then every list's S~ are placed in depth order
+ * and over-composited along the list, giving the plain
+ * volume-rendered image of this rank's strip -- DVR on a non-convex domain
+ * decomposition without synchronisation between PEs.  With limit sub-VDIs
+ * (vdi_generate_limit) the image equals direct volume rendering up to fp32
+ * rounding.  Overlapping records are composited in (t_front, PE id) order
+ * without subdivision.  strip_rgba: device [rows*W][4] premultiplied,
+ * 16-byte aligned.  Collective (n_ranks > 1); never synchronises the host. */
+vdi_status vdi_composite_image(vdi_ctx* ctx, const vdi_dense_view* local_pes, uint32_t n_local, float* strip_rgba);
+
+/* Gather of the strips of vdi_composite_image onto vdi_config.root:
+ * image_rgba (root only, device [H*W][4]) receives every strip at its rows
+ * (pushed into the root's window over NVLink).  Collective. */
+vdi_status vdi_gather_image(vdi_ctx* ctx, const float* strip_rgba, float* image_rgba);
+
+/* A VDI rendered from its generation viewpoint: the over of each list's
+ * supersegments front to back -- the exact image by associativity of over
+ * (PAPER.md:77).  vdi: any rows (device, k_out slots); out_rgba: device
+ * [rows*W][4] premultiplied, 16-byte aligned.  Local. */
+vdi_status vdi_render_generation_view(vdi_ctx* ctx, const vdi_full_view* vdi, float* out_rgba);
+
+/* A full VDI (rows [0, H), k_out slots, generated with camera gen_cam)
+ * rendered from camera view_cam at w_out x h_out: rays
+ * through the new pixel centres are marched through the volume's world box
+ * (dims, longest side 1) one voxel per step; each sample is projected into
+ * gen_cam, the supersegment of the nearest list containing its depth along
+ * that list's ray contributes opacity 1 - (1 - a)^(dt / L) (L its length;
+ * Eq. 2) and colour scaled alike, over-composited front to
+ * back.  out_rgba: device [h_out*w_out][4] premultiplied.  Local. */
+vdi_status vdi_render_novel_view(vdi_ctx* ctx, const vdi_full_view* vdi, const vdi_camera* gen_cam,
+                                 const vdi_camera* view_cam, const uint32_t dims[3], uint32_t w_out, uint32_t h_out,
+                                 float* out_rgba);
+
+/* Ground truth for the quality evaluation: direct volume
+ * rendering of the whole volume with camera cam at w_out x h_out -- the
+ * over of every sample of the global grid (the generator's sampling, Q18,
+ * Q19), fp32, no early termination (Q21).  out_rgba: device [h_out*w_out][4]. */
+vdi_status vdi_render_dvr(vdi_ctx* ctx, const vdi_volume_desc* vol, const vdi_tf_desc* tf, const vdi_camera* cam,
+                          uint32_t w_out, uint32_t h_out, float* out_rgba);
 
 /* ---- introspection ---------------------------------------------------------- */
 /* Per-list gamma* (0 for pass-through), tie margin and m (samples after

@@ -81,7 +81,17 @@ SIGNATURES = {
     "vdi_generate_subvdi": (C.c_int, [C.c_void_p, C.POINTER(vdi_volume_desc), C.POINTER(vdi_tf_desc),
                                       C.POINTER(vdi_camera), C.POINTER(vdi_decomp_desc), C.c_uint32,
                                       C.POINTER(vdi_dense_view)]),
+    "vdi_generate_limit": (C.c_int, [C.c_void_p, C.POINTER(vdi_volume_desc), C.POINTER(vdi_tf_desc),
+                                     C.POINTER(vdi_camera), C.POINTER(vdi_decomp_desc), C.c_uint32,
+                                     C.POINTER(vdi_dense_view)]),
     "vdi_composite": (C.c_int, [C.c_void_p, C.POINTER(vdi_dense_view), C.c_uint32, C.POINTER(vdi_full_view)]),
+    "vdi_composite_image": (C.c_int, [C.c_void_p, C.POINTER(vdi_dense_view), C.c_uint32, C.c_void_p]),
+    "vdi_gather_image": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
+    "vdi_render_generation_view": (C.c_int, [C.c_void_p, C.POINTER(vdi_full_view), C.c_void_p]),
+    "vdi_render_novel_view": (C.c_int, [C.c_void_p, C.POINTER(vdi_full_view), C.POINTER(vdi_camera),
+                                        C.POINTER(vdi_camera), C.c_void_p, C.c_uint32, C.c_uint32, C.c_void_p]),
+    "vdi_render_dvr": (C.c_int, [C.c_void_p, C.POINTER(vdi_volume_desc), C.POINTER(vdi_tf_desc),
+                                 C.POINTER(vdi_camera), C.c_uint32, C.c_uint32, C.c_void_p]),
     "vdi_composite_host": (C.c_int, [C.c_void_p, C.POINTER(vdi_dense_view), C.c_uint32,
                                      C.POINTER(vdi_full_view)]),
     "vdi_composite_fullrep": (C.c_int, [C.c_void_p, C.POINTER(vdi_full_view), C.c_void_p, C.c_uint32,

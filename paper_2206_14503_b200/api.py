@@ -135,18 +135,27 @@ class Compositor:
             pass
 
     # -- Phase 1 (SUPPORT) ---------------------------------------------------
-    def generate_subvdi(self, volume: torch.Tensor, tf_table: torch.Tensor, camera, decomposition,
-                        pe_id: int) -> DenseSubVDI:
-        """vdi_generate_subvdi: volume [dz][dy][dx] u8 (or u16 bits in int16),
-        tf_table [256,4] f32 (device), camera with eye/fwd/right/up/tan_x/tan_y,
-        decomposition with xb/yb/zb/owner int arrays.  Returns tensors that
-        alias ctx-owned memory (valid until the next call for this pe_id)."""
+    @staticmethod
+    def _cam(camera) -> L.vdi_camera:
+        return L.vdi_camera((C.c_float * 3)(*camera.eye), (C.c_float * 3)(*camera.fwd),
+                            (C.c_float * 3)(*camera.right), (C.c_float * 3)(*camera.up), camera.tan_x, camera.tan_y)
+
+    @staticmethod
+    def _vol(volume, tf_table):
         assert volume.is_cuda and tf_table.is_cuda
         dz, dy, dx = volume.shape
         vol = L.vdi_volume_desc(volume.data_ptr(), volume.element_size(), (C.c_uint32 * 3)(dx, dy, dz))
-        tf = L.vdi_tf_desc(tf_table.contiguous().data_ptr())
-        cam = L.vdi_camera((C.c_float * 3)(*camera.eye), (C.c_float * 3)(*camera.fwd),
-                           (C.c_float * 3)(*camera.right), (C.c_float * 3)(*camera.up), camera.tan_x, camera.tan_y)
+        return vol, L.vdi_tf_desc(tf_table.contiguous().data_ptr())
+
+    def generate_subvdi(self, volume: torch.Tensor, tf_table: torch.Tensor, camera, decomposition,
+                        pe_id: int, limit: bool = False) -> DenseSubVDI:
+        """vdi_generate_subvdi (limit=True: vdi_generate_limit, one S~ per
+        sub-domain intersection): volume [dz][dy][dx] u8 (or u16 bits in int16),
+        tf_table [256,4] f32 (device), camera with eye/fwd/right/up/tan_x/tan_y,
+        decomposition with xb/yb/zb/owner int arrays.  Returns tensors that
+        alias ctx-owned memory (valid until the next call for this pe_id)."""
+        vol, tf = self._vol(volume, tf_table)
+        cam = self._cam(camera)
         xb = np.ascontiguousarray(decomposition.xb, np.int32)
         yb = np.ascontiguousarray(decomposition.yb, np.int32)
         zb = np.ascontiguousarray(decomposition.zb, np.int32)
@@ -154,8 +163,9 @@ class Compositor:
         dec = L.vdi_decomp_desc((C.c_uint32 * 3)(len(xb) - 1, len(yb) - 1, len(zb) - 1), xb.ctypes.data,
                                 yb.ctypes.data, zb.ctypes.data, ow.ctypes.data)
         out = L.vdi_dense_view()
-        L.check(self.lib.vdi_generate_subvdi(self.ctx, C.byref(vol), C.byref(tf), C.byref(cam), C.byref(dec),
-                                             pe_id, C.byref(out)), "vdi_generate_subvdi")
+        fn = self.lib.vdi_generate_limit if limit else self.lib.vdi_generate_subvdi
+        L.check(fn(self.ctx, C.byref(vol), C.byref(tf), C.byref(cam), C.byref(dec), pe_id, C.byref(out)),
+                "vdi_generate_limit" if limit else "vdi_generate_subvdi")
         P = self.width * self.height
         S = int(out.total)
         return DenseSubVDI(pe_id, S, _wrap(out.count, (P,), "|u1", self), _wrap(out.offset, (P + 1,), "<u4", self),
@@ -268,6 +278,52 @@ class Compositor:
         else:
             L.check(self.lib.vdi_gather_root(self.ctx, root, C.byref(sv), ip), "vdi_gather_root")
         return image
+
+    # -- limit case and rendering ---------------------------
+    def composite_image(self, local_pes, strip_rgba: torch.Tensor | None = None) -> torch.Tensor:
+        """vdi_composite_image: the plain volume-rendered image of this rank's
+        strip, premultiplied RGBA [rows*W, 4]."""
+        P = (self.row_end - self.row_begin) * self.width
+        if strip_rgba is None:
+            strip_rgba = torch.empty((P, 4), dtype=torch.float32, device="cuda")
+        views = (L.vdi_dense_view * max(1, len(local_pes)))(*[p.view() for p in local_pes])
+        L.check(self.lib.vdi_composite_image(self.ctx, views, len(local_pes), strip_rgba.data_ptr()),
+                "vdi_composite_image")
+        return strip_rgba
+
+    def gather_image(self, strip_rgba: torch.Tensor, image_rgba: torch.Tensor | None):
+        """vdi_gather_image: strips of vdi_composite_image -> the root's [H*W, 4] image."""
+        L.check(self.lib.vdi_gather_image(self.ctx, strip_rgba.data_ptr(),
+                                          image_rgba.data_ptr() if image_rgba is not None else None),
+                "vdi_gather_image")
+        return image_rgba
+
+    def render_generation_view(self, vdi: FullVDI) -> torch.Tensor:
+        """vdi_render_generation_view: over of each list -> RGBA [rows*W, 4]."""
+        out = torch.empty((vdi.count.numel(), 4), dtype=torch.float32, device="cuda")
+        v = vdi.view()
+        L.check(self.lib.vdi_render_generation_view(self.ctx, C.byref(v), out.data_ptr()),
+                "vdi_render_generation_view")
+        return out
+
+    def render_novel_view(self, vdi: FullVDI, gen_camera, view_camera, dims, w, h) -> torch.Tensor:
+        """vdi_render_novel_view: the full VDI (rows [0, H)) from view_camera -> RGBA [h*w, 4]."""
+        out = torch.empty((w * h, 4), dtype=torch.float32, device="cuda")
+        v = vdi.view()
+        g, c = self._cam(gen_camera), self._cam(view_camera)
+        d = (C.c_uint32 * 3)(*dims)
+        L.check(self.lib.vdi_render_novel_view(self.ctx, C.byref(v), C.byref(g), C.byref(c), d, w, h, out.data_ptr()),
+                "vdi_render_novel_view")
+        return out
+
+    def render_dvr(self, volume, tf_table, camera, w, h) -> torch.Tensor:
+        """vdi_render_dvr: ground-truth DVR of the whole volume -> RGBA [h*w, 4]."""
+        out = torch.empty((w * h, 4), dtype=torch.float32, device="cuda")
+        vol, tf = self._vol(volume, tf_table)
+        cam = self._cam(camera)
+        L.check(self.lib.vdi_render_dvr(self.ctx, C.byref(vol), C.byref(tf), C.byref(cam), w, h, out.data_ptr()),
+                "vdi_render_dvr")
+        return out
 
     def pixel_stats(self, with_margin=False):
         """vdi_pixel_stats: per-list gamma*, m (and the tie margin) of the last composite."""

@@ -28,6 +28,7 @@
 
 #include "comm.h"
 #include "internal.h"
+#include "render.h"
 
 using namespace vdi;
 
@@ -619,6 +620,7 @@ vdi_status vdi_composite_init(const vdi_config* cfg, vdi_ctx** out) {
       std::call_once(once, [] {
         preload_merge();
         preload_comm();
+        preload_render();
       });
       ctx->loop_key.assign(reinterpret_cast<const char*>(cfg->nccl_unique_id), 128);
       std::lock_guard<std::mutex> lk(g_loop_mu);
@@ -722,9 +724,8 @@ void vdi_composite_destroy(vdi_ctx* ctx) { delete ctx; }
 // ---------------------------------------------------------------------------
 // Phase 1 (SUPPORT)
 // ---------------------------------------------------------------------------
-vdi_status vdi_generate_subvdi(vdi_ctx* ctx, const vdi_volume_desc* vol, const vdi_tf_desc* tf,
-                               const vdi_camera* cam, const vdi_decomp_desc* dec, uint32_t pe_id,
-                               vdi_dense_view* out) {
+static vdi_status generate(vdi_ctx* ctx, const vdi_volume_desc* vol, const vdi_tf_desc* tf, const vdi_camera* cam,
+                           const vdi_decomp_desc* dec, uint32_t pe_id, vdi_dense_view* out, bool limit) {
   if (vdi_status s = check_ctx(ctx)) return s;
   if (!vol || !tf || !cam || !dec || !out || !vol->voxels || !tf->table)
     return fail(VDI_ERR_INVALID_ARG, "NULL argument");
@@ -787,6 +788,7 @@ vdi_status vdi_generate_subvdi(vdi_ctx* ctx, const vdi_volume_desc* vol, const v
   gp.k = (int)ctx->cfg.k_in;
   gp.max_iters = (int)ctx->cfg.max_iters;
   gp.gamma_max = ctx->cfg.gamma_max;
+  gp.limit = limit ? 1 : 0;
 
   GenOut& g = ctx->gen[pe_id];
   const size_t P = (size_t)ctx->cfg.width * ctx->cfg.height;
@@ -822,6 +824,17 @@ vdi_status vdi_generate_subvdi(vdi_ctx* ctx, const vdi_volume_desc* vol, const v
   out->depth = g.depth.as<float>();
   out->rgba = g.rgba.as<float>();
   return VDI_OK;
+}
+
+vdi_status vdi_generate_subvdi(vdi_ctx* ctx, const vdi_volume_desc* vol, const vdi_tf_desc* tf,
+                               const vdi_camera* cam, const vdi_decomp_desc* dec, uint32_t pe_id,
+                               vdi_dense_view* out) {
+  return generate(ctx, vol, tf, cam, dec, pe_id, out, false);
+}
+
+vdi_status vdi_generate_limit(vdi_ctx* ctx, const vdi_volume_desc* vol, const vdi_tf_desc* tf, const vdi_camera* cam,
+                              const vdi_decomp_desc* dec, uint32_t pe_id, vdi_dense_view* out) {
+  return generate(ctx, vol, tf, cam, dec, pe_id, out, true);
 }
 
 // ---------------------------------------------------------------------------
@@ -1798,6 +1811,187 @@ vdi_status vdi_composite_host_dense_frames(vdi_ctx* ctx, uint32_t F, const vdi_d
   CUDA_TRY(ctx, cudaStreamSynchronize(st));
   ctx->last.kernel_launches += (uint32_t)launches;
   return first_err;
+}
+
+// ---------------------------------------------------------------------------
+// The limit case and the renderers
+// ---------------------------------------------------------------------------
+vdi_status vdi_composite_image(vdi_ctx* ctx, const vdi_dense_view* local, uint32_t n_local, float* strip_rgba) {
+  if (vdi_status s = check_ctx(ctx)) return s;
+  const vdi_config& cf = ctx->cfg;
+  const uint32_t G = cf.n_ranks, n = cf.n_pes;
+  if (!strip_rgba || (reinterpret_cast<uintptr_t>(strip_rgba) & 15))
+    return fail(VDI_ERR_INVALID_ARG, "strip_rgba is NULL or not 16-byte aligned");
+  std::vector<int> slot;
+  if (vdi_status s = check_local(ctx, local, n_local, slot)) return s;
+  cudaStream_t st = ctx->stream;
+  int launches = 0;
+  MergeParams mp{};
+  mp.n_src = (int)n;
+  mp.P = (uint32_t)ctx->P;
+  mp.n_groups = (uint32_t)((ctx->P + 31) / 32);
+  if (G == 1) {
+    for (uint32_t s = 0; s < n; ++s) {
+      const vdi_dense_view& v = local[slot[s]];
+      mp.src[s] = SrcDesc{v.count, reinterpret_cast<const float2*>(v.depth), reinterpret_cast<const float4*>(v.rgba),
+                          v.offset, nullptr};
+    }
+  } else {
+    uint32_t e = 0;
+    if (vdi_status s = exchange_push(ctx, local, nullptr, n_local, nullptr, launches, st, 0, &e)) return s;
+    if (vdi_status s = exchange_recv(ctx, local, nullptr, slot, e, 0, mp, launches)) return s;
+  }
+  bool scan = false;
+  for (uint32_t s = 0; s < n; ++s) scan |= !mp.src[s].offset && !mp.src[s].gbase;
+  CUDA_TRY(ctx, ctx->group_sum.grow((size_t)scan_chunks(mp.P) * n * 4 + 64));
+  CUDA_TRY(ctx, ctx->group_base.grow((size_t)mp.n_groups * n * 4 + 64));
+  mp.group_base = ctx->group_base.as<uint32_t>();
+  if (scan && mp.P)
+    CUDA_TRY(ctx, launch_scan(mp, ctx->group_sum.as<uint32_t>(), ctx->group_base.as<uint32_t>(), st, &launches));
+  CUDA_TRY(ctx, launch_image(mp, reinterpret_cast<float4*>(strip_rgba), st));
+  ++launches;
+  if (G > 1) {
+    CUDA_TRY(ctx, cudaEventRecord(ctx->xev_merged[0], st));
+    if (vdi_status s = release_slots(ctx, launches)) return s;
+  }
+  ctx->last = vdi_counters{};
+  ctx->last.kernel_launches = (uint32_t)launches;
+  return VDI_OK;
+}
+
+vdi_status vdi_gather_image(vdi_ctx* ctx, const float* strip_rgba, float* image_rgba) {
+  if (vdi_status s = check_ctx(ctx)) return s;
+  const vdi_config& cf = ctx->cfg;
+  const Layout& L = ctx->lay;
+  const uint32_t G = cf.n_ranks, me = cf.rank, W = cf.width, R = cf.root;
+  if (!strip_rgba) return fail(VDI_ERR_INVALID_ARG, "strip_rgba is NULL");
+  if (me == R && !image_rgba) return fail(VDI_ERR_INVALID_ARG, "image_rgba is NULL on the root");
+  cudaStream_t st = ctx->stream;
+  const size_t o = (size_t)ctx->row0 * W;
+  int launches = 0;
+  if (G == 1) {
+    if (image_rgba != strip_rgba)
+      CUDA_TRY(ctx, cudaMemcpyAsync(image_rgba, strip_rgba, ctx->P * 16, cudaMemcpyDeviceToDevice, st));
+    return VDI_OK;
+  }
+  if (vdi_status s = resolve_peers(ctx)) return s;
+  const uint32_t j = ++ctx->gcalls_to[R];
+  char* gp = ctx->peer[R] + L.g_off(R, j & 1);
+  float4* win = reinterpret_cast<float4*>(gp + L.g_rgba_off());  // the rows of the image, W*H float4
+  if (me != R) {
+    if (j > (ctx->grp ? 1u : 2u)) {
+      if (vdi_status s = wait_flags(ctx, GFREE, {{R, j - 2, j - 1}}, st)) return s;
+      ++launches;
+    }
+    CUDA_TRY(ctx, launch_rows_push(reinterpret_cast<const float4*>(strip_rgba), win + o, (uint32_t)ctx->P,
+                                   compact_push_blocks((uint32_t)ctx->P), flag_at(ctx->peer[R], GREADY, me), st));
+    ++launches;
+    if (ctx->grp)
+      if (vdi_status s = loop_post(ctx, GREADY, {R}, j, st)) return s;
+  } else {
+    std::vector<WaitOn> wt;
+    std::vector<uint32_t> others;
+    for (uint32_t g = 0; g < G; ++g)
+      if (g != R) {
+        wt.push_back({g, j * compact_push_blocks(L.rows(g) * W), j});
+        others.push_back(g);
+      }
+    if (vdi_status s = wait_flags(ctx, GREADY, wt, st)) return s;
+    ++launches;
+    const size_t a1 = o, b0 = (size_t)ctx->row1 * W, img = L.img();
+    float4* im = reinterpret_cast<float4*>(image_rgba);
+    if (a1) CUDA_TRY(ctx, cudaMemcpyAsync(im, win, a1 * 16, cudaMemcpyDeviceToDevice, st));
+    if (img > b0) CUDA_TRY(ctx, cudaMemcpyAsync(im + b0, win + b0, (img - b0) * 16, cudaMemcpyDeviceToDevice, st));
+    if (image_rgba + o * 4 != strip_rgba)
+      CUDA_TRY(ctx, cudaMemcpyAsync(im + o, strip_rgba, ctx->P * 16, cudaMemcpyDeviceToDevice, st));
+    if (vdi_status s = signal_peers(ctx, GFREE, others, j, st, j)) return s;
+    ++launches;
+  }
+  ctx->last.kernel_launches += (uint32_t)launches;
+  return VDI_OK;
+}
+
+vdi_status vdi_render_generation_view(vdi_ctx* ctx, const vdi_full_view* vdi, float* out_rgba) {
+  if (vdi_status s = check_ctx(ctx)) return s;
+  if (!vdi || !vdi->count || !vdi->rgba || !out_rgba || vdi->row_end < vdi->row_begin)
+    return fail(VDI_ERR_INVALID_ARG, "vdi / out_rgba is NULL");
+  if ((reinterpret_cast<uintptr_t>(vdi->rgba) | reinterpret_cast<uintptr_t>(out_rgba)) & 15)
+    return fail(VDI_ERR_INVALID_ARG, "rgba arrays must be 16-byte aligned");
+  const uint32_t P = (vdi->row_end - vdi->row_begin) * ctx->cfg.width;
+  CUDA_TRY(ctx, launch_gen_view(vdi->count, reinterpret_cast<const float4*>(vdi->rgba), P, (int)ctx->cfg.k_out,
+                                reinterpret_cast<float4*>(out_rgba), ctx->stream));
+  return VDI_OK;
+}
+
+static CamF camf(const vdi_camera& c) {
+  CamF f;
+  for (int a = 0; a < 3; ++a) {
+    f.eye[a] = c.eye[a];
+    f.fwd[a] = c.fwd[a];
+    f.right[a] = c.right[a];
+    f.up[a] = c.up[a];
+  }
+  f.tan_x = c.tan_x;
+  f.tan_y = c.tan_y;
+  return f;
+}
+
+vdi_status vdi_render_novel_view(vdi_ctx* ctx, const vdi_full_view* vdi, const vdi_camera* gen_cam,
+                                 const vdi_camera* view_cam, const uint32_t dims[3], uint32_t w_out, uint32_t h_out,
+                                 float* out_rgba) {
+  if (vdi_status s = check_ctx(ctx)) return s;
+  const vdi_config& cf = ctx->cfg;
+  if (!vdi || !vdi->count || !vdi->depth || !vdi->rgba || !gen_cam || !view_cam || !dims || !out_rgba)
+    return fail(VDI_ERR_INVALID_ARG, "NULL argument");
+  if (vdi->row_begin != 0 || vdi->row_end != cf.height) return fail(VDI_ERR_INVALID_ARG, "vdi must cover rows [0, H)");
+  if (!w_out || !h_out || !dims[0] || !dims[1] || !dims[2]) return fail(VDI_ERR_INVALID_ARG, "empty image or volume");
+  if ((reinterpret_cast<uintptr_t>(vdi->rgba) | reinterpret_cast<uintptr_t>(out_rgba)) & 15)
+    return fail(VDI_ERR_INVALID_ARG, "rgba arrays must be 16-byte aligned");
+  NovelParams np{};
+  np.count = vdi->count;
+  np.depth = reinterpret_cast<const float2*>(vdi->depth);
+  np.rgba = reinterpret_cast<const float4*>(vdi->rgba);
+  np.W = cf.width;
+  np.H = cf.height;
+  np.k = (int)cf.k_out;
+  np.gen = camf(*gen_cam);
+  np.view = camf(*view_cam);
+  const uint32_t md = std::max(dims[0], std::max(dims[1], dims[2]));
+  for (int a = 0; a < 3; ++a) np.half[a] = (float)dims[a] / (2.0f * (float)md);
+  np.dt = 1.0f / (float)md;
+  np.W_out = w_out;
+  np.H_out = h_out;
+  np.out = reinterpret_cast<float4*>(out_rgba);
+  CUDA_TRY(ctx, launch_novel_view(np, ctx->stream));
+  return VDI_OK;
+}
+
+vdi_status vdi_render_dvr(vdi_ctx* ctx, const vdi_volume_desc* vol, const vdi_tf_desc* tf, const vdi_camera* cam,
+                          uint32_t w_out, uint32_t h_out, float* out_rgba) {
+  if (vdi_status s = check_ctx(ctx)) return s;
+  if (!vol || !tf || !cam || !out_rgba || !vol->voxels || !tf->table) return fail(VDI_ERR_INVALID_ARG, "NULL argument");
+  if (vol->bytes_per_voxel != 1 && vol->bytes_per_voxel != 2)
+    return fail(VDI_ERR_INVALID_ARG, "bytes_per_voxel must be 1 or 2");
+  if (!w_out || !h_out || !vol->dims[0] || !vol->dims[1] || !vol->dims[2])
+    return fail(VDI_ERR_INVALID_ARG, "empty image or volume");
+  if (reinterpret_cast<uintptr_t>(out_rgba) & 15) return fail(VDI_ERR_INVALID_ARG, "out_rgba must be 16-byte aligned");
+  GenParams gp{};
+  gp.vox = vol->voxels;
+  gp.bytes = (int)vol->bytes_per_voxel;
+  for (int a = 0; a < 3; ++a) {
+    gp.dims[a] = (int)vol->dims[a];
+    gp.eye[a] = cam->eye[a];
+    gp.fwd[a] = cam->fwd[a];
+    gp.right[a] = cam->right[a];
+    gp.up[a] = cam->up[a];
+  }
+  gp.tf = reinterpret_cast<const float4*>(tf->table);
+  gp.tan_x = cam->tan_x;
+  gp.tan_y = cam->tan_y;
+  gp.W = (int)w_out;
+  gp.H = (int)h_out;
+  CUDA_TRY(ctx, launch_dvr(gp, reinterpret_cast<float4*>(out_rgba), ctx->stream));
+  return VDI_OK;
 }
 
 vdi_status vdi_pixel_stats(vdi_ctx* ctx, float* gamma, float* min_margin, uint16_t* m) {

@@ -217,6 +217,13 @@ __global__ void gen_pass1_kernel(GenParams gp, uint32_t* __restrict__ count32, f
     const RayG r = make_ray(gp, (int)(p % gp.W), (int)(p / gp.W));
     int64_t i0, i1;
     clip_range(gp, r, &i0, &i1);
+    if (gp.limit) {  // one S~ per sub-domain intersection: gamma = inf, only domain exits split
+      const int c = gen_sweep(gp, r, i0, i1, CUDART_INF_F, gp.k, nullptr, nullptr);
+      if (c > gp.k) atomicOr(err, 2);  // capacity (Q20)
+      count32[p] = (uint32_t)min(c, gp.k);
+      gamma_out[p] = CUDART_INF_F;
+      continue;
+    }
     int c = gen_sweep(gp, r, i0, i1, 0.0f, gp.k, nullptr, nullptr);
     float g = 0.0f;
     if (c > gp.k) {
@@ -255,6 +262,50 @@ __global__ void gen_pass2_kernel(GenParams gp, const uint32_t* __restrict__ offs
     const uint32_t o = offset[p];
     gen_sweep(gp, r, i0, i1, gamma[p], gp.k, depth + o, rgba + o);
   }
+}
+
+// Ground-truth direct volume rendering (A19): over of ALL
+// samples of the global grid front to back, fp32, no early termination
+// (Q21) -- the generator's sampling without segmentation.  One thread per ray.
+__global__ void dvr_kernel(GenParams gp, float4* __restrict__ out) {
+  const int64_t P = (int64_t)gp.W * gp.H;
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < P; p += (int64_t)gridDim.x * blockDim.x) {
+    const RayG r = make_ray(gp, (int)(p % gp.W), (int)(p / gp.W));
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (r.t_out > r.t_in) {
+      for (int64_t i = 0;; ++i) {
+        const float t = r.t_in + ((float)i + 0.5f) * r.dt;
+        if (!(t < r.t_out)) break;
+        float c[3];
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+          const float pp = r.o[q] + t * r.d[q];
+          c[q] = (pp - r.bmin[q]) * r.scale;
+        }
+        bool inside = true;
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+          const float fl = floorf(c[q]);
+          inside &= fl >= 0.0f && fl < (float)gp.dims[q];
+        }
+        if (!inside) continue;
+        const float4 s = classify(gp, sample_trilinear(gp, c));
+        const float tr = 1.0f - acc.w;
+        acc.x = fmaf(tr, s.x, acc.x);
+        acc.y = fmaf(tr, s.y, acc.y);
+        acc.z = fmaf(tr, s.z, acc.z);
+        acc.w = fmaf(tr, s.w, acc.w);
+      }
+    }
+    out[p] = acc;
+  }
+}
+
+cudaError_t launch_dvr(const GenParams& gp, float4* out, cudaStream_t st) {
+  const int64_t P = (int64_t)gp.W * gp.H;
+  const unsigned blocks = (unsigned)((P + 127) / 128);
+  dvr_kernel<<<blocks ? blocks : 1, 128, 0, st>>>(gp, out);
+  return cudaGetLastError();
 }
 
 __global__ void u32_to_u8_kernel(const uint32_t* __restrict__ in, uint8_t* __restrict__ out, size_t n) {

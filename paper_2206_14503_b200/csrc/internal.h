@@ -132,7 +132,9 @@ struct GenParams {
   int k;
   int max_iters;
   float gamma_max;
+  int limit;  // 1: one S~ per sub-domain intersection (gamma = inf)
 };
+cudaError_t launch_dvr(const GenParams& gp, float4* out, cudaStream_t st);  // ground-truth DVR image [H][W]
 cudaError_t launch_gen_pass1(const GenParams& gp, uint32_t* count32, float* gamma, int* err,
                              cudaStream_t st);
 cudaError_t launch_gen_pass2(const GenParams& gp, const uint32_t* offset, const float* gamma,
