@@ -312,6 +312,15 @@ def _run_ours(args, world, rank, local, clk):
     rotations = [10.0 * r for r in range(args.rotations)]
     views = [0, 1] if not args.no_v1 else [0]
     sets = {}
+    # bound the resident input sets (~32 GB of HBM): the first set's size decides
+    cam_probe = synth.make_camera(W, H, view=0)
+    probe = [comp.generate_subvdi(vol, tft, cam_probe, dec, pe) for pe in local_ids]
+    set_bytes = sum(24 * p.total + 5 * W * H for p in probe)
+    max_sets = max(1, int((32 << 30) // max(1, set_bytes)))
+    while len(views) * len(rotations) > max_sets and len(rotations) > 1:
+        rotations = rotations[:-1]
+    if len(views) * len(rotations) > max_sets:
+        views = [0]
     for v in views:
         for a in rotations:
             cam = synth.make_camera(W, H, view=v, angle_deg=a)
@@ -566,6 +575,55 @@ def _run_ours(args, world, rank, local, clk):
                        "f-2's D2H; frames cycle over the protocol's input sets"}
         compe.close()
 
+    # ---- SURVEY §8(f) f4 (N = 1): the limit case (one S~ per sub-domain
+    # intersection composited to a plain image) timed like a
+    # step, and the rendering quality of the composited VDI from novel
+    # viewpoints (SSIM / PSNR vs DVR)
+    f4 = None
+    if G == 1 and not args.no_f4:
+        from evaluation import psnr, ssim, to_rgb
+        cl = vdi.Compositor(W, H, 32, 1, n, stream=stream)
+        lim = [cl.generate_subvdi(vol, tft, cam0, dec, pe, limit=True) for pe in range(n)]
+        lim = [vdi.DenseSubVDI(p.pe_id, p.total, p.count.clone(), p.offset.clone(), p.depth.clone(), p.rgba.clone())
+               for p in lim]
+        img = cl.composite_image(lim)
+        dv = cl.render_dvr(vol, tft, cam0, W, H)
+        torch.cuda.synchronize()
+        err = (img - dv).abs().max().item()
+        lm, dm = [], []
+        for _ in range(10):
+            flush.zero_()
+            ev0.record(stream)
+            cl.composite_image(lim, img)
+            ev1.record(stream)
+            torch.cuda.synchronize()
+            lm.append(ev0.elapsed_time(ev1))
+            ev0.record(stream)
+            cl.render_dvr(vol, tft, cam0, W, H)
+            ev1.record(stream)
+            torch.cuda.synchronize()
+            dm.append(ev0.elapsed_time(ev1))
+        recs = sum(p.total for p in lim)
+        frame(base, 0)
+        torch.cuda.synchronize()
+        qual = {}
+        for ang in (5.0, 20.0):
+            vc = synth.make_camera(W, H, view=0, angle_deg=ang)
+            gt = to_rgb(comp.render_dvr(vol, tft, vc, W, H), W, H)
+            nv = to_rgb(comp.render_novel_view(image, cam0, vc, cfg.dims, W, H), W, H)
+            qual[f"{ang:g}deg"] = {"ssim": ssim(nv, gt), "psnr_db": psnr(nv, gt)}
+        f4 = {"limit_case": {"ms_per_image": statistics.median(lm), "images_per_s": 1e3 / statistics.median(lm),
+                             "records": int(recs), "max_abs_err_vs_dvr": err,
+                             "dvr_ms_same_view": statistics.median(dm),
+                             "note": "vdi_composite_image over limit sub-VDIs (vdi_generate_limit, one S~ per "
+                                     "sub-domain intersection, PAPER.md:198) vs vdi_render_dvr of the whole volume"},
+              "novel_view_quality_vs_dvr": qual,
+              "quality_note": "the composited VDI of V0 rendered at V0 rotated by 5 / 20 degrees "
+                              "(vdi_render_novel_view) vs DVR at that view (vdi_render_dvr); SSIM 11x11 Gaussian, "
+                              "PSNR peak 1, RGB over black (PAPER.md:213, :364)"}
+        cl.close()
+        del lim
+
     # ---- CPU oracle baseline (rank 0, N = 1 only) + a parity band
     cpu = parity = None
     if rank == 0 and G == 1 and not args.no_cpu:
@@ -629,6 +687,7 @@ def _run_ours(args, world, rank, local, clk):
             "latency_mode": latency,
             "rotating_root": rotating,
             "full_representation_mode": full_rep,
+            "f4": f4,
             "supersegments_merged_per_s": S_total * value,
             "searched_lists": cnts[-1]["searched_lists"],
             "search_buckets": cnts[-1]["bucket_lists"], "fast_fallback_groups": cnts[-1]["fallback_groups"],
@@ -670,6 +729,7 @@ def main():
     ap.add_argument("--cpu-rows", type=int, default=64)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-f4", action="store_true", help="skip the limit-case / rendering-quality measurements")
     ap.add_argument("--rotating", action="store_true", help="N > 1: also time a root rotating over the frames")
     ap.add_argument("--frames", type=int, default=0, help="N > 1: VDIs per step (default 4)")
     args = ap.parse_args()

@@ -234,7 +234,7 @@ struct vdi_ctx {
   int xpar = 0;                          // parity of the exchange buffers of the current call
   // merge scratch
   DevBuf group_sum, group_base, wl, scratch, dcnt, stat_gamma, stat_m, stat_margin, srch, slots;
-  DevBuf lpool, lbatch;
+  DevBuf lpool;
   DevBuf g_misc;  // inflate counters
   // vdi_composite_fullrep: per-source dense scratch of the compaction + its scan
   std::vector<std::unique_ptr<DevBuf>> xdense;
@@ -388,15 +388,14 @@ static vdi_status reserve_merge(vdi_ctx* ctx, uint64_t P, uint64_t S_est, uint32
   CUDA_TRY(ctx, ctx->scratch.grow((size_t)general_threads(m_max) * 4 * std::max<uint32_t>(m_max, 1) * sizeof(Rec)));
   // short-list search pool: a list in bucket 0/1 has m > k_out samples, so at
   // most S / (k_out + 1) such lists exist; + one partial batch per bucket
-  const uint64_t pool_cap = std::min<uint64_t>((S_est / (k + 1) + 31) / 32 + 4, ng + 4);
+  // (at most 2 GB: lists that find no slot take the general path)
+  const uint64_t pool_cap =
+      std::min<uint64_t>(std::min<uint64_t>((S_est / (k + 1) + 31) / 32 + 4, ng + 4), (2ull << 30) / kShortSlotBytes);
   CUDA_TRY(ctx, ctx->srch.grow(pool_cap * kShortSlotBytes + 256));
-  // long-list pool: slots of stride maxm per 32-list batch; a list of bucket
-  // 2/3 has m > 40, so the pool needs at most 24 B x (S + 32 x batches of
-  // padding); batches <= S / 41 / 32 + 1 per bucket; + 32 rows x 32 lanes x
-  // 16 B of slack (the long sweeps read up to 24 rows past a list's end)
-  const uint64_t lb = S_est / 41 / 32 + 2;
-  CUDA_TRY(ctx, ctx->lpool.grow(24ull * S_est * 2 + lb * 2 * (128 + 24 * 32) + 4096 + 32 * 32 * 16));
-  CUDA_TRY(ctx, ctx->lbatch.grow((size_t)(P / 32 + 2) * 2 * 16));
+  // long-list search: warp-private slots (independent of S)
+  size_t lslot = 0;
+  const uint32_t lw = long_warps(m_max, &lslot);
+  CUDA_TRY(ctx, ctx->lpool.grow((size_t)lw * lslot));
   CUDA_TRY(ctx, ctx->g_misc.grow(sizeof(DevCounters) + 256));
   return VDI_OK;
 }
@@ -437,14 +436,11 @@ static vdi_status merge_lists(vdi_ctx* ctx, MergeParams& mp, uint64_t P, uint64_
     mp.pool_gap = reinterpret_cast<uint32_t*>(q);
     mp.pool_cap = (uint32_t)pool_cap;
   }
-  const unsigned long long lcap = ctx->lpool.bytes;
   mp.long_pool = ctx->lpool.as<char>();
-  mp.long_cap = lcap;
-  mp.long_batch[0] = ctx->lbatch.as<PoolBatch>();
-  mp.long_batch[1] = ctx->lbatch.as<PoolBatch>() + (P / 32 + 2);
+  mp.long_warps = long_warps(m_max, &mp.long_slot);
+  mp.long_maxm = std::min<uint32_t>(std::max<uint32_t>(m_max, 41), 1024);
   DevCounters* dc = ctx->dcnt.as<DevCounters>();
   CUDA_TRY(ctx, cudaMemsetAsync(dc, 0, sizeof(DevCounters), st));
-  mp.long_used = &dc->long_used;
   mp.group_base = ctx->group_base.as<uint32_t>();
   mp.out_count = so->count;
   mp.out_depth = reinterpret_cast<float2*>(so->depth);

@@ -14,13 +14,6 @@
 #define VDI_MAX_GRID_AXIS 16  // bricks per axis in a decomposition
 
 namespace vdi {
-// one 32-list batch of the long-list search pool
-struct PoolBatch {
-  unsigned long long off;  // byte offset in the pool
-  uint32_t maxm;           // longest list of the batch (slot stride)
-  uint32_t ok;             // 1 if the slot was allocated
-};
-
 // 24-byte record of the sub-supersegment scratch (AoS).
 struct Rec {
   float tf, tb, r, g, b, a;
@@ -86,11 +79,12 @@ struct MergeParams {
   uint32_t* pool_next;
   uint32_t pool_cap;
   uint32_t* batch_slot[2];
-  // long-list pool (buckets 2, 3): byte pool + per-batch {offset, stride, ok}
+  // long-list search (buckets 2, 3): long_warps warp-private slots of long_slot
+  // bytes, each [long_maxm + 32][32] rgba then [long_maxm][32] depth
   char* long_pool;
-  unsigned long long long_cap;
-  unsigned long long* long_used;
-  PoolBatch* long_batch[2];
+  size_t long_slot;
+  uint32_t long_maxm;
+  uint32_t long_warps;
   int* err;            // bit 0: work-list overflow (cannot happen: capacity = lists)
   int validate;
 };
@@ -113,6 +107,7 @@ cudaError_t launch_general(const MergeParams& mp, cudaStream_t st, int* launches
 // VDI_FLAG_PIXEL_STATS: tie margins of the searched lists (replays their bisection from the pools)
 cudaError_t launch_margins(const MergeParams& mp, cudaStream_t st, int* launches);
 uint32_t general_threads(uint32_t m_max);
+uint32_t long_warps(uint32_t m_max, size_t* slot_bytes);  // warps (and slot bytes) of the long-list search
 cudaError_t preload_merge();  // load every merge kernel now (loopback groups spin-wait across contexts)  // threads of the general kernel for lists of <= m_max records
 
 // Generator (generate.cu)

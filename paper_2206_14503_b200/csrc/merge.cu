@@ -972,151 +972,111 @@ __device__ __forceinline__ void sweep_batch(const MergeParams& mp, int bucket, u
 #endif
 
 // ---------------------------------------------------------------------------
-// Search path for long lists (40 < m <= 255): the lists of a warp (one batch
-// of 32 work-list entries) are written in depth order to a slot of a global
-// pool in [sample][lane] layout (rgba with the gap flag in the sign of alpha,
-// then depth), sized by the batch's longest list; the sweeps stream each
-// lane's column through a register double buffer (coalesced, independent of
-// the accumulator, and L2-resident across the bisection's sweeps).
+// Search path for long lists (m > 40), one fused kernel: every warp owns a
+// private slot of global memory ([sample][lane] layout: rgba with the gap flag
+// in the sign of alpha, then depth) that it refills batch after batch, so the
+// slots in flight stay resident in L2 while the bisection sweeps re-read them
+// (PAPER.md:176's "multiple passes" do not become HBM passes); the lists'
+// records are read from the sources once.
 // ---------------------------------------------------------------------------
+// Gather of the lanes' lists (valid lanes) into the slot columns orgba/odep
+// (stride 32): run-based k-way merge over the runs' head
+// t_front kept in registers, 8 records loaded per trip.  Returns false for a
+// transparent or overlapping record (Q23, Q12: the general path).
 template <int NS>
-__global__ void __launch_bounds__(128) long_gather_kernel(MergeParams mp) {
-  const int n = mp.n_src;
-  const uint32_t c2 = min(mp.wl_count[2], mp.wl_cap), c3 = min(mp.wl_count[3], mp.wl_cap);
-  const uint32_t nb2 = (c2 + 31) / 32, nb3 = (c3 + 31) / 32;
-  const uint32_t lane = threadIdx.x & 31;
-  // a warp claims one batch of 32 work-list entries at a time, the longest
-  // bucket (3) first
-  for (;;) {
-    uint32_t bt0 = 0;
-    if (lane == 0) bt0 = atomicAdd(&mp.search_ticket[3], 1u);
-    bt0 = __shfl_sync(kFull, bt0, 0);
-    if (bt0 >= nb2 + nb3) break;
-    const int bucket = bt0 < nb3 ? 3 : 2;
-    const uint32_t i = (bucket == 3 ? bt0 : bt0 - nb3) * 32 + lane;
-    const bool valid = i < (bucket == 2 ? c2 : c3);
-    const uint32_t* ent = mp.wl[bucket] + (size_t)(valid ? i : 0) * (3 + n);
-    const uint32_t p = valid ? ent[0] : 0u, m = valid ? ent[2] : 0u;
-    uint32_t goff[NS], cnt[NS];
+__device__ __forceinline__ bool long_gather_lane(const MergeParams& mp, uint32_t m, const uint32_t (&goff)[NS],
+                                                 const uint32_t (&cnt)[NS], float4* orgba, float2* odep) {
+  bool bad = false;
+  uint32_t hp[NS];
+  float ht[NS];  // t_front of each run's head, kept in registers (one load per record)
 #pragma unroll
-    for (int s = 0; s < NS; ++s) {
-      goff[s] = cnt[s] = 0;
-      if (valid && s < n) {
-        goff[s] = ent[3 + s];
-        cnt[s] = __ldg(mp.src[s].count + p);
-      }
-    }
-    const uint32_t maxm = __reduce_max_sync(kFull, m);
-    PoolBatch* pbt = mp.long_batch[bucket - 2] + (i >> 5);
-    unsigned long long off = 0;
-    if (lane == 0) {
-      const unsigned long long bytes = (unsigned long long)maxm * 32 * 24 + 128;
-      off = atomicAdd(mp.long_used, bytes);
-      const bool fits = off + bytes <= mp.long_cap;
-      *pbt = PoolBatch{off, maxm, fits ? 1u : 0u};
-    }
-    off = __shfl_sync(kFull, off, 0);
-    const bool fits = off + (unsigned long long)maxm * 32 * 24 + 128 <= mp.long_cap;
-    char* base = mp.long_pool + off;
-    float4* orgba = reinterpret_cast<float4*>(base) + lane;
-    float2* odep = reinterpret_cast<float2*>(base + (size_t)maxm * 32 * 16) + lane;
-    uint32_t* obad = reinterpret_cast<uint32_t*>(base + (size_t)maxm * 32 * 24) + lane;
-    bool bad = !fits;
-    if (valid && fits) {
-      uint32_t hp[NS];
-      float ht[NS];  // t_front of each run's head, kept in registers (one load per record)
+  for (int s = 0; s < NS; ++s) {
+    hp[s] = 0;
+    ht[s] = cnt[s] ? __ldg(&mp.src[s].depth[goff[s]].x) : CUDART_INF_F;
+  }
+  float prev_tb = -CUDART_INF_F;
+  uint32_t r = 0;
+  while (r < m) {
+    int b = -1, b2 = NS;
+    float bt = CUDART_INF_F, b2t = CUDART_INF_F;
 #pragma unroll
-      for (int s = 0; s < NS; ++s) {
-        hp[s] = 0;
-        ht[s] = cnt[s] ? __ldg(&mp.src[s].depth[goff[s]].x) : CUDART_INF_F;
-      }
-      float prev_tb = -CUDART_INF_F;
-      uint32_t r = 0;
-      while (r < m) {  // run-based k-way merge over the runs' head t_front values
-        int b = -1, b2 = NS;
-        float bt = CUDART_INF_F, b2t = CUDART_INF_F;
-#pragma unroll
-        for (int s = 0; s < NS; ++s)
-          if (hp[s] < cnt[s]) {
-            const float t = ht[s];
-            if (b < 0 || t < bt) {
-              if (b >= 0) {
-                b2t = bt;
-                b2 = b;
-              }
-              bt = t;
-              b = s;
-            } else if (t < b2t) {
-              b2t = t;
-              b2 = s;
-            }
+    for (int s = 0; s < NS; ++s)
+      if (hp[s] < cnt[s]) {
+        const float t = ht[s];
+        if (b < 0 || t < bt) {
+          if (b >= 0) {
+            b2t = bt;
+            b2 = b;
           }
-        uint32_t ii = 0, cb = 0, gb = 0;
-        const float2* dp = nullptr;
-        const float4* cp = nullptr;
+          bt = t;
+          b = s;
+        } else if (t < b2t) {
+          b2t = t;
+          b2 = s;
+        }
+      }
+    uint32_t ii = 0, cb = 0, gb = 0;
+    const float2* dp = nullptr;
+    const float4* cp = nullptr;
 #pragma unroll
-        for (int s = 0; s < NS; ++s)
-          if (s == b) {
-            ii = hp[s];
-            cb = cnt[s];
-            gb = goff[s];
-            dp = mp.src[s].depth;
-            cp = mp.src[s].rgba;
-          }
-        // take records of run b while they precede the next run's head
-        // (ties: lower PE first, Q11), 8 of them loaded per trip (the ones
-        // past the cut are reloaded, from L1/L2, when b is chosen again)
-        float tn = CUDART_INF_F;
-        for (bool first = true;;) {
-          const uint32_t nch = min(8u, cb - ii);
-          float2 dv[8];
-          float4 cv[8];
+    for (int s = 0; s < NS; ++s)
+      if (s == b) {
+        ii = hp[s];
+        cb = cnt[s];
+        gb = goff[s];
+        dp = mp.src[s].depth;
+        cp = mp.src[s].rgba;
+      }
+    // take records of run b while they precede the next run's head (ties:
+    // lower PE first, Q11), 8 loaded per trip (the ones past the cut are
+    // reloaded, from L1/L2, when b is chosen again)
+    float tn = CUDART_INF_F;
+    for (bool first = true;;) {
+      const uint32_t nch = min(8u, cb - ii);
+      float2 dv[8];
+      float4 cv[8];
 #pragma unroll
-          for (int u = 0; u < 8; ++u)
-            if ((uint32_t)u < nch) {
-              dv[u] = __ldg(dp + gb + ii + u);
-              cv[u] = __ldg(cp + gb + ii + u);
-            }
-          uint32_t taken = 0;
-          bool stop = false;
+      for (int u = 0; u < 8; ++u)
+        if ((uint32_t)u < nch) {
+          dv[u] = __ldg(dp + gb + ii + u);
+          cv[u] = __ldg(cp + gb + ii + u);
+        }
+      uint32_t taken = 0;
+      bool stop = false;
 #pragma unroll
-          for (int u = 0; u < 8; ++u)
-            if (!stop && (uint32_t)u < nch) {
-              const float2 d = dv[u];
-              if (!(first && u == 0) && !(d.x < b2t || (d.x == b2t && b < b2))) {
-                stop = true;
-                tn = d.x;
-              } else {
-                float4 c = cv[u];
-                bad |= c.w == 0.f || d.x < prev_tb;  // Q23 / Q12
-                if (r > 0 && d.x > prev_tb) c.w = -c.w;  // gap before this sample: sign of alpha
-                prev_tb = d.y;
-                orgba[r * 32] = c;
-                odep[r * 32] = d;
-                ++r;
-                ++taken;
-              }
-            }
-          ii += taken;
-          first = false;
-          if (stop) break;  // tn = head of run b
-          if (ii >= cb) {
-            tn = CUDART_INF_F;
-            break;
+      for (int u = 0; u < 8; ++u)
+        if (!stop && (uint32_t)u < nch) {
+          const float2 d = dv[u];
+          if (!(first && u == 0) && !(d.x < b2t || (d.x == b2t && b < b2))) {
+            stop = true;
+            tn = d.x;
+          } else {
+            float4 c = cv[u];
+            bad |= c.w == 0.f || d.x < prev_tb;  // Q23 / Q12
+            if (r > 0 && d.x > prev_tb) c.w = -c.w;  // gap before this sample: sign of alpha
+            prev_tb = d.y;
+            orgba[r * 32] = c;
+            odep[r * 32] = d;
+            ++r;
+            ++taken;
           }
         }
-#pragma unroll
-        for (int s = 0; s < NS; ++s)
-          if (s == b) {
-            hp[s] = ii;
-            ht[s] = tn;
-          }
+      ii += taken;
+      first = false;
+      if (stop) break;  // tn = head of run b
+      if (ii >= cb) {
+        tn = CUDART_INF_F;
+        break;
       }
     }
-    if (fits) *obad = bad ? 1u : 0u;
-    const int bk = (valid && bad) ? VDI_BUCKET_GENERAL : -1;  // overlap / alpha == 0, or no pool room
-    if (__any_sync(kFull, bk >= 0)) push_entries<NS>(mp, bk, p, m, goff, lane);
+#pragma unroll
+    for (int s = 0; s < NS; ++s)
+      if (s == b) {
+        hp[s] = ii;
+        ht[s] = tn;
+      }
   }
+  return !bad;
 }
 
 // Eight steps of a count-mode sweep over a pool column (same decisions as
@@ -1194,6 +1154,47 @@ __device__ __forceinline__ int long_count(const float4* __restrict__ col, int m,
   return sc;
 }
 
+// long_count with the warp in lock step: every lane sweeps the same rows at
+// the same time (coalesced 512-B row loads of the slot), the loop ends when
+// no lane still needs a sample (its bisection active, q < m, count <= k).
+// Lanes that went past their end keep stepping harmlessly: samples past m are
+// not counted, and extra constraints only shrink the memo interval.
+__device__ __forceinline__ int long_count_sync(const float4* __restrict__ col, int m, float g2, int k, bool act,
+                                               float& L, float& U) {
+  float ar = 0.f, ag = 0.f, ab = 0.f, aa = 0.f;
+  int sc = 0;
+  L = -1.f;
+  U = CUDART_INF_F;
+  float4 A[8], B[8], C[8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    A[u] = col[u * 32];
+    B[u] = col[(8 + u) * 32];
+  }
+  const float4* pp = col + 16 * 32;
+  for (int q0 = 0;;) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) C[u] = pp[u * 32];
+    pp += 8 * 32;
+    long_step8(A, q0, m, g2, ar, ag, ab, aa, sc, L, U);
+    q0 += 8;
+    if (!__any_sync(kFull, act && q0 < m && sc <= k)) break;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) A[u] = pp[u * 32];
+    pp += 8 * 32;
+    long_step8(B, q0, m, g2, ar, ag, ab, aa, sc, L, U);
+    q0 += 8;
+    if (!__any_sync(kFull, act && q0 < m && sc <= k)) break;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) B[u] = pp[u * 32];
+    pp += 8 * 32;
+    long_step8(C, q0, m, g2, ar, ag, ab, aa, sc, L, U);
+    q0 += 8;
+    if (!__any_sync(kFull, act && q0 < m && sc <= k)) break;
+  }
+  return sc;
+}
+
 // The final write sweep over a pool column (same decisions and output as
 // sweep(), the gap taken from the sign of alpha): rgba and depth in chunks of
 // 8 with the next chunk's loads in flight, so the sweep does not wait on one
@@ -1254,10 +1255,10 @@ __device__ __forceinline__ int long_write(const float4* __restrict__ col, const 
   return c;
 }
 
-// Few long lists (C4: ~1000 at 1080p) leave the lane-per-list sweep latency
-// bound: ~34 warps on the whole GPU, each lane running ~10 dependent sweeps.
-// Then every list gets a warp: lane j (heap node j + 1 of the next five
-// bisection levels) evaluates the midpoint the sequential procedure would
+// Few long lists (C4: ~1000 at 1080p) would leave a lane-per-list sweep
+// latency bound (~34 warps on the whole GPU, each lane running ~10 dependent
+// sweeps).  Then every list gets a warp: lane j (heap node j + 1 of the next
+// five bisection levels) evaluates the midpoint the sequential procedure would
 // reach along that path (the same fp32 mid = 0.5 (lo + hi) recurrence), all
 // lanes sweep the same samples (broadcast loads), and the warp walks the five
 // levels with the counts, stopping where the procedure stops (count == k_out,
@@ -1265,108 +1266,130 @@ __device__ __forceinline__ int long_write(const float4* __restrict__ col, const 
 #ifndef VDI_SPEC_MAX
 #define VDI_SPEC_MAX 8192
 #endif
-__device__ __forceinline__ void long_spec_body(const MergeParams& mp) {
+__device__ __forceinline__ float long_spec_bisect(const MergeParams& mp, const float4* col, int m, int lane) {
+  const int k = mp.k_out;
+  const uint32_t jn = lane < 31 ? (uint32_t)lane + 1 : 1u;  // heap node of this lane
+  const int depth = 31 - __clz(jn);
+  float lo = 0.f, hi = mp.gamma_max, best = mp.gamma_max;
+  int it = 0;
+  bool done = mp.max_iters <= 0;
+  while (!done) {
+    float lw = lo, hg = hi, md = 0.5f * (lw + hg);
+    for (int b = depth - 1; b >= 0; --b) {  // bit 1: count > k (lo = mid), bit 0: count <= k (hi = mid)
+      if ((jn >> b) & 1u) lw = md;
+      else hg = md;
+      md = 0.5f * (lw + hg);
+    }
+    float L, U;
+    const int c = long_count(col, m, md * md, k, L, U);
+    uint32_t node = 1;
+    for (int lev = 0; lev < 5 && !done; ++lev) {
+      const int cn = __shfl_sync(kFull, c, (int)node - 1);
+      const float mid = __shfl_sync(kFull, md, (int)node - 1);
+      if (cn <= k) {
+        best = hi = mid;
+        if (cn == k) done = true;
+        node = 2 * node;
+      } else {
+        lo = mid;
+        node = 2 * node + 1;
+      }
+      if (++it >= mp.max_iters) done = true;
+    }
+  }
+  return best;
+}
+
+#ifndef VDI_LONG_SYNC
+#define VDI_LONG_SYNC 1  // lock-step sweeps (coalesced) vs lanes sweeping independently
+#endif
+#ifndef VDI_LONG_WPS
+#define VDI_LONG_WPS 8  // resident long-search warps per SM (their slots in flight stay in L2)
+#endif
+template <int NS>
+__global__ void __launch_bounds__(32) long_search_kernel(MergeParams mp) {
   const int lane = threadIdx.x;
   const int k = mp.k_out, n = mp.n_src;
   const uint32_t c2 = min(mp.wl_count[2], mp.wl_cap), c3 = min(mp.wl_count[3], mp.wl_cap);
-  const uint32_t jn = lane < 31 ? (uint32_t)lane + 1 : 1u;  // heap node of this lane
-  const int depth = 31 - __clz(jn);
+  const uint32_t cap = mp.long_maxm;  // rows of a slot
+  char* slot = mp.long_pool + (size_t)blockIdx.x * mp.long_slot;
+  float4* col0 = reinterpret_cast<float4*>(slot);
+  float2* dcol0 = reinterpret_cast<float2*>(slot + (size_t)(cap + 32) * 32 * 16);
+  const bool spec = c2 + c3 <= VDI_SPEC_MAX;
+  const uint32_t nb2 = (c2 + 31) / 32, nb3 = (c3 + 31) / 32;
   for (;;) {
+    // claim: a batch of 32 lists (lane = list), or one list (spec: the warp)
     uint32_t t = 0;
-    if (lane == 0) t = atomicAdd(&mp.search_ticket[4], 1u);
+    if (lane == 0) t = atomicAdd(&mp.search_ticket[spec ? 4 : 3], 1u);
     t = __shfl_sync(kFull, t, 0);
-    if (t >= c2 + c3) break;
-    const int bucket = t < c3 ? 3 : 2;
-    const uint32_t e = t < c3 ? t : t - c3;
-    const PoolBatch pb = mp.long_batch[bucket - 2][e >> 5];
-    if (!pb.ok) continue;
-    const uint32_t* ent = mp.wl[bucket] + (size_t)e * (3 + n);
-    const uint32_t p = ent[0];
-    const int m = (int)ent[2];
-    const char* base = mp.long_pool + pb.off;
-    const uint32_t l = e & 31;
-    const float4* col = reinterpret_cast<const float4*>(base) + l;
-    const float2* dcol = reinterpret_cast<const float2*>(base + (size_t)pb.maxm * 32 * 16) + l;
-    const bool bad = reinterpret_cast<const uint32_t*>(base + (size_t)pb.maxm * 32 * 24)[l] != 0u;
-    if (bad) continue;
-    float lo = 0.f, hi = mp.gamma_max, best = mp.gamma_max;
-    int it = 0;
-    bool done = mp.max_iters <= 0;
-    while (!done) {
-      float lw = lo, hg = hi, md = 0.5f * (lw + hg);
-      for (int b = depth - 1; b >= 0; --b) {  // bit 1: count > k (lo = mid), bit 0: count <= k (hi = mid)
-        if ((jn >> b) & 1u) lw = md;
-        else hg = md;
-        md = 0.5f * (lw + hg);
-      }
-      float L, U;
-      const int c = long_count(col, m, md * md, k, L, U);
-      uint32_t node = 1;
-      for (int lev = 0; lev < 5 && !done; ++lev) {
-        const int cn = __shfl_sync(kFull, c, (int)node - 1);
-        const float mid = __shfl_sync(kFull, md, (int)node - 1);
-        if (cn <= k) {
-          best = hi = mid;
-          if (cn == k) done = true;
-          node = 2 * node;
-        } else {
-          lo = mid;
-          node = 2 * node + 1;
-        }
-        if (++it >= mp.max_iters) done = true;
+    if (t >= (spec ? c2 + c3 : nb2 + nb3)) break;
+    uint32_t e;
+    int bucket;
+    bool valid;
+    if (spec) {
+      bucket = t < c3 ? 3 : 2;  // the longest bucket first
+      e = t < c3 ? t : t - c3;
+      valid = lane == 0;        // lane 0 gathers the list into column 0
+    } else {
+      bucket = t < nb3 ? 3 : 2;
+      e = (t < nb3 ? t : t - nb3) * 32 + lane;
+      valid = e < (bucket == 2 ? c2 : c3);
+    }
+    const uint32_t* ent = mp.wl[bucket] + (size_t)(valid ? e : (spec ? e : 0)) * (3 + n);
+    const uint32_t p = (valid || spec) ? ent[0] : 0u, m = (valid || spec) ? ent[2] : 0u;
+    uint32_t goff[NS], cnt[NS];
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      goff[s] = cnt[s] = 0;
+      if (valid && s < n) {
+        goff[s] = ent[3 + s];
+        cnt[s] = __ldg(mp.src[s].count + p);
       }
     }
-    if (lane == 0) {
-      const int c = long_write(col, dcol, m, best, k, mp.out_depth + (size_t)p * k, mp.out_rgba + (size_t)p * k);
-      mp.out_count[p] = (uint8_t)c;
-      if (mp.stat_gamma) mp.stat_gamma[p] = best;
-    }
-  }
-}
-
-#ifndef VDI_LONG_WPS
-#define VDI_LONG_WPS 16  // resident long-sweep warps per SM
+    bool bad = valid && m > cap;  // cannot hold it: general path
+    if (valid && !bad) bad = !long_gather_lane<NS>(mp, m, goff, cnt, col0 + (spec ? 0 : lane), dcol0 + (spec ? 0 : lane));
+    __syncwarp();  // the slot columns are complete (and visible to the warp)
+    if (__any_sync(kFull, bad)) push_entries<NS>(mp, bad ? VDI_BUCKET_GENERAL : -1, p, m, goff, lane);
+    if (spec) {
+      if (__shfl_sync(kFull, bad ? 1 : 0, 0)) continue;
+      const float best = long_spec_bisect(mp, col0, (int)m, lane);
+      if (lane == 0) {
+        const int c = long_write(col0, dcol0, (int)m, best, k, mp.out_depth + (size_t)p * k, mp.out_rgba + (size_t)p * k);
+        mp.out_count[p] = (uint8_t)c;
+        if (mp.stat_gamma) mp.stat_gamma[p] = best;
+      }
+    } else {
+      // bisection (Q3-Q6), memoised per lane, the
+      // warp sweeping in lock step (coalesced slot rows)
+      const bool ok = valid && !bad;
+      const float4* col = col0 + lane;
+      Bisection bs;
+      bs.init(mp.gamma_max, ok && mp.max_iters > 0);
+#if VDI_LONG_SYNC
+      for (;;) {
+        bs.advance(k, mp.max_iters);
+        if (!__any_sync(kFull, bs.active)) break;
+        float L, U;
+        const int c = long_count_sync(col, ok ? (int)m : 0, bs.g2, k, bs.active, L, U);
+        if (bs.active) bs.swept(c, L, U, k, mp.max_iters);
+      }
+#else
+      for (;;) {
+        bs.advance(k, mp.max_iters);
+        if (!bs.active) break;
+        float L, U;
+        const int c = long_count(col, (int)m, bs.g2, k, L, U);
+        bs.swept(c, L, U, k, mp.max_iters);
+      }
 #endif
-__global__ void __launch_bounds__(32) long_sweep_kernel(MergeParams mp) {
-  const int k = mp.k_out, n = mp.n_src;
-  const uint32_t c2 = min(mp.wl_count[2], mp.wl_cap), c3 = min(mp.wl_count[3], mp.wl_cap);
-  if (c2 + c3 <= VDI_SPEC_MAX) {  // few lists: a warp per list
-    long_spec_body(mp);
-    return;
-  }
-  // every lane claims its own lists (lanes diverge freely here: no warp
-  // collectives), the longest bucket first, so a lane that finishes early
-  // takes the next list instead of idling until the warp's longest list ends
-  for (;;) {
-    const uint32_t t = atomicAdd(&mp.search_ticket[2], 1u);
-    if (t >= c2 + c3) break;
-    const int bucket = t < c3 ? 3 : 2;
-    const uint32_t e = t < c3 ? t : t - c3;
-    const PoolBatch pb = mp.long_batch[bucket - 2][e >> 5];
-    if (!pb.ok) continue;
-    const uint32_t* ent = mp.wl[bucket] + (size_t)e * (3 + n);
-    const uint32_t p = ent[0];
-    const int m = (int)ent[2];
-    const char* base = mp.long_pool + pb.off;
-    const uint32_t l = e & 31;
-    const float4* col = reinterpret_cast<const float4*>(base) + l;
-    const float2* dcol = reinterpret_cast<const float2*>(base + (size_t)pb.maxm * 32 * 16) + l;
-    const bool bad = reinterpret_cast<const uint32_t*>(base + (size_t)pb.maxm * 32 * 24)[l] != 0u;
-    if (bad) continue;
-    // bisection (Q3-Q6)
-    Bisection bs;
-    bs.init(mp.gamma_max, mp.max_iters > 0);
-    for (;;) {
-      bs.advance(k, mp.max_iters);
-      if (!bs.active) break;
-      float L, U;
-      const int c = long_count(col, m, bs.g2, k, L, U);
-      bs.swept(c, L, U, k, mp.max_iters);
+      if (ok) {
+        const int c = long_write(col, dcol0 + lane, (int)m, bs.best, k, mp.out_depth + (size_t)p * k,
+                                 mp.out_rgba + (size_t)p * k);
+        mp.out_count[p] = (uint8_t)c;
+        if (mp.stat_gamma) mp.stat_gamma[p] = bs.best;
+      }
     }
-    const float best = bs.best;
-    const int c = long_write(col, dcol, m, best, k, mp.out_depth + (size_t)p * k, mp.out_rgba + (size_t)p * k);
-    mp.out_count[p] = (uint8_t)c;
-    if (mp.stat_gamma) mp.stat_gamma[p] = best;
+    __syncwarp();  // every lane is done with the slot before the next batch overwrites it
   }
 }
 
@@ -1515,49 +1538,55 @@ __global__ void __launch_bounds__(kSlowThreads) merge_general_kernel(MergeParams
 }
 
 // Tie margins of the searched lists (VDI_FLAG_PIXEL_STATS, debug): thread per
-// work-list entry of buckets 0-3, replaying the bisection and the final sweep
-// (the same procedure as the search kernels: same gamma*, same comparisons)
-// over the depth-ordered samples the gather kernels left in the pools, with
-// the margin min |sqrt(D^2) - gamma| of every executed comparison in double.
-__global__ void __launch_bounds__(128) margins_kernel(MergeParams mp) {
+// work-list entry of buckets 0-3 (scratch slice of the general path), the
+// list gathered in depth order from its sources (step 1) and its bisection and
+// final sweep replayed (the same procedure as the search kernels: same gamma*,
+// same comparisons), with the margin min |sqrt(D^2) - gamma| of every
+// executed comparison in double.  Lists with transparent or overlapping
+// records are the general path's (it records their margins).
+__global__ void __launch_bounds__(kSlowThreads) margins_kernel(MergeParams mp) {
   const uint32_t c[4] = {min(mp.wl_count[0], mp.wl_cap), min(mp.wl_count[1], mp.wl_cap),
                          min(mp.wl_count[2], mp.wl_cap), min(mp.wl_count[3], mp.wl_cap)};
   const uint32_t tot = c[0] + c[1] + c[2] + c[3];
   const int n = mp.n_src, k = mp.k_out;
+  const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x;
   unsigned long long steps = 0;
+  Rec* A = mp.scratch + (size_t)tid * mp.gen_stride;
   const uint32_t t_end = (tot + 31) / 32 * 32;  // whole warps iterate (warp reduction below)
-  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < t_end; t += gridDim.x * blockDim.x) {
+  for (uint32_t t = tid; t < t_end && tid < mp.gen_threads; t += mp.gen_threads) {
     if (t >= tot) continue;
     int b = 0;
     uint32_t e = t;
     while (e >= c[b]) e -= c[b++];
     const uint32_t* ent = mp.wl[b] + (size_t)e * (3 + n);
     const uint32_t p = ent[0];
-    const int m = (int)ent[2];
-    const float4* col;
-    const float2* dcol;
-    if (b < 2) {
-      const uint32_t slot = mp.batch_slot[b][e >> 5];
-      if (slot >= mp.pool_cap) continue;
-      const uint32_t* gp = mp.pool_gap + (size_t)slot * 64 + (e & 31);
-      if (gp[0] == 0xffffffffu && gp[32] == 0xffffffffu) continue;  // general path
-      col = mp.pool_rgba + (size_t)slot * 40 * 32 + (e & 31);
-      dcol = mp.pool_depth + (size_t)slot * 40 * 32 + (e & 31);
-    } else {
-      const PoolBatch pb = mp.long_batch[b - 2][e >> 5];
-      if (!pb.ok) continue;
-      const char* base = mp.long_pool + pb.off;
-      if (reinterpret_cast<const uint32_t*>(base + (size_t)pb.maxm * 32 * 24)[e & 31]) continue;
-      col = reinterpret_cast<const float4*>(base) + (e & 31);
-      dcol = reinterpret_cast<const float2*>(base + (size_t)pb.maxm * 32 * 16) + (e & 31);
+    uint32_t pos[VDI_MAX_SRC], end[VDI_MAX_SRC];
+    for (int s = 0; s < n; ++s) {
+      pos[s] = ent[3 + s];
+      end[s] = pos[s] + __ldg(mp.src[s].count + p);
     }
-    // pool samples carry the gap flag in the sign of alpha; rebuild records whose
-    // t_front exceeds the previous t_back exactly where a gap was flagged
-    auto get = [&](int i) {
-      const float4 v = col[(size_t)i * 32];
-      const float2 d = dcol[(size_t)i * 32];
-      return Rec{d.x, d.y, v.x, v.y, v.z, fabsf(v.w)};
-    };
+    int m = 0;
+    bool bad = false;
+    for (;;) {
+      int best = -1;
+      float bt = 0.f;
+      for (int s = 0; s < n; ++s)
+        if (pos[s] < end[s]) {
+          const float tt = __ldg(&mp.src[s].depth[pos[s]].x);
+          if (best < 0 || tt < bt) {
+            best = s;
+            bt = tt;
+          }
+        }
+      if (best < 0) break;
+      const float2 d = __ldg(mp.src[best].depth + pos[best]);
+      const float4 cc = __ldg(mp.src[best].rgba + pos[best]);
+      pos[best]++;
+      bad |= cc.w == 0.f || (m > 0 && d.x < A[m - 1].tb);
+      A[m++] = Rec{d.x, d.y, cc.x, cc.y, cc.z, cc.w};
+    }
+    if (bad) continue;
+    auto get = [&](int i) { return A[i]; };
     double mgn = CUDART_INF;
     unsigned long long st = 0;
     const float g = bisect(get, m, k, mp.max_iters, mp.gamma_max, &mgn, &st);
@@ -1761,20 +1790,18 @@ static cudaError_t launch_search_ns(const MergeParams& mp, cudaStream_t st, int*
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     ++*launches;
   }
-  {
-    static int per_sm = 0;  // resident blocks: the warps claim batches dynamically
-    if (!per_sm) {
-      if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, long_gather_kernel<NS>, 128, 0)) != cudaSuccess)
-        return e;
-      if (per_sm < 1) per_sm = 1;
-    }
-    long_gather_kernel<NS><<<sm_count() * per_sm, 128, 0, st>>>(mp);
-  }
-  if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  ++*launches;
-  long_sweep_kernel<<<sm_count() * VDI_LONG_WPS, 32, 0, st>>>(mp);
+  long_search_kernel<NS><<<mp.long_warps, 32, 0, st>>>(mp);
   ++*launches;
   return cudaGetLastError();
+}
+
+uint32_t long_warps(uint32_t m_max, size_t* slot_bytes) {
+  // warp-private slots of min(m_max, 1024) rows (+32 rows of read slack); at
+  // most VDI_LONG_WPS warps per SM and ~1 GB of slots
+  const uint32_t rows = std::min<uint32_t>(std::max<uint32_t>(m_max, 41), 1024);
+  *slot_bytes = ((size_t)(rows + 32) * 32 * 16 + (size_t)rows * 32 * 8 + 255) & ~(size_t)255;
+  const uint64_t fit = (1ull << 30) / *slot_bytes;
+  return (uint32_t)std::max<uint64_t>(148, std::min<uint64_t>(fit, (uint64_t)sm_count() * VDI_LONG_WPS));
 }
 
 uint32_t general_threads(uint32_t m_max) {
@@ -1791,7 +1818,7 @@ cudaError_t launch_general(const MergeParams& mp, cudaStream_t st, int* launches
 }
 
 cudaError_t launch_margins(const MergeParams& mp, cudaStream_t st, int* launches) {
-  margins_kernel<<<sm_count() * 8, 128, 0, st>>>(mp);
+  margins_kernel<<<(mp.gen_threads + kSlowThreads - 1) / kSlowThreads, kSlowThreads, 0, st>>>(mp);
   ++*launches;
   return cudaGetLastError();
 }
@@ -1819,7 +1846,7 @@ template <int NS>
 static void preload_ns(cudaFuncAttributes* fa) {
   cudaFuncGetAttributes(fa, merge_fast_kernel<NS>);
   cudaFuncGetAttributes(fa, search_gather_kernel<NS>);
-  cudaFuncGetAttributes(fa, long_gather_kernel<NS>);
+  cudaFuncGetAttributes(fa, long_search_kernel<NS>);
 }
 
 cudaError_t preload_merge() {
@@ -1833,7 +1860,6 @@ cudaError_t preload_merge() {
   cudaFuncGetAttributes(&fa, chunk_sums_kernel);
   cudaFuncGetAttributes(&fa, group_base_kernel);
   cudaFuncGetAttributes(&fa, search_sweep_kernel);
-  cudaFuncGetAttributes(&fa, long_sweep_kernel);
   cudaFuncGetAttributes(&fa, merge_general_kernel);
   cudaFuncGetAttributes(&fa, margins_kernel);
   cudaFuncGetAttributes(&fa, sum_u32_kernel);

@@ -16,7 +16,7 @@ from parity import compare
 
 pytestmark = pytest.mark.gpu
 
-CONFIGS = ["C2", "C3", "C4", "C5"]
+CONFIGS = [("C2", 0), ("C3", 0), ("C4", 0), ("C5", 0), ("C5", 16)]  # C5 strong-scaling sweep: up to 16 PEs (m <= 512)
 
 
 @pytest.fixture(scope="module")
@@ -42,9 +42,9 @@ def _lists_at(pe, pix, k):
     return cnt, d, c
 
 
-@pytest.mark.parametrize("name", CONFIGS)
-def test_end_to_end_sampled(vdi, orc, name):
-    cfg = synth.config_by_name(name)
+@pytest.mark.parametrize("name,pes", CONFIGS, ids=[f"{c}-{p or 'default'}" for c, p in CONFIGS])
+def test_end_to_end_sampled(vdi, orc, name, pes):
+    cfg = synth.config_by_name(name, n_pes=pes) if pes else synth.config_by_name(name)
     W, H, n = cfg.W, cfg.H, cfg.n_pes
     vol = synth.make_volume(cfg, device="cuda")
     tf = synth.tf_table(cfg.tf, cfg.tf_scale)
@@ -62,9 +62,10 @@ def test_end_to_end_sampled(vdi, orc, name):
     srch = np.nonzero(m > cfg.k_out)[0]
     busy = np.nonzero(m > 0)[0]
     pix = np.unique(np.concatenate([
-        rng.choice(W * H, 100, replace=False),
-        rng.choice(busy, min(100, len(busy)), replace=False) if len(busy) else [],
-        rng.choice(srch, min(100, len(srch)), replace=False) if len(srch) else [],
+        rng.choice(W * H, 1000, replace=False),
+        rng.choice(busy, min(1000, len(busy)), replace=False) if len(busy) else [],
+        rng.choice(srch, min(1000, len(srch)), replace=False) if len(srch) else [],
+        np.argsort(m)[-20:],  # the longest lists
     ]).astype(np.int64))
     # the oracle regenerates the sampled rays itself
     sc = orc.scene(orc.volume_numpy(vol), cfg.dims, tf, cam, dec)
