@@ -301,10 +301,13 @@ vdi_status vdi_gather_root(vdi_ctx* ctx, uint32_t root, const vdi_full_view* str
  * vdi_gather of that frame bit for bit.  local_pes: [n_frames][n_local]
  * (frame-major) dense views homed on this rank; images[n_frames]: full
  * representations of rows [0, H), read only for the frames this rank is the
- * root of (others may be zeroed structs).  The call is complete when the
- * caller's stream passes it; never synchronises the host.  ctx-owned scratch:
- * two strips (rows*W*(1 + 24 k_out) bytes each).  n_ranks == 1: one
- * vdi_composite per frame into images[f]. */
+ * root of (others may be zeroed structs); distinct buffers per frame (frames
+ * overlap: frame f's search kernels run on a third ctx-owned stream beside
+ * frame f+1's pass-through, with two parities of merge scratch; not with
+ * VDI_FLAG_PIXEL_STATS).  The call is complete when the caller's stream
+ * passes it; never synchronises the host.  ctx-owned scratch: two strips
+ * (rows*W*(1 + 24 k_out) bytes each) and a second set of merge scratch.
+ * n_ranks == 1: frames in flight on one GPU, images[f] written whole. */
 vdi_status vdi_composite_frames(vdi_ctx* ctx, uint32_t n_frames, const vdi_dense_view* local_pes,
                                 uint32_t n_local, vdi_full_view* images, const uint32_t* roots);
 

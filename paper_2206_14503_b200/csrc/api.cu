@@ -18,6 +18,7 @@
 #include <condition_variable>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -232,9 +233,17 @@ struct vdi_ctx {
   cudaStream_t xst = nullptr;            // vdi_composite_frames: the push stream
   cudaStream_t xpst = nullptr;           // push stream of the current call (null: the ctx stream)
   int xpar = 0;                          // parity of the exchange buffers of the current call
-  // merge scratch
-  DevBuf group_sum, group_base, wl, scratch, dcnt, stat_gamma, stat_m, stat_margin, srch, slots;
-  DevBuf lpool;
+  // merge scratch; the work lists, counters and search pools come in two
+  // parities (frames in flight: frame f's search overlaps frame f+1's pass-through)
+  DevBuf group_sum, group_base, stat_gamma, stat_m, stat_margin;
+  struct MScratch {
+    DevBuf wl, slots, dcnt, scratch, srch, lpool;
+  } ms[2];
+  int mpar = 0;                   // parity of the current merge
+  int last_mpar = 0;              // parity of the last merge (counters)
+  cudaStream_t msst = nullptr;    // search stream of the current merge (null: the ctx stream)
+  cudaStream_t sst = nullptr;     // vdi_composite_frames: the search stream
+  cudaEvent_t mev_fast[2] = {}, mev_done[2] = {};
   DevBuf g_misc;  // inflate counters
   // vdi_composite_fullrep: per-source dense scratch of the compaction + its scan
   std::vector<std::unique_ptr<DevBuf>> xdense;
@@ -267,6 +276,14 @@ struct vdi_ctx {
   cudaEvent_t gev_in = nullptr, gev_out = nullptr;
   DevBuf fs_count[2], fs_depth[2], fs_rgba[2];
   ~vdi_ctx() {
+    if (sst) {
+      cudaStreamSynchronize(sst);
+      cudaStreamDestroy(sst);
+    }
+    for (int i = 0; i < 2; ++i) {
+      if (mev_fast[i]) cudaEventDestroy(mev_fast[i]);
+      if (mev_done[i]) cudaEventDestroy(mev_done[i]);
+    }
     if (xst) {
       cudaStreamSynchronize(xst);
       cudaStreamDestroy(xst);
@@ -371,31 +388,32 @@ vdi_status resolve_peers(vdi_ctx* ctx) {
 // so an estimate never changes a result); m_max bounds a list's records.
 // Buffers of a merge of P lists (grow-only; S_est sizes the search pools,
 // m_max the general path's per-thread scratch)
-static vdi_status reserve_merge(vdi_ctx* ctx, uint64_t P, uint64_t S_est, uint32_t m_max) {
+static vdi_status reserve_merge(vdi_ctx* ctx, uint64_t P, uint64_t S_est, uint32_t m_max, int b = 0) {
   const vdi_config& cf = ctx->cfg;
+  vdi_ctx::MScratch& sc = ctx->ms[b];
   const uint32_t n = cf.n_pes, k = cf.k_out;
   const size_t ng = (P + 31) / 32;
   CUDA_TRY(ctx, ctx->group_sum.grow((size_t)scan_chunks((uint32_t)P) * n * 4 + 64));
   CUDA_TRY(ctx, ctx->group_base.grow(ng * n * 4 + 64));
-  CUDA_TRY(ctx, ctx->wl.grow(((size_t)std::max<uint64_t>(P, 1) * (3 + n) * VDI_N_BUCKETS + 64) * 4));
-  CUDA_TRY(ctx, ctx->slots.grow((2 * ng + 64) * 4));
-  CUDA_TRY(ctx, ctx->dcnt.grow(sizeof(DevCounters)));
+  CUDA_TRY(ctx, sc.wl.grow(((size_t)std::max<uint64_t>(P, 1) * (3 + n) * VDI_N_BUCKETS + 64) * 4));
+  CUDA_TRY(ctx, sc.slots.grow((2 * ng + 64) * 4));
+  CUDA_TRY(ctx, sc.dcnt.grow(sizeof(DevCounters)));
   if (cf.flags & VDI_FLAG_PIXEL_STATS) {
     CUDA_TRY(ctx, ctx->stat_gamma.grow(P * 4 + 64));
     CUDA_TRY(ctx, ctx->stat_m.grow(P * 2 + 64));
     CUDA_TRY(ctx, ctx->stat_margin.grow(P * 4 + 64));
   }
-  CUDA_TRY(ctx, ctx->scratch.grow((size_t)general_threads(m_max) * 4 * std::max<uint32_t>(m_max, 1) * sizeof(Rec)));
+  CUDA_TRY(ctx, sc.scratch.grow((size_t)general_threads(m_max) * 4 * std::max<uint32_t>(m_max, 1) * sizeof(Rec)));
   // short-list search pool: a list in bucket 0/1 has m > k_out samples, so at
   // most S / (k_out + 1) such lists exist; + one partial batch per bucket
   // (at most 2 GB: lists that find no slot take the general path)
   const uint64_t pool_cap =
       std::min<uint64_t>(std::min<uint64_t>((S_est / (k + 1) + 31) / 32 + 4, ng + 4), (2ull << 30) / kShortSlotBytes);
-  CUDA_TRY(ctx, ctx->srch.grow(pool_cap * kShortSlotBytes + 256));
+  CUDA_TRY(ctx, sc.srch.grow(pool_cap * kShortSlotBytes + 256));
   // long-list search: warp-private slots (independent of S)
   size_t lslot = 0;
   const uint32_t lw = long_warps(m_max, &lslot);
-  CUDA_TRY(ctx, ctx->lpool.grow((size_t)lw * lslot));
+  CUDA_TRY(ctx, sc.lpool.grow((size_t)lw * lslot));
   CUDA_TRY(ctx, ctx->g_misc.grow(sizeof(DevCounters) + 256));
   return VDI_OK;
 }
@@ -410,6 +428,10 @@ static vdi_status merge_lists(vdi_ctx* ctx, MergeParams& mp, uint64_t P, uint64_
   const vdi_config& cf = ctx->cfg;
   const uint32_t n = cf.n_pes, k = cf.k_out;
   cudaStream_t st = ctx->stream;
+  const int b = ctx->mpar;
+  cudaStream_t sst = ctx->msst ? ctx->msst : st;  // the search kernels' stream
+  vdi_ctx::MScratch& sc = ctx->ms[b];
+  ctx->last_mpar = b;
   int launches = 0;
   mp.P = (uint32_t)P;
   mp.n_groups = (uint32_t)((P + 31) / 32);
@@ -417,18 +439,23 @@ static vdi_status merge_lists(vdi_ctx* ctx, MergeParams& mp, uint64_t P, uint64_
   mp.g_end = mp.n_groups;
   ctx->mP = P;
   const size_t ng = mp.n_groups;
-  if (vdi_status s = reserve_merge(ctx, P, S_est, m_max)) return s;
+  if (vdi_status s = reserve_merge(ctx, P, S_est, m_max, b)) return s;
   const bool stats = cf.flags & VDI_FLAG_PIXEL_STATS;
-  // One pass: pass-through -> search kernels -> general path on one stream.
-  // Measured on C3 (profiles/README.md): overlapping the search with the
-  // pass-through on a second stream is slower (the latency-bound search
-  // kernels run ~2x slower beside the HBM-bound pass-through).
+  // pass-through -> search kernels -> general path.  One VDI: one stream
+  // (within a VDI the search needs the pass-through's work lists; measured,
+  // profiles/README.md: overlapping them on a second stream runs the
+  // latency-bound search ~2x slower beside the HBM-bound pass-through).
+  // Frames in flight (vdi_composite_frames): the search kernels of this VDI
+  // run on a second stream beside the next VDI's pass-through, with their own
+  // parity of work lists, counters and pools (this parity's previous search
+  // must be done first).
+  if (sst != st) CUDA_TRY(ctx, cudaStreamWaitEvent(st, ctx->mev_done[b], 0));
   mp.wl_cap = (uint32_t)std::max<uint64_t>(P, 1);
   mp.gen_threads = general_threads(m_max);
   mp.gen_stride = 4 * std::max<uint32_t>(m_max, 1);
-  const uint64_t pool_cap = std::min<uint64_t>((ctx->srch.bytes - 256) / kShortSlotBytes, ng + 4);
+  const uint64_t pool_cap = std::min<uint64_t>((sc.srch.bytes - 256) / kShortSlotBytes, ng + 4);
   {
-    char* q = ctx->srch.as<char>();
+    char* q = sc.srch.as<char>();
     mp.pool_rgba = reinterpret_cast<float4*>(q);
     q += pool_cap * 40 * 32 * 16;
     mp.pool_depth = reinterpret_cast<float2*>(q);
@@ -436,10 +463,10 @@ static vdi_status merge_lists(vdi_ctx* ctx, MergeParams& mp, uint64_t P, uint64_
     mp.pool_gap = reinterpret_cast<uint32_t*>(q);
     mp.pool_cap = (uint32_t)pool_cap;
   }
-  mp.long_pool = ctx->lpool.as<char>();
+  mp.long_pool = sc.lpool.as<char>();
   mp.long_warps = long_warps(m_max, &mp.long_slot);
   mp.long_maxm = std::min<uint32_t>(std::max<uint32_t>(m_max, 41), 1024);
-  DevCounters* dc = ctx->dcnt.as<DevCounters>();
+  DevCounters* dc = sc.dcnt.as<DevCounters>();
   CUDA_TRY(ctx, cudaMemsetAsync(dc, 0, sizeof(DevCounters), st));
   mp.group_base = ctx->group_base.as<uint32_t>();
   mp.out_count = so->count;
@@ -447,7 +474,7 @@ static vdi_status merge_lists(vdi_ctx* ctx, MergeParams& mp, uint64_t P, uint64_
   mp.out_rgba = reinterpret_cast<float4*>(so->rgba);
   mp.fallback_groups = &dc->fallback_groups;
   mp.pool_next = &dc->pool_next;
-  mp.scratch = ctx->scratch.as<Rec>();
+  mp.scratch = sc.scratch.as<Rec>();
   mp.stat_gamma = stats ? ctx->stat_gamma.as<float>() : nullptr;
   mp.stat_m = stats ? ctx->stat_m.as<uint16_t>() : nullptr;
   mp.stat_margin = stats ? ctx->stat_margin.as<float>() : nullptr;
@@ -456,10 +483,17 @@ static vdi_status merge_lists(vdi_ctx* ctx, MergeParams& mp, uint64_t P, uint64_
   mp.sweep_steps = stats ? &dc->sweep_steps : nullptr;
   mp.err = &dc->err;
   mp.validate = (cf.flags & VDI_FLAG_VALIDATE) ? 1 : 0;
-  uint32_t* slp = ctx->slots.as<uint32_t>();
+  if (sst != st) {  // frames in flight: leave room for the next VDI's pass-through
+    static const float share = [] {
+      const char* e = getenv("VDI_SEARCH_SHARE");
+      return e ? (float)atof(e) : 1.0f;  // measured (C3, F = 4): 0.25 / 0.5 / 0.75 / 1.0 -> 0.528 / 0.396 / 0.365 / 0.357 ms per VDI
+    }();
+    mp.search_share = share;
+  }
+  uint32_t* slp = sc.slots.as<uint32_t>();
   mp.batch_slot[0] = slp;
   mp.batch_slot[1] = slp + ng + 32;
-  uint32_t* wlp = ctx->wl.as<uint32_t>();
+  uint32_t* wlp = sc.wl.as<uint32_t>();
   for (int b = 0; b < VDI_N_BUCKETS; ++b) mp.wl[b] = wlp + (size_t)b * mp.wl_cap * (3 + n);
   mp.wl_count = dc->wl_count;
   mp.search_ticket = dc->search_ticket;
@@ -472,10 +506,14 @@ static vdi_status merge_lists(vdi_ctx* ctx, MergeParams& mp, uint64_t P, uint64_
     // pass-through (writes every slot of the strip) -> search kernels -> general path
     CUDA_TRY(ctx, launch_fast(mp, st, &launches));
     if (timing) CUDA_TRY(ctx, cudaEventRecord(ctx->ev[4], st));
-    CUDA_TRY(ctx, launch_search(mp, st, &launches));
-    if (timing) CUDA_TRY(ctx, cudaEventRecord(ctx->ev[5], st));
-    CUDA_TRY(ctx, launch_general(mp, st, &launches));
-    if (stats) CUDA_TRY(ctx, launch_margins(mp, st, &launches));
+    if (sst != st) {
+      CUDA_TRY(ctx, cudaEventRecord(ctx->mev_fast[b], st));
+      CUDA_TRY(ctx, cudaStreamWaitEvent(sst, ctx->mev_fast[b], 0));
+    }
+    CUDA_TRY(ctx, launch_search(mp, sst, &launches));
+    if (timing) CUDA_TRY(ctx, cudaEventRecord(ctx->ev[5], sst));
+    CUDA_TRY(ctx, launch_general(mp, sst, &launches));
+    if (stats) CUDA_TRY(ctx, launch_margins(mp, sst, &launches));
   }
   launches_ref += launches;
   return VDI_OK;
@@ -1098,12 +1136,12 @@ static vdi_status exchange_recv(vdi_ctx* ctx, const vdi_dense_view* local, const
 }
 
 // after the merge: the senders may reuse this call's slots (XFREE)
-static vdi_status release_slots(vdi_ctx* ctx, int& launches) {
+static vdi_status release_slots(vdi_ctx* ctx, int& launches, cudaStream_t st = nullptr) {
   std::vector<uint32_t> senders;
   for (uint32_t g = 0; g < ctx->cfg.n_ranks; ++g)
     if (g != ctx->cfg.rank && ctx->lay.n_local(g)) senders.push_back(g);
   if (senders.empty()) return VDI_OK;
-  if (vdi_status s = signal_peers(ctx, XFREE, senders, ctx->xcalls, nullptr, ctx->xcalls)) return s;
+  if (vdi_status s = signal_peers(ctx, XFREE, senders, ctx->xcalls, st, ctx->xcalls)) return s;
   ++launches;
   return VDI_OK;
 }
@@ -1157,12 +1195,13 @@ vdi_status vdi_composite(vdi_ctx* ctx, const vdi_dense_view* local, uint32_t n_l
   }
   if (timing) CUDA_TRY(ctx, cudaEventRecord(ctx->ev[1], st));
   if (vdi_status s = merge_lists(ctx, mp, ctx->P, S_est, n * cf.k_in, so, timing, launches)) return s;
+  cudaStream_t sst = ctx->msst ? ctx->msst : st;  // where the merge ends
   if (G > 1) {
-    CUDA_TRY(ctx, cudaEventRecord(ctx->xev_merged[ctx->xpar], st));  // the exchange buffers of this parity are read
-    if (vdi_status s = release_slots(ctx, launches)) return s;
+    CUDA_TRY(ctx, cudaEventRecord(ctx->xev_merged[ctx->xpar], sst));  // the exchange buffers of this parity are read
+    if (vdi_status s = release_slots(ctx, launches, sst)) return s;
   }
   if (timing) {
-    CUDA_TRY(ctx, cudaEventRecord(ctx->ev[2], st));
+    CUDA_TRY(ctx, cudaEventRecord(ctx->ev[2], sst));
     ctx->timing_pending = true;
   }
   ctx->have_stats = cf.flags & VDI_FLAG_PIXEL_STATS;
@@ -1459,66 +1498,79 @@ vdi_status vdi_composite_frames(vdi_ctx* ctx, uint32_t F, const vdi_dense_view* 
   }
   cudaStream_t st = ctx->stream;
   const size_t P = ctx->P, o = (size_t)ctx->row0 * W;
-  if (G == 1) {
-    for (uint32_t f = 0; f < F; ++f) {
-      vdi_full_view so{0, H, images[f].count, images[f].depth, images[f].rgba};
-      if (vdi_status s = vdi_composite(ctx, local + (size_t)f * n_local, n_local, &so)) return s;
-    }
-    return VDI_OK;
-  }
-  if (vdi_status s = resolve_peers(ctx)) return s;
-  if (!ctx->gst) {
+  if (G > 1)
+    if (vdi_status s = resolve_peers(ctx)) return s;
+  // frame f's search kernels run on the search stream beside frame f+1's
+  // pass-through (not with VDI_FLAG_PIXEL_STATS: the statistics arrays are single)
+  const bool overlap = !(cf.flags & VDI_FLAG_PIXEL_STATS);
+  if (!ctx->sst) {
+    CUDA_TRY(ctx, cudaStreamCreateWithFlags(&ctx->sst, cudaStreamNonBlocking));
     CUDA_TRY(ctx, cudaStreamCreateWithFlags(&ctx->xst, cudaStreamNonBlocking));
     CUDA_TRY(ctx, cudaStreamCreateWithFlags(&ctx->gst, cudaStreamNonBlocking));
     CUDA_TRY(ctx, cudaEventCreateWithFlags(&ctx->gev_in, cudaEventDisableTiming));
     CUDA_TRY(ctx, cudaEventCreateWithFlags(&ctx->gev_out, cudaEventDisableTiming));
+    for (int i = 0; i < 2; ++i) {
+      CUDA_TRY(ctx, cudaEventCreateWithFlags(&ctx->mev_fast[i], cudaEventDisableTiming));
+      CUDA_TRY(ctx, cudaEventCreateWithFlags(&ctx->mev_done[i], cudaEventDisableTiming));
+    }
   }
-  for (int i = 0; i < 2; ++i) {
-    CUDA_TRY(ctx, ctx->fs_count[i].grow(P));
-    CUDA_TRY(ctx, ctx->fs_depth[i].grow(P * k * 8));
-    CUDA_TRY(ctx, ctx->fs_rgba[i].grow(P * k * 16));
-  }
-  // the push and inflate streams start once the caller's stream has reached this call
+  if (G > 1)
+    for (int i = 0; i < 2; ++i) {
+      CUDA_TRY(ctx, ctx->fs_count[i].grow(P));
+      CUDA_TRY(ctx, ctx->fs_depth[i].grow(P * k * 8));
+      CUDA_TRY(ctx, ctx->fs_rgba[i].grow(P * k * 16));
+    }
+  // the side streams start once the caller's stream has reached this call
   CUDA_TRY(ctx, cudaEventRecord(ctx->gev_in, st));
-  CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->gst, ctx->gev_in, 0));
-  CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->xst, ctx->gev_in, 0));
+  for (cudaStream_t x : {ctx->gst, ctx->xst, ctx->sst}) CUDA_TRY(ctx, cudaStreamWaitEvent(x, ctx->gev_in, 0));
   int launches = 0;
-  uint32_t nf = 0;
-  for (uint32_t f = 0; f < F; ++f) {
+  vdi_status err = VDI_OK;
+  for (uint32_t f = 0; f < F && err == VDI_OK; ++f) {
     const uint32_t R = roots ? roots[f] : cf.root;
+    const int b = (int)(f & 1);
     vdi_full_view so;
-    if (R == me) {  // the root's strip is its image rows
+    if (G == 1) {
+      so = vdi_full_view{0, H, images[f].count, images[f].depth, images[f].rgba};
+    } else if (R == me) {  // the root's strip is its image rows
       so = vdi_full_view{ctx->row0, ctx->row1, images[f].count + o, images[f].depth + o * k * 2,
                          images[f].rgba + o * k * 4};
     } else {
-      const int b = nf++ & 1;
       so = vdi_full_view{ctx->row0, ctx->row1, ctx->fs_count[b].as<uint8_t>(), ctx->fs_depth[b].as<float>(),
                          ctx->fs_rgba[b].as<float>()};
     }
     // frame f's push runs on the push stream beside frame f-1's merge; its
     // double-buffered exchange arrays wait for the merge of frame f-2
-    ctx->xpst = ctx->xst;
-    ctx->xpar = (int)(f & 1);
-    if (f >= 2) CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->xst, ctx->xev_merged[f & 1], 0));
-    const vdi_status cs = vdi_composite(ctx, local + (size_t)f * n_local, n_local, &so);
+    ctx->mpar = b;
+    ctx->msst = overlap ? ctx->sst : nullptr;
+    if (G > 1) {
+      ctx->xpst = ctx->xst;
+      ctx->xpar = b;
+      if (f >= 2) err = cudaStreamWaitEvent(ctx->xst, ctx->xev_merged[b], 0) == cudaSuccess ? VDI_OK : VDI_ERR_CUDA;
+    }
+    if (err == VDI_OK) err = vdi_composite(ctx, local + (size_t)f * n_local, n_local, &so);
     ctx->xpst = nullptr;
     ctx->xpar = 0;
-    if (cs != VDI_OK) return cs;
+    ctx->mpar = 0;
+    ctx->msst = nullptr;
+    if (err != VDI_OK) break;
     launches += ctx->last.kernel_launches;
-    const uint32_t j = ++ctx->gcalls_to[R];
-    if (R != me) {
-      if (vdi_status s = gather_send(ctx, &so, R, j, st, launches)) return s;
-    } else {
-      if (vdi_status s = gather_recv(ctx, &images[f], j, ctx->gst, launches)) return s;
+    cudaStream_t es = overlap ? ctx->sst : st;  // the stream the frame's merge ends on
+    if (G > 1) {
+      const uint32_t j = ++ctx->gcalls_to[R];
+      if (R != me) err = gather_send(ctx, &so, R, j, es, launches);
+      else err = gather_recv(ctx, &images[f], j, ctx->gst, launches);
+      ctx->last_gather_root = (int)R;
+      ctx->last_gather_parity = j & 1;
     }
-    ctx->last_gather_root = (int)R;
-    ctx->last_gather_parity = j & 1;
+    // this parity's merge scratch and strip buffer are free again
+    if (err == VDI_OK && overlap) CUDA_TRY(ctx, cudaEventRecord(ctx->mev_done[b], es));
   }
-  // the call ends on the caller's stream once the pushes and inflates have too
-  CUDA_TRY(ctx, cudaEventRecord(ctx->gev_out, ctx->gst));
-  CUDA_TRY(ctx, cudaStreamWaitEvent(st, ctx->gev_out, 0));
-  CUDA_TRY(ctx, cudaEventRecord(ctx->gev_out, ctx->xst));
-  CUDA_TRY(ctx, cudaStreamWaitEvent(st, ctx->gev_out, 0));
+  if (err != VDI_OK) return err;
+  // the call ends on the caller's stream once the side streams have too
+  for (cudaStream_t x : {ctx->gst, ctx->xst, ctx->sst}) {
+    CUDA_TRY(ctx, cudaEventRecord(ctx->gev_out, x));
+    CUDA_TRY(ctx, cudaStreamWaitEvent(st, ctx->gev_out, 0));
+  }
   ctx->last.kernel_launches = (uint32_t)launches;
   return VDI_OK;
 }
@@ -2007,7 +2059,8 @@ vdi_status vdi_get_counters(vdi_ctx* ctx, vdi_counters* out) {
   const vdi_config& cf = ctx->cfg;
   const Layout& L = ctx->lay;
   DevCounters h{};
-  if (ctx->dcnt.p) CUDA_TRY(ctx, cudaMemcpyAsync(&h, ctx->dcnt.p, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
+  if (ctx->ms[ctx->last_mpar].dcnt.p)
+    CUDA_TRY(ctx, cudaMemcpyAsync(&h, ctx->ms[ctx->last_mpar].dcnt.p, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
   unsigned long long cc[3] = {0, 0, 0};
   if (ctx->ccnt.p) CUDA_TRY(ctx, cudaMemcpyAsync(cc, ctx->ccnt.p, 24, cudaMemcpyDeviceToHost, ctx->stream));
   // records received in the last exchange (slot headers) and, at the root,

@@ -1776,7 +1776,11 @@ static cudaError_t launch_fast_ns(const MergeParams& mp, cudaStream_t st, int* l
 template <int NS>
 static cudaError_t launch_search_ns(const MergeParams& mp, cudaStream_t st, int* launches) {
   cudaError_t e;
-  search_gather_kernel<NS><<<sm_count() * 4, 128, 0, st>>>(mp);
+  // mp.search_share < 1 (frames in flight): the search kernels keep to that
+  // share of the SMs' residency, so the next VDI's pass-through can run beside them
+  const float sh = mp.search_share > 0.f && mp.search_share < 1.f ? mp.search_share : 1.f;
+  auto part = [&](uint32_t full) { return std::max<uint32_t>(1, (uint32_t)(full * sh)); };
+  search_gather_kernel<NS><<<part(sm_count() * 4), 128, 0, st>>>(mp);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   ++*launches;
   {
@@ -1786,11 +1790,11 @@ static cudaError_t launch_search_ns(const MergeParams& mp, cudaStream_t st, int*
         return e;
       if (per_sm < 1) per_sm = 1;
     }
-    search_sweep_kernel<<<sm_count() * per_sm, 32, 0, st>>>(mp);
+    search_sweep_kernel<<<part(sm_count() * per_sm), 32, 0, st>>>(mp);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     ++*launches;
   }
-  long_search_kernel<NS><<<mp.long_warps, 32, 0, st>>>(mp);
+  long_search_kernel<NS><<<part(mp.long_warps), 32, 0, st>>>(mp);
   ++*launches;
   return cudaGetLastError();
 }

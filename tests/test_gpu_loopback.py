@@ -35,11 +35,12 @@ def vdi():
     return vdi
 
 
-def _group(vdi, G, W, H, k_in, k_out, n, flags=0, root=0):
+def _group(vdi, G, W, H, k_in, k_out, n, flags=0, root=0, stats=True):
     key = os.urandom(128)
     L = vdi._lib
+    extra = L.VDI_FLAG_PIXEL_STATS if stats else 0
     return [vdi.Compositor(W, H, k_in, k_out, n, n_ranks=G, rank=r, root=root, unique_id=key,
-                           flags=flags | L.VDI_FLAG_LOOPBACK | L.VDI_FLAG_PIXEL_STATS | L.VDI_FLAG_STAGE_TIMING,
+                           flags=flags | L.VDI_FLAG_LOOPBACK | extra | L.VDI_FLAG_STAGE_TIMING,
                            stream=torch.cuda.Stream()) for r in range(G)]
 
 
@@ -270,15 +271,15 @@ def test_loopback_host_entries(vdi, span):
         c.close()
 
 
-@pytest.mark.parametrize("rotate", [False, True])
-def test_loopback_composite_frames(vdi, rotate):
+@pytest.mark.parametrize("rotate,overlap", [(False, True), (True, True), (True, False)])
+def test_loopback_composite_frames(vdi, rotate, overlap):
     """vdi_composite_frames (frames in flight through strip mode): the root
     merges into its image rows and inflates the others on a second stream;
     six frames, one root or a rotating one -- each image equals the
     one-context composite of its frame bit for bit."""
     G, n, W, H, k = 3, 6, 128, 72, 10
     F = 6
-    comps = _group(vdi, G, W, H, k, k, n)
+    comps = _group(vdi, G, W, H, k, k, n, stats=not overlap)  # PIXEL_STATS turns the search overlap off
     frames = []
     for f in range(F):
         pes = synth.random_subvdis(n, W, H, k, lam=7.0 + f, seed=1500 + f)

@@ -327,3 +327,27 @@ def test_multi_gpu_strip_invariance(vdi):
            "--master-addr", "127.0.0.1", "--master-port", "29533", os.path.join(root, "tests", "mgpu_check.py")]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+
+
+@pytest.mark.parametrize("stats", [False, True])
+def test_composite_frames_one_gpu(vdi, stats):
+    """vdi_composite_frames on one GPU (frames in flight: frame f's search
+    kernels beside frame f+1's pass-through, two parities of merge scratch;
+    PIXEL_STATS turns the overlap off): every frame equals its own
+    vdi_composite bit for bit."""
+    n, W, H, k = 6, 200, 90, 12
+    frames = [[dense_to_device(p, i) for i, p in enumerate(synth.random_subvdis(n, W, H, k, lam=9.0 + f, seed=700 + f))]
+              for f in range(5)]
+    comp = vdi.Compositor(W, H, k, k, n, flags=vdi._lib.VDI_FLAG_PIXEL_STATS if stats else 0)
+    ones = []
+    for fr in frames:
+        o = comp.empty_strip()
+        comp.composite(fr, o)
+        ones.append(o)
+    images = [vdi.FullVDI.empty(W, 0, H, k) for _ in frames]
+    torch.cuda.synchronize()
+    comp.composite_frames(frames, images)
+    torch.cuda.synchronize()
+    for f in range(len(frames)):
+        for a, b in ((images[f].count, ones[f].count), (images[f].depth, ones[f].depth), (images[f].rgba, ones[f].rgba)):
+            assert torch.equal(a, b), f
