@@ -17,6 +17,8 @@
 //     the sender's window slot with a one-CTA signal kernel after their merge.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "comm.h"
 
 namespace vdi {
@@ -45,14 +47,14 @@ template <class V>
 __device__ __forceinline__ void copy_span(const V* __restrict__ s, V* __restrict__ d, unsigned long long n,
                                           unsigned long long i0, unsigned long long stride) {
   unsigned long long i = i0;
-  for (; i + 3 * stride < n; i += 4 * stride) {
-    const V a = s[i], b = s[i + stride], c = s[i + 2 * stride], e = s[i + 3 * stride];
-    d[i] = a;
-    d[i + stride] = b;
-    d[i + 2 * stride] = c;
-    d[i + 3 * stride] = e;
+  for (; i + 7 * stride < n; i += 8 * stride) {  // 8 loads in flight per thread
+    V v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = __ldg(s + i + u * stride);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) d[i + u * stride] = v[u];
   }
-  for (; i < n; i += stride) d[i] = s[i];
+  for (; i < n; i += stride) d[i] = __ldg(s + i);
 }
 
 // bytes [0, n) from s to d; the widest vector both addresses allow
@@ -102,7 +104,7 @@ __global__ void bounds_kernel(BoundsArgs a) {
 // Push of (local PE, destination strip) slices into the destination windows
 // (a4): blockIdx.y = segment, blockIdx.x = share of it.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) push_kernel(const PushSeg* __restrict__ segs) {
+__global__ void __launch_bounds__(256, 4) push_kernel(const PushSeg* __restrict__ segs) {
   const PushSeg sg = segs[blockIdx.y];
   const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
   const unsigned long long i0 = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -150,14 +152,25 @@ __device__ __forceinline__ uint32_t warp_incl_scan_c(uint32_t v, int lane) {
   return v;
 }
 
-__global__ void __launch_bounds__(128) compact_push_kernel(CompactPushArgs a) {
+__global__ void __launch_bounds__(256) compact_push_kernel(CompactPushArgs a) {
   const int lane = threadIdx.x & 31;
   const uint32_t ng = (a.P + 31) / 32;
-  for (uint32_t g = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); g < ng;
-       g += gridDim.x * (blockDim.x >> 5)) {
+  const uint32_t gstep = gridDim.x * (blockDim.x >> 5);
+  uint32_t g = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  // the next group's count and base are loaded while this one is copied
+  uint32_t c_nx = 0, gb_nx = 0;
+  if (g < ng) {
+    c_nx = g * 32 + lane < a.P ? __ldg(a.count + g * 32 + lane) : 0u;
+    gb_nx = __ldg(a.group_base + g);
+  }
+  for (; g < ng; g += gstep) {
     const uint32_t p = g * 32 + lane;
-    const uint32_t c = p < a.P ? a.count[p] : 0u;
-    const uint32_t gb = a.group_base[g];
+    const uint32_t c = c_nx, gb = gb_nx;
+    const uint32_t gn = g + gstep;
+    if (gn < ng) {
+      c_nx = gn * 32 + lane < a.P ? __ldg(a.count + gn * 32 + lane) : 0u;
+      gb_nx = __ldg(a.group_base + gn);
+    }
     if (p < a.P) a.dst_count[p] = (uint8_t)c;
     if (lane == 0) a.dst_gbase[g] = a.region + gb;
     // the group's records are contiguous in the root window: record d goes to
@@ -234,7 +247,7 @@ cudaError_t launch_push(const PushSeg* dsegs, uint32_t n_segs, uint32_t blocks_p
 }
 
 cudaError_t launch_compact_push(const CompactPushArgs& a, uint32_t blocks, cudaStream_t st) {
-  compact_push_kernel<<<blocks, 128, 0, st>>>(a);
+  compact_push_kernel<<<blocks, 256, 0, st>>>(a);
   return cudaGetLastError();
 }
 

@@ -83,11 +83,13 @@ cudaError_t launch_signal(const SignalArgs& a, cudaStream_t st);
 cudaError_t launch_check(const WaitArgs& a, unsigned long long* fails, cudaStream_t st);
 cudaError_t preload_comm();   // load the comm kernels now (see preload_merge)
 
-// blocks of the gather compaction of a P-list strip (both ends derive it)
+// blocks (256 threads) of the gather compaction of a P-list strip (both ends
+// derive it): up to 8 per SM (full occupancy: the copy is latency bound), each
+// looping over its share of 32-list groups
 inline uint32_t compact_push_blocks(uint32_t P) {
   const uint32_t ng = (P + 31) / 32;
-  const uint32_t b = (ng + 3) / 4;
-  return b < 1 ? 1 : (b > 148 * 16 ? 148 * 16 : b);
+  const uint32_t b = (ng + 7) / 8;
+  return b < 1 ? 1 : (b > 148 * 8 ? 148 * 8 : b);
 }
 // blocks per (PE, destination) segment of the exchange push (both ends derive it)
 inline uint32_t push_blocks(uint32_t n_local, uint32_t G) {

@@ -159,7 +159,7 @@ __global__ void __launch_bounds__(128) novel_view_kernel(NovelParams np) {
 
 // rows of an RGBA strip into the root's window (the image gather), one
 // counter bump per block at the root
-__global__ void __launch_bounds__(128) rows_push_kernel(const float4* __restrict__ src, float4* __restrict__ dst,
+__global__ void __launch_bounds__(256) rows_push_kernel(const float4* __restrict__ src, float4* __restrict__ dst,
                                                         uint32_t n, uint32_t* flag) {
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) dst[i] = __ldg(src + i);
   __syncthreads();
@@ -193,7 +193,7 @@ cudaError_t launch_novel_view(const NovelParams& np, cudaStream_t st) {
 
 cudaError_t launch_rows_push(const float4* src, float4* dst, uint32_t n, uint32_t blocks, uint32_t* flag,
                              cudaStream_t st) {
-  rows_push_kernel<<<blocks, 128, 0, st>>>(src, dst, n, flag);
+  rows_push_kernel<<<blocks, 256, 0, st>>>(src, dst, n, flag);
   return cudaGetLastError();
 }
 
