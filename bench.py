@@ -438,18 +438,7 @@ def _run_ours(args, world, rank, local, clk):
             r_tot = allreduce_max(sum(r_ms), G)
             rotating = {"vdis_per_s": F * args.steps / (r_tot / 1e3), "ms_per_vdi": stats_ms([t / F for t in r_ms]),
                         "note": "frame f gathered on rank f mod G (vdi_gather_root): the root's inflate is shared"}
-    latency = rotating = full_rep = None
-    K1 = max(10, args.steps // 4)
-    l_ms, lstage, _ = timed(K1, 0, frames=1)
-    l_tot = allreduce_max(sum(l_ms), G)
-    latency = {"ms_per_vdi": l_tot / K1, "value": 1e3 * K1 / l_tot, "steps": K1,
-               "ms_per_vdi_stats": stats_ms(l_ms),
-               "stages_ms": {s_: statistics.mean(c_[f"ms_{s_}"] for c_ in lstage)
-                             for s_ in ("exchange", "merge", "gather")},
-               "note": "one VDI per step (vdi_composite + vdi_gather, no overlap between VDIs)"}
-    cnts = lstage  # per-stage numbers below come from the one-VDI steps
-    if G > 1:
-        if args.rotating:        compx = vdi.Compositor(W, H, cfg.k_in, k, n, n_ranks=G, rank=rank, unique_id=new_uid(), stream=stream,
+        compx = vdi.Compositor(W, H, cfg.k_in, k, n, n_ranks=G, rank=rank, unique_id=new_uid(), stream=stream,
                                flags=L.VDI_FLAG_STAGE_TIMING)
         fulls = [compx.dense_to_full(p) for p in base]
         ids = [p.pe_id for p in base]
@@ -501,7 +490,7 @@ def _run_ours(args, world, rank, local, clk):
     if os.path.exists(tp):
         try:
             tj = json.load(open(tp)).get(cfg.name if not args.pes else f"{cfg.name}-{cfg.n_pes}")
-            if isinstance(tj, dict):
+            if isinstance(tj, dict) and G == 1:  # captured on one GPU (whole image)
                 traffic, traffic_fast = tj.get("merge_stage"), tj.get("merge_fast")
         except Exception:
             pass
