@@ -23,7 +23,19 @@ $(LIB): $(OBJS)
 oracle/liboracle.so: oracle/oracle.cpp
 	g++ -std=c++17 -O2 -ffp-contract=off -fno-fast-math -fopenmp -fPIC -shared -o $@ $<
 
-clean:
-	rm -rf build $(LIB) oracle/liboracle.so
+# debug build with device-side bounds checks (VDI_CHECKS): build_dbg/libvdi.so;
+# select it with VDI_LIB_PATH=$PWD/build_dbg/libvdi.so
+DBG_OBJS := $(patsubst $(PKG)/csrc/%.cu,build_dbg/%.o,$(SRCS))
+build_dbg/%.o: $(PKG)/csrc/%.cu $(PKG)/csrc/internal.h $(PKG)/csrc/comm.h $(PKG)/csrc/render.h include/vdi.h
+	@mkdir -p build_dbg
+	$(NVCC) $(NVFLAGS) -DVDI_CHECKS -dc -o $@ $< 2> build_dbg/$*.ptxas.log || (cat build_dbg/$*.ptxas.log; false)
 
-.PHONY: all clean
+build_dbg/libvdi.so: $(DBG_OBJS)
+	$(NVCC) $(ARCH) -shared -o $@ $(DBG_OBJS) -L$(NCCL)/lib -l:libnccl.so.2 -Xlinker -rpath -Xlinker $(NCCL)/lib
+
+debug: build_dbg/libvdi.so
+
+clean:
+	rm -rf build build_dbg $(LIB) oracle/liboracle.so
+
+.PHONY: all clean debug

@@ -39,7 +39,10 @@ typedef enum {
 
 /* vdi_config.flags */
 #define VDI_FLAG_PIXEL_STATS 0x1u  /* keep per-list gamma*, tie margin and m of the last composite (vdi_pixel_stats) */
-#define VDI_FLAG_VALIDATE 0x2u     /* check inputs: count <= k_in, tf < tb, 0 < alpha <= 1, sorted runs */
+#define VDI_FLAG_VALIDATE 0x2u     /* vdi_composite checks its inputs on the device first (count <= k_in, offsets =
+                                      exclusive scan of count, tf < tb, 0 <= alpha <= 1, a list's records
+                                      front-to-back and disjoint) and returns VDI_ERR_INVALID_ARG naming the
+                                      violation; costs one host synchronisation per call */
 #define VDI_FLAG_STAGE_TIMING 0x4u /* record CUDA-event times of the exchange / merge / gather stages */
 #define VDI_FLAG_LOOPBACK 0x10u    /* n_ranks > 1 contexts in ONE process (any devices, e.g. all on one GPU):
                                       nccl_unique_id is only the group's key, the windows are exchanged

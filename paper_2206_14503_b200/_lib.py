@@ -15,6 +15,13 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("VDI_LIB_PATH") or os.path.join(_HERE, "lib", "libvdi.so")
 
 VDI_OK = 0
+VDI_ERR_INVALID_ARG = 1
+VDI_ERR_OUT_OF_MEMORY = 2
+VDI_ERR_CUDA = 3
+VDI_ERR_NCCL = 4
+VDI_ERR_STATE = 5
+VDI_ERR_CAPACITY = 6
+VDI_ERR_INTERNAL = 7
 VDI_FLAG_PIXEL_STATS = 0x1
 VDI_FLAG_VALIDATE = 0x2
 VDI_FLAG_STAGE_TIMING = 0x4

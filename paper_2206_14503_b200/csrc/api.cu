@@ -1061,6 +1061,8 @@ static vdi_status exchange_push(vdi_ctx* ctx, const vdi_dense_view* local, const
         }
       }
       sg.n_count = Pg;
+      sg.cap_rec = (unsigned long long)Pg * K;
+      sg.src_total = flocal ? (unsigned long long)cf.width * cf.height * K : local[l].total;
       sg.dst_hdr = sl.hdr;
       sg.dst_count = sl.count;
       sg.dst_depth = sl.depth;
@@ -1120,7 +1122,7 @@ static vdi_status exchange_recv(vdi_ctx* ctx, const vdi_dense_view* local, const
         const vdi_dense_view& v = local[slot[s]];
         const size_t o = (size_t)ctx->row0 * W;
         mp.src[s] = SrcDesc{v.count + o, reinterpret_cast<const float2*>(v.depth),
-                            reinterpret_cast<const float4*>(v.rgba), nullptr, nullptr};
+                            reinterpret_cast<const float4*>(v.rgba), nullptr, nullptr, v.total};
         if (direct) {
           if (v.offset) mp.src[s].offset = v.offset + o;  // absolute record indices
           else mp.src[s].gbase = ctx->gbase_x.as<uint32_t>() + ((size_t)par * L.n_local(me) + l_of[s]) * ngimg + o / 32;
@@ -1128,7 +1130,8 @@ static vdi_status exchange_recv(vdi_ctx* ctx, const vdi_dense_view* local, const
       }
     } else {
       const Slot sl = slot_at(ctx->peer[me] + L.x_off(me, q, s), Pm, K);
-      mp.src[s] = SrcDesc{sl.count, sl.depth, sl.rgba, nullptr, direct ? sl.gbase : nullptr};
+      mp.src[s] = SrcDesc{sl.count, sl.depth, sl.rgba, nullptr, direct ? sl.gbase : nullptr,
+                          (unsigned long long)Pm * K};
     }
   }
   mp.src_base = flocal ? nullptr : ctx->srcbase.as<uint32_t>() + (size_t)par * VDI_MAX_SRC;
@@ -1159,6 +1162,23 @@ vdi_status vdi_composite(vdi_ctx* ctx, const vdi_dense_view* local, uint32_t n_l
   std::vector<int> slot;
   if (vdi_status s = check_local(ctx, local, n_local, slot)) return s;
   cudaStream_t st = ctx->stream;
+  if (cf.flags & VDI_FLAG_VALIDATE) {  // debug: check the inputs on the device, one host sync
+    CUDA_TRY(ctx, ctx->gen_tmp.grow(16));
+    int* derr = ctx->gen_tmp.as<int>();
+    CUDA_TRY(ctx, cudaMemsetAsync(derr, 0, 4, st));
+    for (uint32_t l = 0; l < n_local; ++l)
+      CUDA_TRY(ctx, launch_validate(local[l].count, local[l].offset, reinterpret_cast<const float2*>(local[l].depth),
+                                    reinterpret_cast<const float4*>(local[l].rgba), cf.width * cf.height,
+                                    (int)cf.k_in, local[l].total, derr, st));
+    int herr = 0;
+    CUDA_TRY(ctx, cudaMemcpyAsync(&herr, derr, 4, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(ctx, cudaStreamSynchronize(st));
+    if (herr)
+      return fail(VDI_ERR_INVALID_ARG, "VDI_FLAG_VALIDATE: invalid input (%s%s%s%s%s)", herr & 1 ? "count > k_in; " : "",
+                  herr & 2 ? "offsets are not the exclusive scan of count / total; " : "",
+                  herr & 4 ? "t_front >= t_back; " : "", herr & 8 ? "alpha outside [0, 1]; " : "",
+                  herr & 16 ? "records not front-to-back and disjoint within a list" : "");
+  }
   const bool timing = cf.flags & VDI_FLAG_STAGE_TIMING;
   int launches = 0;
   if (timing) CUDA_TRY(ctx, cudaEventRecord(ctx->ev[0], st));
@@ -1179,7 +1199,7 @@ vdi_status vdi_composite(vdi_ctx* ctx, const vdi_dense_view* local, uint32_t n_l
     for (uint32_t s = 0; s < n; ++s) {
       const vdi_dense_view& v = local[slot[s]];
       mp.src[s] = SrcDesc{v.count, reinterpret_cast<const float2*>(v.depth), reinterpret_cast<const float4*>(v.rgba),
-                          all_off ? v.offset : nullptr};
+                          all_off ? v.offset : nullptr, nullptr, v.total};
     }
     S_est = S_loc;
   } else {
@@ -1358,6 +1378,7 @@ static vdi_status gather_send(vdi_ctx* ctx, const vdi_full_view* strip, uint32_t
   a.k = (int)k;
   a.group_base = ctx->gbase_loc.as<uint32_t>();
   a.region = (uint32_t)((size_t)ctx->row0 * W * k);
+  a.region_cap = (unsigned long long)P * k;
   a.dst_count = reinterpret_cast<uint8_t*>(gp + L.g_count_off()) + (size_t)ctx->row0 * W;
   a.dst_gbase = reinterpret_cast<uint32_t*>(gp + L.g_gbase_off()) + L.gbase_index(me);
   a.dst_depth = reinterpret_cast<float2*>(gp + L.g_depth_off());

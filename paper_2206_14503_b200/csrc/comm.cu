@@ -20,6 +20,7 @@
 #include <cstdlib>
 
 #include "comm.h"
+#include "internal.h"
 
 namespace vdi {
 
@@ -116,6 +117,8 @@ __global__ void __launch_bounds__(256, 4) push_kernel(const PushSeg* __restrict_
     r0 = sg.rec0;
     nrec = sg.nrec;
   }
+  VDI_CHECK(nrec <= sg.cap_rec, "push: slice larger than the destination slot");
+  VDI_CHECK(!sg.src_total || r0 + nrec <= sg.src_total, "push: slice past the source's records");
   copy_bytes(sg.src_count, sg.dst_count, sg.n_count, i0, stride);
   if (sg.dst_gbase) {  // group bases relative to the slice's first record: the receiver needs no scan
     if (sg.src_offset) {
@@ -179,6 +182,7 @@ __global__ void __launch_bounds__(256) compact_push_kernel(CompactPushArgs a) {
     const uint32_t incl = warp_incl_scan_c(c, lane), excl = incl - c;
     const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
     const size_t base = (size_t)a.region + gb;
+    VDI_CHECK(gb + tot <= a.region_cap, "compact_push: records past the rank's region");
     for (uint32_t d0 = 0; d0 < tot; d0 += 32) {
       const uint32_t d = d0 + lane;
       uint32_t l = 0;

@@ -43,6 +43,8 @@ struct PushSeg {
   unsigned long long* dst_hdr;  // receives the record count of the slice
   unsigned long long* bytes;    // local counter of pushed bytes (or null)
   uint32_t* flag;               // the destination's counter word for this sender
+  unsigned long long src_total; // records of the source PE (bounds of the VDI_CHECKS build)
+  unsigned long long cap_rec;   // records the destination slot holds
 };
 
 // the gather's compaction into the root's window (a11)
@@ -61,6 +63,7 @@ struct CompactPushArgs {
   unsigned long long* total_out;  // root window header: records pushed
   unsigned long long* bytes;    // local counter of pushed bytes (or null)
   uint32_t* flag;
+  unsigned long long region_cap;  // records the root's region for this rank holds
 };
 
 struct WaitArgs {

@@ -11,6 +11,24 @@
 #include "vdi.h"
 
 #define VDI_MAX_SRC 64        // sources (PEs) supported by one composite
+
+// Debug build (make debug, -DVDI_CHECKS): device-side bounds checks of every
+// index computed from the inputs; a failed check prints and traps.
+#ifdef VDI_CHECKS
+#include <cstdio>
+#define VDI_CHECK(c, what)                                                          \
+  do {                                                                              \
+    if (!(c)) {                                                                     \
+      printf("VDI_CHECK failed %s:%d: %s (block %d thread %d)\n", __FILE__, __LINE__, what, \
+             (int)blockIdx.x, (int)threadIdx.x);                                    \
+      __trap();                                                                     \
+    }                                                                               \
+  } while (0)
+#else
+#define VDI_CHECK(c, what) \
+  do {                     \
+  } while (0)
+#endif
 #define VDI_MAX_GRID_AXIS 16  // bricks per axis in a decomposition
 
 namespace vdi {
@@ -31,6 +49,7 @@ struct SrcDesc {
   const uint32_t* gbase;   // or: the index of the first record of each 32-list group of the strip (pushed by
                            // the sender / from its scan); neither: the merge scans the counts itself
                            // (receive-side scan)
+  unsigned long long nrec; // records addressable in depth/rgba (0: unknown; bounds of the VDI_CHECKS build)
 };
 
 // Work-list buckets of lists that need more than the pass-through:
@@ -109,7 +128,10 @@ cudaError_t launch_general(const MergeParams& mp, cudaStream_t st, int* launches
 cudaError_t launch_margins(const MergeParams& mp, cudaStream_t st, int* launches);
 uint32_t general_threads(uint32_t m_max);
 uint32_t long_warps(uint32_t m_max, size_t* slot_bytes);  // warps (and slot bytes) of the long-list search
-cudaError_t preload_merge();  // load every merge kernel now (loopback groups spin-wait across contexts)  // threads of the general kernel for lists of <= m_max records
+cudaError_t preload_merge();
+// VDI_FLAG_VALIDATE: input checks of one dense sub-VDI; error bits ORed into *err (merge.cu)
+cudaError_t launch_validate(const uint8_t* count, const uint32_t* offset, const float2* depth, const float4* rgba,
+                            uint32_t P, int k, unsigned long long total, int* err, cudaStream_t st);  // load every merge kernel now (loopback groups spin-wait across contexts)  // threads of the general kernel for lists of <= m_max records
 
 // Generator (generate.cu)
 struct GenParams {

@@ -619,6 +619,9 @@ __global__ void __launch_bounds__(kFastThreads) merge_fast_kernel(MergeParams mp
       }
     }
     rec_acc += m;
+#pragma unroll
+    for (int s = 0; s < NS; ++s)
+      if (s < n) VDI_CHECK(!mp.src[s].nrec || gidx[s] + cnt[s] <= mp.src[s].nrec, "merge_fast: record index past the source");
     const bool cand = valid && m > 0 && (int)m <= k;
     int bk = (valid && (int)m > k) ? bucket_of(m) : -1;
     const bool bulk = bulk_ok && p0 + 32 <= mp.P;  // tail group / unaligned output: plain stores
@@ -783,6 +786,10 @@ __device__ __forceinline__ void gather_short_batch(const MergeParams& mp, uint32
       j += cnt[s];
     }
   }
+#pragma unroll
+  for (int s = 0; s < NS; ++s)
+    if (s < n) VDI_CHECK(!mp.src[s].nrec || goff[s] + cnt[s] <= mp.src[s].nrec, "short gather: record index past the source");
+  VDI_CHECK(!valid || (m > (uint32_t)mp.k_out && m <= 40), "short gather: m outside (k_out, 40]");
   // one pool slot per batch of 32 entries (a warp here = one batch)
   uint32_t slot = 0;
   if (lane == 0) {
@@ -1346,6 +1353,9 @@ __global__ void __launch_bounds__(32) long_search_kernel(MergeParams mp) {
         cnt[s] = __ldg(mp.src[s].count + p);
       }
     }
+#pragma unroll
+    for (int s = 0; s < NS; ++s)
+      if (s < n) VDI_CHECK(!mp.src[s].nrec || goff[s] + cnt[s] <= mp.src[s].nrec, "long search: record index past the source");
     bool bad = valid && m > cap;  // cannot hold it: general path
     if (valid && !bad) bad = !long_gather_lane<NS>(mp, m, goff, cnt, col0 + (spec ? 0 : lane), dcol0 + (spec ? 0 : lane));
     __syncwarp();  // the slot columns are complete (and visible to the warp)
@@ -1418,9 +1428,11 @@ __device__ __forceinline__ void general_body(const MergeParams& mp, uint32_t tid
     float* E = reinterpret_cast<float*>(B + 2 * m0);
     // step 1: k-way merge of the per-PE sorted runs, dropping alpha == 0 (Q23)
     uint32_t pos[VDI_MAX_SRC], end[VDI_MAX_SRC];
+    VDI_CHECK(4 * m0 <= mp.gen_stride, "general: list longer than its scratch slice");
     for (int s = 0; s < n; ++s) {
       pos[s] = ent[3 + s];
       end[s] = pos[s] + __ldg(mp.src[s].count + p);
+      VDI_CHECK(!mp.src[s].nrec || end[s] <= mp.src[s].nrec, "general: record index past the source");
     }
     int m = 0;
     for (;;) {
@@ -1841,6 +1853,50 @@ cudaError_t launch_fast(const MergeParams& mp, cudaStream_t st, int* launches) {
 
 cudaError_t launch_search(const MergeParams& mp, cudaStream_t st, int* launches) {
   VDI_DISPATCH_NS(launch_search_ns, mp, st, launches)
+}
+
+// VDI_FLAG_VALIDATE: input checks of one dense sub-VDI (thread per list):
+// bit 0 count > k_in, bit 1 offset[p+1] - offset[p] != count[p] (or the last
+// offset != total), bit 2 t_front >= t_back or NaN, bit 3 alpha outside
+// [0, 1] or NaN, bit 4 a list's records not front-to-back and disjoint
+// (t_front < previous t_back) -- the dense layout of PAPER.md:113-115 and
+// the record invariants the merge relies on (Q7, Q23).
+__global__ void __launch_bounds__(256) validate_kernel(const uint8_t* __restrict__ count,
+                                                       const uint32_t* __restrict__ offset,
+                                                       const float2* __restrict__ depth,
+                                                       const float4* __restrict__ rgba, uint32_t P, int k,
+                                                       unsigned long long total, int* err) {
+  int e = 0;
+  for (uint32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < P; p += gridDim.x * blockDim.x) {
+    const uint32_t c = count[p];
+    if ((int)c > k) e |= 1;
+    if (!offset) continue;
+    const uint32_t o = offset[p];
+    if (offset[p + 1] - o != c) e |= 2;
+    if (p + 1 == P && offset[P] != total) e |= 2;
+    if (o + c > total) {
+      e |= 2;
+      continue;
+    }
+    float prev_tb = -CUDART_INF_F;
+    for (uint32_t j = 0; j < c; ++j) {
+      const float2 d = depth[o + j];
+      const float a = rgba[o + j].w;
+      if (!(d.x < d.y)) e |= 4;
+      if (!(a >= 0.f && a <= 1.f)) e |= 8;
+      if (d.x < prev_tb) e |= 16;
+      prev_tb = d.y;
+    }
+  }
+  if (e) atomicOr(err, e);
+}
+
+cudaError_t launch_validate(const uint8_t* count, const uint32_t* offset, const float2* depth, const float4* rgba,
+                            uint32_t P, int k, unsigned long long total, int* err, cudaStream_t st) {
+  if (!P) return cudaSuccess;
+  validate_kernel<<<std::min<uint32_t>((P + 255) / 256, (uint32_t)sm_count() * 8), 256, 0, st>>>(count, offset, depth,
+                                                                                               rgba, P, k, total, err);
+  return cudaGetLastError();
 }
 
 // Load every merge kernel now (lazy module loading could otherwise try to
