@@ -862,11 +862,22 @@ __device__ __forceinline__ void gather_short_batch(const MergeParams& mp, uint32
 }
 
 // Short-list sweep of one batch (32 work-list entries, lane = list): the
-// samples are loaded once into a statically indexed register file, then the
-// memoised bisection (see Bisection) sweeps while any lane still needs a
-// count; (|acc|^2, |acc - s|^2) are one packed f32x2 chain.
-template <int MS>
-__device__ __forceinline__ void sweep_batch(const MergeParams& mp, int bucket, uint32_t batch) {
+// samples are loaded once -- the first R into a statically indexed register
+// file, the rest (cp.async) into the warp's shared-memory rows [q - R][lane]
+// -- then the memoised bisection (see Bisection) sweeps while any lane still
+// needs a count; (|acc|^2, |acc - s|^2) are one packed f32x2 chain.  Keeping
+// only R samples in registers raises the resident warps per SM (8 at 40
+// register samples, 12 at 24).
+#ifndef VDI_SWEEP_R
+#define VDI_SWEEP_R 24  // measured (C3 search stage): R = 8 / 16 / 24 / 40 -> 0.160 / 0.161 / 0.153 / 0.160 ms
+#endif
+__device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(sdst)), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
+template <int MS, int R>
+__device__ __forceinline__ void sweep_batch(const MergeParams& mp, int bucket, uint32_t batch, float4* __restrict__ sm) {
   const int lane = threadIdx.x;
   const int k = mp.k_out, n = mp.n_src;
   const uint32_t total = min(mp.wl_count[bucket], mp.wl_cap);
@@ -886,10 +897,19 @@ __device__ __forceinline__ void sweep_batch(const MergeParams& mp, int bucket, u
     const float2* dcol = mp.pool_depth + (size_t)slot * 40 * 32 + lane;
     // samples past m are NaN: D^2 = NaN never exceeds g^2 and their gap bits
     // are 0, so they never split and the count sweeps need no "q < m" test
-    float4 S[MS];
+    float4 S[R];
     const float qnan = __int_as_float(0x7fc00000);
+    const float4 nan4 = make_float4(qnan, qnan, qnan, qnan);
+    __syncwarp();  // the previous batch's reads of the shared rows are done
 #pragma unroll
-    for (int q = 0; q < MS; ++q) S[q] = (q < mi && !bad) ? col[q * 32] : make_float4(qnan, qnan, qnan, qnan);
+    for (int q = R; q < MS; ++q) {
+      if (q < mi && !bad) cp_async16(sm + (q - R) * 32 + lane, col + q * 32);
+      else sm[(q - R) * 32 + lane] = nan4;
+    }
+#pragma unroll
+    for (int q = 0; q < R; ++q) S[q] = (q < mi && !bad) ? col[q * 32] : nan4;
+    cp_async_wait_all();  // each lane reads only its own column: no warp barrier needed
+    auto smp = [&](int q) -> float4 { return q < R ? S[q < R ? q : 0] : sm[(q - R) * 32 + lane]; };
     // memoised bisection: a count sweep at g2 takes the same decisions for
     // every g2' in [L, U), so a later midpoint inside the interval of the
     // latest sweep on either side of the bracket reuses its count; each lane
@@ -906,7 +926,7 @@ __device__ __forceinline__ void sweep_batch(const MergeParams& mp, int bucket, u
 #pragma unroll
       for (int q = 0; q < MS; ++q) {
         if ((q & 7) == 0 && q > 0 && !__any_sync(kFull, bs.active && q < mi && sc <= k)) break;
-        const float4 sv = S[q];
+        const float4 sv = smp(q);
         const bool gap = sv.w < 0.f;  // NaN padding: false
         const float sa = fabsf(sv.w);
         float n2, d2;
@@ -943,7 +963,7 @@ __device__ __forceinline__ void sweep_batch(const MergeParams& mp, int bucket, u
             if (q + u < MS && q + u < mi) dq[u] = dcol[(q + u) * 32];
         }
         if (q < mi) {
-          const float4 sv = S[q];
+          const float4 sv = smp(q);
           const float2 d = dq[q & 7];
           const bool gap = sv.w < 0.f;
           const float sa = fabsf(sv.w);
@@ -975,7 +995,7 @@ __device__ __forceinline__ void sweep_batch(const MergeParams& mp, int bucket, u
 }
 
 #ifndef VDI_SWEEP_MINB
-#define VDI_SWEEP_MINB 8
+#define VDI_SWEEP_MINB 12  // 168 registers at R = 24: 12 warps per SM
 #endif
 
 // ---------------------------------------------------------------------------
@@ -1753,7 +1773,9 @@ __global__ void __launch_bounds__(128, VDI_GATHER_MINB) search_gather_kernel(Mer
 }
 
 // Short-list sweeps, warp per batch (dynamic claims, longest bucket first).
+static constexpr int kSweepSmem = (40 - VDI_SWEEP_R) * 32 * 16;  // shared rows of the warp's samples
 __global__ void __launch_bounds__(32, VDI_SWEEP_MINB) search_sweep_kernel(MergeParams mp) {
+  extern __shared__ float4 sweep_rows[];
   const uint32_t c0 = min(mp.wl_count[0], mp.wl_cap), c1 = min(mp.wl_count[1], mp.wl_cap);
   const uint32_t nb0 = (c0 + 31) / 32, nb1 = (c1 + 31) / 32;
   for (;;) {
@@ -1761,7 +1783,7 @@ __global__ void __launch_bounds__(32, VDI_SWEEP_MINB) search_sweep_kernel(MergeP
     if (threadIdx.x == 0) v = atomicAdd(&mp.search_ticket[0], 1u);
     v = __shfl_sync(kFull, v, 0);
     if (v >= nb0 + nb1) break;
-    sweep_batch<40>(mp, v < nb1 ? 1 : 0, v < nb1 ? v : v - nb1);
+    sweep_batch<40, VDI_SWEEP_R>(mp, v < nb1 ? 1 : 0, v < nb1 ? v : v - nb1, sweep_rows);
   }
 }
 
@@ -1798,11 +1820,9 @@ static cudaError_t launch_search_ns(const MergeParams& mp, cudaStream_t st, int*
   {
     static int per_sm = 0;
     if (!per_sm) {
-      if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, search_sweep_kernel, 32, 0)) != cudaSuccess)
-        return e;
-      if (per_sm < 1) per_sm = 1;
+      if ((e = prep(search_sweep_kernel, kSweepSmem, 32, &per_sm)) != cudaSuccess) return e;
     }
-    search_sweep_kernel<<<part(sm_count() * per_sm), 32, 0, st>>>(mp);
+    search_sweep_kernel<<<part(sm_count() * per_sm), 32, kSweepSmem, st>>>(mp);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     ++*launches;
   }
