@@ -440,62 +440,6 @@ __device__ __forceinline__ bool direct_list(const MergeParams& mp, uint32_t p, c
   return true;
 }
 
-// global address of the record with PE-concatenated index ci of one list
-template <int NS>
-__device__ __forceinline__ uint32_t concat_src(const uint32_t (&cs)[NS], const uint32_t (&cnt)[NS],
-                                               const uint32_t (&goff)[NS], uint32_t ci, int* src) {
-  uint32_t gi = 0;
-  int sb = 0;
-#pragma unroll
-  for (int s = 0; s < NS; ++s)
-    if (ci >= cs[s] && ci < cs[s] + cnt[s]) {
-      gi = goff[s] + (ci - cs[s]);
-      sb = s;
-    }
-  *src = sb;
-  return gi;
-}
-
-// Load the records of one list in PE-concatenated order (PE s's run at
-// [cs[s], cs[s] + cnt[s])) with CH loads in flight per trip, instead of one
-// dependent round trip per record.  dst_d[q * stride], dst_c[q * stride]
-// (dst_c may be null).
-template <int NS, int CH>
-__device__ __forceinline__ void load_concat(const MergeParams& mp, const uint32_t (&goff)[NS],
-                                            const uint32_t (&cnt)[NS], const uint32_t (&cs)[NS], uint32_t m,
-                                            float2* dst_d, float4* dst_c, int stride) {
-  for (uint32_t q0 = 0; q0 < m; q0 += CH) {
-    float2 dv[CH];
-    float4 cv[CH];
-#pragma unroll
-    for (int u = 0; u < CH; ++u) {
-      const uint32_t q = q0 + u;
-      if (q < m) {
-        const float2* dp = nullptr;
-        const float4* cp = nullptr;
-        uint32_t gi = 0;
-#pragma unroll
-        for (int s = 0; s < NS; ++s)
-          if (q >= cs[s] && q < cs[s] + cnt[s]) {
-            gi = goff[s] + (q - cs[s]);
-            dp = mp.src[s].depth;
-            cp = mp.src[s].rgba;
-          }
-        dv[u] = __ldg(dp + gi);
-        if (dst_c) cv[u] = __ldg(cp + gi);
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < CH; ++u) {
-      const uint32_t q = q0 + u;
-      if (q < m) {
-        dst_d[q * stride] = dv[u];
-        if (dst_c) dst_c[q * stride] = cv[u];
-      }
-    }
-  }
-}
-
 // ---------------------------------------------------------------------------
 // Fast path: warp per 32 consecutive lists, lane = list.
 //   * counts of the n sources (coalesced bytes) + warp scans -> each list's
@@ -758,32 +702,29 @@ __global__ void __launch_bounds__(kFastThreads) merge_fast_kernel(MergeParams mp
 __device__ __forceinline__ int short_ms(int b) { return b == 0 ? 32 : 40; }
 
 // Gather of one batch of short search lists (k_out < m <= 40), thread per
-// list: the run-based k-way merge over the per-PE runs staged
-// in shared memory ([q][thread], stride ST), then the samples are written in
-// depth order to the batch's pool slot in [sample][lane] layout with the gap
-// flag in the sign of alpha; transparent / overlapping records -> general path.
-#ifndef VDI_GATHER_CH
-#define VDI_GATHER_CH 8  // loads in flight per thread in the short gather
-#endif
-template <int NS, int ST, int CH = VDI_GATHER_CH>
+// list: the run-based k-way merge over the per-PE runs, their
+// heads in registers (long_gather_lane), writes the samples in depth order to
+// the batch's pool slot in [sample][lane] layout with the gap flag in the sign
+// of alpha; transparent / overlapping records -> general path.
+template <int NS>
+__device__ __forceinline__ bool long_gather_lane(const MergeParams& mp, uint32_t m, const uint32_t (&goff)[NS],
+                                                 const uint32_t (&cnt)[NS], float4* orgba, float2* odep);
+template <int NS>
 __device__ __forceinline__ void gather_short_batch(const MergeParams& mp, uint32_t b, uint32_t nb1, uint32_t c0,
-                                                   uint32_t c1, float2* my_d, uint8_t* my_p, uint32_t lane) {
+                                                   uint32_t c1, uint32_t lane) {
   const int n = mp.n_src;
   const int bucket = b < nb1 ? 1 : 0;
   const uint32_t i = (bucket == 1 ? b : b - nb1) * 32 + lane;
   const bool valid = i < (bucket == 0 ? c0 : c1);
   const uint32_t* ent = mp.wl[bucket] + (size_t)(valid ? i : 0) * (3 + n);
   const uint32_t p = valid ? ent[0] : 0u, m = valid ? ent[2] : 0u;
-  uint32_t goff[NS], cnt[NS], cs[NS];
-  uint32_t j = 0;
+  uint32_t goff[NS], cnt[NS];
 #pragma unroll
   for (int s = 0; s < NS; ++s) {
-    goff[s] = cnt[s] = cs[s] = 0;
+    goff[s] = cnt[s] = 0;
     if (valid && s < n) {
       goff[s] = ent[3 + s];
       cnt[s] = __ldg(mp.src[s].count + p);
-      cs[s] = j;
-      j += cnt[s];
     }
   }
 #pragma unroll
@@ -803,59 +744,15 @@ __device__ __forceinline__ void gather_short_batch(const MergeParams& mp, uint32
   }
   float4* orgba = mp.pool_rgba + (size_t)slot * 40 * 32 + lane;
   float2* odep = mp.pool_depth + (size_t)slot * 40 * 32 + lane;
-  // depth column in PE order (independent loads), then the depth order
-  load_concat<NS, CH>(mp, goff, cnt, cs, m, my_d, nullptr, ST);
-  uint32_t g0 = 0, g1 = 0;
+  // run-based k-way merge with the run heads in registers, straight into the
+  // slot columns (measured C3 search stage 0.152 -> 0.142 ms vs staging the
+  // depths in shared memory and merging there)
   bool bad = false;
   if (valid) {
-    bad = !run_merge<NS>(my_d, ST, cs, cnt, m, my_p, ST, [](uint32_t) { return 1.f; });  // overlap, Q12
-    if (!bad) {
-      float prev_tb = 0.f;
-      for (uint32_t r = 0; r < m; ++r) {  // gap bits from the staged depths
-        const float2 d = my_d[(uint32_t)my_p[r * ST] * ST];
-        if (r > 0 && d.x > prev_tb) {
-          if (r < 32) g0 |= 1u << r;
-          else g1 |= 1u << (r - 32);
-        }
-        prev_tb = d.y;
-      }
-      // records in depth order, 8 loads in flight per trip, to the scratch
-      for (uint32_t r0 = 0; r0 < m; r0 += CH) {
-        float4 cv[CH];
-#pragma unroll
-        for (int u = 0; u < CH; ++u) {
-          const uint32_t r = r0 + u;
-          if (r < m) {
-            const uint32_t ci = my_p[r * ST];
-            const float4* cp = nullptr;
-            uint32_t gi = 0;
-#pragma unroll
-            for (int s = 0; s < NS; ++s)
-              if (ci >= cs[s] && ci < cs[s] + cnt[s]) {
-                gi = goff[s] + (ci - cs[s]);
-                cp = mp.src[s].rgba;
-              }
-            cv[u] = __ldg(cp + gi);
-          }
-        }
-#pragma unroll
-        for (int u = 0; u < CH; ++u) {
-          const uint32_t r = r0 + u;
-          if (r < m) {
-            bad |= cv[u].w == 0.f;  // Q23
-            // gap before sample r: flagged in the sign of alpha (alpha > 0
-            // for every stored sample), tested by the sweeps with one FSETP
-            const bool gp = r < 32 ? ((g0 >> r) & 1u) : ((g1 >> (r - 32)) & 1u);
-            if (gp) cv[u].w = -cv[u].w;
-            orgba[r * 32] = cv[u];
-            odep[r * 32] = my_d[(uint32_t)my_p[r * ST] * ST];
-          }
-        }
-      }
-    }
+    bad = !long_gather_lane<NS>(mp, m, goff, cnt, orgba, odep);
     uint32_t* og = mp.pool_gap + (size_t)slot * 64 + lane;
-    og[0] = bad ? 0xffffffffu : g0;  // skip marker (bit 0 of a real gap word is never set)
-    og[32] = bad ? 0xffffffffu : g1;
+    og[0] = bad ? 0xffffffffu : 0u;  // skip marker
+    og[32] = bad ? 0xffffffffu : 0u;
   }
   const int bk = (valid && bad) ? VDI_BUCKET_GENERAL : -1;
   if (__any_sync(kFull, bk >= 0)) push_entries<NS>(mp, bk, p, m, goff, lane);
@@ -1006,6 +903,63 @@ __device__ __forceinline__ void sweep_batch(const MergeParams& mp, int bucket, u
 // (PAPER.md:176's "multiple passes" do not become HBM passes); the lists'
 // records are read from the sources once.
 // ---------------------------------------------------------------------------
+// L2 eviction priorities of the long search (VDI_LONG_POLICY): the slot rows
+// re-read by every bisection sweep evict last, the streamed source records and
+// output slots evict first.
+#ifndef VDI_LONG_POLICY
+#define VDI_LONG_POLICY 1  // measured C5 long search 16.03 -> 15.43 ms (2: slots only, 16.06), C2 neutral
+#endif
+__device__ __forceinline__ unsigned long long pol_last() {
+  unsigned long long p;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ unsigned long long pol_first() {
+  unsigned long long p;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ float4 slot_ld(const float4* a) {
+#if VDI_LONG_POLICY
+  float4 v;
+  asm volatile("ld.global.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(a), "l"(pol_last()));
+  return v;
+#else
+  return *a;
+#endif
+}
+__device__ __forceinline__ void slot_st(float4* a, float4 v) {
+#if VDI_LONG_POLICY
+  asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(a), "f"(v.x), "f"(v.y), "f"(v.z),
+               "f"(v.w), "l"(pol_last())
+               : "memory");
+#else
+  *a = v;
+#endif
+}
+__device__ __forceinline__ float4 src_ld4(const float4* a) {
+#if VDI_LONG_POLICY == 1
+  float4 v;
+  asm volatile("ld.global.nc.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(a), "l"(pol_first()));
+  return v;
+#else
+  return __ldg(a);
+#endif
+}
+__device__ __forceinline__ void out_st4(float4* a, float4 v) {
+#if VDI_LONG_POLICY == 1
+  asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(a), "f"(v.x), "f"(v.y), "f"(v.z),
+               "f"(v.w), "l"(pol_first())
+               : "memory");
+#else
+  *a = v;
+#endif
+}
+
 // Gather of the lanes' lists (valid lanes) into the slot columns orgba/odep
 // (stride 32): run-based k-way merge over the runs' head
 // t_front kept in registers, 8 records loaded per trip.  Returns false for a
@@ -1066,7 +1020,7 @@ __device__ __forceinline__ bool long_gather_lane(const MergeParams& mp, uint32_t
       for (int u = 0; u < 8; ++u)
         if ((uint32_t)u < nch) {
           dv[u] = __ldg(dp + gb + ii + u);
-          cv[u] = __ldg(cp + gb + ii + u);
+          cv[u] = src_ld4(cp + gb + ii + u);
         }
       uint32_t taken = 0;
       bool stop = false;
@@ -1082,7 +1036,7 @@ __device__ __forceinline__ bool long_gather_lane(const MergeParams& mp, uint32_t
             bad |= c.w == 0.f || d.x < prev_tb;  // Q23 / Q12
             if (r > 0 && d.x > prev_tb) c.w = -c.w;  // gap before this sample: sign of alpha
             prev_tb = d.y;
-            orgba[r * 32] = c;
+            slot_st(orgba + r * 32, c);
             odep[r * 32] = d;
             ++r;
             ++taken;
@@ -1154,25 +1108,25 @@ __device__ __forceinline__ int long_count(const float4* __restrict__ col, int m,
   float4 A[8], B[8], C[8];
 #pragma unroll
   for (int u = 0; u < 8; ++u) {
-    A[u] = col[u * 32];
-    B[u] = col[(8 + u) * 32];
+    A[u] = slot_ld(col + u * 32);
+    B[u] = slot_ld(col + (8 + u) * 32);
   }
   const float4* pp = col + 16 * 32;
   for (int q0 = 0;;) {
 #pragma unroll
-    for (int u = 0; u < 8; ++u) C[u] = pp[u * 32];
+    for (int u = 0; u < 8; ++u) C[u] = slot_ld(pp + u * 32);
     pp += 8 * 32;
     long_step8(A, q0, m, g2, ar, ag, ab, aa, sc, L, U);
     q0 += 8;
     if (q0 >= m || sc > k) break;
 #pragma unroll
-    for (int u = 0; u < 8; ++u) A[u] = pp[u * 32];
+    for (int u = 0; u < 8; ++u) A[u] = slot_ld(pp + u * 32);
     pp += 8 * 32;
     long_step8(B, q0, m, g2, ar, ag, ab, aa, sc, L, U);
     q0 += 8;
     if (q0 >= m || sc > k) break;
 #pragma unroll
-    for (int u = 0; u < 8; ++u) B[u] = pp[u * 32];
+    for (int u = 0; u < 8; ++u) B[u] = slot_ld(pp + u * 32);
     pp += 8 * 32;
     long_step8(C, q0, m, g2, ar, ag, ab, aa, sc, L, U);
     q0 += 8;
@@ -1195,25 +1149,25 @@ __device__ __forceinline__ int long_count_sync(const float4* __restrict__ col, i
   float4 A[8], B[8], C[8];
 #pragma unroll
   for (int u = 0; u < 8; ++u) {
-    A[u] = col[u * 32];
-    B[u] = col[(8 + u) * 32];
+    A[u] = slot_ld(col + u * 32);
+    B[u] = slot_ld(col + (8 + u) * 32);
   }
   const float4* pp = col + 16 * 32;
   for (int q0 = 0;;) {
 #pragma unroll
-    for (int u = 0; u < 8; ++u) C[u] = pp[u * 32];
+    for (int u = 0; u < 8; ++u) C[u] = slot_ld(pp + u * 32);
     pp += 8 * 32;
     long_step8(A, q0, m, g2, ar, ag, ab, aa, sc, L, U);
     q0 += 8;
     if (!__any_sync(kFull, act && q0 < m && sc <= k)) break;
 #pragma unroll
-    for (int u = 0; u < 8; ++u) A[u] = pp[u * 32];
+    for (int u = 0; u < 8; ++u) A[u] = slot_ld(pp + u * 32);
     pp += 8 * 32;
     long_step8(B, q0, m, g2, ar, ag, ab, aa, sc, L, U);
     q0 += 8;
     if (!__any_sync(kFull, act && q0 < m && sc <= k)) break;
 #pragma unroll
-    for (int u = 0; u < 8; ++u) B[u] = pp[u * 32];
+    for (int u = 0; u < 8; ++u) B[u] = slot_ld(pp + u * 32);
     pp += 8 * 32;
     long_step8(C, q0, m, g2, ar, ag, ab, aa, sc, L, U);
     q0 += 8;
@@ -1235,13 +1189,13 @@ __device__ __forceinline__ int long_write(const float4* __restrict__ col, const 
   float2 dv[8], dn[8];
 #pragma unroll
   for (int u = 0; u < 8; ++u) {
-    cv[u] = col[u * 32];
+    cv[u] = slot_ld(col + u * 32);
     dv[u] = dcol[u * 32];
   }
   for (int q0 = 0; q0 < m; q0 += 8) {
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
-      cn[u] = col[(q0 + 8 + u) * 32];
+      cn[u] = slot_ld(col + (q0 + 8 + u) * 32);
       dn[u] = dcol[(q0 + 8 + u) * 32];
     }
 #pragma unroll
@@ -1257,7 +1211,7 @@ __device__ __forceinline__ int long_write(const float4* __restrict__ col, const 
         const bool st = (q == 0) | (gap & (n2 > gg)) | (d2 > gg);
         if (st && q > 0 && c <= k) {  // close the open segment (ends at its last content sample)
           od[c - 1] = make_float2(tf, tb);
-          oc[c - 1] = make_float4(ar, ag, ab, aa);
+          out_st4(oc + (c - 1), make_float4(ar, ag, ab, aa));
         }
         const float tr = 1.0f - aa;
         ar = st ? sv.x : fmaf(tr, sv.x, ar);
@@ -1277,7 +1231,7 @@ __device__ __forceinline__ int long_write(const float4* __restrict__ col, const 
   }
   if (m > 0 && c <= k) {
     od[c - 1] = make_float2(tf, tb);
-    oc[c - 1] = make_float4(ar, ag, ab, aa);
+    out_st4(oc + (c - 1), make_float4(ar, ag, ab, aa));
   }
   return c;
 }
@@ -1338,6 +1292,7 @@ __global__ void __launch_bounds__(32) long_search_kernel(MergeParams mp) {
   const int lane = threadIdx.x;
   const int k = mp.k_out, n = mp.n_src;
   const uint32_t c2 = min(mp.wl_count[2], mp.wl_cap), c3 = min(mp.wl_count[3], mp.wl_cap);
+  if (c2 + c3 == 0) return;  // no long lists: leave before the claim atomics
   const uint32_t cap = mp.long_maxm;  // rows of a slot
   char* slot = mp.long_pool + (size_t)blockIdx.x * mp.long_slot;
   float4* col0 = reinterpret_cast<float4*>(slot);
@@ -1746,20 +1701,10 @@ static cudaError_t prep(K kernel, size_t smem, int threads, int* per_sm) {
   return e;
 }
 
-// Short search as two kernels: a gather kernel with its own register budget
-// (16 loads in flight per thread, 12 warps per SM) followed by a sweep-only kernel.
-// Measured on C3: search 0.1655 ms vs 0.172 fused, 0.170 with 8 loads in
-// flight (spills at 40).
-#ifndef VDI_SPLIT_CH
-#define VDI_SPLIT_CH 16
-#endif
-#ifndef VDI_GATHER_MINB
-#define VDI_GATHER_MINB 1  // resident 128-thread blocks per SM asked of ptxas (3 at 167 registers)
-#endif
+// Short search as two kernels: a gather kernel (thread per list, 16 warps per
+// SM) followed by a sweep-only kernel (register-heavy, warp per batch).
 template <int NS>
-__global__ void __launch_bounds__(128, VDI_GATHER_MINB) search_gather_kernel(MergeParams mp) {
-  __shared__ float2 sd[40 * 128];
-  __shared__ uint8_t sp[40 * 128];
+__global__ void __launch_bounds__(128) search_gather_kernel(MergeParams mp) {
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t c0 = min(mp.wl_count[0], mp.wl_cap), c1 = min(mp.wl_count[1], mp.wl_cap);
   const uint32_t nb0 = (c0 + 31) / 32, nb1 = (c1 + 31) / 32;
@@ -1768,7 +1713,7 @@ __global__ void __launch_bounds__(128, VDI_GATHER_MINB) search_gather_kernel(Mer
     if (lane == 0) v = atomicAdd(&mp.search_ticket[1], 1u);
     v = __shfl_sync(kFull, v, 0);
     if (v >= nb0 + nb1) break;
-    gather_short_batch<NS, 128, VDI_SPLIT_CH>(mp, v, nb1, c0, c1, sd + threadIdx.x, sp + threadIdx.x, lane);
+    gather_short_batch<NS>(mp, v, nb1, c0, c1, lane);
   }
 }
 
