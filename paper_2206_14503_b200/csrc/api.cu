@@ -102,6 +102,51 @@ struct DevCounters {
   unsigned long long sweep_steps;
 };
 
+// VDI_TRACE=1 (debug): timing events around the merge kernels of
+// vdi_composite_frames, printed to stderr at the end of the call (one sync)
+struct TraceEv {
+  const char* what;
+  int frame;
+  cudaEvent_t ev;
+};
+static std::vector<TraceEv>& trace_log() {
+  static std::vector<TraceEv> v;
+  return v;
+}
+static bool trace_on() {
+  static const bool on = getenv("VDI_TRACE") != nullptr;
+  return on;
+}
+static int g_trace_frame = -1;
+static int g_trace_rank = 0;
+static void trace(const char* what, cudaStream_t st) {
+  if (!trace_on() || g_trace_frame < 0) return;
+  static std::vector<cudaEvent_t> pool;
+  static size_t used = 0;
+  auto& log = trace_log();
+  if (log.empty()) used = 0;
+  if (used == pool.size()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    pool.push_back(e);
+  }
+  cudaEvent_t e = pool[used++];
+  cudaEventRecord(e, st);
+  log.push_back(TraceEv{what, g_trace_frame, e});
+}
+static void trace_dump(cudaStream_t st) {
+  auto& log = trace_log();
+  if (!trace_on() || log.empty()) return;
+  cudaStreamSynchronize(st);
+  cudaDeviceSynchronize();
+  for (auto& t : log) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, log[0].ev, t.ev);
+    fprintf(stderr, "trace r%d f%d %-14s %9.4f\n", g_trace_rank, t.frame, t.what, ms);
+  }
+  log.clear();
+}
+
 inline size_t al256(size_t b) { return (b + 255) & ~(size_t)255; }
 constexpr size_t kShortSlotBytes = 40 * 32 * 16 + 40 * 32 * 8 + 64 * 4;  // one short-search pool slot
 uint32_t strip_row(uint32_t H, uint32_t G, uint32_t g) { return (uint32_t)((uint64_t)g * H / G); }
@@ -273,8 +318,12 @@ struct vdi_ctx {
   cudaEvent_t gev[2] = {nullptr, nullptr};
   // vdi_composite_frames: the root's inflate stream and the non-root strips
   cudaStream_t gst = nullptr;
+  cudaStream_t gsst = nullptr;  // the non-root strips' gather sends (beside the next frame's search)
+  cudaEvent_t sev_merged[2] = {};
   cudaEvent_t gev_in = nullptr, gev_out = nullptr;
-  DevBuf fs_count[2], fs_depth[2], fs_rgba[2];
+  static constexpr int kStripBufs = 4;  // non-root strips in flight (frame f reuses frame f-4's)
+  DevBuf fs_count[kStripBufs], fs_depth[kStripBufs], fs_rgba[kStripBufs];
+  cudaEvent_t fsev[kStripBufs] = {};  // strip buffer read by its gather send
   ~vdi_ctx() {
     if (sst) {
       cudaStreamSynchronize(sst);
@@ -292,6 +341,14 @@ struct vdi_ctx {
       if (xev_bounds[i]) cudaEventDestroy(xev_bounds[i]);
       if (xev_merged[i]) cudaEventDestroy(xev_merged[i]);
     }
+    if (gsst) {
+      cudaStreamSynchronize(gsst);
+      cudaStreamDestroy(gsst);
+    }
+    for (int i = 0; i < kStripBufs; ++i)
+      if (fsev[i]) cudaEventDestroy(fsev[i]);
+    for (int i = 0; i < 2; ++i)
+      if (sev_merged[i]) cudaEventDestroy(sev_merged[i]);
     if (gst) {
       cudaStreamSynchronize(gst);
       cudaStreamDestroy(gst);
@@ -504,15 +561,20 @@ static vdi_status merge_lists(vdi_ctx* ctx, MergeParams& mp, uint64_t P, uint64_
       CUDA_TRY(ctx, launch_scan(mp, ctx->group_sum.as<uint32_t>(), ctx->group_base.as<uint32_t>(), st, &launches));
     if (timing) CUDA_TRY(ctx, cudaEventRecord(ctx->ev[3], st));
     // pass-through (writes every slot of the strip) -> search kernels -> general path
+    trace("fast_start", st);
     CUDA_TRY(ctx, launch_fast(mp, st, &launches));
+    trace("fast_end", st);
     if (timing) CUDA_TRY(ctx, cudaEventRecord(ctx->ev[4], st));
     if (sst != st) {
       CUDA_TRY(ctx, cudaEventRecord(ctx->mev_fast[b], st));
       CUDA_TRY(ctx, cudaStreamWaitEvent(sst, ctx->mev_fast[b], 0));
     }
+    trace("search_start", sst);
     CUDA_TRY(ctx, launch_search(mp, sst, &launches));
+    trace("search_end", sst);
     if (timing) CUDA_TRY(ctx, cudaEventRecord(ctx->ev[5], sst));
     CUDA_TRY(ctx, launch_general(mp, sst, &launches));
+    trace("general_end", sst);
     if (stats) CUDA_TRY(ctx, launch_margins(mp, sst, &launches));
   }
   launches_ref += launches;
@@ -983,6 +1045,7 @@ static vdi_status exchange_push(vdi_ctx* ctx, const vdi_dense_view* local, const
   const uint64_t Pimg = (uint64_t)W * cf.height;
   const uint32_t ngimg = (uint32_t)((Pimg + 31) / 32);
   const bool aligned = L.aligned();
+  trace("push_begin", pst);
   CUDA_TRY(ctx, cudaMemsetAsync(ctx->ccnt.p, 0, 8, pst));
   CUDA_TRY(ctx, cudaMemsetAsync(ctx->srcbase.as<uint32_t>() + (size_t)par * VDI_MAX_SRC, 0, (size_t)n * 4, pst));
   unsigned long long* bnd = ctx->bnd.as<unsigned long long>();
@@ -1032,6 +1095,7 @@ static vdi_status exchange_push(vdi_ctx* ctx, const vdi_dense_view* local, const
     if (vdi_status s = wait_flags(ctx, XFREE, wt, pst)) return s;
     ++launches;
   }
+  trace("push_free", pst);
   std::vector<PushSeg> segs;
   for (uint32_t l = 0; l < n_local; ++l) {
     const uint32_t pe = flocal ? full_ids[l] : local[l].pe_id;
@@ -1077,6 +1141,7 @@ static vdi_status exchange_push(vdi_ctx* ctx, const vdi_dense_view* local, const
     CUDA_TRY(ctx, cudaMemcpyAsync(dsegs, segs.data(), segs.size() * sizeof(PushSeg), cudaMemcpyHostToDevice, pst));
     CUDA_TRY(ctx, launch_push(dsegs, (uint32_t)segs.size(), push_blocks(n_local, G), pst));
     ++launches;
+    trace("push_end", pst);
     if (ctx->grp)
       if (vdi_status s = loop_post(ctx, XREADY, dests, e, pst)) return s;
   }
@@ -1104,10 +1169,12 @@ static vdi_status exchange_recv(vdi_ctx* ctx, const vdi_dense_view* local, const
       const uint32_t nl = L.n_local(s);
       wt.push_back({s, e * nl * push_blocks(nl, G), e});
     }
+  trace("recv_wait", ctx->stream);
   if (!wt.empty()) {
     if (vdi_status st = wait_flags(ctx, XREADY, wt)) return st;
     ++launches;
   }
+  trace("recv_ready", ctx->stream);
   const size_t Pm = ctx->P;
   uint32_t l_of[VDI_MAX_SRC];
   for (uint32_t s = 0; s < n; ++s) l_of[s] = slot[s] >= 0 ? (uint32_t)slot[s] : 0u;
@@ -1358,11 +1425,13 @@ static vdi_status gather_send(vdi_ctx* ctx, const vdi_full_view* strip, uint32_t
   const Layout& L = ctx->lay;
   const uint32_t me = ctx->cfg.rank, W = ctx->cfg.width, k = ctx->cfg.k_out;
   char* gp = ctx->peer[R] + L.g_off(R, j & 1);
+  trace("gsend_begin", st);
   CUDA_TRY(ctx, cudaMemsetAsync(ctx->ccnt.as<unsigned long long>() + 1, 0, 8, st));
   if (j > (ctx->grp ? 1u : 2u)) {  // the root has inflated this buffer's previous contents
     if (vdi_status s = wait_flags(ctx, GFREE, {{R, j - 2, j - 1}}, st)) return s;
     ++launches;
   }
+  trace("gsend_free", st);
   const uint32_t P = (uint32_t)ctx->P, ng = (P + 31) / 32;
   MergeParams ms{};
   ms.n_src = 1;
@@ -1388,6 +1457,7 @@ static vdi_status gather_send(vdi_ctx* ctx, const vdi_full_view* strip, uint32_t
   a.flag = flag_at(ctx->peer[R], GREADY, me);
   CUDA_TRY(ctx, launch_compact_push(a, compact_push_blocks(P), st));
   ++launches;
+  trace("gsend_end", st);
   if (ctx->grp) return loop_post(ctx, GREADY, {R}, j, st);
   return VDI_OK;
 }
@@ -1402,8 +1472,10 @@ static vdi_status gather_recv(vdi_ctx* ctx, vdi_full_view* image, uint32_t j, cu
   std::vector<WaitOn> wt;
   for (uint32_t g = 0; g < G; ++g)
     if (g != R) wt.push_back({g, j * compact_push_blocks(L.rows(g) * W), j});
+  trace("grecv_wait", st);
   if (vdi_status s = wait_flags(ctx, GREADY, wt, st)) return s;
   ++launches;
+  trace("grecv_ready", st);
   const uint8_t* gc = reinterpret_cast<const uint8_t*>(gp + L.g_count_off());
   const uint32_t* gb = reinterpret_cast<const uint32_t*>(gp + L.g_gbase_off());
   const float2* gd = reinterpret_cast<const float2*>(gp + L.g_depth_off());
@@ -1424,6 +1496,7 @@ static vdi_status gather_recv(vdi_ctx* ctx, vdi_full_view* image, uint32_t j, cu
   std::vector<uint32_t> others;
   for (uint32_t g = 0; g < G; ++g)
     if (g != R) others.push_back(g);
+  trace("grecv_inflated", st);
   if (vdi_status s = signal_peers(ctx, GFREE, others, j, st, j)) return s;
   ++launches;
   return VDI_OK;
@@ -1499,7 +1572,7 @@ vdi_status vdi_gather_root(vdi_ctx* ctx, uint32_t root, const vdi_full_view* str
 // straight into the rows of images[f] and re-inflates the other rows on a
 // second stream, so that its exchange and merge of frame f+1 do not wait for
 // its inflate of frame f (and neither do the other ranks, whose next slices
-// it pushes right after its merge).  Non-root strips: two ctx-owned buffers.
+// it pushes right after its merge).  Non-root strips: four ctx-owned buffers, each compacted to the root on its own stream.
 vdi_status vdi_composite_frames(vdi_ctx* ctx, uint32_t F, const vdi_dense_view* local, uint32_t n_local,
                                 vdi_full_view* images, const uint32_t* roots) {
   if (vdi_status s = check_ctx(ctx)) return s;
@@ -1528,6 +1601,10 @@ vdi_status vdi_composite_frames(vdi_ctx* ctx, uint32_t F, const vdi_dense_view* 
     CUDA_TRY(ctx, cudaStreamCreateWithFlags(&ctx->sst, cudaStreamNonBlocking));
     CUDA_TRY(ctx, cudaStreamCreateWithFlags(&ctx->xst, cudaStreamNonBlocking));
     CUDA_TRY(ctx, cudaStreamCreateWithFlags(&ctx->gst, cudaStreamNonBlocking));
+    CUDA_TRY(ctx, cudaStreamCreateWithFlags(&ctx->gsst, cudaStreamNonBlocking));
+    for (int i = 0; i < 2; ++i) CUDA_TRY(ctx, cudaEventCreateWithFlags(&ctx->sev_merged[i], cudaEventDisableTiming));
+    for (int i = 0; i < vdi_ctx::kStripBufs; ++i)
+      CUDA_TRY(ctx, cudaEventCreateWithFlags(&ctx->fsev[i], cudaEventDisableTiming));
     CUDA_TRY(ctx, cudaEventCreateWithFlags(&ctx->gev_in, cudaEventDisableTiming));
     CUDA_TRY(ctx, cudaEventCreateWithFlags(&ctx->gev_out, cudaEventDisableTiming));
     for (int i = 0; i < 2; ++i) {
@@ -1536,14 +1613,14 @@ vdi_status vdi_composite_frames(vdi_ctx* ctx, uint32_t F, const vdi_dense_view* 
     }
   }
   if (G > 1)
-    for (int i = 0; i < 2; ++i) {
+    for (uint32_t i = 0; i < std::min<uint32_t>(F, vdi_ctx::kStripBufs); ++i) {
       CUDA_TRY(ctx, ctx->fs_count[i].grow(P));
       CUDA_TRY(ctx, ctx->fs_depth[i].grow(P * k * 8));
       CUDA_TRY(ctx, ctx->fs_rgba[i].grow(P * k * 16));
     }
   // the side streams start once the caller's stream has reached this call
   CUDA_TRY(ctx, cudaEventRecord(ctx->gev_in, st));
-  for (cudaStream_t x : {ctx->gst, ctx->xst, ctx->sst}) CUDA_TRY(ctx, cudaStreamWaitEvent(x, ctx->gev_in, 0));
+  for (cudaStream_t x : {ctx->gst, ctx->gsst, ctx->xst, ctx->sst}) CUDA_TRY(ctx, cudaStreamWaitEvent(x, ctx->gev_in, 0));
   int launches = 0;
   vdi_status err = VDI_OK;
   for (uint32_t f = 0; f < F && err == VDI_OK; ++f) {
@@ -1555,9 +1632,11 @@ vdi_status vdi_composite_frames(vdi_ctx* ctx, uint32_t F, const vdi_dense_view* 
     } else if (R == me) {  // the root's strip is its image rows
       so = vdi_full_view{ctx->row0, ctx->row1, images[f].count + o, images[f].depth + o * k * 2,
                          images[f].rgba + o * k * 4};
-    } else {
-      so = vdi_full_view{ctx->row0, ctx->row1, ctx->fs_count[b].as<uint8_t>(), ctx->fs_depth[b].as<float>(),
-                         ctx->fs_rgba[b].as<float>()};
+    } else {  // a ctx-owned strip buffer; frame f - kStripBufs's gather send must have read it
+      const int sb = (int)(f % vdi_ctx::kStripBufs);
+      so = vdi_full_view{ctx->row0, ctx->row1, ctx->fs_count[sb].as<uint8_t>(), ctx->fs_depth[sb].as<float>(),
+                         ctx->fs_rgba[sb].as<float>()};
+      if (f >= (uint32_t)vdi_ctx::kStripBufs) CUDA_TRY(ctx, cudaStreamWaitEvent(st, ctx->fsev[sb], 0));
     }
     // frame f's push runs on the push stream beside frame f-1's merge; its
     // double-buffered exchange arrays wait for the merge of frame f-2
@@ -1568,6 +1647,7 @@ vdi_status vdi_composite_frames(vdi_ctx* ctx, uint32_t F, const vdi_dense_view* 
       ctx->xpar = b;
       if (f >= 2) err = cudaStreamWaitEvent(ctx->xst, ctx->xev_merged[b], 0) == cudaSuccess ? VDI_OK : VDI_ERR_CUDA;
     }
+    g_trace_frame = (int)f;
     if (err == VDI_OK) err = vdi_composite(ctx, local + (size_t)f * n_local, n_local, &so);
     ctx->xpst = nullptr;
     ctx->xpar = 0;
@@ -1578,21 +1658,30 @@ vdi_status vdi_composite_frames(vdi_ctx* ctx, uint32_t F, const vdi_dense_view* 
     cudaStream_t es = overlap ? ctx->sst : st;  // the stream the frame's merge ends on
     if (G > 1) {
       const uint32_t j = ++ctx->gcalls_to[R];
-      if (R != me) err = gather_send(ctx, &so, R, j, es, launches);
-      else err = gather_recv(ctx, &images[f], j, ctx->gst, launches);
+      if (R != me) {  // the compaction on its own stream: the next frame's search does not wait for it
+        CUDA_TRY(ctx, cudaEventRecord(ctx->sev_merged[b], es));
+        CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->gsst, ctx->sev_merged[b], 0));
+        err = gather_send(ctx, &so, R, j, ctx->gsst, launches);
+        if (err == VDI_OK) CUDA_TRY(ctx, cudaEventRecord(ctx->fsev[f % vdi_ctx::kStripBufs], ctx->gsst));
+      } else {
+        err = gather_recv(ctx, &images[f], j, ctx->gst, launches);
+      }
       ctx->last_gather_root = (int)R;
       ctx->last_gather_parity = j & 1;
     }
-    // this parity's merge scratch and strip buffer are free again
+    g_trace_frame = -1;
+    // this parity's merge scratch is free again
     if (err == VDI_OK && overlap) CUDA_TRY(ctx, cudaEventRecord(ctx->mev_done[b], es));
   }
   if (err != VDI_OK) return err;
   // the call ends on the caller's stream once the side streams have too
-  for (cudaStream_t x : {ctx->gst, ctx->xst, ctx->sst}) {
+  for (cudaStream_t x : {ctx->gst, ctx->gsst, ctx->xst, ctx->sst}) {
     CUDA_TRY(ctx, cudaEventRecord(ctx->gev_out, x));
     CUDA_TRY(ctx, cudaStreamWaitEvent(st, ctx->gev_out, 0));
   }
   ctx->last.kernel_launches = (uint32_t)launches;
+  g_trace_rank = (int)me;
+  trace_dump(st);
   return VDI_OK;
 }
 
