@@ -764,9 +764,13 @@ __device__ __forceinline__ void gather_short_batch(const MergeParams& mp, uint32
 // -- then the memoised bisection (see Bisection) sweeps while any lane still
 // needs a count; (|acc|^2, |acc - s|^2) are one packed f32x2 chain.  Keeping
 // only R samples in registers raises the resident warps per SM (8 at 40
-// register samples, 12 at 24).
+// register samples, 16 at 16); the shared rows are swept by a rolled loop of
+// 8-step chunks, which keeps the kernel's code (and instruction-cache misses)
+// small.
 #ifndef VDI_SWEEP_R
-#define VDI_SWEEP_R 24  // measured (C3 search stage): R = 8 / 16 / 24 / 40 -> 0.160 / 0.161 / 0.153 / 0.160 ms
+// measured (C3 search stage; shared part rolled): R = 8 / 16 / 24 -> 0.146 / 0.138 / 0.143 ms
+// (fully unrolled: R = 8 / 16 / 24 / 40 -> 0.160 / 0.161 / 0.153 / 0.160)
+#define VDI_SWEEP_R 16
 #endif
 __device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(sdst)), "l"(gsrc) : "memory");
@@ -806,7 +810,6 @@ __device__ __forceinline__ void sweep_batch(const MergeParams& mp, int bucket, u
 #pragma unroll
     for (int q = 0; q < R; ++q) S[q] = (q < mi && !bad) ? col[q * 32] : nan4;
     cp_async_wait_all();  // each lane reads only its own column: no warp barrier needed
-    auto smp = [&](int q) -> float4 { return q < R ? S[q < R ? q : 0] : sm[(q - R) * 32 + lane]; };
     // memoised bisection: a count sweep at g2 takes the same decisions for
     // every g2' in [L, U), so a later midpoint inside the interval of the
     // latest sweep on either side of the bracket reuses its count; each lane
@@ -820,66 +823,88 @@ __device__ __forceinline__ void sweep_batch(const MergeParams& mp, int bucket, u
       const float g2 = bs.g2;
       float ar = 0.f, ag = 0.f, ab = 0.f, aa = 0.f, L = -1.f, U = CUDART_INF_F;
       int sc = 0;
-#pragma unroll
-      for (int q = 0; q < MS; ++q) {
-        if ((q & 7) == 0 && q > 0 && !__any_sync(kFull, bs.active && q < mi && sc <= k)) break;
-        const float4 sv = smp(q);
+      auto cstep = [&](const float4 sv, bool first) {
         const bool gap = sv.w < 0.f;  // NaN padding: false
         const float sa = fabsf(sv.w);
         float n2, d2;
         n2d2_packed(ar, ag, ab, aa, sv.x, sv.y, sv.z, sa, n2, d2);
         const bool gcl = gap & (n2 > g2);
         const bool dsp = d2 > g2;
-        if (q > 0) {  // comparisons that did not happen contribute NaN (ignored by fminf / fmaxf)
+        if (!first) {  // comparisons that did not happen contribute NaN (ignored by fminf / fmaxf)
           U = fminf(U, fminf(gcl ? n2 : qnan, (!gcl & dsp) ? d2 : qnan));
           L = fmaxf(L, fmaxf((gap & !gcl) ? n2 : qnan, (!gcl & !dsp) ? d2 : qnan));
         }
-        const bool st = (q == 0) | gcl | dsp;
+        const bool st = first | gcl | dsp;
         const float tr = 1.0f - aa;
         ar = st ? sv.x : fmaf(tr, sv.x, ar);
         ag = st ? sv.y : fmaf(tr, sv.y, ag);
         ab = st ? sv.z : fmaf(tr, sv.z, ab);
         aa = st ? sa : fmaf(tr, sa, aa);
         sc += st ? 1 : 0;
+      };
+      bool more = true;
+#pragma unroll
+      for (int q = 0; q < R; ++q) {  // the register samples: static indices
+        if ((q & 7) == 0 && q > 0 && !__any_sync(kFull, bs.active && q < mi && sc <= k)) {
+          more = false;
+          break;
+        }
+        cstep(S[q], q == 0);
+      }
+      if (more) {
+#pragma unroll 1
+        for (int q0 = R; q0 < MS; q0 += 8) {  // the shared rows: a rolled loop of 8-step chunks (code size)
+          if (!__any_sync(kFull, bs.active && q0 < mi && sc <= k)) break;
+#pragma unroll
+          for (int u = 0; u < 8; ++u) cstep(sm[(q0 - R + u) * 32 + lane], false);
+        }
       }
       if (bs.active) bs.swept(sc, L, U, k, mp.max_iters);
     }
     const float best = bs.best;
-    if (valid && !bad) {  // final write sweep, unrolled: static sample indices
+    if (valid && !bad) {  // final write sweep
       const float gg = best * best;
       float2* od = mp.out_depth + (size_t)p * k;
       float4* oc = mp.out_rgba + (size_t)p * k;
       float ar = 0.f, ag = 0.f, ab = 0.f, aa = 0.f, tf = 0.f, tb = 0.f;
       int c = 0;
+      auto wstep = [&](const float4 sv, const float2 d, int q) {
+        const bool gap = sv.w < 0.f;
+        const float sa = fabsf(sv.w);
+        const float n2 = fmaf(aa, aa, fmaf(ab, ab, fmaf(ag, ag, ar * ar)));
+        const float d2 = dist2(ar, ag, ab, aa, sv.x, sv.y, sv.z, sa);
+        const bool st = (q == 0) | (gap & (n2 > gg)) | (d2 > gg);
+        if (st && q > 0 && c <= k) {  // close the open segment (ends at its last content sample)
+          od[c - 1] = make_float2(tf, tb);
+          oc[c - 1] = make_float4(ar, ag, ab, aa);
+        }
+        const float tr = 1.0f - aa;
+        ar = st ? sv.x : fmaf(tr, sv.x, ar);
+        ag = st ? sv.y : fmaf(tr, sv.y, ag);
+        ab = st ? sv.z : fmaf(tr, sv.z, ab);
+        aa = st ? sa : fmaf(tr, sa, aa);
+        tf = st ? d.x : tf;
+        tb = d.y;
+        c += st ? 1 : 0;
+      };
       float2 dq[8];
 #pragma unroll
-      for (int q = 0; q < MS; ++q) {
+      for (int q = 0; q < R; ++q) {
         if ((q & 7) == 0) {  // depth of the next 8 samples: loads issued together, before the stores
 #pragma unroll
           for (int u = 0; u < 8; ++u)
-            if (q + u < MS && q + u < mi) dq[u] = dcol[(q + u) * 32];
+            if (q + u < mi) dq[u] = dcol[(q + u) * 32];
         }
-        if (q < mi) {
-          const float4 sv = smp(q);
-          const float2 d = dq[q & 7];
-          const bool gap = sv.w < 0.f;
-          const float sa = fabsf(sv.w);
-          const float n2 = fmaf(aa, aa, fmaf(ab, ab, fmaf(ag, ag, ar * ar)));
-          const float d2 = dist2(ar, ag, ab, aa, sv.x, sv.y, sv.z, sa);
-          const bool st = (q == 0) | (gap & (n2 > gg)) | (d2 > gg);
-          if (st && q > 0 && c <= k) {  // close the open segment (ends at its last content sample)
-            od[c - 1] = make_float2(tf, tb);
-            oc[c - 1] = make_float4(ar, ag, ab, aa);
-          }
-          const float tr = 1.0f - aa;
-          ar = st ? sv.x : fmaf(tr, sv.x, ar);
-          ag = st ? sv.y : fmaf(tr, sv.y, ag);
-          ab = st ? sv.z : fmaf(tr, sv.z, ab);
-          aa = st ? sa : fmaf(tr, sa, aa);
-          tf = st ? d.x : tf;
-          tb = d.y;
-          c += st ? 1 : 0;
-        }
+        if (q < mi) wstep(S[q], dq[q & 7], q);
+      }
+#pragma unroll 1
+      for (int q0 = R; q0 < mi; q0 += 8) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (q0 + u < mi) dq[u] = dcol[(q0 + u) * 32];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (q0 + u < mi) wstep(sm[(q0 - R + u) * 32 + lane], dq[u], q0 + u);
       }
       if (mi > 0 && c <= k) {
         od[c - 1] = make_float2(tf, tb);
@@ -892,7 +917,7 @@ __device__ __forceinline__ void sweep_batch(const MergeParams& mp, int bucket, u
 }
 
 #ifndef VDI_SWEEP_MINB
-#define VDI_SWEEP_MINB 12  // 168 registers at R = 24: 12 warps per SM
+#define VDI_SWEEP_MINB 16  // 128 registers at R = 16: 16 warps per SM
 #endif
 
 // ---------------------------------------------------------------------------
