@@ -767,6 +767,12 @@ __device__ __forceinline__ void gather_short_batch(const MergeParams& mp, uint32
 // register samples, 16 at 16); the shared rows are swept by a rolled loop of
 // 8-step chunks, which keeps the kernel's code (and instruction-cache misses)
 // small.
+#ifndef VDI_MEMO_CHEAP
+#define VDI_MEMO_CHEAP 1  // interval bookkeeping with one select per comparison
+#endif
+#ifndef VDI_MEMO
+#define VDI_MEMO 1  // 0: plain bisection in the short sweep (A/B of the memo's cost)
+#endif
 #ifndef VDI_SWEEP_R
 // measured (C3 search stage; shared part rolled): R = 8 / 16 / 24 -> 0.146 / 0.138 / 0.143 ms
 // (fully unrolled: R = 8 / 16 / 24 / 40 -> 0.160 / 0.161 / 0.153 / 0.160)
@@ -828,12 +834,27 @@ __device__ __forceinline__ void sweep_batch(const MergeParams& mp, int bucket, u
         const float sa = fabsf(sv.w);
         float n2, d2;
         n2d2_packed(ar, ag, ab, aa, sv.x, sv.y, sv.z, sa, n2, d2);
+#if VDI_MEMO_CHEAP
+        // the comparisons of this step: v1 = |acc|^2 at a gap (Q8), v2 = D^2
+        // unless the gap closed the segment; NaN = not made (ignored below)
+        const float v1 = gap ? n2 : qnan;
+        const bool gcl = v1 > g2;
+        const float v2 = gcl ? qnan : d2;
+        const bool dsp = v2 > g2;
+        if (!first && VDI_MEMO) {  // a split tightens U, a merge raises L
+          U = gcl ? fminf(U, v1) : U;
+          L = gcl ? L : fmaxf(L, v1);
+          U = dsp ? fminf(U, v2) : U;
+          L = dsp ? L : fmaxf(L, v2);
+        }
+#else
         const bool gcl = gap & (n2 > g2);
         const bool dsp = d2 > g2;
         if (!first) {  // comparisons that did not happen contribute NaN (ignored by fminf / fmaxf)
           U = fminf(U, fminf(gcl ? n2 : qnan, (!gcl & dsp) ? d2 : qnan));
           L = fmaxf(L, fmaxf((gap & !gcl) ? n2 : qnan, (!gcl & !dsp) ? d2 : qnan));
         }
+#endif
         const bool st = first | gcl | dsp;
         const float tr = 1.0f - aa;
         ar = st ? sv.x : fmaf(tr, sv.x, ar);
@@ -859,7 +880,7 @@ __device__ __forceinline__ void sweep_batch(const MergeParams& mp, int bucket, u
           for (int u = 0; u < 8; ++u) cstep(sm[(q0 - R + u) * 32 + lane], false);
         }
       }
-      if (bs.active) bs.swept(sc, L, U, k, mp.max_iters);
+      if (bs.active) bs.swept(sc, VDI_MEMO ? L : 1.f, VDI_MEMO ? U : 0.f, k, mp.max_iters);
     }
     const float best = bs.best;
     if (valid && !bad) {  // final write sweep
