@@ -520,6 +520,8 @@ def _run_ours(args, world, rank, local, clk):
     ing_max = allreduce_max(bytes_recv, G)
     eg_max = allreduce_max(bytes_sent, G)
     ms_ex_max = allreduce_max(ms_ex, G)
+    ms_push = statistics.mean(c.get("ms_push", 0.0) for c in cnts)
+    push_rate_min = -allreduce_max(-(bytes_sent / max(ms_push, 1e-6) / 1e6), G) if G > 1 else 0.0
 
     # ---- Phase 1 + Phase 2 of one VDI
     v2r = []
@@ -719,6 +721,9 @@ def _run_ours(args, world, rank, local, clk):
                 "exchange_frac": max(ing_max, eg_max) / max(ms_ex_max, 1e-6) / 1e6 / 900.0,
                 "exchange_note": "max over ranks of max(egress, ingress) bytes / the exchange stage time (strip "
                                  "bounds + push + ready wait), one-VDI steps",
+                "push_kernel_GBs": push_rate_min, "push_kernel_frac": push_rate_min / 900.0,
+                "push_kernel_note": "min over ranks of the rank's pushed bytes / its push kernel's CUDA-event time "
+                                    "(the NVLink egress rate of the exchange kernel itself), one-VDI steps",
                 "gather_into_root_GBs": cnts[-1]["bytes_gather"] / max(ms_ga, 1e-6) / 1e6,
                 "gather_into_root_frac": cnts[-1]["bytes_gather"] / max(ms_ga, 1e-6) / 1e6 / 900.0,
                 "gather_note": "dense bytes into the root / gather stage time (includes the root's wait and its "

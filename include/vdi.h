@@ -383,6 +383,8 @@ typedef struct {
   uint64_t sweep_steps;      /* VDI_FLAG_PIXEL_STATS: sample-steps of the plain bisection procedure (every count
                                 sweep to its early exit + the final sweep) over the searched lists -- the
                                 algorithmic work of the search (the kernels' memoised bisection skips some) */
+  float ms_push;             /* VDI_FLAG_STAGE_TIMING, n_ranks > 1: the exchange push kernel alone (CUDA events on
+                                the push stream): bytes_sent / ms_push is this rank's NVLink egress rate */
 } vdi_counters;
 vdi_status vdi_get_counters(vdi_ctx* ctx, vdi_counters* out);
 

@@ -74,7 +74,8 @@ class vdi_counters(C.Structure):
                 ("bytes_received", C.c_uint64), ("kernel_launches", C.c_uint32), ("ms_exchange", C.c_float),
                 ("ms_merge", C.c_float), ("ms_gather", C.c_float), ("bucket_lists", C.c_uint64 * 4),
                 ("general_lists", C.c_uint64), ("bytes_gather", C.c_uint64), ("fallback_groups", C.c_uint64),
-                ("ms_scan", C.c_float), ("ms_fast", C.c_float), ("ms_search", C.c_float), ("sweep_steps", C.c_uint64)]
+                ("ms_scan", C.c_float), ("ms_fast", C.c_float), ("ms_search", C.c_float), ("sweep_steps", C.c_uint64),
+                ("ms_push", C.c_float)]
 
 
 # name -> (restype, argtypes) exactly as declared in include/vdi.h

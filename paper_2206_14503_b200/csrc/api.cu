@@ -316,6 +316,8 @@ struct vdi_ctx {
   bool timing_pending = false;
   bool gather_timing_pending = false;
   cudaEvent_t gev[2] = {nullptr, nullptr};
+  cudaEvent_t pev_t[2] = {nullptr, nullptr};  // STAGE_TIMING: around the exchange push kernel
+  bool push_timing_pending = false;
   // vdi_composite_frames: the root's inflate stream and the non-root strips
   cudaStream_t gst = nullptr;
   cudaStream_t gsst = nullptr;  // the non-root strips' gather sends (beside the next frame's search)
@@ -347,8 +349,10 @@ struct vdi_ctx {
     }
     for (int i = 0; i < kStripBufs; ++i)
       if (fsev[i]) cudaEventDestroy(fsev[i]);
-    for (int i = 0; i < 2; ++i)
+    for (int i = 0; i < 2; ++i) {
       if (sev_merged[i]) cudaEventDestroy(sev_merged[i]);
+      if (pev_t[i]) cudaEventDestroy(pev_t[i]);
+    }
     if (gst) {
       cudaStreamSynchronize(gst);
       cudaStreamDestroy(gst);
@@ -1139,8 +1143,18 @@ static vdi_status exchange_push(vdi_ctx* ctx, const vdi_dense_view* local, const
   if (!segs.empty()) {
     PushSeg* dsegs = ctx->segbuf.as<PushSeg>() + (size_t)par * VDI_MAX_SRC * VDI_MAX_RANKS;
     CUDA_TRY(ctx, cudaMemcpyAsync(dsegs, segs.data(), segs.size() * sizeof(PushSeg), cudaMemcpyHostToDevice, pst));
+    const bool ptime = cf.flags & VDI_FLAG_STAGE_TIMING;
+    if (ptime) {
+      if (!ctx->pev_t[0])
+        for (int i = 0; i < 2; ++i) CUDA_TRY(ctx, cudaEventCreate(&ctx->pev_t[i]));
+      CUDA_TRY(ctx, cudaEventRecord(ctx->pev_t[0], pst));
+    }
     CUDA_TRY(ctx, launch_push(dsegs, (uint32_t)segs.size(), push_blocks(n_local, G), pst));
     ++launches;
+    if (ptime) {
+      CUDA_TRY(ctx, cudaEventRecord(ctx->pev_t[1], pst));
+      ctx->push_timing_pending = true;
+    }
     trace("push_end", pst);
     if (ctx->grp)
       if (vdi_status s = loop_post(ctx, XREADY, dests, e, pst)) return s;
@@ -2228,6 +2242,10 @@ vdi_status vdi_get_counters(vdi_ctx* ctx, vdi_counters* out) {
   if (ctx->gather_timing_pending) {
     CUDA_TRY(ctx, cudaEventElapsedTime(&ctx->last.ms_gather, ctx->gev[0], ctx->gev[1]));
     ctx->gather_timing_pending = false;
+  }
+  if (ctx->push_timing_pending) {
+    CUDA_TRY(ctx, cudaEventElapsedTime(&ctx->last.ms_push, ctx->pev_t[0], ctx->pev_t[1]));
+    ctx->push_timing_pending = false;
   }
   *out = ctx->last;
   return VDI_OK;
