@@ -286,7 +286,12 @@ def _run_ours(args, world, rank, local, clk):
 
     cfg = get_config(args)
     G, n, W, H, k = world, cfg.n_pes, cfg.W, cfg.H, cfg.k_out
-    F = args.frames if args.frames > 0 else 4  # VDIs per step (frames in flight)
+    # VDIs per step (frames in flight): 4 per GPU -- a rank's pipeline (push,
+    # merge, search, gather send / inflate on their own streams) needs about
+    # four frames to keep its kernels overlapped (profiles/r2_frames_probe_g*.json)
+    F = args.frames if args.frames > 0 else 4 * G
+    img_bytes = W * H * (1 + 24 * k)
+    F = max(1, min(F, int((48 << 30) // img_bytes)))  # every frame has its own full image (<= 48 GB of them)
     stream = torch.cuda.current_stream()
 
     def new_uid():
@@ -422,7 +427,7 @@ def _run_ours(args, world, rank, local, clk):
     # ---- N > 1: secondary modes -- a rotating root (frame f gathered on
     # rank f mod G), latency mode (1 VDI per step, stage breakdown), and the
     # full-representation pipeline of Fig. 6
-    latency = rotating = full_rep = None
+    latency = rotating = full_rep = replicas = None
     K1 = max(10, args.steps // 4)
     l_ms, lstage, _ = timed(K1, 0, frames=1)
     l_tot = allreduce_max(sum(l_ms), G)
@@ -463,6 +468,29 @@ def _run_ours(args, world, rank, local, clk):
             torch.cuda.synchronize()
             xs[-1]["ms"] = e0.elapsed_time(e1)
         xm = allreduce_max(statistics.mean(x["ms"] for x in xs), G)
+        # secondary: replicas -- every GPU composites whole VDIs of its own (all
+        # n sub-VDIs resident on each GPU, no strips, no exchange, no gather)
+        comp1 = vdi.Compositor(W, H, cfg.k_in, k, n, stream=stream)
+        allpes = [comp1.generate_subvdi(vol, tft, synth.make_camera(W, H, view=0), dec, pe) for pe in range(n)]
+        ims1 = [vdi.FullVDI.empty(W, 0, H, k) for _ in range(F)]
+        for _ in range(3):
+            comp1.composite_frames([allpes] * F, ims1)
+        K2 = max(10, args.steps // 4)
+        r_evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K2)]
+        torch.cuda.synchronize()
+        barrier(G)
+        for i in range(K2):
+            flush.zero_()
+            r_evs[i][0].record(stream)
+            comp1.composite_frames([allpes] * F, ims1)
+            r_evs[i][1].record(stream)
+        torch.cuda.synchronize()
+        barrier(G)
+        rep_tot = allreduce_max(sum(a_.elapsed_time(b_) for a_, b_ in r_evs), G)
+        replicas = {"vdis_per_s": G * F * K2 / (rep_tot / 1e3), "ms_per_vdi_per_gpu": rep_tot / (K2 * F), "steps": K2,
+                    "note": "secondary (not the paper's split): every GPU composites whole VDIs of its own, all n "
+                            "sub-VDIs resident on each GPU, no exchange or gather; view V0"}
+        del comp1, allpes, ims1
         full_rep = {"ms_per_vdi": xm, "value": 1e3 / xm, "steps": Kx,
                     "stages_ms": {s_: statistics.mean(c_[f"ms_{s_}"] for c_ in xs) for s_ in ("exchange", "merge", "gather")},
                     "exchange_bytes_sent_rank0": xs[-1]["bytes_sent"],
@@ -708,6 +736,7 @@ def _run_ours(args, world, rank, local, clk):
             "volume_to_root_vdi": volume_to_root,
             "latency_mode": latency,
             "rotating_root": rotating,
+            "replicas_whole_frames": replicas,
             "full_representation_mode": full_rep,
             "f4": f4,
             "supersegments_merged_per_s": S_total * value,
@@ -756,7 +785,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-f4", action="store_true", help="skip the limit-case / rendering-quality measurements")
     ap.add_argument("--rotating", action="store_true", help="N > 1: also time a root rotating over the frames")
-    ap.add_argument("--frames", type=int, default=0, help="N > 1: VDIs per step (default 4)")
+    ap.add_argument("--frames", type=int, default=0, help="VDIs per step (frames in flight; default 4 per GPU)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     world, rank, local = dist_setup()

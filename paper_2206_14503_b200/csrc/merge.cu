@@ -996,6 +996,25 @@ __device__ __forceinline__ float4 src_ld4(const float4* a) {
   return __ldg(a);
 #endif
 }
+// the slots' depth column: written by the gather, read once by the final
+// write sweep -- evict first, so the rgba rows the sweeps re-read stay in L2
+__device__ __forceinline__ void dep_st(float2* a, float2 v) {
+#if VDI_LONG_POLICY == 1
+  asm volatile("st.global.L2::cache_hint.v2.f32 [%0], {%1,%2}, %3;" ::"l"(a), "f"(v.x), "f"(v.y), "l"(pol_first())
+               : "memory");
+#else
+  *a = v;
+#endif
+}
+__device__ __forceinline__ float2 dep_ld(const float2* a) {
+#if VDI_LONG_POLICY == 1
+  float2 v;
+  asm volatile("ld.global.L2::cache_hint.v2.f32 {%0,%1}, [%2], %3;" : "=f"(v.x), "=f"(v.y) : "l"(a), "l"(pol_first()));
+  return v;
+#else
+  return *a;
+#endif
+}
 __device__ __forceinline__ void out_st4(float4* a, float4 v) {
 #if VDI_LONG_POLICY == 1
   asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(a), "f"(v.x), "f"(v.y), "f"(v.z),
@@ -1083,7 +1102,7 @@ __device__ __forceinline__ bool long_gather_lane(const MergeParams& mp, uint32_t
             if (r > 0 && d.x > prev_tb) c.w = -c.w;  // gap before this sample: sign of alpha
             prev_tb = d.y;
             slot_st(orgba + r * 32, c);
-            odep[r * 32] = d;
+            dep_st(odep + r * 32, d);
             ++r;
             ++taken;
           }
@@ -1236,13 +1255,13 @@ __device__ __forceinline__ int long_write(const float4* __restrict__ col, const 
 #pragma unroll
   for (int u = 0; u < 8; ++u) {
     cv[u] = slot_ld(col + u * 32);
-    dv[u] = dcol[u * 32];
+    dv[u] = dep_ld(dcol + u * 32);
   }
   for (int q0 = 0; q0 < m; q0 += 8) {
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
       cn[u] = slot_ld(col + (q0 + 8 + u) * 32);
-      dn[u] = dcol[(q0 + 8 + u) * 32];
+      dn[u] = dep_ld(dcol + (q0 + 8 + u) * 32);
     }
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
