@@ -286,10 +286,12 @@ def _run_ours(args, world, rank, local, clk):
 
     cfg = get_config(args)
     G, n, W, H, k = world, cfg.n_pes, cfg.W, cfg.H, cfg.k_out
-    # VDIs per step (frames in flight): 4 per GPU -- a rank's pipeline (push,
-    # merge, search, gather send / inflate on their own streams) needs about
-    # four frames to keep its kernels overlapped (profiles/r2_frames_probe_g*.json)
-    F = args.frames if args.frames > 0 else 4 * G
+    # VDIs per step (frames in flight): 16, at least 4 per GPU -- within a call
+    # the frames overlap (push, merge, search, gather send / inflate on their
+    # own streams); every call ends with a join of its streams on the caller's
+    # stream, which costs ~0.05 ms per call (C3, 1 GPU: F = 4 / 8 / 16 ->
+    # 0.331 / 0.319 / 0.314 ms per VDI; profiles/r2_frames_probe_g*.json for G > 1)
+    F = args.frames if args.frames > 0 else max(16, 4 * G)
     img_bytes = W * H * (1 + 24 * k)
     F = max(1, min(F, int((48 << 30) // img_bytes)))  # every frame has its own full image (<= 48 GB of them)
     stream = torch.cuda.current_stream()
@@ -785,7 +787,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-f4", action="store_true", help="skip the limit-case / rendering-quality measurements")
     ap.add_argument("--rotating", action="store_true", help="N > 1: also time a root rotating over the frames")
-    ap.add_argument("--frames", type=int, default=0, help="VDIs per step (frames in flight; default 4 per GPU)")
+    ap.add_argument("--frames", type=int, default=0, help="VDIs per step (frames in flight; default max(16, 4 per GPU))")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     world, rank, local = dist_setup()
