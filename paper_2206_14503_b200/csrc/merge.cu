@@ -706,9 +706,15 @@ __device__ __forceinline__ int short_ms(int b) { return b == 0 ? 32 : 40; }
 // heads in registers (long_gather_lane), writes the samples in depth order to
 // the batch's pool slot in [sample][lane] layout with the gap flag in the sign
 // of alpha; transparent / overlapping records -> general path.
-template <int NS>
+template <int NS, int CH = 8>
 __device__ __forceinline__ bool long_gather_lane(const MergeParams& mp, uint32_t m, const uint32_t (&goff)[NS],
                                                  const uint32_t (&cnt)[NS], float4* orgba, float2* odep);
+#ifndef VDI_SGATHER_CH
+#define VDI_SGATHER_CH 8  // records loaded per trip in the short gather
+#endif
+#ifndef VDI_SGATHER_MINB
+#define VDI_SGATHER_MINB 1
+#endif
 template <int NS>
 __device__ __forceinline__ void gather_short_batch(const MergeParams& mp, uint32_t b, uint32_t nb1, uint32_t c0,
                                                    uint32_t c1, uint32_t lane) {
@@ -749,7 +755,7 @@ __device__ __forceinline__ void gather_short_batch(const MergeParams& mp, uint32
   // depths in shared memory and merging there)
   bool bad = false;
   if (valid) {
-    bad = !long_gather_lane<NS>(mp, m, goff, cnt, orgba, odep);
+    bad = !long_gather_lane<NS, VDI_SGATHER_CH>(mp, m, goff, cnt, orgba, odep);
     uint32_t* og = mp.pool_gap + (size_t)slot * 64 + lane;
     og[0] = bad ? 0xffffffffu : 0u;  // skip marker
     og[32] = bad ? 0xffffffffu : 0u;
@@ -1029,7 +1035,7 @@ __device__ __forceinline__ void out_st4(float4* a, float4 v) {
 // (stride 32): run-based k-way merge over the runs' head
 // t_front kept in registers, 8 records loaded per trip.  Returns false for a
 // transparent or overlapping record (Q23, Q12: the general path).
-template <int NS>
+template <int NS, int CH>
 __device__ __forceinline__ bool long_gather_lane(const MergeParams& mp, uint32_t m, const uint32_t (&goff)[NS],
                                                  const uint32_t (&cnt)[NS], float4* orgba, float2* odep) {
   bool bad = false;
@@ -1078,11 +1084,11 @@ __device__ __forceinline__ bool long_gather_lane(const MergeParams& mp, uint32_t
     // reloaded, from L1/L2, when b is chosen again)
     float tn = CUDART_INF_F;
     for (bool first = true;;) {
-      const uint32_t nch = min(8u, cb - ii);
-      float2 dv[8];
-      float4 cv[8];
+      const uint32_t nch = min((uint32_t)CH, cb - ii);
+      float2 dv[CH];
+      float4 cv[CH];
 #pragma unroll
-      for (int u = 0; u < 8; ++u)
+      for (int u = 0; u < CH; ++u)
         if ((uint32_t)u < nch) {
           dv[u] = __ldg(dp + gb + ii + u);
           cv[u] = src_ld4(cp + gb + ii + u);
@@ -1090,7 +1096,7 @@ __device__ __forceinline__ bool long_gather_lane(const MergeParams& mp, uint32_t
       uint32_t taken = 0;
       bool stop = false;
 #pragma unroll
-      for (int u = 0; u < 8; ++u)
+      for (int u = 0; u < CH; ++u)
         if (!stop && (uint32_t)u < nch) {
           const float2 d = dv[u];
           if (!(first && u == 0) && !(d.x < b2t || (d.x == b2t && b < b2))) {
@@ -1769,7 +1775,7 @@ static cudaError_t prep(K kernel, size_t smem, int threads, int* per_sm) {
 // Short search as two kernels: a gather kernel (thread per list, 16 warps per
 // SM) followed by a sweep-only kernel (register-heavy, warp per batch).
 template <int NS>
-__global__ void __launch_bounds__(128) search_gather_kernel(MergeParams mp) {
+__global__ void __launch_bounds__(128, VDI_SGATHER_MINB) search_gather_kernel(MergeParams mp) {
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t c0 = min(mp.wl_count[0], mp.wl_cap), c1 = min(mp.wl_count[1], mp.wl_cap);
   const uint32_t nb0 = (c0 + 31) / 32, nb1 = (c1 + 31) / 32;
@@ -1824,7 +1830,13 @@ static cudaError_t launch_search_ns(const MergeParams& mp, cudaStream_t st, int*
   // share of the SMs' residency, so the next VDI's pass-through can run beside them
   const float sh = mp.search_share > 0.f && mp.search_share < 1.f ? mp.search_share : 1.f;
   auto part = [&](uint32_t full) { return std::max<uint32_t>(1, (uint32_t)(full * sh)); };
-  search_gather_kernel<NS><<<part(sm_count() * 4), 128, 0, st>>>(mp);
+  static int g_per_sm = 0;  // one static per NS instantiation
+  if (!g_per_sm) {
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_per_sm, search_gather_kernel<NS>, 128, 0)) != cudaSuccess)
+      return e;
+    if (g_per_sm < 1) g_per_sm = 1;
+  }
+  search_gather_kernel<NS><<<part(sm_count() * g_per_sm), 128, 0, st>>>(mp);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   ++*launches;
   {
