@@ -789,39 +789,16 @@ __device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc) {
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
-template <int MS, int R>
-__device__ __forceinline__ void sweep_batch(const MergeParams& mp, int bucket, uint32_t batch, float4* __restrict__ sm) {
-  const int lane = threadIdx.x;
-  const int k = mp.k_out, n = mp.n_src;
-  const uint32_t total = min(mp.wl_count[bucket], mp.wl_cap);
-  const uint32_t* wl = mp.wl[bucket];
+// The sweeps of one batch whose samples are in place: rows 0..R-1 in the
+// register array S, row q >= R at sm[(q - OFF) * 32 + lane] (NaN past m).
+template <int MS, int R, int OFF>
+__device__ __forceinline__ void sweep_rows(const MergeParams& mp, uint32_t p, int mi, bool valid, bool bad,
+                                           const float4 (&S)[R], const float4* __restrict__ sm,
+                                           const float2* __restrict__ dcol) {
+  const int lane = threadIdx.x & 31;
+  const int k = mp.k_out;
+  const float qnan = __int_as_float(0x7fc00000);
   {
-    const uint32_t e = batch * 32 + lane;
-    const bool valid = e < total;
-    const uint32_t* ent = wl + (size_t)(valid ? e : 0) * (3 + n);
-    const uint32_t p = valid ? ent[0] : 0u;
-    const int mi = valid ? (int)ent[2] : 0;
-    const uint32_t slot = mp.batch_slot[bucket][batch];
-    if (slot >= mp.pool_cap) return;
-    const uint32_t* gp = mp.pool_gap + (size_t)slot * 64 + lane;
-    const uint32_t gw0 = valid ? gp[0] : 0u, gw1 = valid ? gp[32] : 0u;
-    const bool bad = valid && gw0 == 0xffffffffu && gw1 == 0xffffffffu;  // sent to the general path
-    const float4* col = mp.pool_rgba + (size_t)slot * 40 * 32 + lane;
-    const float2* dcol = mp.pool_depth + (size_t)slot * 40 * 32 + lane;
-    // samples past m are NaN: D^2 = NaN never exceeds g^2 and their gap bits
-    // are 0, so they never split and the count sweeps need no "q < m" test
-    float4 S[R];
-    const float qnan = __int_as_float(0x7fc00000);
-    const float4 nan4 = make_float4(qnan, qnan, qnan, qnan);
-    __syncwarp();  // the previous batch's reads of the shared rows are done
-#pragma unroll
-    for (int q = R; q < MS; ++q) {
-      if (q < mi && !bad) cp_async16(sm + (q - R) * 32 + lane, col + q * 32);
-      else sm[(q - R) * 32 + lane] = nan4;
-    }
-#pragma unroll
-    for (int q = 0; q < R; ++q) S[q] = (q < mi && !bad) ? col[q * 32] : nan4;
-    cp_async_wait_all();  // each lane reads only its own column: no warp barrier needed
     // memoised bisection: a count sweep at g2 takes the same decisions for
     // every g2' in [L, U), so a later midpoint inside the interval of the
     // latest sweep on either side of the bracket reuses its count; each lane
@@ -883,7 +860,7 @@ __device__ __forceinline__ void sweep_batch(const MergeParams& mp, int bucket, u
         for (int q0 = R; q0 < MS; q0 += 8) {  // the shared rows: a rolled loop of 8-step chunks (code size)
           if (!__any_sync(kFull, bs.active && q0 < mi && sc <= k)) break;
 #pragma unroll
-          for (int u = 0; u < 8; ++u) cstep(sm[(q0 - R + u) * 32 + lane], false);
+          for (int u = 0; u < 8; ++u) cstep(sm[(q0 - OFF + u) * 32 + lane], false);
         }
       }
       if (bs.active) bs.swept(sc, VDI_MEMO ? L : 1.f, VDI_MEMO ? U : 0.f, k, mp.max_iters);
@@ -931,7 +908,7 @@ __device__ __forceinline__ void sweep_batch(const MergeParams& mp, int bucket, u
           if (q0 + u < mi) dq[u] = dcol[(q0 + u) * 32];
 #pragma unroll
         for (int u = 0; u < 8; ++u)
-          if (q0 + u < mi) wstep(sm[(q0 - R + u) * 32 + lane], dq[u], q0 + u);
+          if (q0 + u < mi) wstep(sm[(q0 - OFF + u) * 32 + lane], dq[u], q0 + u);
       }
       if (mi > 0 && c <= k) {
         od[c - 1] = make_float2(tf, tb);
@@ -941,6 +918,43 @@ __device__ __forceinline__ void sweep_batch(const MergeParams& mp, int bucket, u
       if (mp.stat_gamma) mp.stat_gamma[p] = best;
     }
   }
+}
+
+// Short-list sweep of one batch of the pool (two-kernel path): samples
+// 0..R-1 into registers, R..MS-1 into the warp's shared rows (cp.async).
+template <int MS, int R>
+__device__ __forceinline__ void sweep_batch(const MergeParams& mp, int bucket, uint32_t batch, float4* __restrict__ sm) {
+  const int lane = threadIdx.x;
+  const int n = mp.n_src;
+  const uint32_t total = min(mp.wl_count[bucket], mp.wl_cap);
+  const uint32_t* wl = mp.wl[bucket];
+  const uint32_t e = batch * 32 + lane;
+  const bool valid = e < total;
+  const uint32_t* ent = wl + (size_t)(valid ? e : 0) * (3 + n);
+  const uint32_t p = valid ? ent[0] : 0u;
+  const int mi = valid ? (int)ent[2] : 0;
+  const uint32_t slot = mp.batch_slot[bucket][batch];
+  if (slot >= mp.pool_cap) return;
+  const uint32_t* gp = mp.pool_gap + (size_t)slot * 64 + lane;
+  const uint32_t gw0 = valid ? gp[0] : 0u, gw1 = valid ? gp[32] : 0u;
+  const bool bad = valid && gw0 == 0xffffffffu && gw1 == 0xffffffffu;  // sent to the general path
+  const float4* col = mp.pool_rgba + (size_t)slot * 40 * 32 + lane;
+  const float2* dcol = mp.pool_depth + (size_t)slot * 40 * 32 + lane;
+  // samples past m are NaN: D^2 = NaN never exceeds g^2 and their gap bits
+  // are 0, so they never split and the count sweeps need no "q < m" test
+  float4 S[R];
+  const float qnan = __int_as_float(0x7fc00000);
+  const float4 nan4 = make_float4(qnan, qnan, qnan, qnan);
+  __syncwarp();  // the previous batch's reads of the shared rows are done
+#pragma unroll
+  for (int q = R; q < MS; ++q) {
+    if (q < mi && !bad) cp_async16(sm + (q - R) * 32 + lane, col + q * 32);
+    else sm[(q - R) * 32 + lane] = nan4;
+  }
+#pragma unroll
+  for (int q = 0; q < R; ++q) S[q] = (q < mi && !bad) ? col[q * 32] : nan4;
+  cp_async_wait_all();  // each lane reads only its own column: no warp barrier needed
+  sweep_rows<MS, R, R>(mp, p, mi, valid, bad, S, sm, dcol);
 }
 
 #ifndef VDI_SWEEP_MINB
