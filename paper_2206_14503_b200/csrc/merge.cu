@@ -773,6 +773,9 @@ __device__ __forceinline__ void gather_short_batch(const MergeParams& mp, uint32
 // register samples, 16 at 16); the shared rows are swept by a rolled loop of
 // 8-step chunks, which keeps the kernel's code (and instruction-cache misses)
 // small.
+#ifndef VDI_UB_EXIT
+#define VDI_UB_EXIT 1  // count sweeps also stop once the count can no longer reach k
+#endif
 #ifndef VDI_MEMO_CHEAP
 #define VDI_MEMO_CHEAP 1  // interval bookkeeping with one select per comparison
 #endif
@@ -846,11 +849,17 @@ __device__ __forceinline__ void sweep_rows(const MergeParams& mp, uint32_t p, in
         aa = st ? sa : fmaf(tr, sa, aa);
         sc += st ? 1 : 0;
       };
+      // a lane still needs samples while its count can still reach k: past
+      // k the sweep's answer is "> k"; with sc + (samples left) < k it is
+      // "< k" (each sample opens at most one segment) -- both decide the level
+      auto needs = [&](int q) { return bs.active && q < mi && sc <= k && sc + (mi - q) >= k; };
       bool more = true;
+      int qe = MS;  // samples swept
 #pragma unroll
       for (int q = 0; q < R; ++q) {  // the register samples: static indices
-        if ((q & 7) == 0 && q > 0 && !__any_sync(kFull, bs.active && q < mi && sc <= k)) {
+        if ((q & 7) == 0 && q > 0 && !__any_sync(kFull, VDI_UB_EXIT ? needs(q) : (bs.active && q < mi && sc <= k))) {
           more = false;
+          qe = q;
           break;
         }
         cstep(S[q], q == 0);
@@ -858,12 +867,18 @@ __device__ __forceinline__ void sweep_rows(const MergeParams& mp, uint32_t p, in
       if (more) {
 #pragma unroll 1
         for (int q0 = R; q0 < MS; q0 += 8) {  // the shared rows: a rolled loop of 8-step chunks (code size)
-          if (!__any_sync(kFull, bs.active && q0 < mi && sc <= k)) break;
+          if (!__any_sync(kFull, VDI_UB_EXIT ? needs(q0) : (bs.active && q0 < mi && sc <= k))) {
+            qe = q0;
+            break;
+          }
 #pragma unroll
           for (int u = 0; u < 8; ++u) cstep(sm[(q0 - OFF + u) * 32 + lane], false);
         }
       }
-      if (bs.active) bs.swept(sc, VDI_MEMO ? L : 1.f, VDI_MEMO ? U : 0.f, k, mp.max_iters);
+      // an unfinished sweep below k records its bound sc + (samples left) < k
+      // (<= k and != k: the same decision as the exact count)
+      const int cr = (qe < mi && sc <= k) ? sc + (mi - qe) : sc;
+      if (bs.active) bs.swept(cr, VDI_MEMO ? L : 1.f, VDI_MEMO ? U : 0.f, k, mp.max_iters);
     }
     const float best = bs.best;
     if (valid && !bad) {  // final write sweep
@@ -1238,27 +1253,28 @@ __device__ __forceinline__ int long_count_sync(const float4* __restrict__ col, i
     B[u] = slot_ld(col + (8 + u) * 32);
   }
   const float4* pp = col + 16 * 32;
-  for (int q0 = 0;;) {
+  int q0 = 0;
+  for (;;) {
 #pragma unroll
     for (int u = 0; u < 8; ++u) C[u] = slot_ld(pp + u * 32);
     pp += 8 * 32;
     long_step8(A, q0, m, g2, ar, ag, ab, aa, sc, L, U);
     q0 += 8;
-    if (!__any_sync(kFull, act && q0 < m && sc <= k)) break;
+    if (!__any_sync(kFull, act && q0 < m && sc <= k && (!VDI_UB_EXIT || sc + (m - q0) >= k))) break;
 #pragma unroll
     for (int u = 0; u < 8; ++u) A[u] = slot_ld(pp + u * 32);
     pp += 8 * 32;
     long_step8(B, q0, m, g2, ar, ag, ab, aa, sc, L, U);
     q0 += 8;
-    if (!__any_sync(kFull, act && q0 < m && sc <= k)) break;
+    if (!__any_sync(kFull, act && q0 < m && sc <= k && (!VDI_UB_EXIT || sc + (m - q0) >= k))) break;
 #pragma unroll
     for (int u = 0; u < 8; ++u) B[u] = slot_ld(pp + u * 32);
     pp += 8 * 32;
     long_step8(C, q0, m, g2, ar, ag, ab, aa, sc, L, U);
     q0 += 8;
-    if (!__any_sync(kFull, act && q0 < m && sc <= k)) break;
+    if (!__any_sync(kFull, act && q0 < m && sc <= k && (!VDI_UB_EXIT || sc + (m - q0) >= k))) break;
   }
-  return sc;
+  return (q0 < m && sc <= k) ? sc + (m - q0) : sc;  // unfinished below k: the bound (< k), see sweep_rows
 }
 
 // The final write sweep over a pool column (same decisions and output as
