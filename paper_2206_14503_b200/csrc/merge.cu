@@ -1212,27 +1212,28 @@ __device__ __forceinline__ int long_count(const float4* __restrict__ col, int m,
     B[u] = slot_ld(col + (8 + u) * 32);
   }
   const float4* pp = col + 16 * 32;
-  for (int q0 = 0;;) {
+  int q0 = 0;
+  for (;;) {
 #pragma unroll
     for (int u = 0; u < 8; ++u) C[u] = slot_ld(pp + u * 32);
     pp += 8 * 32;
     long_step8(A, q0, m, g2, ar, ag, ab, aa, sc, L, U);
     q0 += 8;
-    if (q0 >= m || sc > k) break;
+    if (q0 >= m || sc > k || (VDI_UB_EXIT && sc + (m - q0) < k)) break;
 #pragma unroll
     for (int u = 0; u < 8; ++u) A[u] = slot_ld(pp + u * 32);
     pp += 8 * 32;
     long_step8(B, q0, m, g2, ar, ag, ab, aa, sc, L, U);
     q0 += 8;
-    if (q0 >= m || sc > k) break;
+    if (q0 >= m || sc > k || (VDI_UB_EXIT && sc + (m - q0) < k)) break;
 #pragma unroll
     for (int u = 0; u < 8; ++u) B[u] = slot_ld(pp + u * 32);
     pp += 8 * 32;
     long_step8(C, q0, m, g2, ar, ag, ab, aa, sc, L, U);
     q0 += 8;
-    if (q0 >= m || sc > k) break;
+    if (q0 >= m || sc > k || (VDI_UB_EXIT && sc + (m - q0) < k)) break;
   }
-  return sc;
+  return (q0 < m && sc <= k) ? sc + (m - q0) : sc;  // unfinished below k: the bound (< k), see sweep_rows
 }
 
 // long_count with the warp in lock step: every lane sweeps the same rows at
