@@ -133,6 +133,70 @@ def bisect(S, m, k, iters=16, gamma_max=2.0):
     return best
 
 
+def prefix_counts(S, m, gamma):
+    """Segments opened after each prefix of samples (the sweep of `sweep`,
+    no early exit): P[r, q] for q = 0..M."""
+    R, M, _ = S.shape
+    g2 = (gamma * gamma).astype(F32)
+    cnt = np.zeros(R, np.int64)
+    opn = np.zeros(R, bool)
+    acc = [np.zeros(R, F32) for _ in range(4)]
+    prev = np.zeros(R, F32)
+    zero = [np.zeros(R, F32)] * 4
+    P = np.zeros((R, M + 1), np.int64)
+    for i in range(M):
+        live = i < m
+        s = [S[:, i, 2 + c] for c in range(4)]
+        gap = live & opn & (S[:, i, 0] > prev)
+        opn = opn & ~(gap & (dist2(acc, zero) > g2))
+        split = live & opn & (dist2(acc, s) > g2)
+        start = live & (~opn | split)
+        merge = live & opn & ~split
+        cnt = cnt + start
+        tr = (F32(1.0) - acc[3]).astype(F32)
+        for c in range(4):
+            acc[c] = np.where(start, s[c], np.where(merge, fma32(tr, s[c], acc[c]), acc[c])).astype(F32)
+        opn = opn | start
+        prev = np.where(live, S[:, i, 1], prev)
+        P[:, i + 1] = cnt
+    return P
+
+
+def bisect_ub(S, m, k, every=8, iters=16, gamma_max=2.0):
+    """The bisection with the GPU sweeps' early exits (merge.cu, sweep_rows):
+    checked every `every` samples, a count sweep stops at count > k (answer
+    "> k") or once count + samples left < k, recording that bound as its
+    count.  Each sample opens at most one segment, so the bound is >= the full
+    count; below k it decides the level as the full count does (<= k, != k).
+    Returns gamma per ray."""
+    R, M, _ = S.shape
+    lo = np.zeros(R, F32)
+    hi = np.full(R, F32(gamma_max))
+    best = np.full(R, F32(gamma_max))
+    act = m > k
+    rows = np.arange(R)
+    for _ in range(iters):
+        if not act.any():
+            break
+        mid = (F32(0.5) * (lo + hi).astype(F32)).astype(F32)
+        P = prefix_counts(S, np.where(act, m, 0), mid)
+        c = P[rows, m].copy()                      # the full count
+        decided = np.zeros(R, bool)
+        for q in range(every, M + 1, every):       # the check points, in order
+            cq = P[:, q]
+            live = act & ~decided & (q < m)
+            over = live & (cq > k)
+            under = live & ~over & (cq + (m - q) < k)
+            c = np.where(over, cq, np.where(under, cq + (m - q), c))
+            decided |= over | under
+        feas = act & (c <= k)
+        best = np.where(feas, mid, best)
+        hi = np.where(feas, mid, hi)
+        lo = np.where(act & ~feas, mid, lo)
+        act = act & ~(feas & (c == k))
+    return best
+
+
 def depth_order(lists):
     """PAPER.md:168 (the lowest starting depth next; Q11 ties by PE id, then
     index) and Q23 (alpha == 0 dropped): one ray's lists -> its samples."""
@@ -255,3 +319,24 @@ def test_fma32_exact():
             if best is None or d < best[0] or (d == best[0] and even):
                 best = (d, v)
         assert r[i] == best[1], (a[i], b[i], c[i], r[i], best[1])
+
+
+@pytest.mark.parametrize("every", [1, 8])
+def test_upper_bound_exit_keeps_gamma(every):
+    """The GPU count sweeps' early exit at count + samples left < k_out
+    (merge.cu sweep_rows / long_count_sync) reaches the same gamma* as the
+    plain procedure, on random rays of every kind and several k_out."""
+    rng = np.random.default_rng(77 + every)
+    for kind in ("plain", "gappy", "dyadic"):
+        rays = [random_ray(rng, kind) for _ in range(800)]
+        samples = [depth_order(l) for l in rays]
+        m = np.array([len(x) for x in samples], np.int64)
+        S = np.zeros((len(samples), max(1, int(m.max())), 6), F32)
+        for r, x in enumerate(samples):
+            S[r, :len(x)] = x
+        for k in (1, 3, 8, 20):
+            g0 = bisect(S, m, k)
+            g1 = bisect_ub(S, m, k, every=every)
+            sel = m > k
+            assert sel.any()
+            assert np.array_equal(g0[sel], g1[sel]), (kind, k, np.nonzero(g0[sel] != g1[sel])[0][:5])
