@@ -197,6 +197,90 @@ def bisect_ub(S, m, k, every=8, iters=16, gamma_max=2.0):
     return best
 
 
+def sweep_interval(S, m, gamma, k):
+    """A count sweep (early exit at count > k) that also returns the interval
+    [L, U) of g^2 over which every comparison it made decides the same way:
+    L = the largest compared value that merged (<= g^2), U = the smallest
+    that split (> g^2); a gap's ||acc||^2 counts as a comparison, and D^2 is
+    not compared after a gap closed the segment (Q8)."""
+    R, M, _ = S.shape
+    g2 = (gamma * gamma).astype(F32)
+    cnt = np.zeros(R, np.int64)
+    opn = np.zeros(R, bool)
+    done = np.zeros(R, bool)
+    acc = [np.zeros(R, F32) for _ in range(4)]
+    prev = np.zeros(R, F32)
+    zero = [np.zeros(R, F32)] * 4
+    L = np.full(R, -1.0)
+    U = np.full(R, np.inf)
+    for i in range(M):
+        live = (i < m) & ~done
+        if not live.any():
+            break
+        s = [S[:, i, 2 + c] for c in range(4)]
+        gap = live & opn & (S[:, i, 0] > prev)
+        n2 = dist2(acc, zero)
+        gcl = gap & (n2 > g2)
+        U = np.where(gcl, np.minimum(U, n2), U)
+        L = np.where(gap & ~gcl, np.maximum(L, n2), L)
+        opn = opn & ~gcl
+        cmp = live & opn
+        d2 = dist2(acc, s)
+        split = cmp & (d2 > g2)
+        U = np.where(split, np.minimum(U, d2), U)
+        L = np.where(cmp & ~split, np.maximum(L, d2), L)
+        start = live & (~opn | split)
+        merge = live & opn & ~split
+        cnt = cnt + start
+        done = done | (cnt > k)
+        tr = (F32(1.0) - acc[3]).astype(F32)
+        for c in range(4):
+            acc[c] = np.where(start, s[c], np.where(merge, fma32(tr, s[c], acc[c]), acc[c])).astype(F32)
+        opn = opn | start
+        prev = np.where(live, S[:, i, 1], prev)
+    return cnt, L, U
+
+
+def bisect_memo(S, m, k, iters=16, gamma_max=2.0):
+    """The GPU's memoised bisection (merge.cu, struct Bisection): a level whose
+    midpoint^2 lies in the interval of the latest sweep on the feasible (<= k)
+    or infeasible (> k) side takes that sweep's answer without sweeping.
+    Returns (gamma per ray, sweeps made, levels evaluated = the plain
+    procedure's sweeps)."""
+    R = S.shape[0]
+    lo = np.zeros(R, F32)
+    hi = np.full(R, F32(gamma_max))
+    best = np.full(R, F32(gamma_max))
+    hL, hU, hc = np.ones(R), np.zeros(R), np.zeros(R, np.int64)
+    lL, lU = np.ones(R), np.zeros(R)
+    act = m > k
+    sweeps = levels = 0
+    for _ in range(iters):
+        if not act.any():
+            break
+        levels += int(act.sum())
+        mid = (F32(0.5) * (lo + hi).astype(F32)).astype(F32)
+        g2 = (mid * mid).astype(F32).astype(np.float64)
+        in_h = act & (g2 >= hL) & (g2 < hU)
+        in_l = act & ~in_h & (g2 >= lL) & (g2 < lU)
+        need = act & ~in_h & ~in_l
+        c = np.where(in_h, hc, k + 1)
+        if need.any():
+            cs, L, U = sweep_interval(S, np.where(need, m, 0), mid, k)
+            sweeps += int(need.sum())
+            c = np.where(need, cs, c)
+            fe = need & (cs <= k)
+            hL, hU, hc = np.where(fe, L, hL), np.where(fe, U, hU), np.where(fe, cs, hc)
+            inf_ = need & (cs > k)
+            lL, lU = np.where(inf_, L, lL), np.where(inf_, U, lU)
+        feas = act & (c <= k)
+        best = np.where(feas, mid, best)
+        hi = np.where(feas, mid, hi)
+        lo = np.where(act & ~feas, mid, lo)
+        act = act & ~(feas & (c == k))
+    return best, sweeps, levels
+
+
 def depth_order(lists):
     """PAPER.md:168 (the lowest starting depth next; Q11 ties by PE id, then
     index) and Q23 (alpha == 0 dropped): one ray's lists -> its samples."""
@@ -340,3 +424,26 @@ def test_upper_bound_exit_keeps_gamma(every):
             sel = m > k
             assert sel.any()
             assert np.array_equal(g0[sel], g1[sel]), (kind, k, np.nonzero(g0[sel] != g1[sel])[0][:5])
+
+
+def test_memoised_bisection_keeps_gamma():
+    """The GPU's memoised bisection (a midpoint inside the validity interval of
+    the latest sweep on either side of the bracket reuses that sweep's count)
+    reaches the plain procedure's gamma* on random rays, and skips sweeps."""
+    rng = np.random.default_rng(91)
+    swept = evaluated = 0
+    for kind in ("plain", "gappy", "dyadic"):
+        rays = [random_ray(rng, kind) for _ in range(800)]
+        samples = [depth_order(l) for l in rays]
+        m = np.array([len(x) for x in samples], np.int64)
+        S = np.zeros((len(samples), max(1, int(m.max())), 6), F32)
+        for r, x in enumerate(samples):
+            S[r, :len(x)] = x
+        for k in (1, 3, 8, 20):
+            sel = m > k
+            g0 = bisect(S, m, k)
+            g1, sweeps, levels = bisect_memo(S, m, k)
+            assert np.array_equal(g0[sel], g1[sel]), (kind, k, np.nonzero(g0[sel] != g1[sel])[0][:5])
+            swept += sweeps
+            evaluated += levels
+    assert swept < 0.95 * evaluated, (swept, evaluated)  # the memo does resolve levels
