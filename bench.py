@@ -470,29 +470,6 @@ def _run_ours(args, world, rank, local, clk):
             torch.cuda.synchronize()
             xs[-1]["ms"] = e0.elapsed_time(e1)
         xm = allreduce_max(statistics.mean(x["ms"] for x in xs), G)
-        # secondary: replicas -- every GPU composites whole VDIs of its own (all
-        # n sub-VDIs resident on each GPU, no strips, no exchange, no gather)
-        comp1 = vdi.Compositor(W, H, cfg.k_in, k, n, stream=stream)
-        allpes = [comp1.generate_subvdi(vol, tft, synth.make_camera(W, H, view=0), dec, pe) for pe in range(n)]
-        ims1 = [vdi.FullVDI.empty(W, 0, H, k) for _ in range(F)]
-        for _ in range(3):
-            comp1.composite_frames([allpes] * F, ims1)
-        K2 = max(10, args.steps // 4)
-        r_evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K2)]
-        torch.cuda.synchronize()
-        barrier(G)
-        for i in range(K2):
-            flush.zero_()
-            r_evs[i][0].record(stream)
-            comp1.composite_frames([allpes] * F, ims1)
-            r_evs[i][1].record(stream)
-        torch.cuda.synchronize()
-        barrier(G)
-        rep_tot = allreduce_max(sum(a_.elapsed_time(b_) for a_, b_ in r_evs), G)
-        replicas = {"vdis_per_s": G * F * K2 / (rep_tot / 1e3), "ms_per_vdi_per_gpu": rep_tot / (K2 * F), "steps": K2,
-                    "note": "secondary (not the paper's split): every GPU composites whole VDIs of its own, all n "
-                            "sub-VDIs resident on each GPU, no exchange or gather; view V0"}
-        del comp1, allpes, ims1
         full_rep = {"ms_per_vdi": xm, "value": 1e3 / xm, "steps": Kx,
                     "stages_ms": {s_: statistics.mean(c_[f"ms_{s_}"] for c_ in xs) for s_ in ("exchange", "merge", "gather")},
                     "exchange_bytes_sent_rank0": xs[-1]["bytes_sent"],
@@ -500,6 +477,34 @@ def _run_ours(args, world, rank, local, clk):
                             "(Fig. 6 'full'); one VDI per step"}
         compx.close()
         del fulls
+    # secondary: replicas -- every GPU composites whole VDIs of its own (all
+    # n sub-VDIs resident on each GPU, no strips, no exchange, no gather);
+    # skipped for 4K images (a second context's scratch beside the strip
+    # context's would not fit next to the frame images)
+    if G > 1 and img_bytes <= (2 << 30):
+        comp1 = vdi.Compositor(W, H, cfg.k_in, k, n, stream=stream)
+        allpes = [comp1.generate_subvdi(vol, tft, synth.make_camera(W, H, view=0), dec, pe) for pe in range(n)]
+        F1 = max(1, min(F, 8, int((24 << 30) // img_bytes)))  # the root reuses its frame images; the others allocate F1
+        ims1 = frame_images[:F1] if frame_images is not None else [vdi.FullVDI.empty(W, 0, H, k) for _ in range(F1)]
+        for _ in range(3):
+            comp1.composite_frames([allpes] * F1, ims1)
+        K2 = max(10, args.steps // 4)
+        r_evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K2)]
+        torch.cuda.synchronize()
+        barrier(G)
+        for i in range(K2):
+            flush.zero_()
+            r_evs[i][0].record(stream)
+            comp1.composite_frames([allpes] * F1, ims1)
+            r_evs[i][1].record(stream)
+        torch.cuda.synchronize()
+        barrier(G)
+        rep_tot = allreduce_max(sum(a_.elapsed_time(b_) for a_, b_ in r_evs), G)
+        replicas = {"vdis_per_s": G * F1 * K2 / (rep_tot / 1e3), "ms_per_vdi_per_gpu": rep_tot / (K2 * F1), "steps": K2,
+                    "frames_per_step": F1,
+                    "note": "secondary (not the paper's split): every GPU composites whole VDIs of its own, all n "
+                            "sub-VDIs resident on each GPU, no exchange or gather; view V0"}
+        del comp1, allpes, ims1
 
     # ---- rooflines.  Headline: the whole merge stage (every
     # merge kernel, one stream) against HBM; beside it the pass-through kernel

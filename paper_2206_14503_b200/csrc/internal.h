@@ -99,7 +99,7 @@ struct MergeParams {
   uint32_t pool_cap;
   uint32_t* batch_slot[2];
   // long-list search (buckets 2, 3): long_warps warp-private slots of long_slot
-  // bytes, each [long_maxm + 32][32] rgba then [long_maxm][32] depth
+  // bytes, each [long_maxm + 32][32] rgba then [long_maxm + 32][32] depth (32 rows of read slack)
   char* long_pool;
   size_t long_slot;
   uint32_t long_maxm;

@@ -1885,10 +1885,11 @@ static cudaError_t launch_search_ns(const MergeParams& mp, cudaStream_t st, int*
 }
 
 uint32_t long_warps(uint32_t m_max, size_t* slot_bytes) {
-  // warp-private slots of min(m_max, 1024) rows (+32 rows of read slack); at
-  // most VDI_LONG_WPS warps per SM and ~1 GB of slots
+  // warp-private slots of min(m_max, 1024) rows (+32 rows of read slack in
+  // both columns: the count and write sweeps load up to 24 / 16 rows ahead);
+  // at most VDI_LONG_WPS warps per SM and ~1 GB of slots
   const uint32_t rows = std::min<uint32_t>(std::max<uint32_t>(m_max, 41), 1024);
-  *slot_bytes = ((size_t)(rows + 32) * 32 * 16 + (size_t)rows * 32 * 8 + 255) & ~(size_t)255;
+  *slot_bytes = ((size_t)(rows + 32) * 32 * 16 + (size_t)(rows + 32) * 32 * 8 + 255) & ~(size_t)255;
   const uint64_t fit = (1ull << 30) / *slot_bytes;
   return (uint32_t)std::max<uint64_t>(148, std::min<uint64_t>(fit, (uint64_t)sm_count() * VDI_LONG_WPS));
 }

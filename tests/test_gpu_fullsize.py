@@ -16,7 +16,7 @@ from parity import compare
 
 pytestmark = pytest.mark.gpu
 
-CONFIGS = [("C2", 0), ("C3", 0), ("C4", 0), ("C5", 0), ("C5", 16)]  # C5 strong-scaling sweep: up to 16 PEs (m <= 512)
+CONFIGS = [("C2", 0), ("C3", 0), ("C4", 0), ("C5", 0), ("C5", 16), ("C5", 2)]  # C5 strong-scaling sweep: 2 to 16 PEs (m <= 64 ... 512)
 
 
 @pytest.fixture(scope="module")
