@@ -27,9 +27,20 @@
 #include <tuple>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "comm.h"
 #include "internal.h"
 #include "render.h"
+
+namespace {
+// NVTX range over one public call (profiler timelines; ncu --nvtx filters by it)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+}  // namespace
+#define VDI_NVTX(name) NvtxRange vdi_nvtx_range_(name)
 
 using namespace vdi;
 
@@ -929,11 +940,13 @@ static vdi_status generate(vdi_ctx* ctx, const vdi_volume_desc* vol, const vdi_t
 vdi_status vdi_generate_subvdi(vdi_ctx* ctx, const vdi_volume_desc* vol, const vdi_tf_desc* tf,
                                const vdi_camera* cam, const vdi_decomp_desc* dec, uint32_t pe_id,
                                vdi_dense_view* out) {
+  VDI_NVTX("vdi_generate_subvdi");
   return generate(ctx, vol, tf, cam, dec, pe_id, out, false);
 }
 
 vdi_status vdi_generate_limit(vdi_ctx* ctx, const vdi_volume_desc* vol, const vdi_tf_desc* tf, const vdi_camera* cam,
                               const vdi_decomp_desc* dec, uint32_t pe_id, vdi_dense_view* out) {
+  VDI_NVTX("vdi_generate_limit");
   return generate(ctx, vol, tf, cam, dec, pe_id, out, true);
 }
 
@@ -1231,6 +1244,7 @@ static vdi_status release_slots(vdi_ctx* ctx, int& launches, cudaStream_t st = n
 }
 
 vdi_status vdi_composite(vdi_ctx* ctx, const vdi_dense_view* local, uint32_t n_local, vdi_full_view* so) {
+  VDI_NVTX("vdi_composite");
   if (vdi_status s = check_ctx(ctx)) return s;
   const vdi_config& cf = ctx->cfg;
   const uint32_t G = cf.n_ranks, n = cf.n_pes, k = cf.k_out;
@@ -1312,6 +1326,7 @@ vdi_status vdi_composite(vdi_ctx* ctx, const vdi_dense_view* local, uint32_t n_l
 }
 
 vdi_status vdi_dense_to_full(vdi_ctx* ctx, const vdi_dense_view* in, vdi_full_view* out) {
+  VDI_NVTX("vdi_dense_to_full");
   if (vdi_status s = check_ctx(ctx)) return s;
   const vdi_config& cf = ctx->cfg;
   if (!in || !out || !in->count || (in->total && (!in->depth || !in->rgba)))
@@ -1339,6 +1354,7 @@ vdi_status vdi_dense_to_full(vdi_ctx* ctx, const vdi_dense_view* in, vdi_full_vi
 
 vdi_status vdi_composite_fullrep(vdi_ctx* ctx, const vdi_full_view* local, const uint32_t* pe_ids, uint32_t n_local,
                                  vdi_full_view* so) {
+  VDI_NVTX("vdi_composite_fullrep");
   if (vdi_status s = check_ctx(ctx)) return s;
   const vdi_config& cf = ctx->cfg;
   const uint32_t G = cf.n_ranks, me = cf.rank, n = cf.n_pes, K = cf.k_in;
@@ -1573,11 +1589,13 @@ static vdi_status gather_to(vdi_ctx* ctx, const vdi_full_view* strip, vdi_full_v
 }
 
 vdi_status vdi_gather(vdi_ctx* ctx, const vdi_full_view* strip, vdi_full_view* image) {
+  VDI_NVTX("vdi_gather");
   if (vdi_status s = check_ctx(ctx)) return s;
   return gather_to(ctx, strip, image, ctx->cfg.root);
 }
 
 vdi_status vdi_gather_root(vdi_ctx* ctx, uint32_t root, const vdi_full_view* strip, vdi_full_view* image) {
+  VDI_NVTX("vdi_gather_root");
   return gather_to(ctx, strip, image, root);
 }
 
@@ -1589,6 +1607,7 @@ vdi_status vdi_gather_root(vdi_ctx* ctx, uint32_t root, const vdi_full_view* str
 // it pushes right after its merge).  Non-root strips: four ctx-owned buffers, each compacted to the root on its own stream.
 vdi_status vdi_composite_frames(vdi_ctx* ctx, uint32_t F, const vdi_dense_view* local, uint32_t n_local,
                                 vdi_full_view* images, const uint32_t* roots) {
+  VDI_NVTX("vdi_composite_frames");
   if (vdi_status s = check_ctx(ctx)) return s;
   const vdi_config& cf = ctx->cfg;
   const uint32_t G = cf.n_ranks, me = cf.rank, W = cf.width, H = cf.height, k = cf.k_out;
@@ -1777,6 +1796,7 @@ static vdi_status upload_host_pes(vdi_ctx* ctx, const vdi_dense_view* local, uin
 }
 
 vdi_status vdi_composite_host(vdi_ctx* ctx, const vdi_dense_view* local, uint32_t n_local, vdi_full_view* so) {
+  VDI_NVTX("vdi_composite_host");
   if (vdi_status s = check_ctx(ctx)) return s;
   const vdi_config& cf = ctx->cfg;
   if (!so || !so->count || !so->depth || !so->rgba) return fail(VDI_ERR_INVALID_ARG, "strip_out is NULL");
@@ -1827,6 +1847,7 @@ static vdi_status compact_strip(vdi_ctx* ctx, const vdi_full_view& ds, unsigned 
 
 vdi_status vdi_composite_host_dense(vdi_ctx* ctx, const vdi_dense_view* local, uint32_t n_local,
                                     vdi_dense_strip* out) {
+  VDI_NVTX("vdi_composite_host_dense");
   if (vdi_status s = check_ctx(ctx)) return s;
   const vdi_config& cf = ctx->cfg;
   if (!out || !out->count || (out->capacity && (!out->depth || !out->rgba)))
@@ -1880,6 +1901,7 @@ vdi_status vdi_composite_host_dense(vdi_ctx* ctx, const vdi_dense_view* local, u
 // is exactly one vdi_composite + dense compaction, as in the single call.
 vdi_status vdi_composite_host_dense_frames(vdi_ctx* ctx, uint32_t F, const vdi_dense_view* local, uint32_t n_local,
                                            vdi_dense_strip* outs) {
+  VDI_NVTX("vdi_composite_host_dense_frames");
   if (vdi_status s = check_ctx(ctx)) return s;
   const vdi_config& cf = ctx->cfg;
   if (F == 0) return VDI_OK;
@@ -1989,6 +2011,7 @@ vdi_status vdi_composite_host_dense_frames(vdi_ctx* ctx, uint32_t F, const vdi_d
 // The limit case and the renderers
 // ---------------------------------------------------------------------------
 vdi_status vdi_composite_image(vdi_ctx* ctx, const vdi_dense_view* local, uint32_t n_local, float* strip_rgba) {
+  VDI_NVTX("vdi_composite_image");
   if (vdi_status s = check_ctx(ctx)) return s;
   const vdi_config& cf = ctx->cfg;
   const uint32_t G = cf.n_ranks, n = cf.n_pes;
@@ -2032,6 +2055,7 @@ vdi_status vdi_composite_image(vdi_ctx* ctx, const vdi_dense_view* local, uint32
 }
 
 vdi_status vdi_gather_image(vdi_ctx* ctx, const float* strip_rgba, float* image_rgba) {
+  VDI_NVTX("vdi_gather_image");
   if (vdi_status s = check_ctx(ctx)) return s;
   const vdi_config& cf = ctx->cfg;
   const Layout& L = ctx->lay;
@@ -2084,6 +2108,7 @@ vdi_status vdi_gather_image(vdi_ctx* ctx, const float* strip_rgba, float* image_
 }
 
 vdi_status vdi_render_generation_view(vdi_ctx* ctx, const vdi_full_view* vdi, float* out_rgba) {
+  VDI_NVTX("vdi_render_generation_view");
   if (vdi_status s = check_ctx(ctx)) return s;
   if (!vdi || !vdi->count || !vdi->rgba || !out_rgba || vdi->row_end < vdi->row_begin)
     return fail(VDI_ERR_INVALID_ARG, "vdi / out_rgba is NULL");
@@ -2111,6 +2136,7 @@ static CamF camf(const vdi_camera& c) {
 vdi_status vdi_render_novel_view(vdi_ctx* ctx, const vdi_full_view* vdi, const vdi_camera* gen_cam,
                                  const vdi_camera* view_cam, const uint32_t dims[3], uint32_t w_out, uint32_t h_out,
                                  float* out_rgba) {
+  VDI_NVTX("vdi_render_novel_view");
   if (vdi_status s = check_ctx(ctx)) return s;
   const vdi_config& cf = ctx->cfg;
   if (!vdi || !vdi->count || !vdi->depth || !vdi->rgba || !gen_cam || !view_cam || !dims || !out_rgba)
@@ -2140,6 +2166,7 @@ vdi_status vdi_render_novel_view(vdi_ctx* ctx, const vdi_full_view* vdi, const v
 
 vdi_status vdi_render_dvr(vdi_ctx* ctx, const vdi_volume_desc* vol, const vdi_tf_desc* tf, const vdi_camera* cam,
                           uint32_t w_out, uint32_t h_out, float* out_rgba) {
+  VDI_NVTX("vdi_render_dvr");
   if (vdi_status s = check_ctx(ctx)) return s;
   if (!vol || !tf || !cam || !out_rgba || !vol->voxels || !tf->table) return fail(VDI_ERR_INVALID_ARG, "NULL argument");
   if (vol->bytes_per_voxel != 1 && vol->bytes_per_voxel != 2)
