@@ -5,19 +5,27 @@
 //                             count slice at 32-list granularity (PAPER.md:166
 //                             ships prefix chunks; we re-derive them, Q17);
 //   merge_fast              : one warp per 32 consecutive lists, lane = list.
-//                             Lists with m <= k_out are loaded into a packed
-//                             shared-memory staging buffer, depth-ordered by a
-//                             run-based k-way merge of the per-PE sorted runs
-//                              and written verbatim (Q9); all 32
-//                             lists' full representation (zeros
-//                             in unused slots) leaves with fully coalesced
-//                             streaming stores.  Lists with m > k_out go to a
-//                             search work list, bucketed by m;
-//   search_gather/sweep     : lists with k_out < m <= 40: depth order into a
-//                             pool slot ([sample][lane]), then a warp per 32
-//                             lists sweeps register-resident samples through
-//                             the gamma bisection;
-//   long_gather/long_sweep  : lists with m > 40, the same from a byte pool;
+//                             Lists with m <= k_out are copied (LDGSTS) into
+//                             their slots of a shared-memory image of the
+//                             output, depth-ordered there by a run-based k-way
+//                             merge of the per-PE sorted runs
+//                             and written verbatim (Q9); the 32 lists' full
+//                             representation (zeros in unused
+//                             slots) leaves with two TMA bulk stores.  Lists
+//                             with m > k_out go to a search work list,
+//                             bucketed by m;
+//   search_gather           : lists with k_out < m <= 40, thread per list: the
+//                             run-based merge with the run heads in registers,
+//                             samples in depth order to a pool slot
+//                             ([sample][lane], gap flag in the sign of alpha);
+//   search_sweep            : warp per 32 of them: samples 0..15 in registers,
+//                             16..39 in shared rows; memoised gamma bisection
+//                              with count sweeps that
+//                             stop once the answer is decided; final sweep;
+//   long_search             : m > 40: gather + bisection + final sweep in one
+//                             kernel from warp-private L2-resident slots (lane
+//                             per list), or warp per list with five bisection
+//                             levels per sweep when there are few long lists;
 //   merge_general           : thread per list for overlapping records
 //                             (subdivision, Eq. 2 generalised, Q12), alpha==0
 //                             records (Q23) and lists whose pool slot could not
@@ -26,13 +34,11 @@
 // order DESIGN.md §2 fixes; the TU is compiled with -fmad=false so no other
 // contraction happens.
 #include <algorithm>
-#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <math_constants.h>
 
 #include "internal.h"
 
-namespace cg = cooperative_groups;
 
 namespace vdi {
 
