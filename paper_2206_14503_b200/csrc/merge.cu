@@ -39,7 +39,6 @@
 
 #include "internal.h"
 
-
 namespace vdi {
 
 static constexpr int kFastThreads = 32;  // 1 warp per block: 13 resident per SM at k = 20 (smem-bound)
@@ -694,18 +693,17 @@ __global__ void __launch_bounds__(kFastThreads) merge_fast_kernel(MergeParams mp
 
 // ---------------------------------------------------------------------------
 // Search path for short lists (m <= 40), in two kernels:
-//   search_gather : thread per list (high occupancy hides the latency): the
+//   search_gather : thread per list (16 warps per SM hide the latency): the
 //                   run-based k-way merge over the per-PE runs,
-//                   then the samples are written in depth order to a scratch
-//                   in [batch][sample][lane] layout, plus the gap bits;
+//                   the samples written in depth order to a pool slot in
+//                   [batch][sample][lane] layout, the gap flag in alpha's sign;
 //                   transparent / overlapping records -> general path;
-//   search_sweep  : warp per batch of 32 lists: one coalesced, independent
-//                   load of each lane's samples into a statically indexed
-//                   register array, the bisection as
-//                   fully unrolled predicated sweeps, and the final write
-//                   sweep -- no loads inside the sweeps.
+//   search_sweep  : warp per batch of 32 lists: each lane's first samples in a
+//                   statically indexed register array, the rest in the warp's
+//                   shared rows (cp.async); the bisection (PAPER.md:100-101,
+//                   :176) as predicated lock-step sweeps, and the final write
+//                   sweep.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ int short_ms(int b) { return b == 0 ? 32 : 40; }
 
 // Gather of one batch of short search lists (k_out < m <= 40), thread per
 // list: the run-based k-way merge over the per-PE runs, their
