@@ -132,17 +132,23 @@ def _ptr_array(arrs):
 
 
 def composite(pes, W, H, G, k_out, max_iters=16, gamma_max=2.0, pix_begin=0, pix_end=-1,
-              n_threads=1, with_stats=True):
+              n_threads=1, with_stats=True, out=None):
     """Direct-send composite of dense sub-VDIs (dicts with count/depth/rgba
-    numpy arrays).  Returns dict(count u8[P], depth f32[P,k,2], rgba f32[P,k,4], stats)."""
+    numpy arrays).  Returns dict(count u8[P], depth f32[P,k,2], rgba f32[P,k,4], stats).
+    `out` (optional): a previous result dict whose arrays are reused (a band
+    composite then does not pay for zeroing whole-image outputs)."""
     P = W * H
     cnt = [np.ascontiguousarray(p["count"], np.uint8) for p in pes]
     dep = [np.ascontiguousarray(p["depth"], np.float32) for p in pes]
     rgb = [np.ascontiguousarray(p["rgba"], np.float32) for p in pes]
-    oc = np.zeros(P, np.uint8)
-    od = np.zeros((P, k_out, 2), np.float32)
-    orgba = np.zeros((P, k_out, 4), np.float32)
-    st = np.zeros(P, STATS_DTYPE) if with_stats else None
+    if out is not None:
+        oc, od, orgba, st = out["count"], out["depth"], out["rgba"], out["stats"]
+        assert oc.shape == (P,) and od.shape == (P, k_out, 2) and (st is not None) == with_stats
+    else:
+        oc = np.zeros(P, np.uint8)
+        od = np.zeros((P, k_out, 2), np.float32)
+        orgba = np.zeros((P, k_out, 4), np.float32)
+        st = np.zeros(P, STATS_DTYPE) if with_stats else None
     lib().orc_composite(C.c_int32(len(pes)), _ptr_array(cnt), _ptr_array(dep), _ptr_array(rgb),
                         C.c_int32(W), C.c_int32(H), C.c_int32(G), C.c_int32(k_out), C.c_int32(max_iters),
                         C.c_float(gamma_max), C.c_int64(pix_begin), C.c_int64(pix_end),
