@@ -95,6 +95,8 @@ CASES = [
     (3, 5, 128, 90, 12, 8, 9.0),
     (4, 8, 256, 64, 20, 20, 14.0),
     (4, 3, 96, 41, 6, 6, 5.0),      # fewer PEs than ranks: rank 3 homes none
+    (8, 8, 256, 64, 20, 20, 14.0),  # the north-star rank count (one PE per rank)
+    (8, 16, 160, 40, 8, 8, 10.0),   # 8 ranks, two PEs each, unaligned strips
 ]
 
 
@@ -271,13 +273,13 @@ def test_loopback_host_entries(vdi, span):
         c.close()
 
 
-@pytest.mark.parametrize("rotate,overlap", [(False, True), (True, True), (True, False)])
-def test_loopback_composite_frames(vdi, rotate, overlap):
+@pytest.mark.parametrize("rotate,overlap,G", [(False, True, 3), (True, True, 3), (True, False, 3), (True, True, 8)])
+def test_loopback_composite_frames(vdi, rotate, overlap, G):
     """vdi_composite_frames (frames in flight through strip mode): the root
     merges into its image rows and inflates the others on a second stream;
     six frames, one root or a rotating one -- each image equals the
     one-context composite of its frame bit for bit."""
-    G, n, W, H, k = 3, 6, 128, 72, 10
+    n, W, H, k = 6, 128, 72, 10
     F = 6
     comps = _group(vdi, G, W, H, k, k, n, stats=not overlap)  # PIXEL_STATS turns the search overlap off
     frames = []
