@@ -89,3 +89,38 @@ def test_product_does_not_import_oracle():
             if f.endswith((".py", ".cu", ".h", ".cpp")):
                 txt = open(os.path.join(dp, f)).read()
                 assert "import oracle" not in txt and "from oracle" not in txt and "liboracle" not in txt, f
+
+
+def test_header_is_plain_c_and_links(tmp_path):
+    """include/vdi.h compiles as C99 (no C++ in the boundary) and a C program
+    links against libvdi.so and calls its host-only entry points."""
+    import shutil
+    import subprocess
+    cc = shutil.which("gcc") or shutil.which("cc")
+    if cc is None:
+        pytest.skip("no C compiler")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    libdir = os.path.join(root, "paper_2206_14503_b200", "lib")
+    if not os.path.exists(os.path.join(libdir, "libvdi.so")):
+        pytest.skip("libvdi.so not built")
+    src = tmp_path / "abi.c"
+    src.write_text(r"""
+#include <stdio.h>
+#include "vdi.h"
+int main(void) {
+  uint32_t a = 0, b = 0;
+  if (vdi_strip_rows(1080, 8, 3, &a, &b) != VDI_OK || a != 405 || b != 540) return 1;
+  if (vdi_strip_rows(1080, 8, 8, &a, &b) == VDI_OK) return 2;          /* g >= n_ranks: an error */
+  if (vdi_pe_home(16, 8, 15) != 7) return 3;
+  if (vdi_full_bytes(1920, 1080, 20) != (uint64_t)1920 * 1080 * (1 + 24 * 20)) return 4;
+  if (!vdi_version() || !vdi_status_string(VDI_ERR_INVALID_ARG)) return 5;
+  printf("%s\n", vdi_version());
+  return 0;
+}
+""")
+    exe = tmp_path / "abi"
+    r = subprocess.run([cc, "-std=c99", "-Wall", "-Werror", "-I", os.path.join(root, "include"), str(src), "-o", str(exe),
+                        "-L", libdir, "-lvdi", "-Wl,-rpath," + libdir], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    r = subprocess.run([str(exe)], capture_output=True, text=True)
+    assert r.returncode == 0, (r.returncode, r.stdout, r.stderr)
