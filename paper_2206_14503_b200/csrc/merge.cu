@@ -479,6 +479,9 @@ __host__ __device__ constexpr size_t fast_warp_bytes(int k) {
          & ~(size_t)15;
 }
 
+#ifndef VDI_PAIR_SCAN
+#define VDI_PAIR_SCAN 1  // the pass-through's count scans two sources at a time (16-bit halves)
+#endif
 #ifndef VDI_FAST_RUN
 #define VDI_FAST_RUN 4
 #endif
@@ -556,6 +559,31 @@ __global__ void __launch_bounds__(kFastThreads) merge_fast_kernel(MergeParams mp
       gidx[s] = nb[s];
     }
     prefetch(next_group(g));
+#if VDI_PAIR_SCAN
+    // the warp scans of the sources' counts, two sources per scan: 16-bit
+    // halves hold the running sums (<= 32 x 255 < 2^16)
+    const bool carry = (g - mp.g_begin) % kRun + 1 < kRun;
+#pragma unroll
+    for (int s = 0; s < NS; s += 2) {
+      if (s < n) {
+        const bool two = s + 1 < n && s + 1 < NS;
+        const uint32_t c0 = cnt[s], c1 = two ? cnt[s + 1 < NS ? s + 1 : s] : 0u;
+        const uint32_t incl = warp_incl_scan(c0 | (c1 << 16), lane);
+        const uint32_t i0 = incl & 0xffffu, i1 = incl >> 16;
+        if (carry && (mp.src[s].offset || (two && mp.src[s + 1 < NS ? s + 1 : s].offset))) {
+          const uint32_t tot = __shfl_sync(kFull, incl, 31);
+          if (mp.src[s].offset) nb[s] = gidx[s] + (tot & 0xffffu);  // base of group g + 1 (same run)
+          if (two && mp.src[s + 1 < NS ? s + 1 : s].offset) nb[s + 1 < NS ? s + 1 : s] = gidx[s + 1 < NS ? s + 1 : s] + (tot >> 16);
+        }
+        gidx[s] += i0 - c0;
+        m += c0;
+        if (two) {
+          gidx[s + 1 < NS ? s + 1 : s] += i1 - c1;
+          m += c1;
+        }
+      }
+    }
+#else
 #pragma unroll
     for (int s = 0; s < NS; ++s) {
       if (s < n) {
@@ -567,6 +595,7 @@ __global__ void __launch_bounds__(kFastThreads) merge_fast_kernel(MergeParams mp
         m += c;
       }
     }
+#endif
     rec_acc += m;
 #pragma unroll
     for (int s = 0; s < NS; ++s)
