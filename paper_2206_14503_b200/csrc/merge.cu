@@ -313,14 +313,15 @@ template <int NS>
 __device__ __forceinline__ void push_entries(const MergeParams& mp, int bk, uint32_t p, uint32_t m,
                                              const uint32_t (&goff)[NS], int lane) {
   const unsigned lt = (1u << lane) - 1u;
-#pragma unroll 1
-  for (int b = 0; b < VDI_N_BUCKETS; ++b) {
-    const unsigned mask = __ballot_sync(kFull, bk == b);
-    if (!mask) continue;
+  {
+    // lanes of the same bucket: one atomic per bucket present, by its lowest lane
+    const unsigned mask = __match_any_sync(kFull, bk);
+    const int leader = __ffs(mask) - 1;
+    const int b = bk;
     uint32_t w0 = 0;
-    if (lane == 0) w0 = atomicAdd(mp.wl_count + b, (uint32_t)__popc(mask));
-    w0 = __shfl_sync(kFull, w0, 0);
-    if (bk == b) {
+    if (b >= 0 && lane == leader) w0 = atomicAdd(mp.wl_count + b, (uint32_t)__popc(mask));
+    w0 = __shfl_sync(kFull, w0, leader);
+    if (b >= 0) {
       const uint32_t idx = w0 + __popc(mask & lt);
       if (idx < mp.wl_cap) {
         uint32_t* e = mp.wl[b] + (size_t)idx * (3 + mp.n_src);
