@@ -743,6 +743,9 @@ __global__ void __launch_bounds__(kFastThreads) merge_fast_kernel(MergeParams mp
 template <int NS, int CH = 8>
 __device__ __forceinline__ bool long_gather_lane(const MergeParams& mp, uint32_t m, const uint32_t (&goff)[NS],
                                                  const uint32_t (&cnt)[NS], float4* orgba, float2* odep);
+#ifndef VDI_GATHER_PIPE
+#define VDI_GATHER_PIPE 1  // run-based gathers load the next chunk of a run before merging the current one
+#endif
 #ifndef VDI_SGATHER_CH
 #define VDI_SGATHER_CH 8  // records loaded per trip in the short gather
 #endif
@@ -1146,6 +1149,64 @@ __device__ __forceinline__ bool long_gather_lane(const MergeParams& mp, uint32_t
     // lower PE first, Q11), 8 loaded per trip (the ones past the cut are
     // reloaded, from L1/L2, when b is chosen again)
     float tn = CUDART_INF_F;
+#if VDI_GATHER_PIPE
+    // two chunks of CH/2 records: the next chunk of the run is loaded
+    // (speculatively) before the current one is merged, so a run longer than
+    // a chunk costs one round trip, not one per chunk
+    constexpr int CQ = CH / 2;
+    float2 dv[CQ], dn[CQ];
+    float4 cv[CQ], cn[CQ];
+    uint32_t nch = min((uint32_t)CQ, cb - ii);
+#pragma unroll
+    for (int u = 0; u < CQ; ++u)
+      if ((uint32_t)u < nch) {
+        dv[u] = __ldg(dp + gb + ii + u);
+        cv[u] = src_ld4(cp + gb + ii + u);
+      }
+    for (bool first = true;;) {
+      const uint32_t ii2 = ii + nch;
+      const uint32_t nch2 = ii2 < cb ? min((uint32_t)CQ, cb - ii2) : 0u;
+#pragma unroll
+      for (int u = 0; u < CQ; ++u)
+        if ((uint32_t)u < nch2) {
+          dn[u] = __ldg(dp + gb + ii2 + u);
+          cn[u] = src_ld4(cp + gb + ii2 + u);
+        }
+      uint32_t taken = 0;
+      bool stop = false;
+#pragma unroll
+      for (int u = 0; u < CQ; ++u)
+        if (!stop && (uint32_t)u < nch) {
+          const float2 d = dv[u];
+          if (!(first && u == 0) && !(d.x < b2t || (d.x == b2t && b < b2))) {
+            stop = true;
+            tn = d.x;
+          } else {
+            float4 c = cv[u];
+            bad |= c.w == 0.f || d.x < prev_tb;  // Q23 / Q12
+            if (r > 0 && d.x > prev_tb) c.w = -c.w;  // gap before this sample: sign of alpha
+            prev_tb = d.y;
+            slot_st(orgba + r * 32, c);
+            dep_st(odep + r * 32, d);
+            ++r;
+            ++taken;
+          }
+        }
+      ii += taken;
+      first = false;
+      if (stop) break;  // tn = head of run b
+      if (ii >= cb) {
+        tn = CUDART_INF_F;
+        break;
+      }
+#pragma unroll
+      for (int u = 0; u < CQ; ++u) {  // the whole chunk was taken: the next one is current
+        dv[u] = dn[u];
+        cv[u] = cn[u];
+      }
+      nch = nch2;
+    }
+#else
     for (bool first = true;;) {
       const uint32_t nch = min((uint32_t)CH, cb - ii);
       float2 dv[CH];
@@ -1184,6 +1245,7 @@ __device__ __forceinline__ bool long_gather_lane(const MergeParams& mp, uint32_t
         break;
       }
     }
+#endif
 #pragma unroll
     for (int s = 0; s < NS; ++s)
       if (s == b) {
