@@ -36,6 +36,20 @@ __global__ void __launch_bounds__(32) bulk(char* p, size_t nchunks) {
   if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
 }
 
+// the same 15 KB chunks written by the warp itself: ld.shared.v4 + st.global.v4 (512 B per warp store)
+template <int CH>
+__global__ void __launch_bounds__(32) lsu(char* p, size_t nchunks) {
+  extern __shared__ __align__(128) char sm[];
+  float4* s4 = reinterpret_cast<float4*>(sm);
+  for (int i = threadIdx.x; i < CH / 16; i += 32) s4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  __syncwarp();
+  for (size_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
+    float4* d = reinterpret_cast<float4*>(p + c * CH);
+#pragma unroll 8
+    for (int i = threadIdx.x; i < CH / 16; i += 32) d[i] = s4[i];
+  }
+}
+
 static float time_it(void (*f)(void*), void* a, cudaStream_t s, int reps) {
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
@@ -73,6 +87,19 @@ int main() {
   cudaFuncSetAttribute(bulk<15360>, cudaFuncAttributeMaxDynamicSharedMemorySize, 15360);
   t = time_it([](void* v) { Args* a = (Args*)v; bulk<15360><<<148 * 13, 32, 15360, a->s>>>(a->p, a->bytes / 15360); }, &a, a.s, reps);
   printf("bulk15K  %.4f ms  %.1f GB/s (write, 13 warps/SM, wait.read per chunk)\n", t, (a.bytes / 15360) * 15360.0 / t / 1e6);
+  for (int wps : {4, 8, 13}) {
+    static int W;
+    W = wps;
+    t = time_it([](void* v) { Args* a = (Args*)v; bulk<15360><<<148 * W, 32, 15360, a->s>>>(a->p, a->bytes / 15360); }, &a, a.s, reps);
+    printf("bulk15K  %.4f ms  %.1f GB/s (write, %d warps/SM)\n", t, (a.bytes / 15360) * 15360.0 / t / 1e6, wps);
+  }
+  cudaFuncSetAttribute(lsu<15360>, cudaFuncAttributeMaxDynamicSharedMemorySize, 15360);
+  for (int wps : {4, 8, 13}) {
+    static int W;
+    W = wps;
+    t = time_it([](void* v) { Args* a = (Args*)v; lsu<15360><<<148 * W, 32, 15360, a->s>>>(a->p, a->bytes / 15360); }, &a, a.s, reps);
+    printf("lsu15K   %.4f ms  %.1f GB/s (write, ld.shared + st.global.v4, %d warps/SM)\n", t, (a.bytes / 15360) * 15360.0 / t / 1e6, wps);
+  }
   t = time_it([](void* v) { Args* a = (Args*)v; cudaMemcpyAsync(a->q, a->p, a->bytes, cudaMemcpyDeviceToDevice, a->s); }, &a, a.s, reps);
   printf("copy     %.4f ms  %.1f GB/s (read+write)\n", t, 2.0 * bytes / t / 1e6);
   cudaError_t e = cudaDeviceSynchronize();
