@@ -525,9 +525,12 @@ __global__ void __launch_bounds__(kFastThreads) merge_fast_kernel(MergeParams mp
     const uint32_t r = (gg - mp.g_begin) % kRun;
     return r + 1 < kRun ? gg + 1 : gg + 1 + (nw_all - 1) * kRun;
   };
-  uint32_t nc[NS], nb[NS];
+  // nb: bases loaded by the prefetch (in flight until the next iteration);
+  // nbc: bases carried along a run.  Separate registers, so that the carry
+  // written during group g never waits on (or overwrites) a load in flight
+  uint32_t nc[NS], nb[NS], nbc[NS];
 #pragma unroll
-  for (int s = 0; s < NS; ++s) nb[s] = 0;
+  for (int s = 0; s < NS; ++s) nb[s] = nbc[s] = 0;
   auto prefetch = [&](uint32_t gg) {
     const uint32_t pp = gg * 32 + lane;
     const bool run_start = (gg - mp.g_begin) % kRun == 0;
@@ -554,32 +557,54 @@ __global__ void __launch_bounds__(kFastThreads) merge_fast_kernel(MergeParams mp
     const bool valid = p < mp.P;
     uint32_t cnt[NS], gidx[NS];
     uint32_t m = 0;
+    const bool mid_run = (g - mp.g_begin) % kRun != 0;
 #pragma unroll
     for (int s = 0; s < NS; ++s) {
       cnt[s] = nc[s];
-      gidx[s] = nb[s];
+      gidx[s] = (mp.src[s].offset && mid_run) ? nbc[s] : nb[s];
     }
     prefetch(next_group(g));
 #if VDI_PAIR_SCAN
     // the warp scans of the sources' counts, two sources per scan: 16-bit
-    // halves hold the running sums (<= 32 x 255 < 2^16)
+    // halves hold the running sums (<= 32 x 255 < 2^16); the (NS + 1) / 2
+    // scans advance step by step together, so their shuffle latencies overlap
     const bool carry = (g - mp.g_begin) % kRun + 1 < kRun;
+    constexpr int NP = (NS + 1) / 2;
+    uint32_t pc[NP], incl[NP];
 #pragma unroll
-    for (int s = 0; s < NS; s += 2) {
-      if (s < n) {
-        const bool two = s + 1 < n && s + 1 < NS;
-        const uint32_t c0 = cnt[s], c1 = two ? cnt[s + 1 < NS ? s + 1 : s] : 0u;
-        const uint32_t incl = warp_incl_scan(c0 | (c1 << 16), lane);
-        const uint32_t i0 = incl & 0xffffu, i1 = incl >> 16;
-        if (carry && (mp.src[s].offset || (two && mp.src[s + 1 < NS ? s + 1 : s].offset))) {
-          const uint32_t tot = __shfl_sync(kFull, incl, 31);
-          if (mp.src[s].offset) nb[s] = gidx[s] + (tot & 0xffffu);  // base of group g + 1 (same run)
-          if (two && mp.src[s + 1 < NS ? s + 1 : s].offset) nb[s + 1 < NS ? s + 1 : s] = gidx[s + 1 < NS ? s + 1 : s] + (tot >> 16);
+    for (int q = 0; q < NP; ++q) {
+      const int s0 = 2 * q, s1 = 2 * q + 1 < NS ? 2 * q + 1 : 2 * q;
+      const uint32_t c0 = s0 < n ? cnt[s0] : 0u, c1 = (2 * q + 1 < NS && s1 < n) ? cnt[s1] : 0u;
+      pc[q] = c0 | (c1 << 16);
+      incl[q] = pc[q];
+    }
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      uint32_t t[NP];
+#pragma unroll
+      for (int q = 0; q < NP; ++q) t[q] = (2 * q < n) ? __shfl_up_sync(kFull, incl[q], d) : 0u;
+#pragma unroll
+      for (int q = 0; q < NP; ++q)
+        if (lane >= d) incl[q] += t[q];
+    }
+    uint32_t tot[NP];  // the group's count totals (lane 31's inclusive sums), all shuffles issued together
+#pragma unroll
+    for (int q = 0; q < NP; ++q) tot[q] = (carry && 2 * q < n) ? __shfl_sync(kFull, incl[q], 31) : 0u;
+#pragma unroll
+    for (int q = 0; q < NP; ++q) {
+      const int s0 = 2 * q, s1 = 2 * q + 1 < NS ? 2 * q + 1 : 2 * q;
+      if (s0 < n) {
+        const bool two = 2 * q + 1 < NS && s1 < n;
+        const uint32_t c0 = pc[q] & 0xffffu, c1 = pc[q] >> 16;
+        const uint32_t i0 = incl[q] & 0xffffu, i1 = incl[q] >> 16;
+        if (carry) {
+          if (mp.src[s0].offset) nbc[s0] = gidx[s0] + (tot[q] & 0xffffu);  // base of group g + 1 (same run)
+          if (two && mp.src[s1].offset) nbc[s1] = gidx[s1] + (tot[q] >> 16);
         }
-        gidx[s] += i0 - c0;
+        gidx[s0] += i0 - c0;
         m += c0;
         if (two) {
-          gidx[s + 1 < NS ? s + 1 : s] += i1 - c1;
+          gidx[s1] += i1 - c1;
           m += c1;
         }
       }
@@ -591,7 +616,7 @@ __global__ void __launch_bounds__(kFastThreads) merge_fast_kernel(MergeParams mp
         const uint32_t c = cnt[s];
         const uint32_t incl = warp_incl_scan(c, lane);
         if (mp.src[s].offset && (g - mp.g_begin) % kRun + 1 < kRun)
-          nb[s] = gidx[s] + __shfl_sync(kFull, incl, 31);  // base of group g + 1 (same run)
+          nbc[s] = gidx[s] + __shfl_sync(kFull, incl, 31);  // base of group g + 1 (same run)
         gidx[s] += incl - c;
         m += c;
       }
