@@ -765,9 +765,10 @@ __global__ void __launch_bounds__(kFastThreads) merge_fast_kernel(MergeParams mp
 // heads in registers (long_gather_lane), writes the samples in depth order to
 // the batch's pool slot in [sample][lane] layout with the gap flag in the sign
 // of alpha; transparent / overlapping records -> general path.
-template <int NS, int CH = 8>
+template <int NS, int CH = 8, int RS = 0>
 __device__ __forceinline__ bool long_gather_lane(const MergeParams& mp, uint32_t m, const uint32_t (&goff)[NS],
-                                                 const uint32_t (&cnt)[NS], float4* orgba, float2* odep);
+                                                 const uint32_t (&cnt)[NS], float4* orgba, float2* odep,
+                                                 float4* srgba = nullptr);
 #ifndef VDI_GATHER_PIPE
 #define VDI_GATHER_PIPE 1  // run-based gathers load the next chunk of a run before merging the current one
 #endif
@@ -1125,10 +1126,12 @@ __device__ __forceinline__ void out_st4(float4* a, float4 v) {
 // Gather of the lanes' lists (valid lanes) into the slot columns orgba/odep
 // (stride 32): run-based k-way merge over the runs' head
 // t_front kept in registers, 8 records loaded per trip.  Returns false for a
-// transparent or overlapping record (Q23, Q12: the general path).
-template <int NS, int CH>
+// transparent or overlapping record (Q23, Q12: the general path).  RS > 0:
+// rgba rows r < RS go to the shared-memory column srgba instead of orgba.
+template <int NS, int CH, int RS>
 __device__ __forceinline__ bool long_gather_lane(const MergeParams& mp, uint32_t m, const uint32_t (&goff)[NS],
-                                                 const uint32_t (&cnt)[NS], float4* orgba, float2* odep) {
+                                                 const uint32_t (&cnt)[NS], float4* orgba, float2* odep,
+                                                 float4* srgba) {
   bool bad = false;
   uint32_t hp[NS];
   float ht[NS];  // t_front of each run's head, kept in registers (one load per record)
@@ -1211,7 +1214,8 @@ __device__ __forceinline__ bool long_gather_lane(const MergeParams& mp, uint32_t
             bad |= c.w == 0.f || d.x < prev_tb;  // Q23 / Q12
             if (r > 0 && d.x > prev_tb) c.w = -c.w;  // gap before this sample: sign of alpha
             prev_tb = d.y;
-            slot_st(orgba + r * 32, c);
+            if (RS > 0 && r < (uint32_t)RS) srgba[r * 32] = c;
+            else slot_st(orgba + r * 32, c);
             dep_st(odep + r * 32, d);
             ++r;
             ++taken;
@@ -1256,7 +1260,8 @@ __device__ __forceinline__ bool long_gather_lane(const MergeParams& mp, uint32_t
             bad |= c.w == 0.f || d.x < prev_tb;  // Q23 / Q12
             if (r > 0 && d.x > prev_tb) c.w = -c.w;  // gap before this sample: sign of alpha
             prev_tb = d.y;
-            slot_st(orgba + r * 32, c);
+            if (RS > 0 && r < (uint32_t)RS) srgba[r * 32] = c;
+            else slot_st(orgba + r * 32, c);
             dep_st(odep + r * 32, d);
             ++r;
             ++taken;
@@ -1314,12 +1319,30 @@ __device__ __forceinline__ void long_step8(const float4 (&v)[8], int q0, int m, 
   }
 }
 
+#ifndef VDI_LONG_SROWS
+#define VDI_LONG_SROWS 32  // rgba rows of each long-search slot column kept in shared memory (multiple of 8)
+#endif
+// Rows q..q+7 of a slot column (q a multiple of 8, the same on every lane that
+// shares the call): rows below RS from the warp's shared-memory column scol,
+// the rest from the global slot column col.
+template <int RS>
+__device__ __forceinline__ void rows8(float4 (&X)[8], const float4* scol, const float4* __restrict__ col, int q) {
+  if (RS > 0 && q < RS) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) X[u] = scol[(q + u) * 32];
+  } else {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) X[u] = slot_ld(col + (q + u) * 32);
+  }
+}
+
 // One count-mode sweep over a pool column: chunks of 8 samples in two register
 // buffers (the next chunk's loads are in flight while one is swept; ping-pong,
 // no copies), leaving as soon as the count exceeds k.  Reads up to 24 rows past
 // m (the pool has slack for that).
-__device__ __forceinline__ int long_count(const float4* __restrict__ col, int m, float g2, int k, float& L,
-                                          float& U) {
+template <int RS>
+__device__ __forceinline__ int long_count(const float4* scol, const float4* __restrict__ col, int m, float g2, int k,
+                                          float& L, float& U) {
   float ar = 0.f, ag = 0.f, ab = 0.f, aa = 0.f;
   int sc = 0;
   L = -1.f;
@@ -1327,29 +1350,23 @@ __device__ __forceinline__ int long_count(const float4* __restrict__ col, int m,
   // three register chunks in rotation: the loads run two chunks (16 samples)
   // ahead of the sweep, which covers the L2 latency of the pool
   float4 A[8], B[8], C[8];
-#pragma unroll
-  for (int u = 0; u < 8; ++u) {
-    A[u] = slot_ld(col + u * 32);
-    B[u] = slot_ld(col + (8 + u) * 32);
-  }
-  const float4* pp = col + 16 * 32;
+  rows8<RS>(A, scol, col, 0);
+  rows8<RS>(B, scol, col, 8);
+  int qn = 16;  // next row to load
   int q0 = 0;
   for (;;) {
-#pragma unroll
-    for (int u = 0; u < 8; ++u) C[u] = slot_ld(pp + u * 32);
-    pp += 8 * 32;
+    rows8<RS>(C, scol, col, qn);
+    qn += 8;
     long_step8(A, q0, m, g2, ar, ag, ab, aa, sc, L, U);
     q0 += 8;
     if (q0 >= m || sc > k || (VDI_UB_EXIT && sc + (m - q0) < k)) break;
-#pragma unroll
-    for (int u = 0; u < 8; ++u) A[u] = slot_ld(pp + u * 32);
-    pp += 8 * 32;
+    rows8<RS>(A, scol, col, qn);
+    qn += 8;
     long_step8(B, q0, m, g2, ar, ag, ab, aa, sc, L, U);
     q0 += 8;
     if (q0 >= m || sc > k || (VDI_UB_EXIT && sc + (m - q0) < k)) break;
-#pragma unroll
-    for (int u = 0; u < 8; ++u) B[u] = slot_ld(pp + u * 32);
-    pp += 8 * 32;
+    rows8<RS>(B, scol, col, qn);
+    qn += 8;
     long_step8(C, q0, m, g2, ar, ag, ab, aa, sc, L, U);
     q0 += 8;
     if (q0 >= m || sc > k || (VDI_UB_EXIT && sc + (m - q0) < k)) break;
@@ -1362,36 +1379,31 @@ __device__ __forceinline__ int long_count(const float4* __restrict__ col, int m,
 // no lane still needs a sample (its bisection active, q < m, count <= k).
 // Lanes that went past their end keep stepping harmlessly: samples past m are
 // not counted, and extra constraints only shrink the memo interval.
-__device__ __forceinline__ int long_count_sync(const float4* __restrict__ col, int m, float g2, int k, bool act,
-                                               float& L, float& U) {
+template <int RS>
+__device__ __forceinline__ int long_count_sync(const float4* scol, const float4* __restrict__ col, int m, float g2,
+                                               int k, bool act, float& L, float& U) {
   float ar = 0.f, ag = 0.f, ab = 0.f, aa = 0.f;
   int sc = 0;
   L = -1.f;
   U = CUDART_INF_F;
   float4 A[8], B[8], C[8];
-#pragma unroll
-  for (int u = 0; u < 8; ++u) {
-    A[u] = slot_ld(col + u * 32);
-    B[u] = slot_ld(col + (8 + u) * 32);
-  }
-  const float4* pp = col + 16 * 32;
+  rows8<RS>(A, scol, col, 0);
+  rows8<RS>(B, scol, col, 8);
+  int qn = 16;
   int q0 = 0;
   for (;;) {
-#pragma unroll
-    for (int u = 0; u < 8; ++u) C[u] = slot_ld(pp + u * 32);
-    pp += 8 * 32;
+    rows8<RS>(C, scol, col, qn);
+    qn += 8;
     long_step8(A, q0, m, g2, ar, ag, ab, aa, sc, L, U);
     q0 += 8;
     if (!__any_sync(kFull, act && q0 < m && sc <= k && (!VDI_UB_EXIT || sc + (m - q0) >= k))) break;
-#pragma unroll
-    for (int u = 0; u < 8; ++u) A[u] = slot_ld(pp + u * 32);
-    pp += 8 * 32;
+    rows8<RS>(A, scol, col, qn);
+    qn += 8;
     long_step8(B, q0, m, g2, ar, ag, ab, aa, sc, L, U);
     q0 += 8;
     if (!__any_sync(kFull, act && q0 < m && sc <= k && (!VDI_UB_EXIT || sc + (m - q0) >= k))) break;
-#pragma unroll
-    for (int u = 0; u < 8; ++u) B[u] = slot_ld(pp + u * 32);
-    pp += 8 * 32;
+    rows8<RS>(B, scol, col, qn);
+    qn += 8;
     long_step8(C, q0, m, g2, ar, ag, ab, aa, sc, L, U);
     q0 += 8;
     if (!__any_sync(kFull, act && q0 < m && sc <= k && (!VDI_UB_EXIT || sc + (m - q0) >= k))) break;
@@ -1403,24 +1415,22 @@ __device__ __forceinline__ int long_count_sync(const float4* __restrict__ col, i
 // sweep(), the gap taken from the sign of alpha): rgba and depth in chunks of
 // 8 with the next chunk's loads in flight, so the sweep does not wait on one
 // L2 round trip per sample.
-__device__ __forceinline__ int long_write(const float4* __restrict__ col, const float2* __restrict__ dcol, int m,
-                                          float gamma, int k, float2* od, float4* oc) {
+template <int RS>
+__device__ __forceinline__ int long_write(const float4* scol, const float4* __restrict__ col,
+                                          const float2* __restrict__ dcol, int m, float gamma, int k, float2* od,
+                                          float4* oc) {
   const float gg = gamma * gamma;
   float ar = 0.f, ag = 0.f, ab = 0.f, aa = 0.f, tf = 0.f, tb = 0.f;
   int c = 0;
   float4 cv[8], cn[8];
   float2 dv[8], dn[8];
+  rows8<RS>(cv, scol, col, 0);
 #pragma unroll
-  for (int u = 0; u < 8; ++u) {
-    cv[u] = slot_ld(col + u * 32);
-    dv[u] = dep_ld(dcol + u * 32);
-  }
+  for (int u = 0; u < 8; ++u) dv[u] = dep_ld(dcol + u * 32);
   for (int q0 = 0; q0 < m; q0 += 8) {
+    rows8<RS>(cn, scol, col, q0 + 8);
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      cn[u] = slot_ld(col + (q0 + 8 + u) * 32);
-      dn[u] = dep_ld(dcol + (q0 + 8 + u) * 32);
-    }
+    for (int u = 0; u < 8; ++u) dn[u] = dep_ld(dcol + (q0 + 8 + u) * 32);
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
       const int q = q0 + u;
@@ -1470,7 +1480,9 @@ __device__ __forceinline__ int long_write(const float4* __restrict__ col, const 
 #ifndef VDI_SPEC_MAX
 #define VDI_SPEC_MAX 8192
 #endif
-__device__ __forceinline__ float long_spec_bisect(const MergeParams& mp, const float4* col, int m, int lane) {
+template <int RS>
+__device__ __forceinline__ float long_spec_bisect(const MergeParams& mp, const float4* scol, const float4* col, int m,
+                                                  int lane) {
   const int k = mp.k_out;
   const uint32_t jn = lane < 31 ? (uint32_t)lane + 1 : 1u;  // heap node of this lane
   const int depth = 31 - __clz(jn);
@@ -1485,7 +1497,7 @@ __device__ __forceinline__ float long_spec_bisect(const MergeParams& mp, const f
       md = 0.5f * (lw + hg);
     }
     float L, U;
-    const int c = long_count(col, m, md * md, k, L, U);
+    const int c = long_count<RS>(scol, col, m, md * md, k, L, U);
     uint32_t node = 1;
     for (int lev = 0; lev < 5 && !done; ++lev) {
       const int cn = __shfl_sync(kFull, c, (int)node - 1);
@@ -1520,6 +1532,8 @@ __global__ void __launch_bounds__(32) long_search_kernel(MergeParams mp) {
   char* slot = mp.long_pool + (size_t)blockIdx.x * mp.long_slot;
   float4* col0 = reinterpret_cast<float4*>(slot);
   float2* dcol0 = reinterpret_cast<float2*>(slot + (size_t)(cap + 32) * 32 * 16);
+  constexpr int RS = VDI_LONG_SROWS;
+  extern __shared__ float4 lsm[];  // rgba rows 0..RS-1 of the slot columns (RS x 32 float4)
   const bool spec = c2 + c3 <= VDI_SPEC_MAX;
   const uint32_t nb2 = (c2 + 31) / 32, nb3 = (c3 + 31) / 32;
   for (;;) {
@@ -1555,14 +1569,17 @@ __global__ void __launch_bounds__(32) long_search_kernel(MergeParams mp) {
     for (int s = 0; s < NS; ++s)
       if (s < n) VDI_CHECK(!mp.src[s].nrec || goff[s] + cnt[s] <= mp.src[s].nrec, "long search: record index past the source");
     bool bad = valid && m > cap;  // cannot hold it: general path
-    if (valid && !bad) bad = !long_gather_lane<NS>(mp, m, goff, cnt, col0 + (spec ? 0 : lane), dcol0 + (spec ? 0 : lane));
+    if (valid && !bad)
+      bad = !long_gather_lane<NS, 8, RS>(mp, m, goff, cnt, col0 + (spec ? 0 : lane), dcol0 + (spec ? 0 : lane),
+                                         lsm + (spec ? 0 : lane));
     __syncwarp();  // the slot columns are complete (and visible to the warp)
     if (__any_sync(kFull, bad)) push_entries<NS>(mp, bad ? VDI_BUCKET_GENERAL : -1, p, m, goff, lane);
     if (spec) {
       if (__shfl_sync(kFull, bad ? 1 : 0, 0)) continue;
-      const float best = long_spec_bisect(mp, col0, (int)m, lane);
+      const float best = long_spec_bisect<RS>(mp, lsm, col0, (int)m, lane);
       if (lane == 0) {
-        const int c = long_write(col0, dcol0, (int)m, best, k, mp.out_depth + (size_t)p * k, mp.out_rgba + (size_t)p * k);
+        const int c = long_write<RS>(lsm, col0, dcol0, (int)m, best, k, mp.out_depth + (size_t)p * k,
+                                     mp.out_rgba + (size_t)p * k);
         mp.out_count[p] = (uint8_t)c;
         if (mp.stat_gamma) mp.stat_gamma[p] = best;
       }
@@ -1571,6 +1588,7 @@ __global__ void __launch_bounds__(32) long_search_kernel(MergeParams mp) {
       // warp sweeping in lock step (coalesced slot rows)
       const bool ok = valid && !bad;
       const float4* col = col0 + lane;
+      const float4* scol = lsm + lane;
       Bisection bs;
       bs.init(mp.gamma_max, ok && mp.max_iters > 0);
 #if VDI_LONG_SYNC
@@ -1578,7 +1596,7 @@ __global__ void __launch_bounds__(32) long_search_kernel(MergeParams mp) {
         bs.advance(k, mp.max_iters);
         if (!__any_sync(kFull, bs.active)) break;
         float L, U;
-        const int c = long_count_sync(col, ok ? (int)m : 0, bs.g2, k, bs.active, L, U);
+        const int c = long_count_sync<RS>(scol, col, ok ? (int)m : 0, bs.g2, k, bs.active, L, U);
         if (bs.active) bs.swept(c, L, U, k, mp.max_iters);
       }
 #else
@@ -1586,13 +1604,13 @@ __global__ void __launch_bounds__(32) long_search_kernel(MergeParams mp) {
         bs.advance(k, mp.max_iters);
         if (!bs.active) break;
         float L, U;
-        const int c = long_count(col, (int)m, bs.g2, k, L, U);
+        const int c = long_count<RS>(scol, col, (int)m, bs.g2, k, L, U);
         bs.swept(c, L, U, k, mp.max_iters);
       }
 #endif
       if (ok) {
-        const int c = long_write(col, dcol0 + lane, (int)m, bs.best, k, mp.out_depth + (size_t)p * k,
-                                 mp.out_rgba + (size_t)p * k);
+        const int c = long_write<RS>(scol, col, dcol0 + lane, (int)m, bs.best, k, mp.out_depth + (size_t)p * k,
+                                     mp.out_rgba + (size_t)p * k);
         mp.out_count[p] = (uint8_t)c;
         if (mp.stat_gamma) mp.stat_gamma[p] = bs.best;
       }
@@ -2000,7 +2018,7 @@ static cudaError_t launch_search_ns(const MergeParams& mp, cudaStream_t st, int*
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     ++*launches;
   }
-  long_search_kernel<NS><<<part(mp.long_warps), 32, 0, st>>>(mp);
+  long_search_kernel<NS><<<part(mp.long_warps), 32, (size_t)VDI_LONG_SROWS * 32 * 16, st>>>(mp);
   ++*launches;
   return cudaGetLastError();
 }
