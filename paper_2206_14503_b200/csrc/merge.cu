@@ -467,21 +467,12 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
-#ifndef VDI_FAST_EVICT_FIRST
-#define VDI_FAST_EVICT_FIRST 1  // the pass-through's output leaves L2 first (the search's slots beside it stay)
-#endif
 __device__ __forceinline__ void bulk_store(void* gdst, const void* ssrc, uint32_t bytes) {
-#if VDI_FAST_EVICT_FIRST
   unsigned long long pol;
   asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
   asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(gdst),
                "r"(smem_u32(ssrc)), "r"(bytes), "l"(pol)
                : "memory");
-#else
-  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(smem_u32(ssrc)),
-               "r"(bytes)
-               : "memory");
-#endif
 }
 
 // bytes of per-warp shared memory of the fast kernel for budget k
@@ -491,9 +482,6 @@ __host__ __device__ constexpr size_t fast_warp_bytes(int k) {
          & ~(size_t)15;
 }
 
-#ifndef VDI_PAIR_SCAN
-#define VDI_PAIR_SCAN 1  // the pass-through's count scans two sources at a time (16-bit halves)
-#endif
 #ifndef VDI_FAST_RUN
 #define VDI_FAST_RUN 4
 #endif
@@ -575,7 +563,6 @@ __global__ void __launch_bounds__(kFastThreads) merge_fast_kernel(MergeParams mp
       gidx[s] = (mp.src[s].offset && mid_run) ? nbc[s] : nb[s];
     }
     prefetch(next_group(g));
-#if VDI_PAIR_SCAN
     // the warp scans of the sources' counts, two sources per scan: 16-bit
     // halves hold the running sums (<= 32 x 255 < 2^16); the (NS + 1) / 2
     // scans advance step by step together, so their shuffle latencies overlap
@@ -620,19 +607,6 @@ __global__ void __launch_bounds__(kFastThreads) merge_fast_kernel(MergeParams mp
         }
       }
     }
-#else
-#pragma unroll
-    for (int s = 0; s < NS; ++s) {
-      if (s < n) {
-        const uint32_t c = cnt[s];
-        const uint32_t incl = warp_incl_scan(c, lane);
-        if (mp.src[s].offset && (g - mp.g_begin) % kRun + 1 < kRun)
-          nbc[s] = gidx[s] + __shfl_sync(kFull, incl, 31);  // base of group g + 1 (same run)
-        gidx[s] += incl - c;
-        m += c;
-      }
-    }
-#endif
     rec_acc += m;
 #pragma unroll
     for (int s = 0; s < NS; ++s)
@@ -780,9 +754,6 @@ template <int NS, int CH = 8, int RS = 0>
 __device__ __forceinline__ bool long_gather_lane(const MergeParams& mp, uint32_t m, const uint32_t (&goff)[NS],
                                                  const uint32_t (&cnt)[NS], float4* orgba, float2* odep,
                                                  float4* srgba = nullptr);
-#ifndef VDI_GATHER_PIPE
-#define VDI_GATHER_PIPE 1  // run-based gathers load the next chunk of a run before merging the current one
-#endif
 #ifndef VDI_SGATHER_CH
 #define VDI_SGATHER_CH 8  // records loaded per trip in the short gather
 #endif
@@ -850,9 +821,6 @@ __device__ __forceinline__ void gather_short_batch(const MergeParams& mp, uint32
 #ifndef VDI_UB_EXIT
 #define VDI_UB_EXIT 1  // count sweeps also stop once the count can no longer reach k
 #endif
-#ifndef VDI_MEMO_CHEAP
-#define VDI_MEMO_CHEAP 1  // interval bookkeeping with one select per comparison
-#endif
 #ifndef VDI_MEMO
 #define VDI_MEMO 1  // 0: plain bisection in the short sweep (A/B of the memo's cost)
 #endif
@@ -894,7 +862,6 @@ __device__ __forceinline__ void sweep_rows(const MergeParams& mp, uint32_t p, in
         const float sa = fabsf(sv.w);
         float n2, d2;
         n2d2_packed(ar, ag, ab, aa, sv.x, sv.y, sv.z, sa, n2, d2);
-#if VDI_MEMO_CHEAP
         // the comparisons of this step: v1 = |acc|^2 at a gap (Q8), v2 = D^2
         // unless the gap closed the segment; NaN = not made (ignored below)
         const float v1 = gap ? n2 : qnan;
@@ -907,14 +874,6 @@ __device__ __forceinline__ void sweep_rows(const MergeParams& mp, uint32_t p, in
           U = dsp ? fminf(U, v2) : U;
           L = dsp ? L : fmaxf(L, v2);
         }
-#else
-        const bool gcl = gap & (n2 > g2);
-        const bool dsp = d2 > g2;
-        if (!first) {  // comparisons that did not happen contribute NaN (ignored by fminf / fmaxf)
-          U = fminf(U, fminf(gcl ? n2 : qnan, (!gcl & dsp) ? d2 : qnan));
-          L = fmaxf(L, fmaxf((gap & !gcl) ? n2 : qnan, (!gcl & !dsp) ? d2 : qnan));
-        }
-#endif
         const bool st = first | gcl | dsp;
         const float tr = 1.0f - aa;
         ar = st ? sv.x : fmaf(tr, sv.x, ar);
@@ -1188,7 +1147,6 @@ __device__ __forceinline__ bool long_gather_lane(const MergeParams& mp, uint32_t
     // lower PE first, Q11), 8 loaded per trip (the ones past the cut are
     // reloaded, from L1/L2, when b is chosen again)
     float tn = CUDART_INF_F;
-#if VDI_GATHER_PIPE
     // two chunks of CH/2 records: the next chunk of the run is loaded
     // (speculatively) before the current one is merged, so a run longer than
     // a chunk costs one round trip, not one per chunk
@@ -1246,47 +1204,6 @@ __device__ __forceinline__ bool long_gather_lane(const MergeParams& mp, uint32_t
       }
       nch = nch2;
     }
-#else
-    for (bool first = true;;) {
-      const uint32_t nch = min((uint32_t)CH, cb - ii);
-      float2 dv[CH];
-      float4 cv[CH];
-#pragma unroll
-      for (int u = 0; u < CH; ++u)
-        if ((uint32_t)u < nch) {
-          dv[u] = __ldg(dp + gb + ii + u);
-          cv[u] = src_ld4(cp + gb + ii + u);
-        }
-      uint32_t taken = 0;
-      bool stop = false;
-#pragma unroll
-      for (int u = 0; u < CH; ++u)
-        if (!stop && (uint32_t)u < nch) {
-          const float2 d = dv[u];
-          if (!(first && u == 0) && !(d.x < b2t || (d.x == b2t && b < b2))) {
-            stop = true;
-            tn = d.x;
-          } else {
-            float4 c = cv[u];
-            bad |= c.w == 0.f || d.x < prev_tb;  // Q23 / Q12
-            if (r > 0 && d.x > prev_tb) c.w = -c.w;  // gap before this sample: sign of alpha
-            prev_tb = d.y;
-            if (RS > 0 && r < (uint32_t)RS) srgba[r * 32] = c;
-            else slot_st(orgba + r * 32, c);
-            dep_st(odep + r * 32, d);
-            ++r;
-            ++taken;
-          }
-        }
-      ii += taken;
-      first = false;
-      if (stop) break;  // tn = head of run b
-      if (ii >= cb) {
-        tn = CUDART_INF_F;
-        break;
-      }
-    }
-#endif
 #pragma unroll
     for (int s = 0; s < NS; ++s)
       if (s == b) {
@@ -1527,9 +1444,6 @@ __device__ __forceinline__ float long_spec_bisect(const MergeParams& mp, const f
   return best;
 }
 
-#ifndef VDI_LONG_SYNC
-#define VDI_LONG_SYNC 1  // lock-step sweeps (coalesced) vs lanes sweeping independently
-#endif
 #ifndef VDI_LONG_WPS
 #define VDI_LONG_WPS 8  // resident long-search warps per SM (their slots in flight stay in L2)
 #endif
@@ -1602,7 +1516,6 @@ __global__ void __launch_bounds__(32) long_search_kernel(MergeParams mp) {
       const float4* scol = lsm + lane;
       Bisection bs;
       bs.init(mp.gamma_max, ok && mp.max_iters > 0);
-#if VDI_LONG_SYNC
       for (;;) {
         bs.advance(k, mp.max_iters);
         if (!__any_sync(kFull, bs.active)) break;
@@ -1610,15 +1523,6 @@ __global__ void __launch_bounds__(32) long_search_kernel(MergeParams mp) {
         const int c = long_count_sync<RS>(scol, col, ok ? (int)m : 0, bs.g2, k, bs.active, L, U);
         if (bs.active) bs.swept(c, L, U, k, mp.max_iters);
       }
-#else
-      for (;;) {
-        bs.advance(k, mp.max_iters);
-        if (!bs.active) break;
-        float L, U;
-        const int c = long_count<RS>(scol, col, (int)m, bs.g2, k, L, U);
-        bs.swept(c, L, U, k, mp.max_iters);
-      }
-#endif
       if (ok) {
         const int c = long_write<RS>(scol, col, dcol0 + lane, (int)m, bs.best, k, mp.out_depth + (size_t)p * k,
                                      mp.out_rgba + (size_t)p * k);
