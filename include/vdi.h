@@ -307,9 +307,13 @@ vdi_status vdi_gather_root(vdi_ctx* ctx, uint32_t root, const vdi_full_view* str
  * root of (others may be zeroed structs); distinct buffers per frame (frames
  * overlap: frame f's search kernels run on a third ctx-owned stream beside
  * frame f+1's pass-through, with two parities of merge scratch; not with
- * VDI_FLAG_PIXEL_STATS).  The call is complete when the caller's stream
- * passes it; never synchronises the host.  ctx-owned scratch: two strips
- * (rows*W*(1 + 24 k_out) bytes each) and a second set of merge scratch.
+ * VDI_FLAG_PIXEL_STATS; a frame whose long-list search fills the GPU for many
+ * waves -- more than 600 000 lists with m > 40 in a recent frame, noted by the
+ * long-search kernel in a mapped host word -- runs without the next
+ * pass-through beside it).  The call is complete when the caller's stream
+ * passes it; never synchronises the host.  ctx-owned scratch (n_ranks > 1):
+ * four non-root strips (rows*W*(1 + 24 k_out) bytes each); a second set of
+ * merge scratch.
  * n_ranks == 1: frames in flight on one GPU, images[f] written whole. */
 vdi_status vdi_composite_frames(vdi_ctx* ctx, uint32_t n_frames, const vdi_dense_view* local_pes,
                                 uint32_t n_local, vdi_full_view* images, const uint32_t* roots);

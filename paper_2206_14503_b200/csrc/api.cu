@@ -298,6 +298,9 @@ struct vdi_ctx {
   int mpar = 0;                   // parity of the current merge
   int last_mpar = 0;              // parity of the last merge (counters)
   cudaStream_t msst = nullptr;    // search stream of the current merge (null: the ctx stream)
+  uint32_t* long_hint = nullptr;      // pinned, mapped host word: a recent frame had > kSerialLong long lists
+  uint32_t* long_hint_dptr = nullptr;  // its device alias
+  DevBuf long_hint_mirror;             // device copy of the last value written
   cudaStream_t sst = nullptr;     // vdi_composite_frames: the search stream
   cudaEvent_t mev_fast[2] = {}, mev_done[2] = {};
   DevBuf g_misc;  // inflate counters
@@ -378,6 +381,7 @@ struct vdi_ctx {
       for (int i = 0; i < 2; ++i)
         if (a[i]) cudaEventDestroy(a[i]);
     if (ptot) cudaFreeHost(ptot);
+    if (long_hint) cudaFreeHost(long_hint);
     if (cub_tmp) cudaFree(cub_tmp);
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
@@ -521,7 +525,26 @@ static vdi_status merge_lists(vdi_ctx* ctx, MergeParams& mp, uint64_t P, uint64_
   // run on a second stream beside the next VDI's pass-through, with their own
   // parity of work lists, counters and pools (this parity's previous search
   // must be done first).
-  if (sst != st) CUDA_TRY(ctx, cudaStreamWaitEvent(st, ctx->mev_done[b], 0));
+  if (sst != st) {
+    CUDA_TRY(ctx, cudaStreamWaitEvent(st, ctx->mev_done[b], 0));
+    // a long search that fills the GPU for many waves does not gain from the
+    // next VDI's pass-through beside it, it loses (C5: 18 % slower search,
+    // profiles/README.md): when a recent frame of this context had more than
+    // kSerialLong long lists, this pass-through also waits for the previous
+    // VDI's search.  The hint is a mapped host word that the long-search kernel
+    // rewrites only when its answer changes; a stale value only changes the
+    // schedule, never a result.
+    if (!ctx->long_hint) {
+      CUDA_TRY(ctx, cudaHostAlloc(reinterpret_cast<void**>(&ctx->long_hint), sizeof(uint32_t), cudaHostAllocMapped));
+      CUDA_TRY(ctx, cudaHostGetDevicePointer(reinterpret_cast<void**>(&ctx->long_hint_dptr), ctx->long_hint, 0));
+      *ctx->long_hint = 0;
+      CUDA_TRY(ctx, ctx->long_hint_mirror.grow(sizeof(uint32_t)));
+      CUDA_TRY(ctx, cudaMemsetAsync(ctx->long_hint_mirror.p, 0, sizeof(uint32_t), st));
+    }
+    if (*static_cast<volatile uint32_t*>(ctx->long_hint)) CUDA_TRY(ctx, cudaStreamWaitEvent(st, ctx->mev_done[b ^ 1], 0));
+    mp.long_hint = ctx->long_hint_dptr;
+    mp.long_hint_dev = ctx->long_hint_mirror.as<uint32_t>();
+  }
   mp.wl_cap = (uint32_t)std::max<uint64_t>(P, 1);
   mp.gen_threads = general_threads(m_max);
   mp.gen_stride = 4 * std::max<uint32_t>(m_max, 1);

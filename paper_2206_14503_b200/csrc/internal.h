@@ -58,6 +58,10 @@ struct SrcDesc {
 // 4 = general path (overlap subdivision, alpha==0 records, and lists whose
 // search-pool slot could not be allocated; thread per list, per-thread scratch).
 #define VDI_N_BUCKETS 5
+// frames in flight: a VDI with more long lists than this (~16 waves of the long
+// kernel: 148 SMs x 8 warps x 32 lists) runs its search without the next VDI's
+// pass-through beside it (vdi_composite_frames; measured C5 +7.4 %)
+static constexpr uint32_t kSerialLong = 600000;
 #define VDI_BUCKET_GENERAL 4
 
 struct MergeParams {
@@ -77,6 +81,8 @@ struct MergeParams {
   // work lists: entry i of bucket b = wl[b][i*(3+n_src) ...] = {p, 0, m, off[0..n_src)}
   uint32_t* wl[VDI_N_BUCKETS];
   uint32_t* wl_count;          // [VDI_N_BUCKETS]
+  uint32_t* long_hint;         // mapped host word or null: 1 when the long buckets hold > kSerialLong lists
+  uint32_t* long_hint_dev;     // device mirror of the last value written to long_hint
   uint32_t wl_cap;             // entries per bucket
   Rec* scratch;            // general path: gen_threads slices of gen_stride records
   uint32_t gen_threads;    // threads of the general kernel (one scratch slice each)

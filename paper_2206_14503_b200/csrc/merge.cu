@@ -1452,6 +1452,13 @@ __global__ void __launch_bounds__(32) long_search_kernel(MergeParams mp) {
   const int lane = threadIdx.x;
   const int k = mp.k_out, n = mp.n_src;
   const uint32_t c2 = min(mp.wl_count[2], mp.wl_cap), c3 = min(mp.wl_count[3], mp.wl_cap);
+  if (mp.long_hint && blockIdx.x == 0 && lane == 0) {  // zero-copy note for the host's frames schedule,
+    const uint32_t h = c2 + c3 > kSerialLong ? 1u : 0u;  // written only when it changes
+    if (*mp.long_hint_dev != h) {
+      *mp.long_hint_dev = h;
+      *(volatile uint32_t*)mp.long_hint = h;
+    }
+  }
   if (c2 + c3 == 0) return;  // no long lists: leave before the claim atomics
   const uint32_t cap = mp.long_maxm;  // rows of a slot
   char* slot = mp.long_pool + (size_t)blockIdx.x * mp.long_slot;
