@@ -1543,8 +1543,8 @@ __global__ void __launch_bounds__(32) long_search_kernel(MergeParams mp) {
 
 // ---------------------------------------------------------------------------
 // General path: thread per work-list entry (steps 1-6 with subdivision),
-// samples in global scratch.  Used for overlapping / transparent records and
-// for m > 128.
+// samples in global scratch.  Used for overlapping / transparent records, for
+// lists longer than a long-search slot (m > 1024) and when a pool is full.
 // ---------------------------------------------------------------------------
 __device__ void over_into(float* acc, const float* b) {
   const float tr = 1.0f - acc[3];
