@@ -578,13 +578,6 @@ static vdi_status merge_lists(vdi_ctx* ctx, MergeParams& mp, uint64_t P, uint64_
   mp.sweep_steps = stats ? &dc->sweep_steps : nullptr;
   mp.err = &dc->err;
   mp.validate = (cf.flags & VDI_FLAG_VALIDATE) ? 1 : 0;
-  if (sst != st) {  // frames in flight: leave room for the next VDI's pass-through
-    static const float share = [] {
-      const char* e = getenv("VDI_SEARCH_SHARE");
-      return e ? (float)atof(e) : 1.0f;  // measured (C3, F = 4): 0.25 / 0.5 / 0.75 / 1.0 -> 0.528 / 0.396 / 0.365 / 0.357 ms per VDI
-    }();
-    mp.search_share = share;
-  }
   uint32_t* slp = sc.slots.as<uint32_t>();
   mp.batch_slot[0] = slp;
   mp.batch_slot[1] = slp + ng + 32;

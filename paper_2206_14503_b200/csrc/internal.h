@@ -111,7 +111,6 @@ struct MergeParams {
   uint32_t long_maxm;
   uint32_t long_warps;
   int* err;            // bit 0: work-list overflow (cannot happen: capacity = lists)
-  float search_share;  // 0 or 1: the search kernels fill the GPU; < 1: that share of it (frames in flight)
   int validate;
 };
 

@@ -1918,10 +1918,9 @@ static cudaError_t launch_fast_ns(const MergeParams& mp, cudaStream_t st, int* l
 template <int NS>
 static cudaError_t launch_search_ns(const MergeParams& mp, cudaStream_t st, int* launches) {
   cudaError_t e;
-  // mp.search_share < 1 (frames in flight): the search kernels keep to that
-  // share of the SMs' residency, so the next VDI's pass-through can run beside them
-  const float sh = mp.search_share > 0.f && mp.search_share < 1.f ? mp.search_share : 1.f;
-  auto part = [&](uint32_t full) { return std::max<uint32_t>(1, (uint32_t)(full * sh)); };
+  // the search kernels fill the GPU (a share of it for the next VDI's
+  // pass-through beside them was measured slower: profiles/README.md)
+  auto part = [&](uint32_t full) { return std::max<uint32_t>(1, full); };
   static int g_per_sm = 0;  // one static per NS instantiation
   if (!g_per_sm) {
     if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_per_sm, search_gather_kernel<NS>, 128, 0)) != cudaSuccess)
