@@ -351,3 +351,34 @@ def test_composite_frames_one_gpu(vdi, stats):
     for f in range(len(frames)):
         for a, b in ((images[f].count, ones[f].count), (images[f].depth, ones[f].depth), (images[f].rgba, ones[f].rgba)):
             assert torch.equal(a, b), f
+
+
+def test_composite_frames_long_schedule(vdi):
+    """vdi_composite_frames over frames whose long search fills the GPU
+    (> 600 000 lists with m > 40): from the second frame
+    on, the long-search kernel's mapped-host hint makes each pass-through wait
+    for the previous VDI's search instead of running beside it.  The schedule
+    never changes a result: every frame equals its own vdi_composite bit for
+    bit (two input sets: the PEs in order and reversed, which changes the
+    sources' tie order, Q11)."""
+    n, W, H, k = 8, 1200, 900, 32
+    base = synth.random_subvdis(n, W, H, k, lam=30.0, seed=900)
+    fwd = [dense_to_device(p, i) for i, p in enumerate(base)]
+    rev = [dense_to_device(p, i) for i, p in enumerate(base[::-1])]
+    frames = [fwd, rev, fwd, rev]
+    comp = vdi.Compositor(W, H, k, k, n)
+    ones = []
+    for fr in frames[:2]:
+        o = comp.empty_strip()
+        comp.composite(fr, o)
+        ones.append(o)
+    torch.cuda.synchronize()
+    b = comp.counters()["bucket_lists"]
+    assert b[2] + b[3] > 600000, b  # the long buckets exceed the schedule's threshold
+    images = [vdi.FullVDI.empty(W, 0, H, k) for _ in frames]
+    comp.composite_frames(frames, images)
+    torch.cuda.synchronize()
+    for f in range(len(frames)):
+        ref = ones[f % 2]
+        for a, c in ((images[f].count, ref.count), (images[f].depth, ref.depth), (images[f].rgba, ref.rgba)):
+            assert torch.equal(a, c), f
