@@ -798,7 +798,13 @@ def _run_ours(args, world, rank, local, clk):
                 "gather_into_root_GBs": cnts[-1]["bytes_gather"] / max(ms_ga, 1e-6) / 1e6,
                 "gather_into_root_frac": cnts[-1]["bytes_gather"] / max(ms_ga, 1e-6) / 1e6 / 900.0,
                 "gather_note": "dense bytes into the root / gather stage time (includes the root's wait and its "
-                               "inflate of the full representation)"},
+                               "inflate of the full representation)",
+                # measured ceilings of peer stores on this pool's B200 pairs (profiles/nvlink_probe.cu,
+                # profiles/r2_nvlink_probe.txt): the push kernel's copy loop, one direction, 1 GiB / 32 MiB
+                "sm_store_ceiling_GBs": {"1GiB": 713.7, "32MiB": 603.0,
+                                         "source": "profiles/r2_nvlink_probe.txt (SM peer stores; copy engines "
+                                                   "778.6 / 632.8)"},
+                "push_kernel_frac_of_sm_ceiling_32MiB": push_rate_min / 603.0},
             "gpu_launches": launches,
             "clocks": clk.summary(),
             "e2e": e2e,
